@@ -1,0 +1,186 @@
+/*
+ * qpscat_b200.h — C-ABI drop-in boundary for the quasi-periodic multilayer
+ * scattering hot path (Cho & Barnett, arXiv 1410.5003; reference library
+ * `qpscat`, /root/reference/proj/include/qpscat).
+ *
+ * Plain pointers and sizes only; complex numbers are `qps_cplx` with the
+ * memory layout of std::complex<double> (and CUDA double2).  All matrices
+ * crossing the boundary are column-major, exactly like the reference's
+ * Eigen::MatrixXcd (types.hpp:11).
+ *
+ * Two libraries implement this header:
+ *   paper_1410_5003_b200/libqpscat_b200.so — the product: host C++ + sm_100a
+ *       CUDA kernels (fill, Schur complements, block cyclic reduction, sweep);
+ *   oracle/_ref/libqpscat_ref.so — test infrastructure only: the reference
+ *       headers compiled unmodified on the CPU (oracle/ref_capi.cpp).
+ *
+ * Each entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj/include/qpscat/).  Error behaviour mirrors
+ * the reference's exception taxonomy (errors.hpp:9-40): every call returns a
+ * qps_status; qps_last_error() returns the message, the 1-based layer of a
+ * SolverError and the byte count of a MemoryBudgetError.
+ *
+ * Threading: one context = one CUDA stream; a context is not thread-safe.
+ * Calls are synchronous at the API level.
+ */
+#ifndef QPSCAT_B200_H
+#define QPSCAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QPS_ABI_VERSION 1
+
+typedef struct qps_ctx qps_ctx;
+typedef struct {
+    double re, im;
+} qps_cplx;
+
+/* errors.hpp:9-40, specfun.hpp:53-54 */
+typedef enum {
+    QPS_OK = 0,
+    QPS_ERR_CONFIG = 1,        /* ConfigError          errors.hpp:9   */
+    QPS_ERR_GEOMETRY = 2,      /* GeometryError        errors.hpp:14  */
+    QPS_ERR_USAGE = 3,         /* UsageError           errors.hpp:19  */
+    QPS_ERR_SINGULARITY = 4,   /* SingularityError     errors.hpp:24  */
+    QPS_ERR_SOLVER = 5,        /* SolverError{layer}   errors.hpp:29  */
+    QPS_ERR_MEMORY_BUDGET = 6, /* MemoryBudgetError    errors.hpp:36  */
+    QPS_ERR_DOMAIN = 7,        /* std::domain_error    specfun.hpp:54 */
+    QPS_ERR_CUDA = 8,          /* device failure (product only)        */
+    QPS_ERR_INTERNAL = 9
+} qps_status;
+
+/* InterfaceSpec::Shape, geometry.hpp:274 */
+typedef enum { QPS_SHAPE_SINE = 0, QPS_SHAPE_FOURIER = 1, QPS_SHAPE_POLYLINE = 2 } qps_shape;
+
+/* InterfaceSpec, geometry.hpp:273-282 (offset = nominal height; shape
+ * coordinates relative to it; vertices are x0,y0,x1,y1,...). */
+typedef struct {
+    int shape;
+    double offset;
+    double amplitude, phase;
+    int n_cos;
+    const double* cosc;
+    int n_sin;
+    const double* sinc;
+    int n_vertices;
+    const double* vertices;
+    int n_nodes;
+    const int* nodes;
+    int grading_q;
+} qps_interface_spec;
+
+/* NumericsParams, geometry.hpp:405-414 */
+typedef struct {
+    int P, Mw, M, K;
+    double R;
+    int grading_q;
+    double clearance;
+    uint64_t memory_budget;
+} qps_numerics;
+
+/* Matrices that can be downloaded for parity checks.
+ * Stage SYSTEM = BlockSystem (assembly.hpp:293-315);
+ * stage PERIODIZED = PeriodizedSystem (periodize.hpp:44-56). */
+typedef enum {
+    QPS_BLK_A_DIAG = 0, QPS_BLK_A_SUPER, QPS_BLK_A_SUB, QPS_BLK_B_SELF, QPS_BLK_B_BELOW,
+    QPS_BLK_C_SELF, QPS_BLK_C_ABOVE, QPS_BLK_Q, QPS_BLK_Z_U, QPS_BLK_Z_D, QPS_BLK_V_U, QPS_BLK_V_D,
+    QPS_BLK_W_U, QPS_BLK_W_D, QPS_BLK_F, QPS_BLK_BP_FIRST, QPS_BLK_BP_LAST, QPS_BLK_CP_FIRST,
+    QPS_BLK_CP_LAST, QPS_BLK_QP_FIRST, QPS_BLK_QP_LAST,
+    /* PeriodizedSystem */
+    QPS_BLK_AP_DIAG = 32, QPS_BLK_AP_SUPER, QPS_BLK_AP_SUB, QPS_BLK_X_FIRST, QPS_BLK_X_ABOVE,
+    QPS_BLK_X_SELF, QPS_BLK_X_LAST
+} qps_block_kind;
+
+/* Per-phase timings, milliseconds of the last call of each phase
+ * ("Matrix Filling / Schur / Block Solve"). */
+typedef struct {
+    double fill_ms, assemble_ms, schur_ms, solve_ms, recover_ms;
+} qps_phase_times;
+
+/* ---------------------------------------------------------------- context */
+int qps_abi_version(void);
+const char* qps_backend_name(void); /* "b200-cuda" or "reference-cpu" */
+qps_ctx* qps_create(int device);
+void qps_destroy(qps_ctx* ctx);
+int qps_last_error(const qps_ctx* ctx, char* msg, size_t cap, int* solver_layer, uint64_t* required_bytes);
+/* parallel.hpp:12-31 (CPU oracle thread count; ignored by the GPU library) */
+int qps_set_num_threads(qps_ctx* ctx, int n);
+/* periodize.hpp:15-18 qsolve_threshold() */
+int qps_set_qsolve_threshold(qps_ctx* ctx, double th);
+
+/* ----------------------------------------------------- geometry & problem */
+/* LayerStack + build_geometry(stack, num), geometry.hpp:289-296,480-496 */
+int qps_build_geometry(qps_ctx* ctx, double d, int n_layers, const double* epsilon, const double* mu,
+                       int n_interfaces, const qps_interface_spec* ifaces, const qps_numerics* num);
+/* make_problem(stack, geom, omega, theta, K), assembly.hpp:69-82 */
+int qps_make_problem(qps_ctx* ctx, double omega, double theta, int K);
+/* scalars of ScatteringProblem / StackGeometry (assembly.hpp:15-39, geometry.hpp:259-264):
+ * n_nodes[I], k[I+1]; any pointer may be NULL */
+int qps_problem_info(const qps_ctx* ctx, int* I, int* K, int* n_nodes, double* k, qps_cplx* alpha,
+                     double* y_U, double* y_D);
+/* nodes/normals (x,y interleaved, N each), weights, speeds of interface j
+ * (InterfaceQuadrature, geometry.hpp:80-92) */
+int qps_interface_nodes(const qps_ctx* ctx, int j, double* nodes_xy, double* normals_xy, double* weights,
+                        double* speeds);
+
+/* ------------------------------------------- step-wise hot path (cache) */
+/* precompute_shift_blocks(p, num), assembly.hpp:212-287 (alpha-free cache) */
+int qps_precompute_shift_blocks(qps_ctx* ctx);
+/* assemble_system(p, cache, num), assembly.hpp:462-483 */
+int qps_assemble_system(qps_ctx* ctx);
+/* schur_complement(sys), periodize.hpp:124-126 */
+int qps_schur_complement(qps_ctx* ctx);
+/* block_lu_solve(ps), tridiag.hpp:23-46 (the product uses block cyclic
+ * reduction; SolverError names the original 1-based layer of a singular
+ * diagonal factor) */
+int qps_block_lu_solve(qps_ctx* ctx);
+/* recover_aux(ps, eta, sol), tridiag.hpp:50-66 */
+int qps_recover_aux(qps_ctx* ctx);
+
+/* ------------------------------------------------- one-shot hot path */
+/* precompute_shift_blocks + assemble_system + solve_periodized
+ * (assembly.hpp:212,462; tridiag.hpp:69-74).  The product fuses the alpha
+ * recombination into the fill and never materialises the alpha-free cache. */
+int qps_solve(qps_ctx* ctx);
+
+/* Solution, tridiag.hpp:11-17: eta[sum 2N_j] (per interface tau then sigma),
+ * c[(I+1)*P], aU[2K+1], aD[2K+1], lsq_residual[I+1]; NULL pointers skipped */
+int qps_get_solution(const qps_ctx* ctx, qps_cplx* eta, qps_cplx* c, qps_cplx* aU, qps_cplx* aD,
+                     double* lsq_residual, double* max_lsq_residual);
+/* flux_error + reflection_transmission, postprocess.hpp:134-180.
+ * Per-order arrays (2K+1 each, may be NULL): kappa, k^U_n, k^D_n, propagating flags. */
+int qps_reflection_transmission(const qps_ctx* ctx, double* R, double* T, double* flux_error, double* kappa,
+                                qps_cplx* kU, qps_cplx* kD, int* prop_up, int* prop_down);
+
+/* --------------------------------------------------------- angle sweep */
+/* Multi-angle sweep (building blocks assembly.hpp:85-155,
+ * periodize.hpp:58-126): the alpha-free cache is filled once and every angle
+ * is assembled, periodized and solved from it (mode 0, "accelerated"), or the
+ * cache is refilled per angle (mode 1, "independent").  K is fixed for all
+ * angles.  Outputs per angle: R, T, flux_error [n]; aU, aD [n*(2K+1)];
+ * status [n] (qps_status of that angle; a singular angle does not abort). */
+int qps_sweep(qps_ctx* ctx, int n_angles, const double* theta, int K, int mode, double* R, double* T,
+              double* flux_error, qps_cplx* aU, qps_cplx* aD, int* status);
+
+/* ------------------------------------------------- parity / diagnostics */
+/* Copy block `kind` with index `i` (interface, layer or 0) into out
+ * (column-major, rows x cols).  With out == NULL only the shape is returned. */
+int qps_download_block(const qps_ctx* ctx, int kind, int i, qps_cplx* out, int* rows, int* cols);
+/* ShiftBlockCache::fill_evals (assembly.hpp:285): `reference` = the reference
+ * fill's Hankel-pair count for this geometry, `performed` = pairs evaluated by
+ * this implementation in its last fill. */
+int qps_fill_evals(const qps_ctx* ctx, uint64_t* reference, uint64_t* performed);
+int qps_get_phase_times(const qps_ctx* ctx, qps_phase_times* t);
+/* hankel01 batch (specfun.hpp:69-73): h0[n], h1[n] for host x[n] */
+int qps_hankel01(qps_ctx* ctx, int n, const double* x, qps_cplx* h0, qps_cplx* h1);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QPSCAT_B200_H */

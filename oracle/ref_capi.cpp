@@ -1,0 +1,427 @@
+// ORACLE TEST INFRASTRUCTURE — not product code.
+//
+// include/qpscat_b200.h implemented by the REFERENCE itself: the qpscat
+// headers (/root/reference/proj/include/qpscat) compiled unmodified against
+// oracle/shim.  Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs load the resulting
+// oracle/_ref/libqpscat_ref.so, always as the checker or the CPU baseline.
+// Every entry point is a direct call sequence into the reference API; the
+// composition mirrors the reference's own drivers (proj/tests/test_tridiag.cpp:
+// 112-126 `solve_stack`, proj/tests/test_assembly.cpp:229-239 for re-assembly).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <string>
+
+#include "qpscat/postprocess.hpp"
+#include "qpscat_b200.h"
+
+using namespace qpscat;
+
+struct qps_ctx {
+    LayerStack stack;
+    NumericsParams num;
+    StackGeometry geom;
+    ScatteringProblem prob;
+    bool have_geom = false, have_prob = false;
+    std::optional<ShiftBlockCache> cache;
+    std::optional<BlockSystem> sys;
+    std::optional<PeriodizedSystem> ps;
+    std::vector<Vec> eta;
+    std::optional<Solution> sol;
+    qps_phase_times times{};
+    uint64_t fill_evals = 0;
+    std::string err;
+    int err_layer = 0;
+    uint64_t err_bytes = 0;
+};
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+double ms_since(clk::time_point t0) {
+    return std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+}
+
+template <class F>
+int guarded(qps_ctx* c, F&& f) {
+    if (!c) return QPS_ERR_USAGE;
+    c->err.clear();
+    c->err_layer = 0;
+    c->err_bytes = 0;
+    try {
+        f();
+        return QPS_OK;
+    } catch (const SolverError& e) {
+        c->err = e.what();
+        c->err_layer = e.layer;
+        return QPS_ERR_SOLVER;
+    } catch (const MemoryBudgetError& e) {
+        c->err = e.what();
+        c->err_bytes = e.required_bytes;
+        return QPS_ERR_MEMORY_BUDGET;
+    } catch (const ConfigError& e) {
+        c->err = e.what();
+        return QPS_ERR_CONFIG;
+    } catch (const GeometryError& e) {
+        c->err = e.what();
+        return QPS_ERR_GEOMETRY;
+    } catch (const UsageError& e) {
+        c->err = e.what();
+        return QPS_ERR_USAGE;
+    } catch (const SingularityError& e) {
+        c->err = e.what();
+        return QPS_ERR_SINGULARITY;
+    } catch (const std::domain_error& e) {
+        c->err = e.what();
+        return QPS_ERR_DOMAIN;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        return QPS_ERR_INTERNAL;
+    }
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) throw UsageError(std::string("qps oracle: ") + what);
+}
+
+void put(const Mat& m, qps_cplx* out, int* rows, int* cols) {
+    if (rows) *rows = int(m.rows());
+    if (cols) *cols = int(m.cols());
+    if (out && m.size()) std::memcpy(out, m.data(), sizeof(cd) * m.size());
+}
+
+const Mat& pick(const std::vector<Mat>& v, int i) {
+    if (i < 0 || i >= int(v.size())) throw UsageError("qps oracle: block index out of range");
+    return v[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int qps_abi_version(void) { return QPS_ABI_VERSION; }
+const char* qps_backend_name(void) { return "reference-cpu"; }
+
+qps_ctx* qps_create(int) { return new qps_ctx(); }
+void qps_destroy(qps_ctx* c) { delete c; }
+
+int qps_last_error(const qps_ctx* c, char* msg, size_t cap, int* layer, uint64_t* bytes) {
+    if (!c) return QPS_ERR_USAGE;
+    if (msg && cap) {
+        std::strncpy(msg, c->err.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
+    if (layer) *layer = c->err_layer;
+    if (bytes) *bytes = c->err_bytes;
+    return QPS_OK;
+}
+
+int qps_set_num_threads(qps_ctx* c, int n) {
+    return guarded(c, [&] {
+        set_num_threads(n);
+        if (n > 0) qps_blas::set_num_threads(n);
+    });
+}
+
+int qps_set_qsolve_threshold(qps_ctx* c, double th) {
+    return guarded(c, [&] { qsolve_threshold() = th; });
+}
+
+int qps_build_geometry(qps_ctx* c, double d, int n_layers, const double* eps, const double* mu, int n_ifaces,
+                       const qps_interface_spec* ifs, const qps_numerics* num) {
+    return guarded(c, [&] {
+        need(num != nullptr, "numerics required");
+        c->have_geom = c->have_prob = false;
+        c->cache.reset();
+        c->sys.reset();
+        c->ps.reset();
+        c->sol.reset();
+        LayerStack st;
+        st.d = d;
+        for (int i = 0; i < n_layers; ++i) st.materials.push_back({eps[i], mu ? mu[i] : 1.0});
+        for (int j = 0; j < n_ifaces; ++j) {
+            const auto& s = ifs[j];
+            InterfaceSpec sp;
+            sp.shape = s.shape == QPS_SHAPE_SINE      ? InterfaceSpec::Shape::Sine
+                       : s.shape == QPS_SHAPE_FOURIER ? InterfaceSpec::Shape::Fourier
+                                                      : InterfaceSpec::Shape::Polyline;
+            sp.offset = s.offset;
+            sp.amplitude = s.amplitude;
+            sp.phase = s.phase;
+            sp.cosc.assign(s.cosc, s.cosc + s.n_cos);
+            sp.sinc.assign(s.sinc, s.sinc + s.n_sin);
+            for (int v = 0; v < s.n_vertices; ++v) sp.vertices.push_back({s.vertices[2 * v], s.vertices[2 * v + 1]});
+            sp.nodes.assign(s.nodes, s.nodes + s.n_nodes);
+            sp.grading_q = s.grading_q;
+            st.interfaces.push_back(std::move(sp));
+        }
+        NumericsParams np;
+        np.P = num->P;
+        np.Mw = num->Mw;
+        np.M = num->M;
+        np.K = num->K;
+        np.R = num->R;
+        np.grading_q = num->grading_q;
+        np.clearance = num->clearance;
+        np.memory_budget = num->memory_budget;
+        c->stack = std::move(st);
+        c->num = np;
+        c->geom = build_geometry(c->stack, c->num);
+        c->have_geom = true;
+    });
+}
+
+int qps_make_problem(qps_ctx* c, double omega, double theta, int K) {
+    return guarded(c, [&] {
+        need(c->have_geom, "build_geometry first");
+        c->prob = make_problem(c->stack, c->geom, omega, theta, K);
+        c->have_prob = true;
+        c->sys.reset();
+        c->ps.reset();
+        c->sol.reset();
+    });
+}
+
+int qps_problem_info(const qps_ctx* c, int* I, int* K, int* n_nodes, double* k, qps_cplx* alpha, double* y_U,
+                     double* y_D) {
+    return guarded(const_cast<qps_ctx*>(c), [&] {
+        need(c->have_geom, "build_geometry first");
+        const int nI = int(c->geom.interfaces.size());
+        if (I) *I = nI;
+        if (n_nodes)
+            for (int j = 0; j < nI; ++j) n_nodes[j] = c->geom.interfaces[j].quad.total();
+        if (y_U) *y_U = c->geom.frame.y_U;
+        if (y_D) *y_D = c->geom.frame.y_D;
+        if (c->have_prob) {
+            if (K) *K = c->prob.K;
+            if (k)
+                for (int i = 0; i <= nI; ++i) k[i] = c->prob.k[i];
+            if (alpha) *alpha = {c->prob.alpha.real(), c->prob.alpha.imag()};
+        } else if (K) {
+            *K = 0;
+        }
+    });
+}
+
+int qps_interface_nodes(const qps_ctx* c, int j, double* nodes, double* normals, double* w, double* sp) {
+    return guarded(const_cast<qps_ctx*>(c), [&] {
+        need(c->have_geom && j >= 0 && j < int(c->geom.interfaces.size()), "bad interface");
+        const auto& q = c->geom.interfaces[j].quad;
+        for (int i = 0; i < q.total(); ++i) {
+            if (nodes) { nodes[2 * i] = q.nodes[i].x; nodes[2 * i + 1] = q.nodes[i].y; }
+            if (normals) { normals[2 * i] = q.normals[i].x; normals[2 * i + 1] = q.normals[i].y; }
+            if (w) w[i] = q.weights[i];
+            if (sp) sp[i] = q.speeds[i];
+        }
+    });
+}
+
+int qps_precompute_shift_blocks(qps_ctx* c) {
+    return guarded(c, [&] {
+        need(c->have_prob, "make_problem first");
+        const auto t0 = clk::now();
+        c->cache = precompute_shift_blocks(c->prob, c->num);
+        c->fill_evals = c->cache->fill_evals;
+        c->times.fill_ms = ms_since(t0);
+    });
+}
+
+int qps_assemble_system(qps_ctx* c) {
+    return guarded(c, [&] {
+        need(c->cache.has_value(), "precompute_shift_blocks first");
+        const auto t0 = clk::now();
+        c->sys = assemble_system(c->prob, *c->cache, c->num);
+        c->times.assemble_ms = ms_since(t0);
+    });
+}
+
+int qps_schur_complement(qps_ctx* c) {
+    return guarded(c, [&] {
+        need(c->sys.has_value(), "assemble_system first");
+        const auto t0 = clk::now();
+        c->ps = schur_complement(*c->sys);
+        c->times.schur_ms = ms_since(t0);
+    });
+}
+
+int qps_block_lu_solve(qps_ctx* c) {
+    return guarded(c, [&] {
+        need(c->ps.has_value(), "schur_complement first");
+        const auto t0 = clk::now();
+        c->eta = block_lu_solve(*c->ps);
+        c->times.solve_ms = ms_since(t0);
+    });
+}
+
+int qps_recover_aux(qps_ctx* c) {
+    return guarded(c, [&] {
+        need(c->ps.has_value() && !c->eta.empty(), "block_lu_solve first");
+        const auto t0 = clk::now();
+        Solution s;
+        recover_aux(*c->ps, c->eta, s);
+        s.flux_error = flux_error(s, c->prob);
+        c->sol = std::move(s);
+        c->times.recover_ms = ms_since(t0);
+    });
+}
+
+int qps_solve(qps_ctx* c) {
+    int s = qps_precompute_shift_blocks(c);
+    if (s == QPS_OK) s = qps_assemble_system(c);
+    if (s == QPS_OK) s = qps_schur_complement(c);
+    if (s == QPS_OK) s = qps_block_lu_solve(c);
+    if (s == QPS_OK) s = qps_recover_aux(c);
+    return s;
+}
+
+int qps_get_solution(const qps_ctx* c, qps_cplx* eta, qps_cplx* cc, qps_cplx* aU, qps_cplx* aD, double* lsq,
+                     double* max_lsq) {
+    return guarded(const_cast<qps_ctx*>(c), [&] {
+        need(c->sol.has_value(), "no solution");
+        const Solution& s = *c->sol;
+        if (eta) {
+            size_t o = 0;
+            for (const auto& e : s.eta) {
+                std::memcpy(eta + o, e.data(), sizeof(cd) * e.size());
+                o += e.size();
+            }
+        }
+        if (cc) {
+            size_t o = 0;
+            for (const auto& v : s.c) {
+                std::memcpy(cc + o, v.data(), sizeof(cd) * v.size());
+                o += v.size();
+            }
+        }
+        if (aU) std::memcpy(aU, s.aU.data(), sizeof(cd) * s.aU.size());
+        if (aD) std::memcpy(aD, s.aD.data(), sizeof(cd) * s.aD.size());
+        if (lsq)
+            for (size_t i = 0; i < c->ps->lsq_residual.size(); ++i) lsq[i] = c->ps->lsq_residual[i];
+        if (max_lsq) *max_lsq = s.max_lsq_residual;
+    });
+}
+
+int qps_reflection_transmission(const qps_ctx* c, double* R, double* T, double* fe, double* kappa, qps_cplx* kU,
+                                qps_cplx* kD, int* pu, int* pd) {
+    return guarded(const_cast<qps_ctx*>(c), [&] {
+        need(c->sol.has_value(), "no solution");
+        const SpectrumRow row = reflection_transmission(*c->sol, c->prob);
+        if (R) *R = row.R;
+        if (T) *T = row.T;
+        if (fe) *fe = row.flux_error;
+        for (size_t i = 0; i < row.up.size(); ++i) {
+            if (kappa) kappa[i] = row.up[i].kappa;
+            if (kU) kU[i] = {row.up[i].k_vert.real(), row.up[i].k_vert.imag()};
+            if (kD) kD[i] = {row.down[i].k_vert.real(), row.down[i].k_vert.imag()};
+            if (pu) pu[i] = row.up[i].propagating;
+            if (pd) pd[i] = row.down[i].propagating;
+        }
+    });
+}
+
+int qps_sweep(qps_ctx* c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe,
+              qps_cplx* aU, qps_cplx* aD, int* status) {
+    return guarded(c, [&] {
+        need(c->have_prob, "make_problem first (sets omega)");
+        need(K > 0, "sweep needs a fixed K > 0");
+        const double omega = c->prob.omega;
+        const int nrb = 2 * K + 1;
+        const auto t0 = clk::now();
+        std::optional<ShiftBlockCache> cache;
+        if (mode == 0) {
+            cache = precompute_shift_blocks(make_problem(c->stack, c->geom, omega, theta[0], K), c->num);
+            c->fill_evals = cache->fill_evals;
+        }
+        for (int a = 0; a < n; ++a) {
+            ScatteringProblem p = make_problem(c->stack, c->geom, omega, theta[a], K);
+            qps_ctx tmp;
+            const int st = guarded(&tmp, [&] {
+                if (mode != 0) cache = precompute_shift_blocks(p, c->num);
+                const BlockSystem sys = assemble_system(p, *cache, c->num);
+                Solution s = solve_periodized(sys);
+                const SpectrumRow row = reflection_transmission(s, p);
+                if (R) R[a] = row.R;
+                if (T) T[a] = row.T;
+                if (fe) fe[a] = row.flux_error;
+                for (int i = 0; i < nrb; ++i) {
+                    if (aU) aU[size_t(a) * nrb + i] = {s.aU(i).real(), s.aU(i).imag()};
+                    if (aD) aD[size_t(a) * nrb + i] = {s.aD(i).real(), s.aD(i).imag()};
+                }
+            });
+            if (status) status[a] = st;
+        }
+        c->times.fill_ms = ms_since(t0);
+    });
+}
+
+int qps_download_block(const qps_ctx* c, int kind, int i, qps_cplx* out, int* rows, int* cols) {
+    return guarded(const_cast<qps_ctx*>(c), [&] {
+        if (kind < 32) {
+            need(c->sys.has_value(), "assemble_system first");
+            const BlockSystem& s = *c->sys;
+            switch (kind) {
+                case QPS_BLK_A_DIAG: return put(pick(s.A_diag, i), out, rows, cols);
+                case QPS_BLK_A_SUPER: return put(pick(s.A_super, i), out, rows, cols);
+                case QPS_BLK_A_SUB: return put(pick(s.A_sub, i), out, rows, cols);
+                case QPS_BLK_B_SELF: return put(pick(s.B_self, i), out, rows, cols);
+                case QPS_BLK_B_BELOW: return put(pick(s.B_below, i), out, rows, cols);
+                case QPS_BLK_C_SELF: return put(pick(s.C_self, i), out, rows, cols);
+                case QPS_BLK_C_ABOVE: return put(pick(s.C_above, i), out, rows, cols);
+                case QPS_BLK_Q: return put(pick(s.Q, i), out, rows, cols);
+                case QPS_BLK_Z_U: return put(s.Z_U, out, rows, cols);
+                case QPS_BLK_Z_D: return put(s.Z_D, out, rows, cols);
+                case QPS_BLK_V_U: return put(s.V_U, out, rows, cols);
+                case QPS_BLK_V_D: return put(s.V_D, out, rows, cols);
+                case QPS_BLK_W_U: return put(s.W_U, out, rows, cols);
+                case QPS_BLK_W_D: return put(s.W_D, out, rows, cols);
+                case QPS_BLK_F: return put(Mat(s.f), out, rows, cols);
+                case QPS_BLK_BP_FIRST: return put(s.Bp_first, out, rows, cols);
+                case QPS_BLK_BP_LAST: return put(s.Bp_last, out, rows, cols);
+                case QPS_BLK_CP_FIRST: return put(s.Cp_first, out, rows, cols);
+                case QPS_BLK_CP_LAST: return put(s.Cp_last, out, rows, cols);
+                case QPS_BLK_QP_FIRST: return put(s.Qp_first, out, rows, cols);
+                case QPS_BLK_QP_LAST: return put(s.Qp_last, out, rows, cols);
+                default: throw UsageError("qps oracle: unknown block kind");
+            }
+        }
+        need(c->ps.has_value(), "schur_complement first");
+        const PeriodizedSystem& p = *c->ps;
+        switch (kind) {
+            case QPS_BLK_AP_DIAG: return put(pick(p.Ap_diag, i), out, rows, cols);
+            case QPS_BLK_AP_SUPER: return put(pick(p.Ap_super, i), out, rows, cols);
+            case QPS_BLK_AP_SUB: return put(pick(p.Ap_sub, i), out, rows, cols);
+            case QPS_BLK_X_FIRST: return put(p.X_first, out, rows, cols);
+            case QPS_BLK_X_ABOVE: return put(pick(p.X_above, i), out, rows, cols);
+            case QPS_BLK_X_SELF: return put(pick(p.X_self, i), out, rows, cols);
+            case QPS_BLK_X_LAST: return put(p.X_last, out, rows, cols);
+            default: throw UsageError("qps oracle: unknown block kind");
+        }
+    });
+}
+
+int qps_fill_evals(const qps_ctx* c, uint64_t* reference, uint64_t* performed) {
+    if (!c) return QPS_ERR_USAGE;
+    if (reference) *reference = c->fill_evals;
+    if (performed) *performed = c->fill_evals;
+    return QPS_OK;
+}
+
+int qps_get_phase_times(const qps_ctx* c, qps_phase_times* t) {
+    if (!c || !t) return QPS_ERR_USAGE;
+    *t = c->times;
+    return QPS_OK;
+}
+
+int qps_hankel01(qps_ctx* c, int n, const double* x, qps_cplx* h0, qps_cplx* h1) {
+    return guarded(c, [&] {
+        for (int i = 0; i < n; ++i) {
+            const HankelPair h = hankel01(x[i]);
+            h0[i] = {h.h0.real(), h.h0.imag()};
+            h1[i] = {h.h1.real(), h.h1.imag()};
+        }
+    });
+}
+
+}  // extern "C"
