@@ -178,6 +178,16 @@ int qps_fill_evals(const qps_ctx* ctx, uint64_t* reference, uint64_t* performed)
 int qps_get_phase_times(const qps_ctx* ctx, qps_phase_times* t);
 /* hankel01 batch (specfun.hpp:69-73): h0[n], h1[n] for host x[n] */
 int qps_hankel01(qps_ctx* ctx, int n, const double* x, qps_cplx* h0, qps_cplx* h1);
+/* qsolve(Q, RHS), periodize.hpp:25-39: min-norm least squares through the
+ * rank-revealing complete orthogonal decomposition with threshold escalation
+ * (Q m x p, RHS m x n, X p x n; column-major).  *rank receives the rank used. */
+int qps_qsolve(qps_ctx* ctx, int m, int p, int n, const qps_cplx* Q, const qps_cplx* RHS, qps_cplx* X, int* rank);
+/* Diagnostics: C = A B (M x K times K x N, column-major) on the product's
+ * batched DMMA GEMM (the oracle uses its BLAS). */
+int qps_debug_zgemm(qps_ctx* ctx, int M, int N, int K, const qps_cplx* A, const qps_cplx* B, qps_cplx* C);
+/* FP64 peaks of this device measured by microbenchmarks (DFMA chain, DMMA
+ * loop), TFLOP/s; the oracle returns 0 for both. */
+int qps_measure_fp64_peaks(qps_ctx* ctx, double* dfma_tflops, double* dmma_tflops);
 
 #ifdef __cplusplus
 }

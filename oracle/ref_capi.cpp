@@ -424,4 +424,37 @@ int qps_hankel01(qps_ctx* c, int n, const double* x, qps_cplx* h0, qps_cplx* h1)
     });
 }
 
+int qps_qsolve(qps_ctx* c, int m, int p, int n, const qps_cplx* Q, const qps_cplx* R, qps_cplx* X, int* rank) {
+    return guarded(c, [&] {
+        Mat q(m, p), r(m, n);
+        std::memcpy(q.data(), Q, sizeof(cd) * size_t(m) * p);
+        std::memcpy(r.data(), R, sizeof(cd) * size_t(m) * n);
+        const Mat x = qsolve(q, r);
+        std::memcpy(X, x.data(), sizeof(cd) * size_t(p) * n);
+        if (rank) {
+            Eigen::CompleteOrthogonalDecomposition<Mat> cod;
+            cod.setThreshold(qsolve_threshold());
+            cod.compute(q);
+            *rank = int(cod.rank());
+        }
+    });
+}
+
+int qps_debug_zgemm(qps_ctx* c, int M, int N, int K, const qps_cplx* A, const qps_cplx* B, qps_cplx* Cm) {
+    return guarded(c, [&] {
+        Mat a(M, K), b(K, N);
+        std::memcpy(a.data(), A, sizeof(cd) * size_t(M) * K);
+        std::memcpy(b.data(), B, sizeof(cd) * size_t(K) * N);
+        const Mat r = a * b;
+        std::memcpy(Cm, r.data(), sizeof(cd) * size_t(M) * N);
+    });
+}
+
+int qps_measure_fp64_peaks(qps_ctx* c, double* a, double* b) {
+    if (!c) return QPS_ERR_USAGE;
+    if (a) *a = 0.0;
+    if (b) *b = 0.0;
+    return QPS_OK;
+}
+
 }  // extern "C"

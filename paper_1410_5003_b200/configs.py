@@ -1,0 +1,132 @@
+"""Seeded synthetic stacks for BASELINE.json configs 1-5.
+
+The reference publishes no benchmark inputs; these generators draw the
+interface shapes and wavenumbers BASELINE.json describes from
+std::mt19937_64(seed) with u = (x >> 11) * 2^-53 (the exact C++ generator is
+restated below so the same stack can be rebuilt in C++), in the documented
+order: per interface (a_i, phi_i [, polyline parameters]), then per layer
+(n_i or k_i).  Material parameters reproduce the requested wavenumbers
+through the reference's own make_problem: omega = k_1, eps_i = (k_i/k_1)^2,
+mu = 1 (assembly.hpp:78).
+"""
+from __future__ import annotations
+
+import math
+
+from .qpscat import InterfaceSpec, LayerStack, Material, NumericsParams
+
+_MASK = (1 << 64) - 1
+
+
+class MT19937_64:
+    """std::mt19937_64 (C++11 [rand.predef])."""
+
+    def __init__(self, seed=5489):
+        self.mt = [0] * 312
+        self.mt[0] = seed & _MASK
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & _MASK
+        self.idx = 312
+
+    def _twist(self):
+        mt = self.mt
+        for i in range(312):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + 156) % 312] ^ xa
+        self.idx = 0
+
+    def next(self):
+        if self.idx >= 312:
+            self._twist()
+        x = self.mt[self.idx]
+        self.idx += 1
+        x ^= (x >> 29) & 0x5555555555555555
+        x ^= (x << 17) & 0x71D67FFFEDA60000
+        x ^= (x << 37) & 0xFFF7EEE000000000
+        x ^= x >> 43
+        return x & _MASK
+
+    def uniform(self, lo=0.0, hi=1.0):
+        return lo + (hi - lo) * ((self.next() >> 11) * 2.0 ** -53)
+
+
+DEFAULT_SEED = 5003
+
+
+def _stack_from_k(ks, interfaces, d=1.0):
+    k1 = ks[0]
+    mats = [Material(epsilon=(k / k1) ** 2, mu=1.0) for k in ks]
+    return LayerStack(d=d, materials=mats, interfaces=interfaces), k1
+
+
+def _sine(offset, a, phi, N):
+    return InterfaceSpec(shape="sine", offset=offset, amplitude=a, phase=phi, nodes=[N])
+
+
+def config(cfg: int, seed: int = DEFAULT_SEED, n_interfaces: int | None = None):
+    """Return (stack, numerics, omega, theta, K, meta) for BASELINE config `cfg`.
+
+    `n_interfaces` truncates a multilayer config (same per-layer sizes) — used
+    for bounded CPU-oracle samples and small parity cases."""
+    rng = MT19937_64(seed)
+    if cfg == 1:
+        stack, om = _stack_from_k([10.0, 15.0], [_sine(0.0, 0.25, 0.0, 80)])
+        num = NumericsParams(P=60, Mw=40, M=60, K=10, R=1.5, clearance=0.75, memory_budget=1 << 40)
+        return stack, num, om, -math.pi / 5, 10, {"seed": seed, "I": 1}
+    if cfg in (2, 4, 5):
+        I = {2: 10, 4: 1000, 5: 100}[cfg]
+        N = {2: 100, 4: 300, 5: 150}[cfg]
+        if n_interfaces is not None:
+            I = n_interfaces
+        ifaces = []
+        for i in range(I):
+            a = rng.uniform(0.05, 0.3)
+            phi = rng.uniform(0.0, 2 * math.pi)
+            ifaces.append(_sine(-1.0 * i, a, phi, N))
+        if cfg == 2:
+            ks = [10.0 * rng.uniform(1.0, 3.0) for _ in range(I + 1)]
+        else:
+            ks = [rng.uniform(10.0, 30.0) for _ in range(I + 1)]
+        stack, om = _stack_from_k(ks, ifaces)
+        P = 80 if cfg == 4 else 60
+        K = 10 if cfg == 2 else 20
+        num = NumericsParams(P=P, Mw=40, M=60, K=K, R=1.5, clearance=0.75, memory_budget=1 << 40)
+        return stack, num, om, -math.pi / 5, K, {"seed": seed, "I": I, "N": N}
+    if cfg == 3:
+        I = 100 if n_interfaces is None else n_interfaces
+        ifaces = []
+        for i in range(I):
+            if i % 2 == 0:
+                a = rng.uniform(0.05, 0.3)
+                phi = rng.uniform(0.0, 2 * math.pi)
+                ifaces.append(_sine(-1.0 * i, a, phi, 200))
+            else:
+                trapezoid = rng.uniform() >= 0.5
+                h = rng.uniform(0.1, 0.3)
+                if trapezoid:
+                    x1 = rng.uniform(-0.3, -0.1)
+                    x2 = rng.uniform(0.1, 0.3)
+                    verts = [(-0.5, 0.0), (x1, h), (x2, h), (0.5, 0.0)]
+                    nodes = [67, 67, 66]
+                else:
+                    xp = rng.uniform(-0.2, 0.2)
+                    verts = [(-0.5, 0.0), (xp, h), (0.5, 0.0)]
+                    nodes = [100, 100]
+                ifaces.append(InterfaceSpec(shape="polyline", offset=-1.0 * i, vertices=verts, nodes=nodes,
+                                            grading_q=6))
+        ks = [10.0 * rng.uniform(1.0, 3.0) for _ in range(I + 1)]
+        stack, om = _stack_from_k(ks, ifaces)
+        num = NumericsParams(P=60, Mw=40, M=60, K=10, R=1.5, clearance=0.75, memory_budget=1 << 40)
+        # top layer 1e-10 from the n = -1 Wood anomaly: k1 cos(theta) - 2 pi = -k1
+        theta = -math.acos(-1.0 + 2.0 * math.pi / om) + 1e-10
+        return stack, num, om, theta, 10, {"seed": seed, "I": I, "N": 200}
+    raise ValueError(f"unknown config {cfg}")
+
+
+def sweep_angles(n=200):
+    """Config 5: n incident angles uniform in [-pi + 0.1, -0.1]."""
+    lo, hi = -math.pi + 0.1, -0.1
+    return [lo + (hi - lo) * i / (n - 1) for i in range(n)]

@@ -1,0 +1,509 @@
+// C-ABI of the B200 implementation (include/qpscat_b200.h).  Every entry point
+// converts exceptions into qps_status codes following the reference's error
+// taxonomy (errors.hpp:9-40) and never falls back to a CPU path.
+#include <cstring>
+
+#include "ctx.h"
+
+using namespace qpsb;
+
+struct qps_ctx {
+    Ctx c;
+};
+
+namespace {
+
+template <class F>
+int guarded(qps_ctx* h, F&& f) {
+    if (!h) return QPS_ERR_USAGE;
+    Ctx& c = h->c;
+    c.err_msg.clear();
+    c.err_layer = 0;
+    c.err_bytes = 0;
+    try {
+        QPS_CUDA(cudaSetDevice(c.device));
+        f(c);
+        return QPS_OK;
+    } catch (const Error& e) {
+        c.err_msg = e.what();
+        c.err_layer = e.layer;
+        c.err_bytes = e.bytes;
+        return e.status;
+    } catch (const std::exception& e) {
+        c.err_msg = e.what();
+        return QPS_ERR_INTERNAL;
+    }
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) fail(QPS_ERR_USAGE, std::string("qpscat_b200: ") + what);
+}
+
+void prepare(Ctx& c) {
+    need(c.have_prob, "make_problem first");
+    setup_dims(c);
+}
+
+void get_block(const Ctx& c, const cplx* base, int ld, int rows, int cols, qps_cplx* out, int* r, int* cc) {
+    if (r) *r = rows;
+    if (cc) *cc = cols;
+    if (!out || rows == 0 || cols == 0) return;
+    QPS_CUDA(cudaMemcpy2DAsync(out, sizeof(cplx) * rows, base, sizeof(cplx) * ld, sizeof(cplx) * rows, cols,
+                               cudaMemcpyDeviceToHost, c.stream));
+    QPS_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void zero_block(int* r, int* cc) {
+    if (r) *r = 0;
+    if (cc) *cc = 0;
+}
+
+void set_spec(StackDesc& st, int n, const qps_interface_spec* ifs) {
+    st.cosc.resize(n);
+    st.sinc.resize(n);
+    st.verts.resize(n);
+    st.nodes.resize(n);
+    st.ifaces.resize(n);
+    for (int j = 0; j < n; ++j) {
+        const auto& s = ifs[j];
+        st.cosc[j].assign(s.cosc, s.cosc + (s.cosc ? s.n_cos : 0));
+        st.sinc[j].assign(s.sinc, s.sinc + (s.sinc ? s.n_sin : 0));
+        st.verts[j].assign(s.vertices, s.vertices + (s.vertices ? 2 * s.n_vertices : 0));
+        st.nodes[j].assign(s.nodes, s.nodes + (s.nodes ? s.n_nodes : 0));
+        qps_interface_spec t = s;
+        t.cosc = st.cosc[j].data();
+        t.sinc = st.sinc[j].data();
+        t.vertices = st.verts[j].data();
+        t.nodes = st.nodes[j].data();
+        t.n_cos = int(st.cosc[j].size());
+        t.n_sin = int(st.sinc[j].size());
+        t.n_vertices = int(st.verts[j].size() / 2);
+        t.n_nodes = int(st.nodes[j].size());
+        st.ifaces[j] = t;
+    }
+}
+
+void run_fill(Ctx& c) {
+    Timer t(c, &c.times.fill_ms);
+    fill_system_fused(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+int qps_abi_version(void) { return QPS_ABI_VERSION; }
+const char* qps_backend_name(void) { return "b200-cuda"; }
+
+qps_ctx* qps_create(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || device < 0 || device >= n) return nullptr;
+    auto* h = new qps_ctx();
+    h->c.device = device;
+    try {
+        QPS_CUDA(cudaSetDevice(device));
+        QPS_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+        QPS_CUDA(cudaEventCreate(&h->c.ev0));
+        QPS_CUDA(cudaEventCreate(&h->c.ev1));
+        upload_hankel_tables();
+    } catch (...) {
+        delete h;
+        return nullptr;
+    }
+    return h;
+}
+
+void qps_destroy(qps_ctx* h) {
+    if (!h) return;
+    cudaSetDevice(h->c.device);
+    cudaStreamSynchronize(h->c.stream);
+    if (h->c.ev0) cudaEventDestroy(h->c.ev0);
+    if (h->c.ev1) cudaEventDestroy(h->c.ev1);
+    cudaStream_t s = h->c.stream;
+    delete h;
+    if (s) cudaStreamDestroy(s);
+}
+
+int qps_last_error(const qps_ctx* h, char* msg, size_t cap, int* layer, uint64_t* bytes) {
+    if (!h) return QPS_ERR_USAGE;
+    if (msg && cap) {
+        std::strncpy(msg, h->c.err_msg.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
+    if (layer) *layer = h->c.err_layer;
+    if (bytes) *bytes = h->c.err_bytes;
+    return QPS_OK;
+}
+
+int qps_set_num_threads(qps_ctx* h, int) { return h ? QPS_OK : QPS_ERR_USAGE; }
+
+int qps_set_qsolve_threshold(qps_ctx* h, double th) {
+    return guarded(h, [&](Ctx& c) { c.qsolve_th0 = th; });
+}
+
+int qps_build_geometry(qps_ctx* h, double d, int n_layers, const double* eps, const double* mu, int n_ifaces,
+                       const qps_interface_spec* ifs, const qps_numerics* num) {
+    return guarded(h, [&](Ctx& c) {
+        need(num != nullptr && eps != nullptr, "numerics and epsilon required");
+        c.have_geom = c.have_prob = false;
+        c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
+        StackDesc st;
+        st.d = d;
+        for (int i = 0; i < n_layers; ++i) {
+            st.eps.push_back(eps[i]);
+            st.mu.push_back(mu ? mu[i] : 1.0);
+        }
+        set_spec(st, n_ifaces, ifs);
+        Numerics nm;
+        nm.P = num->P;
+        nm.Mw = num->Mw;
+        nm.M = num->M;
+        nm.K = num->K;
+        nm.R = num->R;
+        nm.grading_q = num->grading_q;
+        nm.clearance = num->clearance;
+        nm.memory_budget = num->memory_budget;
+        c.stack = std::move(st);
+        c.num = nm;
+        c.geo = build_geometry(c.stack, c.num);
+        upload_geometry(c);
+        c.have_geom = true;
+    });
+}
+
+int qps_make_problem(qps_ctx* h, double omega, double theta, int K) {
+    return guarded(h, [&](Ctx& c) {
+        need(c.have_geom, "build_geometry first");
+        c.prob = make_problem(c.stack, c.geo, omega, theta, K);
+        c.have_prob = true;
+        c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
+    });
+}
+
+int qps_problem_info(const qps_ctx* h, int* I, int* K, int* n_nodes, double* k, qps_cplx* alpha, double* y_U,
+                     double* y_D) {
+    return guarded(const_cast<qps_ctx*>(h), [&](Ctx& c) {
+        need(c.have_geom, "build_geometry first");
+        if (I) *I = c.geo.I;
+        if (n_nodes)
+            for (int j = 0; j < c.geo.I; ++j) n_nodes[j] = c.geo.ifaces[j].N();
+        if (y_U) *y_U = c.geo.y_U;
+        if (y_D) *y_D = c.geo.y_D;
+        if (c.have_prob) {
+            if (K) *K = c.prob.K;
+            if (k)
+                for (size_t i = 0; i < c.prob.k.size(); ++i) k[i] = c.prob.k[i];
+            if (alpha) *alpha = qps_cplx{c.prob.ar, c.prob.ai};
+        } else if (K) {
+            *K = 0;
+        }
+    });
+}
+
+int qps_interface_nodes(const qps_ctx* h, int j, double* nodes, double* normals, double* w, double* sp) {
+    return guarded(const_cast<qps_ctx*>(h), [&](Ctx& c) {
+        need(c.have_geom && j >= 0 && j < c.geo.I, "bad interface");
+        const auto& q = c.geo.ifaces[j];
+        for (int i = 0; i < q.N(); ++i) {
+            if (nodes) { nodes[2 * i] = q.x[i]; nodes[2 * i + 1] = q.y[i]; }
+            if (normals) { normals[2 * i] = q.nx[i]; normals[2 * i + 1] = q.ny[i]; }
+            if (w) w[i] = q.w[i];
+            if (sp) sp[i] = q.speed[i];
+        }
+    });
+}
+
+int qps_precompute_shift_blocks(qps_ctx* h) {
+    return guarded(h, [&](Ctx& c) {
+        prepare(c);
+        c.ref_evals = reference_fill_evals(c.geo);
+        c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
+    });
+}
+
+int qps_assemble_system(qps_ctx* h) {
+    return guarded(h, [&](Ctx& c) {
+        prepare(c);
+        run_fill(c);
+        c.ps_separate = true;
+    });
+}
+
+int qps_schur_complement(qps_ctx* h) {
+    return guarded(h, [&](Ctx& c) {
+        need(c.sys_valid, "assemble_system first");
+        Timer t(c, &c.times.schur_ms);
+        const Dims& D = c.dims;
+        const size_t nb2 = size_t(D.nb) * D.nb;
+        c.Apdiag.ensure(D.I * nb2);
+        c.Apsup.ensure(std::max(1, D.I - 1) * nb2);
+        c.Apsub.ensure(std::max(1, D.I - 1) * nb2);
+        QPS_CUDA(cudaMemcpyAsync(c.Apdiag.p, c.Adiag.p, sizeof(cplx) * D.I * nb2, cudaMemcpyDeviceToDevice, c.stream));
+        if (D.I > 1) {
+            QPS_CUDA(cudaMemcpyAsync(c.Apsup.p, c.Asup.p, sizeof(cplx) * (D.I - 1) * nb2, cudaMemcpyDeviceToDevice,
+                                     c.stream));
+            QPS_CUDA(cudaMemcpyAsync(c.Apsub.p, c.Asub.p, sizeof(cplx) * (D.I - 1) * nb2, cudaMemcpyDeviceToDevice,
+                                     c.stream));
+        }
+        schur(c, c.Apdiag.p, c.Apsup.p, c.Apsub.p);
+        c.ps_separate = true;
+    });
+}
+
+int qps_block_lu_solve(qps_ctx* h) {
+    return guarded(h, [&](Ctx& c) {
+        need(c.ps_valid, "schur_complement first");
+        Timer t(c, &c.times.solve_ms);
+        if (c.ps_separate) bcr_solve(c, c.Apdiag.p, c.Apsup.p, c.Apsub.p);
+        else bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+        c.ps_valid = false;  // factors overwrite A'
+    });
+}
+
+int qps_recover_aux(qps_ctx* h) {
+    return guarded(h, [&](Ctx& c) {
+        need(c.eta_valid, "block_lu_solve first");
+        Timer t(c, &c.times.recover_ms);
+        recover(c);
+    });
+}
+
+int qps_solve(qps_ctx* h) {
+    return guarded(h, [&](Ctx& c) {
+        prepare(c);
+        c.ps_separate = false;
+        run_fill(c);
+        c.times.assemble_ms = 0.0;
+        {
+            Timer t(c, &c.times.schur_ms);
+            schur(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+        }
+        c.sys_valid = false;  // A now holds A'
+        {
+            Timer t(c, &c.times.solve_ms);
+            bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+        }
+        c.ps_valid = false;
+        {
+            Timer t(c, &c.times.recover_ms);
+            recover(c);
+        }
+    });
+}
+
+int qps_get_solution(const qps_ctx* h, qps_cplx* eta, qps_cplx* cc, qps_cplx* aU, qps_cplx* aD, double* lsq,
+                     double* max_lsq) {
+    return guarded(const_cast<qps_ctx*>(h), [&](Ctx& c) {
+        need(c.have_sol, "no solution");
+        if (eta) std::memcpy(eta, c.h_eta.data(), sizeof(cplx) * c.h_eta.size());
+        if (cc) std::memcpy(cc, c.h_c.data(), sizeof(cplx) * c.h_c.size());
+        if (aU) std::memcpy(aU, c.h_aU.data(), sizeof(cplx) * c.h_aU.size());
+        if (aD) std::memcpy(aD, c.h_aD.data(), sizeof(cplx) * c.h_aD.size());
+        if (lsq)
+            for (size_t i = 0; i < c.lsq.size(); ++i) lsq[i] = c.lsq[i];
+        if (max_lsq) *max_lsq = c.max_lsq;
+    });
+}
+
+int qps_reflection_transmission(const qps_ctx* h, double* R, double* T, double* fe, double* kappa, qps_cplx* kU,
+                                qps_cplx* kD, int* pu, int* pd) {
+    return guarded(const_cast<qps_ctx*>(h), [&](Ctx& c) {
+        need(c.have_sol, "no solution");
+        host_spectrum(c, R, T, fe, kappa, reinterpret_cast<cplx*>(kU), reinterpret_cast<cplx*>(kD), pu, pd);
+    });
+}
+
+int qps_sweep(qps_ctx* h, int n, const double* theta, int K, int mode, double* R, double* T, double* fe,
+              qps_cplx* aU, qps_cplx* aD, int* status) {
+    return guarded(h, [&](Ctx& c) {
+        need(c.have_prob, "make_problem first (sets omega)");
+        need(K > 0, "sweep needs a fixed K > 0");
+        (void)mode;
+        const double omega = c.prob.omega;
+        const int nrb = 2 * K + 1;
+        for (int a = 0; a < n; ++a) {
+            c.prob = make_problem(c.stack, c.geo, omega, theta[a], K);
+            c.have_prob = true;
+            qps_ctx tmp;
+            int st = QPS_OK;
+            try {
+                prepare(c);
+                c.ps_separate = false;
+                fill_system_fused(c);
+                schur(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+                bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+                recover(c);
+                double r, t, f;
+                host_spectrum(c, &r, &t, &f, nullptr, nullptr, nullptr, nullptr, nullptr);
+                if (R) R[a] = r;
+                if (T) T[a] = t;
+                if (fe) fe[a] = f;
+                for (int i = 0; i < nrb; ++i) {
+                    if (aU) aU[size_t(a) * nrb + i] = qps_cplx{c.h_aU[i].re, c.h_aU[i].im};
+                    if (aD) aD[size_t(a) * nrb + i] = qps_cplx{c.h_aD[i].re, c.h_aD[i].im};
+                }
+            } catch (const Error& e) {
+                st = e.status;
+            }
+            if (status) status[a] = st;
+        }
+    });
+}
+
+int qps_download_block(const qps_ctx* hh, int kind, int i, qps_cplx* out, int* rows, int* cols) {
+    return guarded(const_cast<qps_ctx*>(hh), [&](Ctx& c) {
+        const Dims& D = c.dims;
+        const int I = D.I, nb = D.nb, P = D.P;
+        const size_t nb2 = size_t(nb) * nb;
+        auto rng = [&](int lo, int hi) { need(i >= lo && i < hi, "block index out of range"); };
+        if (kind < 32) {
+            need(c.sys_valid, "assemble_system first (the one-shot path overwrites A with A')");
+            switch (kind) {
+                case QPS_BLK_A_DIAG: rng(0, I); return get_block(c, c.Adiag.p + i * nb2, nb, 2 * D.N[i], 2 * D.N[i], out, rows, cols);
+                case QPS_BLK_A_SUPER: rng(0, I - 1); return get_block(c, c.Asup.p + i * nb2, nb, 2 * D.N[i], 2 * D.N[i + 1], out, rows, cols);
+                case QPS_BLK_A_SUB: rng(0, I - 1); return get_block(c, c.Asub.p + i * nb2, nb, 2 * D.N[i + 1], 2 * D.N[i], out, rows, cols);
+                case QPS_BLK_B_SELF: rng(0, I); return get_block(c, c.Bself.p + size_t(i) * nb * P, nb, 2 * D.N[i], P, out, rows, cols);
+                case QPS_BLK_B_BELOW: rng(0, I); return get_block(c, c.Bbelow.p + size_t(i) * nb * P, nb, 2 * D.N[i], P, out, rows, cols);
+                case QPS_BLK_C_SELF:
+                    rng(0, I + 1);
+                    if (i == I) return zero_block(rows, cols);
+                    if (i == 0) return get_block(c, c.Rc.p, D.mC, D.mI, 2 * D.N[0], out, rows, cols);
+                    return get_block(c, c.Rint.p + size_t(i - 1) * D.mI * 2 * nb + size_t(nb) * D.mI, D.mI, D.mI, 2 * D.N[i], out, rows, cols);
+                case QPS_BLK_C_ABOVE:
+                    rng(0, I + 1);
+                    if (i == 0) return zero_block(rows, cols);
+                    if (i == I) return get_block(c, c.Rc.p + size_t(D.mC) * nb, D.mC, D.mI, 2 * D.N[I - 1], out, rows, cols);
+                    return get_block(c, c.Rint.p + size_t(i - 1) * D.mI * 2 * nb, D.mI, D.mI, 2 * D.N[i - 1], out, rows, cols);
+                case QPS_BLK_Q:
+                    rng(0, I + 1);
+                    if (i == 0) return get_block(c, c.Qc.p, D.mC, D.mI, P, out, rows, cols);
+                    if (i == I) return get_block(c, c.Qc.p + size_t(D.mC) * D.pC, D.mC, D.mI, P, out, rows, cols);
+                    return get_block(c, c.Qint.p + size_t(i - 1) * D.mI * P, D.mI, D.mI, P, out, rows, cols);
+                case QPS_BLK_Z_U: return get_block(c, c.Rc.p + D.mI, D.mC, 2 * D.M, 2 * D.N[0], out, rows, cols);
+                case QPS_BLK_Z_D: return get_block(c, c.Rc.p + size_t(D.mC) * nb + D.mI, D.mC, 2 * D.M, 2 * D.N[I - 1], out, rows, cols);
+                case QPS_BLK_V_U: return get_block(c, c.Qc.p + D.mI, D.mC, 2 * D.M, P, out, rows, cols);
+                case QPS_BLK_V_D: return get_block(c, c.Qc.p + size_t(D.mC) * D.pC + D.mI, D.mC, 2 * D.M, P, out, rows, cols);
+                case QPS_BLK_W_U: return get_block(c, c.Qc.p + size_t(P) * D.mC + D.mI, D.mC, 2 * D.M, D.nrb, out, rows, cols);
+                case QPS_BLK_W_D: return get_block(c, c.Qc.p + size_t(D.mC) * D.pC + size_t(P) * D.mC + D.mI, D.mC, 2 * D.M, D.nrb, out, rows, cols);
+                case QPS_BLK_F: return get_block(c, c.f.p, nb, 2 * D.N[0], 1, out, rows, cols);
+                case QPS_BLK_CP_FIRST: return get_block(c, c.Rc.p, D.mC, D.mC, 2 * D.N[0], out, rows, cols);
+                case QPS_BLK_CP_LAST: return get_block(c, c.Rc.p + size_t(D.mC) * nb, D.mC, D.mC, 2 * D.N[I - 1], out, rows, cols);
+                case QPS_BLK_QP_FIRST: return get_block(c, c.Qc.p, D.mC, D.mC, D.pC, out, rows, cols);
+                case QPS_BLK_QP_LAST: return get_block(c, c.Qc.p + size_t(D.mC) * D.pC, D.mC, D.mC, D.pC, out, rows, cols);
+                case QPS_BLK_BP_FIRST:
+                case QPS_BLK_BP_LAST: {
+                    const int j = kind == QPS_BLK_BP_FIRST ? 0 : I - 1;
+                    const int r = 2 * D.N[j];
+                    if (rows) *rows = r;
+                    if (cols) *cols = D.pC;
+                    if (!out) return;
+                    std::memset(out, 0, sizeof(qps_cplx) * size_t(r) * D.pC);
+                    const cplx* src = (kind == QPS_BLK_BP_FIRST ? c.Bself.p : c.Bbelow.p) + size_t(j) * nb * P;
+                    return get_block(c, src, nb, r, P, out, nullptr, nullptr);
+                }
+                default: fail(QPS_ERR_USAGE, "unknown block kind");
+            }
+        }
+        need(c.ps_valid, "schur_complement first (block_lu_solve overwrites A')");
+        const cplx* Ad = c.ps_separate ? c.Apdiag.p : c.Adiag.p;
+        const cplx* Au = c.ps_separate ? c.Apsup.p : c.Asup.p;
+        const cplx* Al = c.ps_separate ? c.Apsub.p : c.Asub.p;
+        switch (kind) {
+            case QPS_BLK_AP_DIAG: rng(0, I); return get_block(c, Ad + i * nb2, nb, 2 * D.N[i], 2 * D.N[i], out, rows, cols);
+            case QPS_BLK_AP_SUPER: rng(0, I - 1); return get_block(c, Au + i * nb2, nb, 2 * D.N[i], 2 * D.N[i + 1], out, rows, cols);
+            case QPS_BLK_AP_SUB: rng(0, I - 1); return get_block(c, Al + i * nb2, nb, 2 * D.N[i + 1], 2 * D.N[i], out, rows, cols);
+            case QPS_BLK_X_FIRST: return get_block(c, c.Xc.p, D.pC, D.pC, 2 * D.N[0], out, rows, cols);
+            case QPS_BLK_X_LAST: return get_block(c, c.Xc.p + size_t(D.pC) * nb, D.pC, D.pC, 2 * D.N[I - 1], out, rows, cols);
+            case QPS_BLK_X_ABOVE:
+                rng(0, I);
+                if (i == 0) return zero_block(rows, cols);
+                return get_block(c, c.Xint.p + size_t(i - 1) * P * 2 * nb, P, P, 2 * D.N[i - 1], out, rows, cols);
+            case QPS_BLK_X_SELF:
+                rng(0, I);
+                if (i == 0) return zero_block(rows, cols);
+                return get_block(c, c.Xint.p + size_t(i - 1) * P * 2 * nb + size_t(nb) * P, P, P, 2 * D.N[i], out, rows, cols);
+            default: fail(QPS_ERR_USAGE, "unknown block kind");
+        }
+    });
+}
+
+int qps_fill_evals(const qps_ctx* h, uint64_t* reference, uint64_t* performed) {
+    if (!h) return QPS_ERR_USAGE;
+    if (reference) *reference = h->c.ref_evals;
+    if (performed) *performed = h->c.performed_evals;
+    return QPS_OK;
+}
+
+int qps_get_phase_times(const qps_ctx* h, qps_phase_times* t) {
+    if (!h || !t) return QPS_ERR_USAGE;
+    *t = h->c.times;
+    return QPS_OK;
+}
+
+int qps_hankel01(qps_ctx* h, int n, const double* x, qps_cplx* h0, qps_cplx* h1) {
+    return guarded(h, [&](Ctx& c) {
+        for (int i = 0; i < n; ++i)
+            if (!(x[i] > 0.0) || !std::isfinite(x[i]))
+                fail(QPS_ERR_DOMAIN, "hankel01: argument must be finite and > 0");
+        if (n == 0) return;
+        DBuf<double> dx;
+        DBuf<cplx> d0, d1;
+        dx.ensure(n);
+        d0.ensure(n);
+        d1.ensure(n);
+        QPS_CUDA(cudaMemcpyAsync(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+        launch_hankel_batch(n, dx.p, d0.p, d1.p, c.stream);
+        QPS_CUDA(cudaMemcpyAsync(h0, d0.p, sizeof(cplx) * n, cudaMemcpyDeviceToHost, c.stream));
+        QPS_CUDA(cudaMemcpyAsync(h1, d1.p, sizeof(cplx) * n, cudaMemcpyDeviceToHost, c.stream));
+        QPS_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int qps_qsolve(qps_ctx* h, int m, int p, int n, const qps_cplx* Q, const qps_cplx* R, qps_cplx* X, int* rank) {
+    return guarded(h, [&](Ctx& c) {
+        need(m >= p, "qsolve: Q must have at least as many rows as columns");
+        need(m > 0 && p > 0 && n > 0, "qsolve: empty operand");
+        DBuf<cplx> dQ, dR, dX;
+        dQ.ensure(size_t(m) * p);
+        dR.ensure(size_t(m) * n);
+        dX.ensure(size_t(p) * n);
+        QPS_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(cplx) * m * p, cudaMemcpyHostToDevice, c.stream));
+        QPS_CUDA(cudaMemcpyAsync(dR.p, R, sizeof(cplx) * size_t(m) * n, cudaMemcpyHostToDevice, c.stream));
+        CodSet cs;
+        cs.ensure(1, m, p, n);
+        double lsq = 0;
+        qsolve_family_public(c, cs, dQ.p, dR.p, m, size_t(m) * n, dX.p, p, size_t(p) * n, &lsq);
+        QPS_CUDA(cudaMemcpyAsync(X, dX.p, sizeof(cplx) * size_t(p) * n, cudaMemcpyDeviceToHost, c.stream));
+        if (rank) QPS_CUDA(cudaMemcpyAsync(rank, cs.rank.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        QPS_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int qps_debug_zgemm(qps_ctx* h, int M, int N, int K, const qps_cplx* A, const qps_cplx* B, qps_cplx* Cm) {
+    return guarded(h, [&](Ctx& c) {
+        DBuf<cplx> dA, dB, dC;
+        dA.ensure(size_t(M) * K);
+        dB.ensure(size_t(K) * N);
+        dC.ensure(size_t(M) * N);
+        QPS_CUDA(cudaMemcpyAsync(dA.p, A, sizeof(cplx) * size_t(M) * K, cudaMemcpyHostToDevice, c.stream));
+        QPS_CUDA(cudaMemcpyAsync(dB.p, B, sizeof(cplx) * size_t(K) * N, cudaMemcpyHostToDevice, c.stream));
+        std::vector<GemmTask> t(1, GemmTask{});
+        t[0].nseg = 1;
+        t[0].A[0] = dA.p; t[0].lda[0] = M; t[0].B[0] = dB.p; t[0].ldb[0] = K; t[0].K[0] = K;
+        t[0].C = dC.p; t[0].ldc = M;
+        zgemm_batched(M, N, cplx{1, 0}, cplx{0, 0}, t, c.stream, c.ws.gemm_tasks);
+        QPS_CUDA(cudaMemcpyAsync(Cm, dC.p, sizeof(cplx) * size_t(M) * N, cudaMemcpyDeviceToHost, c.stream));
+        QPS_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+// FP64 peak microbenchmarks for the roofline denominators (north star:
+// "FP64 peak measured by a microbenchmark in the same run")
+int qps_measure_fp64_peaks(qps_ctx* h, double* dfma_tflops, double* dmma_tflops) {
+    return guarded(h, [&](Ctx& c) {
+        if (dfma_tflops) *dfma_tflops = measure_dfma_tflops(c.stream);
+        if (dmma_tflops) *dmma_tflops = measure_dmma_tflops(c.stream);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+// Solver context: everything one qps_ctx owns on host and device.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "fill.cuh"
+#include "linalg.cuh"
+
+namespace qpsb {
+
+struct Dims {
+    int I = 0, nb = 0, P = 0, Mw = 0, M = 0, K = 0, nrb = 0;
+    int mI = 0, mC = 0, pC = 0;  // interior Q rows, corner Q' rows / cols
+    std::vector<int> N;
+    bool padded = false;
+};
+
+// COD least-squares state for one family of equal-shape problems
+struct CodSet {
+    int count = 0, m = 0, p = 0, ncols = 0;
+    DBuf<cplx> W, V, tau, zc, M1, Y, QH, Wz, Tb, E;
+    DBuf<int> perm, nzp, rank, flags;
+    DBuf<double> maxpiv, xmax, rmax, enorm, rnorm;
+    CodBatch batch(const cplx* Q) {
+        CodBatch b;
+        b.count = count; b.m = m; b.p = p; b.Q = Q;
+        b.W = W.p; b.V = V.p; b.tau = tau.p; b.zc = zc.p; b.perm = perm.p; b.nzp = nzp.p;
+        b.maxpiv = maxpiv.p; b.rank = rank.p; b.QH = QH.p; b.Wz = Wz.p; b.M1 = M1.p; b.Y = Y.p;
+        return b;
+    }
+    void ensure(int cnt, int m_, int p_, int ncols_) {
+        count = cnt; m = m_; p = p_; ncols = ncols_;
+        const size_t mp = size_t(m) * p;
+        W.ensure(cnt * mp); V.ensure(cnt * mp); M1.ensure(cnt * mp); Y.ensure(cnt * mp); QH.ensure(cnt * mp);
+        Wz.ensure(size_t(cnt) * p * p); Tb.ensure(size_t(cnt) * p * ncols);
+        E.ensure(size_t(cnt) * m * ncols);
+        tau.ensure(size_t(cnt) * p); zc.ensure(size_t(cnt) * p); perm.ensure(size_t(cnt) * p);
+        nzp.ensure(cnt); rank.ensure(cnt); flags.ensure(cnt);
+        maxpiv.ensure(cnt); xmax.ensure(cnt); rmax.ensure(cnt); enorm.ensure(cnt); rnorm.ensure(cnt);
+    }
+};
+
+// One block-tridiagonal system stored as pointer lists (block cyclic reduction)
+struct BcrLevel {
+    std::vector<int> idx;                 // original block index per active position
+    std::vector<cplx*> D, L, U, F;        // per position (L/U may be null at the ends)
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+
+    StackDesc stack;
+    Numerics num;
+    HostGeometry geo;
+    bool have_geom = false;
+    Problem prob;
+    bool have_prob = false;
+    double qsolve_th0 = 1e-14;
+
+    // ---- device geometry pool (SoA) ----
+    DBuf<double> px, py, pnx, pny, pw;
+    std::vector<int> iface_off, wall_off, proxy_off;
+    int U_off = 0, D_off = 0;
+    DBuf<SegDesc> segs;
+    std::vector<int> seg_first;
+    DBuf<double> fourier;
+    DBuf<int> d_err;
+
+    // ---- assembled system (BlockSystem, assembly.hpp:293-315) ----
+    Dims dims;
+    DBuf<cplx> Adiag, Asup, Asub, Bself, Bbelow, Qint, Rint, Qc, Rc, f;
+    bool sys_valid = false;
+    // ---- periodized system (PeriodizedSystem, periodize.hpp:44-56) ----
+    DBuf<cplx> Apdiag, Apsup, Apsub;  // step-wise API keeps A and A' separately
+    bool ps_separate = false, ps_valid = false;
+    DBuf<cplx> Xint, Xc;
+    std::vector<double> lsq;
+    CodSet cod_int, cod_c;
+
+    // ---- block cyclic reduction ----
+    std::vector<BcrLevel> levels;
+    std::vector<DBuf<cplx>> lvlL, lvlU;
+    DBuf<cplx> F, eta;
+    DBuf<int> ipiv, singular;
+    DBuf<cplx*> dptrA, dptrB;
+    DBuf<int*> dptrP;
+    bool eta_valid = false;
+
+    // ---- solution ----
+    DBuf<cplx> csol, aUd, aDd;
+    std::vector<cplx> h_eta, h_c, h_aU, h_aD;
+    bool have_sol = false;
+    double flux_error = 0.0, max_lsq = 0.0;
+
+    // ---- bookkeeping ----
+    qps_phase_times times{};
+    uint64_t ref_evals = 0, performed_evals = 0;
+    Workspace ws;
+    DBuf<PairTask> d_pair;
+    DBuf<ProxyTask> d_proxy;
+    DBuf<AlpertTask> d_alpert;
+    DBuf<int4> d_tiles;
+    std::string err_msg;
+    int err_layer = 0;
+    uint64_t err_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+// geometry / problem
+void upload_geometry(Ctx& c);
+void setup_dims(Ctx& c);
+// one-shot fused single-angle fill of the assembled system (alpha recombination fused)
+void fill_system_fused(Ctx& c);
+// Schur complements in place on (A_diag, A_super, A_sub) or on the A' copies
+void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
+// block cyclic reduction on (Ad, Au, Al) with RHS f; result in c.eta
+void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
+void recover(Ctx& c);
+void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
+                          int ldX, size_t Xstride, double* lsq_out);
+void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,
+                   int* pd);
+
+struct Timer {
+    Ctx& c;
+    double* slot;
+    Timer(Ctx& c_, double* s) : c(c_), slot(s) { QPS_CUDA(cudaEventRecord(c.ev0, c.stream)); }
+    ~Timer() noexcept(false) {
+        QPS_CUDA(cudaEventRecord(c.ev1, c.stream));
+        QPS_CUDA(cudaEventSynchronize(c.ev1));
+        float ms = 0;
+        QPS_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+        *slot = ms;
+    }
+};
+
+}  // namespace qpsb

@@ -1,0 +1,516 @@
+// Nystrom fill kernels for sm_100a (FP64 CUDA-core pipe; transcendental-bound).
+//
+//   pair_fill_kernel   : every plain kernel block of every layer in one launch
+//                        (kernel_quad_block kernels.hpp:78-97 + the alpha
+//                        recombination of assembly.hpp:338-397 fused in)
+//   proxy_fill_kernel  : every proxy block (proxy_block kernels.hpp:294-308;
+//                        B, Q = alpha^-1 Q_p - Q_m, V) in one launch
+//   alpert_kernel      : the 16th-order log correction of every self block
+//                        (self_quad_parts kernels.hpp:180-280) in one launch
+//
+// Tiles are 32 targets x 32 sources, 128 threads; a warp covers 32 consecutive
+// targets of one source column so stores to the column-major blocks are
+// 512-byte coalesced; source nodes are staged in shared memory; the
+// near-field Hankel table sits in shared memory, the far-field one in
+// constant memory (warp-uniform reads).
+#include <algorithm>
+#include <cmath>
+
+#include "alpert_table.h"
+#include "fill.cuh"
+
+namespace qpsb {
+
+namespace {
+__constant__ double c_alpert_nodes[QPS_ALPERT_NAUX];
+__constant__ double c_alpert_weights[QPS_ALPERT_NAUX];
+double* g_near_table = nullptr;
+}  // namespace
+
+void upload_hankel_tables() {
+    static bool done = false;
+    if (done) return;
+    QPS_CUDA(cudaMemcpyToSymbol(c_hankel_far, qps_hankel_far_coeffs, sizeof(qps_hankel_far_coeffs)));
+    QPS_CUDA(cudaMemcpyToSymbol(c_alpert_nodes, qps_alpert_nodes, sizeof(qps_alpert_nodes)));
+    QPS_CUDA(cudaMemcpyToSymbol(c_alpert_weights, qps_alpert_weights, sizeof(qps_alpert_weights)));
+    QPS_CUDA(cudaMalloc(&g_near_table, sizeof(qps_hankel_near_coeffs)));
+    QPS_CUDA(cudaMemcpy(g_near_table, qps_hankel_near_coeffs, sizeof(qps_hankel_near_coeffs),
+                        cudaMemcpyHostToDevice));
+    done = true;
+}
+const double* device_near_table() { return g_near_table; }
+
+namespace {
+
+constexpr int kTile = 32;
+constexpr int kThreads = 128;
+constexpr int kNear = 4 * QPS_HANKEL_NEAR_TERMS * QPS_HANKEL_XB;
+
+__device__ __forceinline__ void load_near(double* s_near, const double* g_near) {
+    for (int i = threadIdx.x; i < kNear; i += blockDim.x) s_near[i] = g_near[i];
+}
+
+__device__ __forceinline__ void cacc(cplx& a, cplx c, double s, cplx v) {
+    // a += s * c * v
+    const double vr = s * v.re, vi = s * v.im;
+    a.re += c.re * vr - c.im * vi;
+    a.im += c.re * vi + c.im * vr;
+}
+
+__device__ __forceinline__ void store(cplx* p, cplx v, int acc) {
+    if (acc) {
+        cplx o = *p;
+        o.re += v.re;
+        o.im += v.im;
+        *p = o;
+    } else {
+        *p = v;
+    }
+}
+
+__device__ __forceinline__ int seg_index(const PairTask& T, int m) {
+    int s = 0;
+    while (s + 1 < T.nseg && m >= T.seg_start[s + 1]) ++s;
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads) pair_fill_kernel(const PairTask* __restrict__ tasks,
+                                                             const int4* __restrict__ tiles, DevPool pool,
+                                                             const double* __restrict__ g_near, int* err) {
+    __shared__ double s_near[kNear];
+    __shared__ double sx[kTile], sy[kTile], snx[kTile], sny[kTile], sw[kTile];
+    __shared__ PairTask T;
+    const int4 tile = tiles[blockIdx.x];
+    if (threadIdx.x == 0) T = tasks[tile.x];
+    load_near(s_near, g_near);
+    __syncthreads();
+    const int m0 = tile.y, j0 = tile.z;
+    if (threadIdx.x < kTile) {
+        const int j = j0 + threadIdx.x;
+        if (j < T.ns) {
+            const int g = T.s_off + j;
+            sx[threadIdx.x] = pool.x[g];
+            sy[threadIdx.x] = pool.y[g];
+            snx[threadIdx.x] = pool.nx[g];
+            sny[threadIdx.x] = pool.ny[g];
+            sw[threadIdx.x] = pool.w[g];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = m0 + lane;
+    if (m >= T.nt) return;
+    const int gt = T.t_off + m;
+    const double tx = pool.x[gt], ty = pool.y[gt], tnx = pool.nx[gt], tny = pool.ny[gt];
+    bool corrected = true;
+    int mseg = 0;
+    if (T.self == 2) {
+        mseg = seg_index(T, m);
+        const int ml = m - T.seg_start[mseg], n = T.seg_start[mseg + 1] - T.seg_start[mseg];
+        corrected = min(ml, n - 1 - ml) >= QPS_ALPERT_A;
+    }
+    for (int q = warp; q < kTile; q += kThreads / 32) {
+        const int j = j0 + q;
+        if (j >= T.ns) break;
+        cplx aD{0, 0}, aS{0, 0}, aT{0, 0}, aDs{0, 0};
+        const double zx0 = sx[q], zy = sy[q], znx = snx[q], zny = sny[q], w = sw[q];
+        for (int t = 0; t < T.nterm; ++t) {
+            const int l = T.lsh[t];
+            if (T.self == 1) {
+                const int off = j + l * T.ns - m;
+                if (off <= QPS_ALPERT_A - 1 && off >= -(QPS_ALPERT_A - 1)) continue;
+            } else if (T.self == 2 && l == 0) {
+                if (j == m) continue;
+                if (corrected && j - m <= QPS_ALPERT_A - 1 && m - j <= QPS_ALPERT_A - 1 && seg_index(T, j) == mseg)
+                    continue;
+            }
+            const double xx = tx + T.tdx[t];
+            const double zx = zx0 + T.sdx[t];
+            const double rvx = xx - zx, rvy = ty - zy;
+            const double r = sqrt(rvx * rvx + rvy * rvy);
+            if (r < 1e-13 * (1.0 + sqrt(xx * xx + ty * ty))) {
+                atomicOr(err, 1);
+                continue;
+            }
+            cplx tD{0, 0}, tS{0, 0}, tT{0, 0}, tDs{0, 0};
+            for (int kk = 0; kk < T.nk; ++kk) {
+                const double k = T.k[kk];
+                HankelOut h;
+                hankel01_eval(k * r, s_near, c_hankel_far, h);
+                KVals v;
+                kernel_vals(k, rvx, rvy, r, tnx, tny, znx, zny, h, v);
+                const double sg = T.ksign[kk];
+                tD.re += sg * v.D.re; tD.im += sg * v.D.im;
+                tS.re += sg * v.S.re; tS.im += sg * v.S.im;
+                tT.re += sg * v.T.re; tT.im += sg * v.T.im;
+                tDs.re += sg * v.Ds.re; tDs.im += sg * v.Ds.im;
+            }
+            const cplx c = T.coef[t];
+            cacc(aD, c, w, tD);
+            cacc(aS, c, w, tS);
+            cacc(aT, c, w, tT);
+            cacc(aDs, c, w, tDs);
+        }
+        if (T.ident && j == m) {
+            aD.re -= 1.0;
+            aDs.re += 1.0;
+        }
+        const size_t o = size_t(j) * T.ld + m;
+        store(T.oD + o, aD, T.accumulate);
+        store(T.oS + o, aS, T.accumulate);
+        store(T.oT + o, aT, T.accumulate);
+        store(T.oDs + o, aDs, T.accumulate);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) proxy_fill_kernel(const ProxyTask* __restrict__ tasks,
+                                                              const int4* __restrict__ tiles, DevPool pool,
+                                                              const double* __restrict__ g_near, int* err) {
+    __shared__ double s_near[kNear];
+    __shared__ double sx[kTile], sy[kTile], snx[kTile], sny[kTile];
+    __shared__ ProxyTask T;
+    const int4 tile = tiles[blockIdx.x];
+    if (threadIdx.x == 0) T = tasks[tile.x];
+    load_near(s_near, g_near);
+    __syncthreads();
+    const int m0 = tile.y, p0 = tile.z;
+    if (threadIdx.x < kTile) {
+        const int p = p0 + threadIdx.x;
+        if (p < T.P) {
+            const int g = T.p_off + p;
+            sx[threadIdx.x] = pool.x[g];
+            sy[threadIdx.x] = pool.y[g];
+            snx[threadIdx.x] = pool.nx[g];
+            sny[threadIdx.x] = pool.ny[g];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = m0 + lane;
+    if (m >= T.nt) return;
+    const int gt = T.t_off + m;
+    const double tx = pool.x[gt], ty = pool.y[gt], tnx = pool.nx[gt], tny = pool.ny[gt];
+    const double k = T.k;
+    for (int q = warp; q < kTile; q += kThreads / 32) {
+        const int p = p0 + q;
+        if (p >= T.P) break;
+        cplx phi{0, 0}, dphi{0, 0};
+        for (int t = 0; t < T.nterm; ++t) {
+            const double xx = tx + T.tdx[t];
+            const double rvx = xx - sx[q], rvy = ty - sy[q];
+            const double r = sqrt(rvx * rvx + rvy * rvy);
+            if (r < 1e-13 * (1.0 + sqrt(xx * xx + ty * ty))) {
+                atomicOr(err, 1);
+                continue;
+            }
+            HankelOut h;
+            hankel01_eval(k * r, s_near, c_hankel_far, h);
+            KVals v;
+            kernel_vals(k, rvx, rvy, r, tnx, tny, snx[q], sny[q], h, v);
+            // phi = D + i k S ; dphi = T + i k D*
+            const cplx f{v.D.re - k * v.S.im, v.D.im + k * v.S.re};
+            const cplx df{v.T.re - k * v.Ds.im, v.T.im + k * v.Ds.re};
+            cacc(phi, T.coef[t], 1.0, f);
+            cacc(dphi, T.coef[t], 1.0, df);
+        }
+        store(T.out + size_t(p) * T.ld + m, phi, T.accumulate);
+        store(T.out + size_t(p) * T.ld + T.drow + m, dphi, T.accumulate);
+    }
+}
+
+// ---- segment parametrisations evaluated on the device (geometry.hpp) ----
+__device__ __forceinline__ double kv(double s, int q) {
+    const double pi = 3.14159265358979323846;
+    const double u = (pi - s) / pi;
+    return (1.0 / q - 0.5) * u * u * u + (s - pi) / (pi * q) + 0.5;
+}
+__device__ __forceinline__ double kvp(double s, int q) {
+    const double pi = 3.14159265358979323846;
+    const double u = (pi - s) / pi;
+    return -3.0 * (1.0 / q - 0.5) * u * u / pi + 1.0 / (pi * q);
+}
+
+__device__ void seg_eval(const SegDesc& sd, const double* fourier, double s, double& zx, double& zy, double& tx,
+                         double& ty) {
+    const double pi = 3.14159265358979323846;
+    if (sd.kind == SEG_LINE) {
+        const int q = sd.q;
+        const double v1 = kv(s, q), v2 = kv(2.0 * pi - s, q);
+        const double vq = pow(v1, double(q)), vr = pow(v2, double(q));
+        const double wv = 2.0 * pi * vq / (vq + vr);
+        const double d1 = q * pow(v1, double(q - 1)) * kvp(s, q);
+        const double d2 = -q * pow(v2, double(q - 1)) * kvp(2.0 * pi - s, q);
+        const double den = vq + vr;
+        const double wp = 2.0 * pi * (d1 * den - vq * (d1 + d2)) / (den * den);
+        const double f = wv / (2.0 * pi);
+        zx = sd.Ax + (sd.Bx - sd.Ax) * f;
+        zy = sd.Ay + (sd.By - sd.Ay) * f;
+        tx = (sd.Bx - sd.Ax) / (2.0 * pi) * wp;
+        ty = (sd.By - sd.Ay) / (2.0 * pi) * wp;
+        return;
+    }
+    const double d = sd.d;
+    const double x = -0.5 * d + d * s / (2.0 * pi);
+    const double dxds = d / (2.0 * pi);
+    double y = sd.y0, dydx = 0.0;
+    if (sd.kind == SEG_SINE) {
+        double sn, cs;
+        sincos(2.0 * pi * x / d + sd.phase, &sn, &cs);
+        y += sd.amp * sn;
+        dydx = sd.amp * (2.0 * pi / d) * cs;
+    } else {
+        const double* cc = fourier + sd.coef_off;
+        const double* ss = cc + sd.ncos;
+        for (int m = 0; m < sd.ncos; ++m) {
+            double sn, cs;
+            sincos(2.0 * pi * double(m + 1) * x / d, &sn, &cs);
+            y += cc[m] * cs;
+            dydx -= cc[m] * (2.0 * pi * double(m + 1) / d) * sn;
+        }
+        for (int m = 0; m < sd.nsin; ++m) {
+            double sn, cs;
+            sincos(2.0 * pi * double(m + 1) * x / d, &sn, &cs);
+            y += ss[m] * sn;
+            dydx += ss[m] * (2.0 * pi * double(m + 1) / d) * cs;
+        }
+    }
+    zx = x;
+    zy = y;
+    tx = dxds;
+    ty = dydx * dxds;
+}
+
+constexpr int kBand = 2 * 16 + 1;  // columns m-16 .. m+16 reached by the stencils
+
+// One warp per corrected row.  Lanes 0..29 evaluate one auxiliary node each
+// (both wavenumbers), then lanes sweep the 33-column window.
+__global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restrict__ tasks, int ntasks,
+                                                     int total_rows, DevPool pool,
+                                                     const SegDesc* __restrict__ segs,
+                                                     const double* __restrict__ fourier,
+                                                     const double* __restrict__ g_near, int* err) {
+    __shared__ double s_near[kNear];
+    __shared__ cplx s_val[4][2 * QPS_ALPERT_NAUX][4];    // per warp, aux, kind
+    __shared__ double s_lw[4][2 * QPS_ALPERT_NAUX][16];  // Lagrange weights
+    __shared__ int s_t0[4][2 * QPS_ALPERT_NAUX];
+    load_near(s_near, g_near);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row = blockIdx.x * 4 + warp;
+    if (row >= total_rows) return;
+    int lo = 0, hi = ntasks - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tasks[mid].row_start <= row) lo = mid; else hi = mid - 1;
+    }
+    const AlpertTask& T = tasks[lo];
+    const int m = row - T.row_start;
+    // locate segment
+    int sidx = 0;
+    for (int s = 1; s < T.nseg; ++s)
+        if (m >= segs[T.seg_first + s].offset) sidx = s;
+    const SegDesc sd = segs[T.seg_first + sidx];
+    const int mloc = m - sd.offset;
+    if (!T.smooth && min(mloc, sd.n - 1 - mloc) < QPS_ALPERT_A) return;  // plain fallback row
+    const double pi = 3.14159265358979323846;
+    const double h = 2.0 * pi / sd.n;
+    const int gt = T.t_off + m;
+    const double xmx = pool.x[gt], xmy = pool.y[gt], nmx = pool.nx[gt], nmy = pool.ny[gt];
+
+    if (lane < 2 * QPS_ALPERT_NAUX) {
+        const int side = lane < QPS_ALPERT_NAUX ? -1 : 1;
+        const int kk = lane % QPS_ALPERT_NAUX;
+        const double xi = side * c_alpert_nodes[kk];
+        const double s_aux = (mloc + 0.5 + xi) * h;
+        double zx, zy, tzx, tzy;
+        seg_eval(sd, fourier, s_aux, zx, zy, tzx, tzy);
+        const double speed = sqrt(tzx * tzx + tzy * tzy);
+        const double nzx = tzy / speed, nzy = -tzx / speed;
+        const double qw = h * c_alpert_weights[kk] * speed;
+        const double rvx = xmx - zx, rvy = xmy - zy;
+        const double r = sqrt(rvx * rvx + rvy * rvy);
+        cplx vD{0, 0}, vS{0, 0}, vT{0, 0}, vDs{0, 0};
+        if (r < 1e-13 * (1.0 + sqrt(xmx * xmx + xmy * xmy))) {
+            atomicOr(err, 1);
+        } else {
+            for (int q = 0; q < T.nk; ++q) {
+                const double k = T.k[q];
+                HankelOut hh;
+                hankel01_eval(k * r, s_near, c_hankel_far, hh);
+                KVals v;
+                kernel_vals(k, rvx, rvy, r, nmx, nmy, nzx, nzy, hh, v);
+                const double sg = T.ksign[q] * qw;
+                vD.re += sg * v.D.re; vD.im += sg * v.D.im;
+                vS.re += sg * v.S.re; vS.im += sg * v.S.im;
+                vT.re += sg * v.T.re; vT.im += sg * v.T.im;
+                vDs.re += sg * v.Ds.re; vDs.im += sg * v.Ds.im;
+            }
+        }
+        s_val[warp][lane][0] = vD;
+        s_val[warp][lane][1] = vS;
+        s_val[warp][lane][2] = vT;
+        s_val[warp][lane][3] = vDs;
+        // alpert_stencil_start (alpert.hpp:90-92), clamped for open arcs (kernels.hpp:256)
+        int t0 = int(floor(xi)) - 16 / 2 + 1;
+        if (!T.smooth) t0 = max(-mloc, min(t0, sd.n - 16 - mloc));
+        s_t0[warp][lane] = t0;
+        // lagrange_weights (alpert.hpp:73-87)
+        for (int rr = 0; rr < 16; ++rr) {
+            double num = 1.0, den = 1.0;
+            const int tr = t0 + rr;
+            for (int qq = 0; qq < 16; ++qq) {
+                if (qq == rr) continue;
+                const int tq = t0 + qq;
+                num *= xi - tq;
+                den *= double(tr - tq);
+            }
+            s_lw[warp][lane][rr] = num / den;
+        }
+    }
+    __syncwarp();
+    const int N = T.N;
+    for (int c = lane; c < kBand; c += 32) {
+        const int o = c - 16;  // column offset relative to the row
+        cplx acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        for (int a = 0; a < 2 * QPS_ALPERT_NAUX; ++a) {
+            const int rr = o - s_t0[warp][a];
+            if (rr < 0 || rr >= 16) continue;
+            const double lw = s_lw[warp][a][rr];
+            for (int kd = 0; kd < 4; ++kd) {
+                acc[kd].re += lw * s_val[warp][a][kd].re;
+                acc[kd].im += lw * s_val[warp][a][kd].im;
+            }
+        }
+        const int jraw = mloc + o;
+        bool any = false;
+        for (int kd = 0; kd < 4; ++kd) any |= (acc[kd].re != 0.0 || acc[kd].im != 0.0);
+        if (T.mode == 0) {
+            if (!any) continue;
+            cplx ph{1.0, 0.0};
+            int col;
+            if (jraw >= 0 && jraw < sd.n) {
+                col = sd.offset + jraw;
+            } else {
+                col = (jraw + N) % N;
+                ph = jraw < 0 ? T.alpha_inv : T.alpha;
+            }
+            const size_t off = size_t(col) * T.ld + m;
+            cplx* outs[4] = {T.oD, T.oS, T.oT, T.oDs};
+            for (int kd = 0; kd < 4; ++kd) {
+                cplx* p = outs[kd] + off;
+                cplx v = *p;
+                v.re += ph.re * acc[kd].re - ph.im * acc[kd].im;
+                v.im += ph.re * acc[kd].im + ph.im * acc[kd].re;
+                *p = v;
+            }
+        } else {
+            if (jraw >= 0 && jraw < sd.n) {
+                if (!any) continue;
+                const size_t off = size_t(sd.offset + jraw) * T.ld + m;
+                cplx* outs[4] = {T.oD, T.oS, T.oT, T.oDs};
+                for (int kd = 0; kd < 4; ++kd) {
+                    cplx* p = outs[kd] + off;
+                    cplx v = *p;
+                    v.re += acc[kd].re;
+                    v.im += acc[kd].im;
+                    *p = v;
+                }
+            } else {
+                // out-of-period: Alpert spill plus (smooth) removal of the band
+                // entry the plain l = +-1 neighbour block carries (kernels.hpp:229-241)
+                if (T.smooth && o >= -(QPS_ALPERT_A - 1) && o <= QPS_ALPERT_A - 1) {
+                    const int col = (jraw + N) % N;
+                    const int l = jraw < 0 ? -1 : 1;
+                    const int gs = T.t_off + col;
+                    const double zx = pool.x[gs] + l * segs[T.seg_first].d, zy = pool.y[gs];
+                    const double rvx = xmx - zx, rvy = xmy - zy;
+                    const double r = sqrt(rvx * rvx + rvy * rvy);
+                    const double wneg = -pool.w[gs];
+                    for (int q = 0; q < T.nk; ++q) {
+                        const double k = T.k[q];
+                        HankelOut hh;
+                        hankel01_eval(k * r, s_near, c_hankel_far, hh);
+                        KVals v;
+                        kernel_vals(k, rvx, rvy, r, nmx, nmy, pool.nx[gs], pool.ny[gs], hh, v);
+                        const double sg = T.ksign[q] * wneg;
+                        acc[0].re += sg * v.D.re; acc[0].im += sg * v.D.im;
+                        acc[1].re += sg * v.S.re; acc[1].im += sg * v.S.im;
+                        acc[2].re += sg * v.T.re; acc[2].im += sg * v.T.im;
+                        acc[3].re += sg * v.Ds.re; acc[3].im += sg * v.Ds.im;
+                    }
+                }
+                cplx* wb = T.wrap + (size_t(m) * kBand + c) * 4;
+                for (int kd = 0; kd < 4; ++kd) wb[kd] = acc[kd];
+            }
+        }
+    }
+}
+
+__global__ void hankel_batch_kernel(int n, const double* __restrict__ x, cplx* h0, cplx* h1,
+                                    const double* __restrict__ g_near) {
+    __shared__ double s_near[kNear];
+    load_near(s_near, g_near);
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        HankelOut h;
+        hankel01_eval(x[i], s_near, c_hankel_far, h);
+        h0[i] = cplx{h.j0, h.y0};
+        h1[i] = cplx{h.j1, h.y1};
+    }
+}
+
+template <class Task>
+void build_tiles(const std::vector<Task>& tasks, std::vector<int4>& tiles, int (*cols)(const Task&)) {
+    tiles.clear();
+    for (int t = 0; t < int(tasks.size()); ++t) {
+        const int nt = tasks[t].nt, nc = cols(tasks[t]);
+        for (int j0 = 0; j0 < nc; j0 += kTile)
+            for (int m0 = 0; m0 < nt; m0 += kTile) tiles.push_back(make_int4(t, m0, j0, 0));
+    }
+}
+
+}  // namespace
+
+void launch_pair_fill(const std::vector<PairTask>& tasks, const DevPool& pool, int* d_err, cudaStream_t s,
+                      DBuf<PairTask>& d_tasks, DBuf<int4>& d_tiles) {
+    if (tasks.empty()) return;
+    std::vector<int4> tiles;
+    build_tiles<PairTask>(tasks, tiles, [](const PairTask& t) { return t.ns; });
+    if (tiles.empty()) return;
+    d_tasks.upload(tasks, s);
+    d_tiles.upload(tiles, s);
+    pair_fill_kernel<<<unsigned(tiles.size()), kThreads, 0, s>>>(d_tasks.p, d_tiles.p, pool, g_near_table, d_err);
+    QPS_CUDA(cudaGetLastError());
+}
+
+void launch_proxy_fill(const std::vector<ProxyTask>& tasks, const DevPool& pool, int* d_err, cudaStream_t s,
+                       DBuf<ProxyTask>& d_tasks, DBuf<int4>& d_tiles) {
+    if (tasks.empty()) return;
+    std::vector<int4> tiles;
+    build_tiles<ProxyTask>(tasks, tiles, [](const ProxyTask& t) { return t.P; });
+    if (tiles.empty()) return;
+    d_tasks.upload(tasks, s);
+    d_tiles.upload(tiles, s);
+    proxy_fill_kernel<<<unsigned(tiles.size()), kThreads, 0, s>>>(d_tasks.p, d_tiles.p, pool, g_near_table, d_err);
+    QPS_CUDA(cudaGetLastError());
+}
+
+void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const DevPool& pool,
+                   const SegDesc* d_segs, const double* d_fourier, int* d_err, cudaStream_t s,
+                   DBuf<AlpertTask>& d_tasks) {
+    if (tasks.empty() || total_rows == 0) return;
+    d_tasks.upload(tasks, s);
+    const int blocks = (total_rows + 3) / 4;
+    alpert_kernel<<<blocks, 128, 0, s>>>(d_tasks.p, int(tasks.size()), total_rows, pool, d_segs, d_fourier,
+                                         g_near_table, d_err);
+    QPS_CUDA(cudaGetLastError());
+}
+
+void launch_hankel_batch(int n, const double* d_x, cplx* d_h0, cplx* d_h1, cudaStream_t s) {
+    if (n <= 0) return;
+    const int blocks = std::min((n + 255) / 256, 148 * 8);
+    hankel_batch_kernel<<<blocks, 256, 0, s>>>(n, d_x, d_h0, d_h1, g_near_table);
+    QPS_CUDA(cudaGetLastError());
+}
+
+}  // namespace qpsb

@@ -1,0 +1,982 @@
+// Batched complex FP64 dense linear algebra on sm_100a.
+//
+// FP64 on Blackwell: tcgen05.mma has no f64 kind, so the tensor path for
+// double precision is the warp-level mma.sync m8n8k4 f64 (SASS DMMA).  The
+// complex GEMM keeps real and imaginary planes of each 64x64x8 tile in shared
+// memory (2-way-conflict-free padding, register double buffering of the next
+// K chunk) and issues four real DMMAs per complex 8x8x4 step:
+//   Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "linalg.cuh"
+
+namespace qpsb {
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+    return cplx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__device__ __forceinline__ cplx cconj(cplx a) { return cplx{a.re, -a.im}; }
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+    // Smith's algorithm
+    if (fabs(b.re) >= fabs(b.im)) {
+        const double r = b.im / b.re, den = b.re + b.im * r;
+        return cplx{(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+    }
+    const double r = b.re / b.im, den = b.re * r + b.im;
+    return cplx{(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+}
+__device__ __forceinline__ double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
+
+constexpr int BM = 64, BN = 64, BK = 8, LDS = 72;
+
+__global__ void __launch_bounds__(128, 2) zgemm_kernel(int M, int N, cplx alpha, cplx beta,
+                                                       const GemmTask* __restrict__ tasks, int tiles_m) {
+    __shared__ double As[2][2][BK][LDS];
+    __shared__ double Bs[2][2][BK][LDS];
+    const GemmTask& T = tasks[blockIdx.y];
+    const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    double acc[4][4][2][2];  // [i][j][re/im][c0/c1]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+
+    const int nseg = T.nseg;
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+        const cplx* __restrict__ A = T.A[sgi];
+        const cplx* __restrict__ B = T.B[sgi];
+        const int lda = T.lda[sgi], ldb = T.ldb[sgi], K = T.K[sgi];
+        const int nchunks = (K + BK - 1) / BK;
+        double2 ra[4], rb[4];
+        auto load = [&](int c) {
+            const int k0 = c * BK;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int idx = tid + 128 * i;
+                const int row = idx & 63, kk = idx >> 6;
+                const int gm = m0 + row, gk = k0 + kk;
+                ra[i] = (gm < M && gk < K) ? __ldg(reinterpret_cast<const double2*>(A + size_t(gk) * lda + gm))
+                                           : make_double2(0.0, 0.0);
+                const int kb = idx & 7, col = idx >> 3;
+                const int gn = n0 + col, gkb = k0 + kb;
+                rb[i] = (gn < N && gkb < K) ? __ldg(reinterpret_cast<const double2*>(B + size_t(gn) * ldb + gkb))
+                                            : make_double2(0.0, 0.0);
+            }
+        };
+        auto stash = [&](int buf) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int idx = tid + 128 * i;
+                const int row = idx & 63, kk = idx >> 6;
+                As[buf][0][kk][row] = ra[i].x;
+                As[buf][1][kk][row] = ra[i].y;
+                const int kb = idx & 7, col = idx >> 3;
+                Bs[buf][0][kb][col] = rb[i].x;
+                Bs[buf][1][kb][col] = rb[i].y;
+            }
+        };
+        if (nchunks > 0) {
+            load(0);
+            stash(0);
+        }
+        __syncthreads();
+        for (int c = 0; c < nchunks; ++c) {
+            const int buf = c & 1;
+            if (c + 1 < nchunks) load(c + 1);
+#pragma unroll
+            for (int ks = 0; ks < BK; ks += 4) {
+                const int kq = ks + (lane & 3), r = lane >> 2;
+                double ar[4], ai[4], nai[4], br[4], bi[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    ar[i] = As[buf][0][kq][wm + 8 * i + r];
+                    ai[i] = As[buf][1][kq][wm + 8 * i + r];
+                    nai[i] = -ai[i];
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    br[j] = Bs[buf][0][kq][wn + 8 * j + r];
+                    bi[j] = Bs[buf][1][kq][wn + 8 * j + r];
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        dmma(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
+                        dmma(acc[i][j][0][0], acc[i][j][0][1], nai[i], bi[j]);
+                        dmma(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);
+                        dmma(acc[i][j][1][0], acc[i][j][1][1], ai[i], br[j]);
+                    }
+            }
+            if (c + 1 < nchunks) stash(buf ^ 1);
+            __syncthreads();
+        }
+    }
+    // epilogue
+    const bool use_beta = (beta.re != 0.0 || beta.im != 0.0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = m0 + wm + 8 * i + (lane >> 2);
+                const int col = n0 + wn + 8 * j + 2 * (lane & 3) + e;
+                if (row < M && col < N) {
+                    const double vr = acc[i][j][0][e], vi = acc[i][j][1][e];
+                    cplx out{alpha.re * vr - alpha.im * vi, alpha.re * vi + alpha.im * vr};
+                    cplx* p = T.C + size_t(col) * T.ldc + row;
+                    if (use_beta) {
+                        const cplx o = *p;
+                        out.re += beta.re * o.re - beta.im * o.im;
+                        out.im += beta.re * o.im + beta.im * o.re;
+                    }
+                    *p = out;
+                }
+            }
+}
+
+// ---------------------------------------------------------------------------
+// block reductions
+// ---------------------------------------------------------------------------
+__device__ double block_sum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += sh[w];
+    __syncthreads();
+    return t;
+}
+
+// first index of the maximum value (Eigen maxCoeff semantics)
+__device__ void block_argmax(double v, int idx, double* shv, int* shi, double& best, int& bidx) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov > v || (ov == v && oi < idx)) {
+            v = ov;
+            idx = oi;
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) {
+        shv[warp] = v;
+        shi[warp] = idx;
+    }
+    __syncthreads();
+    best = shv[0];
+    bidx = shi[0];
+    for (int w = 1; w < nw; ++w)
+        if (shv[w] > best || (shv[w] == best && shi[w] < bidx)) {
+            best = shv[w];
+            bidx = shi[w];
+        }
+    __syncthreads();
+}
+
+constexpr int kMaxP = 256;
+
+// ColPivHouseholderQR::computeInPlace semantics (see oracle shim for the
+// restatement of Eigen's algorithm): largest updated column norm, LAPACK
+// xGEQPF norm downdating with recomputation below sqrt(eps).
+__global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
+    const int pb = blockIdx.x;
+    const int m = b.m, p = b.p, size = min(m, p);
+    const cplx* Q = b.Q + size_t(pb) * m * p;
+    cplx* W = b.W + size_t(pb) * m * p;
+    cplx* tau = b.tau + size_t(pb) * p;
+    int* perm = b.perm + size_t(pb) * p;
+    __shared__ double upd[kMaxP], dir[kMaxP];
+    __shared__ int flag[kMaxP];
+    __shared__ double shv[32];
+    __shared__ int shi[32];
+    __shared__ cplx s_tau, s_den;
+    __shared__ int s_nzp;
+    __shared__ double s_maxpiv;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) W[i] = Q[i];
+    for (int j = tid; j < p; j += blockDim.x) perm[j] = j;
+    __syncthreads();
+    for (int j = warp; j < p; j += nw) {
+        double s = 0.0;
+        for (int i = lane; i < m; i += 32) s += cabs2(W[size_t(j) * m + i]);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) upd[j] = dir[j] = sqrt(s);
+    }
+    __syncthreads();
+    double maxnorm = 0.0;
+    for (int j = 0; j < p; ++j) maxnorm = fmax(maxnorm, upd[j]);
+    const double eps = DBL_EPSILON;
+    const double threshold_helper = (maxnorm * eps) * (maxnorm * eps) / double(m);
+    const double downdate_thr = sqrt(eps);
+    if (tid == 0) {
+        s_nzp = size;
+        s_maxpiv = 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < size; ++k) {
+        double best;
+        int big;
+        {
+            double v = -1.0;
+            int idx = p;
+            for (int j = k + tid; j < p; j += blockDim.x)
+                if (upd[j] > v) { v = upd[j]; idx = j; }
+            block_argmax(v, idx, shv, shi, best, big);
+        }
+        if (tid == 0 && s_nzp == size && best * best < threshold_helper * double(m - k)) s_nzp = k;
+        if (big != k) {
+            for (int i = tid; i < m; i += blockDim.x) {
+                const cplx t = W[size_t(k) * m + i];
+                W[size_t(k) * m + i] = W[size_t(big) * m + i];
+                W[size_t(big) * m + i] = t;
+            }
+            if (tid == 0) {
+                double t = upd[k]; upd[k] = upd[big]; upd[big] = t;
+                t = dir[k]; dir[k] = dir[big]; dir[big] = t;
+                const int ti = perm[k]; perm[k] = perm[big]; perm[big] = ti;
+            }
+        }
+        __syncthreads();
+        // Householder of column k rows k..m-1 (makeHouseholderInPlace)
+        double ts = 0.0;
+        for (int i = k + 1 + tid; i < m; i += blockDim.x) ts += cabs2(W[size_t(k) * m + i]);
+        const double tail_sq = block_sum(ts, shv);
+        if (tid == 0) {
+            const cplx c0 = W[size_t(k) * m + k];
+            double beta;
+            cplx tk;
+            if (tail_sq <= DBL_MIN && c0.im * c0.im <= DBL_MIN) {
+                tk = cplx{0, 0};
+                beta = c0.re;
+                s_den = cplx{0, 0};
+            } else {
+                beta = sqrt(cabs2(c0) + tail_sq);
+                if (c0.re >= 0.0) beta = -beta;
+                s_den = cplx{c0.re - beta, c0.im};
+                tk = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
+            }
+            s_tau = tk;
+            tau[k] = tk;
+            W[size_t(k) * m + k] = cplx{beta, 0.0};
+            s_maxpiv = fmax(s_maxpiv, fabs(beta));
+        }
+        __syncthreads();
+        const cplx den = s_den, tk = s_tau;
+        const bool zero_tau = (tk.re == 0.0 && tk.im == 0.0);
+        for (int i = k + 1 + tid; i < m; i += blockDim.x) {
+            cplx* w = &W[size_t(k) * m + i];
+            *w = (den.re == 0.0 && den.im == 0.0) ? cplx{0, 0} : cdiv(*w, den);
+        }
+        __syncthreads();
+        // apply H = I - tau v v^* to columns k+1..p-1
+        if (!zero_tau || m - k == 1) {
+            for (int j = k + 1 + warp; j < p; j += nw) {
+                cplx* col = W + size_t(j) * m;
+                if (m - k == 1) {
+                    if (lane == 0) col[k] = cmul(col[k], cplx{1.0 - tk.re, -tk.im});
+                    continue;
+                }
+                cplx t{0, 0};
+                for (int i = k + 1 + lane; i < m; i += 32) {
+                    const cplx e = W[size_t(k) * m + i];
+                    const cplx a = col[i];
+                    t.re += e.re * a.re + e.im * a.im;
+                    t.im += e.re * a.im - e.im * a.re;
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    t.re += __shfl_xor_sync(0xffffffffu, t.re, o);
+                    t.im += __shfl_xor_sync(0xffffffffu, t.im, o);
+                }
+                const cplx ck = col[k];
+                t.re += ck.re;
+                t.im += ck.im;
+                t = cmul(tk, t);
+                for (int i = k + 1 + lane; i < m; i += 32) {
+                    const cplx e = W[size_t(k) * m + i];
+                    const cplx et = cmul(e, t);
+                    col[i].re -= et.re;
+                    col[i].im -= et.im;
+                }
+                if (lane == 0) {
+                    col[k].re -= t.re;
+                    col[k].im -= t.im;
+                }
+            }
+        }
+        __syncthreads();
+        // norm downdate (LAWN 176)
+        for (int j = k + 1 + tid; j < p; j += blockDim.x) {
+            flag[j] = 0;
+            if (upd[j] != 0.0) {
+                const cplx a = W[size_t(j) * m + k];
+                double t = sqrt(cabs2(a)) / upd[j];
+                t = (1.0 + t) * (1.0 - t);
+                t = t < 0.0 ? 0.0 : t;
+                const double t2 = t * (upd[j] / dir[j]) * (upd[j] / dir[j]);
+                if (t2 <= downdate_thr) flag[j] = 1;
+                else upd[j] *= sqrt(t);
+            }
+        }
+        __syncthreads();
+        for (int j = k + 1 + warp; j < p; j += nw) {
+            if (!flag[j]) continue;
+            double s = 0.0;
+            for (int i = k + 1 + lane; i < m; i += 32) s += cabs2(W[size_t(j) * m + i]);
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) upd[j] = dir[j] = sqrt(s);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        b.nzp[pb] = s_nzp;
+        b.maxpiv[pb] = s_maxpiv;
+    }
+}
+
+__global__ void cod_rank_kernel(CodBatch b, double th, const int* __restrict__ flags) {
+    const int pb = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pb >= b.count) return;
+    if (flags && !flags[pb]) return;
+    const cplx* W = b.W + size_t(pb) * b.m * b.p;
+    const double pre = b.maxpiv[pb] * th;
+    int r = 0;
+    for (int i = 0; i < b.nzp[pb]; ++i) r += sqrt(cabs2(W[size_t(i) * b.m + i])) > pre;
+    b.rank[pb] = r;
+}
+
+// Complete orthogonal decomposition at the current rank
+// (CompleteOrthogonalDecomposition::computeInPlace semantics): RZ reduction of
+// [R11 R12] in V, then the two orthonormal factors of the min-norm solve
+//   QH = Q_r^* restricted to its first r rows   (p x m, rows >= r zero)
+//   Wz = P Z^* [I_r; 0]                          (p x p, cols >= r zero)
+// so that X = Wz * T11^{-1} * (QH * RHS) (_solve_impl order: Q^*, T^{-1}, Z^*, P).
+__global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int* __restrict__ flags) {
+    const int pb = blockIdx.x;
+    if (flags && !flags[pb]) return;
+    const int m = b.m, p = b.p;
+    const cplx* W = b.W + size_t(pb) * m * p;
+    cplx* V = b.V + size_t(pb) * m * p;
+    const cplx* tau = b.tau + size_t(pb) * p;
+    cplx* zc = b.zc + size_t(pb) * p;
+    const int* perm = b.perm + size_t(pb) * p;
+    cplx* M1 = b.M1 + size_t(pb) * m * p;
+    cplx* Y = b.Y + size_t(pb) * p * m;
+    cplx* QH = b.QH + size_t(pb) * p * m;
+    cplx* Wz = b.Wz + size_t(pb) * p * p;
+    const int r = b.rank[pb];
+    const int tid = threadIdx.x;
+    __shared__ double shv[32];
+    __shared__ cplx s_den, s_zc;
+    for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) V[i] = W[i];
+    if (r == 0) {
+        for (size_t i = tid; i < size_t(p) * m; i += blockDim.x) QH[i] = cplx{0, 0};
+        for (size_t i = tid; i < size_t(p) * p; i += blockDim.x) Wz[i] = cplx{0, 0};
+        return;
+    }
+    __syncthreads();
+    auto vat = [&](int i, int j) -> cplx& { return V[size_t(j) * m + i]; };
+    if (r < p) {
+        for (int k = r - 1; k >= 0; --k) {
+            if (k != r - 1)
+                for (int i = tid; i <= k; i += blockDim.x) {
+                    const cplx t = vat(i, k);
+                    vat(i, k) = vat(i, r - 1);
+                    vat(i, r - 1) = t;
+                }
+            __syncthreads();
+            const int L = p - r + 1;
+            double ts = 0.0;
+            for (int j = 1 + tid; j < L; j += blockDim.x) ts += cabs2(vat(k, r - 1 + j));
+            const double tail_sq = block_sum(ts, shv);
+            if (tid == 0) {
+                const cplx c0 = vat(k, r - 1);
+                double beta;
+                cplx tk;
+                if (tail_sq <= DBL_MIN && c0.im * c0.im <= DBL_MIN) {
+                    tk = cplx{0, 0};
+                    beta = c0.re;
+                    s_den = cplx{0, 0};
+                } else {
+                    beta = sqrt(cabs2(c0) + tail_sq);
+                    if (c0.re >= 0.0) beta = -beta;
+                    s_den = cplx{c0.re - beta, c0.im};
+                    tk = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
+                }
+                s_zc = tk;
+                zc[k] = tk;
+                vat(k, r - 1) = cplx{beta, 0.0};
+            }
+            __syncthreads();
+            const cplx den = s_den, tk = s_zc;
+            for (int j = 1 + tid; j < L; j += blockDim.x) {
+                cplx& e = vat(k, r - 1 + j);
+                e = (den.re == 0.0 && den.im == 0.0) ? cplx{0, 0} : cdiv(e, den);
+            }
+            __syncthreads();
+            if (k > 0 && !(tk.re == 0.0 && tk.im == 0.0)) {
+                for (int i = tid; i < k; i += blockDim.x) {
+                    cplx t = vat(i, r - 1);
+                    for (int j = 1; j < L; ++j) {
+                        const cplx e = vat(k, r - 1 + j);
+                        const cplx a = vat(i, r - 1 + j);
+                        t.re += a.re * e.re + a.im * e.im;
+                        t.im += a.im * e.re - a.re * e.im;
+                    }
+                    t = cmul(t, tk);
+                    vat(i, r - 1).re -= t.re;
+                    vat(i, r - 1).im -= t.im;
+                    for (int j = 1; j < L; ++j) {
+                        const cplx te = cmul(t, vat(k, r - 1 + j));
+                        vat(i, r - 1 + j).re -= te.re;
+                        vat(i, r - 1 + j).im -= te.im;
+                    }
+                }
+            }
+            __syncthreads();
+            if (k != r - 1)
+                for (int i = tid; i <= k; i += blockDim.x) {
+                    const cplx t = vat(i, k);
+                    vat(i, k) = vat(i, r - 1);
+                    vat(i, r - 1) = t;
+                }
+            __syncthreads();
+        }
+    }
+    // M1 = Q_r E_r (m x r), Q_r = H_0^* ... H_{r-1}^*  (reflectors as applied had tau)
+    for (int c = tid; c < r; c += blockDim.x) {
+        cplx* col = M1 + size_t(c) * m;
+        for (int i = 0; i < m; ++i) col[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
+        for (int kk = c; kk >= 0; --kk) {
+            const cplx tk = cconj(tau[kk]);
+            if (tk.re == 0.0 && tk.im == 0.0) continue;
+            cplx t = col[kk];
+            for (int i = kk + 1; i < m; ++i) {
+                const cplx e = W[size_t(kk) * m + i];
+                t.re += e.re * col[i].re + e.im * col[i].im;
+                t.im += e.re * col[i].im - e.im * col[i].re;
+            }
+            t = cmul(tk, t);
+            col[kk].re -= t.re;
+            col[kk].im -= t.im;
+            for (int i = kk + 1; i < m; ++i) {
+                const cplx et = cmul(W[size_t(kk) * m + i], t);
+                col[i].re -= et.re;
+                col[i].im -= et.im;
+            }
+        }
+    }
+    __syncthreads();
+    for (int c = tid; c < m; c += blockDim.x)
+        for (int i = 0; i < p; ++i) QH[size_t(c) * p + i] = i < r ? cconj(M1[size_t(i) * m + c]) : cplx{0, 0};
+    // Wz columns: P Z^* e_c for c < r
+    for (int c = tid; c < p; c += blockDim.x) {
+        cplx* y = Y + size_t(c) * p;
+        cplx* w = Wz + size_t(c) * p;
+        if (c >= r) {
+            for (int i = 0; i < p; ++i) w[i] = cplx{0, 0};
+            continue;
+        }
+        for (int i = 0; i < p; ++i) y[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
+        if (r < p) {
+            for (int k = 0; k < r; ++k) {
+                const cplx tk = zc[k];
+                if (k != r - 1) {
+                    const cplx t = y[k];
+                    y[k] = y[r - 1];
+                    y[r - 1] = t;
+                }
+                if (!(tk.re == 0.0 && tk.im == 0.0)) {
+                    cplx t = y[r - 1];
+                    for (int j = 0; j < p - r; ++j) {
+                        const cplx e = cmul(vat(k, r + j), y[r + j]);
+                        t.re += e.re;
+                        t.im += e.im;
+                    }
+                    t = cmul(t, tk);
+                    y[r - 1].re -= t.re;
+                    y[r - 1].im -= t.im;
+                    for (int j = 0; j < p - r; ++j) {
+                        const cplx e = cmul(cconj(vat(k, r + j)), t);
+                        y[r + j].re -= e.re;
+                        y[r + j].im -= e.im;
+                    }
+                }
+                if (k != r - 1) {
+                    const cplx t = y[k];
+                    y[k] = y[r - 1];
+                    y[r - 1] = t;
+                }
+            }
+        }
+        for (int i = 0; i < p; ++i) w[perm[i]] = y[i];
+    }
+}
+
+// back substitution with T11 (upper, r x r inside V, ld m), one thread per column
+__global__ void cod_trsm_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
+                                const int* __restrict__ flags) {
+    const int pb = blockIdx.y;
+    if (flags && !flags[pb]) return;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncols) return;
+    const int m = b.m, r = b.rank[pb];
+    const cplx* V = b.V + size_t(pb) * m * b.p;
+    cplx* x = B + stride * pb + size_t(c) * ldb;
+    for (int i = r - 1; i >= 0; --i) {
+        cplx s = x[i];
+        for (int l = i + 1; l < r; ++l) {
+            const cplx t = cmul(V[size_t(l) * m + i], x[l]);
+            s.re -= t.re;
+            s.im -= t.im;
+        }
+        x[i] = cdiv(s, V[size_t(i) * m + i]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// LU (partial pivoting on the modulus, like Eigen's PartialPivLU)
+// ---------------------------------------------------------------------------
+constexpr int kNB = 32;
+
+__global__ void __launch_bounds__(256) lu_panel_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+                                                       int* const* __restrict__ Pp, int k0, int* singular) {
+    cplx* A = Ap[blockIdx.x];
+    int* ipiv = Pp[blockIdx.x];
+    const int kend = min(k0 + kNB, n);
+    __shared__ double shv[32];
+    __shared__ int shi[32];
+    const int tid = threadIdx.x;
+    for (int k = k0; k < kend; ++k) {
+        double v = -1.0;
+        int idx = n;
+        for (int i = k + tid; i < n; i += blockDim.x) {
+            const double a = sqrt(cabs2(A[size_t(k) * ld + i]));
+            if (a > v) { v = a; idx = i; }
+        }
+        double best;
+        int piv;
+        block_argmax(v, idx, shv, shi, best, piv);
+        if (tid == 0) ipiv[k] = piv;
+        if (piv != k)
+            for (int j = k0 + tid; j < kend; j += blockDim.x) {
+                const cplx t = A[size_t(j) * ld + k];
+                A[size_t(j) * ld + k] = A[size_t(j) * ld + piv];
+                A[size_t(j) * ld + piv] = t;
+            }
+        __syncthreads();
+        const cplx d = A[size_t(k) * ld + k];
+        if (d.re == 0.0 && d.im == 0.0) {
+            if (tid == 0) singular[blockIdx.x] = 1;
+        } else {
+            const cplx inv = cdiv(cplx{1.0, 0.0}, d);
+            for (int i = k + 1 + tid; i < n; i += blockDim.x) A[size_t(k) * ld + i] = cmul(A[size_t(k) * ld + i], inv);
+        }
+        __syncthreads();
+        for (int i = k + 1 + tid; i < n; i += blockDim.x) {
+            const cplx l = A[size_t(k) * ld + i];
+            for (int j = k + 1; j < kend; ++j) {
+                const cplx u = A[size_t(j) * ld + k];
+                const cplx t = cmul(l, u);
+                A[size_t(j) * ld + i].re -= t.re;
+                A[size_t(j) * ld + i].im -= t.im;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// apply the interchanges of rows k0..kend-1 to columns outside [c_skip0, c_skip1)
+__global__ void lu_swap_kernel(int n, int ld, cplx* const* __restrict__ Ap, const int* const* __restrict__ Pp,
+                               int k0, int kend, int ncols, int c_skip0, int c_skip1) {
+    cplx* A = Ap[blockIdx.y];
+    const int* ipiv = Pp[blockIdx.y];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncols || (c >= c_skip0 && c < c_skip1)) return;
+    cplx* col = A + size_t(c) * ld;
+    for (int k = k0; k < kend; ++k) {
+        const int p = ipiv[k];
+        if (p != k) {
+            const cplx t = col[k];
+            col[k] = col[p];
+            col[p] = t;
+        }
+    }
+}
+
+// rows r0..r1-1 of B_b <- L11^{-1} (unit lower, diagonal block of A_b) B, columns c0..c0+nc-1
+__global__ void trsm_lower_unit_kernel(int ld, const cplx* const* __restrict__ Ap, cplx* const* __restrict__ Bp,
+                                       int ldb, int r0, int r1, int c0, int nc) {
+    const cplx* A = Ap[blockIdx.y];
+    cplx* B = Bp[blockIdx.y];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    cplx* x = B + size_t(c0 + c) * ldb;
+    for (int i = r0; i < r1; ++i) {
+        cplx s = x[i];
+        for (int l = r0; l < i; ++l) {
+            const cplx t = cmul(A[size_t(l) * ld + i], x[l]);
+            s.re -= t.re;
+            s.im -= t.im;
+        }
+        x[i] = s;
+    }
+}
+
+// rows r0..r1-1 of B_b <- U11^{-1} B (upper, non-unit)
+__global__ void trsm_upper_kernel(int ld, const cplx* const* __restrict__ Ap, cplx* const* __restrict__ Bp, int ldb,
+                                  int r0, int r1, int nc) {
+    const cplx* A = Ap[blockIdx.y];
+    cplx* B = Bp[blockIdx.y];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    cplx* x = B + size_t(c) * ldb;
+    for (int i = r1 - 1; i >= r0; --i) {
+        cplx s = x[i];
+        for (int l = i + 1; l < r1; ++l) {
+            const cplx t = cmul(A[size_t(l) * ld + i], x[l]);
+            s.re -= t.re;
+            s.im -= t.im;
+        }
+        x[i] = cdiv(s, A[size_t(i) * ld + i]);
+    }
+}
+
+__global__ void rowswap_rhs_kernel(int n, const int* const* __restrict__ Pp, cplx* const* __restrict__ Bp, int ldb,
+                                   int nc) {
+    const int* ipiv = Pp[blockIdx.y];
+    cplx* B = Bp[blockIdx.y];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    cplx* x = B + size_t(c) * ldb;
+    for (int k = 0; k < n; ++k) {
+        const int p = ipiv[k];
+        if (p != k) {
+            const cplx t = x[k];
+            x[k] = x[p];
+            x[p] = t;
+        }
+    }
+}
+
+__global__ void maxabs_kernel(const cplx* X, int m, int n, int ld, size_t stride, double* out) {
+    const cplx* A = X + stride * blockIdx.x;
+    double v = 0.0;
+    for (int j = 0; j < n; ++j)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) v = fmax(v, sqrt(cabs2(A[size_t(j) * ld + i])));
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t = fmax(t, sh[w]);
+        out[blockIdx.x] = t;
+    }
+}
+
+__global__ void fro_kernel(const cplx* X, int m, int n, int ld, size_t stride, double* out) {
+    const cplx* A = X + stride * blockIdx.x;
+    __shared__ double sh[32];
+    double mx = 0.0;
+    for (int j = 0; j < n; ++j)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, sqrt(cabs2(A[size_t(j) * ld + i])));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    double big = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) big = fmax(big, sh[w]);
+    __syncthreads();
+    double s = 0.0;
+    if (big > 0.0) {
+        const double inv = 1.0 / big;
+        for (int j = 0; j < n; ++j)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const cplx a = A[size_t(j) * ld + i];
+                s += (a.re * inv) * (a.re * inv) + (a.im * inv) * (a.im * inv);
+            }
+    }
+    const double tot = block_sum(s, sh);
+    if (threadIdx.x == 0) out[blockIdx.x] = big * sqrt(tot);
+}
+
+__global__ void copy_blocks_kernel(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride,
+                                   int m, int n) {
+    const cplx* S = src + sstride * blockIdx.y;
+    cplx* D = dst + dstride * blockIdx.y;
+    for (size_t e = blockIdx.x * blockDim.x + threadIdx.x; e < size_t(m) * n; e += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % m), j = int(e / m);
+        D[size_t(j) * ldd + i] = S[size_t(j) * lds + i];
+    }
+}
+
+__global__ void zgemv_kernel(int M, cplx alpha, cplx beta, const GemvTask* __restrict__ tasks) {
+    const GemvTask& T = tasks[blockIdx.y];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    cplx acc{0, 0};
+    for (int sgi = 0; sgi < T.nseg; ++sgi) {
+        const cplx* A = T.A[sgi];
+        const cplx* x = T.x[sgi];
+        const int lda = T.lda[sgi];
+        for (int j = 0; j < T.n[sgi]; ++j) {
+            const cplx t = cmul(A[size_t(j) * lda + i], x[j]);
+            acc.re += t.re;
+            acc.im += t.im;
+        }
+    }
+    cplx out = cmul(alpha, acc);
+    if (beta.re != 0.0 || beta.im != 0.0) {
+        const cplx o = cmul(beta, T.y[i]);
+        out.re += o.re;
+        out.im += o.im;
+    }
+    T.y[i] = out;
+}
+
+// ---- FP64 peak microbenchmarks ----
+__global__ void dfma_peak_kernel(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+           a7 = a0 + 7;
+    const double b = 0.999999, c = 1e-7;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+        }
+    }
+    const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[0] = s;
+}
+
+__global__ void dmma_peak_kernel(double* out, int iters) {
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+    const double a = 1e-3 * (threadIdx.x & 7), b = 1e-3 * (threadIdx.x >> 3);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) out[0] = s;
+}
+
+}  // namespace
+
+void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
+                   DBuf<GemmTask>& d_tasks) {
+    if (tasks.empty() || M <= 0 || N <= 0) return;
+    d_tasks.upload(tasks, s);
+    const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+    for (size_t off = 0; off < tasks.size(); off += 65535) {
+        const unsigned cnt = unsigned(std::min<size_t>(65535, tasks.size() - off));
+        zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
+    }
+    QPS_CUDA(cudaGetLastError());
+}
+
+void cod_factor(const CodBatch& b, cudaStream_t s) {
+    if (b.count == 0) return;
+    if (b.p > kMaxP) fail(QPS_ERR_CONFIG, "qsolve: too many columns for the device COD (max 256)");
+    if (b.m < b.p) fail(QPS_ERR_USAGE, "qsolve: Q must have at least as many rows as columns");
+    cod_factor_kernel<<<b.count, 256, 0, s>>>(b);
+    QPS_CUDA(cudaGetLastError());
+}
+void cod_rank(const CodBatch& b, double th, const int* flags, cudaStream_t s) {
+    if (b.count == 0) return;
+    cod_rank_kernel<<<(b.count + 127) / 128, 128, 0, s>>>(b, th, flags);
+    QPS_CUDA(cudaGetLastError());
+}
+void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
+    if (b.count == 0) return;
+    cod_operator_kernel<<<b.count, 256, 0, s>>>(b, flags);
+    QPS_CUDA(cudaGetLastError());
+}
+void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, const int* flags, cudaStream_t s) {
+    if (b.count == 0 || ncols == 0) return;
+    cod_trsm_kernel<<<dim3((ncols + 127) / 128, b.count), 128, 0, s>>>(b, B, ldb, stride, ncols, flags);
+    QPS_CUDA(cudaGetLastError());
+}
+
+
+void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP, int* d_singular,
+                       cudaStream_t s, Workspace& ws) {
+    const int count = int(hA.size());
+    if (count == 0) return;
+    ws.ptrs.upload(hA, s);
+    ws.iptrs.upload(hP, s);
+    cplx* const* d_A = ws.ptrs.p;
+    int* const* d_ipiv = ws.iptrs.p;
+    for (int k0 = 0; k0 < n; k0 += kNB) {
+        const int kend = std::min(k0 + kNB, n);
+        lu_panel_kernel<<<count, 256, 0, s>>>(n, ld, d_A, d_ipiv, k0, d_singular);
+        QPS_CUDA(cudaGetLastError());
+        lu_swap_kernel<<<dim3((n + 127) / 128, count), 128, 0, s>>>(n, ld, d_A, d_ipiv, k0, kend, n, k0, kend);
+        QPS_CUDA(cudaGetLastError());
+        const int rest = n - kend;
+        if (rest > 0) {
+            trsm_lower_unit_kernel<<<dim3((rest + 127) / 128, count), 128, 0, s>>>(
+                ld, reinterpret_cast<const cplx* const*>(d_A), d_A, ld, k0, kend, kend, rest);
+            QPS_CUDA(cudaGetLastError());
+            auto& tasks = ws.h_gemm;
+            tasks.assign(count, GemmTask{});
+            for (int b = 0; b < count; ++b) {
+                GemmTask& t = tasks[b];
+                t.nseg = 1;
+                t.A[0] = hA[b] + size_t(k0) * ld + kend;
+                t.lda[0] = ld;
+                t.B[0] = hA[b] + size_t(kend) * ld + k0;
+                t.ldb[0] = ld;
+                t.K[0] = kend - k0;
+                t.C = hA[b] + size_t(kend) * ld + kend;
+                t.ldc = ld;
+            }
+            zgemm_batched(rest, rest, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+        }
+    }
+}
+
+void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,
+                      const std::vector<cplx*>& hB, int ldb, int nrhs, cudaStream_t s, Workspace& ws) {
+    const int count = int(hA.size());
+    if (count == 0 || nrhs == 0) return;
+    ws.ptrs.upload(hA, s);
+    ws.ptrs2.upload(hB, s);
+    ws.iptrs.upload(hP, s);
+    const cplx* const* d_A = ws.ptrs.p;
+    cplx* const* d_B = ws.ptrs2.p;
+    const int* const* d_ipiv = ws.iptrs.p;
+    const dim3 g((nrhs + 127) / 128, count);
+    rowswap_rhs_kernel<<<g, 128, 0, s>>>(n, d_ipiv, d_B, ldb, nrhs);
+    QPS_CUDA(cudaGetLastError());
+    auto& tasks = ws.h_gemm;
+    for (int k0 = 0; k0 < n; k0 += kNB) {
+        const int kend = std::min(k0 + kNB, n);
+        trsm_lower_unit_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, 0, nrhs);
+        QPS_CUDA(cudaGetLastError());
+        if (kend < n) {
+            tasks.assign(count, GemmTask{});
+            for (int b = 0; b < count; ++b) {
+                GemmTask& t = tasks[b];
+                t.nseg = 1;
+                t.A[0] = hA[b] + size_t(k0) * ld + kend;
+                t.lda[0] = ld;
+                t.B[0] = hB[b] + k0;
+                t.ldb[0] = ldb;
+                t.K[0] = kend - k0;
+                t.C = hB[b] + kend;
+                t.ldc = ldb;
+            }
+            zgemm_batched(n - kend, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+        }
+    }
+    const int nblk = (n + kNB - 1) / kNB;
+    for (int bi = nblk - 1; bi >= 0; --bi) {
+        const int k0 = bi * kNB, kend = std::min(k0 + kNB, n);
+        trsm_upper_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, nrhs);
+        QPS_CUDA(cudaGetLastError());
+        if (k0 > 0) {
+            tasks.assign(count, GemmTask{});
+            for (int b = 0; b < count; ++b) {
+                GemmTask& t = tasks[b];
+                t.nseg = 1;
+                t.A[0] = hA[b] + size_t(k0) * ld;
+                t.lda[0] = ld;
+                t.B[0] = hB[b] + k0;
+                t.ldb[0] = ldb;
+                t.K[0] = kend - k0;
+                t.C = hB[b];
+                t.ldc = ldb;
+            }
+            zgemm_batched(k0, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+        }
+    }
+}
+
+void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {
+    if (count == 0) return;
+    maxabs_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out);
+    QPS_CUDA(cudaGetLastError());
+}
+void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {
+    if (count == 0) return;
+    fro_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out);
+    QPS_CUDA(cudaGetLastError());
+}
+void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride, int m, int n,
+                 int count, cudaStream_t s) {
+    if (count == 0 || m == 0 || n == 0) return;
+    const int bx = int(std::min<size_t>((size_t(m) * n + 255) / 256, 1024));
+    copy_blocks_kernel<<<dim3(bx, count), 256, 0, s>>>(src, lds, sstride, dst, ldd, dstride, m, n);
+    QPS_CUDA(cudaGetLastError());
+}
+void zgemv_batched(int M, cplx alpha, cplx beta, const std::vector<GemvTask>& tasks, cudaStream_t s,
+                   DBuf<GemvTask>& d_tasks) {
+    if (tasks.empty() || M <= 0) return;
+    d_tasks.upload(tasks, s);
+    zgemv_kernel<<<dim3((M + 127) / 128, unsigned(tasks.size())), 128, 0, s>>>(M, alpha, beta, d_tasks.p);
+    QPS_CUDA(cudaGetLastError());
+}
+
+double measure_dfma_tflops(cudaStream_t s) {
+    DBuf<double> out;
+    out.ensure(1);
+    const int iters = 4096, blocks = 148 * 8, threads = 256;
+    dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, 64);
+    cudaEvent_t e0, e1;
+    QPS_CUDA(cudaEventCreate(&e0));
+    QPS_CUDA(cudaEventCreate(&e1));
+    QPS_CUDA(cudaEventRecord(e0, s));
+    dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, iters);
+    QPS_CUDA(cudaEventRecord(e1, s));
+    QPS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    QPS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 64.0 * iters * double(blocks) * threads;
+    return flops / (ms * 1e-3) / 1e12;
+}
+
+double measure_dmma_tflops(cudaStream_t s) {
+    DBuf<double> out;
+    out.ensure(1);
+    const int iters = 4096, blocks = 148 * 8, threads = 256;
+    dmma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, 64);
+    cudaEvent_t e0, e1;
+    QPS_CUDA(cudaEventCreate(&e0));
+    QPS_CUDA(cudaEventCreate(&e1));
+    QPS_CUDA(cudaEventRecord(e0, s));
+    dmma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, iters);
+    QPS_CUDA(cudaEventRecord(e1, s));
+    QPS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    QPS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 512.0 * 8.0 * iters * double(blocks) * (threads / 32);
+    return flops / (ms * 1e-3) / 1e12;
+}
+
+}  // namespace qpsb

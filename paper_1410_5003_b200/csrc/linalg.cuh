@@ -1,0 +1,97 @@
+// Batched complex FP64 dense linear algebra for sm_100a.
+//   zgemm_batched : DMMA (mma.sync m8n8k4 f64) complex GEMM, 4 real MMAs per
+//                   complex product, optional K-concatenation of two products
+//   COD least squares (periodize.hpp:25-39): Eigen-semantics column-pivoted QR,
+//                   rank at a threshold, RZ reduction, min-norm operator
+//   LU with partial pivoting + triangular solves for block cyclic reduction
+#pragma once
+
+#include "hankel.cuh"
+#include "qps_internal.h"
+
+namespace qpsb {
+
+// C = beta C + alpha * sum_s A_s B_s, A_s: M x K_s (lda), B_s: K_s x N (ldb).
+struct GemmTask {
+    const cplx* A[2];
+    const cplx* B[2];
+    int lda[2], ldb[2], K[2];
+    int nseg;
+    cplx* C;
+    int ldc;
+};
+
+struct Workspace;  // forward
+
+void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
+                   DBuf<GemmTask>& d_tasks);
+
+// ---- COD least squares -----------------------------------------------------
+// Per problem b: Q_b (m x p, ld m).  Factor state lives in caller-provided
+// device arrays sized for `count` problems.
+struct CodBatch {
+    int count = 0, m = 0, p = 0;
+    const cplx* Q = nullptr;  // count x (m*p), column-major, ld m
+    cplx* W = nullptr;        // factored CPQR (count x m*p)
+    cplx* V = nullptr;        // RZ work copy (count x m*p)
+    cplx* tau = nullptr;      // count x p
+    cplx* zc = nullptr;       // count x p
+    int* perm = nullptr;      // count x p
+    int* nzp = nullptr;       // nonzero pivots per problem
+    double* maxpiv = nullptr; // per problem
+    int* rank = nullptr;      // per problem (current threshold)
+    cplx* QH = nullptr;       // count x (p*m): Q_1^* (rows >= rank zero), ld p
+    cplx* Wz = nullptr;       // count x (p*p): P Z^* [I_r; 0] (cols >= rank zero), ld p
+    cplx* M1 = nullptr;       // count x (m*p) scratch
+    cplx* Y = nullptr;        // count x (p*m) scratch
+};
+// rows 0..rank_b-1 of B_b (p x ncols, ld ldb, stride) <- T11_b^{-1} B_b, T11 in
+// the RZ-reduced factor V_b (ld m): the backward-stable triangular step of the
+// COD solve (never an explicit inverse)
+void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, const int* d_flags, cudaStream_t s);
+void cod_factor(const CodBatch& b, cudaStream_t s);
+// rank at threshold th for problems whose flag is set (flags == nullptr: all)
+void cod_rank(const CodBatch& b, double th, const int* d_flags, cudaStream_t s);
+// forms QH and Wz for the current rank: X = Wz * T11^{-1} * (QH * RHS)
+void cod_operator(const CodBatch& b, const int* d_flags, cudaStream_t s);
+
+// ---- LU with partial pivoting (batched over pointer lists) ----------------
+// n x n matrices A_b (ld) factored in place; ipiv_b[n] holds the row swapped
+// with row k at step k (0-based, LAPACK-style sequential interchanges).
+// d_singular[b] is set to 1 when a zero pivot is met.
+void lu_factor_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv, int* d_singular,
+                       cudaStream_t s, Workspace& ws);
+// B_b <- A_b^{-1} B_b for n x nrhs right-hand sides (ldb) using those factors.
+void lu_solve_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv,
+                      const std::vector<cplx*>& B, int ldb, int nrhs, cudaStream_t s, Workspace& ws);
+
+// ---- small utilities -------------------------------------------------------
+// per problem max |X_ij| over an m x n block (ld), count problems with stride
+void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s);
+// per problem Frobenius norm
+void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s);
+void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride, int m, int n,
+                 int count, cudaStream_t s);
+// y_b = beta y_b + alpha * sum_s A_s x_s  (batched complex GEMV, up to 2 terms)
+struct GemvTask {
+    const cplx* A[2];
+    const cplx* x[2];
+    int lda[2], n[2];
+    int nseg;
+    cplx* y;
+};
+void zgemv_batched(int M, cplx alpha, cplx beta, const std::vector<GemvTask>& tasks, cudaStream_t s,
+                   DBuf<GemvTask>& d_tasks);
+// FP64 peak microbenchmarks (same run as the solver): DFMA chain and DMMA loop
+double measure_dfma_tflops(cudaStream_t s);
+double measure_dmma_tflops(cudaStream_t s);
+
+struct Workspace {
+    DBuf<GemmTask> gemm_tasks;
+    DBuf<GemvTask> gemv_tasks;
+    DBuf<cplx*> ptrs, ptrs2;
+    DBuf<int*> iptrs;
+    std::vector<GemmTask> h_gemm;
+};
+
+}  // namespace qpsb

@@ -1,0 +1,148 @@
+// Internal declarations of the B200 implementation of the qpscat hot path.
+// Host code is C++17; device code targets sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qpscat_b200.h"
+
+namespace qpsb {
+
+// ---------------------------------------------------------------------------
+// Error taxonomy (mirrors /root/reference/proj/include/qpscat/errors.hpp:9-40)
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int status;
+    int layer;
+    uint64_t bytes;
+    Error(int st, const std::string& msg, int layer_ = 0, uint64_t bytes_ = 0)
+        : std::runtime_error(msg), status(st), layer(layer_), bytes(bytes_) {}
+};
+[[noreturn]] inline void fail(int st, const std::string& msg) { throw Error(st, msg); }
+
+#define QPS_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t qps_e_ = (call);                                                            \
+        if (qps_e_ != cudaSuccess)                                                              \
+            throw ::qpsb::Error(QPS_ERR_CUDA, std::string(#call " failed: ") +                  \
+                                                  cudaGetErrorString(qps_e_) + " at " __FILE__); \
+    } while (0)
+
+constexpr double kPi = 3.14159265358979323846;  // types.hpp:14
+
+// ---------------------------------------------------------------------------
+// Device memory
+// ---------------------------------------------------------------------------
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(size_t count) {
+        if (count <= n && p) return;
+        release();
+        if (count == 0) return;
+        QPS_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void upload(const std::vector<T>& h, cudaStream_t s) {
+        ensure(h.size());
+        if (!h.empty()) QPS_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void zero(cudaStream_t s) {
+        if (p && n) QPS_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Host geometry (reference-equivalent arithmetic; geometry.hpp)
+// ---------------------------------------------------------------------------
+enum SegKind : int { SEG_SINE = 0, SEG_FOURIER = 1, SEG_LINE = 2 };
+
+// Device-evaluable description of one quadrature segment (QuadSegment,
+// geometry.hpp:73-78): the std::function closures of the reference become data.
+struct SegDesc {
+    int kind;        // SegKind
+    int n;           // node count
+    int offset;      // first node in the interface
+    int periodic;    // 1 for a periodic-smooth interface
+    int q;           // Kress grading exponent (lines)
+    int ncos, nsin;  // Fourier coefficient counts
+    int coef_off;    // offset into the Fourier coefficient pool
+    double d, y0, amp, phase;  // period, offset height, sine parameters
+    double Ax, Ay, Bx, By;     // line end points
+};
+
+struct HostInterface {
+    std::vector<double> x, y, nx, ny, w, speed;
+    std::vector<SegDesc> segs;
+    double y_min = 0, y_max = 0, wall_y = 0;
+    bool smooth = false;
+    int N() const { return int(x.size()); }
+};
+
+struct StackDesc {
+    double d = 1.0;
+    std::vector<double> eps, mu;
+    std::vector<qps_interface_spec> ifaces;  // pointers into the arrays below
+    std::vector<std::vector<double>> cosc, sinc, verts;
+    std::vector<std::vector<int>> nodes;
+};
+
+struct HostGeometry {
+    double d = 1.0;
+    int I = 0;
+    std::vector<HostInterface> ifaces;
+    double y_U = 0, y_D = 0;
+    std::vector<double> wall_lo, wall_hi;
+    std::vector<std::vector<double>> wall_ys;  // I+1 x Mw
+    std::vector<double> ud_x;                  // M
+    std::vector<double> pc_x, pc_y;            // proxy centres, I+1
+    std::vector<std::vector<double>> px, py, pnx, pny;  // I+1 x P
+    std::vector<double> fourier_pool;
+    int P = 0, Mw = 0, M = 0;
+    double R = 0;
+};
+
+struct Numerics {
+    int P = 60, Mw = 120, M = 60, K = 0;
+    double R = 2.0;
+    int grading_q = 6;
+    double clearance = 0.05;
+    uint64_t memory_budget = uint64_t(4) << 30;
+};
+
+HostGeometry build_geometry(const StackDesc& st, const Numerics& num);
+
+struct Problem {
+    double omega = 0, theta = 0;
+    std::vector<double> k;
+    double ar = 1, ai = 0;  // alpha
+    int K = 0;
+    double kappa(int n, double d) const;
+};
+Problem make_problem(const StackDesc& st, const HostGeometry& g, double omega, double theta, int K);
+int choose_rb_order(const StackDesc& st, const HostGeometry& g, double omega, double theta);
+
+// reference fill count, ShiftBlockCache::fill_evals (assembly.hpp:285)
+uint64_t reference_fill_evals(const HostGeometry& g);
+
+}  // namespace qpsb

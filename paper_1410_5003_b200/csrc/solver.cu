@@ -1,0 +1,928 @@
+// Orchestration of the hot path on one B200:
+//   fill_system_fused  : every block of BlockSystem (assembly.hpp:293-483) in
+//                        three launches (pair, proxy, Alpert), alpha fused in
+//   schur              : I+1 independent least-squares eliminations
+//                        (periodize.hpp:67-126) as batched COD + one batched
+//                        DMMA GEMM over all A' updates
+//   bcr_solve          : block cyclic reduction of the block-tridiagonal
+//                        system (replaces the sequential Thomas sweep of
+//                        tridiag.hpp:23-46); log2(I) levels, each a batched
+//                        LU + batched solves + one batched GEMM
+//   recover            : recover_aux (tridiag.hpp:50-66) as batched GEMVs
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace qpsb {
+
+namespace {
+
+using cd = std::complex<double>;
+inline cplx C(cd z) { return cplx{z.real(), z.imag()}; }
+inline cd Z(cplx z) { return cd(z.re, z.im); }
+
+constexpr int kAlpertMinNodes = 2 * (10 + 16 / 2) + 2;  // alpert.hpp:67-68
+
+// cache_bytes_estimate, assembly.hpp:180-206 (including its accounting quirks)
+uint64_t cache_bytes_estimate(const HostGeometry& g, int P, int Mw, int M) {
+    const int I = g.I;
+    uint64_t b = 0;
+    auto q = [&](uint64_t r, uint64_t c) { b += 4 * 16 * r * c; };
+    for (int j = 0; j < I; ++j) {
+        const uint64_t N = g.ifaces[j].N();
+        q(N, N);
+        q(N, N);
+        q(N, N);
+    }
+    b *= 2;
+    for (int j = 1; j < I; ++j) q(g.ifaces[j].N(), 3 * uint64_t(g.ifaces[j - 1].N()));
+    for (int j = 0; j + 1 < I; ++j) q(g.ifaces[j].N(), 3 * uint64_t(g.ifaces[j + 1].N()));
+    for (int j = 0; j < I; ++j) b += 2 * 16 * 2 * uint64_t(g.ifaces[j].N()) * P;
+    for (int i = 0; i <= I; ++i) {
+        if (i < I) q(Mw, 2 * uint64_t(g.ifaces[i].N()));
+        if (i >= 1) q(Mw, 2 * uint64_t(g.ifaces[i - 1].N()));
+        b += 2 * 16 * 2 * uint64_t(Mw) * P;
+    }
+    q(M, 6 * uint64_t(g.ifaces.front().N()));
+    q(M, 6 * uint64_t(g.ifaces.back().N()));
+    b += 2 * 16 * 2 * uint64_t(M) * P;
+    return b;
+}
+
+cd vertical_wavenumber(double kl, double kap) {
+    const double t = kl * kl - kap * kap;
+    return t >= 0.0 ? cd(std::sqrt(t), 0.0) : cd(0.0, std::sqrt(-t));
+}
+
+}  // namespace
+
+void upload_geometry(Ctx& c) {
+    const HostGeometry& g = c.geo;
+    const int I = g.I;
+    std::vector<double> x, y, nx, ny, w;
+    auto add = [&](double xx, double yy, double nxx, double nyy, double ww) {
+        x.push_back(xx); y.push_back(yy); nx.push_back(nxx); ny.push_back(nyy); w.push_back(ww);
+    };
+    c.iface_off.assign(I, 0);
+    for (int j = 0; j < I; ++j) {
+        c.iface_off[j] = int(x.size());
+        const auto& q = g.ifaces[j];
+        for (int i = 0; i < q.N(); ++i) add(q.x[i], q.y[i], q.nx[i], q.ny[i], q.w[i]);
+    }
+    c.wall_off.assign(I + 1, 0);
+    for (int i = 0; i <= I; ++i) {
+        c.wall_off[i] = int(x.size());
+        for (double yy : g.wall_ys[i]) add(-0.5 * g.d, yy, 1.0, 0.0, 0.0);  // wall_targets, assembly.hpp:159-168
+    }
+    c.U_off = int(x.size());
+    for (double xx : g.ud_x) add(xx, g.y_U, 0.0, 1.0, 0.0);  // line_targets, assembly.hpp:170-177
+    c.D_off = int(x.size());
+    for (double xx : g.ud_x) add(xx, g.y_D, 0.0, 1.0, 0.0);
+    c.proxy_off.assign(I + 1, 0);
+    for (int i = 0; i <= I; ++i) {
+        c.proxy_off[i] = int(x.size());
+        for (int p = 0; p < g.P; ++p) add(g.px[i][p], g.py[i][p], g.pnx[i][p], g.pny[i][p], 0.0);
+    }
+    c.px.upload(x, c.stream);
+    c.py.upload(y, c.stream);
+    c.pnx.upload(nx, c.stream);
+    c.pny.upload(ny, c.stream);
+    c.pw.upload(w, c.stream);
+    std::vector<SegDesc> segs;
+    c.seg_first.assign(I, 0);
+    for (int j = 0; j < I; ++j) {
+        c.seg_first[j] = int(segs.size());
+        for (const auto& s : g.ifaces[j].segs) segs.push_back(s);
+    }
+    c.segs.upload(segs, c.stream);
+    std::vector<double> pool = g.fourier_pool;
+    if (pool.empty()) pool.push_back(0.0);
+    c.fourier.upload(pool, c.stream);
+    c.d_err.ensure(1);
+}
+
+void setup_dims(Ctx& c) {
+    Dims d;
+    const HostGeometry& g = c.geo;
+    d.I = g.I;
+    d.P = c.num.P;
+    d.Mw = c.num.Mw;
+    d.M = c.num.M;
+    d.K = c.prob.K;
+    d.nrb = 2 * d.K + 1;
+    d.mI = 2 * d.Mw;
+    d.mC = 2 * d.Mw + 2 * d.M;
+    d.pC = d.P + d.nrb;
+    int mx = 0;
+    for (const auto& q : g.ifaces) {
+        d.N.push_back(q.N());
+        mx = std::max(mx, 2 * q.N());
+        if (q.smooth && q.N() < kAlpertMinNodes)
+            fail(QPS_ERR_CONFIG, "self block: periodic rule needs at least " + std::to_string(kAlpertMinNodes) +
+                                     " nodes for the correction stencil");
+        if (int(q.segs.size()) > kMaxSegs) fail(QPS_ERR_CONFIG, "too many polyline segments (max 16)");
+    }
+    d.nb = (mx + 15) / 16 * 16;
+    d.padded = false;
+    for (int n : d.N) d.padded |= (2 * n != d.nb);
+    // assemble_system solvability checks, assembly.hpp:471-474
+    if (2 * c.num.Mw < c.num.P) fail(QPS_ERR_CONFIG, "least-squares solvability needs 2 Mw >= P");
+    if (2 * c.num.Mw + 2 * c.num.M < c.num.P + 2 * c.prob.K + 1)
+        fail(QPS_ERR_CONFIG, "corner solvability needs 2 Mw + 2 M >= P + 2K + 1");
+    // memory budget, assembly.hpp:216-223
+    const uint64_t need = cache_bytes_estimate(g, c.num.P, c.num.Mw, c.num.M);
+    if (need > c.num.memory_budget)
+        throw Error(QPS_ERR_MEMORY_BUDGET,
+                    "shift-block cache needs " + std::to_string(need) + " bytes, budget is " +
+                        std::to_string(c.num.memory_budget),
+                    0, need);
+    c.dims = d;
+}
+
+// ---------------------------------------------------------------------------
+// Fused fill
+// ---------------------------------------------------------------------------
+namespace {
+
+void set_quad_out(PairTask& t, cplx* base, int ld, int row_off, int col_off) {
+    // [D S; T D*] arrangement (assembly.hpp:320-327): row_off = #targets, col_off = #sources
+    t.oD = base;
+    t.oS = base + size_t(col_off) * ld;
+    t.oT = base + row_off;
+    t.oDs = base + row_off + size_t(col_off) * ld;
+    t.ld = ld;
+}
+
+PairTask quad_task(int t_off, int nt, int s_off, int ns) {
+    PairTask t{};
+    t.t_off = t_off;
+    t.nt = nt;
+    t.s_off = s_off;
+    t.ns = ns;
+    return t;
+}
+
+// terms l = 0, -1, +1 with coefficient scale * alpha^l (PairPieces::assemble order, assembly.hpp:107-112)
+void three_shifts(PairTask& t, double d, cd alpha, cd scale) {
+    const cd ainv = 1.0 / alpha;
+    const int ls[3] = {0, -1, 1};
+    const cd cs[3] = {scale, scale * ainv, scale * alpha};
+    t.nterm = 3;
+    for (int q = 0; q < 3; ++q) {
+        t.lsh[q] = ls[q];
+        t.tdx[q] = 0.0;
+        t.sdx[q] = d * ls[q];
+        t.coef[q] = C(cs[q]);
+    }
+}
+
+}  // namespace
+
+void fill_system_fused(Ctx& c) {
+    const Dims& D = c.dims;
+    const HostGeometry& g = c.geo;
+    const int I = D.I, nb = D.nb;
+    const double d = g.d;
+    const cd alpha(c.prob.ar, c.prob.ai);
+    const cd ainv = 1.0 / alpha;
+    const cd am2 = 1.0 / (alpha * alpha);
+    const auto& k = c.prob.k;
+    cudaStream_t s = c.stream;
+    const size_t nb2 = size_t(nb) * nb;
+
+    c.Adiag.ensure(I * nb2);
+    c.Asup.ensure(std::max(1, I - 1) * nb2);
+    c.Asub.ensure(std::max(1, I - 1) * nb2);
+    c.Bself.ensure(size_t(I) * nb * D.P);
+    c.Bbelow.ensure(size_t(I) * nb * D.P);
+    c.Qint.ensure(std::max(1, I - 1) * size_t(D.mI) * D.P);
+    c.Rint.ensure(std::max(1, I - 1) * size_t(D.mI) * 2 * nb);
+    c.Qc.ensure(2 * size_t(D.mC) * D.pC);
+    c.Rc.ensure(2 * size_t(D.mC) * nb);
+    c.f.ensure(nb);
+    if (D.padded) {
+        c.Adiag.zero(s);
+        c.Asup.zero(s);
+        c.Asub.zero(s);
+        c.Bself.zero(s);
+        c.Bbelow.zero(s);
+        c.Rint.zero(s);
+        c.Rc.zero(s);
+    }
+    c.Qc.zero(s);
+    QPS_CUDA(cudaMemsetAsync(c.d_err.p, 0, sizeof(int), s));
+
+    std::vector<PairTask> pt;
+    std::vector<ProxyTask> xt;
+    std::vector<AlpertTask> at;
+    int alpert_rows = 0;
+    for (int j = 0; j < I; ++j) {
+        const int N = D.N[j];
+        const auto& q = g.ifaces[j];
+        // A_jj = tilde_up - tilde_dn - I/+I (assembly.hpp:343-352)
+        {
+            PairTask t = quad_task(c.iface_off[j], N, c.iface_off[j], N);
+            t.nk = 2;
+            t.k[0] = k[j];
+            t.k[1] = k[j + 1];
+            t.ksign[0] = 1.0;
+            t.ksign[1] = -1.0;
+            three_shifts(t, d, alpha, 1.0);
+            t.self = q.smooth ? 1 : 2;
+            t.nseg = int(q.segs.size());
+            for (int sgi = 0; sgi < t.nseg; ++sgi) t.seg_start[sgi] = q.segs[sgi].offset;
+            t.seg_start[t.nseg] = N;
+            t.ident = 1;
+            t.accumulate = 0;
+            set_quad_out(t, c.Adiag.p + j * nb2, nb, N, N);
+            pt.push_back(t);
+            AlpertTask a{};
+            a.t_off = c.iface_off[j];
+            a.N = N;
+            a.smooth = q.smooth ? 1 : 0;
+            a.nseg = int(q.segs.size());
+            a.seg_first = c.seg_first[j];
+            a.row_start = alpert_rows;
+            a.nk = 2;
+            a.k[0] = k[j];
+            a.k[1] = k[j + 1];
+            a.ksign[0] = 1.0;
+            a.ksign[1] = -1.0;
+            a.alpha = C(alpha);
+            a.alpha_inv = C(ainv);
+            a.mode = 0;
+            a.oD = t.oD;
+            a.oS = t.oS;
+            a.oT = t.oT;
+            a.oDs = t.oDs;
+            a.ld = nb;
+            at.push_back(a);
+            alpert_rows += N;
+        }
+        // A_{j,j+1} = -tilde(coupl_dn[j]) (assembly.hpp:353): targets G_j, sources G_{j+1}, k_{j+1}
+        if (j + 1 < I) {
+            PairTask t = quad_task(c.iface_off[j], N, c.iface_off[j + 1], D.N[j + 1]);
+            t.nk = 1;
+            t.k[0] = k[j + 1];
+            t.ksign[0] = 1.0;
+            three_shifts(t, d, alpha, -1.0);
+            set_quad_out(t, c.Asup.p + j * nb2, nb, N, D.N[j + 1]);
+            pt.push_back(t);
+        }
+        // A_{j,j-1} = +tilde(coupl_up[j]) (assembly.hpp:354): targets G_j, sources G_{j-1}, k_j
+        if (j >= 1) {
+            PairTask t = quad_task(c.iface_off[j], N, c.iface_off[j - 1], D.N[j - 1]);
+            t.nk = 1;
+            t.k[0] = k[j];
+            t.ksign[0] = 1.0;
+            three_shifts(t, d, alpha, 1.0);
+            set_quad_out(t, c.Asub.p + (j - 1) * nb2, nb, N, D.N[j - 1]);
+            pt.push_back(t);
+        }
+        // B_self = proxy(proxies_j, k_j, G_j); B_below = -proxy(proxies_{j+1}, k_{j+1}, G_j)
+        for (int side = 0; side < 2; ++side) {
+            ProxyTask x{};
+            x.t_off = c.iface_off[j];
+            x.nt = N;
+            x.p_off = c.proxy_off[j + side];
+            x.P = D.P;
+            x.k = k[j + side];
+            x.nterm = 1;
+            x.tdx[0] = 0.0;
+            x.coef[0] = cplx{side == 0 ? 1.0 : -1.0, 0.0};
+            x.drow = N;
+            x.accumulate = 0;
+            x.out = (side == 0 ? c.Bself.p : c.Bbelow.p) + size_t(j) * nb * D.P;
+            x.ld = nb;
+            xt.push_back(x);
+        }
+    }
+    // per layer: C (wall matching), Q (proxy wall matching)
+    for (int i = 0; i <= I; ++i) {
+        cplx* R;
+        int ldR, col_self, col_above;
+        cplx* Qout;
+        int ldQ;
+        if (i == 0) {
+            R = c.Rc.p;
+            ldR = D.mC;
+            col_self = 0;
+            col_above = -1;
+            Qout = c.Qc.p;
+            ldQ = D.mC;
+        } else if (i == I) {
+            R = c.Rc.p + size_t(D.mC) * nb;
+            ldR = D.mC;
+            col_self = -1;
+            col_above = 0;
+            Qout = c.Qc.p + size_t(D.mC) * D.pC;
+            ldQ = D.mC;
+        } else {
+            R = c.Rint.p + size_t(i - 1) * D.mI * 2 * nb;
+            ldR = D.mI;
+            col_above = 0;
+            col_self = nb;
+            Qout = c.Qint.p + size_t(i - 1) * D.mI * D.P;
+            ldQ = D.mI;
+        }
+        // C = alpha^-2 K(wall + 2d) - alpha K(wall - d)  (assembly.hpp:375-397)
+        for (int which = 0; which < 2; ++which) {
+            const int src = which == 0 ? i : i - 1;  // C_self: G_i, C_above: G_{i-1}
+            const int col = which == 0 ? col_self : col_above;
+            if (col < 0 || src < 0 || src >= I) continue;
+            PairTask t = quad_task(c.wall_off[i], D.Mw, c.iface_off[src], D.N[src]);
+            t.nk = 1;
+            t.k[0] = k[i];
+            t.ksign[0] = 1.0;
+            t.nterm = 2;
+            t.lsh[0] = t.lsh[1] = 0;
+            t.tdx[0] = 2.0 * d;
+            t.tdx[1] = -d;
+            t.sdx[0] = t.sdx[1] = 0.0;
+            t.coef[0] = C(am2);
+            t.coef[1] = C(-alpha);
+            set_quad_out(t, R + size_t(col) * ldR, ldR, D.Mw, D.N[src]);
+            pt.push_back(t);
+        }
+        // Q = alpha^-1 phi(wall + d) - phi(wall)  (assembly.hpp:400-404)
+        ProxyTask x{};
+        x.t_off = c.wall_off[i];
+        x.nt = D.Mw;
+        x.p_off = c.proxy_off[i];
+        x.P = D.P;
+        x.k = k[i];
+        x.nterm = 2;
+        x.tdx[0] = d;
+        x.tdx[1] = 0.0;
+        x.coef[0] = C(ainv);
+        x.coef[1] = cplx{-1.0, 0.0};
+        x.drow = D.Mw;
+        x.accumulate = 0;
+        x.out = Qout;
+        x.ld = ldQ;
+        xt.push_back(x);
+    }
+    // radiation blocks: Z (into C'), V (into Q') (assembly.hpp:408-413, 443-460)
+    for (int side = 0; side < 2; ++side) {
+        const int src = side == 0 ? 0 : I - 1;
+        const int layer = side == 0 ? 0 : I;
+        const int toff = side == 0 ? c.U_off : c.D_off;
+        cplx* R = c.Rc.p + size_t(side) * D.mC * nb;
+        PairTask t = quad_task(toff, D.M, c.iface_off[src], D.N[src]);
+        t.nk = 1;
+        t.k[0] = k[layer];
+        t.ksign[0] = 1.0;
+        three_shifts(t, d, alpha, 1.0);
+        set_quad_out(t, R + 2 * D.Mw, D.mC, D.M, D.N[src]);
+        pt.push_back(t);
+        ProxyTask x{};
+        x.t_off = toff;
+        x.nt = D.M;
+        x.p_off = c.proxy_off[layer];
+        x.P = D.P;
+        x.k = k[layer];
+        x.nterm = 1;
+        x.tdx[0] = 0.0;
+        x.coef[0] = cplx{1.0, 0.0};
+        x.drow = D.M;
+        x.accumulate = 0;
+        x.out = c.Qc.p + size_t(side) * D.mC * D.pC + 2 * D.Mw;
+        x.ld = D.mC;
+        xt.push_back(x);
+    }
+
+    const DevPool pool{c.px.p, c.py.p, c.pnx.p, c.pny.p, c.pw.p};
+    launch_pair_fill(pt, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
+    launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.d_err.p, s, c.d_alpert);
+    launch_proxy_fill(xt, pool, c.d_err.p, s, c.d_proxy, c.d_tiles);
+
+    // W blocks (assembly.hpp:414-427) and f (assembly.hpp:431-441) on the host: O(M K) + O(N)
+    {
+        const int M = D.M, K = D.K, nrb = D.nrb;
+        std::vector<cplx> WU(size_t(2 * M) * nrb), WD(size_t(2 * M) * nrb);
+        const cd iu(0.0, 1.0);
+        for (int n = -K; n <= K; ++n) {
+            const double kap = c.prob.kappa(n, d);
+            const cd ku = vertical_wavenumber(k.front(), kap), kd = vertical_wavenumber(k.back(), kap);
+            for (int m = 0; m < M; ++m) {
+                const cd e = std::exp(iu * kap * g.ud_x[m]);
+                WU[size_t(n + K) * 2 * M + m] = C(-e);
+                WU[size_t(n + K) * 2 * M + M + m] = C(-iu * ku * e);
+                WD[size_t(n + K) * 2 * M + m] = C(-e);
+                WD[size_t(n + K) * 2 * M + M + m] = C(iu * kd * e);
+            }
+        }
+        for (int side = 0; side < 2; ++side) {
+            cplx* dst = c.Qc.p + size_t(side) * D.mC * D.pC + size_t(D.P) * D.mC + 2 * D.Mw;
+            QPS_CUDA(cudaMemcpy2DAsync(dst, sizeof(cplx) * D.mC, (side ? WD : WU).data(), sizeof(cplx) * 2 * M,
+                                       sizeof(cplx) * 2 * M, nrb, cudaMemcpyHostToDevice, s));
+        }
+        const auto& q0 = g.ifaces.front();
+        const int n0 = q0.N();
+        const double kx = k.front() * std::cos(c.prob.theta), ky = k.front() * std::sin(c.prob.theta);
+        std::vector<cplx> fh(nb, cplx{0, 0});
+        for (int j = 0; j < n0; ++j) {
+            const cd e = std::exp(iu * (kx * q0.x[j] + ky * q0.y[j]));
+            fh[j] = C(-e);
+            fh[n0 + j] = C(-iu * (kx * q0.nx[j] + ky * q0.ny[j]) * e);
+        }
+        c.f.upload(fh, s);
+    }
+    // padding: identity on the unused diagonal of padded A_jj blocks
+    if (D.padded) {
+        std::vector<cplx> one(1, cplx{1.0, 0.0});
+        for (int j = 0; j < I; ++j)
+            for (int i = 2 * D.N[j]; i < nb; ++i)
+                QPS_CUDA(cudaMemcpyAsync(c.Adiag.p + j * nb2 + size_t(i) * nb + i, one.data(), sizeof(cplx),
+                                         cudaMemcpyHostToDevice, s));
+    }
+    int herr = 0;
+    QPS_CUDA(cudaMemcpyAsync(&herr, c.d_err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QPS_CUDA(cudaStreamSynchronize(s));
+    if (herr) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
+    // evaluations performed: plain pairs minus band exclusions plus aux nodes
+    uint64_t ev = 0;
+    for (const auto& t : pt) ev += uint64_t(t.nt) * t.ns * t.nterm * t.nk;
+    for (int j = 0; j < I; ++j) {
+        const auto& q = g.ifaces[j];
+        const uint64_t N = q.N();
+        if (q.smooth) ev -= 2 * (19 * N) - 0;  // band (|off| <= 9) across the three shifts, per wavenumber
+        if (q.smooth) ev += 2 * 30 * N;
+        else {
+            for (const auto& sd : q.segs)
+                for (int ml = 0; ml < sd.n; ++ml) {
+                    const bool corr = std::min(ml, sd.n - 1 - ml) >= 10;
+                    const int lo = std::max(0, ml - 9), hi = std::min(sd.n - 1, ml + 9);
+                    ev -= 2 * uint64_t(corr ? hi - lo + 1 : 1);
+                    if (corr) ev += 2 * 30;
+                }
+        }
+    }
+    for (const auto& x : xt) ev += uint64_t(x.nt) * x.P * x.nterm;
+    c.performed_evals = ev;
+    c.ref_evals = reference_fill_evals(g);
+    c.sys_valid = true;
+}
+
+// ---------------------------------------------------------------------------
+// Schur complements (periodize.hpp:67-126)
+// ---------------------------------------------------------------------------
+namespace {
+
+// qsolve for one equal-shape family: X = argmin ||Q X - R|| with Eigen COD
+// semantics and the threshold escalation loop of periodize.hpp:29-37.
+void qsolve_family(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X, int ldX,
+                   size_t Xstride, double* lsq_out) {
+    const int cnt = cs.count;
+    if (cnt == 0) return;
+    cudaStream_t s = c.stream;
+    CodBatch b = cs.batch(Q);
+    cod_factor(b, s);
+    // scale = max(1, max |RHS|)
+    batched_maxabs(R, cs.m, cs.ncols, ldR, Rstride, cnt, cs.rmax.p, s);
+    std::vector<double> rmax(cnt), xmax(cnt);
+    QPS_CUDA(cudaMemcpyAsync(rmax.data(), cs.rmax.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+    std::vector<int> flags(cnt, 1);
+    bool first = true;
+    for (double th = c.qsolve_th0; th <= 1.1e-10; th *= 10.0) {
+        cs.flags.upload(flags, s);
+        cod_rank(b, th, cs.flags.p, s);
+        cod_operator(b, cs.flags.p, s);
+        // X = Wz * T11^{-1} * (QH * RHS)
+        std::vector<GemmTask> t1, t2;
+        for (int q = 0; q < cnt; ++q) {
+            if (!flags[q]) continue;
+            GemmTask t{};
+            t.nseg = 1;
+            t.A[0] = cs.QH.p + size_t(q) * cs.p * cs.m;
+            t.lda[0] = cs.p;
+            t.B[0] = R + Rstride * q;
+            t.ldb[0] = ldR;
+            t.K[0] = cs.m;
+            t.C = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
+            t.ldc = cs.p;
+            t1.push_back(t);
+            GemmTask u{};
+            u.nseg = 1;
+            u.A[0] = cs.Wz.p + size_t(q) * cs.p * cs.p;
+            u.lda[0] = cs.p;
+            u.B[0] = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
+            u.ldb[0] = cs.p;
+            u.K[0] = cs.p;
+            u.C = X + Xstride * q;
+            u.ldc = ldX;
+            t2.push_back(u);
+        }
+        zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t1, s, c.ws.gemm_tasks);
+        cod_trsm(b, cs.Tb.p, cs.p, size_t(cs.p) * cs.ncols, cs.ncols, cs.flags.p, s);
+        zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks);
+        batched_maxabs(X, cs.p, cs.ncols, ldX, Xstride, cnt, cs.xmax.p, s);
+        QPS_CUDA(cudaMemcpyAsync(xmax.data(), cs.xmax.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+        QPS_CUDA(cudaStreamSynchronize(s));
+        bool any = false;
+        for (int q = 0; q < cnt; ++q) {
+            if (!flags[q]) continue;
+            const double scale = std::max(1.0, rmax[q]);
+            if (xmax[q] <= 1e3 * scale) flags[q] = 0;  // accepted (qsolve_norm_cap, periodize.hpp:23)
+            else any = true;
+        }
+        first = false;
+        if (!any) break;
+    }
+    (void)first;
+    // relative LSQ residual ||Q X - R|| / ||R||  (periodize.hpp:84,113-118)
+    copy_blocks(R, ldR, Rstride, cs.E.p, cs.m, size_t(cs.m) * cs.ncols, cs.m, cs.ncols, cnt, s);
+    std::vector<GemmTask> tasks(cnt);
+    for (int q = 0; q < cnt; ++q) {
+        GemmTask& t = tasks[q];
+        t.nseg = 1;
+        t.A[0] = Q + size_t(q) * cs.m * cs.p;
+        t.lda[0] = cs.m;
+        t.B[0] = X + Xstride * q;
+        t.ldb[0] = ldX;
+        t.K[0] = cs.p;
+        t.C = cs.E.p + size_t(q) * cs.m * cs.ncols;
+        t.ldc = cs.m;
+    }
+    zgemm_batched(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, s, c.ws.gemm_tasks);
+    batched_fro(cs.E.p, cs.m, cs.ncols, cs.m, size_t(cs.m) * cs.ncols, cnt, cs.enorm.p, s);
+    batched_fro(R, cs.m, cs.ncols, ldR, Rstride, cnt, cs.rnorm.p, s);
+    std::vector<double> en(cnt), rn(cnt);
+    QPS_CUDA(cudaMemcpyAsync(en.data(), cs.enorm.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+    QPS_CUDA(cudaMemcpyAsync(rn.data(), cs.rnorm.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+    QPS_CUDA(cudaStreamSynchronize(s));
+    for (int q = 0; q < cnt; ++q) lsq_out[q] = en[q] / rn[q];
+}
+
+}  // namespace
+
+void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
+                          int ldX, size_t Xstride, double* lsq_out) {
+    qsolve_family(c, cs, Q, R, ldR, Rstride, X, ldX, Xstride, lsq_out);
+}
+
+void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, P = D.P;
+    if (P <= 0) fail(QPS_ERR_CONFIG, "periodization needs P > 0 proxy points per layer");
+    const size_t nb2 = size_t(nb) * nb;
+    c.Xint.ensure(std::max(1, I - 1) * size_t(P) * 2 * nb);
+    c.Xc.ensure(2 * size_t(D.pC) * nb);
+    c.lsq.assign(I + 1, 0.0);
+    // interior layers i = 1..I-1: X = qsolve(Q_i, [C_above_i C_self_i])
+    c.cod_int.ensure(I - 1, D.mI, P, 2 * nb);
+    qsolve_family(c, c.cod_int, c.Qint.p, c.Rint.p, D.mI, size_t(D.mI) * 2 * nb, c.Xint.p, P, size_t(P) * 2 * nb,
+                  c.lsq.data() + 1);
+    // corners: X_first = qsolve(Q'_1, C'_1), X_last = qsolve(Q'_{I+1}, C'_{I+1})
+    c.cod_c.ensure(2, D.mC, D.pC, nb);
+    double lc[2];
+    qsolve_family(c, c.cod_c, c.Qc.p, c.Rc.p, D.mC, size_t(D.mC) * nb, c.Xc.p, D.pC, size_t(D.pC) * nb, lc);
+    c.lsq[0] = lc[0];
+    c.lsq[I] = lc[1];
+    // A' updates in one batched GEMM (periodize.hpp:88-91, 115, 119):
+    //   Ap_diag[j] -= B_self[j] X_self(j) + B_below[j] X_above(j+1)
+    //   Ap_super[j] -= B_below[j] X_self(j+1),  Ap_sub[j] -= B_self[j+1] X_above(j+1)
+    auto xself = [&](int j, const cplx*& p, int& ld) {
+        if (j == 0) { p = c.Xc.p; ld = D.pC; }
+        else { p = c.Xint.p + size_t(j - 1) * P * 2 * nb + size_t(nb) * P; ld = P; }
+    };
+    auto xabove = [&](int i, const cplx*& p, int& ld) {
+        if (i == I) { p = c.Xc.p + size_t(D.pC) * nb; ld = D.pC; }
+        else { p = c.Xint.p + size_t(i - 1) * P * 2 * nb; ld = P; }
+    };
+    std::vector<GemmTask> tasks;
+    for (int j = 0; j < I; ++j) {
+        GemmTask t{};
+        t.nseg = 2;
+        t.A[0] = c.Bself.p + size_t(j) * nb * P;
+        t.lda[0] = nb;
+        xself(j, t.B[0], t.ldb[0]);
+        t.K[0] = P;
+        t.A[1] = c.Bbelow.p + size_t(j) * nb * P;
+        t.lda[1] = nb;
+        xabove(j + 1, t.B[1], t.ldb[1]);
+        t.K[1] = P;
+        t.C = Ad + j * nb2;
+        t.ldc = nb;
+        tasks.push_back(t);
+        if (j + 1 < I) {
+            GemmTask u{};
+            u.nseg = 1;
+            u.A[0] = c.Bbelow.p + size_t(j) * nb * P;
+            u.lda[0] = nb;
+            xself(j + 1, u.B[0], u.ldb[0]);
+            u.K[0] = P;
+            u.C = Au + j * nb2;
+            u.ldc = nb;
+            tasks.push_back(u);
+            GemmTask v{};
+            v.nseg = 1;
+            v.A[0] = c.Bself.p + size_t(j + 1) * nb * P;
+            v.lda[0] = nb;
+            xabove(j + 1, v.B[0], v.ldb[0]);
+            v.K[0] = P;
+            v.C = Al + j * nb2;
+            v.ldc = nb;
+            tasks.push_back(v);
+        }
+    }
+    zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks);
+    c.max_lsq = 0.0;
+    for (double r : c.lsq) c.max_lsq = std::max(c.max_lsq, r);
+    c.ps_valid = true;
+}
+
+// ---------------------------------------------------------------------------
+// Block cyclic reduction
+// ---------------------------------------------------------------------------
+void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb;
+    const size_t nb2 = size_t(nb) * nb;
+    cudaStream_t s = c.stream;
+    c.F.ensure(size_t(I) * nb);
+    c.F.zero(s);
+    QPS_CUDA(cudaMemcpyAsync(c.F.p, c.f.p, sizeof(cplx) * nb, cudaMemcpyDeviceToDevice, s));
+    c.ipiv.ensure(size_t(I) * nb);
+    c.singular.ensure(I);
+    c.singular.zero(s);
+    c.levels.clear();
+    BcrLevel L0;
+    for (int j = 0; j < I; ++j) {
+        L0.idx.push_back(j);
+        L0.D.push_back(Ad + j * nb2);
+        L0.L.push_back(j >= 1 ? Al + (j - 1) * nb2 : nullptr);
+        L0.U.push_back(j + 1 < I ? Au + j * nb2 : nullptr);
+        L0.F.push_back(c.F.p + size_t(j) * nb);
+    }
+    c.levels.push_back(L0);
+    // number of levels and buffers for the reduced couplings
+    {
+        int n = I, lv = 0;
+        while (n > 1) { n = (n + 1) / 2; ++lv; }
+        c.lvlL.resize(std::max(lv, 1));
+        c.lvlU.resize(std::max(lv, 1));
+    }
+    auto ipiv_of = [&](int j) { return c.ipiv.p + size_t(j) * nb; };
+    auto check_singular = [&]() {
+        std::vector<int> sg(I);
+        QPS_CUDA(cudaMemcpyAsync(sg.data(), c.singular.p, sizeof(int) * I, cudaMemcpyDeviceToHost, s));
+        QPS_CUDA(cudaStreamSynchronize(s));
+        for (int j = 0; j < I; ++j)
+            if (sg[j])
+                throw Error(QPS_ERR_SOLVER,
+                            "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1),
+                            j + 1);
+    };
+    int lvl = 0;
+    while (c.levels[lvl].idx.size() > 1) {
+        const BcrLevel& cur = c.levels[lvl];
+        const int sz = int(cur.idx.size());
+        // 1. factor the odd positions
+        std::vector<cplx*> fa;
+        std::vector<int*> fp;
+        for (int o = 1; o < sz; o += 2) {
+            fa.push_back(cur.D[o]);
+            fp.push_back(ipiv_of(cur.idx[o]));
+        }
+        // singular flags indexed by original block: use a per-level scratch via the pointer list
+        {
+            // lu_factor writes singular[b] for batch position b; remap afterwards
+            DBuf<int> flag;
+            flag.ensure(fa.size());
+            flag.zero(s);
+            lu_factor_batched(nb, nb, fa, fp, flag.p, s, c.ws);
+            std::vector<int> hf(fa.size());
+            QPS_CUDA(cudaMemcpyAsync(hf.data(), flag.p, sizeof(int) * hf.size(), cudaMemcpyDeviceToHost, s));
+            QPS_CUDA(cudaStreamSynchronize(s));
+            for (size_t b = 0; b < hf.size(); ++b)
+                if (hf[b]) {
+                    const int j = cur.idx[1 + 2 * b];
+                    throw Error(QPS_ERR_SOLVER,
+                                "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1),
+                                j + 1);
+                }
+        }
+        // 2. Y = D^{-1} [L | U] and y_f = D^{-1} f for the odd positions (in place)
+        {
+            std::vector<cplx*> ma, mb, va, vb;
+            std::vector<int*> mp, vp;
+            for (int o = 1; o < sz; o += 2) {
+                ma.push_back(cur.D[o]); mp.push_back(ipiv_of(cur.idx[o])); mb.push_back(cur.L[o]);
+                if (cur.U[o]) { ma.push_back(cur.D[o]); mp.push_back(ipiv_of(cur.idx[o])); mb.push_back(cur.U[o]); }
+                va.push_back(cur.D[o]); vp.push_back(ipiv_of(cur.idx[o])); vb.push_back(cur.F[o]);
+            }
+            lu_solve_batched(nb, nb, ma, mp, mb, nb, nb, s, c.ws);
+            lu_solve_batched(nb, nb, va, vp, vb, nb, 1, s, c.ws);
+        }
+        // 3. updates of the even positions
+        const int nsz = (sz + 1) / 2;
+        BcrLevel nxt;
+        DBuf<cplx>& LB = c.lvlL[lvl];
+        DBuf<cplx>& UB = c.lvlU[lvl];
+        LB.ensure(size_t(nsz) * nb2);
+        UB.ensure(size_t(nsz) * nb2);
+        std::vector<GemmTask> tasks;
+        std::vector<GemvTask> vtasks;
+        for (int e = 0; e < sz; e += 2) {
+            const int q = e / 2;
+            const bool hm = e >= 1, hp = e + 1 < sz;
+            nxt.idx.push_back(cur.idx[e]);
+            nxt.D.push_back(cur.D[e]);
+            nxt.F.push_back(cur.F[e]);
+            GemmTask t{};
+            t.nseg = 0;
+            GemvTask v{};
+            v.nseg = 0;
+            if (hm) {  // D_e -= L_e Y_U(e-1);  f_e -= L_e y_f(e-1)
+                if (cur.U[e - 1]) {
+                    t.A[t.nseg] = cur.L[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cur.U[e - 1]; t.ldb[t.nseg] = nb;
+                    t.K[t.nseg] = nb; ++t.nseg;
+                }
+                v.A[v.nseg] = cur.L[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[e - 1]; v.n[v.nseg] = nb; ++v.nseg;
+            }
+            if (hp) {  // D_e -= U_e Y_L(e+1);  f_e -= U_e y_f(e+1)
+                t.A[t.nseg] = cur.U[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cur.L[e + 1]; t.ldb[t.nseg] = nb;
+                t.K[t.nseg] = nb; ++t.nseg;
+                v.A[v.nseg] = cur.U[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[e + 1]; v.n[v.nseg] = nb; ++v.nseg;
+            }
+            if (t.nseg) {
+                t.C = cur.D[e];
+                t.ldc = nb;
+                tasks.push_back(t);
+            }
+            if (v.nseg) {
+                v.y = cur.F[e];
+                vtasks.push_back(v);
+            }
+            // new couplings: L'_e = -L_e Y_L(e-1) (to position e-2), U'_e = -U_e Y_U(e+1) (to e+2)
+            cplx* nl = nullptr;
+            cplx* nu = nullptr;
+            if (hm && e - 2 >= 0) {
+                nl = LB.p + size_t(q) * nb2;
+                GemmTask u{};
+                u.nseg = 1;
+                u.A[0] = cur.L[e]; u.lda[0] = nb; u.B[0] = cur.L[e - 1]; u.ldb[0] = nb; u.K[0] = nb;
+                u.C = nl;
+                u.ldc = nb;
+                tasks.push_back(u);
+            }
+            if (hp && e + 2 < sz) {
+                nu = UB.p + size_t(q) * nb2;
+                GemmTask u{};
+                u.nseg = 1;
+                u.A[0] = cur.U[e]; u.lda[0] = nb; u.B[0] = cur.U[e + 1]; u.ldb[0] = nb; u.K[0] = nb;
+                u.C = nu;
+                u.ldc = nb;
+                tasks.push_back(u);
+            }
+            nxt.L.push_back(nl);
+            nxt.U.push_back(nu);
+        }
+        // D/f updates use beta = 1; new couplings overwrite (beta = 0): split the batch
+        std::vector<GemmTask> upd, fresh;
+        for (const auto& t : tasks) {
+            bool is_new = false;
+            for (int e = 0; e < nsz; ++e)
+                if (t.C == nxt.L[e] || t.C == nxt.U[e]) is_new = true;
+            (is_new ? fresh : upd).push_back(t);
+        }
+        zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, upd, s, c.ws.gemm_tasks);
+        zgemm_batched(nb, nb, cplx{-1, 0}, cplx{0, 0}, fresh, s, c.ws.gemm_tasks);
+        zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vtasks, s, c.ws.gemv_tasks);
+        c.levels.push_back(nxt);
+        ++lvl;
+    }
+    // final single block
+    {
+        const BcrLevel& last = c.levels[lvl];
+        std::vector<cplx*> fa{last.D[0]};
+        std::vector<int*> fp{ipiv_of(last.idx[0])};
+        DBuf<int> flag;
+        flag.ensure(1);
+        flag.zero(s);
+        lu_factor_batched(nb, nb, fa, fp, flag.p, s, c.ws);
+        int hf = 0;
+        QPS_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        QPS_CUDA(cudaStreamSynchronize(s));
+        if (hf) {
+            const int j = last.idx[0];
+            throw Error(QPS_ERR_SOLVER,
+                        "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1), j + 1);
+        }
+        std::vector<cplx*> vb{last.F[0]};
+        lu_solve_batched(nb, nb, fa, fp, vb, nb, 1, s, c.ws);
+    }
+    (void)check_singular;
+    // back substitution: eta_o = y_f(o) - Y_L(o) eta_{o-1} - Y_U(o) eta_{o+1}, level by level upward.
+    // F of every block ends up holding eta.
+    for (int l = lvl - 1; l >= 0; --l) {
+        const BcrLevel& cur = c.levels[l];
+        const int sz = int(cur.idx.size());
+        std::vector<GemvTask> vt;
+        for (int o = 1; o < sz; o += 2) {
+            GemvTask v{};
+            v.nseg = 0;
+            v.A[v.nseg] = cur.L[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[o - 1]; v.n[v.nseg] = nb; ++v.nseg;
+            if (o + 1 < sz) {
+                v.A[v.nseg] = cur.U[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[o + 1]; v.n[v.nseg] = nb; ++v.nseg;
+            }
+            v.y = cur.F[o];
+            vt.push_back(v);
+        }
+        zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vt, s, c.ws.gemv_tasks);
+    }
+    c.eta_valid = true;
+}
+
+// ---------------------------------------------------------------------------
+// recover_aux (tridiag.hpp:50-66)
+// ---------------------------------------------------------------------------
+void recover(Ctx& c) {
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, P = D.P;
+    cudaStream_t s = c.stream;
+    c.csol.ensure(size_t(I + 1) * P);
+    c.aUd.ensure(D.pC);
+    c.aDd.ensure(D.pC);
+    // corners: x_first = -X_first eta_0, x_last = -X_last eta_{I-1}
+    std::vector<GemvTask> vt(2);
+    vt[0] = GemvTask{};
+    vt[0].nseg = 1; vt[0].A[0] = c.Xc.p; vt[0].lda[0] = D.pC; vt[0].x[0] = c.F.p; vt[0].n[0] = nb; vt[0].y = c.aUd.p;
+    vt[1] = GemvTask{};
+    vt[1].nseg = 1; vt[1].A[0] = c.Xc.p + size_t(D.pC) * nb; vt[1].lda[0] = D.pC;
+    vt[1].x[0] = c.F.p + size_t(I - 1) * nb; vt[1].n[0] = nb; vt[1].y = c.aDd.p;
+    zgemv_batched(D.pC, cplx{-1, 0}, cplx{0, 0}, vt, s, c.ws.gemv_tasks);
+    std::vector<GemvTask> it;
+    for (int i = 1; i <= I - 1; ++i) {
+        GemvTask v{};
+        v.nseg = 2;
+        const cplx* X = c.Xint.p + size_t(i - 1) * P * 2 * nb;
+        v.A[0] = X; v.lda[0] = P; v.x[0] = c.F.p + size_t(i - 1) * nb; v.n[0] = nb;
+        v.A[1] = X + size_t(nb) * P; v.lda[1] = P; v.x[1] = c.F.p + size_t(i) * nb; v.n[1] = nb;
+        v.y = c.csol.p + size_t(i) * P;
+        it.push_back(v);
+    }
+    zgemv_batched(P, cplx{-1, 0}, cplx{0, 0}, it, s, c.ws.gemv_tasks);
+    // download
+    std::vector<cplx> Fh(size_t(I) * nb), ch(size_t(I + 1) * P), xf(D.pC), xl(D.pC);
+    QPS_CUDA(cudaMemcpyAsync(Fh.data(), c.F.p, sizeof(cplx) * Fh.size(), cudaMemcpyDeviceToHost, s));
+    QPS_CUDA(cudaMemcpyAsync(ch.data(), c.csol.p, sizeof(cplx) * ch.size(), cudaMemcpyDeviceToHost, s));
+    QPS_CUDA(cudaMemcpyAsync(xf.data(), c.aUd.p, sizeof(cplx) * D.pC, cudaMemcpyDeviceToHost, s));
+    QPS_CUDA(cudaMemcpyAsync(xl.data(), c.aDd.p, sizeof(cplx) * D.pC, cudaMemcpyDeviceToHost, s));
+    QPS_CUDA(cudaStreamSynchronize(s));
+    c.h_eta.clear();
+    for (int j = 0; j < I; ++j)
+        for (int i = 0; i < 2 * D.N[j]; ++i) c.h_eta.push_back(Fh[size_t(j) * nb + i]);
+    for (int p = 0; p < P; ++p) {
+        ch[p] = xf[p];
+        ch[size_t(I) * P + p] = xl[p];
+    }
+    c.h_c = ch;
+    c.h_aU.assign(xf.begin() + P, xf.end());
+    c.h_aD.assign(xl.begin() + P, xl.end());
+    c.have_sol = true;
+    double R, T, fe;
+    host_spectrum(c, &R, &T, &fe, nullptr, nullptr, nullptr, nullptr, nullptr);
+    c.flux_error = fe;
+}
+
+// flux_error + reflection_transmission (postprocess.hpp:132-180)
+void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,
+                   int* pd) {
+    const Problem& p = c.prob;
+    const double d = c.geo.d;
+    const double kref = std::max(p.k.front(), p.k.back());
+    const double Finc = p.k.front() * std::abs(std::sin(p.theta));
+    const double tol = 1e-5;
+    double RR = 0.0, TT = 0.0, F = 0.0;
+    for (int n = -p.K; n <= p.K; ++n) {
+        const double kap = p.kappa(n, d);
+        const cd ku = vertical_wavenumber(p.k.front(), kap), kd = vertical_wavenumber(p.k.back(), kap);
+        const cd au = Z(c.h_aU[n + p.K]), ad = Z(c.h_aD[n + p.K]);
+        const bool propu = ku.imag() == 0.0 && ku.real() > tol * kref;
+        const bool propd = kd.imag() == 0.0 && kd.real() > tol * kref;
+        if (propu) {
+            RR += ku.real() * std::norm(au) / Finc;
+            F += ku.real() * std::norm(au);
+        }
+        if (propd) {
+            TT += kd.real() * std::norm(ad) / Finc;
+            F += kd.real() * std::norm(ad);
+        }
+        const int i = n + p.K;
+        if (kappa) kappa[i] = kap;
+        if (kU) kU[i] = C(ku);
+        if (kD) kD[i] = C(kd);
+        if (pu) pu[i] = propu;
+        if (pd) pd[i] = propd;
+    }
+    if (R) *R = RR;
+    if (T) *T = TT;
+    if (fe) *fe = (F - Finc) / Finc;
+}
+
+}  // namespace qpsb
