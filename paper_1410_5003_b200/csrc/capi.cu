@@ -21,7 +21,7 @@ int guarded(qps_ctx* h, F&& f) {
     c.err_layer = 0;
     c.err_bytes = 0;
     try {
-        QPS_CUDA(cudaSetDevice(c.device));
+        if (!c.host_only) QPS_CUDA(cudaSetDevice(c.device));
         f(c);
         return QPS_OK;
     } catch (const Error& e) {
@@ -39,9 +39,13 @@ void need(bool ok, const char* what) {
     if (!ok) fail(QPS_ERR_USAGE, std::string("qpscat_b200: ") + what);
 }
 
-void prepare(Ctx& c) {
+void need_device(const Ctx& c) {
+    if (c.host_only) fail(QPS_ERR_CUDA, "qpscat_b200: host-only context (device -1) cannot run device work");
+}
+
+void prepare(Ctx& c, bool check_solvable = true) {
     need(c.have_prob, "make_problem first");
-    setup_dims(c);
+    setup_dims(c, check_solvable);
 }
 
 void get_block(const Ctx& c, const cplx* base, int ld, int rows, int cols, qps_cplx* out, int* r, int* cc) {
@@ -96,6 +100,12 @@ int qps_abi_version(void) { return QPS_ABI_VERSION; }
 const char* qps_backend_name(void) { return "b200-cuda"; }
 
 qps_ctx* qps_create(int device) {
+    if (device == -1) {  // host-only context for CPU-side logic (tests, planning)
+        auto* h = new qps_ctx();
+        h->c.host_only = true;
+        h->c.device = -1;
+        return h;
+    }
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || device < 0 || device >= n) return nullptr;
     auto* h = new qps_ctx();
@@ -115,6 +125,10 @@ qps_ctx* qps_create(int device) {
 
 void qps_destroy(qps_ctx* h) {
     if (!h) return;
+    if (h->c.host_only) {
+        delete h;
+        return;
+    }
     cudaSetDevice(h->c.device);
     cudaStreamSynchronize(h->c.stream);
     if (h->c.ev0) cudaEventDestroy(h->c.ev0);
@@ -166,7 +180,7 @@ int qps_build_geometry(qps_ctx* h, double d, int n_layers, const double* eps, co
         c.stack = std::move(st);
         c.num = nm;
         c.geo = build_geometry(c.stack, c.num);
-        upload_geometry(c);
+        if (!c.host_only) upload_geometry(c);
         c.have_geom = true;
     });
 }
@@ -215,7 +229,7 @@ int qps_interface_nodes(const qps_ctx* h, int j, double* nodes, double* normals,
 
 int qps_precompute_shift_blocks(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
-        prepare(c);
+        prepare(c, false);
         c.ref_evals = reference_fill_evals(c.geo);
         c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
     });
@@ -223,6 +237,7 @@ int qps_precompute_shift_blocks(qps_ctx* h) {
 
 int qps_assemble_system(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         prepare(c);
         run_fill(c);
         c.ps_separate = true;
@@ -231,6 +246,7 @@ int qps_assemble_system(qps_ctx* h) {
 
 int qps_schur_complement(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         need(c.sys_valid, "assemble_system first");
         Timer t(c, &c.times.schur_ms);
         const Dims& D = c.dims;
@@ -252,6 +268,7 @@ int qps_schur_complement(qps_ctx* h) {
 
 int qps_block_lu_solve(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         need(c.ps_valid, "schur_complement first");
         Timer t(c, &c.times.solve_ms);
         if (c.ps_separate) bcr_solve(c, c.Apdiag.p, c.Apsup.p, c.Apsub.p);
@@ -262,6 +279,7 @@ int qps_block_lu_solve(qps_ctx* h) {
 
 int qps_recover_aux(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         need(c.eta_valid, "block_lu_solve first");
         Timer t(c, &c.times.recover_ms);
         recover(c);
@@ -270,7 +288,8 @@ int qps_recover_aux(qps_ctx* h) {
 
 int qps_solve(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
-        prepare(c);
+        prepare(c);  // input validation first (same errors with or without a device)
+        need_device(c);
         c.ps_separate = false;
         run_fill(c);
         c.times.assemble_ms = 0.0;
@@ -316,6 +335,7 @@ int qps_reflection_transmission(const qps_ctx* h, double* R, double* T, double* 
 int qps_sweep(qps_ctx* h, int n, const double* theta, int K, int mode, double* R, double* T, double* fe,
               qps_cplx* aU, qps_cplx* aD, int* status) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         need(c.have_prob, "make_problem first (sets omega)");
         need(K > 0, "sweep needs a fixed K > 0");
         (void)mode;
@@ -352,6 +372,7 @@ int qps_sweep(qps_ctx* h, int n, const double* theta, int K, int mode, double* R
 
 int qps_download_block(const qps_ctx* hh, int kind, int i, qps_cplx* out, int* rows, int* cols) {
     return guarded(const_cast<qps_ctx*>(hh), [&](Ctx& c) {
+        need_device(c);
         const Dims& D = c.dims;
         const int I = D.I, nb = D.nb, P = D.P;
         const size_t nb2 = size_t(nb) * nb;
@@ -442,6 +463,7 @@ int qps_get_phase_times(const qps_ctx* h, qps_phase_times* t) {
 
 int qps_hankel01(qps_ctx* h, int n, const double* x, qps_cplx* h0, qps_cplx* h1) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         for (int i = 0; i < n; ++i)
             if (!(x[i] > 0.0) || !std::isfinite(x[i]))
                 fail(QPS_ERR_DOMAIN, "hankel01: argument must be finite and > 0");
@@ -461,6 +483,7 @@ int qps_hankel01(qps_ctx* h, int n, const double* x, qps_cplx* h0, qps_cplx* h1)
 
 int qps_qsolve(qps_ctx* h, int m, int p, int n, const qps_cplx* Q, const qps_cplx* R, qps_cplx* X, int* rank) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         need(m >= p, "qsolve: Q must have at least as many rows as columns");
         need(m > 0 && p > 0 && n > 0, "qsolve: empty operand");
         DBuf<cplx> dQ, dR, dX;
@@ -481,6 +504,7 @@ int qps_qsolve(qps_ctx* h, int m, int p, int n, const qps_cplx* Q, const qps_cpl
 
 int qps_debug_zgemm(qps_ctx* h, int M, int N, int K, const qps_cplx* A, const qps_cplx* B, qps_cplx* Cm) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         DBuf<cplx> dA, dB, dC;
         dA.ensure(size_t(M) * K);
         dB.ensure(size_t(K) * N);
@@ -501,6 +525,7 @@ int qps_debug_zgemm(qps_ctx* h, int M, int N, int K, const qps_cplx* A, const qp
 // "FP64 peak measured by a microbenchmark in the same run")
 int qps_measure_fp64_peaks(qps_ctx* h, double* dfma_tflops, double* dmma_tflops) {
     return guarded(h, [&](Ctx& c) {
+        need_device(c);
         if (dfma_tflops) *dfma_tflops = measure_dfma_tflops(c.stream);
         if (dmma_tflops) *dmma_tflops = measure_dmma_tflops(c.stream);
     });

@@ -49,6 +49,7 @@ struct BcrLevel {
 
 struct Ctx {
     int device = 0;
+    bool host_only = false;  // device == -1: geometry/problem logic only, every device call fails
     cudaStream_t stream = nullptr;
 
     StackDesc stack;
@@ -110,7 +111,7 @@ struct Ctx {
 
 // geometry / problem
 void upload_geometry(Ctx& c);
-void setup_dims(Ctx& c);
+void setup_dims(Ctx& c, bool check_solvable = true);
 // one-shot fused single-angle fill of the assembled system (alpha recombination fused)
 void fill_system_fused(Ctx& c);
 // Schur complements in place on (A_diag, A_super, A_sub) or on the A' copies

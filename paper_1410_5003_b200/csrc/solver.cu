@@ -104,7 +104,7 @@ void upload_geometry(Ctx& c) {
     c.d_err.ensure(1);
 }
 
-void setup_dims(Ctx& c) {
+void setup_dims(Ctx& c, bool check_solvable) {
     Dims d;
     const HostGeometry& g = c.geo;
     d.I = g.I;
@@ -128,9 +128,9 @@ void setup_dims(Ctx& c) {
     d.nb = (mx + 15) / 16 * 16;
     d.padded = false;
     for (int n : d.N) d.padded |= (2 * n != d.nb);
-    // assemble_system solvability checks, assembly.hpp:471-474
-    if (2 * c.num.Mw < c.num.P) fail(QPS_ERR_CONFIG, "least-squares solvability needs 2 Mw >= P");
-    if (2 * c.num.Mw + 2 * c.num.M < c.num.P + 2 * c.prob.K + 1)
+    // assemble_system solvability checks, assembly.hpp:471-474 (raised at assembly time)
+    if (check_solvable && 2 * c.num.Mw < c.num.P) fail(QPS_ERR_CONFIG, "least-squares solvability needs 2 Mw >= P");
+    if (check_solvable && 2 * c.num.Mw + 2 * c.num.M < c.num.P + 2 * c.prob.K + 1)
         fail(QPS_ERR_CONFIG, "corner solvability needs 2 Mw + 2 M >= P + 2K + 1");
     // memory budget, assembly.hpp:216-223
     const uint64_t need = cache_bytes_estimate(g, c.num.P, c.num.Mw, c.num.M);
