@@ -139,6 +139,12 @@ int qps_schur_complement(qps_ctx* ctx);
  * reduction; SolverError names the original 1-based layer of a singular
  * diagonal factor) */
 int qps_block_lu_solve(qps_ctx* ctx);
+/* block_lu_solve(ps) on a caller-built PeriodizedSystem (tridiag.hpp:23-46, as
+ * the reference's own tests build one, proj/tests/test_tridiag.cpp:27-44):
+ * I diagonal blocks n x n (Ad, I*n*n), I-1 super/sub blocks (Au, Al), RHS f
+ * for block 0 (n); eta receives I*n.  SolverError names a singular layer. */
+int qps_block_lu_solve_blocks(qps_ctx* ctx, int I, int n, const qps_cplx* Ad, const qps_cplx* Au,
+                              const qps_cplx* Al, const qps_cplx* f, qps_cplx* eta);
 /* recover_aux(ps, eta, sol), tridiag.hpp:50-66 */
 int qps_recover_aux(qps_ctx* ctx);
 

@@ -255,6 +255,32 @@ int qps_block_lu_solve(qps_ctx* c) {
     });
 }
 
+int qps_block_lu_solve_blocks(qps_ctx* c, int I, int n, const qps_cplx* Ad, const qps_cplx* Au, const qps_cplx* Al,
+                              const qps_cplx* f, qps_cplx* eta) {
+    return guarded(c, [&] {
+        PeriodizedSystem ps;
+        ps.I = I;
+        ps.P = 0;
+        ps.K = 0;
+        ps.N.assign(I, n / 2);
+        const size_t nn = size_t(n) * n;
+        auto mat = [&](const qps_cplx* p) {
+            Mat m(n, n);
+            std::memcpy(m.data(), p, sizeof(cd) * nn);
+            return m;
+        };
+        for (int j = 0; j < I; ++j) ps.Ap_diag.push_back(mat(Ad + j * nn));
+        for (int j = 0; j + 1 < I; ++j) {
+            ps.Ap_super.push_back(mat(Au + j * nn));
+            ps.Ap_sub.push_back(mat(Al + j * nn));
+        }
+        ps.f.resize(n);
+        std::memcpy(ps.f.data(), f, sizeof(cd) * n);
+        const auto e = block_lu_solve(ps);
+        for (int j = 0; j < I; ++j) std::memcpy(eta + size_t(j) * n, e[j].data(), sizeof(cd) * n);
+    });
+}
+
 int qps_recover_aux(qps_ctx* c) {
     return guarded(c, [&] {
         need(c->ps.has_value() && !c->eta.empty(), "block_lu_solve first");

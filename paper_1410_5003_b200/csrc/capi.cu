@@ -277,6 +277,38 @@ int qps_block_lu_solve(qps_ctx* h) {
     });
 }
 
+int qps_block_lu_solve_blocks(qps_ctx* h, int I, int n, const qps_cplx* Ad, const qps_cplx* Au, const qps_cplx* Al,
+                              const qps_cplx* f, qps_cplx* eta) {
+    return guarded(h, [&](Ctx& c) {
+        need(I >= 1 && n >= 1, "block_lu_solve_blocks: empty system");
+        need_device(c);
+        const size_t nn = size_t(n) * n;
+        Dims D;
+        D.I = I;
+        D.nb = n;
+        D.N.assign(I, n / 2);
+        c.dims = D;
+        DBuf<cplx> dA, dU, dL;
+        dA.ensure(I * nn);
+        dU.ensure(std::max(1, I - 1) * nn);
+        dL.ensure(std::max(1, I - 1) * nn);
+        c.f.ensure(n);
+        QPS_CUDA(cudaMemcpyAsync(dA.p, Ad, sizeof(cplx) * I * nn, cudaMemcpyHostToDevice, c.stream));
+        if (I > 1) {
+            QPS_CUDA(cudaMemcpyAsync(dU.p, Au, sizeof(cplx) * (I - 1) * nn, cudaMemcpyHostToDevice, c.stream));
+            QPS_CUDA(cudaMemcpyAsync(dL.p, Al, sizeof(cplx) * (I - 1) * nn, cudaMemcpyHostToDevice, c.stream));
+        }
+        QPS_CUDA(cudaMemcpyAsync(c.f.p, f, sizeof(cplx) * n, cudaMemcpyHostToDevice, c.stream));
+        {
+            Timer t(c, &c.times.solve_ms);
+            bcr_solve(c, dA.p, dU.p, dL.p);
+        }
+        QPS_CUDA(cudaMemcpyAsync(eta, c.F.p, sizeof(cplx) * I * size_t(n), cudaMemcpyDeviceToHost, c.stream));
+        QPS_CUDA(cudaStreamSynchronize(c.stream));
+        c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
+    });
+}
+
 int qps_recover_aux(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
         need_device(c);

@@ -219,15 +219,20 @@ __global__ void __launch_bounds__(kThreads) proxy_fill_kernel(const ProxyTask* _
 }
 
 // ---- segment parametrisations evaluated on the device (geometry.hpp) ----
+// Kress grading evaluated without FMA contraction so the auxiliary nodes
+// round exactly like the host's (geometry.hpp:37-65): near a corner v(s) is a
+// difference of O(1) terms and contraction changes its last bits.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double kv(double s, int q) {
     const double pi = 3.14159265358979323846;
     const double u = (pi - s) / pi;
-    return (1.0 / q - 0.5) * u * u * u + (s - pi) / (pi * q) + 0.5;
+    return add(add(mul(mul(mul(add(1.0 / q, -0.5), u), u), u), (s - pi) / (pi * q)), 0.5);
 }
 __device__ __forceinline__ double kvp(double s, int q) {
     const double pi = 3.14159265358979323846;
     const double u = (pi - s) / pi;
-    return -3.0 * (1.0 / q - 0.5) * u * u / pi + 1.0 / (pi * q);
+    return add(mul(mul(mul(-3.0, add(1.0 / q, -0.5)), u), u) / pi, 1.0 / (pi * q));
 }
 
 __device__ void seg_eval(const SegDesc& sd, const double* fourier, double s, double& zx, double& zy, double& tx,
@@ -237,16 +242,16 @@ __device__ void seg_eval(const SegDesc& sd, const double* fourier, double s, dou
         const int q = sd.q;
         const double v1 = kv(s, q), v2 = kv(2.0 * pi - s, q);
         const double vq = pow(v1, double(q)), vr = pow(v2, double(q));
-        const double wv = 2.0 * pi * vq / (vq + vr);
-        const double d1 = q * pow(v1, double(q - 1)) * kvp(s, q);
-        const double d2 = -q * pow(v2, double(q - 1)) * kvp(2.0 * pi - s, q);
-        const double den = vq + vr;
-        const double wp = 2.0 * pi * (d1 * den - vq * (d1 + d2)) / (den * den);
+        const double wv = mul(2.0 * pi, vq) / add(vq, vr);
+        const double d1 = mul(mul(double(q), pow(v1, double(q - 1))), kvp(s, q));
+        const double d2 = mul(mul(double(-q), pow(v2, double(q - 1))), kvp(2.0 * pi - s, q));
+        const double den = add(vq, vr);
+        const double wp = mul(2.0 * pi, add(mul(d1, den), -mul(vq, add(d1, d2)))) / mul(den, den);
         const double f = wv / (2.0 * pi);
-        zx = sd.Ax + (sd.Bx - sd.Ax) * f;
-        zy = sd.Ay + (sd.By - sd.Ay) * f;
-        tx = (sd.Bx - sd.Ax) / (2.0 * pi) * wp;
-        ty = (sd.By - sd.Ay) / (2.0 * pi) * wp;
+        zx = add(sd.Ax, mul(sd.Bx - sd.Ax, f));
+        zy = add(sd.Ay, mul(sd.By - sd.Ay, f));
+        tx = mul((sd.Bx - sd.Ax) / (2.0 * pi), wp);
+        ty = mul((sd.By - sd.Ay) / (2.0 * pi), wp);
         return;
     }
     const double d = sd.d;

