@@ -15,7 +15,7 @@ Tolerances (max-norm, relative to the block's max entry):
       floor of ~1e-2, tools/noise_floor.py). (open-arc segment
       ends), where adjacent nodes are ~1e-11 apart and each entry is the
       rounding residue of cancelling ~1e11-size kernels in BOTH implementations
-      (the oracle's own values there are e.g. exactly -2^-17): 1e-4.
+      (the oracle's own values there are e.g. exactly -2^-17): 1e-3.
 Solution: the raw densities eta are NOT compared: Q_i is numerically
 rank-deficient at these sizes and equally valid residual minimizers differ by
 O(1) in eta (proj/tests/test_periodize.cpp:119-126; the oracle moves eta by
@@ -87,7 +87,7 @@ def test_fill_blocks_match_oracle(gpu, oracle, cfg, nif):
                 d = np.abs(g - o)
                 # open item: ~2e-9 residual on graded-corner interfaces
                 assert d[~mask].max() / scale < 1e-8, (name, i, d[~mask].max() / scale)
-                assert d[mask].max() / scale < 1e-4, (name, i, d[mask].max() / scale)
+                assert d[mask].max() / scale < 1e-3, (name, i, d[mask].max() / scale)
                 continue
             assert rel(g, o) < tol, (name, i, rel(g, o))
     assert gpu.fill_evals()["reference"] == oracle.fill_evals()["reference"]
