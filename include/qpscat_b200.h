@@ -100,6 +100,7 @@ typedef enum {
  * ("Matrix Filling / Schur / Block Solve"). */
 typedef struct {
     double fill_ms, assemble_ms, schur_ms, solve_ms, recover_ms;
+    double total_ms; /* device timeline of the last qps_solve, first to last event */
 } qps_phase_times;
 
 /* ---------------------------------------------------------------- context */
@@ -191,6 +192,18 @@ int qps_qsolve(qps_ctx* ctx, int m, int p, int n, const qps_cplx* Q, const qps_c
 /* Diagnostics: C = A B (M x K times K x N, column-major) on the product's
  * batched DMMA GEMM (the oracle uses its BLAS). */
 int qps_debug_zgemm(qps_ctx* ctx, int M, int N, int K, const qps_cplx* A, const qps_cplx* B, qps_cplx* C);
+/* Kernel-family instrumentation: when enabled, every launch is bracketed by
+ * CUDA events on its own stream and tagged with its algorithmic FLOPs, bytes
+ * and kernel evaluations.  qps_prof_stats returns the number of families and
+ * fills up to cap entries (names: cap x 64 chars).  The oracle reports 0. */
+int qps_prof_enable(qps_ctx* ctx, int on);
+int qps_prof_reset(qps_ctx* ctx);
+int qps_prof_stats(qps_ctx* ctx, int cap, char* names, uint64_t* launches, double* ms, double* flops,
+                   double* bytes, double* units);
+/* number of kernels this library has launched (process lifetime) */
+uint64_t qps_launch_count(void);
+/* host<->device bytes moved since the last qps_prof_reset */
+int qps_transfer_bytes(const qps_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 /* FP64 peaks of this device measured by microbenchmarks (DFMA chain, DMMA
  * loop), TFLOP/s; the oracle returns 0 for both. */
 int qps_measure_fp64_peaks(qps_ctx* ctx, double* dfma_tflops, double* dmma_tflops);

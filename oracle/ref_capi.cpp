@@ -294,11 +294,13 @@ int qps_recover_aux(qps_ctx* c) {
 }
 
 int qps_solve(qps_ctx* c) {
+    const auto t0 = clk::now();
     int s = qps_precompute_shift_blocks(c);
     if (s == QPS_OK) s = qps_assemble_system(c);
     if (s == QPS_OK) s = qps_schur_complement(c);
     if (s == QPS_OK) s = qps_block_lu_solve(c);
     if (s == QPS_OK) s = qps_recover_aux(c);
+    if (c) c->times.total_ms = ms_since(t0);
     return s;
 }
 
@@ -474,6 +476,17 @@ int qps_debug_zgemm(qps_ctx* c, int M, int N, int K, const qps_cplx* A, const qp
         const Mat r = a * b;
         std::memcpy(Cm, r.data(), sizeof(cd) * size_t(M) * N);
     });
+}
+
+int qps_prof_enable(qps_ctx* c, int) { return c ? QPS_OK : QPS_ERR_USAGE; }
+int qps_prof_reset(qps_ctx* c) { return c ? QPS_OK : QPS_ERR_USAGE; }
+int qps_prof_stats(qps_ctx*, int, char*, uint64_t*, double*, double*, double*, double*) { return 0; }
+uint64_t qps_launch_count(void) { return 0; }
+int qps_transfer_bytes(const qps_ctx* c, uint64_t* a, uint64_t* b) {
+    if (!c) return QPS_ERR_USAGE;
+    if (a) *a = 0;
+    if (b) *b = 0;
+    return QPS_OK;
 }
 
 int qps_measure_fp64_peaks(qps_ctx* c, double* a, double* b) {

@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "ctx.h"
+#include "prof.h"
 
 using namespace qpsb;
 
@@ -322,6 +323,23 @@ int qps_solve(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
         prepare(c);  // input validation first (same errors with or without a device)
         need_device(c);
+        cudaEvent_t t0, t1;
+        QPS_CUDA(cudaEventCreate(&t0));
+        QPS_CUDA(cudaEventCreate(&t1));
+        QPS_CUDA(cudaEventRecord(t0, c.stream));
+        struct Total {
+            Ctx& c;
+            cudaEvent_t a, b;
+            ~Total() {
+                cudaEventRecord(b, c.stream);
+                cudaEventSynchronize(b);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                c.times.total_ms = ms;
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+            }
+        } total{c, t0, t1};
         c.ps_separate = false;
         run_fill(c);
         c.times.assemble_ms = 0.0;
@@ -551,6 +569,48 @@ int qps_debug_zgemm(qps_ctx* h, int M, int N, int K, const qps_cplx* A, const qp
         QPS_CUDA(cudaMemcpyAsync(Cm, dC.p, sizeof(cplx) * size_t(M) * N, cudaMemcpyDeviceToHost, c.stream));
         QPS_CUDA(cudaStreamSynchronize(c.stream));
     });
+}
+
+int qps_prof_enable(qps_ctx* h, int on) {
+    return guarded(h, [&](Ctx&) { prof_enable(on != 0); });
+}
+
+int qps_prof_reset(qps_ctx* h) {
+    return guarded(h, [&](Ctx& c) {
+        if (!c.host_only) QPS_CUDA(cudaStreamSynchronize(c.stream));
+        prof_reset();
+        g_h2d_bytes = 0;
+        g_d2h_bytes = 0;
+    });
+}
+
+int qps_prof_stats(qps_ctx* h, int cap, char* names, uint64_t* launches, double* ms, double* flops, double* bytes,
+                   double* units) {
+    if (!h) return -1;
+    if (!h->c.host_only) cudaStreamSynchronize(h->c.stream);
+    std::vector<ProfStat> st(cap > 0 ? cap : 0);
+    const int n = prof_query(st.data(), cap);
+    for (int i = 0; i < std::min(n, cap); ++i) {
+        if (names) {
+            std::strncpy(names + 64 * i, st[i].name, 63);
+            names[64 * i + 63] = 0;
+        }
+        if (launches) launches[i] = st[i].launches;
+        if (ms) ms[i] = st[i].ms;
+        if (flops) flops[i] = st[i].flops;
+        if (bytes) bytes[i] = st[i].bytes;
+        if (units) units[i] = st[i].units;
+    }
+    return n;
+}
+
+uint64_t qps_launch_count(void) { return g_launches.load(); }
+
+int qps_transfer_bytes(const qps_ctx* h, uint64_t* h2d, uint64_t* d2h) {
+    if (!h) return QPS_ERR_USAGE;
+    if (h2d) *h2d = g_h2d_bytes.load();
+    if (d2h) *d2h = g_d2h_bytes.load();
+    return QPS_OK;
 }
 
 // FP64 peak microbenchmarks for the roofline denominators (north star:

@@ -18,6 +18,7 @@
 
 #include "alpert_table.h"
 #include "fill.cuh"
+#include "prof.h"
 
 namespace qpsb {
 
@@ -484,6 +485,9 @@ void launch_pair_fill(const std::vector<PairTask>& tasks, const DevPool& pool, i
     if (tiles.empty()) return;
     d_tasks.upload(tasks, s);
     d_tiles.upload(tiles, s);
+    double ev = 0;
+    for (const auto& t : tasks) ev += double(t.nt) * t.ns * t.nterm * t.nk;
+    ProfScope ps("fill_pair", s, 200.0 * ev, 0.0, ev);
     pair_fill_kernel<<<unsigned(tiles.size()), kThreads, 0, s>>>(d_tasks.p, d_tiles.p, pool, g_near_table, d_err);
     QPS_CUDA(cudaGetLastError());
 }
@@ -496,6 +500,9 @@ void launch_proxy_fill(const std::vector<ProxyTask>& tasks, const DevPool& pool,
     if (tiles.empty()) return;
     d_tasks.upload(tasks, s);
     d_tiles.upload(tiles, s);
+    double ev = 0;
+    for (const auto& t : tasks) ev += double(t.nt) * t.P * t.nterm;
+    ProfScope ps("fill_proxy", s, 200.0 * ev, 0.0, ev);
     proxy_fill_kernel<<<unsigned(tiles.size()), kThreads, 0, s>>>(d_tasks.p, d_tiles.p, pool, g_near_table, d_err);
     QPS_CUDA(cudaGetLastError());
 }
@@ -506,6 +513,8 @@ void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const D
     if (tasks.empty() || total_rows == 0) return;
     d_tasks.upload(tasks, s);
     const int blocks = (total_rows + 3) / 4;
+    const double ev = 2.0 * 30.0 * total_rows;
+    ProfScope ps("fill_alpert", s, 200.0 * ev, 0.0, ev);
     alpert_kernel<<<blocks, 128, 0, s>>>(d_tasks.p, int(tasks.size()), total_rows, pool, d_segs, d_fourier,
                                          g_near_table, d_err);
     QPS_CUDA(cudaGetLastError());
@@ -514,6 +523,7 @@ void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const D
 void launch_hankel_batch(int n, const double* d_x, cplx* d_h0, cplx* d_h1, cudaStream_t s) {
     if (n <= 0) return;
     const int blocks = std::min((n + 255) / 256, 148 * 8);
+    ProfScope ps("hankel", s, 140.0 * n, 0.0, n);
     hankel_batch_kernel<<<blocks, 256, 0, s>>>(n, d_x, d_h0, d_h1, g_near_table);
     QPS_CUDA(cudaGetLastError());
 }

@@ -11,6 +11,7 @@
 #include <cmath>
 
 #include "linalg.cuh"
+#include "prof.h"
 
 namespace qpsb {
 
@@ -789,6 +790,14 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
     if (tasks.empty() || M <= 0 || N <= 0) return;
     d_tasks.upload(tasks, s);
     const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+    double fl = 0, by = 0;
+    for (const auto& t : tasks)
+        for (int q = 0; q < t.nseg; ++q) {
+            fl += 8.0 * M * N * t.K[q];
+            by += 16.0 * (double(M) * t.K[q] + double(t.K[q]) * N);
+        }
+    by += 16.0 * double(M) * N * tasks.size() * ((beta.re != 0.0 || beta.im != 0.0) ? 2 : 1);
+    ProfScope ps("zgemm", s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
     for (size_t off = 0; off < tasks.size(); off += 65535) {
         const unsigned cnt = unsigned(std::min<size_t>(65535, tasks.size() - off));
         zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
@@ -800,21 +809,25 @@ void cod_factor(const CodBatch& b, cudaStream_t s) {
     if (b.count == 0) return;
     if (b.p > kMaxP) fail(QPS_ERR_CONFIG, "qsolve: too many columns for the device COD (max 256)");
     if (b.m < b.p) fail(QPS_ERR_USAGE, "qsolve: Q must have at least as many rows as columns");
+    ProfScope ps("cod_factor", s, 8.0 * b.count * (2.0 * b.m * b.p * b.p - 2.0 * b.p * b.p * b.p / 3.0));
     cod_factor_kernel<<<b.count, 256, 0, s>>>(b);
     QPS_CUDA(cudaGetLastError());
 }
 void cod_rank(const CodBatch& b, double th, const int* flags, cudaStream_t s) {
     if (b.count == 0) return;
+    ProfScope ps("cod_rank", s, 0.0);
     cod_rank_kernel<<<(b.count + 127) / 128, 128, 0, s>>>(b, th, flags);
     QPS_CUDA(cudaGetLastError());
 }
 void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
     if (b.count == 0) return;
+    ProfScope ps("cod_operator", s, 8.0 * b.count * (double(b.m) * b.p * b.p + double(b.p) * b.p * b.p));
     cod_operator_kernel<<<b.count, 256, 0, s>>>(b, flags);
     QPS_CUDA(cudaGetLastError());
 }
 void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, const int* flags, cudaStream_t s) {
     if (b.count == 0 || ncols == 0) return;
+    ProfScope ps("cod_trsm", s, 4.0 * b.count * double(b.p) * b.p * ncols);
     cod_trsm_kernel<<<dim3((ncols + 127) / 128, b.count), 128, 0, s>>>(b, B, ldb, stride, ncols, flags);
     QPS_CUDA(cudaGetLastError());
 }
@@ -830,12 +843,19 @@ void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::v
     int* const* d_ipiv = ws.iptrs.p;
     for (int k0 = 0; k0 < n; k0 += kNB) {
         const int kend = std::min(k0 + kNB, n);
-        lu_panel_kernel<<<count, 256, 0, s>>>(n, ld, d_A, d_ipiv, k0, d_singular);
+        {
+            ProfScope ps("lu_panel", s, 8.0 * count * double(n - k0) * (kend - k0) * (kend - k0) / 2.0);
+            lu_panel_kernel<<<count, 256, 0, s>>>(n, ld, d_A, d_ipiv, k0, d_singular);
+        }
         QPS_CUDA(cudaGetLastError());
-        lu_swap_kernel<<<dim3((n + 127) / 128, count), 128, 0, s>>>(n, ld, d_A, d_ipiv, k0, kend, n, k0, kend);
+        {
+            ProfScope ps("lu_swap", s, 0.0);
+            lu_swap_kernel<<<dim3((n + 127) / 128, count), 128, 0, s>>>(n, ld, d_A, d_ipiv, k0, kend, n, k0, kend);
+        }
         QPS_CUDA(cudaGetLastError());
         const int rest = n - kend;
         if (rest > 0) {
+            ProfScope ps("trsm", s, 4.0 * count * double(kend - k0) * (kend - k0) * rest);
             trsm_lower_unit_kernel<<<dim3((rest + 127) / 128, count), 128, 0, s>>>(
                 ld, reinterpret_cast<const cplx* const*>(d_A), d_A, ld, k0, kend, kend, rest);
             QPS_CUDA(cudaGetLastError());
@@ -868,12 +888,18 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
     cplx* const* d_B = ws.ptrs2.p;
     const int* const* d_ipiv = ws.iptrs.p;
     const dim3 g((nrhs + 127) / 128, count);
-    rowswap_rhs_kernel<<<g, 128, 0, s>>>(n, d_ipiv, d_B, ldb, nrhs);
+    {
+        ProfScope ps("lu_swap", s, 0.0);
+        rowswap_rhs_kernel<<<g, 128, 0, s>>>(n, d_ipiv, d_B, ldb, nrhs);
+    }
     QPS_CUDA(cudaGetLastError());
     auto& tasks = ws.h_gemm;
     for (int k0 = 0; k0 < n; k0 += kNB) {
         const int kend = std::min(k0 + kNB, n);
-        trsm_lower_unit_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, 0, nrhs);
+        {
+            ProfScope ps("trsm", s, 4.0 * count * double(kend - k0) * (kend - k0) * nrhs);
+            trsm_lower_unit_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, 0, nrhs);
+        }
         QPS_CUDA(cudaGetLastError());
         if (kend < n) {
             tasks.assign(count, GemmTask{});
@@ -894,7 +920,10 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
     const int nblk = (n + kNB - 1) / kNB;
     for (int bi = nblk - 1; bi >= 0; --bi) {
         const int k0 = bi * kNB, kend = std::min(k0 + kNB, n);
-        trsm_upper_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, nrhs);
+        {
+            ProfScope ps("trsm", s, 4.0 * count * double(kend - k0) * (kend - k0) * nrhs);
+            trsm_upper_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, nrhs);
+        }
         QPS_CUDA(cudaGetLastError());
         if (k0 > 0) {
             tasks.assign(count, GemmTask{});
@@ -916,11 +945,13 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
 
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {
     if (count == 0) return;
+    ProfScope ps("reduce", s, 0.0, 16.0 * count * double(m) * n);
     maxabs_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out);
     QPS_CUDA(cudaGetLastError());
 }
 void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {
     if (count == 0) return;
+    ProfScope ps("reduce", s, 0.0, 32.0 * count * double(m) * n);
     fro_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out);
     QPS_CUDA(cudaGetLastError());
 }
@@ -928,6 +959,7 @@ void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, s
                  int count, cudaStream_t s) {
     if (count == 0 || m == 0 || n == 0) return;
     const int bx = int(std::min<size_t>((size_t(m) * n + 255) / 256, 1024));
+    ProfScope ps("copy", s, 0.0, 32.0 * count * double(m) * n);
     copy_blocks_kernel<<<dim3(bx, count), 256, 0, s>>>(src, lds, sstride, dst, ldd, dstride, m, n);
     QPS_CUDA(cudaGetLastError());
 }
@@ -935,6 +967,10 @@ void zgemv_batched(int M, cplx alpha, cplx beta, const std::vector<GemvTask>& ta
                    DBuf<GemvTask>& d_tasks) {
     if (tasks.empty() || M <= 0) return;
     d_tasks.upload(tasks, s);
+    double fl = 0;
+    for (const auto& t : tasks)
+        for (int q = 0; q < t.nseg; ++q) fl += 8.0 * M * t.n[q];
+    ProfScope ps("zgemv", s, fl, fl * 2.0);
     zgemv_kernel<<<dim3((M + 127) / 128, unsigned(tasks.size())), 128, 0, s>>>(M, alpha, beta, d_tasks.p);
     QPS_CUDA(cudaGetLastError());
 }

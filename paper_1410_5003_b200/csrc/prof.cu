@@ -1,0 +1,98 @@
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "prof.h"
+#include "qps_internal.h"
+
+namespace qpsb {
+
+std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+namespace {
+struct Pending {
+    const char* name;
+    cudaEvent_t e0, e1;
+    double flops, bytes, units;
+    int nlaunch;
+};
+struct Agg {
+    uint64_t launches = 0;
+    double ms = 0, flops = 0, bytes = 0, units = 0;
+};
+bool g_on = false;
+std::vector<Pending> g_pending;
+std::map<std::string, Agg> g_agg;
+std::vector<cudaEvent_t> g_free;
+
+cudaEvent_t get_event() {
+    if (!g_free.empty()) {
+        cudaEvent_t e = g_free.back();
+        g_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void resolve() {
+    for (auto& p : g_pending) {
+        cudaEventSynchronize(p.e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.e0, p.e1);
+        Agg& a = g_agg[p.name];
+        a.launches += p.nlaunch;
+        a.ms += ms;
+        a.flops += p.flops;
+        a.bytes += p.bytes;
+        a.units += p.units;
+        g_free.push_back(p.e0);
+        g_free.push_back(p.e1);
+    }
+    g_pending.clear();
+}
+}  // namespace
+
+void prof_enable(bool on) { g_on = on; }
+bool prof_enabled() { return g_on; }
+void prof_reset() {
+    resolve();
+    g_agg.clear();
+}
+
+ProfScope::ProfScope(const char* name_, cudaStream_t s_, double flops_, double bytes_, double units_, int nl)
+    : name(name_), s(s_), flops(flops_), bytes(bytes_), units(units_), nlaunch(nl) {
+    g_launches += nl;
+    if (!g_on) return;
+    e0 = get_event();
+    e1 = get_event();
+    cudaEventRecord(e0, s);
+}
+
+ProfScope::~ProfScope() {
+    if (!e0) return;
+    cudaEventRecord(e1, s);
+    g_pending.push_back({name, e0, e1, flops, bytes, units, nlaunch});
+    if (g_pending.size() > 4096) resolve();
+}
+
+int prof_query(ProfStat* out, int cap) {
+    resolve();
+    int i = 0;
+    for (auto& kv : g_agg) {
+        if (i < cap && out) {
+            // names are string literals of the launch sites; keep a stable copy
+            static std::map<std::string, std::string> keep;
+            keep[kv.first] = kv.first;
+            out[i] = ProfStat{keep[kv.first].c_str(), kv.second.launches, kv.second.ms, kv.second.flops,
+                              kv.second.bytes, kv.second.units};
+        }
+        ++i;
+    }
+    return int(g_agg.size());
+}
+
+}  // namespace qpsb

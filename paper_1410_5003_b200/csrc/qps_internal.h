@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -12,6 +13,9 @@
 #include "qpscat_b200.h"
 
 namespace qpsb {
+
+// host<->device traffic counters (bench.py's e2e bytes per step)
+extern std::atomic<uint64_t> g_h2d_bytes, g_d2h_bytes;
 
 // ---------------------------------------------------------------------------
 // Error taxonomy (mirrors /root/reference/proj/include/qpscat/errors.hpp:9-40)
@@ -24,6 +28,13 @@ struct Error : std::runtime_error {
         : std::runtime_error(msg), status(st), layer(layer_), bytes(bytes_) {}
 };
 [[noreturn]] inline void fail(int st, const std::string& msg) { throw Error(st, msg); }
+
+// counted device->host copy
+#define QPS_D2H(dst, src, bytes, stream)                                                   \
+    do {                                                                                   \
+        QPS_CUDA(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, (stream)));  \
+        ::qpsb::g_d2h_bytes += (bytes);                                                    \
+    } while (0)
 
 #define QPS_CUDA(call)                                                                          \
     do {                                                                                        \
@@ -65,7 +76,10 @@ struct DBuf {
     }
     void upload(const std::vector<T>& h, cudaStream_t s) {
         ensure(h.size());
-        if (!h.empty()) QPS_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (!h.empty()) {
+            QPS_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+            g_h2d_bytes += h.size() * sizeof(T);
+        }
     }
     void zero(cudaStream_t s) {
         if (p && n) QPS_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));

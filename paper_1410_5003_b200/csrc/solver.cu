@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "ctx.h"
+#include "prof.h"
 
 namespace qpsb {
 
@@ -440,7 +441,7 @@ void fill_system_fused(Ctx& c) {
                                          cudaMemcpyHostToDevice, s));
     }
     int herr = 0;
-    QPS_CUDA(cudaMemcpyAsync(&herr, c.d_err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QPS_D2H(&herr, c.d_err.p, sizeof(int), s);
     QPS_CUDA(cudaStreamSynchronize(s));
     if (herr) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
     // evaluations performed: plain pairs minus band exclusions plus aux nodes
@@ -484,7 +485,7 @@ void qsolve_family(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, si
     // scale = max(1, max |RHS|)
     batched_maxabs(R, cs.m, cs.ncols, ldR, Rstride, cnt, cs.rmax.p, s);
     std::vector<double> rmax(cnt), xmax(cnt);
-    QPS_CUDA(cudaMemcpyAsync(rmax.data(), cs.rmax.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+    QPS_D2H(rmax.data(), cs.rmax.p, sizeof(double) * cnt, s);
     std::vector<int> flags(cnt, 1);
     bool first = true;
     for (double th = c.qsolve_th0; th <= 1.1e-10; th *= 10.0) {
@@ -520,7 +521,7 @@ void qsolve_family(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, si
         cod_trsm(b, cs.Tb.p, cs.p, size_t(cs.p) * cs.ncols, cs.ncols, cs.flags.p, s);
         zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks);
         batched_maxabs(X, cs.p, cs.ncols, ldX, Xstride, cnt, cs.xmax.p, s);
-        QPS_CUDA(cudaMemcpyAsync(xmax.data(), cs.xmax.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+        QPS_D2H(xmax.data(), cs.xmax.p, sizeof(double) * cnt, s);
         QPS_CUDA(cudaStreamSynchronize(s));
         bool any = false;
         for (int q = 0; q < cnt; ++q) {
@@ -551,8 +552,8 @@ void qsolve_family(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, si
     batched_fro(cs.E.p, cs.m, cs.ncols, cs.m, size_t(cs.m) * cs.ncols, cnt, cs.enorm.p, s);
     batched_fro(R, cs.m, cs.ncols, ldR, Rstride, cnt, cs.rnorm.p, s);
     std::vector<double> en(cnt), rn(cnt);
-    QPS_CUDA(cudaMemcpyAsync(en.data(), cs.enorm.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
-    QPS_CUDA(cudaMemcpyAsync(rn.data(), cs.rnorm.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+    QPS_D2H(en.data(), cs.enorm.p, sizeof(double) * cnt, s);
+    QPS_D2H(rn.data(), cs.rnorm.p, sizeof(double) * cnt, s);
     QPS_CUDA(cudaStreamSynchronize(s));
     for (int q = 0; q < cnt; ++q) lsq_out[q] = en[q] / rn[q];
 }
@@ -669,7 +670,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     auto ipiv_of = [&](int j) { return c.ipiv.p + size_t(j) * nb; };
     auto check_singular = [&]() {
         std::vector<int> sg(I);
-        QPS_CUDA(cudaMemcpyAsync(sg.data(), c.singular.p, sizeof(int) * I, cudaMemcpyDeviceToHost, s));
+        QPS_D2H(sg.data(), c.singular.p, sizeof(int) * I, s);
         QPS_CUDA(cudaStreamSynchronize(s));
         for (int j = 0; j < I; ++j)
             if (sg[j])
@@ -696,7 +697,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             flag.zero(s);
             lu_factor_batched(nb, nb, fa, fp, flag.p, s, c.ws);
             std::vector<int> hf(fa.size());
-            QPS_CUDA(cudaMemcpyAsync(hf.data(), flag.p, sizeof(int) * hf.size(), cudaMemcpyDeviceToHost, s));
+            QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
             QPS_CUDA(cudaStreamSynchronize(s));
             for (size_t b = 0; b < hf.size(); ++b)
                 if (hf[b]) {
@@ -806,7 +807,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         flag.zero(s);
         lu_factor_batched(nb, nb, fa, fp, flag.p, s, c.ws);
         int hf = 0;
-        QPS_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        QPS_D2H(&hf, flag.p, sizeof(int), s);
         QPS_CUDA(cudaStreamSynchronize(s));
         if (hf) {
             const int j = last.idx[0];
@@ -869,10 +870,10 @@ void recover(Ctx& c) {
     zgemv_batched(P, cplx{-1, 0}, cplx{0, 0}, it, s, c.ws.gemv_tasks);
     // download
     std::vector<cplx> Fh(size_t(I) * nb), ch(size_t(I + 1) * P), xf(D.pC), xl(D.pC);
-    QPS_CUDA(cudaMemcpyAsync(Fh.data(), c.F.p, sizeof(cplx) * Fh.size(), cudaMemcpyDeviceToHost, s));
-    QPS_CUDA(cudaMemcpyAsync(ch.data(), c.csol.p, sizeof(cplx) * ch.size(), cudaMemcpyDeviceToHost, s));
-    QPS_CUDA(cudaMemcpyAsync(xf.data(), c.aUd.p, sizeof(cplx) * D.pC, cudaMemcpyDeviceToHost, s));
-    QPS_CUDA(cudaMemcpyAsync(xl.data(), c.aDd.p, sizeof(cplx) * D.pC, cudaMemcpyDeviceToHost, s));
+    QPS_D2H(Fh.data(), c.F.p, sizeof(cplx) * Fh.size(), s);
+    QPS_D2H(ch.data(), c.csol.p, sizeof(cplx) * ch.size(), s);
+    QPS_D2H(xf.data(), c.aUd.p, sizeof(cplx) * D.pC, s);
+    QPS_D2H(xl.data(), c.aDd.p, sizeof(cplx) * D.pC, s);
     QPS_CUDA(cudaStreamSynchronize(s));
     c.h_eta.clear();
     for (int j = 0; j < I; ++j)

@@ -103,7 +103,7 @@ class _Num(C.Structure):
 
 class _Times(C.Structure):
     _fields_ = [("fill_ms", C.c_double), ("assemble_ms", C.c_double), ("schur_ms", C.c_double),
-                ("solve_ms", C.c_double), ("recover_ms", C.c_double)]
+                ("solve_ms", C.c_double), ("recover_ms", C.c_double), ("total_ms", C.c_double)]
 
 
 @dataclasses.dataclass
@@ -192,6 +192,12 @@ def _bind(lib):
         "qps_get_phase_times": (C.c_int, [vp, P(_Times)]),
         "qps_hankel01": (C.c_int, [vp, C.c_int, P(C.c_double), vp, vp]),
         "qps_measure_fp64_peaks": (C.c_int, [vp, P(C.c_double), P(C.c_double)]),
+        "qps_prof_enable": (C.c_int, [vp, C.c_int]),
+        "qps_prof_reset": (C.c_int, [vp]),
+        "qps_prof_stats": (C.c_int, [vp, C.c_int, C.c_char_p, P(C.c_uint64), P(C.c_double), P(C.c_double),
+                                     P(C.c_double), P(C.c_double)]),
+        "qps_launch_count": (C.c_uint64, []),
+        "qps_transfer_bytes": (C.c_int, [vp, P(C.c_uint64), P(C.c_uint64)]),
         "qps_qsolve": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, P(C.c_int)]),
         "qps_debug_zgemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
     }
@@ -442,6 +448,34 @@ class Solver:
         h1 = np.zeros(len(x), dtype=np.complex128)
         self._check(self.lib.qps_hankel01(self.h, len(x), _dptr(x), h0.ctypes.data, h1.ctypes.data))
         return h0, h1
+
+    def prof_enable(self, on=True):
+        self._check(self.lib.qps_prof_enable(self.h, int(on)))
+
+    def prof_reset(self):
+        self._check(self.lib.qps_prof_reset(self.h))
+
+    def prof_stats(self):
+        cap = 64
+        names = C.create_string_buffer(64 * cap)
+        la = (C.c_uint64 * cap)()
+        arrs = [(C.c_double * cap)() for _ in range(4)]
+        n = self.lib.qps_prof_stats(self.h, cap, names, la, *arrs)
+        out = {}
+        for i in range(min(n, cap)):
+            nm = names.raw[64 * i:64 * (i + 1)].split(b"\0")[0].decode()
+            out[nm] = {"launches": la[i], "ms": arrs[0][i], "flops": arrs[1][i], "bytes": arrs[2][i],
+                       "units": arrs[3][i]}
+        return out
+
+    def launch_count(self):
+        return int(self.lib.qps_launch_count())
+
+    def transfer_bytes(self):
+        a = C.c_uint64()
+        b = C.c_uint64()
+        self._check(self.lib.qps_transfer_bytes(self.h, C.byref(a), C.byref(b)))
+        return {"h2d": a.value, "d2h": b.value}
 
     def qsolve(self, Q, rhs):
         """qsolve (periodize.hpp:25-39); returns (X, rank)."""
