@@ -83,7 +83,7 @@ struct Ctx {
     // ---- block cyclic reduction ----
     std::vector<BcrLevel> levels;
     std::vector<DBuf<cplx>> lvlL, lvlU;
-    DBuf<cplx> F, eta;
+    DBuf<cplx> F, eta, dinv;
     DBuf<int> ipiv, singular;
     DBuf<cplx*> dptrA, dptrB;
     DBuf<int*> dptrP;

@@ -555,7 +555,8 @@ __global__ void cod_trsm_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int
 // ---------------------------------------------------------------------------
 // LU (partial pivoting on the modulus, like Eigen's PartialPivLU)
 // ---------------------------------------------------------------------------
-constexpr int kNB = 32;
+constexpr int kNB = 32;  // LU panel width
+constexpr int kTB = 64;  // triangular-solve block (inverse diagonal tiles)
 
 __global__ void __launch_bounds__(256) lu_panel_kernel(int n, int ld, cplx* const* __restrict__ Ap,
                                                        int* const* __restrict__ Pp, int k0, int* singular) {
@@ -657,6 +658,66 @@ __global__ void trsm_upper_kernel(int ld, const cplx* const* __restrict__ Ap, cp
             s.im -= t.im;
         }
         x[i] = cdiv(s, A[size_t(i) * ld + i]);
+    }
+}
+
+// Inverse of the bs x bs diagonal blocks of a factored LU (unit-lower L and/or
+// upper U), one CTA per (block, matrix), one thread per column.  Output per
+// block: [L^{-1} | U^{-1}] as two bs x bs column-major tiles (ld bs).
+__global__ void tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap, cplx* const* __restrict__ Op, int bs,
+                               int k0_first, int mode) {
+    extern __shared__ cplx smem[];
+    cplx* T = smem;            // bs x bs block of the factor
+    cplx* X = smem + bs * bs;  // inverse being built
+    const cplx* A = Ap[blockIdx.y];
+    cplx* O = Op[blockIdx.y] + size_t(blockIdx.x) * 2 * bs * bs;
+    const int k0 = k0_first + blockIdx.x * bs;
+    const int sz = min(bs, n - k0);
+    for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) {
+        const int i = e % bs, j = e / bs;
+        T[e] = (i < sz && j < sz) ? A[size_t(k0 + j) * ld + k0 + i] : cplx{0, 0};
+    }
+    __syncthreads();
+    const int j = threadIdx.x;
+    if (mode & 1) {
+        if (j < bs)
+            for (int i = 0; i < bs; ++i) {
+                cplx v{0, 0};
+                if (i == j) v = cplx{1, 0};
+                else if (i > j && i < sz) {
+                    for (int l = j; l < i; ++l) {
+                        const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
+                        v.re -= t.re;
+                        v.im -= t.im;
+                    }
+                }
+                X[j * bs + i] = v;
+            }
+        __syncthreads();
+        for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) O[e] = X[e];
+        __syncthreads();
+    }
+    if (mode & 2) {
+        if (j < bs) {
+            for (int i = bs - 1; i >= 0; --i) {
+                cplx v{0, 0};
+                if (i < sz && j < sz && i <= j) {
+                    cplx s = (i == j) ? cplx{1, 0} : cplx{0, 0};
+                    for (int l = i + 1; l <= j; ++l) {
+                        const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
+                        s.re -= t.re;
+                        s.im -= t.im;
+                    }
+                    const cplx d = T[i * bs + i];
+                    v = (d.re == 0.0 && d.im == 0.0) ? cplx{0, 0} : cdiv(s, d);
+                } else if (i == j) {
+                    v = cplx{1, 0};
+                }
+                X[j * bs + i] = v;
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) O[bs * bs + e] = X[e];
     }
 }
 
@@ -833,34 +894,62 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
 }
 
 
-void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP, int* d_singular,
-                       cudaStream_t s, Workspace& ws) {
+size_t lu_dinv_elems(int n) { return size_t(2) * ((n + kTB - 1) / kTB) * kTB * kTB; }
+
+namespace {
+void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, int bs, int k0_first, int nblk,
+                    int mode, cudaStream_t s) {
+    const size_t sh = 2 * size_t(bs) * bs * sizeof(cplx);
+    static bool attr = false;
+    if (!attr) {
+        QPS_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(2 * kTB * kTB * sizeof(cplx))));
+        attr = true;
+    }
+    ProfScope ps("tri_inv", s, 8.0 / 3.0 * count * nblk * double(bs) * bs * bs * ((mode == 3) ? 2 : 1));
+    tri_inv_kernel<<<dim3(nblk, count), bs, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
+    QPS_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,
+                       const std::vector<cplx*>& hDinv, int* d_singular, cudaStream_t s, Workspace& ws) {
     const int count = int(hA.size());
     if (count == 0) return;
     ws.ptrs.upload(hA, s);
     ws.iptrs.upload(hP, s);
+    ws.ptrs2.upload(hDinv, s);
     cplx* const* d_A = ws.ptrs.p;
     int* const* d_ipiv = ws.iptrs.p;
+    cplx* const* d_D = ws.ptrs2.p;
+    auto& tasks = ws.h_gemm;
     for (int k0 = 0; k0 < n; k0 += kNB) {
         const int kend = std::min(k0 + kNB, n);
         {
             ProfScope ps("lu_panel", s, 8.0 * count * double(n - k0) * (kend - k0) * (kend - k0) / 2.0);
             lu_panel_kernel<<<count, 256, 0, s>>>(n, ld, d_A, d_ipiv, k0, d_singular);
         }
-        QPS_CUDA(cudaGetLastError());
         {
             ProfScope ps("lu_swap", s, 0.0);
             lu_swap_kernel<<<dim3((n + 127) / 128, count), 128, 0, s>>>(n, ld, d_A, d_ipiv, k0, kend, n, k0, kend);
         }
-        QPS_CUDA(cudaGetLastError());
         const int rest = n - kend;
         if (rest > 0) {
-            ProfScope ps("trsm", s, 4.0 * count * double(kend - k0) * (kend - k0) * rest);
-            trsm_lower_unit_kernel<<<dim3((rest + 127) / 128, count), 128, 0, s>>>(
-                ld, reinterpret_cast<const cplx* const*>(d_A), d_A, ld, k0, kend, kend, rest);
-            QPS_CUDA(cudaGetLastError());
-            auto& tasks = ws.h_gemm;
+            // U12 = L11^{-1} A12 via the explicit inverse of the unit-lower 32x32 L11 (scratch in Dinv)
+            launch_tri_inv(n, ld, d_A, d_D, count, kNB, k0, 1, 1, s);
             tasks.assign(count, GemmTask{});
+            for (int b = 0; b < count; ++b) {
+                GemmTask& t = tasks[b];
+                t.nseg = 1;
+                t.A[0] = hDinv[b];
+                t.lda[0] = kNB;
+                t.B[0] = hA[b] + size_t(kend) * ld + k0;
+                t.ldb[0] = ld;
+                t.K[0] = kend - k0;
+                t.C = hA[b] + size_t(kend) * ld + k0;  // in place: M <= 64 rows, one CTA per column tile
+                t.ldc = ld;
+            }
+            zgemm_batched(kend - k0, rest, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks);
             for (int b = 0; b < count; ++b) {
                 GemmTask& t = tasks[b];
                 t.nseg = 1;
@@ -875,32 +964,45 @@ void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::v
             zgemm_batched(rest, rest, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
         }
     }
+    // inverse 64x64 diagonal blocks of L and U for the GEMM-shaped solves
+    launch_tri_inv(n, ld, d_A, d_D, count, kTB, 0, (n + kTB - 1) / kTB, 3, s);
 }
 
 void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,
-                      const std::vector<cplx*>& hB, int ldb, int nrhs, cudaStream_t s, Workspace& ws) {
+                      const std::vector<cplx*>& hDinv, const std::vector<cplx*>& hB, int ldb, int nrhs,
+                      cudaStream_t s, Workspace& ws) {
     const int count = int(hA.size());
     if (count == 0 || nrhs == 0) return;
-    ws.ptrs.upload(hA, s);
     ws.ptrs2.upload(hB, s);
     ws.iptrs.upload(hP, s);
-    const cplx* const* d_A = ws.ptrs.p;
     cplx* const* d_B = ws.ptrs2.p;
     const int* const* d_ipiv = ws.iptrs.p;
-    const dim3 g((nrhs + 127) / 128, count);
     {
         ProfScope ps("lu_swap", s, 0.0);
-        rowswap_rhs_kernel<<<g, 128, 0, s>>>(n, d_ipiv, d_B, ldb, nrhs);
-    }
-    QPS_CUDA(cudaGetLastError());
-    auto& tasks = ws.h_gemm;
-    for (int k0 = 0; k0 < n; k0 += kNB) {
-        const int kend = std::min(k0 + kNB, n);
-        {
-            ProfScope ps("trsm", s, 4.0 * count * double(kend - k0) * (kend - k0) * nrhs);
-            trsm_lower_unit_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, 0, nrhs);
-        }
+        rowswap_rhs_kernel<<<dim3((nrhs + 127) / 128, count), 128, 0, s>>>(n, d_ipiv, d_B, ldb, nrhs);
         QPS_CUDA(cudaGetLastError());
+    }
+    auto& tasks = ws.h_gemm;
+    const int nblk = (n + kTB - 1) / kTB;
+    auto diag = [&](int bi, int which) {  // B_k <- inv(tile) B_k in place (rows <= 64)
+        const int k0 = bi * kTB, kend = std::min(k0 + kTB, n);
+        tasks.assign(count, GemmTask{});
+        for (int b = 0; b < count; ++b) {
+            GemmTask& t = tasks[b];
+            t.nseg = 1;
+            t.A[0] = hDinv[b] + size_t(bi) * 2 * kTB * kTB + (which ? size_t(kTB) * kTB : 0);
+            t.lda[0] = kTB;
+            t.B[0] = hB[b] + k0;
+            t.ldb[0] = ldb;
+            t.K[0] = kend - k0;
+            t.C = hB[b] + k0;
+            t.ldc = ldb;
+        }
+        zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks);
+    };
+    for (int bi = 0; bi < nblk; ++bi) {  // forward: unit-lower L
+        const int k0 = bi * kTB, kend = std::min(k0 + kTB, n);
+        diag(bi, 0);
         if (kend < n) {
             tasks.assign(count, GemmTask{});
             for (int b = 0; b < count; ++b) {
@@ -917,14 +1019,9 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
             zgemm_batched(n - kend, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
         }
     }
-    const int nblk = (n + kNB - 1) / kNB;
-    for (int bi = nblk - 1; bi >= 0; --bi) {
-        const int k0 = bi * kNB, kend = std::min(k0 + kNB, n);
-        {
-            ProfScope ps("trsm", s, 4.0 * count * double(kend - k0) * (kend - k0) * nrhs);
-            trsm_upper_kernel<<<g, 128, 0, s>>>(ld, d_A, d_B, ldb, k0, kend, nrhs);
-        }
-        QPS_CUDA(cudaGetLastError());
+    for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: upper U
+        const int k0 = bi * kTB, kend = std::min(k0 + kTB, n);
+        diag(bi, 1);
         if (k0 > 0) {
             tasks.assign(count, GemmTask{});
             for (int b = 0; b < count; ++b) {

@@ -58,12 +58,16 @@ void cod_operator(const CodBatch& b, const int* d_flags, cudaStream_t s);
 // ---- LU with partial pivoting (batched over pointer lists) ----------------
 // n x n matrices A_b (ld) factored in place; ipiv_b[n] holds the row swapped
 // with row k at step k (0-based, LAPACK-style sequential interchanges).
-// d_singular[b] is set to 1 when a zero pivot is met.
-void lu_factor_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv, int* d_singular,
-                       cudaStream_t s, Workspace& ws);
+// d_singular[b] is set to 1 when a zero pivot is met.  Dinv_b (lu_dinv_elems(n)
+// entries) receives the inverses of the 64x64 diagonal tiles of L and U so the
+// triangular solves run as DMMA GEMMs.
+size_t lu_dinv_elems(int n);
+void lu_factor_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv,
+                       const std::vector<cplx*>& Dinv, int* d_singular, cudaStream_t s, Workspace& ws);
 // B_b <- A_b^{-1} B_b for n x nrhs right-hand sides (ldb) using those factors.
 void lu_solve_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv,
-                      const std::vector<cplx*>& B, int ldb, int nrhs, cudaStream_t s, Workspace& ws);
+                      const std::vector<cplx*>& Dinv, const std::vector<cplx*>& B, int ldb, int nrhs,
+                      cudaStream_t s, Workspace& ws);
 
 // ---- small utilities -------------------------------------------------------
 // per problem max |X_ij| over an m x n block (ld), count problems with stride

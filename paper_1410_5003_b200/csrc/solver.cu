@@ -648,6 +648,8 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     c.F.zero(s);
     QPS_CUDA(cudaMemcpyAsync(c.F.p, c.f.p, sizeof(cplx) * nb, cudaMemcpyDeviceToDevice, s));
     c.ipiv.ensure(size_t(I) * nb);
+    const size_t dsz = lu_dinv_elems(nb);
+    c.dinv.ensure(size_t(I) * dsz);
     c.singular.ensure(I);
     c.singular.zero(s);
     c.levels.clear();
@@ -668,6 +670,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         c.lvlU.resize(std::max(lv, 1));
     }
     auto ipiv_of = [&](int j) { return c.ipiv.p + size_t(j) * nb; };
+    auto dinv_of = [&](int j) { return c.dinv.p + size_t(j) * dsz; };
     auto check_singular = [&]() {
         std::vector<int> sg(I);
         QPS_D2H(sg.data(), c.singular.p, sizeof(int) * I, s);
@@ -683,11 +686,12 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         const BcrLevel& cur = c.levels[lvl];
         const int sz = int(cur.idx.size());
         // 1. factor the odd positions
-        std::vector<cplx*> fa;
+        std::vector<cplx*> fa, fd;
         std::vector<int*> fp;
         for (int o = 1; o < sz; o += 2) {
             fa.push_back(cur.D[o]);
             fp.push_back(ipiv_of(cur.idx[o]));
+            fd.push_back(dinv_of(cur.idx[o]));
         }
         // singular flags indexed by original block: use a per-level scratch via the pointer list
         {
@@ -695,7 +699,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             DBuf<int> flag;
             flag.ensure(fa.size());
             flag.zero(s);
-            lu_factor_batched(nb, nb, fa, fp, flag.p, s, c.ws);
+            lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
             std::vector<int> hf(fa.size());
             QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
             QPS_CUDA(cudaStreamSynchronize(s));
@@ -709,15 +713,16 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         }
         // 2. Y = D^{-1} [L | U] and y_f = D^{-1} f for the odd positions (in place)
         {
-            std::vector<cplx*> ma, mb, va, vb;
+            std::vector<cplx*> ma, mb, md, va, vb, vd;
             std::vector<int*> mp, vp;
             for (int o = 1; o < sz; o += 2) {
-                ma.push_back(cur.D[o]); mp.push_back(ipiv_of(cur.idx[o])); mb.push_back(cur.L[o]);
-                if (cur.U[o]) { ma.push_back(cur.D[o]); mp.push_back(ipiv_of(cur.idx[o])); mb.push_back(cur.U[o]); }
-                va.push_back(cur.D[o]); vp.push_back(ipiv_of(cur.idx[o])); vb.push_back(cur.F[o]);
+                const int j = cur.idx[o];
+                ma.push_back(cur.D[o]); mp.push_back(ipiv_of(j)); md.push_back(dinv_of(j)); mb.push_back(cur.L[o]);
+                if (cur.U[o]) { ma.push_back(cur.D[o]); mp.push_back(ipiv_of(j)); md.push_back(dinv_of(j)); mb.push_back(cur.U[o]); }
+                va.push_back(cur.D[o]); vp.push_back(ipiv_of(j)); vd.push_back(dinv_of(j)); vb.push_back(cur.F[o]);
             }
-            lu_solve_batched(nb, nb, ma, mp, mb, nb, nb, s, c.ws);
-            lu_solve_batched(nb, nb, va, vp, vb, nb, 1, s, c.ws);
+            lu_solve_batched(nb, nb, ma, mp, md, mb, nb, nb, s, c.ws);
+            lu_solve_batched(nb, nb, va, vp, vd, vb, nb, 1, s, c.ws);
         }
         // 3. updates of the even positions
         const int nsz = (sz + 1) / 2;
@@ -800,12 +805,12 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     // final single block
     {
         const BcrLevel& last = c.levels[lvl];
-        std::vector<cplx*> fa{last.D[0]};
+        std::vector<cplx*> fa{last.D[0]}, fd{dinv_of(last.idx[0])};
         std::vector<int*> fp{ipiv_of(last.idx[0])};
         DBuf<int> flag;
         flag.ensure(1);
         flag.zero(s);
-        lu_factor_batched(nb, nb, fa, fp, flag.p, s, c.ws);
+        lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
         int hf = 0;
         QPS_D2H(&hf, flag.p, sizeof(int), s);
         QPS_CUDA(cudaStreamSynchronize(s));
@@ -815,7 +820,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                         "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1), j + 1);
         }
         std::vector<cplx*> vb{last.F[0]};
-        lu_solve_batched(nb, nb, fa, fp, vb, nb, 1, s, c.ws);
+        lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
     }
     (void)check_singular;
     // back substitution: eta_o = y_f(o) - Y_L(o) eta_{o-1} - Y_U(o) eta_{o+1}, level by level upward.
