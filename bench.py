@@ -1,0 +1,270 @@
+"""Benchmark: the 1000-layer quasi-periodic multilayer solve on B200.
+
+Workload (BASELINE.json configs[3]): 1000 seeded sinusoidal
+interfaces, N = 300 nodes each (6e5 density unknowns), k_i ~ U[10, 30],
+P = 80, Mw = 40, M = 60, K = 20, theta = -pi/5.  One step = one full solve
+through the product library: Nystrom fill -> Schur complements -> block
+cyclic reduction -> recovery of proxies/Bragg amplitudes.
+
+  value : layers/s = (I x ranks) / device step time (CUDA events on the
+          solver's stream, barrier + synchronize around the timed region, max
+          over ranks); the geometry is already resident in HBM.
+  e2e   : the same metric through the public C-ABI from HOST data: geometry
+          build + H2D, solve, D2H of eta/c/aU/aD, timed per step.
+  roofline : dominant kernel family over the timed region (library
+          CUDA-event instrumentation), achieved TFLOP/s vs the FP64 DMMA peak
+          measured by a microbenchmark in the same run.
+  cpu_baseline : the reference (oracle/_ref, the qpscat headers compiled
+          unmodified against oracle/shim) on a bounded I-layer sample of the
+          same per-layer sizes, all host threads, rank 0 only.
+
+Multi-GPU (--gpus N under torchrun): replicas only — each rank solves its own
+1000-layer stack (the north star keeps one solve on one GPU), no collective on
+the data path; "scaling": "weak".
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "1000-layer solve wall time & layers/s; kernel evals/s; % of FP64 peak"
+ORACLE = os.path.join(ROOT, "oracle", "_ref", "libqpscat_ref.so")
+CFG = 4
+
+
+def workload_config(I, N, num, K, theta, seed):
+    return {"workload": f"cfg4: {I} seeded sinusoidal interfaces, N={N}, P={num.P}, Mw={num.Mw}, M={num.M}, "
+                        f"K={K}, k~U[10,30], theta={theta:.6f}",
+            "I": I, "N": N, "P": num.P, "Mw": num.Mw, "M": num.M, "K": K, "seed": seed,
+            "density_unknowns": 2 * N * I, "parallelism": "replicas",
+            "l2": "inputs larger than L2 (A' alone is 17.3 GB >> 126 MB), no flush needed"}
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    return world, rank, local, dist
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def allmax(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(I_sample, threads, reps=1):
+    """Time the reference (oracle/_ref) on a bounded sample of the same workload."""
+    from paper_1410_5003_b200 import configs
+    from paper_1410_5003_b200.qpscat import Solver
+    st, num, om, th, K, meta = configs.config(CFG, n_interfaces=I_sample)
+    s = Solver(lib=ORACLE)
+    s.set_num_threads(threads)
+    s.build_geometry(st, num)
+    s.make_problem(om, th, K)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        s.solve()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    ph = s.phase_times()
+    evals = s.fill_evals()["reference"]
+    s.close()
+    return {"value": I_sample / best, "unit": "layers/s", "cores": threads, "kind": "reference",
+            "sample": f"{I_sample}-layer prefix of the cfg4 stack (same N={meta['N']}, P, Mw, M, K), "
+                      f"one full solve (fill {ph['fill_ms'] + ph['assemble_ms']:.0f} ms, schur {ph['schur_ms']:.0f} ms, "
+                      f"thomas {ph['solve_ms'] + ph['recover_ms']:.0f} ms)",
+            "seconds": best, "kernel_evals_per_s": evals / ((ph["fill_ms"] + ph["assemble_ms"]) * 1e-3)}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.ref_layers, threads)
+        if i >= args.warmup:
+            vals.append(cb)
+    v = statistics.median(c["value"] for c in vals)
+    from paper_1410_5003_b200 import configs
+    st, num, om, th, K, meta = configs.config(CFG)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "layers/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * 1000 / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)",
+            "data": "synthetic (seeded, paper_1410_5003_b200/configs.py)",
+            "config": workload_config(meta["I"], meta["N"], num, K, th, meta["seed"]),
+            "cpu_baseline": {k: vals[-1][k] for k in ("cores", "kind", "sample")} | {"value": v, "unit": "layers/s"},
+            "e2e": {"value": v, "unit": "layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--layers", type=int, default=None, help="override I (default: the config's 1000)")
+    ap.add_argument("--ref-layers", type=int, default=8, help="I of the bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    from paper_1410_5003_b200 import configs
+    from paper_1410_5003_b200.qpscat import Solver
+    st, num, om, th, K, meta = configs.config(CFG, n_interfaces=args.layers)
+    I, N = meta["I"], meta["N"]
+    s = Solver(device=local)
+    peaks = s.fp64_peaks()  # same-run FP64 microbenchmarks (north star)
+    s.build_geometry(st, num)
+    s.make_problem(om, th, K)
+    for _ in range(args.warmup):
+        s.solve()
+    # ---- device-timed region (inputs resident in HBM) ----
+    launches0 = s.launch_count()
+    s.prof_reset()
+    s.prof_enable(True)
+    barrier(dist)
+    totals = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            s.solve()
+            totals.append(s.phase_times()["total_ms"])
+        barrier(dist)
+    s.prof_enable(False)
+    launches = s.launch_count() - launches0
+    stats = s.prof_stats()
+    phases = s.phase_times()
+    step_ms = allmax(dist, sum(totals) / len(totals))
+    value = world * I / (step_ms * 1e-3)
+    rt = s.reflection_transmission()
+    evals = s.fill_evals()
+    # dominant kernel family over the timed region
+    dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    fams = {k: v for k, v in stats.items()}
+    gemm_ms = sum(v["ms"] for k, v in fams.items() if k.startswith("zgemm"))
+    gemm_fl = sum(v["flops"] for k, v in fams.items() if k.startswith("zgemm"))
+    fill = {k: v for k, v in fams.items() if k.startswith("fill_")}
+    fill_ms = sum(v["ms"] for v in fill.values())
+    fill_units = sum(v["units"] for v in fill.values())
+    peak = peaks["dmma_tflops"]
+    dname, dv = dom
+    d_tf = dv["flops"] / (dv["ms"] * 1e-3) / 1e12
+    roofline = {"kernel": dname, "bound": "tensor", "achieved": d_tf, "peak": peak, "unit": "TFLOP/s",
+                "frac": d_tf / peak, "traffic": None,
+                "peak_source": "FP64 DMMA (mma.sync m8n8k4 f64) microbenchmark in this run; bf16 peaks of "
+                               "MEASURED_PEAKS.json do not apply to FP64",
+                "algorithmic": "8*M*N*K real flops per complex GEMM task, summed over the batched launches",
+                "launches": dv["launches"], "avg_launch_ms": dv["ms"] / max(1, dv["launches"])}
+    # ---- end-to-end through the public API from host data ----
+    barrier(dist)
+    e2e_ms = []
+    s.prof_reset()
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        s.build_geometry(st, num)
+        s.make_problem(om, th, K)
+        s.solve()
+        sol = s.solution()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    xfer = s.transfer_bytes()
+    e2e_step = allmax(dist, statistics.median(e2e_ms))
+    e2e = {"value": world * I / (e2e_step * 1e-3), "unit": "layers/s",
+           "h2d_bytes_per_step": xfer["h2d"] // max(1, len(e2e_ms)),
+           "d2h_bytes_per_step": xfer["d2h"] // max(1, len(e2e_ms)), "ms_per_step": e2e_step}
+    cb = None
+    if rank == 0 and not args.no_cpu_baseline and os.path.exists(ORACLE):
+        cb = cpu_baseline(args.ref_layers, os.cpu_count() or 1)
+        cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "layers/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "c128 (f64 complex)",
+                "data": "synthetic (seeded, paper_1410_5003_b200/configs.py)",
+                "config": workload_config(I, N, num, K, th, meta["seed"]),
+                "e2e": e2e, "roofline": roofline, "cpu_baseline": cb,
+                "clocks": clk.summary(), "gpu_launches": launches,
+                "phases_ms": {k: round(v, 3) for k, v in phases.items()},
+                "kernel_evals_per_s": evals["performed"] / (fill_ms * 1e-3) if fill_ms else None,
+                "fill_evals": evals, "fill_tflops_nominal": 200.0 * fill_units / (fill_ms * 1e-3) / 1e12
+                if fill_ms else None,
+                "fill_frac_of_dfma_peak": (200.0 * fill_units / (fill_ms * 1e-3) / 1e12) / peaks["dfma_tflops"]
+                if fill_ms else None,
+                "gemm_tflops": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
+                "fp64_peaks_tflops": peaks, "flux_error": rt["flux_error"], "R": rt["R"], "T": rt["T"],
+                "families_ms": {k: round(v["ms"] / args.steps, 3) for k, v in sorted(fams.items(),
+                                                                                     key=lambda kv: -kv[1]["ms"])}}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -858,7 +858,11 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
             by += 16.0 * (double(M) * t.K[q] + double(t.K[q]) * N);
         }
     by += 16.0 * double(M) * N * tasks.size() * ((beta.re != 0.0 || beta.im != 0.0) ? 2 : 1);
-    ProfScope ps("zgemm", s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
+    int kmax = 0;
+    for (const auto& t : tasks)
+        for (int q = 0; q < t.nseg; ++q) kmax = std::max(kmax, t.K[q]);
+    const char* nm = (kmax <= 64) ? (M <= 64 ? "zgemm_k64_m64" : "zgemm_k64") : (M >= 256 && N >= 256 ? "zgemm_big" : "zgemm_mid");
+    ProfScope ps(nm, s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
     for (size_t off = 0; off < tasks.size(); off += 65535) {
         const unsigned cnt = unsigned(std::min<size_t>(65535, tasks.size() - off));
         zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
