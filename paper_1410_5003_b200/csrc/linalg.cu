@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <functional>
 
 #include "linalg.cuh"
 #include "prof.h"
@@ -623,6 +624,24 @@ __global__ void lu_swap_kernel(int n, int ld, cplx* const* __restrict__ Ap, cons
     }
 }
 
+// apply the interchanges of rows k0..kend-1 to columns [c0, c1)
+__global__ void lu_swap_range_kernel(int ld, cplx* const* __restrict__ Ap, const int* const* __restrict__ Pp, int k0,
+                                     int kend, int c0, int c1) {
+    cplx* A = Ap[blockIdx.y];
+    const int* ipiv = Pp[blockIdx.y];
+    const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= c1) return;
+    cplx* col = A + size_t(c) * ld;
+    for (int k = k0; k < kend; ++k) {
+        const int p = ipiv[k];
+        if (p != k) {
+            const cplx t = col[k];
+            col[k] = col[p];
+            col[p] = t;
+        }
+    }
+}
+
 // rows r0..r1-1 of B_b <- L11^{-1} (unit lower, diagonal block of A_b) B, columns c0..c0+nc-1
 __global__ void trsm_lower_unit_kernel(int ld, const cplx* const* __restrict__ Ap, cplx* const* __restrict__ Bp,
                                        int ldb, int r0, int r1, int c0, int nc) {
@@ -662,13 +681,15 @@ __global__ void trsm_upper_kernel(int ld, const cplx* const* __restrict__ Ap, cp
 }
 
 // Inverse of the bs x bs diagonal blocks of a factored LU (unit-lower L and/or
-// upper U), one CTA per (block, matrix), one thread per column.  Output per
+// upper U), one CTA per (block, matrix).  4 lanes per column (bs = 64 -> 256
+// threads) split each dot product; a column's lanes share a warp, so the
+// row-by-row recurrences need only warp-level synchronisation.  Output per
 // block: [L^{-1} | U^{-1}] as two bs x bs column-major tiles (ld bs).
-__global__ void tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap, cplx* const* __restrict__ Op, int bs,
-                               int k0_first, int mode) {
+__global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+                                                      cplx* const* __restrict__ Op, int bs, int k0_first, int mode) {
     extern __shared__ cplx smem[];
-    cplx* T = smem;            // bs x bs block of the factor
-    cplx* X = smem + bs * bs;  // inverse being built
+    cplx* T = smem;            // bs x bs block of the factor (column-major)
+    cplx* X = smem + bs * bs;  // inverse being built (column-major)
     const cplx* A = Ap[blockIdx.y];
     cplx* O = Op[blockIdx.y] + size_t(blockIdx.x) * 2 * bs * bs;
     const int k0 = k0_first + blockIdx.x * bs;
@@ -678,43 +699,54 @@ __global__ void tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap, cplx
         T[e] = (i < sz && j < sz) ? A[size_t(k0 + j) * ld + k0 + i] : cplx{0, 0};
     }
     __syncthreads();
-    const int j = threadIdx.x;
+    const int j = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const bool active = j < bs;
     if (mode & 1) {
-        if (j < bs)
-            for (int i = 0; i < bs; ++i) {
-                cplx v{0, 0};
-                if (i == j) v = cplx{1, 0};
-                else if (i > j && i < sz) {
-                    for (int l = j; l < i; ++l) {
-                        const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
-                        v.re -= t.re;
-                        v.im -= t.im;
-                    }
+        for (int i = 0; i < bs; ++i) {
+            cplx sacc{0, 0};
+            if (active && i > j)
+                for (int l = j + part; l < i; l += 4) {
+                    const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
+                    sacc.re += t.re;
+                    sacc.im += t.im;
                 }
-                X[j * bs + i] = v;
-            }
+            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 1);
+            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 1);
+            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 2);
+            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
+            if (active && part == 0)
+                X[j * bs + i] = (i == j) ? cplx{1, 0} : (i > j && i < sz) ? cplx{-sacc.re, -sacc.im} : cplx{0, 0};
+            __syncwarp();
+        }
         __syncthreads();
         for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) O[e] = X[e];
         __syncthreads();
     }
     if (mode & 2) {
-        if (j < bs) {
-            for (int i = bs - 1; i >= 0; --i) {
+        for (int i = bs - 1; i >= 0; --i) {
+            cplx sacc{0, 0};
+            if (active && i < j)
+                for (int l = i + 1 + part; l <= j; l += 4) {
+                    const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
+                    sacc.re += t.re;
+                    sacc.im += t.im;
+                }
+            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 1);
+            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 1);
+            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 2);
+            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
+            if (active && part == 0) {
                 cplx v{0, 0};
                 if (i < sz && j < sz && i <= j) {
-                    cplx s = (i == j) ? cplx{1, 0} : cplx{0, 0};
-                    for (int l = i + 1; l <= j; ++l) {
-                        const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
-                        s.re -= t.re;
-                        s.im -= t.im;
-                    }
+                    const cplx num{(i == j ? 1.0 : 0.0) - sacc.re, -sacc.im};
                     const cplx d = T[i * bs + i];
-                    v = (d.re == 0.0 && d.im == 0.0) ? cplx{0, 0} : cdiv(s, d);
+                    v = (d.re == 0.0 && d.im == 0.0) ? cplx{0, 0} : cdiv(num, d);
                 } else if (i == j) {
                     v = cplx{1, 0};
                 }
                 X[j * bs + i] = v;
             }
+            __syncwarp();
         }
         __syncthreads();
         for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) O[bs * bs + e] = X[e];
@@ -911,9 +943,101 @@ void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, 
         attr = true;
     }
     ProfScope ps("tri_inv", s, 8.0 / 3.0 * count * nblk * double(bs) * bs * bs * ((mode == 3) ? 2 : 1));
-    tri_inv_kernel<<<dim3(nblk, count), bs, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
+    tri_inv_kernel<<<dim3(nblk, count), 4 * bs, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
     QPS_CUDA(cudaGetLastError());
 }
+}  // namespace
+
+namespace {
+
+struct LuCtx {
+    int n, ld, count;
+    const std::vector<cplx*>& hA;
+    const std::vector<int*>& hP;
+    const std::vector<cplx*>& hD;
+    cplx* const* dA;
+    int* const* dP;
+    cplx* const* dD;
+    int* sing;
+    cudaStream_t s;
+    Workspace& ws;
+};
+
+void gemm_update(LuCtx& L, int M, int N, int K, size_t aoff, size_t boff, size_t coff, cplx alpha, cplx beta,
+                 const std::vector<cplx*>& Abase, const std::vector<cplx*>& Bbase, int ldb) {
+    auto& tasks = L.ws.h_gemm;
+    tasks.assign(L.count, GemmTask{});
+    for (int b = 0; b < L.count; ++b) {
+        GemmTask& t = tasks[b];
+        t.nseg = 1;
+        t.A[0] = Abase[b] + aoff;
+        t.lda[0] = L.ld;
+        t.B[0] = Bbase[b] + boff;
+        t.ldb[0] = ldb;
+        t.K[0] = K;
+        t.C = Bbase[b] + coff;
+        t.ldc = ldb;
+    }
+    zgemm_batched(M, N, alpha, beta, tasks, L.s, L.ws.gemm_tasks);
+}
+
+// X[r0:r1, c0:c0+nc] <- L[r0:r1, r0:r1]^{-1} X (unit lower) inside the factor itself
+// (U12 of the recursive LU), leaves of <= 64 rows through on-demand tile inverses.
+void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc) {
+    const int m = r1 - r0;
+    if (m <= kTB) {
+        launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, kTB, r0, 1, 1, L.s);  // tile 0 of Dinv as scratch
+        auto& tasks = L.ws.h_gemm;
+        tasks.assign(L.count, GemmTask{});
+        for (int b = 0; b < L.count; ++b) {
+            GemmTask& t = tasks[b];
+            t.nseg = 1;
+            t.A[0] = L.hD[b];
+            t.lda[0] = kTB;
+            t.B[0] = L.hA[b] + size_t(c0) * L.ld + r0;
+            t.ldb[0] = L.ld;
+            t.K[0] = m;
+            t.C = L.hA[b] + size_t(c0) * L.ld + r0;  // in place: <= 64 rows, one CTA per column tile
+            t.ldc = L.ld;
+        }
+        zgemm_batched(m, nc, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks);
+        return;
+    }
+    const int h = ((m + kTB - 1) / kTB + 1) / 2 * kTB;
+    trsm_lower_in_factor(L, r0, r0 + h, c0, nc);
+    // X[r0+h:r1] -= L[r0+h:r1, r0:r0+h] X[r0:r0+h]
+    gemm_update(L, m - h, nc, h, size_t(r0) * L.ld + r0 + h, size_t(c0) * L.ld + r0, size_t(c0) * L.ld + r0 + h,
+                cplx{-1, 0}, cplx{1, 0}, L.hA, L.hA, L.ld);
+    trsm_lower_in_factor(L, r0 + h, r1, c0, nc);
+}
+
+// recursive LU of columns [c0, c0 + nc) (rows c0..n), Toledo's algorithm
+void lu_rec(LuCtx& L, int c0, int nc) {
+    if (nc <= kNB) {
+        ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(L.n - c0) * nc * nc / 2.0);
+        lu_panel_kernel<<<L.count, 256, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, L.sing);
+        QPS_CUDA(cudaGetLastError());
+        return;
+    }
+    const int h = ((nc + kNB - 1) / kNB) / 2 * kNB;
+    lu_rec(L, c0, h);
+    {  // left-half interchanges onto the right half
+        ProfScope ps("lu_swap", L.s, 0.0);
+        lu_swap_range_kernel<<<dim3((nc - h + 127) / 128, L.count), 128, 0, L.s>>>(L.ld, L.dA, L.dP, c0, c0 + h,
+                                                                                    c0 + h, c0 + nc);
+    }
+    trsm_lower_in_factor(L, c0, c0 + h, c0 + h, nc - h);
+    // A22 -= A21 A12 over rows c0+h..n, cols c0+h..c0+nc
+    gemm_update(L, L.n - c0 - h, nc - h, h, size_t(c0) * L.ld + c0 + h, size_t(c0 + h) * L.ld + c0,
+                size_t(c0 + h) * L.ld + c0 + h, cplx{-1, 0}, cplx{1, 0}, L.hA, L.hA, L.ld);
+    lu_rec(L, c0 + h, nc - h);
+    {  // right-half interchanges back onto the left half
+        ProfScope ps("lu_swap", L.s, 0.0);
+        lu_swap_range_kernel<<<dim3((h + 127) / 128, L.count), 128, 0, L.s>>>(L.ld, L.dA, L.dP, c0 + h, c0 + nc,
+                                                                               c0, c0 + h);
+    }
+}
+
 }  // namespace
 
 void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,
@@ -922,54 +1046,11 @@ void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::v
     if (count == 0) return;
     ws.ptrs.upload(hA, s);
     ws.iptrs.upload(hP, s);
-    ws.ptrs2.upload(hDinv, s);
-    cplx* const* d_A = ws.ptrs.p;
-    int* const* d_ipiv = ws.iptrs.p;
-    cplx* const* d_D = ws.ptrs2.p;
-    auto& tasks = ws.h_gemm;
-    for (int k0 = 0; k0 < n; k0 += kNB) {
-        const int kend = std::min(k0 + kNB, n);
-        {
-            ProfScope ps("lu_panel", s, 8.0 * count * double(n - k0) * (kend - k0) * (kend - k0) / 2.0);
-            lu_panel_kernel<<<count, 256, 0, s>>>(n, ld, d_A, d_ipiv, k0, d_singular);
-        }
-        {
-            ProfScope ps("lu_swap", s, 0.0);
-            lu_swap_kernel<<<dim3((n + 127) / 128, count), 128, 0, s>>>(n, ld, d_A, d_ipiv, k0, kend, n, k0, kend);
-        }
-        const int rest = n - kend;
-        if (rest > 0) {
-            // U12 = L11^{-1} A12 via the explicit inverse of the unit-lower 32x32 L11 (scratch in Dinv)
-            launch_tri_inv(n, ld, d_A, d_D, count, kNB, k0, 1, 1, s);
-            tasks.assign(count, GemmTask{});
-            for (int b = 0; b < count; ++b) {
-                GemmTask& t = tasks[b];
-                t.nseg = 1;
-                t.A[0] = hDinv[b];
-                t.lda[0] = kNB;
-                t.B[0] = hA[b] + size_t(kend) * ld + k0;
-                t.ldb[0] = ld;
-                t.K[0] = kend - k0;
-                t.C = hA[b] + size_t(kend) * ld + k0;  // in place: M <= 64 rows, one CTA per column tile
-                t.ldc = ld;
-            }
-            zgemm_batched(kend - k0, rest, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks);
-            for (int b = 0; b < count; ++b) {
-                GemmTask& t = tasks[b];
-                t.nseg = 1;
-                t.A[0] = hA[b] + size_t(k0) * ld + kend;
-                t.lda[0] = ld;
-                t.B[0] = hA[b] + size_t(kend) * ld + k0;
-                t.ldb[0] = ld;
-                t.K[0] = kend - k0;
-                t.C = hA[b] + size_t(kend) * ld + kend;
-                t.ldc = ld;
-            }
-            zgemm_batched(rest, rest, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
-        }
-    }
-    // inverse 64x64 diagonal blocks of L and U for the GEMM-shaped solves
-    launch_tri_inv(n, ld, d_A, d_D, count, kTB, 0, (n + kTB - 1) / kTB, 3, s);
+    ws.ptrs3.upload(hDinv, s);
+    LuCtx L{n, ld, count, hA, hP, hDinv, ws.ptrs.p, ws.iptrs.p, ws.ptrs3.p, d_singular, s, ws};
+    lu_rec(L, 0, n);
+    // inverse 64x64 diagonal tiles of L and U for the GEMM-shaped solves
+    launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 3, s);
 }
 
 void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,
@@ -987,8 +1068,8 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
         QPS_CUDA(cudaGetLastError());
     }
     auto& tasks = ws.h_gemm;
-    const int nblk = (n + kTB - 1) / kTB;
-    auto diag = [&](int bi, int which) {  // B_k <- inv(tile) B_k in place (rows <= 64)
+    // leaf: B[k0:kend] <- inverse tile * B[k0:kend] (in place, <= 64 rows)
+    auto leaf = [&](int bi, int which) {
         const int k0 = bi * kTB, kend = std::min(k0 + kTB, n);
         tasks.assign(count, GemmTask{});
         for (int b = 0; b < count; ++b) {
@@ -1004,44 +1085,42 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
         }
         zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks);
     };
-    for (int bi = 0; bi < nblk; ++bi) {  // forward: unit-lower L
-        const int k0 = bi * kTB, kend = std::min(k0 + kTB, n);
-        diag(bi, 0);
-        if (kend < n) {
-            tasks.assign(count, GemmTask{});
-            for (int b = 0; b < count; ++b) {
-                GemmTask& t = tasks[b];
-                t.nseg = 1;
-                t.A[0] = hA[b] + size_t(k0) * ld + kend;
-                t.lda[0] = ld;
-                t.B[0] = hB[b] + k0;
-                t.ldb[0] = ldb;
-                t.K[0] = kend - k0;
-                t.C = hB[b] + kend;
-                t.ldc = ldb;
-            }
-            zgemm_batched(n - kend, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+    auto update = [&](int M, int K, size_t aoff, int brow, int crow) {
+        tasks.assign(count, GemmTask{});
+        for (int b = 0; b < count; ++b) {
+            GemmTask& t = tasks[b];
+            t.nseg = 1;
+            t.A[0] = hA[b] + aoff;
+            t.lda[0] = ld;
+            t.B[0] = hB[b] + brow;
+            t.ldb[0] = ldb;
+            t.K[0] = K;
+            t.C = hB[b] + crow;
+            t.ldc = ldb;
         }
-    }
-    for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: upper U
-        const int k0 = bi * kTB, kend = std::min(k0 + kTB, n);
-        diag(bi, 1);
-        if (k0 > 0) {
-            tasks.assign(count, GemmTask{});
-            for (int b = 0; b < count; ++b) {
-                GemmTask& t = tasks[b];
-                t.nseg = 1;
-                t.A[0] = hA[b] + size_t(k0) * ld;
-                t.lda[0] = ld;
-                t.B[0] = hB[b] + k0;
-                t.ldb[0] = ldb;
-                t.K[0] = kend - k0;
-                t.C = hB[b];
-                t.ldc = ldb;
-            }
-            zgemm_batched(k0, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
-        }
-    }
+        zgemm_batched(M, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+    };
+    // recursive triangular solves on 64-aligned splits: the top levels carry most
+    // flops as GEMMs with K = n/2, n/4, ...
+    std::function<void(int, int)> lower = [&](int b0, int b1) {  // tile range [b0, b1)
+        if (b1 - b0 == 1) return leaf(b0, 0);
+        const int bm = (b0 + b1 + 1) / 2;
+        lower(b0, bm);
+        const int r0 = b0 * kTB, rm = bm * kTB, r1 = std::min(b1 * kTB, n);
+        update(r1 - rm, rm - r0, size_t(r0) * ld + rm, r0, rm);
+        lower(bm, b1);
+    };
+    std::function<void(int, int)> upper = [&](int b0, int b1) {
+        if (b1 - b0 == 1) return leaf(b0, 1);
+        const int bm = (b0 + b1 + 1) / 2;
+        upper(bm, b1);
+        const int r0 = b0 * kTB, rm = bm * kTB, r1 = std::min(b1 * kTB, n);
+        update(rm - r0, r1 - rm, size_t(rm) * ld + r0, rm, r0);
+        upper(b0, bm);
+    };
+    const int nblk = (n + kTB - 1) / kTB;
+    lower(0, nblk);
+    upper(0, nblk);
 }
 
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {

@@ -93,7 +93,7 @@ double measure_dmma_tflops(cudaStream_t s);
 struct Workspace {
     DBuf<GemmTask> gemm_tasks;
     DBuf<GemvTask> gemv_tasks;
-    DBuf<cplx*> ptrs, ptrs2;
+    DBuf<cplx*> ptrs, ptrs2, ptrs3;
     DBuf<int*> iptrs;
     std::vector<GemmTask> h_gemm;
 };
