@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 
 #include "linalg.cuh"
@@ -19,7 +20,7 @@ namespace qpsb {
 namespace {
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
@@ -113,13 +114,20 @@ __global__ void __launch_bounds__(128, 2) zgemm_kernel(int M, int N, cplx alpha,
                     br[j] = Bs[buf][0][kq][wn + 8 * j + r];
                     bi[j] = Bs[buf][1][kq][wn + 8 * j + r];
                 }
+                // two passes of 32 independent DMMAs (dependent updates of one
+                // accumulator 32 instructions apart)
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         dmma(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
-                        dmma(acc[i][j][0][0], acc[i][j][0][1], nai[i], bi[j]);
                         dmma(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);
+                    }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        dmma(acc[i][j][0][0], acc[i][j][0][1], nai[i], bi[j]);
                         dmma(acc[i][j][1][0], acc[i][j][1][1], ai[i], br[j]);
                     }
             }
@@ -128,6 +136,144 @@ __global__ void __launch_bounds__(128, 2) zgemm_kernel(int M, int N, cplx alpha,
         }
     }
     // epilogue
+    const bool use_beta = (beta.re != 0.0 || beta.im != 0.0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = m0 + wm + 8 * i + (lane >> 2);
+                const int col = n0 + wn + 8 * j + 2 * (lane & 3) + e;
+                if (row < M && col < N) {
+                    const double vr = acc[i][j][0][e], vi = acc[i][j][1][e];
+                    cplx out{alpha.re * vr - alpha.im * vi, alpha.re * vi + alpha.im * vr};
+                    cplx* p = T.C + size_t(col) * T.ldc + row;
+                    if (use_beta) {
+                        const cplx o = *p;
+                        out.re += beta.re * o.re - beta.im * o.im;
+                        out.im += beta.re * o.im + beta.im * o.re;
+                    }
+                    *p = out;
+                }
+            }
+}
+
+// ---------------------------------------------------------------------------
+// v2: cp.async multi-stage pipeline.  Tiles are copied 16 B (one complex) at a
+// time straight into shared memory (interleaved re/im, [k][m] and [k][n]
+// layouts, leading dimension = tile + 2 complex so that the DMMA fragment
+// pattern (k = lane & 3, m = lane >> 2) hits 8 distinct 16-byte bank groups
+// per quarter warp).  Out-of-range elements are zero-filled by cp.async's
+// src-size operand.  K may be the concatenation of two products (nseg = 2).
+// ---------------------------------------------------------------------------
+constexpr int G2_BM = 64, G2_BN = 64, G2_BK = 16, G2_ST = 3;
+constexpr int G2_LDA = G2_BM + 2, G2_LDB = G2_BN + 2;
+constexpr int G2_STAGE = G2_BK * (G2_LDA + G2_LDB);  // complex elements per stage
+constexpr size_t G2_SMEM = size_t(G2_ST) * G2_STAGE * sizeof(double2);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__global__ void __launch_bounds__(128, 2) zgemm_v2_kernel(int M, int N, cplx alpha, cplx beta,
+                                                          const GemmTask* __restrict__ tasks, int tiles_m) {
+    extern __shared__ double2 g2_smem[];
+    const GemmTask& T = tasks[blockIdx.y];
+    const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
+    const int m0 = tm * G2_BM, n0 = tn * G2_BN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int nseg = T.nseg;
+    const int K0 = T.K[0], K1 = nseg > 1 ? T.K[1] : 0;
+    const int c0n = (K0 + G2_BK - 1) / G2_BK, c1n = (K1 + G2_BK - 1) / G2_BK;
+    const int nchunks = c0n + c1n;
+
+    auto issue = [&](int c, int stage) {
+        const int sgi = c < c0n ? 0 : 1;
+        const int k0 = (c < c0n ? c : c - c0n) * G2_BK;
+        const cplx* __restrict__ A = T.A[sgi];
+        const cplx* __restrict__ B = T.B[sgi];
+        const int lda = T.lda[sgi], ldb = T.ldb[sgi], K = T.K[sgi];
+        double2* As = g2_smem + stage * G2_STAGE;
+        double2* Bs = As + G2_BK * G2_LDA;
+#pragma unroll
+        for (int i = 0; i < (G2_BM * G2_BK) / 128; ++i) {
+            const int idx = tid + 128 * i;
+            const int row = idx % G2_BM, kk = idx / G2_BM;
+            const int gm = m0 + row, gk = k0 + kk;
+            const bool ok = gm < M && gk < K;
+            cp_async16(As + kk * G2_LDA + row, ok ? (const void*)(A + size_t(gk) * lda + gm) : (const void*)A, ok);
+        }
+#pragma unroll
+        for (int i = 0; i < (G2_BN * G2_BK) / 128; ++i) {
+            const int idx = tid + 128 * i;
+            const int kk = idx % G2_BK, col = idx / G2_BK;
+            const int gn = n0 + col, gk = k0 + kk;
+            const bool ok = gn < N && gk < K;
+            cp_async16(Bs + kk * G2_LDB + col, ok ? (const void*)(B + size_t(gn) * ldb + gk) : (const void*)B, ok);
+        }
+    };
+
+    double acc[4][4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+
+#pragma unroll
+    for (int st = 0; st < G2_ST - 1; ++st) {
+        if (st < nchunks) issue(st, st);
+        cp_async_commit();
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        cp_async_wait<G2_ST - 2>();
+        __syncthreads();
+        if (c + G2_ST - 1 < nchunks) issue(c + G2_ST - 1, (c + G2_ST - 1) % G2_ST);
+        cp_async_commit();
+        const double2* As = g2_smem + (c % G2_ST) * G2_STAGE;
+        const double2* Bs = As + G2_BK * G2_LDA;
+#pragma unroll
+        for (int ks = 0; ks < G2_BK; ks += 4) {
+            const int kq = ks + (lane & 3), r = lane >> 2;
+            double ar[4], ai[4], nai[4], br[4], bi[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double2 v = As[kq * G2_LDA + wm + 8 * i + r];
+                ar[i] = v.x;
+                ai[i] = v.y;
+                nai[i] = -v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double2 v = Bs[kq * G2_LDB + wn + 8 * j + r];
+                br[j] = v.x;
+                bi[j] = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    dmma(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
+                    dmma(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);
+                }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    dmma(acc[i][j][0][0], acc[i][j][0][1], nai[i], bi[j]);
+                    dmma(acc[i][j][1][0], acc[i][j][1][1], ai[i], br[j]);
+                }
+        }
+    }
+    cp_async_wait<0>();
     const bool use_beta = (beta.re != 0.0 || beta.im != 0.0);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -462,32 +608,50 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
             __syncthreads();
         }
     }
-    // M1 = Q_r E_r (m x r), Q_r = H_0^* ... H_{r-1}^*  (reflectors as applied had tau)
-    for (int c = tid; c < r; c += blockDim.x) {
-        cplx* col = M1 + size_t(c) * m;
-        for (int i = 0; i < m; ++i) col[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
-        for (int kk = c; kk >= 0; --kk) {
-            const cplx tk = cconj(tau[kk]);
-            if (tk.re == 0.0 && tk.im == 0.0) continue;
-            cplx t = col[kk];
-            for (int i = kk + 1; i < m; ++i) {
-                const cplx e = W[size_t(kk) * m + i];
-                t.re += e.re * col[i].re + e.im * col[i].im;
-                t.im += e.re * col[i].im - e.im * col[i].re;
+    // QH = first r rows of Q_r^* = H_{r-1} ... H_0 (reflectors exactly as applied):
+    // column c of QH = H_{r-1} ... H_0 e_c.  Columns are independent; reflectors
+    // are applied in sequence, one warp per column with lanes over rows.
+    {
+        const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+        for (int c = warp; c < m; c += nw) {
+            cplx* col = M1 + size_t(warp) * m;  // per-warp scratch column (M1 holds >= 8 m entries)
+            for (int i = lane; i < m; i += 32) col[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
+            __syncwarp();
+            for (int kk = 0; kk < r; ++kk) {
+                const cplx tk = tau[kk];
+                if (tk.re == 0.0 && tk.im == 0.0) continue;
+                cplx t{0, 0};
+                for (int i = kk + 1 + lane; i < m; i += 32) {
+                    const cplx e = W[size_t(kk) * m + i];
+                    const cplx a = col[i];
+                    t.re += e.re * a.re + e.im * a.im;
+                    t.im += e.re * a.im - e.im * a.re;
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    t.re += __shfl_xor_sync(0xffffffffu, t.re, o);
+                    t.im += __shfl_xor_sync(0xffffffffu, t.im, o);
+                }
+                const cplx ck = col[kk];
+                t.re += ck.re;
+                t.im += ck.im;
+                t = cmul(tk, t);
+                __syncwarp();
+                if (lane == 0) {
+                    col[kk].re -= t.re;
+                    col[kk].im -= t.im;
+                }
+                for (int i = kk + 1 + lane; i < m; i += 32) {
+                    const cplx et = cmul(W[size_t(kk) * m + i], t);
+                    col[i].re -= et.re;
+                    col[i].im -= et.im;
+                }
+                __syncwarp();
             }
-            t = cmul(tk, t);
-            col[kk].re -= t.re;
-            col[kk].im -= t.im;
-            for (int i = kk + 1; i < m; ++i) {
-                const cplx et = cmul(W[size_t(kk) * m + i], t);
-                col[i].re -= et.re;
-                col[i].im -= et.im;
-            }
+            for (int i = lane; i < p; i += 32) QH[size_t(c) * p + i] = i < r ? col[i] : cplx{0, 0};
+            __syncwarp();
         }
     }
     __syncthreads();
-    for (int c = tid; c < m; c += blockDim.x)
-        for (int i = 0; i < p; ++i) QH[size_t(c) * p + i] = i < r ? cconj(M1[size_t(i) * m + c]) : cplx{0, 0};
     // Wz columns: P Z^* e_c for c < r
     for (int c = tid; c < p; c += blockDim.x) {
         cplx* y = Y + size_t(c) * p;
@@ -532,24 +696,42 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
     }
 }
 
-// back substitution with T11 (upper, r x r inside V, ld m), one thread per column
-__global__ void cod_trsm_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
-                                const int* __restrict__ flags) {
+// back substitution with T11 (upper, r x r inside V, ld m), one thread per
+// column of the right-hand side; T11 is staged in shared memory (every thread
+// reads the same entry at the same time: broadcast).
+template <bool kSmem>
+__global__ void __launch_bounds__(128) cod_trsm_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
+                                                       const int* __restrict__ flags) {
+    extern __shared__ cplx tsm_dyn[];
     const int pb = blockIdx.y;
     if (flags && !flags[pb]) return;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncols) return;
     const int m = b.m, r = b.rank[pb];
     const cplx* V = b.V + size_t(pb) * m * b.p;
+    const cplx* tsm;
+    int ldt;
+    if (kSmem) {  // T11 staged in shared memory (interior layers: r <= P = 60..80)
+        for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+            const int i = e % r, j = e / r;
+            tsm_dyn[e] = (i <= j) ? V[size_t(j) * m + i] : cplx{0, 0};
+        }
+        __syncthreads();
+        tsm = tsm_dyn;
+        ldt = r;
+    } else {  // large corner systems read T11 through L1
+        tsm = V;
+        ldt = m;
+    }
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncols) return;
     cplx* x = B + stride * pb + size_t(c) * ldb;
     for (int i = r - 1; i >= 0; --i) {
         cplx s = x[i];
         for (int l = i + 1; l < r; ++l) {
-            const cplx t = cmul(V[size_t(l) * m + i], x[l]);
+            const cplx t = cmul(tsm[size_t(l) * ldt + i], x[l]);
             s.re -= t.re;
             s.im -= t.im;
         }
-        x[i] = cdiv(s, V[size_t(i) * m + i]);
+        x[i] = cdiv(s, tsm[size_t(i) * ldt + i]);
     }
 }
 
@@ -895,9 +1077,19 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
         for (int q = 0; q < t.nseg; ++q) kmax = std::max(kmax, t.K[q]);
     const char* nm = (kmax <= 64) ? (M <= 64 ? "zgemm_k64_m64" : "zgemm_k64") : (M >= 256 && N >= 256 ? "zgemm_big" : "zgemm_mid");
     ProfScope ps(nm, s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
+    static bool attr = false;
+    if (!attr) {
+        QPS_CUDA(cudaFuncSetAttribute(zgemm_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G2_SMEM)));
+        attr = true;
+    }
+    static const bool use_v1 = getenv("QPS_ZGEMM_V2") == nullptr;  // register-staged v1 is faster on B200
     for (size_t off = 0; off < tasks.size(); off += 65535) {
         const unsigned cnt = unsigned(std::min<size_t>(65535, tasks.size() - off));
-        zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
+        if (use_v1)
+            zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
+        else
+            zgemm_v2_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, G2_SMEM, s>>>(M, N, alpha, beta, d_tasks.p + off,
+                                                                              tiles_m);
     }
     QPS_CUDA(cudaGetLastError());
 }
@@ -925,7 +1117,19 @@ void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
 void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, const int* flags, cudaStream_t s) {
     if (b.count == 0 || ncols == 0) return;
     ProfScope ps("cod_trsm", s, 4.0 * b.count * double(b.p) * b.p * ncols);
-    cod_trsm_kernel<<<dim3((ncols + 127) / 128, b.count), 128, 0, s>>>(b, B, ldb, stride, ncols, flags);
+    const size_t sh = size_t(b.p) * b.p * sizeof(cplx);
+    const dim3 grid((ncols + 127) / 128, b.count);
+    if (sh <= 160 * 1024) {
+        static size_t attr = 0;
+        if (sh > attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(160 * 1024)));
+            attr = 160 * 1024;
+        }
+        cod_trsm_kernel<true><<<grid, 128, sh, s>>>(b, B, ldb, stride, ncols, flags);
+    } else {
+        cod_trsm_kernel<false><<<grid, 128, 0, s>>>(b, B, ldb, stride, ncols, flags);
+    }
     QPS_CUDA(cudaGetLastError());
 }
 
