@@ -699,6 +699,59 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
 // back substitution with T11 (upper, r x r inside V, ld m), one thread per
 // column of the right-hand side; T11 is staged in shared memory (every thread
 // reads the same entry at the same time: broadcast).
+// Interior-layer variant: T11 (r x r) and a 64-column chunk of the RHS staged
+// in shared memory; 4 lanes per column split each dot product (warp-level
+// synchronisation only: a column's lanes share a warp).  Backward-stable
+// substitution, no explicit inverse.
+constexpr int kTrsmCols = 64;
+__global__ void __launch_bounds__(256) cod_trsm_chunk_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
+                                                             const int* __restrict__ flags) {
+    extern __shared__ cplx tch[];
+    const int pb = blockIdx.y;
+    if (flags && !flags[pb]) return;
+    const int m = b.m, r = b.rank[pb];
+    const cplx* V = b.V + size_t(pb) * m * b.p;
+    cplx* T = tch;           // r x r (ld r)
+    cplx* X = tch + r * r;   // r x kTrsmCols (ld r)
+    const int c0 = blockIdx.x * kTrsmCols;
+    const int nc = min(kTrsmCols, ncols - c0);
+    cplx* Bp = B + stride * pb + size_t(c0) * ldb;
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+        const int i = e % r, j = e / r;
+        T[e] = (i <= j) ? V[size_t(j) * m + i] : cplx{0, 0};
+    }
+    for (int e = threadIdx.x; e < r * nc; e += blockDim.x) {
+        const int i = e % r, j = e / r;
+        X[j * r + i] = Bp[size_t(j) * ldb + i];
+    }
+    __syncthreads();
+    const int col = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const bool active = col < nc;
+    for (int i = r - 1; i >= 0; --i) {
+        cplx sacc{0, 0};
+        if (active)
+            for (int l = i + 1 + part; l < r; l += 4) {
+                const cplx t = cmul(T[l * r + i], X[col * r + l]);
+                sacc.re += t.re;
+                sacc.im += t.im;
+            }
+        sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 1);
+        sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 1);
+        sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 2);
+        sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
+        if (active && part == 0) {
+            const cplx bi = X[col * r + i];
+            X[col * r + i] = cdiv(cplx{bi.re - sacc.re, bi.im - sacc.im}, T[i * r + i]);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < r * nc; e += blockDim.x) {
+        const int i = e % r, j = e / r;
+        Bp[size_t(j) * ldb + i] = X[j * r + i];
+    }
+}
+
 template <bool kSmem>
 __global__ void __launch_bounds__(128) cod_trsm_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
                                                        const int* __restrict__ flags) {
@@ -1119,7 +1172,17 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
     ProfScope ps("cod_trsm", s, 4.0 * b.count * double(b.p) * b.p * ncols);
     const size_t sh = size_t(b.p) * b.p * sizeof(cplx);
     const dim3 grid((ncols + 127) / 128, b.count);
-    if (sh <= 160 * 1024) {
+    const size_t shc = (size_t(b.p) * b.p + size_t(b.p) * kTrsmCols) * sizeof(cplx);
+    if (shc <= 200 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_trsm_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(200 * 1024)));
+            attr = true;
+        }
+        cod_trsm_chunk_kernel<<<dim3((ncols + kTrsmCols - 1) / kTrsmCols, b.count), 256, shc, s>>>(b, B, ldb, stride,
+                                                                                                   ncols, flags);
+    } else if (sh <= 160 * 1024) {
         static size_t attr = 0;
         if (sh > attr) {
             QPS_CUDA(cudaFuncSetAttribute(cod_trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
