@@ -988,6 +988,106 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
     }
 }
 
+// Row interchanges as a gather: perm_build_kernel composes the pivots
+// [k0, kend) of each matrix into a permutation of rows [k0, n) once (global
+// scratch); row_permute_kernel then permutes columns with one warp per column
+// (coalesced reads/writes through a shared-memory staging column).
+constexpr int kPermWarps = 8;
+__global__ void perm_build_kernel(int n, const int* const* __restrict__ Pp, int* __restrict__ perm_out, int k0,
+                                  int kend) {
+    const int* ipiv = Pp[blockIdx.x];
+    int* perm = perm_out + size_t(blockIdx.x) * n;
+    const int rows = n - k0;
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) perm[i] = k0 + i;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int k = k0; k < kend; ++k) {
+            const int p = ipiv[k];
+            if (p != k) {
+                const int t = perm[k - k0];
+                perm[k - k0] = perm[p - k0];
+                perm[p - k0] = t;
+            }
+        }
+}
+
+__global__ void __launch_bounds__(256) row_permute_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+                                                          const int* __restrict__ perm_all, int k0, int c0, int c1) {
+    extern __shared__ cplx tmp_smem[];
+    cplx* A = Ap[blockIdx.y];
+    const int* perm = perm_all + size_t(blockIdx.y) * n;
+    const int rows = n - k0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    cplx* tw = tmp_smem + size_t(warp) * rows;
+    for (int c = c0 + blockIdx.x * kPermWarps + warp; c < c1; c += gridDim.x * kPermWarps) {
+        cplx* col = A + size_t(c) * ld;
+        for (int i = lane; i < rows; i += 32) tw[i] = col[perm[i]];
+        __syncwarp();
+        for (int i = lane; i < rows; i += 32) col[k0 + i] = tw[i];
+        __syncwarp();
+    }
+}
+
+// LU of one panel of w <= 16 columns held entirely in shared memory
+// (rows c0..n-1), partial pivoting on the modulus like Eigen's PartialPivLU.
+constexpr int kLeaf = 16;
+__global__ void __launch_bounds__(256) lu_panel_smem_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+                                                            int* const* __restrict__ Pp, int c0, int w, int* singular) {
+    extern __shared__ cplx pnl[];
+    cplx* A = Ap[blockIdx.x];
+    int* ipiv = Pp[blockIdx.x];
+    const int rows = n - c0;
+    __shared__ double shv[32];
+    __shared__ int shi[32];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < rows * w; e += blockDim.x) {
+        const int i = e % rows, j = e / rows;
+        pnl[j * rows + i] = A[size_t(c0 + j) * ld + c0 + i];
+    }
+    __syncthreads();
+    for (int k = 0; k < w; ++k) {
+        double v = -1.0;
+        int idx = rows;
+        for (int i = k + tid; i < rows; i += blockDim.x) {
+            const double a = sqrt(cabs2(pnl[k * rows + i]));
+            if (a > v) { v = a; idx = i; }
+        }
+        double best;
+        int piv;
+        block_argmax(v, idx, shv, shi, best, piv);
+        if (tid == 0) ipiv[c0 + k] = c0 + piv;
+        if (piv != k && tid < w) {
+            const cplx t = pnl[tid * rows + k];
+            pnl[tid * rows + k] = pnl[tid * rows + piv];
+            pnl[tid * rows + piv] = t;
+        }
+        __syncthreads();
+        const cplx d = pnl[k * rows + k];
+        const bool zero = (d.re == 0.0 && d.im == 0.0);
+        if (zero) {
+            if (tid == 0) singular[blockIdx.x] = 1;
+        }
+        const cplx inv = zero ? cplx{0, 0} : cdiv(cplx{1.0, 0.0}, d);
+        for (int i = k + 1 + tid; i < rows; i += blockDim.x) {
+            cplx l = pnl[k * rows + i];
+            if (!zero) {
+                l = cmul(l, inv);
+                pnl[k * rows + i] = l;
+            }
+            for (int j = k + 1; j < w; ++j) {
+                const cplx t = cmul(l, pnl[j * rows + k]);
+                pnl[j * rows + i].re -= t.re;
+                pnl[j * rows + i].im -= t.im;
+            }
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < rows * w; e += blockDim.x) {
+        const int i = e % rows, j = e / rows;
+        A[size_t(c0 + j) * ld + c0 + i] = pnl[j * rows + i];
+    }
+}
+
 __global__ void rowswap_rhs_kernel(int n, const int* const* __restrict__ Pp, cplx* const* __restrict__ Bp, int ldb,
                                    int nc) {
     const int* ipiv = Pp[blockIdx.y];
@@ -1056,28 +1156,41 @@ __global__ void copy_blocks_kernel(const cplx* src, int lds, size_t sstride, cpl
     }
 }
 
-__global__ void zgemv_kernel(int M, cplx alpha, cplx beta, const GemvTask* __restrict__ tasks) {
+// y = beta y + alpha sum_s A_s x_s: 32 rows x 8 column groups per CTA, partial
+// sums reduced through shared memory; reads of A are 512-byte coalesced.
+__global__ void __launch_bounds__(256) zgemv_kernel(int M, cplx alpha, cplx beta, const GemvTask* __restrict__ tasks) {
     const GemvTask& T = tasks[blockIdx.y];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
+    const int tx = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int i = blockIdx.x * 32 + tx;
+    __shared__ cplx part[8][32];
     cplx acc{0, 0};
-    for (int sgi = 0; sgi < T.nseg; ++sgi) {
-        const cplx* A = T.A[sgi];
-        const cplx* x = T.x[sgi];
-        const int lda = T.lda[sgi];
-        for (int j = 0; j < T.n[sgi]; ++j) {
-            const cplx t = cmul(A[size_t(j) * lda + i], x[j]);
-            acc.re += t.re;
-            acc.im += t.im;
+    if (i < M)
+        for (int sgi = 0; sgi < T.nseg; ++sgi) {
+            const cplx* A = T.A[sgi];
+            const cplx* x = T.x[sgi];
+            const int lda = T.lda[sgi], nn = T.n[sgi];
+            for (int j = g; j < nn; j += 8) {
+                const cplx t = cmul(A[size_t(j) * lda + i], x[j]);
+                acc.re += t.re;
+                acc.im += t.im;
+            }
         }
+    part[g][tx] = acc;
+    __syncthreads();
+    if (g == 0 && i < M) {
+        cplx s{0, 0};
+        for (int q = 0; q < 8; ++q) {
+            s.re += part[q][tx].re;
+            s.im += part[q][tx].im;
+        }
+        cplx out = cmul(alpha, s);
+        if (beta.re != 0.0 || beta.im != 0.0) {
+            const cplx o = cmul(beta, T.y[i]);
+            out.re += o.re;
+            out.im += o.im;
+        }
+        T.y[i] = out;
     }
-    cplx out = cmul(alpha, acc);
-    if (beta.re != 0.0 || beta.im != 0.0) {
-        const cplx o = cmul(beta, T.y[i]);
-        out.re += o.re;
-        out.im += o.im;
-    }
-    T.y[i] = out;
 }
 
 // ---- FP64 peak microbenchmarks ----
@@ -1217,6 +1330,26 @@ void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, 
 
 namespace {
 
+DBuf<int> g_perm;  // per-matrix permutation scratch
+
+void launch_row_permute(int n, int ld, cplx* const* dA, const int* const* dP, int count, int k0, int kend, int c0,
+                        int c1, cudaStream_t s) {
+    if (c1 <= c0) return;
+    g_perm.ensure(size_t(count) * n);
+    perm_build_kernel<<<count, 128, 0, s>>>(n, dP, g_perm.p, k0, kend);
+    QPS_CUDA(cudaGetLastError());
+    const size_t sh = size_t(kPermWarps) * (n - k0) * sizeof(cplx);
+    static size_t attr = 0;
+    if (sh > attr) {
+        QPS_CUDA(cudaFuncSetAttribute(row_permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(std::max<size_t>(sh, 64 * 1024))));
+        attr = std::max<size_t>(sh, 64 * 1024);
+    }
+    const int nx = std::min((c1 - c0 + kPermWarps - 1) / kPermWarps, 32);
+    row_permute_kernel<<<dim3(nx, count), 256, sh, s>>>(n, ld, dA, g_perm.p, k0, c0, c1);
+    QPS_CUDA(cudaGetLastError());
+}
+
 struct LuCtx {
     int n, ld, count;
     const std::vector<cplx*>& hA;
@@ -1253,14 +1386,15 @@ void gemm_update(LuCtx& L, int M, int N, int K, size_t aoff, size_t boff, size_t
 void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc) {
     const int m = r1 - r0;
     if (m <= kTB) {
-        launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, kTB, r0, 1, 1, L.s);  // tile 0 of Dinv as scratch
+        const int bs = (m + 15) / 16 * 16;  // tile sized to the leaf (16, 32, 48 or 64 rows)
+        launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, bs, r0, 1, 1, L.s);  // tile 0 of Dinv as scratch
         auto& tasks = L.ws.h_gemm;
         tasks.assign(L.count, GemmTask{});
         for (int b = 0; b < L.count; ++b) {
             GemmTask& t = tasks[b];
             t.nseg = 1;
             t.A[0] = L.hD[b];
-            t.lda[0] = kTB;
+            t.lda[0] = bs;
             t.B[0] = L.hA[b] + size_t(c0) * L.ld + r0;
             t.ldb[0] = L.ld;
             t.K[0] = m;
@@ -1280,18 +1414,30 @@ void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc) {
 
 // recursive LU of columns [c0, c0 + nc) (rows c0..n), Toledo's algorithm
 void lu_rec(LuCtx& L, int c0, int nc) {
-    if (nc <= kNB) {
+    const size_t psm = size_t(L.n - c0) * kLeaf * sizeof(cplx);
+    const bool smem_leaf = size_t(L.n) * kLeaf * sizeof(cplx) <= 200 * 1024;
+    const int leaf = smem_leaf ? kLeaf : kNB;
+    if (nc <= leaf) {
         ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(L.n - c0) * nc * nc / 2.0);
-        lu_panel_kernel<<<L.count, 256, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, L.sing);
+        if (smem_leaf) {
+            static bool attr = false;
+            if (!attr) {
+                QPS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              200 * 1024));
+                attr = true;
+            }
+            lu_panel_smem_kernel<<<L.count, 256, psm, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc, L.sing);
+        } else {
+            lu_panel_kernel<<<L.count, 256, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, L.sing);
+        }
         QPS_CUDA(cudaGetLastError());
         return;
     }
-    const int h = ((nc + kNB - 1) / kNB) / 2 * kNB;
+    const int h = ((nc + leaf - 1) / leaf) / 2 * leaf;
     lu_rec(L, c0, h);
     {  // left-half interchanges onto the right half
         ProfScope ps("lu_swap", L.s, 0.0);
-        lu_swap_range_kernel<<<dim3((nc - h + 127) / 128, L.count), 128, 0, L.s>>>(L.ld, L.dA, L.dP, c0, c0 + h,
-                                                                                    c0 + h, c0 + nc);
+        launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0, c0 + h, c0 + h, c0 + nc, L.s);
     }
     trsm_lower_in_factor(L, c0, c0 + h, c0 + h, nc - h);
     // A22 -= A21 A12 over rows c0+h..n, cols c0+h..c0+nc
@@ -1300,8 +1446,7 @@ void lu_rec(LuCtx& L, int c0, int nc) {
     lu_rec(L, c0 + h, nc - h);
     {  // right-half interchanges back onto the left half
         ProfScope ps("lu_swap", L.s, 0.0);
-        lu_swap_range_kernel<<<dim3((h + 127) / 128, L.count), 128, 0, L.s>>>(L.ld, L.dA, L.dP, c0 + h, c0 + nc,
-                                                                               c0, c0 + h);
+        launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0 + h, c0 + nc, c0, c0 + h, L.s);
     }
 }
 
@@ -1331,7 +1476,7 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
     const int* const* d_ipiv = ws.iptrs.p;
     {
         ProfScope ps("lu_swap", s, 0.0);
-        rowswap_rhs_kernel<<<dim3((nrhs + 127) / 128, count), 128, 0, s>>>(n, d_ipiv, d_B, ldb, nrhs);
+        launch_row_permute(n, ldb, d_B, d_ipiv, count, 0, n, 0, nrhs, s);
         QPS_CUDA(cudaGetLastError());
     }
     auto& tasks = ws.h_gemm;
@@ -1418,7 +1563,7 @@ void zgemv_batched(int M, cplx alpha, cplx beta, const std::vector<GemvTask>& ta
     for (const auto& t : tasks)
         for (int q = 0; q < t.nseg; ++q) fl += 8.0 * M * t.n[q];
     ProfScope ps("zgemv", s, fl, fl * 2.0);
-    zgemv_kernel<<<dim3((M + 127) / 128, unsigned(tasks.size())), 128, 0, s>>>(M, alpha, beta, d_tasks.p);
+    zgemv_kernel<<<dim3((M + 31) / 32, unsigned(tasks.size())), 256, 0, s>>>(M, alpha, beta, d_tasks.p);
     QPS_CUDA(cudaGetLastError());
 }
 
