@@ -14,6 +14,17 @@ struct Dims {
     int mI = 0, mC = 0, pC = 0;  // interior Q rows, corner Q' rows / cols
     std::vector<int> N;
     bool padded = false;
+    int nsys = 1;  // independent systems (incidence angles) held at once
+    // per-system strides (complex elements); B blocks are alpha-free and shared
+    size_t nb2() const { return size_t(nb) * nb; }
+    size_t sA() const { return size_t(I) * nb2(); }
+    size_t sU() const { return size_t(I > 1 ? I - 1 : 1) * nb2(); }
+    size_t sQi() const { return size_t(I > 1 ? I - 1 : 1) * mI * P; }
+    size_t sRi() const { return size_t(I > 1 ? I - 1 : 1) * mI * 2 * nb; }
+    size_t sQc() const { return size_t(2) * mC * pC; }
+    size_t sRc() const { return size_t(2) * mC * nb; }
+    size_t sXi() const { return size_t(I > 1 ? I - 1 : 1) * P * 2 * nb; }
+    size_t sXc() const { return size_t(2) * pC * nb; }
 };
 
 // COD least-squares state for one family of equal-shape problems
@@ -46,6 +57,7 @@ struct BcrLevel {
     std::vector<int> idx;                 // original block index per active position
     std::vector<cplx*> D, L, U, F;        // per position (L/U may be null at the ends)
 };
+using BcrLevels = std::vector<BcrLevel>;  // one per system
 
 struct Ctx {
     int device = 0;
@@ -81,7 +93,7 @@ struct Ctx {
     CodSet cod_int, cod_c;
 
     // ---- block cyclic reduction ----
-    std::vector<BcrLevel> levels;
+    std::vector<BcrLevels> levels;  // [level][system]
     std::vector<DBuf<cplx>> lvlL, lvlU;
     DBuf<cplx> F, eta, dinv;
     DBuf<int> ipiv, singular;
@@ -91,7 +103,9 @@ struct Ctx {
 
     // ---- solution ----
     DBuf<cplx> csol, aUd, aDd;
-    std::vector<cplx> h_eta, h_c, h_aU, h_aD;
+    std::vector<cplx> h_eta, h_c, h_aU, h_aD;        // system 0
+    std::vector<cplx> h_aU_all, h_aD_all;            // nsys x (2K+1)
+    std::vector<double> lsq_all;                     // nsys x (I+1)
     bool have_sol = false;
     double flux_error = 0.0, max_lsq = 0.0;
 
@@ -114,10 +128,13 @@ void upload_geometry(Ctx& c);
 void setup_dims(Ctx& c, bool check_solvable = true);
 // one-shot fused single-angle fill of the assembled system (alpha recombination fused)
 void fill_system_fused(Ctx& c);
-// Schur complements in place on (A_diag, A_super, A_sub) or on the A' copies
+// Schur complements in place on (A_diag, A_super, A_sub) or on the A' copies,
+// for all dims.nsys systems (system a at base + a * stride)
 void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
-// block cyclic reduction on (Ad, Au, Al) with RHS f; result in c.eta
+// block cyclic reduction of all systems with RHS f (per system); eta in c.F
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
+// allocate the per-system buffers of the assembled system for dims.nsys systems
+void alloc_system(Ctx& c);
 void recover(Ctx& c);
 void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
                           int ldX, size_t Xstride, double* lsq_out);

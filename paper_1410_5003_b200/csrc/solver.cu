@@ -182,6 +182,21 @@ void three_shifts(PairTask& t, double d, cd alpha, cd scale) {
 
 }  // namespace
 
+void alloc_system(Ctx& c) {
+    const Dims& D = c.dims;
+    const size_t ns = size_t(D.nsys);
+    c.Adiag.ensure(ns * D.sA());
+    c.Asup.ensure(ns * D.sU());
+    c.Asub.ensure(ns * D.sU());
+    c.Bself.ensure(size_t(D.I) * D.nb * D.P);
+    c.Bbelow.ensure(size_t(D.I) * D.nb * D.P);
+    c.Qint.ensure(ns * D.sQi());
+    c.Rint.ensure(ns * D.sRi());
+    c.Qc.ensure(ns * D.sQc());
+    c.Rc.ensure(ns * D.sRc());
+    c.f.ensure(ns * D.nb);
+}
+
 void fill_system_fused(Ctx& c) {
     const Dims& D = c.dims;
     const HostGeometry& g = c.geo;
@@ -194,16 +209,7 @@ void fill_system_fused(Ctx& c) {
     cudaStream_t s = c.stream;
     const size_t nb2 = size_t(nb) * nb;
 
-    c.Adiag.ensure(I * nb2);
-    c.Asup.ensure(std::max(1, I - 1) * nb2);
-    c.Asub.ensure(std::max(1, I - 1) * nb2);
-    c.Bself.ensure(size_t(I) * nb * D.P);
-    c.Bbelow.ensure(size_t(I) * nb * D.P);
-    c.Qint.ensure(std::max(1, I - 1) * size_t(D.mI) * D.P);
-    c.Rint.ensure(std::max(1, I - 1) * size_t(D.mI) * 2 * nb);
-    c.Qc.ensure(2 * size_t(D.mC) * D.pC);
-    c.Rc.ensure(2 * size_t(D.mC) * nb);
-    c.f.ensure(nb);
+    alloc_system(c);
     if (D.padded) {
         c.Adiag.zero(s);
         c.Asup.zero(s);
@@ -567,67 +573,83 @@ void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int 
 
 void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     const Dims& D = c.dims;
-    const int I = D.I, nb = D.nb, P = D.P;
+    const int I = D.I, nb = D.nb, P = D.P, ns = D.nsys;
     if (P <= 0) fail(QPS_ERR_CONFIG, "periodization needs P > 0 proxy points per layer");
-    const size_t nb2 = size_t(nb) * nb;
-    c.Xint.ensure(std::max(1, I - 1) * size_t(P) * 2 * nb);
-    c.Xc.ensure(2 * size_t(D.pC) * nb);
-    c.lsq.assign(I + 1, 0.0);
-    // interior layers i = 1..I-1: X = qsolve(Q_i, [C_above_i C_self_i])
-    c.cod_int.ensure(I - 1, D.mI, P, 2 * nb);
-    qsolve_family(c, c.cod_int, c.Qint.p, c.Rint.p, D.mI, size_t(D.mI) * 2 * nb, c.Xint.p, P, size_t(P) * 2 * nb,
-                  c.lsq.data() + 1);
+    const size_t nb2 = D.nb2();
+    c.Xint.ensure(size_t(ns) * D.sXi());
+    c.Xc.ensure(size_t(ns) * D.sXc());
+    c.lsq_all.assign(size_t(ns) * (I + 1), 0.0);
+    // interior layers i = 1..I-1 of every system: X = qsolve(Q_i, [C_above_i C_self_i])
+    // (system a's interior layers are contiguous after system a-1's)
+    std::vector<double> li(size_t(ns) * (I > 1 ? I - 1 : 0));
+    if (I > 1) {
+        c.cod_int.ensure(ns * (I - 1), D.mI, P, 2 * nb);
+        qsolve_family(c, c.cod_int, c.Qint.p, c.Rint.p, D.mI, size_t(D.mI) * 2 * nb, c.Xint.p, P,
+                      size_t(P) * 2 * nb, li.data());
+    }
     // corners: X_first = qsolve(Q'_1, C'_1), X_last = qsolve(Q'_{I+1}, C'_{I+1})
-    c.cod_c.ensure(2, D.mC, D.pC, nb);
-    double lc[2];
-    qsolve_family(c, c.cod_c, c.Qc.p, c.Rc.p, D.mC, size_t(D.mC) * nb, c.Xc.p, D.pC, size_t(D.pC) * nb, lc);
-    c.lsq[0] = lc[0];
-    c.lsq[I] = lc[1];
-    // A' updates in one batched GEMM (periodize.hpp:88-91, 115, 119):
+    std::vector<double> lc(2 * size_t(ns));
+    c.cod_c.ensure(2 * ns, D.mC, D.pC, nb);
+    qsolve_family(c, c.cod_c, c.Qc.p, c.Rc.p, D.mC, size_t(D.mC) * nb, c.Xc.p, D.pC, size_t(D.pC) * nb, lc.data());
+    for (int a = 0; a < ns; ++a) {
+        double* l = c.lsq_all.data() + size_t(a) * (I + 1);
+        l[0] = lc[2 * a];
+        l[I] = lc[2 * a + 1];
+        for (int i = 1; i < I; ++i) l[i] = li[size_t(a) * (I - 1) + (i - 1)];
+    }
+    c.lsq.assign(c.lsq_all.begin(), c.lsq_all.begin() + (I + 1));
+    // A' updates of all systems in one batched GEMM (periodize.hpp:88-91, 115, 119):
     //   Ap_diag[j] -= B_self[j] X_self(j) + B_below[j] X_above(j+1)
     //   Ap_super[j] -= B_below[j] X_self(j+1),  Ap_sub[j] -= B_self[j+1] X_above(j+1)
-    auto xself = [&](int j, const cplx*& p, int& ld) {
-        if (j == 0) { p = c.Xc.p; ld = D.pC; }
-        else { p = c.Xint.p + size_t(j - 1) * P * 2 * nb + size_t(nb) * P; ld = P; }
-    };
-    auto xabove = [&](int i, const cplx*& p, int& ld) {
-        if (i == I) { p = c.Xc.p + size_t(D.pC) * nb; ld = D.pC; }
-        else { p = c.Xint.p + size_t(i - 1) * P * 2 * nb; ld = P; }
-    };
     std::vector<GemmTask> tasks;
-    for (int j = 0; j < I; ++j) {
-        GemmTask t{};
-        t.nseg = 2;
-        t.A[0] = c.Bself.p + size_t(j) * nb * P;
-        t.lda[0] = nb;
-        xself(j, t.B[0], t.ldb[0]);
-        t.K[0] = P;
-        t.A[1] = c.Bbelow.p + size_t(j) * nb * P;
-        t.lda[1] = nb;
-        xabove(j + 1, t.B[1], t.ldb[1]);
-        t.K[1] = P;
-        t.C = Ad + j * nb2;
-        t.ldc = nb;
-        tasks.push_back(t);
-        if (j + 1 < I) {
-            GemmTask u{};
-            u.nseg = 1;
-            u.A[0] = c.Bbelow.p + size_t(j) * nb * P;
-            u.lda[0] = nb;
-            xself(j + 1, u.B[0], u.ldb[0]);
-            u.K[0] = P;
-            u.C = Au + j * nb2;
-            u.ldc = nb;
-            tasks.push_back(u);
-            GemmTask v{};
-            v.nseg = 1;
-            v.A[0] = c.Bself.p + size_t(j + 1) * nb * P;
-            v.lda[0] = nb;
-            xabove(j + 1, v.B[0], v.ldb[0]);
-            v.K[0] = P;
-            v.C = Al + j * nb2;
-            v.ldc = nb;
-            tasks.push_back(v);
+    for (int a = 0; a < ns; ++a) {
+        const cplx* Xi = c.Xint.p + size_t(a) * D.sXi();
+        const cplx* Xc = c.Xc.p + size_t(a) * D.sXc();
+        auto xself = [&](int j, const cplx*& p, int& ld) {
+            if (j == 0) { p = Xc; ld = D.pC; }
+            else { p = Xi + size_t(j - 1) * P * 2 * nb + size_t(nb) * P; ld = P; }
+        };
+        auto xabove = [&](int i, const cplx*& p, int& ld) {
+            if (i == I) { p = Xc + size_t(D.pC) * nb; ld = D.pC; }
+            else { p = Xi + size_t(i - 1) * P * 2 * nb; ld = P; }
+        };
+        cplx* Ada = Ad + size_t(a) * D.sA();
+        cplx* Aua = Au + size_t(a) * D.sU();
+        cplx* Ala = Al + size_t(a) * D.sU();
+        for (int j = 0; j < I; ++j) {
+            GemmTask t{};
+            t.nseg = 2;
+            t.A[0] = c.Bself.p + size_t(j) * nb * P;
+            t.lda[0] = nb;
+            xself(j, t.B[0], t.ldb[0]);
+            t.K[0] = P;
+            t.A[1] = c.Bbelow.p + size_t(j) * nb * P;
+            t.lda[1] = nb;
+            xabove(j + 1, t.B[1], t.ldb[1]);
+            t.K[1] = P;
+            t.C = Ada + j * nb2;
+            t.ldc = nb;
+            tasks.push_back(t);
+            if (j + 1 < I) {
+                GemmTask u{};
+                u.nseg = 1;
+                u.A[0] = c.Bbelow.p + size_t(j) * nb * P;
+                u.lda[0] = nb;
+                xself(j + 1, u.B[0], u.ldb[0]);
+                u.K[0] = P;
+                u.C = Aua + j * nb2;
+                u.ldc = nb;
+                tasks.push_back(u);
+                GemmTask v{};
+                v.nseg = 1;
+                v.A[0] = c.Bself.p + size_t(j + 1) * nb * P;
+                v.lda[0] = nb;
+                xabove(j + 1, v.B[0], v.ldb[0]);
+                v.K[0] = P;
+                v.C = Ala + j * nb2;
+                v.ldc = nb;
+                tasks.push_back(v);
+            }
         }
     }
     zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks);
@@ -637,164 +659,154 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
 }
 
 // ---------------------------------------------------------------------------
-// Block cyclic reduction
+// Block cyclic reduction (all systems of the batch advance level by level)
 // ---------------------------------------------------------------------------
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     const Dims& D = c.dims;
-    const int I = D.I, nb = D.nb;
-    const size_t nb2 = size_t(nb) * nb;
+    const int I = D.I, nb = D.nb, ns = D.nsys;
+    const size_t nb2 = D.nb2();
     cudaStream_t s = c.stream;
-    c.F.ensure(size_t(I) * nb);
+    c.F.ensure(size_t(ns) * I * nb);
     c.F.zero(s);
-    QPS_CUDA(cudaMemcpyAsync(c.F.p, c.f.p, sizeof(cplx) * nb, cudaMemcpyDeviceToDevice, s));
-    c.ipiv.ensure(size_t(I) * nb);
+    for (int a = 0; a < ns; ++a)
+        QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
+                                 cudaMemcpyDeviceToDevice, s));
+    c.ipiv.ensure(size_t(ns) * I * nb);
     const size_t dsz = lu_dinv_elems(nb);
-    c.dinv.ensure(size_t(I) * dsz);
-    c.singular.ensure(I);
-    c.singular.zero(s);
+    c.dinv.ensure(size_t(ns) * I * dsz);
     c.levels.clear();
-    BcrLevel L0;
-    for (int j = 0; j < I; ++j) {
-        L0.idx.push_back(j);
-        L0.D.push_back(Ad + j * nb2);
-        L0.L.push_back(j >= 1 ? Al + (j - 1) * nb2 : nullptr);
-        L0.U.push_back(j + 1 < I ? Au + j * nb2 : nullptr);
-        L0.F.push_back(c.F.p + size_t(j) * nb);
+    BcrLevels L0(ns);
+    for (int a = 0; a < ns; ++a) {
+        cplx* Ada = Ad + size_t(a) * D.sA();
+        cplx* Aua = Au + size_t(a) * D.sU();
+        cplx* Ala = Al + size_t(a) * D.sU();
+        for (int j = 0; j < I; ++j) {
+            L0[a].idx.push_back(j);
+            L0[a].D.push_back(Ada + j * nb2);
+            L0[a].L.push_back(j >= 1 ? Ala + (j - 1) * nb2 : nullptr);
+            L0[a].U.push_back(j + 1 < I ? Aua + j * nb2 : nullptr);
+            L0[a].F.push_back(c.F.p + (size_t(a) * I + j) * nb);
+        }
     }
     c.levels.push_back(L0);
-    // number of levels and buffers for the reduced couplings
     {
         int n = I, lv = 0;
         while (n > 1) { n = (n + 1) / 2; ++lv; }
         c.lvlL.resize(std::max(lv, 1));
         c.lvlU.resize(std::max(lv, 1));
     }
-    auto ipiv_of = [&](int j) { return c.ipiv.p + size_t(j) * nb; };
-    auto dinv_of = [&](int j) { return c.dinv.p + size_t(j) * dsz; };
-    auto check_singular = [&]() {
-        std::vector<int> sg(I);
-        QPS_D2H(sg.data(), c.singular.p, sizeof(int) * I, s);
+    auto ipiv_of = [&](int a, int j) { return c.ipiv.p + (size_t(a) * I + j) * nb; };
+    auto dinv_of = [&](int a, int j) { return c.dinv.p + (size_t(a) * I + j) * dsz; };
+    auto singular_error = [&](int j) {
+        throw Error(QPS_ERR_SOLVER, "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1),
+                    j + 1);
+    };
+    DBuf<int> flag;
+    auto factor = [&](const std::vector<cplx*>& fa, const std::vector<int*>& fp, const std::vector<cplx*>& fd,
+                      const std::vector<int>& orig) {
+        flag.ensure(fa.size());
+        flag.zero(s);
+        lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
+        std::vector<int> hf(fa.size());
+        QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
         QPS_CUDA(cudaStreamSynchronize(s));
-        for (int j = 0; j < I; ++j)
-            if (sg[j])
-                throw Error(QPS_ERR_SOLVER,
-                            "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1),
-                            j + 1);
+        int worst = -1;
+        for (size_t b = 0; b < hf.size(); ++b)
+            if (hf[b] && (worst < 0 || orig[b] < worst)) worst = orig[b];
+        if (worst >= 0) singular_error(worst);
     };
     int lvl = 0;
-    while (c.levels[lvl].idx.size() > 1) {
-        const BcrLevel& cur = c.levels[lvl];
-        const int sz = int(cur.idx.size());
-        // 1. factor the odd positions
+    while (c.levels[lvl][0].idx.size() > 1) {
+        const BcrLevels& cur = c.levels[lvl];
+        const int sz = int(cur[0].idx.size());
+        // 1. factor the odd positions of every system
         std::vector<cplx*> fa, fd;
         std::vector<int*> fp;
-        for (int o = 1; o < sz; o += 2) {
-            fa.push_back(cur.D[o]);
-            fp.push_back(ipiv_of(cur.idx[o]));
-            fd.push_back(dinv_of(cur.idx[o]));
-        }
-        // singular flags indexed by original block: use a per-level scratch via the pointer list
-        {
-            // lu_factor writes singular[b] for batch position b; remap afterwards
-            DBuf<int> flag;
-            flag.ensure(fa.size());
-            flag.zero(s);
-            lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
-            std::vector<int> hf(fa.size());
-            QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
-            QPS_CUDA(cudaStreamSynchronize(s));
-            for (size_t b = 0; b < hf.size(); ++b)
-                if (hf[b]) {
-                    const int j = cur.idx[1 + 2 * b];
-                    throw Error(QPS_ERR_SOLVER,
-                                "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1),
-                                j + 1);
-                }
-        }
+        std::vector<int> orig;
+        for (int a = 0; a < ns; ++a)
+            for (int o = 1; o < sz; o += 2) {
+                fa.push_back(cur[a].D[o]);
+                fp.push_back(ipiv_of(a, cur[a].idx[o]));
+                fd.push_back(dinv_of(a, cur[a].idx[o]));
+                orig.push_back(cur[a].idx[o]);
+            }
+        factor(fa, fp, fd, orig);
         // 2. Y = D^{-1} [L | U] and y_f = D^{-1} f for the odd positions (in place)
         {
             std::vector<cplx*> ma, mb, md, va, vb, vd;
             std::vector<int*> mp, vp;
-            for (int o = 1; o < sz; o += 2) {
-                const int j = cur.idx[o];
-                ma.push_back(cur.D[o]); mp.push_back(ipiv_of(j)); md.push_back(dinv_of(j)); mb.push_back(cur.L[o]);
-                if (cur.U[o]) { ma.push_back(cur.D[o]); mp.push_back(ipiv_of(j)); md.push_back(dinv_of(j)); mb.push_back(cur.U[o]); }
-                va.push_back(cur.D[o]); vp.push_back(ipiv_of(j)); vd.push_back(dinv_of(j)); vb.push_back(cur.F[o]);
-            }
+            for (int a = 0; a < ns; ++a)
+                for (int o = 1; o < sz; o += 2) {
+                    const int j = cur[a].idx[o];
+                    ma.push_back(cur[a].D[o]); mp.push_back(ipiv_of(a, j)); md.push_back(dinv_of(a, j)); mb.push_back(cur[a].L[o]);
+                    if (cur[a].U[o]) { ma.push_back(cur[a].D[o]); mp.push_back(ipiv_of(a, j)); md.push_back(dinv_of(a, j)); mb.push_back(cur[a].U[o]); }
+                    va.push_back(cur[a].D[o]); vp.push_back(ipiv_of(a, j)); vd.push_back(dinv_of(a, j)); vb.push_back(cur[a].F[o]);
+                }
             lu_solve_batched(nb, nb, ma, mp, md, mb, nb, nb, s, c.ws);
             lu_solve_batched(nb, nb, va, vp, vd, vb, nb, 1, s, c.ws);
         }
         // 3. updates of the even positions
         const int nsz = (sz + 1) / 2;
-        BcrLevel nxt;
+        BcrLevels nxt(ns);
         DBuf<cplx>& LB = c.lvlL[lvl];
         DBuf<cplx>& UB = c.lvlU[lvl];
-        LB.ensure(size_t(nsz) * nb2);
-        UB.ensure(size_t(nsz) * nb2);
-        std::vector<GemmTask> tasks;
-        std::vector<GemvTask> vtasks;
-        for (int e = 0; e < sz; e += 2) {
-            const int q = e / 2;
-            const bool hm = e >= 1, hp = e + 1 < sz;
-            nxt.idx.push_back(cur.idx[e]);
-            nxt.D.push_back(cur.D[e]);
-            nxt.F.push_back(cur.F[e]);
-            GemmTask t{};
-            t.nseg = 0;
-            GemvTask v{};
-            v.nseg = 0;
-            if (hm) {  // D_e -= L_e Y_U(e-1);  f_e -= L_e y_f(e-1)
-                if (cur.U[e - 1]) {
-                    t.A[t.nseg] = cur.L[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cur.U[e - 1]; t.ldb[t.nseg] = nb;
-                    t.K[t.nseg] = nb; ++t.nseg;
-                }
-                v.A[v.nseg] = cur.L[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[e - 1]; v.n[v.nseg] = nb; ++v.nseg;
-            }
-            if (hp) {  // D_e -= U_e Y_L(e+1);  f_e -= U_e y_f(e+1)
-                t.A[t.nseg] = cur.U[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cur.L[e + 1]; t.ldb[t.nseg] = nb;
-                t.K[t.nseg] = nb; ++t.nseg;
-                v.A[v.nseg] = cur.U[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[e + 1]; v.n[v.nseg] = nb; ++v.nseg;
-            }
-            if (t.nseg) {
-                t.C = cur.D[e];
-                t.ldc = nb;
-                tasks.push_back(t);
-            }
-            if (v.nseg) {
-                v.y = cur.F[e];
-                vtasks.push_back(v);
-            }
-            // new couplings: L'_e = -L_e Y_L(e-1) (to position e-2), U'_e = -U_e Y_U(e+1) (to e+2)
-            cplx* nl = nullptr;
-            cplx* nu = nullptr;
-            if (hm && e - 2 >= 0) {
-                nl = LB.p + size_t(q) * nb2;
-                GemmTask u{};
-                u.nseg = 1;
-                u.A[0] = cur.L[e]; u.lda[0] = nb; u.B[0] = cur.L[e - 1]; u.ldb[0] = nb; u.K[0] = nb;
-                u.C = nl;
-                u.ldc = nb;
-                tasks.push_back(u);
-            }
-            if (hp && e + 2 < sz) {
-                nu = UB.p + size_t(q) * nb2;
-                GemmTask u{};
-                u.nseg = 1;
-                u.A[0] = cur.U[e]; u.lda[0] = nb; u.B[0] = cur.U[e + 1]; u.ldb[0] = nb; u.K[0] = nb;
-                u.C = nu;
-                u.ldc = nb;
-                tasks.push_back(u);
-            }
-            nxt.L.push_back(nl);
-            nxt.U.push_back(nu);
-        }
-        // D/f updates use beta = 1; new couplings overwrite (beta = 0): split the batch
+        LB.ensure(size_t(ns) * nsz * nb2);
+        UB.ensure(size_t(ns) * nsz * nb2);
         std::vector<GemmTask> upd, fresh;
-        for (const auto& t : tasks) {
-            bool is_new = false;
-            for (int e = 0; e < nsz; ++e)
-                if (t.C == nxt.L[e] || t.C == nxt.U[e]) is_new = true;
-            (is_new ? fresh : upd).push_back(t);
+        std::vector<GemvTask> vtasks;
+        for (int a = 0; a < ns; ++a) {
+            const BcrLevel& cu = cur[a];
+            for (int e = 0; e < sz; e += 2) {
+                const int q = e / 2;
+                const bool hm = e >= 1, hp = e + 1 < sz;
+                nxt[a].idx.push_back(cu.idx[e]);
+                nxt[a].D.push_back(cu.D[e]);
+                nxt[a].F.push_back(cu.F[e]);
+                GemmTask t{};
+                GemvTask v{};
+                if (hm) {  // D_e -= L_e Y_U(e-1);  f_e -= L_e y_f(e-1)
+                    t.A[t.nseg] = cu.L[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cu.U[e - 1]; t.ldb[t.nseg] = nb;
+                    t.K[t.nseg] = nb; ++t.nseg;
+                    v.A[v.nseg] = cu.L[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cu.F[e - 1]; v.n[v.nseg] = nb; ++v.nseg;
+                }
+                if (hp) {  // D_e -= U_e Y_L(e+1);  f_e -= U_e y_f(e+1)
+                    t.A[t.nseg] = cu.U[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cu.L[e + 1]; t.ldb[t.nseg] = nb;
+                    t.K[t.nseg] = nb; ++t.nseg;
+                    v.A[v.nseg] = cu.U[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cu.F[e + 1]; v.n[v.nseg] = nb; ++v.nseg;
+                }
+                if (t.nseg) {
+                    t.C = cu.D[e];
+                    t.ldc = nb;
+                    upd.push_back(t);
+                }
+                if (v.nseg) {
+                    v.y = cu.F[e];
+                    vtasks.push_back(v);
+                }
+                // new couplings: L'_e = -L_e Y_L(e-1) (to e-2), U'_e = -U_e Y_U(e+1) (to e+2)
+                cplx* nl = nullptr;
+                cplx* nu = nullptr;
+                if (hm && e - 2 >= 0) {
+                    nl = LB.p + (size_t(a) * nsz + q) * nb2;
+                    GemmTask u{};
+                    u.nseg = 1;
+                    u.A[0] = cu.L[e]; u.lda[0] = nb; u.B[0] = cu.L[e - 1]; u.ldb[0] = nb; u.K[0] = nb;
+                    u.C = nl;
+                    u.ldc = nb;
+                    fresh.push_back(u);
+                }
+                if (hp && e + 2 < sz) {
+                    nu = UB.p + (size_t(a) * nsz + q) * nb2;
+                    GemmTask u{};
+                    u.nseg = 1;
+                    u.A[0] = cu.U[e]; u.lda[0] = nb; u.B[0] = cu.U[e + 1]; u.ldb[0] = nb; u.K[0] = nb;
+                    u.C = nu;
+                    u.ldc = nb;
+                    fresh.push_back(u);
+                }
+                nxt[a].L.push_back(nl);
+                nxt[a].U.push_back(nu);
+            }
         }
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, upd, s, c.ws.gemm_tasks);
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{0, 0}, fresh, s, c.ws.gemm_tasks);
@@ -802,83 +814,88 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         c.levels.push_back(nxt);
         ++lvl;
     }
-    // final single block
+    // final single block of every system
     {
-        const BcrLevel& last = c.levels[lvl];
-        std::vector<cplx*> fa{last.D[0]}, fd{dinv_of(last.idx[0])};
-        std::vector<int*> fp{ipiv_of(last.idx[0])};
-        DBuf<int> flag;
-        flag.ensure(1);
-        flag.zero(s);
-        lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
-        int hf = 0;
-        QPS_D2H(&hf, flag.p, sizeof(int), s);
-        QPS_CUDA(cudaStreamSynchronize(s));
-        if (hf) {
-            const int j = last.idx[0];
-            throw Error(QPS_ERR_SOLVER,
-                        "singular diagonal factor (resonant parameters?) at layer " + std::to_string(j + 1), j + 1);
+        const BcrLevels& last = c.levels[lvl];
+        std::vector<cplx*> fa, fd, vb;
+        std::vector<int*> fp;
+        std::vector<int> orig;
+        for (int a = 0; a < ns; ++a) {
+            fa.push_back(last[a].D[0]);
+            fd.push_back(dinv_of(a, last[a].idx[0]));
+            fp.push_back(ipiv_of(a, last[a].idx[0]));
+            vb.push_back(last[a].F[0]);
+            orig.push_back(last[a].idx[0]);
         }
-        std::vector<cplx*> vb{last.F[0]};
+        factor(fa, fp, fd, orig);
         lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
     }
-    (void)check_singular;
-    // back substitution: eta_o = y_f(o) - Y_L(o) eta_{o-1} - Y_U(o) eta_{o+1}, level by level upward.
-    // F of every block ends up holding eta.
+    // back substitution: eta_o = y_f(o) - Y_L(o) eta_{o-1} - Y_U(o) eta_{o+1}; F ends up holding eta
     for (int l = lvl - 1; l >= 0; --l) {
-        const BcrLevel& cur = c.levels[l];
-        const int sz = int(cur.idx.size());
+        const BcrLevels& cur = c.levels[l];
+        const int sz = int(cur[0].idx.size());
         std::vector<GemvTask> vt;
-        for (int o = 1; o < sz; o += 2) {
-            GemvTask v{};
-            v.nseg = 0;
-            v.A[v.nseg] = cur.L[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[o - 1]; v.n[v.nseg] = nb; ++v.nseg;
-            if (o + 1 < sz) {
-                v.A[v.nseg] = cur.U[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur.F[o + 1]; v.n[v.nseg] = nb; ++v.nseg;
+        for (int a = 0; a < ns; ++a)
+            for (int o = 1; o < sz; o += 2) {
+                GemvTask v{};
+                v.A[v.nseg] = cur[a].L[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur[a].F[o - 1]; v.n[v.nseg] = nb; ++v.nseg;
+                if (o + 1 < sz) {
+                    v.A[v.nseg] = cur[a].U[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur[a].F[o + 1]; v.n[v.nseg] = nb;
+                    ++v.nseg;
+                }
+                v.y = cur[a].F[o];
+                vt.push_back(v);
             }
-            v.y = cur.F[o];
-            vt.push_back(v);
-        }
         zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vt, s, c.ws.gemv_tasks);
     }
     c.eta_valid = true;
 }
 
 // ---------------------------------------------------------------------------
-// recover_aux (tridiag.hpp:50-66)
+// recover_aux (tridiag.hpp:50-66), every system of the batch
 // ---------------------------------------------------------------------------
 void recover(Ctx& c) {
     const Dims& D = c.dims;
-    const int I = D.I, nb = D.nb, P = D.P;
+    const int I = D.I, nb = D.nb, P = D.P, ns = D.nsys;
     cudaStream_t s = c.stream;
-    c.csol.ensure(size_t(I + 1) * P);
-    c.aUd.ensure(D.pC);
-    c.aDd.ensure(D.pC);
+    c.csol.ensure(size_t(ns) * (I + 1) * P);
+    c.aUd.ensure(size_t(ns) * D.pC);
+    c.aDd.ensure(size_t(ns) * D.pC);
     // corners: x_first = -X_first eta_0, x_last = -X_last eta_{I-1}
-    std::vector<GemvTask> vt(2);
-    vt[0] = GemvTask{};
-    vt[0].nseg = 1; vt[0].A[0] = c.Xc.p; vt[0].lda[0] = D.pC; vt[0].x[0] = c.F.p; vt[0].n[0] = nb; vt[0].y = c.aUd.p;
-    vt[1] = GemvTask{};
-    vt[1].nseg = 1; vt[1].A[0] = c.Xc.p + size_t(D.pC) * nb; vt[1].lda[0] = D.pC;
-    vt[1].x[0] = c.F.p + size_t(I - 1) * nb; vt[1].n[0] = nb; vt[1].y = c.aDd.p;
+    std::vector<GemvTask> vt;
+    for (int a = 0; a < ns; ++a) {
+        const cplx* Xc = c.Xc.p + size_t(a) * D.sXc();
+        const cplx* Fa = c.F.p + size_t(a) * I * nb;
+        GemvTask u{};
+        u.nseg = 1; u.A[0] = Xc; u.lda[0] = D.pC; u.x[0] = Fa; u.n[0] = nb; u.y = c.aUd.p + size_t(a) * D.pC;
+        vt.push_back(u);
+        GemvTask w{};
+        w.nseg = 1; w.A[0] = Xc + size_t(D.pC) * nb; w.lda[0] = D.pC; w.x[0] = Fa + size_t(I - 1) * nb; w.n[0] = nb;
+        w.y = c.aDd.p + size_t(a) * D.pC;
+        vt.push_back(w);
+    }
     zgemv_batched(D.pC, cplx{-1, 0}, cplx{0, 0}, vt, s, c.ws.gemv_tasks);
     std::vector<GemvTask> it;
-    for (int i = 1; i <= I - 1; ++i) {
-        GemvTask v{};
-        v.nseg = 2;
-        const cplx* X = c.Xint.p + size_t(i - 1) * P * 2 * nb;
-        v.A[0] = X; v.lda[0] = P; v.x[0] = c.F.p + size_t(i - 1) * nb; v.n[0] = nb;
-        v.A[1] = X + size_t(nb) * P; v.lda[1] = P; v.x[1] = c.F.p + size_t(i) * nb; v.n[1] = nb;
-        v.y = c.csol.p + size_t(i) * P;
-        it.push_back(v);
+    for (int a = 0; a < ns; ++a) {
+        const cplx* Xi = c.Xint.p + size_t(a) * D.sXi();
+        const cplx* Fa = c.F.p + size_t(a) * I * nb;
+        for (int i = 1; i <= I - 1; ++i) {
+            GemvTask v{};
+            v.nseg = 2;
+            const cplx* X = Xi + size_t(i - 1) * P * 2 * nb;
+            v.A[0] = X; v.lda[0] = P; v.x[0] = Fa + size_t(i - 1) * nb; v.n[0] = nb;
+            v.A[1] = X + size_t(nb) * P; v.lda[1] = P; v.x[1] = Fa + size_t(i) * nb; v.n[1] = nb;
+            v.y = c.csol.p + (size_t(a) * (I + 1) + i) * P;
+            it.push_back(v);
+        }
     }
     zgemv_batched(P, cplx{-1, 0}, cplx{0, 0}, it, s, c.ws.gemv_tasks);
-    // download
-    std::vector<cplx> Fh(size_t(I) * nb), ch(size_t(I + 1) * P), xf(D.pC), xl(D.pC);
+    // download: full solution of system 0, Bragg amplitudes of every system
+    std::vector<cplx> Fh(size_t(I) * nb), ch(size_t(I + 1) * P), xf(size_t(ns) * D.pC), xl(size_t(ns) * D.pC);
     QPS_D2H(Fh.data(), c.F.p, sizeof(cplx) * Fh.size(), s);
     QPS_D2H(ch.data(), c.csol.p, sizeof(cplx) * ch.size(), s);
-    QPS_D2H(xf.data(), c.aUd.p, sizeof(cplx) * D.pC, s);
-    QPS_D2H(xl.data(), c.aDd.p, sizeof(cplx) * D.pC, s);
+    QPS_D2H(xf.data(), c.aUd.p, sizeof(cplx) * xf.size(), s);
+    QPS_D2H(xl.data(), c.aDd.p, sizeof(cplx) * xl.size(), s);
     QPS_CUDA(cudaStreamSynchronize(s));
     c.h_eta.clear();
     for (int j = 0; j < I; ++j)
@@ -888,8 +905,14 @@ void recover(Ctx& c) {
         ch[size_t(I) * P + p] = xl[p];
     }
     c.h_c = ch;
-    c.h_aU.assign(xf.begin() + P, xf.end());
-    c.h_aD.assign(xl.begin() + P, xl.end());
+    c.h_aU.assign(xf.begin() + P, xf.begin() + D.pC);
+    c.h_aD.assign(xl.begin() + P, xl.begin() + D.pC);
+    c.h_aU_all.clear();
+    c.h_aD_all.clear();
+    for (int a = 0; a < ns; ++a) {
+        c.h_aU_all.insert(c.h_aU_all.end(), xf.begin() + size_t(a) * D.pC + P, xf.begin() + size_t(a + 1) * D.pC);
+        c.h_aD_all.insert(c.h_aD_all.end(), xl.begin() + size_t(a) * D.pC + P, xl.begin() + size_t(a + 1) * D.pC);
+    }
     c.have_sol = true;
     double R, T, fe;
     host_spectrum(c, &R, &T, &fe, nullptr, nullptr, nullptr, nullptr, nullptr);
