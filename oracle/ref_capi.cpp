@@ -358,15 +358,18 @@ int qps_sweep(qps_ctx* c, int n, const double* theta, int K, int mode, double* R
         const int nrb = 2 * K + 1;
         const auto t0 = clk::now();
         std::optional<ShiftBlockCache> cache;
-        if (mode == 0) {
-            cache = precompute_shift_blocks(make_problem(c->stack, c->geom, omega, theta[0], K), c->num);
-            c->fill_evals = cache->fill_evals;
-        }
+        const double nan = std::nan("");
         for (int a = 0; a < n; ++a) {
-            ScatteringProblem p = make_problem(c->stack, c->geom, omega, theta[a], K);
+            if (R) R[a] = nan;
+            if (T) T[a] = nan;
+            if (fe) fe[a] = nan;
             qps_ctx tmp;
             const int st = guarded(&tmp, [&] {
-                if (mode != 0) cache = precompute_shift_blocks(p, c->num);
+                ScatteringProblem p = make_problem(c->stack, c->geom, omega, theta[a], K);
+                if (mode != 0 || !cache) {  // mode 0: the first valid angle fills the cache
+                    cache = precompute_shift_blocks(p, c->num);
+                    c->fill_evals = cache->fill_evals;
+                }
                 const BlockSystem sys = assemble_system(p, *cache, c->num);
                 Solution s = solve_periodized(sys);
                 const SpectrumRow row = reflection_transmission(s, p);

@@ -161,6 +161,7 @@ int qps_build_geometry(qps_ctx* h, double d, int n_layers, const double* eps, co
     return guarded(h, [&](Ctx& c) {
         need(num != nullptr && eps != nullptr, "numerics and epsilon required");
         c.have_geom = c.have_prob = false;
+        c.cache_valid = false;
         c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
         StackDesc st;
         st.d = d;
@@ -191,6 +192,7 @@ int qps_make_problem(qps_ctx* h, double omega, double theta, int K) {
         need(c.have_geom, "build_geometry first");
         c.prob = make_problem(c.stack, c.geo, omega, theta, K);
         c.have_prob = true;
+        if (c.cache_valid && c.cache_k != c.prob.k) c.cache_valid = false;  // the cache depends on omega only
         c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
     });
 }
@@ -230,9 +232,14 @@ int qps_interface_nodes(const qps_ctx* h, int j, double* nodes, double* normals,
 
 int qps_precompute_shift_blocks(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
-        prepare(c, false);
-        c.ref_evals = reference_fill_evals(c.geo);
+        prepare(c, false);  // memory budget guard, assembly.hpp:216-223
         c.sys_valid = c.ps_valid = c.eta_valid = c.have_sol = false;
+        if (c.host_only) {
+            c.ref_evals = reference_fill_evals(c.geo);
+            return;
+        }
+        Timer t(c, &c.times.fill_ms);
+        cache_fill(c);
     });
 }
 
@@ -240,7 +247,14 @@ int qps_assemble_system(qps_ctx* h) {
     return guarded(h, [&](Ctx& c) {
         need_device(c);
         prepare(c);
-        run_fill(c);
+        if (!(c.cache_valid && c.cache_k == c.prob.k)) {
+            Timer t(c, &c.times.fill_ms);
+            cache_fill(c);
+        }
+        {
+            Timer t(c, &c.times.assemble_ms);
+            assemble_from_cache(c, {c.prob});
+        }
         c.ps_separate = true;
     });
 }
@@ -388,35 +402,9 @@ int qps_sweep(qps_ctx* h, int n, const double* theta, int K, int mode, double* R
         need_device(c);
         need(c.have_prob, "make_problem first (sets omega)");
         need(K > 0, "sweep needs a fixed K > 0");
-        (void)mode;
-        const double omega = c.prob.omega;
-        const int nrb = 2 * K + 1;
-        for (int a = 0; a < n; ++a) {
-            c.prob = make_problem(c.stack, c.geo, omega, theta[a], K);
-            c.have_prob = true;
-            qps_ctx tmp;
-            int st = QPS_OK;
-            try {
-                prepare(c);
-                c.ps_separate = false;
-                fill_system_fused(c);
-                schur(c, c.Adiag.p, c.Asup.p, c.Asub.p);
-                bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p);
-                recover(c);
-                double r, t, f;
-                host_spectrum(c, &r, &t, &f, nullptr, nullptr, nullptr, nullptr, nullptr);
-                if (R) R[a] = r;
-                if (T) T[a] = t;
-                if (fe) fe[a] = f;
-                for (int i = 0; i < nrb; ++i) {
-                    if (aU) aU[size_t(a) * nrb + i] = qps_cplx{c.h_aU[i].re, c.h_aU[i].im};
-                    if (aD) aD[size_t(a) * nrb + i] = qps_cplx{c.h_aD[i].re, c.h_aD[i].im};
-                }
-            } catch (const Error& e) {
-                st = e.status;
-            }
-            if (status) status[a] = st;
-        }
+        need(n >= 0 && (n == 0 || theta != nullptr), "sweep: bad angle list");
+        need(mode == 0 || mode == 1, "sweep: mode is 0 (accelerated) or 1 (independent)");
+        run_sweep(c, n, theta, K, mode, R, T, fe, reinterpret_cast<cplx*>(aU), reinterpret_cast<cplx*>(aD), status);
     });
 }
 

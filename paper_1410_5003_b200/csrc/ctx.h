@@ -1,6 +1,7 @@
 // Solver context: everything one qps_ctx owns on host and device.
 #pragma once
 
+#include <array>
 #include <string>
 #include <vector>
 
@@ -52,6 +53,39 @@ struct CodSet {
     }
 };
 
+// Offsets (complex elements) of the alpha-free pieces inside Ctx::cache_pool:
+// ShiftBlockCache (assembly.hpp:115-155).  Four-plane pieces hold the kinds
+// D, S, T, D* as consecutive rows x cols planes.
+struct CacheLayout {
+    std::vector<std::array<size_t, 2>> self_c, band, nbr_m, nbr_p;  // [j][up k_j / down k_{j+1}]
+    std::vector<std::array<size_t, 3>> cup, cdn;                     // [j][l + 1]
+    std::vector<size_t> Csp, Csm, Cap, Cam, Qp, Qm;                  // [i], walls
+    size_t ZU[3] = {0, 0, 0}, ZD[3] = {0, 0, 0}, VU = 0, VD = 0;
+    size_t total = 0;
+};
+
+// out_a = sum_t coef(a, t) * piece_t over the planes of one cache piece group
+struct CombineTask {
+    int nplanes;  // 4 ([D S; T D*] stacking) or 1 (proxy block)
+    int rows, cols;
+    int npiece;
+    int ident;
+    size_t piece[6];
+    int coef[6];
+    cplx* out;
+    size_t ostride;
+    int ld, row_off, col_off;
+};
+
+// alpha^{+-1}-weighted out-of-period band of one smooth self block
+struct BandTask {
+    int N;
+    size_t up, dn;
+    cplx* out;
+    size_t ostride;
+    int ld;
+};
+
 // One block-tridiagonal system stored as pointer lists (block cyclic reduction)
 struct BcrLevel {
     std::vector<int> idx;                 // original block index per active position
@@ -80,6 +114,16 @@ struct Ctx {
     std::vector<int> seg_first;
     DBuf<double> fourier;
     DBuf<int> d_err;
+
+    // ---- alpha-free shift-block cache (precompute_shift_blocks) ----
+    CacheLayout cache;
+    DBuf<cplx> cache_pool, coef_buf;
+    std::vector<double> cache_k;  // wavenumbers the cache was filled for
+    bool cache_valid = false;
+    DBuf<CombineTask> d_comb;
+    DBuf<int2> d_ctiles;
+    DBuf<BandTask> d_band;
+    DBuf<int> d_nodes2;
 
     // ---- assembled system (BlockSystem, assembly.hpp:293-315) ----
     Dims dims;
@@ -140,6 +184,20 @@ void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int 
                           int ldX, size_t Xstride, double* lsq_out);
 void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,
                    int* pd);
+// flux_error + reflection_transmission of one angle's Bragg amplitudes
+void spectrum_of(const Problem& p, double d, const cplx* aU, const cplx* aD, double* R, double* T, double* fe,
+                 double* kappa, cplx* kU, cplx* kD, int* pu, int* pd);
+// W blocks of Q' and the RHS f of every system of the batch (host, O(M K) + O(N))
+void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs);
+// identity on the unused diagonal of padded A_jj blocks, every system
+void pad_identity(Ctx& c);
+// precompute_shift_blocks (assembly.hpp:212-287) into c.cache_pool
+void cache_fill(Ctx& c);
+// assemble_system (assembly.hpp:462-483) for dims.nsys angles from the cache
+void assemble_from_cache(Ctx& c, const std::vector<Problem>& probs);
+// multi-angle sweep; mode 0 accelerated (cache once, angles batched), 1 independent
+void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe, cplx* aU,
+               cplx* aD, int* status);
 
 struct Timer {
     Ctx& c;

@@ -406,46 +406,8 @@ void fill_system_fused(Ctx& c) {
     launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.d_err.p, s, c.d_alpert);
     launch_proxy_fill(xt, pool, c.d_err.p, s, c.d_proxy, c.d_tiles);
 
-    // W blocks (assembly.hpp:414-427) and f (assembly.hpp:431-441) on the host: O(M K) + O(N)
-    {
-        const int M = D.M, K = D.K, nrb = D.nrb;
-        std::vector<cplx> WU(size_t(2 * M) * nrb), WD(size_t(2 * M) * nrb);
-        const cd iu(0.0, 1.0);
-        for (int n = -K; n <= K; ++n) {
-            const double kap = c.prob.kappa(n, d);
-            const cd ku = vertical_wavenumber(k.front(), kap), kd = vertical_wavenumber(k.back(), kap);
-            for (int m = 0; m < M; ++m) {
-                const cd e = std::exp(iu * kap * g.ud_x[m]);
-                WU[size_t(n + K) * 2 * M + m] = C(-e);
-                WU[size_t(n + K) * 2 * M + M + m] = C(-iu * ku * e);
-                WD[size_t(n + K) * 2 * M + m] = C(-e);
-                WD[size_t(n + K) * 2 * M + M + m] = C(iu * kd * e);
-            }
-        }
-        for (int side = 0; side < 2; ++side) {
-            cplx* dst = c.Qc.p + size_t(side) * D.mC * D.pC + size_t(D.P) * D.mC + 2 * D.Mw;
-            QPS_CUDA(cudaMemcpy2DAsync(dst, sizeof(cplx) * D.mC, (side ? WD : WU).data(), sizeof(cplx) * 2 * M,
-                                       sizeof(cplx) * 2 * M, nrb, cudaMemcpyHostToDevice, s));
-        }
-        const auto& q0 = g.ifaces.front();
-        const int n0 = q0.N();
-        const double kx = k.front() * std::cos(c.prob.theta), ky = k.front() * std::sin(c.prob.theta);
-        std::vector<cplx> fh(nb, cplx{0, 0});
-        for (int j = 0; j < n0; ++j) {
-            const cd e = std::exp(iu * (kx * q0.x[j] + ky * q0.y[j]));
-            fh[j] = C(-e);
-            fh[n0 + j] = C(-iu * (kx * q0.nx[j] + ky * q0.ny[j]) * e);
-        }
-        c.f.upload(fh, s);
-    }
-    // padding: identity on the unused diagonal of padded A_jj blocks
-    if (D.padded) {
-        std::vector<cplx> one(1, cplx{1.0, 0.0});
-        for (int j = 0; j < I; ++j)
-            for (int i = 2 * D.N[j]; i < nb; ++i)
-                QPS_CUDA(cudaMemcpyAsync(c.Adiag.p + j * nb2 + size_t(i) * nb + i, one.data(), sizeof(cplx),
-                                         cudaMemcpyHostToDevice, s));
-    }
+    write_radiation_and_rhs(c, {c.prob});
+    if (D.padded) pad_identity(c);
     int herr = 0;
     QPS_D2H(&herr, c.d_err.p, sizeof(int), s);
     QPS_CUDA(cudaStreamSynchronize(s));
@@ -920,10 +882,8 @@ void recover(Ctx& c) {
 }
 
 // flux_error + reflection_transmission (postprocess.hpp:132-180)
-void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,
-                   int* pd) {
-    const Problem& p = c.prob;
-    const double d = c.geo.d;
+void spectrum_of(const Problem& p, double d, const cplx* aU, const cplx* aD, double* R, double* T, double* fe,
+                 double* kappa, cplx* kU, cplx* kD, int* pu, int* pd) {
     const double kref = std::max(p.k.front(), p.k.back());
     const double Finc = p.k.front() * std::abs(std::sin(p.theta));
     const double tol = 1e-5;
@@ -931,7 +891,7 @@ void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa
     for (int n = -p.K; n <= p.K; ++n) {
         const double kap = p.kappa(n, d);
         const cd ku = vertical_wavenumber(p.k.front(), kap), kd = vertical_wavenumber(p.k.back(), kap);
-        const cd au = Z(c.h_aU[n + p.K]), ad = Z(c.h_aD[n + p.K]);
+        const cd au = Z(aU[n + p.K]), ad = Z(aD[n + p.K]);
         const bool propu = ku.imag() == 0.0 && ku.real() > tol * kref;
         const bool propd = kd.imag() == 0.0 && kd.real() > tol * kref;
         if (propu) {
@@ -952,6 +912,60 @@ void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa
     if (R) *R = RR;
     if (T) *T = TT;
     if (fe) *fe = (F - Finc) / Finc;
+}
+
+void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,
+                   int* pd) {
+    spectrum_of(c.prob, c.geo.d, c.h_aU.data(), c.h_aD.data(), R, T, fe, kappa, kU, kD, pu, pd);
+}
+
+// W blocks (assembly.hpp:414-427) and f (assembly.hpp:431-441) on the host: O(M K) + O(N) per system
+void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs) {
+    const Dims& D = c.dims;
+    const HostGeometry& g = c.geo;
+    const int M = D.M, K = D.K, nrb = D.nrb, nb = D.nb;
+    const double d = g.d;
+    cudaStream_t s = c.stream;
+    const cd iu(0.0, 1.0);
+    const int ns = int(probs.size());
+    std::vector<cplx> W(size_t(ns) * 2 * size_t(2 * M) * nrb), fh(size_t(ns) * nb, cplx{0, 0});
+    const auto& q0 = g.ifaces.front();
+    const int n0 = q0.N();
+    for (int a = 0; a < ns; ++a) {
+        const Problem& p = probs[a];
+        const auto& k = p.k;
+        cplx* WU = W.data() + size_t(2 * a) * 2 * M * nrb;
+        cplx* WD = WU + size_t(2 * M) * nrb;
+        for (int n = -K; n <= K; ++n) {
+            const double kap = p.kappa(n, d);
+            const cd ku = vertical_wavenumber(k.front(), kap), kd = vertical_wavenumber(k.back(), kap);
+            for (int m = 0; m < M; ++m) {
+                const cd e = std::exp(iu * kap * g.ud_x[m]);
+                WU[size_t(n + K) * 2 * M + m] = C(-e);
+                WU[size_t(n + K) * 2 * M + M + m] = C(-iu * ku * e);
+                WD[size_t(n + K) * 2 * M + m] = C(-e);
+                WD[size_t(n + K) * 2 * M + M + m] = C(iu * kd * e);
+            }
+        }
+        const double kx = k.front() * std::cos(p.theta), ky = k.front() * std::sin(p.theta);
+        cplx* f = fh.data() + size_t(a) * nb;
+        for (int j = 0; j < n0; ++j) {
+            const cd e = std::exp(iu * (kx * q0.x[j] + ky * q0.y[j]));
+            f[j] = C(-e);
+            f[n0 + j] = C(-iu * (kx * q0.nx[j] + ky * q0.ny[j]) * e);
+        }
+    }
+    for (int a = 0; a < ns; ++a)
+        for (int side = 0; side < 2; ++side) {
+            cplx* dst = c.Qc.p + size_t(a) * D.sQc() + size_t(side) * D.mC * D.pC + size_t(D.P) * D.mC + 2 * D.Mw;
+            QPS_CUDA(cudaMemcpy2DAsync(dst, sizeof(cplx) * D.mC, W.data() + size_t(2 * a + side) * 2 * M * nrb,
+                                       sizeof(cplx) * 2 * M, sizeof(cplx) * 2 * M, nrb, cudaMemcpyHostToDevice, s));
+        }
+    c.f.ensure(fh.size());
+    QPS_CUDA(cudaMemcpyAsync(c.f.p, fh.data(), sizeof(cplx) * fh.size(), cudaMemcpyHostToDevice, s));
+    g_h2d_bytes += sizeof(cplx) * (W.size() + fh.size());
+    // the pageable sources must outlive the copies
+    QPS_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace qpsb
