@@ -25,6 +25,8 @@ SELF_TOL = 1e-9
 
 
 def rel(a, b):
+    if b.size == 0:
+        return 0.0
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
 
 
@@ -78,12 +80,14 @@ def _sweep_cases(n):
 
 
 def test_sweep_matches_oracle(gpu, oracle):
+    # 8 interfaces: a well-resolved prefix of config 5 (flux error ~1e-11; the
+    # 4-interface prefix is resolved only to ~1e-7, tools/sweep_parity_report.py)
     thetas = _sweep_cases(6)
-    om, K = setup(gpu, 5, 4)
+    om, K = setup(gpu, 5, 8)
     g = gpu.sweep(thetas, K, mode=0)
-    setup(oracle, 5, 4)
+    setup(oracle, 5, 8)
     o = oracle.sweep(thetas, K, mode=0)
-    setup(oracle, 5, 4, omega_ulp=True)
+    setup(oracle, 5, 8, omega_ulp=True)
     o1 = oracle.sweep(thetas, K, mode=0)
     assert np.all(g["status"] == 0) and np.all(o["status"] == 0)
     for a in range(len(thetas)):
@@ -102,15 +106,15 @@ def test_sweep_equals_single_solves(gpu):
     """Each sweep angle equals the one-shot solve at that angle (fused fill vs
     cache + recombination: same sums in a different order)."""
     thetas = _sweep_cases(3)
-    om, K = setup(gpu, 5, 4)
+    om, K = setup(gpu, 5, 8)
     g = gpu.sweep(thetas, K, mode=0)
     for a, th in enumerate(thetas):
-        setup(gpu, 5, 4, theta=th)
+        setup(gpu, 5, 8, theta=th)
         gpu.solve()
         sol = gpu.solution()
         ref = np.concatenate([sol["aU"], sol["aD"]])
         got = np.concatenate([g["aU"][a], g["aD"][a]])
-        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-8, a
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-9, a
 
 
 def test_sweep_modes_and_batching_agree(gpu):
