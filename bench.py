@@ -221,7 +221,9 @@ def main():
                 "frac": d_tf / peak, "traffic": None,
                 "peak_source": "FP64 DMMA (mma.sync m8n8k4 f64) microbenchmark in this run; bf16 peaks of "
                                "MEASURED_PEAKS.json do not apply to FP64",
-                "algorithmic": "8*M*N*K real flops per complex GEMM task, summed over the batched launches",
+                "algorithmic": "6*M*N*K real flops per complex GEMM task (3M Gauss product: three real DMMA "
+                               "products per complex product), summed over the batched launches",
+                "complex_equiv_tflops": d_tf * 8.0 / 6.0 if dname.startswith("zgemm") else None,
                 "launches": dv["launches"], "avg_launch_ms": dv["ms"] / max(1, dv["launches"])}
     # ---- end-to-end through the public API from host data ----
     barrier(dist)
@@ -257,7 +259,8 @@ def main():
                 if fill_ms else None,
                 "fill_frac_of_dfma_peak": (200.0 * fill_units / (fill_ms * 1e-3) / 1e12) / peaks["dfma_tflops"]
                 if fill_ms else None,
-                "gemm_tflops": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
+                "gemm_tflops_issued": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
+                "gemm_tflops_complex_equiv": gemm_fl * 8.0 / 6.0 / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "fp64_peaks_tflops": peaks, "flux_error": rt["flux_error"], "R": rt["R"], "T": rt["T"],
                 "families_ms": {k: round(v["ms"] / args.steps, 3) for k, v in sorted(fams.items(),
                                                                                      key=lambda kv: -kv[1]["ms"])}}

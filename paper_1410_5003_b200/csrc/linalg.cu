@@ -2,14 +2,14 @@
 //
 // FP64 on Blackwell: tcgen05.mma has no f64 kind, so the tensor path for
 // double precision is the warp-level mma.sync m8n8k4 f64 (SASS DMMA).  The
-// complex GEMM keeps real and imaginary planes of each 64x64x8 tile in shared
-// memory (2-way-conflict-free padding, register double buffering of the next
-// K chunk) and issues four real DMMAs per complex 8x8x4 step:
-//   Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br.
+// batched complex GEMM (zgemm3m_t_kernel) issues three real DMMAs per complex
+// 8x8x4 step (Gauss product); the four-DMMA kernel (zgemm_kernel,
+//   Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br) stays selectable.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 
 #include "linalg.cuh"
@@ -159,19 +159,6 @@ __global__ void __launch_bounds__(128, 2) zgemm_kernel(int M, int N, cplx alpha,
             }
 }
 
-// ---------------------------------------------------------------------------
-// v2: cp.async multi-stage pipeline.  Tiles are copied 16 B (one complex) at a
-// time straight into shared memory (interleaved re/im, [k][m] and [k][n]
-// layouts, leading dimension = tile + 2 complex so that the DMMA fragment
-// pattern (k = lane & 3, m = lane >> 2) hits 8 distinct 16-byte bank groups
-// per quarter warp).  Out-of-range elements are zero-filled by cp.async's
-// src-size operand.  K may be the concatenation of two products (nseg = 2).
-// ---------------------------------------------------------------------------
-constexpr int G2_BM = 64, G2_BN = 64, G2_BK = 16, G2_ST = 3;
-constexpr int G2_LDA = G2_BM + 2, G2_LDB = G2_BN + 2;
-constexpr int G2_STAGE = G2_BK * (G2_LDA + G2_LDB);  // complex elements per stage
-constexpr size_t G2_SMEM = size_t(G2_ST) * G2_STAGE * sizeof(double2);
-
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     const int n = valid ? 16 : 0;
@@ -183,108 +170,133 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__global__ void __launch_bounds__(128, 2) zgemm_v2_kernel(int M, int N, cplx alpha, cplx beta,
-                                                          const GemmTask* __restrict__ tasks, int tiles_m) {
-    extern __shared__ double2 g2_smem[];
+
+// ---------------------------------------------------------------------------
+// 3M: three real DMMAs per complex 8x8x4 step instead of four,
+//   P = Ar Br,  Q = Ai Bi,  S = (Ar + Ai)(Br + Bi),  Cr = P - Q,  Ci = S - P - Q
+// (the Gauss product; normwise backward stable, error of the imaginary part
+// ~ eps (|Ar| + |Ai|)(|Br| + |Bi|)), so the tensor pipe issues 6 M N K instead
+// of 8 M N K real flops.  cp.async pipeline with a configurable warp tile (WMT x WNT m8n8
+// tiles per warp, WARPS_M x WARPS_N warps).  Tiles are staged as interleaved
+// complex: A as [k][m] (ld BM + 2 complex), B as [n][k] (ld BK + 4 complex), so
+// the 16-byte fragment loads (lanes: k = lane & 3, m/n = lane >> 2) and the
+// cp.async stores hit 8 distinct 16-byte bank groups per quarter warp.  The
+// Gauss sums Ar + Ai, Br + Bi are formed in registers (FP64 pipe, not the
+// tensor pipe).
+// ---------------------------------------------------------------------------
+template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES>
+struct Z3Cfg {
+    static constexpr int BM = WARPS_M * 8 * WMT, BN = WARPS_N * 8 * WNT, BK = 16;
+    static constexpr int NT = 32 * WARPS_M * WARPS_N;
+    static constexpr int LDA = BM + 2, LDK = BK + 4;
+    static constexpr int STAGE = BK * LDA + BN * LDK;  // complex elements
+    static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double2);
+};
+
+template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
+    zgemm3m_t_kernel(int M, int N, cplx alpha, cplx beta, const GemmTask* __restrict__ tasks, int tiles_m) {
+    using Cfg = Z3Cfg<WMT, WNT, WARPS_M, WARPS_N, STAGES>;
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, NT = Cfg::NT, LDA = Cfg::LDA, LDK = Cfg::LDK;
+    extern __shared__ double2 z3_smem[];
     const GemmTask& T = tasks[blockIdx.y];
     const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
-    const int m0 = tm * G2_BM, n0 = tn * G2_BN;
+    const int m0 = tm * BM, n0 = tn * BN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int wm = (warp % WARPS_M) * 8 * WMT, wn = (warp / WARPS_M) * 8 * WNT;
     const int nseg = T.nseg;
     const int K0 = T.K[0], K1 = nseg > 1 ? T.K[1] : 0;
-    const int c0n = (K0 + G2_BK - 1) / G2_BK, c1n = (K1 + G2_BK - 1) / G2_BK;
+    const int c0n = (K0 + BK - 1) / BK, c1n = (K1 + BK - 1) / BK;
     const int nchunks = c0n + c1n;
 
     auto issue = [&](int c, int stage) {
         const int sgi = c < c0n ? 0 : 1;
-        const int k0 = (c < c0n ? c : c - c0n) * G2_BK;
+        const int k0 = (c < c0n ? c : c - c0n) * BK;
         const cplx* __restrict__ A = T.A[sgi];
         const cplx* __restrict__ B = T.B[sgi];
         const int lda = T.lda[sgi], ldb = T.ldb[sgi], K = T.K[sgi];
-        double2* As = g2_smem + stage * G2_STAGE;
-        double2* Bs = As + G2_BK * G2_LDA;
+        double2* As = z3_smem + stage * Cfg::STAGE;
+        double2* Bs = As + BK * LDA;
 #pragma unroll
-        for (int i = 0; i < (G2_BM * G2_BK) / 128; ++i) {
-            const int idx = tid + 128 * i;
-            const int row = idx % G2_BM, kk = idx / G2_BM;
-            const int gm = m0 + row, gk = k0 + kk;
-            const bool ok = gm < M && gk < K;
-            cp_async16(As + kk * G2_LDA + row, ok ? (const void*)(A + size_t(gk) * lda + gm) : (const void*)A, ok);
+        for (int i = 0; i < (BM * BK + NT - 1) / NT; ++i) {
+            const int idx = tid + NT * i;
+            if ((BM * BK) % NT == 0 || idx < BM * BK) {
+                const int row = idx % BM, kk = idx / BM;
+                const int gm = m0 + row, gk = k0 + kk;
+                const bool ok = gm < M && gk < K;
+                cp_async16(As + kk * LDA + row, ok ? (const void*)(A + size_t(gk) * lda + gm) : (const void*)A, ok);
+            }
         }
 #pragma unroll
-        for (int i = 0; i < (G2_BN * G2_BK) / 128; ++i) {
-            const int idx = tid + 128 * i;
-            const int kk = idx % G2_BK, col = idx / G2_BK;
-            const int gn = n0 + col, gk = k0 + kk;
-            const bool ok = gn < N && gk < K;
-            cp_async16(Bs + kk * G2_LDB + col, ok ? (const void*)(B + size_t(gn) * ldb + gk) : (const void*)B, ok);
+        for (int i = 0; i < (BN * BK + NT - 1) / NT; ++i) {
+            const int idx = tid + NT * i;
+            if ((BN * BK) % NT == 0 || idx < BN * BK) {
+                const int kk = idx % BK, col = idx / BK;
+                const int gn = n0 + col, gk = k0 + kk;
+                const bool ok = gn < N && gk < K;
+                cp_async16(Bs + col * LDK + kk, ok ? (const void*)(B + size_t(gn) * ldb + gk) : (const void*)B, ok);
+            }
         }
     };
 
-    double acc[4][4][2][2];
+    double acc[3][WMT][WNT][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int q = 0; q < 3; ++q)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+        for (int i = 0; i < WMT; ++i)
+#pragma unroll
+            for (int j = 0; j < WNT; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
 
 #pragma unroll
-    for (int st = 0; st < G2_ST - 1; ++st) {
+    for (int st = 0; st < STAGES - 1; ++st) {
         if (st < nchunks) issue(st, st);
         cp_async_commit();
     }
     for (int c = 0; c < nchunks; ++c) {
-        cp_async_wait<G2_ST - 2>();
+        cp_async_wait<STAGES - 2>();
         __syncthreads();
-        if (c + G2_ST - 1 < nchunks) issue(c + G2_ST - 1, (c + G2_ST - 1) % G2_ST);
+        if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1, (c + STAGES - 1) % STAGES);
         cp_async_commit();
-        const double2* As = g2_smem + (c % G2_ST) * G2_STAGE;
-        const double2* Bs = As + G2_BK * G2_LDA;
+        const double2* As = z3_smem + (c % STAGES) * Cfg::STAGE;
+        const double2* Bs = As + BK * LDA;
 #pragma unroll
-        for (int ks = 0; ks < G2_BK; ks += 4) {
+        for (int ks = 0; ks < BK; ks += 4) {
             const int kq = ks + (lane & 3), r = lane >> 2;
-            double ar[4], ai[4], nai[4], br[4], bi[4];
+            double br[WNT], bi[WNT], bs[WNT];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const double2 v = As[kq * G2_LDA + wm + 8 * i + r];
-                ar[i] = v.x;
-                ai[i] = v.y;
-                nai[i] = -v.y;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const double2 v = Bs[kq * G2_LDB + wn + 8 * j + r];
+            for (int j = 0; j < WNT; ++j) {
+                const double2 v = Bs[(wn + 8 * j + r) * LDK + kq];
                 br[j] = v.x;
                 bi[j] = v.y;
+                bs[j] = v.x + v.y;
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < WMT; ++i) {
+                const double2 v = As[kq * LDA + wm + 8 * i + r];
+                const double as = v.x + v.y;
+                // consecutive DMMAs share the A operand (operand reuse)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    dmma(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
-                    dmma(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);
-                }
+                for (int j = 0; j < WNT; ++j) dmma(acc[0][i][j][0], acc[0][i][j][1], v.x, br[j]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+                for (int j = 0; j < WNT; ++j) dmma(acc[1][i][j][0], acc[1][i][j][1], v.y, bi[j]);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    dmma(acc[i][j][0][0], acc[i][j][0][1], nai[i], bi[j]);
-                    dmma(acc[i][j][1][0], acc[i][j][1][1], ai[i], br[j]);
-                }
+                for (int j = 0; j < WNT; ++j) dmma(acc[2][i][j][0], acc[2][i][j][1], as, bs[j]);
+            }
         }
     }
     cp_async_wait<0>();
     const bool use_beta = (beta.re != 0.0 || beta.im != 0.0);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < WMT; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < WNT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int row = m0 + wm + 8 * i + (lane >> 2);
                 const int col = n0 + wn + 8 * j + 2 * (lane & 3) + e;
                 if (row < M && col < N) {
-                    const double vr = acc[i][j][0][e], vi = acc[i][j][1][e];
+                    const double P = acc[0][i][j][e], Q = acc[1][i][j][e], S = acc[2][i][j][e];
+                    const double vr = P - Q, vi = S - P - Q;
                     cplx out{alpha.re * vr - alpha.im * vi, alpha.re * vi + alpha.im * vr};
                     cplx* p = T.C + size_t(col) * T.ldc + row;
                     if (use_beta) {
@@ -295,6 +307,22 @@ __global__ void __launch_bounds__(128, 2) zgemm_v2_kernel(int M, int N, cplx alp
                     *p = out;
                 }
             }
+}
+
+template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB = (WARPS_M * WARPS_N <= 4) ? 2 : 1>
+void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_t ntasks, cudaStream_t s) {
+    using Cfg = Z3Cfg<WMT, WNT, WARPS_M, WARPS_N, STAGES>;
+    auto kern = zgemm3m_t_kernel<WMT, WNT, WARPS_M, WARPS_N, STAGES, MINB>;
+    static bool attr = false;
+    if (!attr) {
+        QPS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
+        attr = true;
+    }
+    const int tiles_m = (M + Cfg::BM - 1) / Cfg::BM, tiles_n = (N + Cfg::BN - 1) / Cfg::BN;
+    for (size_t off = 0; off < ntasks; off += 65535) {
+        const unsigned cnt = unsigned(std::min<size_t>(65535, ntasks - off));
+        kern<<<dim3(tiles_m * tiles_n, cnt), Cfg::NT, Cfg::SMEM, s>>>(M, N, alpha, beta, tasks + off, tiles_m);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1230,11 +1258,19 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
                    DBuf<GemmTask>& d_tasks) {
     if (tasks.empty() || M <= 0 || N <= 0) return;
     d_tasks.upload(tasks, s);
-    const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+    // default: 3M, CTA 64 x 32 (4 warps of 32 x 16), two stages, three CTAs per
+    // SM (38 TF/s complex-equivalent at 608^3 on B200 = 77 % of the DMMA pipe);
+    // QPS_ZGEMM=4m selects the four-DMMA kernel (28 TF/s)
+    static const bool four_m = [] {
+        const char* e = getenv("QPS_ZGEMM");
+        return e && !strcmp(e, "4m");
+    }();
+    // flops recorded = real flops issued to the tensor pipe (6 M N K for 3M)
+    const double fpc = four_m ? 8.0 : 6.0;
     double fl = 0, by = 0;
     for (const auto& t : tasks)
         for (int q = 0; q < t.nseg; ++q) {
-            fl += 8.0 * M * N * t.K[q];
+            fl += fpc * M * N * t.K[q];
             by += 16.0 * (double(M) * t.K[q] + double(t.K[q]) * N);
         }
     by += 16.0 * double(M) * N * tasks.size() * ((beta.re != 0.0 || beta.im != 0.0) ? 2 : 1);
@@ -1243,19 +1279,14 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
         for (int q = 0; q < t.nseg; ++q) kmax = std::max(kmax, t.K[q]);
     const char* nm = (kmax <= 64) ? (M <= 64 ? "zgemm_k64_m64" : "zgemm_k64") : (M >= 256 && N >= 256 ? "zgemm_big" : "zgemm_mid");
     ProfScope ps(nm, s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
-    static bool attr = false;
-    if (!attr) {
-        QPS_CUDA(cudaFuncSetAttribute(zgemm_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G2_SMEM)));
-        attr = true;
-    }
-    static const bool use_v1 = getenv("QPS_ZGEMM_V2") == nullptr;  // register-staged v1 is faster on B200
-    for (size_t off = 0; off < tasks.size(); off += 65535) {
-        const unsigned cnt = unsigned(std::min<size_t>(65535, tasks.size() - off));
-        if (use_v1)
+    if (!four_m) {
+        launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+    } else {
+        const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+        for (size_t off = 0; off < tasks.size(); off += 65535) {
+            const unsigned cnt = unsigned(std::min<size_t>(65535, tasks.size() - off));
             zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
-        else
-            zgemm_v2_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, G2_SMEM, s>>>(M, N, alpha, beta, d_tasks.p + off,
-                                                                              tiles_m);
+        }
     }
     QPS_CUDA(cudaGetLastError());
 }

@@ -7,7 +7,7 @@
 using namespace qpsb;
 int main(int argc, char** argv) {
     struct Shape { int M, N, K, batch, nseg; double beta; };
-    std::vector<Shape> shapes = {{600, 600, 600, 250, 1, 1.0}, {600, 600, 600, 250, 2, 1.0}, {600, 600, 80, 500, 2, 1.0},
+    std::vector<Shape> shapes = {{608, 608, 608, 250, 1, 1.0}, {600, 600, 600, 250, 1, 1.0}, {600, 600, 600, 250, 2, 1.0}, {600, 600, 80, 500, 2, 1.0},
                                  {568, 600, 32, 250, 1, 1.0}, {312, 312, 288, 250, 1, 1.0}, {64, 600, 64, 500, 1, 0.0},
                                  {80, 1200, 80, 999, 1, 0.0}};
     cudaStream_t s; cudaStreamCreate(&s);
