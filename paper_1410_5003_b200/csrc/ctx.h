@@ -124,6 +124,7 @@ struct Ctx {
     DBuf<int2> d_ctiles;
     DBuf<BandTask> d_band;
     DBuf<int> d_nodes2;
+    DBuf<cplx> wtmp;  // staging of the radiation W blocks
 
     // ---- assembled system (BlockSystem, assembly.hpp:293-315) ----
     Dims dims;

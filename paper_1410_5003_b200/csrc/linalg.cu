@@ -1116,6 +1116,143 @@ __global__ void __launch_bounds__(256) lu_panel_smem_kernel(int n, int ld, cplx*
     }
 }
 
+// Right-looking LU step for one 16-column panel [k0, k0 + w) of every matrix:
+// lu_rl_panel_kernel (one CTA per matrix) factors the panel with partial
+// pivoting in shared memory (rows k0..n); lu_rl_cols_kernel (one warp per
+// column outside the panel, many CTAs per matrix) applies the panel's row
+// interchanges (LAPACK xGETRF order) and, right of the panel, the unit-lower
+// solve U12 = L11^{-1} A12; the trailing update is one batched 3M GEMM.
+constexpr int kRlW = 16;
+__global__ void __launch_bounds__(256) lu_rl_panel_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+                                                          int* const* __restrict__ Pp, int k0, int w,
+                                                          int* singular) {
+    extern __shared__ cplx pnl[];
+    cplx* A = Ap[blockIdx.x];
+    int* ipiv = Pp[blockIdx.x];
+    const int rows = n - k0;
+    __shared__ double shv[32];
+    __shared__ int shi[32];
+    __shared__ int spiv[kRlW];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < rows * w; e += blockDim.x) {
+        const int i = e % rows, j = e / rows;
+        pnl[j * rows + i] = A[size_t(k0 + j) * ld + k0 + i];
+    }
+    __syncthreads();
+    for (int k = 0; k < w; ++k) {
+        double v = -1.0;
+        int idx = rows;
+        for (int i = k + tid; i < rows; i += blockDim.x) {
+            const double a = cabs2(pnl[k * rows + i]);
+            if (a > v) { v = a; idx = i; }
+        }
+        double best;
+        int piv;
+        block_argmax(v, idx, shv, shi, best, piv);
+        if (tid == 0) {
+            ipiv[k0 + k] = k0 + piv;
+            spiv[k] = piv;
+        }
+        if (piv != k && tid < w) {
+            const cplx t = pnl[tid * rows + k];
+            pnl[tid * rows + k] = pnl[tid * rows + piv];
+            pnl[tid * rows + piv] = t;
+        }
+        __syncthreads();
+        const cplx d = pnl[k * rows + k];
+        const bool zero = (d.re == 0.0 && d.im == 0.0);
+        if (zero && tid == 0) singular[blockIdx.x] = 1;
+        const cplx inv = zero ? cplx{0, 0} : cdiv(cplx{1.0, 0.0}, d);
+        for (int i = k + 1 + tid; i < rows; i += blockDim.x) {
+            cplx l = pnl[k * rows + i];
+            if (!zero) {
+                l = cmul(l, inv);
+                pnl[k * rows + i] = l;
+            }
+            for (int j = k + 1; j < w; ++j) {
+                const cplx t = cmul(l, pnl[j * rows + k]);
+                pnl[j * rows + i].re -= t.re;
+                pnl[j * rows + i].im -= t.im;
+            }
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < rows * w; e += blockDim.x) {
+        const int i = e % rows, j = e / rows;
+        A[size_t(k0 + j) * ld + k0 + i] = pnl[j * rows + i];
+    }
+
+}
+
+// one warp per column: lanes 0..w-1 hold rows k0..k0+w-1, lanes 16.. the
+// external rows the interchanges touch; the interchange sequence is replayed
+// on lane indices, the values move with one shuffle, the unit-lower solve is
+// a w-step shuffle broadcast.
+__global__ void __launch_bounds__(256) lu_rl_cols_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+                                                         const int* const* __restrict__ Pp, int k0, int w) {
+    cplx* A = Ap[blockIdx.y];
+    const int* ipiv = Pp[blockIdx.y];
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (c >= n - w) return;
+    const int col = c < k0 ? c : c + w;
+    cplx* Ac = A + size_t(col) * ld;
+    // replay the interchanges on positions: pos[] = rows currently at each slot
+    // slots 0..w-1 are rows k0..k0+w-1; extra slots hold distinct external rows
+    int ext_row = -1;  // this lane's external row (lanes >= 16)
+    int src = lane;    // slot whose ORIGINAL value ends in this lane's slot
+    {
+        int rowof[32];
+        int nslot = kRlW;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) rowof[q] = q < kRlW ? k0 + q : -1;
+        int perm[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) perm[q] = q;
+        for (int t = 0; t < w; ++t) {
+            const int p = ipiv[k0 + t];
+            if (p == k0 + t) continue;
+            int sp = -1;
+            if (p < k0 + kRlW) sp = p - k0;
+            else {
+                for (int q = kRlW; q < nslot; ++q)
+                    if (rowof[q] == p) sp = q;
+                if (sp < 0) {
+                    sp = nslot++;
+                    rowof[sp] = p;
+                }
+            }
+            const int tmp = perm[t];
+            perm[t] = perm[sp];
+            perm[sp] = tmp;
+        }
+        src = perm[lane];
+        ext_row = lane >= kRlW ? rowof[lane] : -1;
+        if (lane < kRlW && lane >= w) src = lane;
+    }
+    cplx v{0, 0};
+    if (lane < w) v = Ac[k0 + lane];
+    else if (ext_row >= 0) v = Ac[ext_row];
+    cplx nv;
+    nv.re = __shfl_sync(0xffffffffu, v.re, src);
+    nv.im = __shfl_sync(0xffffffffu, v.im, src);
+    if (col > k0) {  // U12 = L11^{-1} A12 (unit lower, L11 in the factored panel)
+        const cplx* Lp = A + size_t(k0) * ld + k0;
+        for (int u = 0; u + 1 < w; ++u) {
+            cplx ru;
+            ru.re = __shfl_sync(0xffffffffu, nv.re, u);
+            ru.im = __shfl_sync(0xffffffffu, nv.im, u);
+            if (lane > u && lane < w) {
+                const cplx l = Lp[size_t(u) * ld + lane];
+                nv.re -= l.re * ru.re - l.im * ru.im;
+                nv.im -= l.re * ru.im + l.im * ru.re;
+            }
+        }
+    }
+    if (lane < w) Ac[k0 + lane] = nv;
+    else if (ext_row >= 0) Ac[ext_row] = nv;
+}
+
 __global__ void rowswap_rhs_kernel(int n, const int* const* __restrict__ Pp, cplx* const* __restrict__ Bp, int ldb,
                                    int nc) {
     const int* ipiv = Pp[blockIdx.y];
@@ -1481,6 +1618,36 @@ void lu_rec(LuCtx& L, int c0, int nc) {
     }
 }
 
+// right-looking LU: n/16 steps of (fused panel kernel, trailing 3M GEMM with
+// K = 16); two launches per step keep the dependent chain short, which is what
+// bounds the deep cyclic-reduction levels (few matrices per launch)
+void lu_rl(LuCtx& L) {
+    const int n = L.n;
+    static bool attr = false;
+    if (!attr) {
+        QPS_CUDA(cudaFuncSetAttribute(lu_rl_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    for (int k0 = 0; k0 < n; k0 += kRlW) {
+        const int w = std::min(kRlW, n - k0);
+        {
+            ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(n - k0) * w * w / 2.0);
+            lu_rl_panel_kernel<<<L.count, 256, size_t(n - k0) * w * sizeof(cplx), L.s>>>(n, L.ld, L.dA, L.dP, k0, w,
+                                                                                         L.sing);
+            QPS_CUDA(cudaGetLastError());
+        }
+        if (n > w) {
+            ProfScope ps("lu_swap", L.s, 0.0);
+            lu_rl_cols_kernel<<<dim3((n - w + 7) / 8, L.count), 256, 0, L.s>>>(n, L.ld, L.dA, L.dP, k0, w);
+            QPS_CUDA(cudaGetLastError());
+        }
+        const int m = n - k0 - w;
+        if (m > 0)
+            gemm_update(L, m, m, w, size_t(k0) * L.ld + k0 + w, size_t(k0 + w) * L.ld + k0,
+                        size_t(k0 + w) * L.ld + k0 + w, cplx{-1, 0}, cplx{1, 0}, L.hA, L.hA, L.ld);
+    }
+}
+
 }  // namespace
 
 void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,
@@ -1491,7 +1658,22 @@ void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::v
     ws.iptrs.upload(hP, s);
     ws.ptrs3.upload(hDinv, s);
     LuCtx L{n, ld, count, hA, hP, hDinv, ws.ptrs.p, ws.iptrs.p, ws.ptrs3.p, d_singular, s, ws};
-    lu_rec(L, 0, n);
+    // Many matrices per launch: the recursive (Toledo) LU, whose big GEMMs run
+    // near peak; few matrices: the right-looking LU, whose short dependent
+    // chain (three launches per 16 columns) sets the latency.  QPS_LU=rec|rl
+    // forces one; QPS_LU_RL_MAX sets the crossover count.
+    static const int mode = [] {
+        const char* e = getenv("QPS_LU");
+        return !e ? 0 : !strcmp(e, "rec") ? 1 : !strcmp(e, "rl") ? 2 : 0;
+    }();
+    static const int rl_max = [] {
+        const char* e = getenv("QPS_LU_RL_MAX");
+        return e ? atoi(e) : 64;
+    }();
+    const bool rl_ok = size_t(n) * kRlW * sizeof(cplx) <= 200 * 1024;
+    const bool use_rl = rl_ok && (mode == 2 || (mode == 0 && count <= rl_max));
+    if (use_rl) lu_rl(L);
+    else lu_rec(L, 0, n);
     // inverse 64x64 diagonal tiles of L and U for the GEMM-shaped solves
     launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 3, s);
 }

@@ -1,5 +1,7 @@
 #include <cstring>
+#include <deque>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -10,6 +12,58 @@ namespace qpsb {
 
 std::atomic<uint64_t> g_launches{0};
 std::atomic<uint64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+namespace {
+struct StagingRing {
+    static constexpr size_t kSize = size_t(64) << 20;
+    std::mutex mu;
+    char* base = nullptr;
+    size_t head = 0;
+    struct Pending {
+        size_t lo, hi;
+        cudaEvent_t ev;
+    };
+    std::deque<Pending> pending;
+    std::vector<cudaEvent_t> free_events;
+};
+StagingRing& ring() {
+    static StagingRing* r = new StagingRing();  // never destroyed: outlives every context
+    return *r;
+}
+}  // namespace
+
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    StagingRing& R = ring();
+    const size_t need = (bytes + 255) & ~size_t(255);
+    if (need > R.kSize / 4) {  // large one-off copies: plain (synchronising) path
+        QPS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    std::lock_guard<std::mutex> lk(R.mu);
+    if (!R.base) QPS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&R.base), R.kSize));
+    if (R.head + need > R.kSize) R.head = 0;
+    const size_t lo = R.head, hi = R.head + need;
+    // wait for earlier copies still reading [lo, hi)
+    for (auto it = R.pending.begin(); it != R.pending.end();) {
+        const bool overlap = it->lo < hi && lo < it->hi;
+        if (overlap || cudaEventQuery(it->ev) == cudaSuccess) {
+            if (overlap) QPS_CUDA(cudaEventSynchronize(it->ev));
+            R.free_events.push_back(it->ev);
+            it = R.pending.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    std::memcpy(R.base + lo, src, bytes);
+    QPS_CUDA(cudaMemcpyAsync(dst, R.base + lo, bytes, cudaMemcpyHostToDevice, s));
+    cudaEvent_t ev;
+    if (R.free_events.empty()) QPS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    else { ev = R.free_events.back(); R.free_events.pop_back(); }
+    QPS_CUDA(cudaEventRecord(ev, s));
+    R.pending.push_back({lo, hi, ev});
+    R.head = hi;
+}
 
 namespace {
 struct Pending {

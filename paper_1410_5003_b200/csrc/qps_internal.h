@@ -17,6 +17,12 @@ namespace qpsb {
 // host<->device traffic counters (bench.py's e2e bytes per step)
 extern std::atomic<uint64_t> g_h2d_bytes, g_d2h_bytes;
 
+// Stream-ordered host->device copy through a pinned staging ring: the source
+// is copied into page-locked memory and the DMA is queued without waiting for
+// the stream (a pageable cudaMemcpyAsync would synchronise it, serialising the
+// host with every small task-table upload of a launch chain).
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // Error taxonomy (mirrors /root/reference/proj/include/qpscat/errors.hpp:9-40)
 // ---------------------------------------------------------------------------
@@ -77,7 +83,7 @@ struct DBuf {
     void upload(const std::vector<T>& h, cudaStream_t s) {
         ensure(h.size());
         if (!h.empty()) {
-            QPS_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+            h2d_staged(p, h.data(), h.size() * sizeof(T), s);
             g_h2d_bytes += h.size() * sizeof(T);
         }
     }

@@ -13,6 +13,8 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ctx.h"
 #include "prof.h"
@@ -678,6 +680,19 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         if (worst >= 0) singular_error(worst);
     };
     int lvl = 0;
+    static const bool trace = getenv("QPS_BCR_TRACE") != nullptr;  // per-level timing to stderr (debug)
+    auto tmark = [&](const char* what, int l, int cnt) {
+        if (!trace) return;
+        static cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (!e0) { cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventRecord(e0, s); return; }
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        fprintf(stderr, "bcr level %d (%d odd) %s: %.3f ms\n", l, cnt, what, ms);
+        cudaEventRecord(e0, s);
+    };
+    tmark("start", 0, 0);
     while (c.levels[lvl][0].idx.size() > 1) {
         const BcrLevels& cur = c.levels[lvl];
         const int sz = int(cur[0].idx.size());
@@ -693,6 +708,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                 orig.push_back(cur[a].idx[o]);
             }
         factor(fa, fp, fd, orig);
+        tmark("factor", lvl, int(fa.size()));
         // 2. Y = D^{-1} [L | U] and y_f = D^{-1} f for the odd positions (in place)
         {
             std::vector<cplx*> ma, mb, md, va, vb, vd;
@@ -707,6 +723,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             lu_solve_batched(nb, nb, ma, mp, md, mb, nb, nb, s, c.ws);
             lu_solve_batched(nb, nb, va, vp, vd, vb, nb, 1, s, c.ws);
         }
+        tmark("solve", lvl, sz / 2);
         // 3. updates of the even positions
         const int nsz = (sz + 1) / 2;
         BcrLevels nxt(ns);
@@ -773,6 +790,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, upd, s, c.ws.gemm_tasks);
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{0, 0}, fresh, s, c.ws.gemm_tasks);
         zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vtasks, s, c.ws.gemv_tasks);
+        tmark("update", lvl, sz / 2);
         c.levels.push_back(nxt);
         ++lvl;
     }
@@ -792,6 +810,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         factor(fa, fp, fd, orig);
         lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
     }
+    tmark("last", lvl, 1);
     // back substitution: eta_o = y_f(o) - Y_L(o) eta_{o-1} - Y_U(o) eta_{o+1}; F ends up holding eta
     for (int l = lvl - 1; l >= 0; --l) {
         const BcrLevels& cur = c.levels[l];
@@ -810,6 +829,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             }
         zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vt, s, c.ws.gemv_tasks);
     }
+    tmark("backsub", lvl, 0);
     c.eta_valid = true;
 }
 
@@ -955,17 +975,17 @@ void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs) {
             f[n0 + j] = C(-iu * (kx * q0.nx[j] + ky * q0.ny[j]) * e);
         }
     }
+    c.wtmp.ensure(W.size());
+    h2d_staged(c.wtmp.p, W.data(), sizeof(cplx) * W.size(), s);
     for (int a = 0; a < ns; ++a)
         for (int side = 0; side < 2; ++side) {
             cplx* dst = c.Qc.p + size_t(a) * D.sQc() + size_t(side) * D.mC * D.pC + size_t(D.P) * D.mC + 2 * D.Mw;
-            QPS_CUDA(cudaMemcpy2DAsync(dst, sizeof(cplx) * D.mC, W.data() + size_t(2 * a + side) * 2 * M * nrb,
-                                       sizeof(cplx) * 2 * M, sizeof(cplx) * 2 * M, nrb, cudaMemcpyHostToDevice, s));
+            QPS_CUDA(cudaMemcpy2DAsync(dst, sizeof(cplx) * D.mC, c.wtmp.p + size_t(2 * a + side) * 2 * M * nrb,
+                                       sizeof(cplx) * 2 * M, sizeof(cplx) * 2 * M, nrb, cudaMemcpyDeviceToDevice, s));
         }
     c.f.ensure(fh.size());
-    QPS_CUDA(cudaMemcpyAsync(c.f.p, fh.data(), sizeof(cplx) * fh.size(), cudaMemcpyHostToDevice, s));
+    h2d_staged(c.f.p, fh.data(), sizeof(cplx) * fh.size(), s);
     g_h2d_bytes += sizeof(cplx) * (W.size() + fh.size());
-    // the pageable sources must outlive the copies
-    QPS_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace qpsb
