@@ -51,11 +51,26 @@ __device__ __forceinline__ void load_near(double* s_near, const double* g_near) 
     for (int i = threadIdx.x; i < kNear; i += blockDim.x) s_near[i] = g_near[i];
 }
 
+// re-layout [interval][function][term] -> [interval][term]{J0, J1}{R0, R1}
+__device__ __forceinline__ void load_near2(double2* s_near2, const double* g_near) {
+    for (int e = threadIdx.x; e < QPS_HANKEL_XB * QPS_HANKEL_NEAR_TERMS * 2; e += blockDim.x) {
+        const int half = e & 1, k = (e >> 1) % QPS_HANKEL_NEAR_TERMS, i = (e >> 1) / QPS_HANKEL_NEAR_TERMS;
+        const double* c = g_near + i * QPS_NEAR_STRIDE;
+        s_near2[e] = make_double2(c[(2 * half) * QPS_HANKEL_NEAR_TERMS + k], c[(2 * half + 1) * QPS_HANKEL_NEAR_TERMS + k]);
+    }
+}
+
 __device__ __forceinline__ void cacc(cplx& a, cplx c, double s, cplx v) {
     // a += s * c * v
     const double vr = s * v.re, vi = s * v.im;
     a.re += c.re * vr - c.im * vi;
     a.im += c.re * vi + c.im * vr;
+}
+
+__device__ __forceinline__ void cmacc(cplx& a, cplx c, cplx v) {
+    // a += c * v
+    a.re = fma(c.re, v.re, fma(-c.im, v.im, a.re));
+    a.im = fma(c.re, v.im, fma(c.im, v.re, a.im));
 }
 
 __device__ __forceinline__ void store(cplx* p, cplx v, int acc) {
@@ -75,15 +90,15 @@ __device__ __forceinline__ int seg_index(const PairTask& T, int m) {
     return s;
 }
 
-__global__ void __launch_bounds__(kThreads) pair_fill_kernel(const PairTask* __restrict__ tasks,
+__global__ void __launch_bounds__(kThreads, 4) pair_fill_kernel(const PairTask* __restrict__ tasks,
                                                              const int4* __restrict__ tiles, DevPool pool,
                                                              const double* __restrict__ g_near, int* err) {
-    __shared__ double s_near[kNear];
+    __shared__ double2 s_near2[QPS_HANKEL_XB * QPS_HANKEL_NEAR_TERMS * 2];
     __shared__ double sx[kTile], sy[kTile], snx[kTile], sny[kTile], sw[kTile];
     __shared__ PairTask T;
     const int4 tile = tiles[blockIdx.x];
     if (threadIdx.x == 0) T = tasks[tile.x];
-    load_near(s_near, g_near);
+    load_near2(s_near2, g_near);
     __syncthreads();
     const int m0 = tile.y, j0 = tile.z;
     if (threadIdx.x < kTile) {
@@ -101,56 +116,88 @@ __global__ void __launch_bounds__(kThreads) pair_fill_kernel(const PairTask* __r
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int m = m0 + lane;
     if (m >= T.nt) return;
+    // task constants in registers
+    const int nterm = T.nterm, nk = T.nk, self = T.self, ns = T.ns;
+    const double k0 = T.k[0], k1 = T.k[1], sg0 = T.ksign[0], sg1 = T.ksign[1];
+    const double ik0 = 1.0 / k0, ik1 = nk > 1 ? 1.0 / k1 : 0.0;
+    // per-wavenumber scale factors: sign/4, sign*k/4 and (8/k)^2 for u = (8/x)^2
+    const double s40 = 0.25 * sg0, s41 = 0.25 * sg1, d40 = s40 * k0, d41 = s41 * k1;
+    const double u0 = 64.0 * ik0 * ik0, u1 = 64.0 * ik1 * ik1;
     const int gt = T.t_off + m;
     const double tx = pool.x[gt], ty = pool.y[gt], tnx = pool.nx[gt], tny = pool.ny[gt];
+    // coincidence threshold of eval_kernels (kernels.hpp:38-39) per shifted target, squared
+    auto thr_of = [&](int t) {
+        const double xx = tx + T.tdx[t];
+        const double th = 1e-13 * (1.0 + sqrt(xx * xx + ty * ty));
+        return th * th;
+    };
+    const double thr2_0 = thr_of(0), thr2_1 = thr_of(1), thr2_2 = thr_of(2);
     bool corrected = true;
     int mseg = 0;
-    if (T.self == 2) {
+    if (self == 2) {
         mseg = seg_index(T, m);
         const int ml = m - T.seg_start[mseg], n = T.seg_start[mseg + 1] - T.seg_start[mseg];
         corrected = min(ml, n - 1 - ml) >= QPS_ALPERT_A;
     }
+#pragma unroll 1
     for (int q = warp; q < kTile; q += kThreads / 32) {
         const int j = j0 + q;
-        if (j >= T.ns) break;
+        if (j >= ns) break;
         cplx aD{0, 0}, aS{0, 0}, aT{0, 0}, aDs{0, 0};
         const double zx0 = sx[q], zy = sy[q], znx = snx[q], zny = sny[q], w = sw[q];
-        for (int t = 0; t < T.nterm; ++t) {
+        const double nn = tnx * znx + tny * zny;
+#pragma unroll 1
+        for (int t = 0; t < nterm; ++t) {
             const int l = T.lsh[t];
-            if (T.self == 1) {
-                const int off = j + l * T.ns - m;
+            if (self == 1) {
+                const int off = j + l * ns - m;
                 if (off <= QPS_ALPERT_A - 1 && off >= -(QPS_ALPERT_A - 1)) continue;
-            } else if (T.self == 2 && l == 0) {
+            } else if (self == 2 && l == 0) {
                 if (j == m) continue;
                 if (corrected && j - m <= QPS_ALPERT_A - 1 && m - j <= QPS_ALPERT_A - 1 && seg_index(T, j) == mseg)
                     continue;
             }
-            const double xx = tx + T.tdx[t];
-            const double zx = zx0 + T.sdx[t];
-            const double rvx = xx - zx, rvy = ty - zy;
-            const double r = sqrt(rvx * rvx + rvy * rvy);
-            if (r < 1e-13 * (1.0 + sqrt(xx * xx + ty * ty))) {
+            const double rvx = (tx + T.tdx[t]) - (zx0 + T.sdx[t]), rvy = ty - zy;
+            const double r2 = rvx * rvx + rvy * rvy;
+            if (r2 < (t == 0 ? thr2_0 : t == 1 ? thr2_1 : thr2_2)) {
                 atomicOr(err, 1);
                 continue;
             }
+            const double inv_r = rsqrt(r2);
+            const double r = r2 * inv_r;
+            const double cn = (rvx * tnx + rvy * tny) * inv_r;
+            const double cdn = (rvx * znx + rvy * zny) * inv_r;
+            const double cc = cn * cdn;
+            const double Bt = inv_r * (nn - 2.0 * cc);  // k-independent factor of the H1 term of T
+            const double ir2 = inv_r * inv_r;
+            // eval_kernels (kernels.hpp:35-52) summed over the wavenumbers with signs:
+            //   S = (i/4) H0, D = (ik/4) H1 cdn, D* = -(ik/4) H1 cn,
+            //   T = (ik/4) [k cn cdn H0 + (nn - 2 cn cdn)/r H1]
             cplx tD{0, 0}, tS{0, 0}, tT{0, 0}, tDs{0, 0};
-            for (int kk = 0; kk < T.nk; ++kk) {
-                const double k = T.k[kk];
+#pragma unroll 1
+            for (int kk = 0; kk < nk; ++kk) {
+                const double k = kk ? k1 : k0;
                 HankelOut h;
-                hankel01_eval(k * r, s_near, c_hankel_far, h);
-                KVals v;
-                kernel_vals(k, rvx, rvy, r, tnx, tny, znx, zny, h, v);
-                const double sg = T.ksign[kk];
-                tD.re += sg * v.D.re; tD.im += sg * v.D.im;
-                tS.re += sg * v.S.re; tS.im += sg * v.S.im;
-                tT.re += sg * v.T.re; tT.im += sg * v.T.im;
-                tDs.re += sg * v.Ds.re; tDs.im += sg * v.Ds.im;
+                hankel01_dev(k * r, inv_r * (kk ? ik1 : ik0), ir2 * (kk ? u1 : u0), s_near2, h);
+                const double s4 = kk ? s41 : s40, d4 = kk ? d41 : d40;
+                tS.re = fma(-s4, h.y0, tS.re);
+                tS.im = fma(s4, h.j0, tS.im);
+                const double h1r = -d4 * h.y1, h1i = d4 * h.j1;
+                tD.re = fma(h1r, cdn, tD.re);
+                tD.im = fma(h1i, cdn, tD.im);
+                tDs.re = fma(-h1r, cn, tDs.re);
+                tDs.im = fma(-h1i, cn, tDs.im);
+                const double A = k * cc;
+                const double br = fma(A, h.j0, Bt * h.j1), bi = fma(A, h.y0, Bt * h.y1);
+                tT.re = fma(-d4, bi, tT.re);
+                tT.im = fma(d4, br, tT.im);
             }
             const cplx c = T.coef[t];
-            cacc(aD, c, w, tD);
-            cacc(aS, c, w, tS);
-            cacc(aT, c, w, tT);
-            cacc(aDs, c, w, tDs);
+            const cplx wc{w * c.re, w * c.im};
+            cmacc(aD, wc, tD);
+            cmacc(aS, wc, tS);
+            cmacc(aT, wc, tT);
+            cmacc(aDs, wc, tDs);
         }
         if (T.ident && j == m) {
             aD.re -= 1.0;

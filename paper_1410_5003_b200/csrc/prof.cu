@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -67,7 +68,7 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 
 namespace {
 struct Pending {
-    const char* name;
+    std::string name;
     cudaEvent_t e0, e1;
     double flops, bytes, units;
     int nlaunch;
@@ -77,6 +78,7 @@ struct Agg {
     double ms = 0, flops = 0, bytes = 0, units = 0;
 };
 bool g_on = false;
+const char* g_phase = nullptr;
 std::vector<Pending> g_pending;
 std::map<std::string, Agg> g_agg;
 std::vector<cudaEvent_t> g_free;
@@ -129,9 +131,14 @@ ProfScope::ProfScope(const char* name_, cudaStream_t s_, double flops_, double b
 ProfScope::~ProfScope() {
     if (!e0) return;
     cudaEventRecord(e1, s);
-    g_pending.push_back({name, e0, e1, flops, bytes, units, nlaunch});
+    static const bool phases = getenv("QPS_PROF_PHASES") != nullptr;
+    std::string key = (phases && g_phase) ? std::string(g_phase) + ":" + name : std::string(name);
+    g_pending.push_back({key, e0, e1, flops, bytes, units, nlaunch});
     if (g_pending.size() > 4096) resolve();
 }
+
+ProfPhase::ProfPhase(const char* tag) : prev(g_phase) { g_phase = tag; }
+ProfPhase::~ProfPhase() { g_phase = prev; }
 
 int prof_query(ProfStat* out, int cap) {
     resolve();

@@ -35,5 +35,11 @@ struct ProfStat {
     double ms, flops, bytes, units;
 };
 int prof_query(ProfStat* out, int cap);
+// with QPS_PROF_PHASES set, families are keyed "phase:name" inside a ProfPhase
+struct ProfPhase {
+    const char* prev;
+    explicit ProfPhase(const char* tag);
+    ~ProfPhase();
+};
 
 }  // namespace qpsb

@@ -536,6 +536,7 @@ void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int 
 }
 
 void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
+    ProfPhase phase("schur");
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, P = D.P, ns = D.nsys;
     if (P <= 0) fail(QPS_ERR_CONFIG, "periodization needs P > 0 proxy points per layer");
@@ -626,6 +627,7 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
 // Block cyclic reduction (all systems of the batch advance level by level)
 // ---------------------------------------------------------------------------
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
+    ProfPhase phase("bcr");
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, ns = D.nsys;
     const size_t nb2 = D.nb2();
