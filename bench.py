@@ -37,6 +37,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "1000-layer solve wall time & layers/s; kernel evals/s; % of FP64 peak"
 ORACLE = os.path.join(ROOT, "oracle", "_ref", "libqpscat_ref.so")
+# ncu --set full summaries of the captured launches (profiles/README.md says how they were taken)
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+
+
+def ncu_summary():
+    try:
+        with open(NCU_SUMMARY) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 CFG = 4
 
 
@@ -217,14 +227,19 @@ def main():
     peak = peaks["dmma_tflops"]
     dname, dv = dom
     d_tf = dv["flops"] / (dv["ms"] * 1e-3) / 1e12
+    ncu = ncu_summary().get(dname, {})
     roofline = {"kernel": dname, "bound": "tensor", "achieved": d_tf, "peak": peak, "unit": "TFLOP/s",
-                "frac": d_tf / peak, "traffic": None,
+                "frac": d_tf / peak,
+                "traffic": ncu.get("dram_bytes"),
+                "traffic_note": ncu.get("note"),
+                "traffic_algorithmic_bytes": ncu.get("algorithmic_bytes"),
                 "peak_source": "FP64 DMMA (mma.sync m8n8k4 f64) microbenchmark in this run; bf16 peaks of "
                                "MEASURED_PEAKS.json do not apply to FP64",
                 "algorithmic": "6*M*N*K real flops per complex GEMM task (3M Gauss product: three real DMMA "
                                "products per complex product), summed over the batched launches",
-                "complex_equiv_tflops": d_tf * 8.0 / 6.0 if dname.startswith("zgemm") else None,
+                "complex_equiv_tflops": d_tf * 8.0 / 6.0 if dv["flops"] else None,
                 "launches": dv["launches"], "avg_launch_ms": dv["ms"] / max(1, dv["launches"])}
+    fill_ncu = ncu_summary().get("fill_pair", {})
     # ---- end-to-end through the public API from host data ----
     barrier(dist)
     e2e_ms = []
@@ -259,6 +274,8 @@ def main():
                 if fill_ms else None,
                 "fill_frac_of_dfma_peak": (200.0 * fill_units / (fill_ms * 1e-3) / 1e12) / peaks["dfma_tflops"]
                 if fill_ms else None,
+                "fill_fp64_frac_ncu": fill_ncu.get("fp64_frac_of_peak"),
+                "fill_fp64_ncu_note": fill_ncu.get("note"),
                 "gemm_tflops_issued": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "gemm_tflops_complex_equiv": gemm_fl * 8.0 / 6.0 / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "fp64_peaks_tflops": peaks, "flux_error": rt["flux_error"], "R": rt["R"], "T": rt["T"],

@@ -114,6 +114,8 @@ qps_ctx* qps_create(int device) {
     try {
         QPS_CUDA(cudaSetDevice(device));
         QPS_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+        QPS_CUDA(cudaStreamCreateWithFlags(&h->c.side, cudaStreamNonBlocking));
+        QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fork, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreate(&h->c.ev0));
         QPS_CUDA(cudaEventCreate(&h->c.ev1));
         upload_hankel_tables();
@@ -134,9 +136,12 @@ void qps_destroy(qps_ctx* h) {
     cudaStreamSynchronize(h->c.stream);
     if (h->c.ev0) cudaEventDestroy(h->c.ev0);
     if (h->c.ev1) cudaEventDestroy(h->c.ev1);
-    cudaStream_t s = h->c.stream;
+    cudaStream_t s = h->c.stream, s2 = h->c.side;
+    if (s2) cudaStreamSynchronize(s2);
+    if (h->c.ev_fork) cudaEventDestroy(h->c.ev_fork);
     delete h;
     if (s) cudaStreamDestroy(s);
+    if (s2) cudaStreamDestroy(s2);
 }
 
 int qps_last_error(const qps_ctx* h, char* msg, size_t cap, int* layer, uint64_t* bytes) {

@@ -34,6 +34,7 @@ struct CodSet {
     DBuf<cplx> W, V, tau, zc, M1, Y, QH, Wz, Tb, E;
     DBuf<int> perm, nzp, rank, flags;
     DBuf<double> maxpiv, xmax, rmax, enorm, rnorm;
+    DBuf<GemmTask> tasks1, tasks2;  // task tables of this family's GEMMs (families run on separate streams)
     CodBatch batch(const cplx* Q) {
         CodBatch b;
         b.count = count; b.m = m; b.p = p; b.Q = Q;
@@ -97,6 +98,8 @@ struct Ctx {
     int device = 0;
     bool host_only = false;  // device == -1: geometry/problem logic only, every device call fails
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // second stream: work independent of the main stream (corner least squares)
+    cudaEvent_t ev_fork = nullptr;
 
     StackDesc stack;
     Numerics num;

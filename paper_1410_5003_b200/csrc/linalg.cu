@@ -724,6 +724,201 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
     }
 }
 
+// Same operator with the working set in shared memory (problems with
+// (m p + max(p^2, 8 m)) complex entries <= kCodSmemMax): region 1 holds the RZ
+// reflectors V, then the QR reflectors W; region 2 the Wz work columns
+// (row-major, conflict-free per thread column), then the per-warp QH columns.
+constexpr size_t kCodSmemMax = 220 * 1024;
+__global__ void __launch_bounds__(256) cod_operator_smem_kernel(CodBatch b, const int* __restrict__ flags) {
+    extern __shared__ cplx cod_sm[];
+    const int pb = blockIdx.x;
+    if (flags && !flags[pb]) return;
+    const int m = b.m, p = b.p;
+    const cplx* W = b.W + size_t(pb) * m * p;
+    const cplx* tau = b.tau + size_t(pb) * p;
+    cplx* zc = b.zc + size_t(pb) * p;
+    const int* perm = b.perm + size_t(pb) * p;
+    cplx* QH = b.QH + size_t(pb) * p * m;
+    cplx* Wz = b.Wz + size_t(pb) * p * p;
+    const int r = b.rank[pb];
+    const int tid = threadIdx.x;
+    __shared__ double shv[32];
+    __shared__ cplx s_den, s_zc;
+    cplx* V = cod_sm;                      // region 1
+    cplx* R2 = cod_sm + size_t(m) * p;     // region 2
+    if (r == 0) {
+        for (size_t i = tid; i < size_t(p) * m; i += blockDim.x) QH[i] = cplx{0, 0};
+        for (size_t i = tid; i < size_t(p) * p; i += blockDim.x) Wz[i] = cplx{0, 0};
+        return;
+    }
+    for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) V[i] = W[i];
+    __syncthreads();
+    auto vat = [&](int i, int j) -> cplx& { return V[size_t(j) * m + i]; };
+    if (r < p) {  // RZ reduction of [R11 R12] (Eigen COD), reflectors into zc and V
+        for (int k = r - 1; k >= 0; --k) {
+            if (k != r - 1)
+                for (int i = tid; i <= k; i += blockDim.x) {
+                    const cplx t = vat(i, k);
+                    vat(i, k) = vat(i, r - 1);
+                    vat(i, r - 1) = t;
+                }
+            __syncthreads();
+            const int L = p - r + 1;
+            double ts = 0.0;
+            for (int j = 1 + tid; j < L; j += blockDim.x) ts += cabs2(vat(k, r - 1 + j));
+            const double tail_sq = block_sum(ts, shv);
+            if (tid == 0) {
+                const cplx c0 = vat(k, r - 1);
+                double beta;
+                cplx tk;
+                if (tail_sq <= DBL_MIN && c0.im * c0.im <= DBL_MIN) {
+                    tk = cplx{0, 0};
+                    beta = c0.re;
+                    s_den = cplx{0, 0};
+                } else {
+                    beta = sqrt(cabs2(c0) + tail_sq);
+                    if (c0.re >= 0.0) beta = -beta;
+                    s_den = cplx{c0.re - beta, c0.im};
+                    tk = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
+                }
+                s_zc = tk;
+                zc[k] = tk;
+                vat(k, r - 1) = cplx{beta, 0.0};
+            }
+            __syncthreads();
+            const cplx den = s_den, tk = s_zc;
+            for (int j = 1 + tid; j < L; j += blockDim.x) {
+                cplx& e = vat(k, r - 1 + j);
+                e = (den.re == 0.0 && den.im == 0.0) ? cplx{0, 0} : cdiv(e, den);
+            }
+            __syncthreads();
+            if (k > 0 && !(tk.re == 0.0 && tk.im == 0.0)) {
+                for (int i = tid; i < k; i += blockDim.x) {
+                    cplx t = vat(i, r - 1);
+                    for (int j = 1; j < L; ++j) {
+                        const cplx e = vat(k, r - 1 + j);
+                        const cplx a = vat(i, r - 1 + j);
+                        t.re += a.re * e.re + a.im * e.im;
+                        t.im += a.im * e.re - a.re * e.im;
+                    }
+                    t = cmul(t, tk);
+                    vat(i, r - 1).re -= t.re;
+                    vat(i, r - 1).im -= t.im;
+                    for (int j = 1; j < L; ++j) {
+                        const cplx te = cmul(t, vat(k, r - 1 + j));
+                        vat(i, r - 1 + j).re -= te.re;
+                        vat(i, r - 1 + j).im -= te.im;
+                    }
+                }
+            }
+            __syncthreads();
+            if (k != r - 1)
+                for (int i = tid; i <= k; i += blockDim.x) {
+                    const cplx t = vat(i, k);
+                    vat(i, k) = vat(i, r - 1);
+                    vat(i, r - 1) = t;
+                }
+            __syncthreads();
+        }
+    }
+    // Wz columns: P Z^* e_c for c < r (thread per column; work column in region 2, row-major)
+    {
+        const cplx* zs = zc;
+        for (int c = tid; c < p; c += blockDim.x) {
+            cplx* w = Wz + size_t(c) * p;
+            if (c >= r) {
+                for (int i = 0; i < p; ++i) w[i] = cplx{0, 0};
+                continue;
+            }
+            auto y = [&](int i) -> cplx& { return R2[size_t(i) * p + c]; };
+            for (int i = 0; i < p; ++i) y(i) = cplx{i == c ? 1.0 : 0.0, 0.0};
+            if (r < p) {
+                for (int k = 0; k < r; ++k) {
+                    const cplx tk = zs[k];
+                    if (k != r - 1) {
+                        const cplx t = y(k);
+                        y(k) = y(r - 1);
+                        y(r - 1) = t;
+                    }
+                    if (!(tk.re == 0.0 && tk.im == 0.0)) {
+                        cplx t = y(r - 1);
+                        for (int j = 0; j < p - r; ++j) {
+                            const cplx e = cmul(vat(k, r + j), y(r + j));
+                            t.re += e.re;
+                            t.im += e.im;
+                        }
+                        t = cmul(t, tk);
+                        y(r - 1).re -= t.re;
+                        y(r - 1).im -= t.im;
+                        for (int j = 0; j < p - r; ++j) {
+                            const cplx e = cmul(cconj(vat(k, r + j)), t);
+                            y(r + j).re -= e.re;
+                            y(r + j).im -= e.im;
+                        }
+                    }
+                    if (k != r - 1) {
+                        const cplx t = y(k);
+                        y(k) = y(r - 1);
+                        y(r - 1) = t;
+                    }
+                }
+            }
+            for (int i = 0; i < p; ++i) w[perm[i]] = y(i);
+        }
+    }
+    // T11 (upper triangle of V) for cod_trsm
+    {
+        cplx* Vg = b.V + size_t(pb) * m * p;
+        for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) Vg[i] = V[i];
+    }
+    __syncthreads();
+    // QR reflectors into region 1 (V is no longer needed)
+    for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) V[i] = W[i];
+    __syncthreads();
+    const cplx* Ws = V;
+    // QH = first r rows of H_{r-1} ... H_0: one warp per column, lanes over rows
+    {
+        const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+        cplx* col = R2 + size_t(warp) * m;
+        for (int c = warp; c < m; c += nw) {
+            for (int i = lane; i < m; i += 32) col[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
+            __syncwarp();
+            for (int kk = 0; kk < r; ++kk) {
+                const cplx tk = tau[kk];
+                if (tk.re == 0.0 && tk.im == 0.0) continue;
+                cplx t{0, 0};
+                for (int i = kk + 1 + lane; i < m; i += 32) {
+                    const cplx e = Ws[size_t(kk) * m + i];
+                    const cplx a = col[i];
+                    t.re += e.re * a.re + e.im * a.im;
+                    t.im += e.re * a.im - e.im * a.re;
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    t.re += __shfl_xor_sync(0xffffffffu, t.re, o);
+                    t.im += __shfl_xor_sync(0xffffffffu, t.im, o);
+                }
+                const cplx ck = col[kk];
+                t.re += ck.re;
+                t.im += ck.im;
+                t = cmul(tk, t);
+                __syncwarp();
+                if (lane == 0) {
+                    col[kk].re -= t.re;
+                    col[kk].im -= t.im;
+                }
+                for (int i = kk + 1 + lane; i < m; i += 32) {
+                    const cplx et = cmul(Ws[size_t(kk) * m + i], t);
+                    col[i].re -= et.re;
+                    col[i].im -= et.im;
+                }
+                __syncwarp();
+            }
+            for (int i = lane; i < p; i += 32) QH[size_t(c) * p + i] = i < r ? col[i] : cplx{0, 0};
+            __syncwarp();
+        }
+    }
+}
+
 // back substitution with T11 (upper, r x r inside V, ld m), one thread per
 // column of the right-hand side; T11 is staged in shared memory (every thread
 // reads the same entry at the same time: broadcast).
@@ -1392,7 +1587,7 @@ __global__ void dmma_peak_kernel(double* out, int iters) {
 }  // namespace
 
 void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
-                   DBuf<GemmTask>& d_tasks) {
+                   DBuf<GemmTask>& d_tasks, const char* family) {
     if (tasks.empty() || M <= 0 || N <= 0) return;
     d_tasks.upload(tasks, s);
     // default: 3M, CTA 64 x 32 (4 warps of 32 x 16), two stages, three CTAs per
@@ -1414,7 +1609,7 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
     int kmax = 0;
     for (const auto& t : tasks)
         for (int q = 0; q < t.nseg; ++q) kmax = std::max(kmax, t.K[q]);
-    const char* nm = (kmax <= 64) ? (M <= 64 ? "zgemm_k64_m64" : "zgemm_k64") : (M >= 256 && N >= 256 ? "zgemm_big" : "zgemm_mid");
+    const char* nm = family ? family : (kmax <= 64) ? (M <= 64 ? "zgemm_k64_m64" : "zgemm_k64") : (M >= 256 && N >= 256 ? "zgemm_big" : "zgemm_mid");
     ProfScope ps(nm, s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
     if (!four_m) {
         launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
@@ -1445,7 +1640,18 @@ void cod_rank(const CodBatch& b, double th, const int* flags, cudaStream_t s) {
 void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
     if (b.count == 0) return;
     ProfScope ps("cod_operator", s, 8.0 * b.count * (double(b.m) * b.p * b.p + double(b.p) * b.p * b.p));
-    cod_operator_kernel<<<b.count, 256, 0, s>>>(b, flags);
+    const size_t sm = (size_t(b.m) * b.p + std::max(size_t(b.p) * b.p, size_t(8) * b.m)) * sizeof(cplx);
+    if (sm <= kCodSmemMax) {
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_operator_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kCodSmemMax)));
+            attr = true;
+        }
+        cod_operator_smem_kernel<<<b.count, 256, sm, s>>>(b, flags);
+    } else {
+        cod_operator_kernel<<<b.count, 256, 0, s>>>(b, flags);
+    }
     QPS_CUDA(cudaGetLastError());
 }
 void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, const int* flags, cudaStream_t s) {

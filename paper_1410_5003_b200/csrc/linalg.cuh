@@ -23,8 +23,9 @@ struct GemmTask {
 
 struct Workspace;  // forward
 
+// family: profiling name (string literal); default by shape
 void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
-                   DBuf<GemmTask>& d_tasks);
+                   DBuf<GemmTask>& d_tasks, const char* family = nullptr);
 
 // ---- COD least squares -----------------------------------------------------
 // Per problem b: Q_b (m x p, ld m).  Factor state lives in caller-provided

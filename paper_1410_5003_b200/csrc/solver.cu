@@ -443,89 +443,135 @@ void fill_system_fused(Ctx& c) {
 // ---------------------------------------------------------------------------
 namespace {
 
-// qsolve for one equal-shape family: X = argmin ||Q X - R|| with Eigen COD
-// semantics and the threshold escalation loop of periodize.hpp:29-37.
+// qsolve for equal-shape families of problems: X = argmin ||Q X - R|| with
+// Eigen COD semantics and the threshold escalation loop of periodize.hpp:29-37.
+// Families run concurrently, each on its own stream (the interior layers and
+// the two corner problems of schur_complement are independent); the host
+// joins them only at the escalation checkpoints.
+struct QFamily {
+    CodSet* cs;
+    const cplx* Q;
+    const cplx* R;
+    int ldR;
+    size_t Rstride;
+    cplx* X;
+    int ldX;
+    size_t Xstride;
+    double* lsq_out;
+    cudaStream_t s;
+    std::vector<double> rmax, xmax;
+    std::vector<int> flags;
+    bool pending = true;
+};
+
+void qsolve_families(Ctx& c, std::vector<QFamily>& fams) {
+    for (auto& f : fams) {
+        CodSet& cs = *f.cs;
+        f.pending = cs.count > 0;
+        if (!f.pending) continue;
+        CodBatch b = cs.batch(f.Q);
+        cod_factor(b, f.s);
+        // scale = max(1, max |RHS|)
+        batched_maxabs(f.R, cs.m, cs.ncols, f.ldR, f.Rstride, cs.count, cs.rmax.p, f.s);
+        f.rmax.assign(cs.count, 0.0);
+        f.xmax.assign(cs.count, 0.0);
+        f.flags.assign(cs.count, 1);
+        QPS_D2H(f.rmax.data(), cs.rmax.p, sizeof(double) * cs.count, f.s);
+    }
+    for (double th = c.qsolve_th0; th <= 1.1e-10; th *= 10.0) {
+        bool any_pending = false;
+        for (auto& f : fams) {
+            if (!f.pending) continue;
+            any_pending = true;
+            CodSet& cs = *f.cs;
+            CodBatch b = cs.batch(f.Q);
+            cs.flags.upload(f.flags, f.s);
+            cod_rank(b, th, cs.flags.p, f.s);
+            cod_operator(b, cs.flags.p, f.s);
+            // X = Wz * T11^{-1} * (QH * RHS)
+            std::vector<GemmTask> t1, t2;
+            for (int q = 0; q < cs.count; ++q) {
+                if (!f.flags[q]) continue;
+                GemmTask t{};
+                t.nseg = 1;
+                t.A[0] = cs.QH.p + size_t(q) * cs.p * cs.m;
+                t.lda[0] = cs.p;
+                t.B[0] = f.R + f.Rstride * q;
+                t.ldb[0] = f.ldR;
+                t.K[0] = cs.m;
+                t.C = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
+                t.ldc = cs.p;
+                t1.push_back(t);
+                GemmTask u{};
+                u.nseg = 1;
+                u.A[0] = cs.Wz.p + size_t(q) * cs.p * cs.p;
+                u.lda[0] = cs.p;
+                u.B[0] = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
+                u.ldb[0] = cs.p;
+                u.K[0] = cs.p;
+                u.C = f.X + f.Xstride * q;
+                u.ldc = f.ldX;
+                t2.push_back(u);
+            }
+            zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t1, f.s, cs.tasks1);
+            cod_trsm(b, cs.Tb.p, cs.p, size_t(cs.p) * cs.ncols, cs.ncols, cs.flags.p, f.s);
+            zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t2, f.s, cs.tasks2);
+            batched_maxabs(f.X, cs.p, cs.ncols, f.ldX, f.Xstride, cs.count, cs.xmax.p, f.s);
+            QPS_D2H(f.xmax.data(), cs.xmax.p, sizeof(double) * cs.count, f.s);
+        }
+        if (!any_pending) break;
+        for (auto& f : fams) {
+            if (!f.pending) continue;
+            QPS_CUDA(cudaStreamSynchronize(f.s));
+            bool any = false;
+            for (int q = 0; q < f.cs->count; ++q) {
+                if (!f.flags[q]) continue;
+                const double scale = std::max(1.0, f.rmax[q]);
+                if (f.xmax[q] <= 1e3 * scale) f.flags[q] = 0;  // accepted (qsolve_norm_cap, periodize.hpp:23)
+                else any = true;
+            }
+            f.pending = any;
+        }
+    }
+    // relative LSQ residual ||Q X - R|| / ||R||  (periodize.hpp:84,113-118)
+    for (auto& f : fams) {
+        CodSet& cs = *f.cs;
+        const int cnt = cs.count;
+        if (cnt == 0) continue;
+        copy_blocks(f.R, f.ldR, f.Rstride, cs.E.p, cs.m, size_t(cs.m) * cs.ncols, cs.m, cs.ncols, cnt, f.s);
+        std::vector<GemmTask> tasks(cnt);
+        for (int q = 0; q < cnt; ++q) {
+            GemmTask& t = tasks[q];
+            t.nseg = 1;
+            t.A[0] = f.Q + size_t(q) * cs.m * cs.p;
+            t.lda[0] = cs.m;
+            t.B[0] = f.X + f.Xstride * q;
+            t.ldb[0] = f.ldX;
+            t.K[0] = cs.p;
+            t.C = cs.E.p + size_t(q) * cs.m * cs.ncols;
+            t.ldc = cs.m;
+        }
+        zgemm_batched(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, f.s, cs.tasks1);
+        batched_fro(cs.E.p, cs.m, cs.ncols, cs.m, size_t(cs.m) * cs.ncols, cnt, cs.enorm.p, f.s);
+        batched_fro(f.R, cs.m, cs.ncols, f.ldR, f.Rstride, cnt, cs.rnorm.p, f.s);
+        f.rmax.assign(cnt, 0.0);  // reused: residual norms
+        f.xmax.assign(cnt, 0.0);
+        QPS_D2H(f.rmax.data(), cs.enorm.p, sizeof(double) * cnt, f.s);
+        QPS_D2H(f.xmax.data(), cs.rnorm.p, sizeof(double) * cnt, f.s);
+    }
+    for (auto& f : fams) {
+        if (f.cs->count == 0) continue;
+        QPS_CUDA(cudaStreamSynchronize(f.s));
+        for (int q = 0; q < f.cs->count; ++q) f.lsq_out[q] = f.rmax[q] / f.xmax[q];
+    }
+}
+
 void qsolve_family(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X, int ldX,
                    size_t Xstride, double* lsq_out) {
-    const int cnt = cs.count;
-    if (cnt == 0) return;
-    cudaStream_t s = c.stream;
-    CodBatch b = cs.batch(Q);
-    cod_factor(b, s);
-    // scale = max(1, max |RHS|)
-    batched_maxabs(R, cs.m, cs.ncols, ldR, Rstride, cnt, cs.rmax.p, s);
-    std::vector<double> rmax(cnt), xmax(cnt);
-    QPS_D2H(rmax.data(), cs.rmax.p, sizeof(double) * cnt, s);
-    std::vector<int> flags(cnt, 1);
-    bool first = true;
-    for (double th = c.qsolve_th0; th <= 1.1e-10; th *= 10.0) {
-        cs.flags.upload(flags, s);
-        cod_rank(b, th, cs.flags.p, s);
-        cod_operator(b, cs.flags.p, s);
-        // X = Wz * T11^{-1} * (QH * RHS)
-        std::vector<GemmTask> t1, t2;
-        for (int q = 0; q < cnt; ++q) {
-            if (!flags[q]) continue;
-            GemmTask t{};
-            t.nseg = 1;
-            t.A[0] = cs.QH.p + size_t(q) * cs.p * cs.m;
-            t.lda[0] = cs.p;
-            t.B[0] = R + Rstride * q;
-            t.ldb[0] = ldR;
-            t.K[0] = cs.m;
-            t.C = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
-            t.ldc = cs.p;
-            t1.push_back(t);
-            GemmTask u{};
-            u.nseg = 1;
-            u.A[0] = cs.Wz.p + size_t(q) * cs.p * cs.p;
-            u.lda[0] = cs.p;
-            u.B[0] = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
-            u.ldb[0] = cs.p;
-            u.K[0] = cs.p;
-            u.C = X + Xstride * q;
-            u.ldc = ldX;
-            t2.push_back(u);
-        }
-        zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t1, s, c.ws.gemm_tasks);
-        cod_trsm(b, cs.Tb.p, cs.p, size_t(cs.p) * cs.ncols, cs.ncols, cs.flags.p, s);
-        zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks);
-        batched_maxabs(X, cs.p, cs.ncols, ldX, Xstride, cnt, cs.xmax.p, s);
-        QPS_D2H(xmax.data(), cs.xmax.p, sizeof(double) * cnt, s);
-        QPS_CUDA(cudaStreamSynchronize(s));
-        bool any = false;
-        for (int q = 0; q < cnt; ++q) {
-            if (!flags[q]) continue;
-            const double scale = std::max(1.0, rmax[q]);
-            if (xmax[q] <= 1e3 * scale) flags[q] = 0;  // accepted (qsolve_norm_cap, periodize.hpp:23)
-            else any = true;
-        }
-        first = false;
-        if (!any) break;
-    }
-    (void)first;
-    // relative LSQ residual ||Q X - R|| / ||R||  (periodize.hpp:84,113-118)
-    copy_blocks(R, ldR, Rstride, cs.E.p, cs.m, size_t(cs.m) * cs.ncols, cs.m, cs.ncols, cnt, s);
-    std::vector<GemmTask> tasks(cnt);
-    for (int q = 0; q < cnt; ++q) {
-        GemmTask& t = tasks[q];
-        t.nseg = 1;
-        t.A[0] = Q + size_t(q) * cs.m * cs.p;
-        t.lda[0] = cs.m;
-        t.B[0] = X + Xstride * q;
-        t.ldb[0] = ldX;
-        t.K[0] = cs.p;
-        t.C = cs.E.p + size_t(q) * cs.m * cs.ncols;
-        t.ldc = cs.m;
-    }
-    zgemm_batched(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, s, c.ws.gemm_tasks);
-    batched_fro(cs.E.p, cs.m, cs.ncols, cs.m, size_t(cs.m) * cs.ncols, cnt, cs.enorm.p, s);
-    batched_fro(R, cs.m, cs.ncols, ldR, Rstride, cnt, cs.rnorm.p, s);
-    std::vector<double> en(cnt), rn(cnt);
-    QPS_D2H(en.data(), cs.enorm.p, sizeof(double) * cnt, s);
-    QPS_D2H(rn.data(), cs.rnorm.p, sizeof(double) * cnt, s);
-    QPS_CUDA(cudaStreamSynchronize(s));
-    for (int q = 0; q < cnt; ++q) lsq_out[q] = en[q] / rn[q];
+    std::vector<QFamily> f(1);
+    f[0].cs = &cs; f[0].Q = Q; f[0].R = R; f[0].ldR = ldR; f[0].Rstride = Rstride;
+    f[0].X = X; f[0].ldX = ldX; f[0].Xstride = Xstride; f[0].lsq_out = lsq_out; f[0].s = c.stream;
+    qsolve_families(c, f);
 }
 
 }  // namespace
@@ -547,15 +593,27 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     // interior layers i = 1..I-1 of every system: X = qsolve(Q_i, [C_above_i C_self_i])
     // (system a's interior layers are contiguous after system a-1's)
     std::vector<double> li(size_t(ns) * (I > 1 ? I - 1 : 0));
+    std::vector<double> lc(2 * size_t(ns));
+    std::vector<QFamily> fams;
     if (I > 1) {
         c.cod_int.ensure(ns * (I - 1), D.mI, P, 2 * nb);
-        qsolve_family(c, c.cod_int, c.Qint.p, c.Rint.p, D.mI, size_t(D.mI) * 2 * nb, c.Xint.p, P,
-                      size_t(P) * 2 * nb, li.data());
+        QFamily f;
+        f.cs = &c.cod_int; f.Q = c.Qint.p; f.R = c.Rint.p; f.ldR = D.mI; f.Rstride = size_t(D.mI) * 2 * nb;
+        f.X = c.Xint.p; f.ldX = P; f.Xstride = size_t(P) * 2 * nb; f.lsq_out = li.data(); f.s = c.stream;
+        fams.push_back(std::move(f));
     }
-    // corners: X_first = qsolve(Q'_1, C'_1), X_last = qsolve(Q'_{I+1}, C'_{I+1})
-    std::vector<double> lc(2 * size_t(ns));
+    // corners: X_first = qsolve(Q'_1, C'_1), X_last = qsolve(Q'_{I+1}, C'_{I+1}), on the side stream
     c.cod_c.ensure(2 * ns, D.mC, D.pC, nb);
-    qsolve_family(c, c.cod_c, c.Qc.p, c.Rc.p, D.mC, size_t(D.mC) * nb, c.Xc.p, D.pC, size_t(D.pC) * nb, lc.data());
+    {
+        QFamily f;
+        f.cs = &c.cod_c; f.Q = c.Qc.p; f.R = c.Rc.p; f.ldR = D.mC; f.Rstride = size_t(D.mC) * nb;
+        f.X = c.Xc.p; f.ldX = D.pC; f.Xstride = size_t(D.pC) * nb; f.lsq_out = lc.data(); f.s = c.side;
+        fams.push_back(std::move(f));
+    }
+    // the side stream starts after everything queued so far (the fill) on the main stream
+    QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    QPS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+    qsolve_families(c, fams);
     for (int a = 0; a < ns; ++a) {
         double* l = c.lsq_all.data() + size_t(a) * (I + 1);
         l[0] = lc[2 * a];
@@ -617,7 +675,7 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             }
         }
     }
-    zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks);
+    zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks, "schur_update");
     c.max_lsq = 0.0;
     for (double r : c.lsq) c.max_lsq = std::max(c.max_lsq, r);
     c.ps_valid = true;
@@ -789,8 +847,8 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                 nxt[a].U.push_back(nu);
             }
         }
-        zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, upd, s, c.ws.gemm_tasks);
-        zgemm_batched(nb, nb, cplx{-1, 0}, cplx{0, 0}, fresh, s, c.ws.gemm_tasks);
+        zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, upd, s, c.ws.gemm_tasks, "bcr_update");
+        zgemm_batched(nb, nb, cplx{-1, 0}, cplx{0, 0}, fresh, s, c.ws.gemm_tasks, "bcr_update");
         zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vtasks, s, c.ws.gemv_tasks);
         tmark("update", lvl, sz / 2);
         c.levels.push_back(nxt);
