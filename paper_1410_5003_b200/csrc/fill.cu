@@ -90,34 +90,20 @@ __device__ __forceinline__ int seg_index(const PairTask& T, int m) {
     return s;
 }
 
-__global__ void __launch_bounds__(kThreads, 4) pair_fill_kernel(const PairTask* __restrict__ tasks,
-                                                             const int4* __restrict__ tiles, DevPool pool,
-                                                             const double* __restrict__ g_near, int* err) {
-    __shared__ double2 s_near2[QPS_HANKEL_XB * QPS_HANKEL_NEAR_TERMS * 2];
-    __shared__ double sx[kTile], sy[kTile], snx[kTile], sny[kTile], sw[kTile];
-    __shared__ PairTask T;
-    const int4 tile = tiles[blockIdx.x];
-    if (threadIdx.x == 0) T = tasks[tile.x];
-    load_near2(s_near2, g_near);
-    __syncthreads();
-    const int m0 = tile.y, j0 = tile.z;
-    if (threadIdx.x < kTile) {
-        const int j = j0 + threadIdx.x;
-        if (j < T.ns) {
-            const int g = T.s_off + j;
-            sx[threadIdx.x] = pool.x[g];
-            sy[threadIdx.x] = pool.y[g];
-            snx[threadIdx.x] = pool.nx[g];
-            sny[threadIdx.x] = pool.ny[g];
-            sw[threadIdx.x] = pool.w[g];
-        }
-    }
-    __syncthreads();
+// body of one 32 x 32 tile, specialised on the self-block kind (0 plain, 1
+// smooth self, 2 open-arc self) and the number of wavenumbers (the A_jj blocks
+// sum two); the specialisation removes per-pair branches and lets the two
+// wavenumber evaluations of a pair interleave
+template <int SELF, int NK>
+__device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, DevPool pool, const double* sx,
+                                          const double* sy, const double* snx, const double* sny, const double* sw,
+                                          const double2* s_near2, int* err) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int m = m0 + lane;
     if (m >= T.nt) return;
     // task constants in registers
-    const int nterm = T.nterm, nk = T.nk, self = T.self, ns = T.ns;
+    const int nterm = T.nterm, ns = T.ns;
+    constexpr int nk = NK, self = SELF;
     const double k0 = T.k[0], k1 = T.k[1], sg0 = T.ksign[0], sg1 = T.ksign[1];
     const double ik0 = 1.0 / k0, ik1 = nk > 1 ? 1.0 / k1 : 0.0;
     // per-wavenumber scale factors: sign/4, sign*k/4 and (8/k)^2 for u = (8/x)^2
@@ -174,8 +160,8 @@ __global__ void __launch_bounds__(kThreads, 4) pair_fill_kernel(const PairTask* 
             //   S = (i/4) H0, D = (ik/4) H1 cdn, D* = -(ik/4) H1 cn,
             //   T = (ik/4) [k cn cdn H0 + (nn - 2 cn cdn)/r H1]
             cplx tD{0, 0}, tS{0, 0}, tT{0, 0}, tDs{0, 0};
-#pragma unroll 1
-            for (int kk = 0; kk < nk; ++kk) {
+#pragma unroll
+            for (int kk = 0; kk < NK; ++kk) {
                 const double k = kk ? k1 : k0;
                 HankelOut h;
                 hankel01_dev(k * r, inv_r * (kk ? ik1 : ik0), ir2 * (kk ? u1 : u0), s_near2, h);
@@ -208,6 +194,39 @@ __global__ void __launch_bounds__(kThreads, 4) pair_fill_kernel(const PairTask* 
         store(T.oS + o, aS, T.accumulate);
         store(T.oT + o, aT, T.accumulate);
         store(T.oDs + o, aDs, T.accumulate);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 4) pair_fill_kernel(const PairTask* __restrict__ tasks,
+                                                             const int4* __restrict__ tiles, DevPool pool,
+                                                             const double* __restrict__ g_near, int* err) {
+    __shared__ double2 s_near2[QPS_HANKEL_XB * QPS_HANKEL_NEAR_TERMS * 2];
+    __shared__ double sx[kTile], sy[kTile], snx[kTile], sny[kTile], sw[kTile];
+    __shared__ PairTask T;
+    const int4 tile = tiles[blockIdx.x];
+    if (threadIdx.x == 0) T = tasks[tile.x];
+    load_near2(s_near2, g_near);
+    __syncthreads();
+    const int m0 = tile.y, j0 = tile.z;
+    if (threadIdx.x < kTile) {
+        const int j = j0 + threadIdx.x;
+        if (j < T.ns) {
+            const int g = T.s_off + j;
+            sx[threadIdx.x] = pool.x[g];
+            sy[threadIdx.x] = pool.y[g];
+            snx[threadIdx.x] = pool.nx[g];
+            sny[threadIdx.x] = pool.ny[g];
+            sw[threadIdx.x] = pool.w[g];
+        }
+    }
+    __syncthreads();
+    switch (T.self * 2 + (T.nk - 1)) {
+        case 0: pair_tile<0, 1>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
+        case 1: pair_tile<0, 2>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
+        case 2: pair_tile<1, 1>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
+        case 3: pair_tile<1, 2>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
+        case 4: pair_tile<2, 1>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
+        default: pair_tile<2, 2>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
     }
 }
 
