@@ -17,6 +17,8 @@
 
 namespace qpsb {
 
+std::atomic<uint64_t> g_zgemm_launches{0};  // ncu --launch-skip bookkeeping (QPS_TRACE_LAUNCH)
+
 namespace {
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -322,6 +324,7 @@ void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_
     for (size_t off = 0; off < ntasks; off += 65535) {
         const unsigned cnt = unsigned(std::min<size_t>(65535, ntasks - off));
         kern<<<dim3(tiles_m * tiles_n, cnt), Cfg::NT, Cfg::SMEM, s>>>(M, N, alpha, beta, tasks + off, tiles_m);
+        ++g_zgemm_launches;
     }
 }
 

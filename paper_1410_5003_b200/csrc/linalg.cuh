@@ -6,6 +6,8 @@
 //   LU with partial pivoting + triangular solves for block cyclic reduction
 #pragma once
 
+#include <atomic>
+
 #include "hankel.cuh"
 #include "qps_internal.h"
 
@@ -22,6 +24,7 @@ struct GemmTask {
 };
 
 struct Workspace;  // forward
+extern std::atomic<uint64_t> g_zgemm_launches;
 
 // family: profiling name (string literal); default by shape
 void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,

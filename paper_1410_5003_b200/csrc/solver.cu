@@ -847,6 +847,9 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                 nxt[a].U.push_back(nu);
             }
         }
+        if (lvl == 0 && getenv("QPS_TRACE_LAUNCH"))
+            fprintf(stderr, "level-0 bcr_update is zgemm3m launch index %llu\n",
+                    (unsigned long long)g_zgemm_launches.load());
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, upd, s, c.ws.gemm_tasks, "bcr_update");
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{0, 0}, fresh, s, c.ws.gemm_tasks, "bcr_update");
         zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vtasks, s, c.ws.gemv_tasks);
