@@ -111,13 +111,6 @@ __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, Dev
     const double u0 = 64.0 * ik0 * ik0, u1 = 64.0 * ik1 * ik1;
     const int gt = T.t_off + m;
     const double tx = pool.x[gt], ty = pool.y[gt], tnx = pool.nx[gt], tny = pool.ny[gt];
-    // coincidence threshold of eval_kernels (kernels.hpp:38-39) per shifted target, squared
-    auto thr_of = [&](int t) {
-        const double xx = tx + T.tdx[t];
-        const double th = 1e-13 * (1.0 + sqrt(xx * xx + ty * ty));
-        return th * th;
-    };
-    const double thr2_0 = thr_of(0), thr2_1 = thr_of(1), thr2_2 = thr_of(2);
     bool corrected = true;
     int mseg = 0;
     if (self == 2) {
@@ -145,9 +138,14 @@ __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, Dev
             }
             const double rvx = (tx + T.tdx[t]) - (zx0 + T.sdx[t]), rvy = ty - zy;
             const double r2 = rvx * rvx + rvy * rvy;
-            if (r2 < (t == 0 ? thr2_0 : t == 1 ? thr2_1 : thr2_2)) {
-                atomicOr(err, 1);
-                continue;
+            // coincidence test of eval_kernels (kernels.hpp:38-39), r < 1e-13 (1 + |x|):
+            // the cheap prefilter r^2 < 1e-16 admits every |x| < 1e5
+            if (r2 < 1e-16) {
+                const double xx = tx + T.tdx[t];
+                if (sqrt(r2) < 1e-13 * (1.0 + sqrt(xx * xx + ty * ty))) {
+                    atomicOr(err, 1);
+                    continue;
+                }
             }
             const double inv_r = rsqrt(r2);
             const double r = r2 * inv_r;

@@ -1266,9 +1266,20 @@ __global__ void __launch_bounds__(256) lu_panel_smem_kernel(int n, int ld, cplx*
     __shared__ double shv[32];
     __shared__ int shi[32];
     const int tid = threadIdx.x;
-    for (int e = tid; e < rows * w; e += blockDim.x) {
-        const int i = e % rows, j = e / rows;
-        pnl[j * rows + i] = A[size_t(c0 + j) * ld + c0 + i];
+    // panel load: 8 independent loads in flight per thread (the loop would
+    // otherwise expose one DRAM latency per element)
+    for (int e0 = tid; e0 < rows * w; e0 += 8 * blockDim.x) {
+        cplx v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < rows * w) v[u] = A[size_t(c0 + e / rows) * ld + c0 + e % rows];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < rows * w) pnl[e] = v[u];
+        }
     }
     __syncthreads();
     for (int k = 0; k < w; ++k) {
@@ -1321,9 +1332,13 @@ __global__ void __launch_bounds__(256) lu_panel_smem_kernel(int n, int ld, cplx*
 // interchanges (LAPACK xGETRF order) and, right of the panel, the unit-lower
 // solve U12 = L11^{-1} A12; the trailing update is one batched 3M GEMM.
 constexpr int kRlW = 16;
+// slot map of a panel's interchanges for lu_rl_cols_kernel: slots 0..w-1 are
+// rows k0..k0+w-1, slots 16..31 the distinct external rows touched; map[q] =
+// slot whose original value ends in slot q, map[32 + q - 16] = row of slot q
+constexpr int kRlMap = 48;
 __global__ void __launch_bounds__(256) lu_rl_panel_kernel(int n, int ld, cplx* const* __restrict__ Ap,
                                                           int* const* __restrict__ Pp, int k0, int w,
-                                                          int* singular) {
+                                                          int* singular, int* __restrict__ rl_map) {
     extern __shared__ cplx pnl[];
     cplx* A = Ap[blockIdx.x];
     int* ipiv = Pp[blockIdx.x];
@@ -1332,9 +1347,20 @@ __global__ void __launch_bounds__(256) lu_rl_panel_kernel(int n, int ld, cplx* c
     __shared__ int shi[32];
     __shared__ int spiv[kRlW];
     const int tid = threadIdx.x;
-    for (int e = tid; e < rows * w; e += blockDim.x) {
-        const int i = e % rows, j = e / rows;
-        pnl[j * rows + i] = A[size_t(k0 + j) * ld + k0 + i];
+    // panel load: 8 independent loads in flight per thread (the loop would
+    // otherwise expose one DRAM latency per element)
+    for (int e0 = tid; e0 < rows * w; e0 += 8 * blockDim.x) {
+        cplx v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < rows * w) v[u] = A[size_t(k0 + e / rows) * ld + k0 + e % rows];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < rows * w) pnl[e] = v[u];
+        }
     }
     __syncthreads();
     for (int k = 0; k < w; ++k) {
@@ -1379,36 +1405,15 @@ __global__ void __launch_bounds__(256) lu_rl_panel_kernel(int n, int ld, cplx* c
         const int i = e % rows, j = e / rows;
         A[size_t(k0 + j) * ld + k0 + i] = pnl[j * rows + i];
     }
-
-}
-
-// one warp per column: lanes 0..w-1 hold rows k0..k0+w-1, lanes 16.. the
-// external rows the interchanges touch; the interchange sequence is replayed
-// on lane indices, the values move with one shuffle, the unit-lower solve is
-// a w-step shuffle broadcast.
-__global__ void __launch_bounds__(256) lu_rl_cols_kernel(int n, int ld, cplx* const* __restrict__ Ap,
-                                                         const int* const* __restrict__ Pp, int k0, int w) {
-    cplx* A = Ap[blockIdx.y];
-    const int* ipiv = Pp[blockIdx.y];
-    const int lane = threadIdx.x & 31;
-    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (c >= n - w) return;
-    const int col = c < k0 ? c : c + w;
-    cplx* Ac = A + size_t(col) * ld;
-    // replay the interchanges on positions: pos[] = rows currently at each slot
-    // slots 0..w-1 are rows k0..k0+w-1; extra slots hold distinct external rows
-    int ext_row = -1;  // this lane's external row (lanes >= 16)
-    int src = lane;    // slot whose ORIGINAL value ends in this lane's slot
-    {
-        int rowof[32];
+    if (tid == 0) {  // replay the interchanges on slots once per matrix
+        int rowof[32], perm[32];
         int nslot = kRlW;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) rowof[q] = q < kRlW ? k0 + q : -1;
-        int perm[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) perm[q] = q;
+        for (int q = 0; q < 32; ++q) {
+            rowof[q] = q < kRlW ? k0 + q : -1;
+            perm[q] = q;
+        }
         for (int t = 0; t < w; ++t) {
-            const int p = ipiv[k0 + t];
+            const int p = k0 + spiv[t];
             if (p == k0 + t) continue;
             int sp = -1;
             if (p < k0 + kRlW) sp = p - k0;
@@ -1424,10 +1429,179 @@ __global__ void __launch_bounds__(256) lu_rl_cols_kernel(int n, int ld, cplx* co
             perm[t] = perm[sp];
             perm[sp] = tmp;
         }
-        src = perm[lane];
-        ext_row = lane >= kRlW ? rowof[lane] : -1;
-        if (lane < kRlW && lane >= w) src = lane;
+        int* mp = rl_map + size_t(blockIdx.x) * kRlMap;
+        for (int q = 0; q < 32; ++q) mp[q] = perm[q];
+        for (int q = kRlW; q < 32; ++q) mp[32 + q - kRlW] = rowof[q];
     }
+}
+
+// Panel of <= 16 columns and <= 640 rows factored with partial pivoting in
+// registers: thread i owns row i of the panel (16 complex values), the pivot
+// search is one block argmax, the interchange and the pivot-row broadcast go
+// through a double-buffered shared row, and the rank-1 updates are register
+// FMAs -- three barriers per column instead of a shared-memory sweep.  Used by
+// both LU variants; optionally emits the interchange slot map of
+// lu_rl_cols_kernel.
+constexpr int kRegPanelMaxRows = 640;
+__global__ void __launch_bounds__(kRegPanelMaxRows, 1)
+    lu_panel_reg_kernel(int n, int ld, cplx* const* __restrict__ Ap, int* const* __restrict__ Pp, int c0, int w,
+                        int* singular, int* __restrict__ rl_map) {
+    cplx* A = Ap[blockIdx.x];
+    int* ipiv = Pp[blockIdx.x];
+    const int rows = n - c0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ double shv[32];
+    __shared__ int shi[32];
+    __shared__ int spiv[kRlW];
+    // per step parity: each warp's candidate (|a|^2, row, row values, 1/a) and a copy of row k
+    __shared__ double cval[2][kRegPanelMaxRows / 32];
+    __shared__ int cidx[2][kRegPanelMaxRows / 32];
+    __shared__ cplx crow[2][kRegPanelMaxRows / 32][kRlW + 1];  // [.][warp][cols..., 1/pivot]
+    __shared__ cplx krow[2][kRlW];
+    const bool own = tid < rows;
+    cplx row[kRlW];
+#pragma unroll
+    for (int j = 0; j < kRlW; ++j)
+        row[j] = (own && j < w) ? A[size_t(c0 + j) * ld + c0 + tid] : cplx{0, 0};
+    // unrolled over the columns: row[k] and the select chains below resolve at
+    // compile time and the row stays in registers
+#pragma unroll
+    for (int k = 0; k < kRlW; ++k) {
+        if (k >= w) break;
+        const int par = k & 1;
+        cplx rk = row[0];
+#pragma unroll
+        for (int j = 1; j < kRlW; ++j)
+            if (j == k) rk = row[j];
+        // warp-level argmax (first index among equal moduli, as GEPP)
+        double v = (own && tid >= k) ? cabs2(rk) : -1.0;
+        int idx = (own && tid >= k) ? tid : 1 << 30;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (ov > v || (ov == v && oi < idx)) {
+                v = ov;
+                idx = oi;
+            }
+        }
+        if (tid == idx) {  // this warp's candidate publishes its row and reciprocal
+            cval[par][warp] = v;
+            cidx[par][warp] = idx;
+#pragma unroll
+            for (int j = 0; j < kRlW; ++j) crow[par][warp][j] = row[j];
+            crow[par][warp][kRlW] = (rk.re == 0.0 && rk.im == 0.0) ? cplx{0, 0} : cdiv(cplx{1.0, 0.0}, rk);
+        }
+        if (lane == 0 && idx == (1 << 30)) {
+            cval[par][warp] = -1.0;
+            cidx[par][warp] = 1 << 30;
+        }
+        if (tid == k) {
+#pragma unroll
+            for (int j = 0; j < kRlW; ++j) krow[par][j] = row[j];
+        }
+        __syncthreads();
+        // every warp reduces the candidates (no second barrier)
+        double bv = lane < nw ? cval[par][lane] : -1.0;
+        int bi = lane < nw ? cidx[par][lane] : 1 << 30;
+        int bw = lane;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, bw, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
+                bw = ow;
+            }
+        }
+        const int piv = bi;
+        const cplx* prow = crow[par][bw];
+        if (tid == 0) {
+            ipiv[c0 + k] = c0 + piv;
+            spiv[k] = piv;
+            if (bv == 0.0) singular[blockIdx.x] = 1;
+        }
+        if (piv != k) {  // interchange rows k and piv
+            if (tid == k) {
+#pragma unroll
+                for (int j = 0; j < kRlW; ++j) row[j] = prow[j];
+            } else if (tid == piv) {
+#pragma unroll
+                for (int j = 0; j < kRlW; ++j) row[j] = krow[par][j];
+                rk = krow[par][0];
+#pragma unroll
+                for (int j = 1; j < kRlW; ++j)
+                    if (j == k) rk = krow[par][j];
+            }
+        }
+        const cplx inv = prow[kRlW];
+        const bool zero = (inv.re == 0.0 && inv.im == 0.0);
+        if (own && tid > k) {
+            const cplx l = zero ? rk : cmul(rk, inv);
+#pragma unroll
+            for (int j = 0; j < kRlW; ++j) {
+                if (j == k) row[j] = l;
+                if (j > k) {
+                    const cplx pj = prow[j];
+                    row[j].re -= l.re * pj.re - l.im * pj.im;
+                    row[j].im -= l.re * pj.im + l.im * pj.re;
+                }
+            }
+        }
+    }
+    if (own) {
+#pragma unroll
+        for (int j = 0; j < kRlW; ++j)
+            if (j < w) A[size_t(c0 + j) * ld + c0 + tid] = row[j];
+    }
+    __syncthreads();
+    if (rl_map && tid == 0) {  // replay the interchanges on slots once per matrix
+        int* rowof = shi;  // 32 ints each, free after the last argmax
+        int* perm = reinterpret_cast<int*>(shv);
+        int nslot = kRlW;
+        for (int q = 0; q < 32; ++q) {
+            rowof[q] = q < kRlW ? c0 + q : -1;
+            perm[q] = q;
+        }
+        for (int t = 0; t < w; ++t) {
+            const int p = c0 + spiv[t];
+            if (p == c0 + t) continue;
+            int sp = -1;
+            if (p < c0 + kRlW) sp = p - c0;
+            else {
+                for (int q = kRlW; q < nslot; ++q)
+                    if (rowof[q] == p) sp = q;
+                if (sp < 0) {
+                    sp = nslot++;
+                    rowof[sp] = p;
+                }
+            }
+            const int tmp = perm[t];
+            perm[t] = perm[sp];
+            perm[sp] = tmp;
+        }
+        int* mp = rl_map + size_t(blockIdx.x) * kRlMap;
+        for (int q = 0; q < 32; ++q) mp[q] = perm[q];
+        for (int q = kRlW; q < 32; ++q) mp[32 + q - kRlW] = rowof[q];
+    }
+}
+
+// one warp per column: lanes 0..w-1 hold rows k0..k0+w-1, lanes 16.. the
+// external rows the interchanges touch; the interchange sequence is replayed
+// on lane indices, the values move with one shuffle, the unit-lower solve is
+// a w-step shuffle broadcast.
+__global__ void __launch_bounds__(256) lu_rl_cols_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+                                                         const int* __restrict__ rl_map, int k0, int w) {
+    cplx* A = Ap[blockIdx.y];
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (c >= n - w) return;
+    const int col = c < k0 ? c : c + w;
+    cplx* Ac = A + size_t(col) * ld;
+    const int* mp = rl_map + size_t(blockIdx.y) * kRlMap;
+    int src = mp[lane];
+    const int ext_row = lane >= kRlW ? mp[32 + lane - kRlW] : -1;
+    if (lane < kRlW && lane >= w) src = lane;
     cplx v{0, 0};
     if (lane < w) v = Ac[k0 + lane];
     else if (ext_row >= 0) v = Ac[ext_row];
@@ -1436,15 +1610,18 @@ __global__ void __launch_bounds__(256) lu_rl_cols_kernel(int n, int ld, cplx* co
     nv.im = __shfl_sync(0xffffffffu, v.im, src);
     if (col > k0) {  // U12 = L11^{-1} A12 (unit lower, L11 in the factored panel)
         const cplx* Lp = A + size_t(k0) * ld + k0;
-        for (int u = 0; u + 1 < w; ++u) {
+        cplx lrow[kRlW];  // this lane's row of L11, loaded up front (independent loads)
+#pragma unroll
+        for (int u = 0; u < kRlW; ++u) lrow[u] = (u < lane && lane < w) ? Lp[size_t(u) * ld + lane] : cplx{0, 0};
+#pragma unroll
+        for (int u = 0; u + 1 < kRlW; ++u) {
+            if (u + 1 >= w) break;
             cplx ru;
             ru.re = __shfl_sync(0xffffffffu, nv.re, u);
             ru.im = __shfl_sync(0xffffffffu, nv.im, u);
-            if (lane > u && lane < w) {
-                const cplx l = Lp[size_t(u) * ld + lane];
-                nv.re -= l.re * ru.re - l.im * ru.im;
-                nv.im -= l.re * ru.im + l.im * ru.re;
-            }
+            const cplx l = lrow[u];
+            nv.re -= l.re * ru.re - l.im * ru.im;
+            nv.im -= l.re * ru.im + l.im * ru.re;
         }
     }
     if (lane < w) Ac[k0 + lane] = nv;
@@ -1796,7 +1973,10 @@ void lu_rec(LuCtx& L, int c0, int nc) {
     const int leaf = smem_leaf ? kLeaf : kNB;
     if (nc <= leaf) {
         ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(L.n - c0) * nc * nc / 2.0);
-        if (smem_leaf) {
+        if (nc <= kRlW && L.n - c0 <= kRegPanelMaxRows) {
+            lu_panel_reg_kernel<<<L.count, ((L.n - c0 + 31) / 32) * 32, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc,
+                                                                                 L.sing, nullptr);
+        } else if (smem_leaf) {
             static bool attr = false;
             if (!attr) {
                 QPS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1837,17 +2017,22 @@ void lu_rl(LuCtx& L) {
         QPS_CUDA(cudaFuncSetAttribute(lu_rl_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
+    L.ws.rl_map.ensure(size_t(L.count) * kRlMap);
     for (int k0 = 0; k0 < n; k0 += kRlW) {
         const int w = std::min(kRlW, n - k0);
         {
             ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(n - k0) * w * w / 2.0);
-            lu_rl_panel_kernel<<<L.count, 256, size_t(n - k0) * w * sizeof(cplx), L.s>>>(n, L.ld, L.dA, L.dP, k0, w,
-                                                                                         L.sing);
+            if (n - k0 <= kRegPanelMaxRows)
+                lu_panel_reg_kernel<<<L.count, ((n - k0 + 31) / 32) * 32, 0, L.s>>>(n, L.ld, L.dA, L.dP, k0, w, L.sing,
+                                                                                   L.ws.rl_map.p);
+            else
+                lu_rl_panel_kernel<<<L.count, 256, size_t(n - k0) * w * sizeof(cplx), L.s>>>(n, L.ld, L.dA, L.dP, k0,
+                                                                                             w, L.sing, L.ws.rl_map.p);
             QPS_CUDA(cudaGetLastError());
         }
         if (n > w) {
             ProfScope ps("lu_swap", L.s, 0.0);
-            lu_rl_cols_kernel<<<dim3((n - w + 7) / 8, L.count), 256, 0, L.s>>>(n, L.ld, L.dA, L.dP, k0, w);
+            lu_rl_cols_kernel<<<dim3((n - w + 7) / 8, L.count), 256, 0, L.s>>>(n, L.ld, L.dA, L.ws.rl_map.p, k0, w);
             QPS_CUDA(cudaGetLastError());
         }
         const int m = n - k0 - w;

@@ -99,6 +99,7 @@ struct Workspace {
     DBuf<GemvTask> gemv_tasks;
     DBuf<cplx*> ptrs, ptrs2, ptrs3;
     DBuf<int*> iptrs;
+    DBuf<int> rl_map;  // right-looking LU: per matrix, the interchange map of the current panel
     std::vector<GemmTask> h_gemm;
 };
 
