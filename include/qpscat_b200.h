@@ -164,6 +164,17 @@ int qps_get_solution(const qps_ctx* ctx, qps_cplx* eta, qps_cplx* c, qps_cplx* a
 int qps_reflection_transmission(const qps_ctx* ctx, double* R, double* T, double* flux_error, double* kappa,
                                 qps_cplx* kU, qps_cplx* kD, int* prop_up, int* prop_down);
 
+/* ------------------------------------------------------ field evaluation */
+/* evaluate_field(sol, p, points), postprocess.hpp:78-123, for the last solve:
+ * xy[2n] interleaved points (any cell: x is mapped into the central cell and
+ * the result phased by alpha^m).  Outputs (NULL skipped): scattered and total
+ * field [n], region [n] (0 above y_U, 1 inside a layer, 2 below y_D) and the
+ * 0-based layer [n].  GeometryError when a point lies on an interface
+ * (classify_point, postprocess.hpp:27-39).  Plain Nystrom sums as the
+ * reference (no close-evaluation correction). */
+int qps_evaluate_field(qps_ctx* ctx, int n_points, const double* xy, qps_cplx* u_scattered, qps_cplx* u_total,
+                       int* region, int* layer);
+
 /* --------------------------------------------------------- angle sweep */
 /* Multi-angle sweep (building blocks assembly.hpp:85-155,
  * periodize.hpp:58-126): the alpha-free cache is filled once and every angle

@@ -387,6 +387,22 @@ int qps_sweep(qps_ctx* c, int n, const double* theta, int K, int mode, double* R
     });
 }
 
+int qps_evaluate_field(qps_ctx* c, int n, const double* xy, qps_cplx* u_scat, qps_cplx* u_tot, int* region,
+                       int* layer) {
+    return guarded(c, [&] {
+        need(c->sol.has_value(), "no solution (solve first)");
+        std::vector<Vec2> pts(n);
+        for (int i = 0; i < n; ++i) pts[i] = Vec2{xy[2 * i], xy[2 * i + 1]};
+        const std::vector<FieldSample> fs = evaluate_field(*c->sol, c->prob, pts);
+        for (int i = 0; i < n; ++i) {
+            if (u_scat) u_scat[i] = {fs[i].u_scattered.real(), fs[i].u_scattered.imag()};
+            if (u_tot) u_tot[i] = {fs[i].u_total.real(), fs[i].u_total.imag()};
+            if (region) region[i] = fs[i].region == Region::AboveU ? 0 : fs[i].region == Region::Layer ? 1 : 2;
+            if (layer) layer[i] = fs[i].layer;
+        }
+    });
+}
+
 int qps_download_block(const qps_ctx* c, int kind, int i, qps_cplx* out, int* rows, int* cols) {
     return guarded(const_cast<qps_ctx*>(c), [&] {
         if (kind < 32) {

@@ -413,6 +413,16 @@ int qps_sweep(qps_ctx* h, int n, const double* theta, int K, int mode, double* R
     });
 }
 
+int qps_evaluate_field(qps_ctx* h, int n, const double* xy, qps_cplx* u_scat, qps_cplx* u_tot, int* region,
+                       int* layer) {
+    return guarded(h, [&](Ctx& c) {
+        need_device(c);
+        need(c.have_sol, "no solution (solve first)");
+        need(n >= 0 && (n == 0 || xy != nullptr), "evaluate_field: bad point list");
+        evaluate_field(c, n, xy, reinterpret_cast<cplx*>(u_scat), reinterpret_cast<cplx*>(u_tot), region, layer);
+    });
+}
+
 int qps_download_block(const qps_ctx* hh, int kind, int i, qps_cplx* out, int* rows, int* cols) {
     return guarded(const_cast<qps_ctx*>(hh), [&](Ctx& c) {
         need_device(c);

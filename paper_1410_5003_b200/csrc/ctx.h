@@ -87,6 +87,17 @@ struct BandTask {
     int ld;
 };
 
+// evaluate_field: one layer's sources and its range of the sorted point list
+struct FieldTask {
+    double k;
+    int nsrc;               // interfaces bounding the layer (0..2)
+    int s_off[2], ns[2];    // pool offsets / node counts
+    const cplx* tau[2];     // densities [tau; sigma] of those interfaces
+    int p_off, P;           // layer proxies
+    const cplx* c;          // proxy coefficients c_layer
+    int pt0, npt;           // this layer's range of the sorted point list
+};
+
 // One block-tridiagonal system stored as pointer lists (block cyclic reduction)
 struct BcrLevel {
     std::vector<int> idx;                 // original block index per active position
@@ -128,6 +139,11 @@ struct Ctx {
     DBuf<BandTask> d_band;
     DBuf<int> d_nodes2;
     DBuf<cplx> wtmp;  // staging of the radiation W blocks
+    // ---- field evaluation ----
+    DBuf<cplx> field_c, field_out;
+    DBuf<double> field_qx, field_qy;
+    DBuf<FieldTask> field_tasks;
+    DBuf<int2> field_tiles;
 
     // ---- assembled system (BlockSystem, assembly.hpp:293-315) ----
     Dims dims;
@@ -199,6 +215,9 @@ void pad_identity(Ctx& c);
 void cache_fill(Ctx& c);
 // assemble_system (assembly.hpp:462-483) for dims.nsys angles from the cache
 void assemble_from_cache(Ctx& c, const std::vector<Problem>& probs);
+// evaluate_field (postprocess.hpp:78-123) for the last solution; region 0 above
+// y_U, 1 inside a layer, 2 below y_D
+void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, int* region, int* layer);
 // multi-angle sweep; mode 0 accelerated (cache once, angles batched), 1 independent
 void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe, cplx* aU,
                cplx* aD, int* status);

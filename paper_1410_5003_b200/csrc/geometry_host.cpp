@@ -374,4 +374,48 @@ uint64_t reference_fill_evals(const HostGeometry& g) {
     return c;
 }
 
+// classify_point (postprocess.hpp:27-39).  The reference scans the interfaces
+// top to bottom and returns the first one the point lies above; for a stack
+// whose interfaces are ordered at this x (y_0(x) > y_1(x) > ...) the same
+// answer comes from a binary search, checked against the scan's conditions
+// at the boundary (and the scan itself is used where the order fails).
+int classify_point(const StackDesc& st, const HostGeometry& g, double x, double y, int* layer) {
+    if (y >= g.y_U) {
+        *layer = 0;
+        return 0;
+    }
+    if (y <= g.y_D) {
+        *layer = g.I;
+        return 2;
+    }
+    const int I = g.I;
+    auto yj = [&](int j) { return spec_y_of_x(st.ifaces[j], st.d, x); };
+    auto scan = [&]() {
+        for (int j = 0; j < I; ++j) {
+            const double v = yj(j);
+            if (std::abs(y - v) < 1e-12 * st.d)
+                fail(QPS_ERR_GEOMETRY, "field point lies on interface " + std::to_string(j + 1));
+            if (y > v) return j;
+        }
+        return I;
+    };
+    int lo = 0, hi = I;  // first j in [lo, hi) with y > y_j(x), assuming decreasing y_j
+    while (lo < hi) {
+        const int mid = (lo + hi) / 2;
+        if (y > yj(mid)) hi = mid;
+        else lo = mid + 1;
+    }
+    // the scan's view: every j < lo has y <= y_j (and not within tolerance), lo has y > y_lo
+    bool ok = true;
+    for (int j = std::max(0, lo - 2); j < std::min(I, lo + 2) && ok; ++j) {
+        const double v = yj(j);
+        if (std::abs(y - v) < 1e-12 * st.d) ok = false;  // let the scan raise in reference order
+        else if (j < lo && y > v) ok = false;
+        else if (j == lo && !(y > v)) ok = false;
+    }
+    if (ok && lo >= 2) ok = yj(lo - 2) > yj(lo - 1);  // locally ordered
+    *layer = ok ? lo : scan();
+    return 1;
+}
+
 }  // namespace qpsb

@@ -162,6 +162,9 @@ struct Problem {
 Problem make_problem(const StackDesc& st, const HostGeometry& g, double omega, double theta, int K);
 int choose_rb_order(const StackDesc& st, const HostGeometry& g, double omega, double theta);
 
+// classify_point (postprocess.hpp:27-39): region 0 above y_U, 1 layer, 2 below y_D
+int classify_point(const StackDesc& st, const HostGeometry& g, double x, double y, int* layer);
+
 // reference fill count, ShiftBlockCache::fill_evals (assembly.hpp:285)
 uint64_t reference_fill_evals(const HostGeometry& g);
 

@@ -185,6 +185,7 @@ def _bind(lib):
         "qps_get_solution": (C.c_int, [vp, vp, vp, vp, vp, P(C.c_double), P(C.c_double)]),
         "qps_reflection_transmission": (C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_double),
                                                   P(C.c_double), vp, vp, P(C.c_int), P(C.c_int)]),
+        "qps_evaluate_field": (C.c_int, [vp, C.c_int, P(C.c_double), vp, vp, P(C.c_int), P(C.c_int)]),
         "qps_sweep": (C.c_int, [vp, C.c_int, P(C.c_double), C.c_int, C.c_int, P(C.c_double), P(C.c_double),
                                 P(C.c_double), vp, vp, P(C.c_int)]),
         "qps_download_block": (C.c_int, [vp, C.c_int, C.c_int, vp, P(C.c_int), P(C.c_int)]),
@@ -420,6 +421,21 @@ class Solver:
         self._check(self.lib.qps_sweep(self.h, n, _dptr(th), K, mode, _dptr(R), _dptr(T), _dptr(fe),
                                        aU.ctypes.data, aD.ctypes.data, st.ctypes.data_as(C.POINTER(C.c_int))))
         return {"R": R, "T": T, "flux_error": fe, "aU": aU, "aD": aD, "status": st}
+
+    def evaluate_field(self, points):
+        """evaluate_field(sol, p, points) (postprocess.hpp:78-123) for the last
+        solve: points (n, 2) -> dict(u_scattered, u_total, region, layer);
+        region 0 above y_U, 1 inside a layer, 2 below y_D."""
+        xy = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 2))
+        n = len(xy)
+        us = np.zeros(n, dtype=np.complex128)
+        ut = np.zeros(n, dtype=np.complex128)
+        reg = np.zeros(n, dtype=np.int32)
+        lay = np.zeros(n, dtype=np.int32)
+        ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+        self._check(self.lib.qps_evaluate_field(self.h, n, _dptr(xy), us.ctypes.data, ut.ctypes.data, ip(reg),
+                                                ip(lay)))
+        return {"u_scattered": us, "u_total": ut, "region": reg, "layer": lay}
 
     def download_block(self, name: str, i: int = 0):
         kind = BLOCKS[name]
