@@ -13,7 +13,9 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <exception>
 #include <limits>
+#include <thread>
 
 #include "qps_internal.h"
 
@@ -247,7 +249,36 @@ HostGeometry build_geometry(const StackDesc& st, const Numerics& num) {
     g.Mw = num.Mw;
     g.M = num.M;
     g.R = num.R;
-    for (const auto& sp : st.ifaces) g.ifaces.push_back(build_interface(sp, st.d, g.fourier_pool));
+    // interfaces are independent: built on host threads, each with its own
+    // Fourier coefficient pool (concatenated afterwards in interface order);
+    // the first failing interface (in order) raises, as the sequential reference
+    {
+        std::vector<HostInterface> ifs(I);
+        std::vector<std::vector<double>> pools(I);
+        std::vector<std::exception_ptr> errs(I);
+        const int nt = std::max(1, std::min<int>(I, std::min(16u, std::max(1u, std::thread::hardware_concurrency()))));
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                for (int j = t; j < I; j += nt) {
+                    try {
+                        ifs[j] = build_interface(st.ifaces[j], st.d, pools[j]);
+                    } catch (...) {
+                        errs[j] = std::current_exception();
+                    }
+                }
+            });
+        for (auto& x : th) x.join();
+        for (int j = 0; j < I; ++j)
+            if (errs[j]) std::rethrow_exception(errs[j]);
+        for (int j = 0; j < I; ++j) {
+            const int base = int(g.fourier_pool.size());
+            for (auto& sd : ifs[j].segs)
+                if (sd.kind == SEG_FOURIER) sd.coef_off += base;
+            g.fourier_pool.insert(g.fourier_pool.end(), pools[j].begin(), pools[j].end());
+            g.ifaces.push_back(std::move(ifs[j]));
+        }
+    }
     // build_frame (:449-478)
     g.y_U = g.ifaces.front().y_max + num.clearance * st.d;
     g.y_D = g.ifaces.back().y_min - num.clearance * st.d;
