@@ -42,6 +42,25 @@ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
 }
 __device__ __forceinline__ double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
 
+// FP64 division costs ~600 cycles of latency on B200: reciprocals on latency-
+// critical paths use an FP32 seed and two Newton steps (~1 ulp), falling back
+// to division outside the FP32 exponent range.
+__device__ __forceinline__ double fast_rcp(double x) {
+    const double ax = fabs(x);
+    if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;
+    double r = double(__frcp_rn(float(x)));
+    r = fma(r, fma(-x, r, 1.0), r);
+    r = fma(r, fma(-x, r, 1.0), r);
+    return r;
+}
+// 1 / d for complex d != 0 (|d|^2 in range)
+__device__ __forceinline__ cplx fast_cinv(cplx d) {
+    const double n2 = d.re * d.re + d.im * d.im;
+    if (!(n2 > 1e-280 && n2 < 1e280)) return cdiv(cplx{1.0, 0.0}, d);
+    const double r = fast_rcp(n2);
+    return cplx{d.re * r, -d.im * r};
+}
+
 constexpr int BM = 64, BN = 64, BK = 8, LDS = 72;
 
 __global__ void __launch_bounds__(128, 2) zgemm_kernel(int M, int N, cplx alpha, cplx beta,
@@ -1489,7 +1508,7 @@ __global__ void __launch_bounds__(kRegPanelMaxRows, 1)
             cidx[par][warp] = idx;
 #pragma unroll
             for (int j = 0; j < kRlW; ++j) crow[par][warp][j] = row[j];
-            crow[par][warp][kRlW] = (rk.re == 0.0 && rk.im == 0.0) ? cplx{0, 0} : cdiv(cplx{1.0, 0.0}, rk);
+            crow[par][warp][kRlW] = (rk.re == 0.0 && rk.im == 0.0) ? cplx{0, 0} : fast_cinv(rk);
         }
         if (lane == 0 && idx == (1 << 30)) {
             cval[par][warp] = -1.0;
@@ -1557,6 +1576,144 @@ __global__ void __launch_bounds__(kRegPanelMaxRows, 1)
     __syncthreads();
     if (rl_map && tid == 0) {  // replay the interchanges on slots once per matrix
         int* rowof = shi;  // 32 ints each, free after the last argmax
+        int* perm = reinterpret_cast<int*>(shv);
+        int nslot = kRlW;
+        for (int q = 0; q < 32; ++q) {
+            rowof[q] = q < kRlW ? c0 + q : -1;
+            perm[q] = q;
+        }
+        for (int t = 0; t < w; ++t) {
+            const int p = c0 + spiv[t];
+            if (p == c0 + t) continue;
+            int sp = -1;
+            if (p < c0 + kRlW) sp = p - c0;
+            else {
+                for (int q = kRlW; q < nslot; ++q)
+                    if (rowof[q] == p) sp = q;
+                if (sp < 0) {
+                    sp = nslot++;
+                    rowof[sp] = p;
+                }
+            }
+            const int tmp = perm[t];
+            perm[t] = perm[sp];
+            perm[sp] = tmp;
+        }
+        int* mp = rl_map + size_t(blockIdx.x) * kRlMap;
+        for (int q = 0; q < 32; ++q) mp[q] = perm[q];
+        for (int q = kRlW; q < 32; ++q) mp[32 + q - kRlW] = rowof[q];
+    }
+}
+
+// Same factorization with the panel in shared memory ([column][row], one
+// thread per row, rolled column loop): no register arrays, so no spills and a
+// small loop body that stays in the instruction cache; one barrier per column
+// (each warp publishes its candidate pivot row, every warp reduces the
+// candidates itself).
+__global__ void __launch_bounds__(kRegPanelMaxRows, 1)
+    lu_panel_sm2_kernel(int n, int ld, cplx* const* __restrict__ Ap, int* const* __restrict__ Pp, int c0, int w,
+                        int* singular, int* __restrict__ rl_map) {
+    extern __shared__ cplx pnl2[];  // [w][rows]
+    cplx* A = Ap[blockIdx.x];
+    int* ipiv = Pp[blockIdx.x];
+    const int rows = n - c0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ double shv[32];
+    __shared__ int shi[32];
+    __shared__ int spiv[kRlW];
+    __shared__ double cval[2][kRegPanelMaxRows / 32];
+    __shared__ int cidx[2][kRegPanelMaxRows / 32];
+    __shared__ cplx crow[2][kRegPanelMaxRows / 32][kRlW + 1];
+    __shared__ cplx krow[2][kRlW];
+    const bool own = tid < rows;
+    if (own) {  // 16 independent loads in flight per thread
+        cplx v[kRlW];
+#pragma unroll
+        for (int j = 0; j < kRlW; ++j)
+            if (j < w) v[j] = A[size_t(c0 + j) * ld + c0 + tid];
+#pragma unroll
+        for (int j = 0; j < kRlW; ++j)
+            if (j < w) pnl2[j * rows + tid] = v[j];
+    }
+    __syncthreads();
+    for (int k = 0; k < w; ++k) {
+        const int par = k & 1;
+        const cplx rk = own ? pnl2[k * rows + tid] : cplx{0, 0};
+        double v = (own && tid >= k) ? cabs2(rk) : -1.0;
+        int idx = (own && tid >= k) ? tid : 1 << 30;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (ov > v || (ov == v && oi < idx)) {
+                v = ov;
+                idx = oi;
+            }
+        }
+        if (idx != (1 << 30)) {  // the warp publishes its candidate row cooperatively
+            if (lane < w) crow[par][warp][lane] = pnl2[lane * rows + idx];
+            if (tid == idx) {
+                cval[par][warp] = v;
+                cidx[par][warp] = idx;
+                crow[par][warp][kRlW] = (rk.re == 0.0 && rk.im == 0.0) ? cplx{0, 0} : fast_cinv(rk);
+            }
+        } else if (lane == 0) {
+            cval[par][warp] = -1.0;
+            cidx[par][warp] = 1 << 30;
+        }
+        if (warp == (k >> 5) && lane < w) krow[par][lane] = pnl2[lane * rows + k];
+        __syncthreads();
+        double bv = lane < nw ? cval[par][lane] : -1.0;
+        int bi = lane < nw ? cidx[par][lane] : 1 << 30;
+        int bw = lane;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, bw, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
+                bw = ow;
+            }
+        }
+        const int piv = bi;
+        const cplx* prow = crow[par][bw];
+        if (tid == 0) {
+            ipiv[c0 + k] = c0 + piv;
+            spiv[k] = piv;
+            if (bv == 0.0) singular[blockIdx.x] = 1;
+        }
+        cplx ak = rk;  // this thread's entry in column k after the interchange
+        if (piv != k) {  // rows k and piv written by their warps' lanes (one column per lane)
+            if (warp == (k >> 5) && lane < w) pnl2[lane * rows + k] = prow[lane];
+            if (warp == (piv >> 5) && lane < w) pnl2[lane * rows + piv] = krow[par][lane];
+            if (tid == piv) ak = krow[par][k];
+            __syncwarp();
+        }
+        const cplx inv = prow[kRlW];
+        const bool zero = (inv.re == 0.0 && inv.im == 0.0);
+        if (own && tid > k) {
+            const cplx l = zero ? ak : cmul(ak, inv);
+            pnl2[k * rows + tid] = l;
+#pragma unroll
+            for (int j = 1; j < kRlW; ++j) {  // predicated, independent read-modify-writes
+                if (j > k && j < w) {
+                    const cplx pj = prow[j];
+                    cplx a = pnl2[j * rows + tid];
+                    a.re -= l.re * pj.re - l.im * pj.im;
+                    a.im -= l.re * pj.im + l.im * pj.re;
+                    pnl2[j * rows + tid] = a;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (own) {
+#pragma unroll
+        for (int j = 0; j < kRlW; ++j)
+            if (j < w) A[size_t(c0 + j) * ld + c0 + tid] = pnl2[j * rows + tid];
+    }
+    if (rl_map && tid == 0) {  // replay the interchanges on slots once per matrix
+        int* rowof = shi;
         int* perm = reinterpret_cast<int*>(shv);
         int nslot = kRlW;
         for (int q = 0; q < 32; ++q) {
@@ -1884,6 +2041,29 @@ void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, 
 
 namespace {
 
+// 16-column panel factorization, <= 640 rows: shared-memory kernel (default)
+// or the register-resident one (QPS_PANEL=reg)
+void launch_panel_fast(int n, int ld, cplx* const* dA, int* const* dP, int c0, int w, int* sing, int* rl_map,
+                       int count, cudaStream_t s) {
+    static const bool reg = [] {
+        const char* e = getenv("QPS_PANEL");
+        return e && !strcmp(e, "reg");
+    }();
+    const int threads = ((n - c0 + 31) / 32) * 32;
+    if (reg) {
+        lu_panel_reg_kernel<<<count, threads, 0, s>>>(n, ld, dA, dP, c0, w, sing, rl_map);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(lu_panel_sm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(size_t(kRegPanelMaxRows) * kRlW * sizeof(cplx))));
+            attr = true;
+        }
+        lu_panel_sm2_kernel<<<count, threads, size_t(n - c0) * w * sizeof(cplx), s>>>(n, ld, dA, dP, c0, w, sing,
+                                                                                      rl_map);
+    }
+}
+
 DBuf<int> g_perm;  // per-matrix permutation scratch
 
 void launch_row_permute(int n, int ld, cplx* const* dA, const int* const* dP, int count, int k0, int kend, int c0,
@@ -1974,8 +2154,7 @@ void lu_rec(LuCtx& L, int c0, int nc) {
     if (nc <= leaf) {
         ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(L.n - c0) * nc * nc / 2.0);
         if (nc <= kRlW && L.n - c0 <= kRegPanelMaxRows) {
-            lu_panel_reg_kernel<<<L.count, ((L.n - c0 + 31) / 32) * 32, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc,
-                                                                                 L.sing, nullptr);
+            launch_panel_fast(L.n, L.ld, L.dA, L.dP, c0, nc, L.sing, nullptr, L.count, L.s);
         } else if (smem_leaf) {
             static bool attr = false;
             if (!attr) {
@@ -2023,8 +2202,7 @@ void lu_rl(LuCtx& L) {
         {
             ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(n - k0) * w * w / 2.0);
             if (n - k0 <= kRegPanelMaxRows)
-                lu_panel_reg_kernel<<<L.count, ((n - k0 + 31) / 32) * 32, 0, L.s>>>(n, L.ld, L.dA, L.dP, k0, w, L.sing,
-                                                                                   L.ws.rl_map.p);
+                launch_panel_fast(n, L.ld, L.dA, L.dP, k0, w, L.sing, L.ws.rl_map.p, L.count, L.s);
             else
                 lu_rl_panel_kernel<<<L.count, 256, size_t(n - k0) * w * sizeof(cplx), L.s>>>(n, L.ld, L.dA, L.dP, k0,
                                                                                              w, L.sing, L.ws.rl_map.p);
