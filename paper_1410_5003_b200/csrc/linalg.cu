@@ -958,6 +958,7 @@ __global__ void __launch_bounds__(256) cod_trsm_chunk_kernel(CodBatch b, cplx* B
     const cplx* V = b.V + size_t(pb) * m * b.p;
     cplx* T = tch;           // r x r (ld r)
     cplx* X = tch + r * r;   // r x kTrsmCols (ld r)
+    cplx* Tinv = X + r * kTrsmCols;  // r reciprocals of the diagonal
     const int c0 = blockIdx.x * kTrsmCols;
     const int nc = min(kTrsmCols, ncols - c0);
     cplx* Bp = B + stride * pb + size_t(c0) * ldb;
@@ -969,6 +970,9 @@ __global__ void __launch_bounds__(256) cod_trsm_chunk_kernel(CodBatch b, cplx* B
         const int i = e % r, j = e / r;
         X[j * r + i] = Bp[size_t(j) * ldb + i];
     }
+    __syncthreads();
+    // reciprocals up front: an FP64 division on the substitution chain costs ~600 cycles per row
+    for (int i = threadIdx.x; i < r; i += blockDim.x) Tinv[i] = cdiv(cplx{1.0, 0.0}, T[i * r + i]);
     __syncthreads();
     const int col = threadIdx.x >> 2, part = threadIdx.x & 3;
     const bool active = col < nc;
@@ -986,7 +990,7 @@ __global__ void __launch_bounds__(256) cod_trsm_chunk_kernel(CodBatch b, cplx* B
         sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
         if (active && part == 0) {
             const cplx bi = X[col * r + i];
-            X[col * r + i] = cdiv(cplx{bi.re - sacc.re, bi.im - sacc.im}, T[i * r + i]);
+            X[col * r + i] = cmul(cplx{bi.re - sacc.re, bi.im - sacc.im}, Tinv[i]);
         }
         __syncwarp();
     }
@@ -1203,6 +1207,14 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
         __syncthreads();
     }
     if (mode & 2) {
+        // reciprocals of the diagonal, all at once (an FP64 division on the
+        // substitution's critical path costs ~600 cycles per row)
+        cplx* Dinv = T + bs * bs + bs * bs;  // bs entries after X
+        for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+            const cplx d = T[i * bs + i];
+            Dinv[i] = (i < sz && !(d.re == 0.0 && d.im == 0.0)) ? cdiv(cplx{1.0, 0.0}, d) : cplx{0, 0};
+        }
+        __syncthreads();
         for (int i = bs - 1; i >= 0; --i) {
             cplx sacc{0, 0};
             if (active && i < j)
@@ -1219,8 +1231,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
                 cplx v{0, 0};
                 if (i < sz && j < sz && i <= j) {
                     const cplx num{(i == j ? 1.0 : 0.0) - sacc.re, -sacc.im};
-                    const cplx d = T[i * bs + i];
-                    v = (d.re == 0.0 && d.im == 0.0) ? cplx{0, 0} : cdiv(num, d);
+                    v = cmul(num, Dinv[i]);
                 } else if (i == j) {
                     v = cplx{1, 0};
                 }
@@ -1996,7 +2007,7 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
     ProfScope ps("cod_trsm", s, 4.0 * b.count * double(b.p) * b.p * ncols);
     const size_t sh = size_t(b.p) * b.p * sizeof(cplx);
     const dim3 grid((ncols + 127) / 128, b.count);
-    const size_t shc = (size_t(b.p) * b.p + size_t(b.p) * kTrsmCols) * sizeof(cplx);
+    const size_t shc = (size_t(b.p) * b.p + size_t(b.p) * kTrsmCols + b.p) * sizeof(cplx);
     if (shc <= 200 * 1024) {
         static bool attr = false;
         if (!attr) {
@@ -2026,11 +2037,11 @@ size_t lu_dinv_elems(int n) { return size_t(2) * ((n + kTB - 1) / kTB) * kTB * k
 namespace {
 void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, int bs, int k0_first, int nblk,
                     int mode, cudaStream_t s) {
-    const size_t sh = 2 * size_t(bs) * bs * sizeof(cplx);
+    const size_t sh = (2 * size_t(bs) * bs + bs) * sizeof(cplx);
     static bool attr = false;
     if (!attr) {
         QPS_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(2 * kTB * kTB * sizeof(cplx))));
+                                      int((2 * kTB * kTB + kTB) * sizeof(cplx))));
         attr = true;
     }
     ProfScope ps("tri_inv", s, 8.0 / 3.0 * count * nblk * double(bs) * bs * bs * ((mode == 3) ? 2 : 1));
