@@ -1090,79 +1090,9 @@ __global__ void __launch_bounds__(256) lu_panel_kernel(int n, int ld, cplx* cons
     }
 }
 
-// apply the interchanges of rows k0..kend-1 to columns outside [c_skip0, c_skip1)
-__global__ void lu_swap_kernel(int n, int ld, cplx* const* __restrict__ Ap, const int* const* __restrict__ Pp,
-                               int k0, int kend, int ncols, int c_skip0, int c_skip1) {
-    cplx* A = Ap[blockIdx.y];
-    const int* ipiv = Pp[blockIdx.y];
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncols || (c >= c_skip0 && c < c_skip1)) return;
-    cplx* col = A + size_t(c) * ld;
-    for (int k = k0; k < kend; ++k) {
-        const int p = ipiv[k];
-        if (p != k) {
-            const cplx t = col[k];
-            col[k] = col[p];
-            col[p] = t;
-        }
-    }
-}
 
-// apply the interchanges of rows k0..kend-1 to columns [c0, c1)
-__global__ void lu_swap_range_kernel(int ld, cplx* const* __restrict__ Ap, const int* const* __restrict__ Pp, int k0,
-                                     int kend, int c0, int c1) {
-    cplx* A = Ap[blockIdx.y];
-    const int* ipiv = Pp[blockIdx.y];
-    const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= c1) return;
-    cplx* col = A + size_t(c) * ld;
-    for (int k = k0; k < kend; ++k) {
-        const int p = ipiv[k];
-        if (p != k) {
-            const cplx t = col[k];
-            col[k] = col[p];
-            col[p] = t;
-        }
-    }
-}
 
-// rows r0..r1-1 of B_b <- L11^{-1} (unit lower, diagonal block of A_b) B, columns c0..c0+nc-1
-__global__ void trsm_lower_unit_kernel(int ld, const cplx* const* __restrict__ Ap, cplx* const* __restrict__ Bp,
-                                       int ldb, int r0, int r1, int c0, int nc) {
-    const cplx* A = Ap[blockIdx.y];
-    cplx* B = Bp[blockIdx.y];
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
-    cplx* x = B + size_t(c0 + c) * ldb;
-    for (int i = r0; i < r1; ++i) {
-        cplx s = x[i];
-        for (int l = r0; l < i; ++l) {
-            const cplx t = cmul(A[size_t(l) * ld + i], x[l]);
-            s.re -= t.re;
-            s.im -= t.im;
-        }
-        x[i] = s;
-    }
-}
 
-// rows r0..r1-1 of B_b <- U11^{-1} B (upper, non-unit)
-__global__ void trsm_upper_kernel(int ld, const cplx* const* __restrict__ Ap, cplx* const* __restrict__ Bp, int ldb,
-                                  int r0, int r1, int nc) {
-    const cplx* A = Ap[blockIdx.y];
-    cplx* B = Bp[blockIdx.y];
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
-    cplx* x = B + size_t(c) * ldb;
-    for (int i = r1 - 1; i >= r0; --i) {
-        cplx s = x[i];
-        for (int l = i + 1; l < r1; ++l) {
-            const cplx t = cmul(A[size_t(l) * ld + i], x[l]);
-            s.re -= t.re;
-            s.im -= t.im;
-        }
-        x[i] = cdiv(s, A[size_t(i) * ld + i]);
-    }
-}
 
 // Inverse of the bs x bs diagonal blocks of a factored LU (unit-lower L and/or
 // upper U), one CTA per (block, matrix).  4 lanes per column (bs = 64 -> 256
@@ -1465,156 +1395,7 @@ __global__ void __launch_bounds__(256) lu_rl_panel_kernel(int n, int ld, cplx* c
     }
 }
 
-// Panel of <= 16 columns and <= 640 rows factored with partial pivoting in
-// registers: thread i owns row i of the panel (16 complex values), the pivot
-// search is one block argmax, the interchange and the pivot-row broadcast go
-// through a double-buffered shared row, and the rank-1 updates are register
-// FMAs -- three barriers per column instead of a shared-memory sweep.  Used by
-// both LU variants; optionally emits the interchange slot map of
-// lu_rl_cols_kernel.
-constexpr int kRegPanelMaxRows = 640;
-__global__ void __launch_bounds__(kRegPanelMaxRows, 1)
-    lu_panel_reg_kernel(int n, int ld, cplx* const* __restrict__ Ap, int* const* __restrict__ Pp, int c0, int w,
-                        int* singular, int* __restrict__ rl_map) {
-    cplx* A = Ap[blockIdx.x];
-    int* ipiv = Pp[blockIdx.x];
-    const int rows = n - c0;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    __shared__ double shv[32];
-    __shared__ int shi[32];
-    __shared__ int spiv[kRlW];
-    // per step parity: each warp's candidate (|a|^2, row, row values, 1/a) and a copy of row k
-    __shared__ double cval[2][kRegPanelMaxRows / 32];
-    __shared__ int cidx[2][kRegPanelMaxRows / 32];
-    __shared__ cplx crow[2][kRegPanelMaxRows / 32][kRlW + 1];  // [.][warp][cols..., 1/pivot]
-    __shared__ cplx krow[2][kRlW];
-    const bool own = tid < rows;
-    cplx row[kRlW];
-#pragma unroll
-    for (int j = 0; j < kRlW; ++j)
-        row[j] = (own && j < w) ? A[size_t(c0 + j) * ld + c0 + tid] : cplx{0, 0};
-    // unrolled over the columns: row[k] and the select chains below resolve at
-    // compile time and the row stays in registers
-#pragma unroll
-    for (int k = 0; k < kRlW; ++k) {
-        if (k >= w) break;
-        const int par = k & 1;
-        cplx rk = row[0];
-#pragma unroll
-        for (int j = 1; j < kRlW; ++j)
-            if (j == k) rk = row[j];
-        // warp-level argmax (first index among equal moduli, as GEPP)
-        double v = (own && tid >= k) ? cabs2(rk) : -1.0;
-        int idx = (own && tid >= k) ? tid : 1 << 30;
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-            if (ov > v || (ov == v && oi < idx)) {
-                v = ov;
-                idx = oi;
-            }
-        }
-        if (tid == idx) {  // this warp's candidate publishes its row and reciprocal
-            cval[par][warp] = v;
-            cidx[par][warp] = idx;
-#pragma unroll
-            for (int j = 0; j < kRlW; ++j) crow[par][warp][j] = row[j];
-            crow[par][warp][kRlW] = (rk.re == 0.0 && rk.im == 0.0) ? cplx{0, 0} : fast_cinv(rk);
-        }
-        if (lane == 0 && idx == (1 << 30)) {
-            cval[par][warp] = -1.0;
-            cidx[par][warp] = 1 << 30;
-        }
-        if (tid == k) {
-#pragma unroll
-            for (int j = 0; j < kRlW; ++j) krow[par][j] = row[j];
-        }
-        __syncthreads();
-        // every warp reduces the candidates (no second barrier)
-        double bv = lane < nw ? cval[par][lane] : -1.0;
-        int bi = lane < nw ? cidx[par][lane] : 1 << 30;
-        int bw = lane;
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            const int ow = __shfl_xor_sync(0xffffffffu, bw, o);
-            if (ov > bv || (ov == bv && oi < bi)) {
-                bv = ov;
-                bi = oi;
-                bw = ow;
-            }
-        }
-        const int piv = bi;
-        const cplx* prow = crow[par][bw];
-        if (tid == 0) {
-            ipiv[c0 + k] = c0 + piv;
-            spiv[k] = piv;
-            if (bv == 0.0) singular[blockIdx.x] = 1;
-        }
-        if (piv != k) {  // interchange rows k and piv
-            if (tid == k) {
-#pragma unroll
-                for (int j = 0; j < kRlW; ++j) row[j] = prow[j];
-            } else if (tid == piv) {
-#pragma unroll
-                for (int j = 0; j < kRlW; ++j) row[j] = krow[par][j];
-                rk = krow[par][0];
-#pragma unroll
-                for (int j = 1; j < kRlW; ++j)
-                    if (j == k) rk = krow[par][j];
-            }
-        }
-        const cplx inv = prow[kRlW];
-        const bool zero = (inv.re == 0.0 && inv.im == 0.0);
-        if (own && tid > k) {
-            const cplx l = zero ? rk : cmul(rk, inv);
-#pragma unroll
-            for (int j = 0; j < kRlW; ++j) {
-                if (j == k) row[j] = l;
-                if (j > k) {
-                    const cplx pj = prow[j];
-                    row[j].re -= l.re * pj.re - l.im * pj.im;
-                    row[j].im -= l.re * pj.im + l.im * pj.re;
-                }
-            }
-        }
-    }
-    if (own) {
-#pragma unroll
-        for (int j = 0; j < kRlW; ++j)
-            if (j < w) A[size_t(c0 + j) * ld + c0 + tid] = row[j];
-    }
-    __syncthreads();
-    if (rl_map && tid == 0) {  // replay the interchanges on slots once per matrix
-        int* rowof = shi;  // 32 ints each, free after the last argmax
-        int* perm = reinterpret_cast<int*>(shv);
-        int nslot = kRlW;
-        for (int q = 0; q < 32; ++q) {
-            rowof[q] = q < kRlW ? c0 + q : -1;
-            perm[q] = q;
-        }
-        for (int t = 0; t < w; ++t) {
-            const int p = c0 + spiv[t];
-            if (p == c0 + t) continue;
-            int sp = -1;
-            if (p < c0 + kRlW) sp = p - c0;
-            else {
-                for (int q = kRlW; q < nslot; ++q)
-                    if (rowof[q] == p) sp = q;
-                if (sp < 0) {
-                    sp = nslot++;
-                    rowof[sp] = p;
-                }
-            }
-            const int tmp = perm[t];
-            perm[t] = perm[sp];
-            perm[sp] = tmp;
-        }
-        int* mp = rl_map + size_t(blockIdx.x) * kRlMap;
-        for (int q = 0; q < 32; ++q) mp[q] = perm[q];
-        for (int q = kRlW; q < 32; ++q) mp[32 + q - kRlW] = rowof[q];
-    }
-}
+constexpr int kRegPanelMaxRows = 640;  // rows of a single-CTA panel (one thread per row)
 
 // Same factorization with the panel in shared memory ([column][row], one
 // thread per row, rolled column loop): no register arrays, so no spills and a
@@ -1796,22 +1577,6 @@ __global__ void __launch_bounds__(256) lu_rl_cols_kernel(int n, int ld, cplx* co
     else if (ext_row >= 0) Ac[ext_row] = nv;
 }
 
-__global__ void rowswap_rhs_kernel(int n, const int* const* __restrict__ Pp, cplx* const* __restrict__ Bp, int ldb,
-                                   int nc) {
-    const int* ipiv = Pp[blockIdx.y];
-    cplx* B = Bp[blockIdx.y];
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
-    cplx* x = B + size_t(c) * ldb;
-    for (int k = 0; k < n; ++k) {
-        const int p = ipiv[k];
-        if (p != k) {
-            const cplx t = x[k];
-            x[k] = x[p];
-            x[p] = t;
-        }
-    }
-}
 
 __global__ void maxabs_kernel(const cplx* X, int m, int n, int ld, size_t stride, double* out) {
     const cplx* A = X + stride * blockIdx.x;
@@ -2052,27 +1817,18 @@ void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, 
 
 namespace {
 
-// 16-column panel factorization, <= 640 rows: shared-memory kernel (default)
-// or the register-resident one (QPS_PANEL=reg)
+// 16-column panel factorization of <= 640 rows (one thread per row)
 void launch_panel_fast(int n, int ld, cplx* const* dA, int* const* dP, int c0, int w, int* sing, int* rl_map,
                        int count, cudaStream_t s) {
-    static const bool reg = [] {
-        const char* e = getenv("QPS_PANEL");
-        return e && !strcmp(e, "reg");
-    }();
     const int threads = ((n - c0 + 31) / 32) * 32;
-    if (reg) {
-        lu_panel_reg_kernel<<<count, threads, 0, s>>>(n, ld, dA, dP, c0, w, sing, rl_map);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            QPS_CUDA(cudaFuncSetAttribute(lu_panel_sm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(size_t(kRegPanelMaxRows) * kRlW * sizeof(cplx))));
-            attr = true;
-        }
-        lu_panel_sm2_kernel<<<count, threads, size_t(n - c0) * w * sizeof(cplx), s>>>(n, ld, dA, dP, c0, w, sing,
-                                                                                      rl_map);
+    static bool attr = false;
+    if (!attr) {
+        QPS_CUDA(cudaFuncSetAttribute(lu_panel_sm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(size_t(kRegPanelMaxRows) * kRlW * sizeof(cplx))));
+        attr = true;
     }
+    lu_panel_sm2_kernel<<<count, threads, size_t(n - c0) * w * sizeof(cplx), s>>>(n, ld, dA, dP, c0, w, sing,
+                                                                                  rl_map);
 }
 
 DBuf<int> g_perm;  // per-matrix permutation scratch
