@@ -1831,13 +1831,11 @@ void launch_panel_fast(int n, int ld, cplx* const* dA, int* const* dP, int c0, i
                                                                                   rl_map);
 }
 
-DBuf<int> g_perm;  // per-matrix permutation scratch
-
 void launch_row_permute(int n, int ld, cplx* const* dA, const int* const* dP, int count, int k0, int kend, int c0,
-                        int c1, cudaStream_t s) {
+                        int c1, cudaStream_t s, DBuf<int>& perm) {
     if (c1 <= c0) return;
-    g_perm.ensure(size_t(count) * n);
-    perm_build_kernel<<<count, 128, 0, s>>>(n, dP, g_perm.p, k0, kend);
+    perm.ensure(size_t(count) * n);
+    perm_build_kernel<<<count, 128, 0, s>>>(n, dP, perm.p, k0, kend);
     QPS_CUDA(cudaGetLastError());
     const size_t sh = size_t(kPermWarps) * (n - k0) * sizeof(cplx);
     static size_t attr = 0;
@@ -1847,7 +1845,7 @@ void launch_row_permute(int n, int ld, cplx* const* dA, const int* const* dP, in
         attr = std::max<size_t>(sh, 64 * 1024);
     }
     const int nx = std::min((c1 - c0 + kPermWarps - 1) / kPermWarps, 32);
-    row_permute_kernel<<<dim3(nx, count), 256, sh, s>>>(n, ld, dA, g_perm.p, k0, c0, c1);
+    row_permute_kernel<<<dim3(nx, count), 256, sh, s>>>(n, ld, dA, perm.p, k0, c0, c1);
     QPS_CUDA(cudaGetLastError());
 }
 
@@ -1940,7 +1938,7 @@ void lu_rec(LuCtx& L, int c0, int nc) {
     lu_rec(L, c0, h);
     {  // left-half interchanges onto the right half
         ProfScope ps("lu_swap", L.s, 0.0);
-        launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0, c0 + h, c0 + h, c0 + nc, L.s);
+        launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0, c0 + h, c0 + h, c0 + nc, L.s, L.ws.perm);
     }
     trsm_lower_in_factor(L, c0, c0 + h, c0 + h, nc - h);
     // A22 -= A21 A12 over rows c0+h..n, cols c0+h..c0+nc
@@ -1949,7 +1947,7 @@ void lu_rec(LuCtx& L, int c0, int nc) {
     lu_rec(L, c0 + h, nc - h);
     {  // right-half interchanges back onto the left half
         ProfScope ps("lu_swap", L.s, 0.0);
-        launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0 + h, c0 + nc, c0, c0 + h, L.s);
+        launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0 + h, c0 + nc, c0, c0 + h, L.s, L.ws.perm);
     }
 }
 
@@ -2028,7 +2026,7 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
     const int* const* d_ipiv = ws.iptrs.p;
     {
         ProfScope ps("lu_swap", s, 0.0);
-        launch_row_permute(n, ldb, d_B, d_ipiv, count, 0, n, 0, nrhs, s);
+        launch_row_permute(n, ldb, d_B, d_ipiv, count, 0, n, 0, nrhs, s, ws.perm);
         QPS_CUDA(cudaGetLastError());
     }
     auto& tasks = ws.h_gemm;

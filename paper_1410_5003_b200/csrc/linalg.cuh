@@ -100,6 +100,7 @@ struct Workspace {
     DBuf<cplx*> ptrs, ptrs2, ptrs3;
     DBuf<int*> iptrs;
     DBuf<int> rl_map;  // right-looking LU: per matrix, the interchange map of the current panel
+    DBuf<int> perm;    // gathered row permutations (row_permute_kernel)
     std::vector<GemmTask> h_gemm;
 };
 
