@@ -113,7 +113,7 @@ def _phys(s):
     return np.concatenate([sol["aU"], sol["aD"]]), rt["R"], rt["T"], rt["flux_error"]
 
 
-@pytest.mark.parametrize("cfg,nif", [(1, None), (2, None), (4, 4), (5, 6)])
+@pytest.mark.parametrize("cfg,nif", [(1, None), (2, None), (4, 4), (4, 50), (5, 6)])
 def test_bragg_coefficients_at_oracle_noise_floor(gpu, oracle, cfg, nif):
     setup(gpu, cfg, nif)
     gpu.solve()
