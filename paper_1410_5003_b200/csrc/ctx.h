@@ -156,6 +156,12 @@ struct Ctx {
     std::vector<double> lsq;
     CodSet cod_int, cod_c;
 
+    // ---- low-rank couplings (bcr_lr.cu) ----
+    DBuf<cplx> lr_omega, lr_Y, lr_P, lr_PH, lr_R, lr_core, lr_T, lr_vec;
+    int lr_omega_n = 0, lr_r = 0;
+    CodSet lr_cod;
+    std::vector<DBuf<cplx>> lr_Z, lr_Rn;
+
     // ---- block cyclic reduction ----
     std::vector<BcrLevels> levels;  // [level][system]
     std::vector<DBuf<cplx>> lvlL, lvlU;
@@ -200,6 +206,10 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
 // allocate the per-system buffers of the assembled system for dims.nsys systems
 void alloc_system(Ctx& c);
 void recover(Ctx& c);
+// low-rank couplings: compress A'_{j,j+1}, A'_{j+1,j} of every system (false if not low rank)
+bool lr_compress(Ctx& c, cplx* Au, cplx* Al);
+// block cyclic reduction on the compressed couplings (after lr_compress)
+void bcr_solve_lr(Ctx& c, cplx* Ad);
 void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
                           int ldX, size_t Xstride, double* lsq_out);
 void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,

@@ -685,6 +685,15 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
 // Block cyclic reduction (all systems of the batch advance level by level)
 // ---------------------------------------------------------------------------
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
+    // low-rank couplings unless disabled (QPS_BCR=dense) or not low rank
+    static const bool dense_only = [] {
+        const char* e = getenv("QPS_BCR");
+        return e && !strcmp(e, "dense");
+    }();
+    if (!dense_only && lr_compress(c, Au, Al)) {
+        bcr_solve_lr(c, Ad);
+        return;
+    }
     ProfPhase phase("bcr");
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, ns = D.nsys;
