@@ -153,19 +153,46 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         const int j = sup ? rem - (I - 1) : rem;
         return (sup ? Au : Al) + size_t(a) * D.sU() + size_t(j) * D.nb2();
     };
-    // Y = C Omega
+    // deferred coupling Schur updates (one-shot path): C = A - Bc X, never formed
+    const bool corr = c.couplings_deferred;
+    auto corr_task = [&](int q) -> const GemmTask& {
+        const int a = q / (2 * (I - 1)), rem = q % (2 * (I - 1));
+        return rem >= I - 1 ? c.coupling_sup[size_t(a) * (I - 1) + rem - (I - 1)]
+                            : c.coupling_sub[size_t(a) * (I - 1) + rem];
+    };
+    const int P = D.P;
+    // Y = C Omega  (= A Omega + Bc (-X Omega) when deferred)
     c.lr_Y.ensure(size_t(nc) * nb * kLrSample);
     {
         std::vector<GemmTask> t(nc);
-        for (int q = 0; q < nc; ++q)
+        if (corr) {
+            c.lr_W.ensure(size_t(nc) * P * kLrSample);
+            std::vector<GemmTask> w(nc);
+            for (int q = 0; q < nc; ++q) {
+                const GemmTask& u = corr_task(q);
+                w[q] = gemm1(u.B[0], u.ldb[0], c.lr_omega.p, nb, nb, c.lr_W.p + size_t(q) * P * kLrSample, P);
+            }
+            zgemm_batched(P, kLrSample, cplx{-1, 0}, cplx{0, 0}, w, s, c.ws.gemm_tasks, "lr_compress");
+        }
+        for (int q = 0; q < nc; ++q) {
             t[q] = gemm1(coupling(q), nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrSample, nb);
+            if (corr) {
+                const GemmTask& u = corr_task(q);
+                t[q].nseg = 2;
+                t[q].A[1] = u.A[0];
+                t[q].lda[1] = u.lda[0];
+                t[q].B[1] = c.lr_W.p + size_t(q) * P * kLrSample;
+                t[q].ldb[1] = P;
+                t[q].K[1] = P;
+            }
+        }
         zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
     }
     // column-pivoted QR of each sample, numerical rank
     CodSet& cs = c.lr_cod;
     cs.ensure(nc, nb, kLrSample, 1);
     CodBatch b = cs.batch(c.lr_Y.p);
-    cod_factor(b, s);
+    cod_factor_fast(b, s);
     cod_rank(b, kLrTol, nullptr, s);
     std::vector<int> rk(nc);
     QPS_D2H(rk.data(), cs.rank.p, sizeof(int) * nc, s);
@@ -200,12 +227,31 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             nb, kLrSample, r, cs.W.p, cs.tau.p, c.lr_P.p, nb, size_t(nb) * r, c.lr_PH.p, size_t(r) * nb);
         QPS_CUDA(cudaGetLastError());
     }
-    // R = P^* C
+    // R = P^* C  (= P^* A + (-P^* Bc) X when deferred)
     c.lr_R.ensure(size_t(nc) * r * nb);
     {
+        if (corr) {
+            c.lr_G.ensure(size_t(nc) * r * P);
+            std::vector<GemmTask> g(nc);
+            for (int q = 0; q < nc; ++q) {
+                const GemmTask& u = corr_task(q);
+                g[q] = gemm1(c.lr_PH.p + size_t(q) * r * nb, r, u.A[0], u.lda[0], nb, c.lr_G.p + size_t(q) * r * P, r);
+            }
+            zgemm_batched(r, P, cplx{-1, 0}, cplx{0, 0}, g, s, c.ws.gemm_tasks, "lr_compress");
+        }
         std::vector<GemmTask> t(nc);
-        for (int q = 0; q < nc; ++q)
+        for (int q = 0; q < nc; ++q) {
             t[q] = gemm1(c.lr_PH.p + size_t(q) * r * nb, r, coupling(q), nb, nb, c.lr_R.p + size_t(q) * r * nb, r);
+            if (corr) {
+                const GemmTask& u = corr_task(q);
+                t[q].nseg = 2;
+                t[q].A[1] = c.lr_G.p + size_t(q) * r * P;
+                t[q].lda[1] = r;
+                t[q].B[1] = u.B[0];
+                t[q].ldb[1] = u.ldb[0];
+                t[q].K[1] = P;
+            }
+        }
         zgemm_batched(r, nb, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
     }
     return true;

@@ -364,7 +364,7 @@ int qps_solve(qps_ctx* h) {
         c.times.assemble_ms = 0.0;
         {
             Timer t(c, &c.times.schur_ms);
-            schur(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+            schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true);
         }
         c.sys_valid = false;  // A now holds A'
         {

@@ -157,8 +157,12 @@ struct Ctx {
     CodSet cod_int, cod_c;
 
     // ---- low-rank couplings (bcr_lr.cu) ----
-    DBuf<cplx> lr_omega, lr_Y, lr_P, lr_PH, lr_R, lr_core, lr_T, lr_vec;
+    DBuf<cplx> lr_omega, lr_Y, lr_P, lr_PH, lr_R, lr_core, lr_T, lr_vec, lr_W, lr_G;
     int lr_omega_n = 0, lr_r = 0;
+    // coupling Schur updates A'_{j,j+1} = A - B X left to the compression
+    // (one-shot path): [system][j] tasks of A_super and A_sub
+    std::vector<GemmTask> coupling_sup, coupling_sub;
+    bool couplings_deferred = false;
     CodSet lr_cod;
     std::vector<DBuf<cplx>> lr_Z, lr_Rn;
 
@@ -200,7 +204,7 @@ void setup_dims(Ctx& c, bool check_solvable = true);
 void fill_system_fused(Ctx& c);
 // Schur complements in place on (A_diag, A_super, A_sub) or on the A' copies,
 // for all dims.nsys systems (system a at base + a * stride)
-void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
+void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings = false);
 // block cyclic reduction of all systems with RHS f (per system); eta in c.F
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
 // allocate the per-system buffers of the assembled system for dims.nsys systems

@@ -394,6 +394,10 @@ constexpr int kMaxP = 256;
 // ColPivHouseholderQR::computeInPlace semantics (see oracle shim for the
 // restatement of Eigen's algorithm): largest updated column norm, LAPACK
 // xGEQPF norm downdating with recomputation below sqrt(eps).
+// kFast (low-rank compression only): reciprocal-multiplies instead of the
+// FP64 divisions on each column's critical path (~600 cycles each on B200);
+// the Schur least squares keep Eigen's divisions.
+template <bool kFast>
 __global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
     const int pb = blockIdx.x;
     const int m = b.m, p = b.p, size = min(m, p);
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
     __shared__ int flag[kMaxP];
     __shared__ double shv[32];
     __shared__ int shi[32];
-    __shared__ cplx s_tau, s_den;
+    __shared__ cplx s_tau, s_den, s_inv;
     __shared__ int s_nzp;
     __shared__ double s_maxpiv;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -471,6 +475,7 @@ __global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
                 s_den = cplx{c0.re - beta, c0.im};
                 tk = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
             }
+            if (kFast) s_inv = (s_den.re == 0.0 && s_den.im == 0.0) ? cplx{0, 0} : fast_cinv(s_den);
             s_tau = tk;
             tau[k] = tk;
             W[size_t(k) * m + k] = cplx{beta, 0.0};
@@ -481,7 +486,8 @@ __global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
         const bool zero_tau = (tk.re == 0.0 && tk.im == 0.0);
         for (int i = k + 1 + tid; i < m; i += blockDim.x) {
             cplx* w = &W[size_t(k) * m + i];
-            *w = (den.re == 0.0 && den.im == 0.0) ? cplx{0, 0} : cdiv(*w, den);
+            if (kFast) *w = cmul(*w, s_inv);
+            else *w = (den.re == 0.0 && den.im == 0.0) ? cplx{0, 0} : cdiv(*w, den);
         }
         __syncthreads();
         // apply H = I - tau v v^* to columns k+1..p-1
@@ -525,10 +531,12 @@ __global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
             flag[j] = 0;
             if (upd[j] != 0.0) {
                 const cplx a = W[size_t(j) * m + k];
-                double t = sqrt(cabs2(a)) / upd[j];
+                const double iu = kFast ? fast_rcp(upd[j]) : 0.0;
+                double t = kFast ? sqrt(cabs2(a)) * iu : sqrt(cabs2(a)) / upd[j];
                 t = (1.0 + t) * (1.0 - t);
                 t = t < 0.0 ? 0.0 : t;
-                const double t2 = t * (upd[j] / dir[j]) * (upd[j] / dir[j]);
+                const double ud = kFast ? upd[j] * fast_rcp(dir[j]) : upd[j] / dir[j];
+                const double t2 = t * ud * ud;
                 if (t2 <= downdate_thr) flag[j] = 1;
                 else upd[j] *= sqrt(t);
             }
@@ -1741,7 +1749,14 @@ void cod_factor(const CodBatch& b, cudaStream_t s) {
     if (b.p > kMaxP) fail(QPS_ERR_CONFIG, "qsolve: too many columns for the device COD (max 256)");
     if (b.m < b.p) fail(QPS_ERR_USAGE, "qsolve: Q must have at least as many rows as columns");
     ProfScope ps("cod_factor", s, 8.0 * b.count * (2.0 * b.m * b.p * b.p - 2.0 * b.p * b.p * b.p / 3.0));
-    cod_factor_kernel<<<b.count, 256, 0, s>>>(b);
+    cod_factor_kernel<false><<<b.count, 256, 0, s>>>(b);
+    QPS_CUDA(cudaGetLastError());
+}
+void cod_factor_fast(const CodBatch& b, cudaStream_t s) {
+    if (b.count == 0) return;
+    if (b.p > kMaxP || b.m < b.p) fail(QPS_ERR_INTERNAL, "cod_factor_fast: bad shape");
+    ProfScope ps("lr_cpqr", s, 8.0 * b.count * (2.0 * b.m * b.p * b.p - 2.0 * b.p * b.p * b.p / 3.0));
+    cod_factor_kernel<true><<<b.count, 256, 0, s>>>(b);
     QPS_CUDA(cudaGetLastError());
 }
 void cod_rank(const CodBatch& b, double th, const int* flags, cudaStream_t s) {

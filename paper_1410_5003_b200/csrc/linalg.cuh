@@ -54,6 +54,8 @@ struct CodBatch {
 // COD solve (never an explicit inverse)
 void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, const int* d_flags, cudaStream_t s);
 void cod_factor(const CodBatch& b, cudaStream_t s);
+// same factorization with reciprocal-multiplies for the divisions (compression only)
+void cod_factor_fast(const CodBatch& b, cudaStream_t s);
 // rank at threshold th for problems whose flag is set (flags == nullptr: all)
 void cod_rank(const CodBatch& b, double th, const int* d_flags, cudaStream_t s);
 // forms QH and Wz for the current rank: X = Wz * T11^{-1} * (QH * RHS)

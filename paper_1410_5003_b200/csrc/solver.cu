@@ -581,7 +581,7 @@ void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int 
     qsolve_family(c, cs, Q, R, ldR, Rstride, X, ldX, Xstride, lsq_out);
 }
 
-void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
+void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
     ProfPhase phase("schur");
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, P = D.P, ns = D.nsys;
@@ -625,6 +625,9 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     //   Ap_diag[j] -= B_self[j] X_self(j) + B_below[j] X_above(j+1)
     //   Ap_super[j] -= B_below[j] X_self(j+1),  Ap_sub[j] -= B_self[j+1] X_above(j+1)
     std::vector<GemmTask> tasks;
+    c.coupling_sup.clear();
+    c.coupling_sub.clear();
+    c.couplings_deferred = false;
     for (int a = 0; a < ns; ++a) {
         const cplx* Xi = c.Xint.p + size_t(a) * D.sXi();
         const cplx* Xc = c.Xc.p + size_t(a) * D.sXc();
@@ -662,7 +665,6 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                 u.K[0] = P;
                 u.C = Aua + j * nb2;
                 u.ldc = nb;
-                tasks.push_back(u);
                 GemmTask v{};
                 v.nseg = 1;
                 v.A[0] = c.Bself.p + size_t(j + 1) * nb * P;
@@ -671,11 +673,18 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                 v.K[0] = P;
                 v.C = Ala + j * nb2;
                 v.ldc = nb;
-                tasks.push_back(v);
+                if (defer_couplings) {
+                    c.coupling_sup.push_back(u);
+                    c.coupling_sub.push_back(v);
+                } else {
+                    tasks.push_back(u);
+                    tasks.push_back(v);
+                }
             }
         }
     }
     zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks, "schur_update");
+    c.couplings_deferred = defer_couplings && I > 1;
     c.max_lsq = 0.0;
     for (double r : c.lsq) c.max_lsq = std::max(c.max_lsq, r);
     c.ps_valid = true;
@@ -684,6 +693,8 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
 // ---------------------------------------------------------------------------
 // Block cyclic reduction (all systems of the batch advance level by level)
 // ---------------------------------------------------------------------------
+static int D_nb(const Ctx& c) { return c.dims.nb; }
+
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     // low-rank couplings unless disabled (QPS_BCR=dense) or not low rank
     static const bool dense_only = [] {
@@ -692,7 +703,14 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     }();
     if (!dense_only && lr_compress(c, Au, Al)) {
         bcr_solve_lr(c, Ad);
+        c.couplings_deferred = false;
         return;
+    }
+    if (c.couplings_deferred) {  // the dense reduction needs the periodized couplings
+        std::vector<GemmTask> t(c.coupling_sup);
+        t.insert(t.end(), c.coupling_sub.begin(), c.coupling_sub.end());
+        zgemm_batched(D_nb(c), D_nb(c), cplx{-1, 0}, cplx{1, 0}, t, c.stream, c.ws.gemm_tasks, "schur_update");
+        c.couplings_deferred = false;
     }
     ProfPhase phase("bcr");
     const Dims& D = c.dims;
