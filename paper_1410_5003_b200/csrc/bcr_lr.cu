@@ -186,6 +186,9 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
                 t[q].K[1] = P;
             }
         }
+        if (getenv("QPS_TRACE_LAUNCH"))
+            fprintf(stderr, "lr_compress sample GEMM is zgemm3m launch index %llu\n",
+                    (unsigned long long)g_zgemm_launches.load());
         zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
     }
     // column-pivoted QR of each sample, numerical rank
