@@ -122,31 +122,73 @@ GemvTask gemv1(const cplx* A, int lda, const cplx* x, int n, cplx* y) {
 
 }  // namespace
 
+namespace {
+// random sample matrix (seeded, fixed), uploaded on stream s
+void lr_omega_setup(Ctx& c, cudaStream_t s) {
+    const int nb = c.dims.nb;
+    if (c.lr_omega_n == nb) return;
+    std::vector<cplx> om(size_t(nb) * kLrSample);
+    uint64_t x = 0x9e3779b97f4a7c15ull;
+    for (auto& z : om) {
+        auto next = [&]() {
+            x ^= x >> 12;
+            x ^= x << 25;
+            x ^= x >> 27;
+            return double((x * 0x2545f4914f6cdd1dull) >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+        };
+        z = cplx{next(), next()};
+    }
+    c.lr_omega.upload(om, s);
+    c.lr_omega_n = nb;
+}
+bool lr_eligible(const Ctx& c) {
+    static const bool dense_only = [] {
+        const char* e = getenv("QPS_BCR");
+        return e && !strcmp(e, "dense");
+    }();
+    return !dense_only && c.dims.I >= 2 && c.dims.nb >= 4 * kLrSample;
+}
+}  // namespace
+
+// The sample's A Omega part needs only the assembled couplings: it runs on a
+// second stream while the Schur least squares (latency-bound) run on the main
+// one.  lr_compress adds the B (-X Omega) correction once X exists.
+void lr_sample_async(Ctx& c) {
+    c.lr_sample_pending = false;
+    if (!lr_eligible(c)) return;
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, ns = D.nsys;
+    const int nc = 2 * ns * (I - 1);
+    QPS_CUDA(cudaEventRecord(c.ev_fill, c.stream));
+    QPS_CUDA(cudaStreamWaitEvent(c.side2, c.ev_fill, 0));
+    lr_omega_setup(c, c.side2);
+    c.lr_Y.ensure(size_t(nc) * nb * kLrSample);
+    std::vector<GemmTask> t(nc);
+    for (int q = 0; q < nc; ++q) {
+        const int a = q / (2 * (I - 1)), rem = q % (2 * (I - 1));
+        const bool sup = rem >= I - 1;
+        const int j = sup ? rem - (I - 1) : rem;
+        const cplx* C = (sup ? c.Asup.p : c.Asub.p) + size_t(a) * D.sU() + size_t(j) * D.nb2();
+        t[q] = gemm1(C, nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrSample, nb);
+    }
+    {
+        ProfPhase phase("lowrank");
+        zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, c.side2, c.lr_tasks, "lr_compress");
+    }
+    QPS_CUDA(cudaEventRecord(c.ev_sample, c.side2));
+    c.lr_sample_pending = true;
+}
+
 // Compress every coupling of every system: c.lr_P / c.lr_R (per coupling,
 // n x r ld nb and r x n ld r), ordered [system][sub 0..I-2][super 0..I-2].
 bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, ns = D.nsys;
-    if (I < 2 || nb < 4 * kLrSample) return false;  // small blocks: dense is cheap
+    if (!lr_eligible(c)) return false;  // small blocks: dense is cheap
     cudaStream_t s = c.stream;
     ProfPhase phase("lowrank");
     const int nc = 2 * ns * (I - 1);
-    // random sample matrix (seeded, fixed)
-    if (c.lr_omega_n != nb) {
-        std::vector<cplx> om(size_t(nb) * kLrSample);
-        uint64_t x = 0x9e3779b97f4a7c15ull;
-        for (auto& z : om) {
-            auto next = [&]() {
-                x ^= x >> 12;
-                x ^= x << 25;
-                x ^= x >> 27;
-                return double((x * 0x2545f4914f6cdd1dull) >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
-            };
-            z = cplx{next(), next()};
-        }
-        c.lr_omega.upload(om, s);
-        c.lr_omega_n = nb;
-    }
+    lr_omega_setup(c, s);
     auto coupling = [&](int q) -> const cplx* {  // q in [0, nc)
         const int a = q / (2 * (I - 1)), rem = q % (2 * (I - 1));
         const bool sup = rem >= I - 1;
@@ -163,6 +205,9 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     const int P = D.P;
     // Y = C Omega  (= A Omega + Bc (-X Omega) when deferred)
     c.lr_Y.ensure(size_t(nc) * nb * kLrSample);
+    const bool early = c.lr_sample_pending && corr;  // Y already holds A Omega
+    if (c.lr_sample_pending) QPS_CUDA(cudaStreamWaitEvent(s, c.ev_sample, 0));
+    c.lr_sample_pending = false;
     {
         std::vector<GemmTask> t(nc);
         if (corr) {
@@ -174,7 +219,13 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             }
             zgemm_batched(P, kLrSample, cplx{-1, 0}, cplx{0, 0}, w, s, c.ws.gemm_tasks, "lr_compress");
         }
-        for (int q = 0; q < nc; ++q) {
+        for (int q = 0; q < nc && early; ++q) {  // Y += Bc (-X Omega)
+            const GemmTask& u = corr_task(q);
+            t[q] = gemm1(u.A[0], u.lda[0], c.lr_W.p + size_t(q) * P * kLrSample, P, P,
+                         c.lr_Y.p + size_t(q) * nb * kLrSample, nb);
+        }
+        if (early) zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        for (int q = 0; q < nc && !early; ++q) {
             t[q] = gemm1(coupling(q), nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrSample, nb);
             if (corr) {
                 const GemmTask& u = corr_task(q);
@@ -186,10 +237,12 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
                 t[q].K[1] = P;
             }
         }
-        if (getenv("QPS_TRACE_LAUNCH"))
-            fprintf(stderr, "lr_compress sample GEMM is zgemm3m launch index %llu\n",
-                    (unsigned long long)g_zgemm_launches.load());
-        zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        if (!early) {
+            if (getenv("QPS_TRACE_LAUNCH"))
+                fprintf(stderr, "lr_compress sample GEMM is zgemm3m launch index %llu\n",
+                        (unsigned long long)g_zgemm_launches.load());
+            zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        }
     }
     // column-pivoted QR of each sample, numerical rank
     CodSet& cs = c.lr_cod;

@@ -115,7 +115,10 @@ qps_ctx* qps_create(int device) {
         QPS_CUDA(cudaSetDevice(device));
         QPS_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
         QPS_CUDA(cudaStreamCreateWithFlags(&h->c.side, cudaStreamNonBlocking));
+        QPS_CUDA(cudaStreamCreateWithFlags(&h->c.side2, cudaStreamNonBlocking));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fork, cudaEventDisableTiming));
+        QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fill, cudaEventDisableTiming));
+        QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_sample, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreate(&h->c.ev0));
         QPS_CUDA(cudaEventCreate(&h->c.ev1));
         upload_hankel_tables();
@@ -136,12 +139,15 @@ void qps_destroy(qps_ctx* h) {
     cudaStreamSynchronize(h->c.stream);
     if (h->c.ev0) cudaEventDestroy(h->c.ev0);
     if (h->c.ev1) cudaEventDestroy(h->c.ev1);
-    cudaStream_t s = h->c.stream, s2 = h->c.side;
+    cudaStream_t s = h->c.stream, s2 = h->c.side, s3 = h->c.side2;
     if (s2) cudaStreamSynchronize(s2);
-    if (h->c.ev_fork) cudaEventDestroy(h->c.ev_fork);
+    if (s3) cudaStreamSynchronize(s3);
+    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample})
+        if (e) cudaEventDestroy(e);
     delete h;
     if (s) cudaStreamDestroy(s);
     if (s2) cudaStreamDestroy(s2);
+    if (s3) cudaStreamDestroy(s3);
 }
 
 int qps_last_error(const qps_ctx* h, char* msg, size_t cap, int* layer, uint64_t* bytes) {
@@ -362,6 +368,7 @@ int qps_solve(qps_ctx* h) {
         c.ps_separate = false;
         run_fill(c);
         c.times.assemble_ms = 0.0;
+        lr_sample_async(c);  // overlaps the Schur least squares
         {
             Timer t(c, &c.times.schur_ms);
             schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true);

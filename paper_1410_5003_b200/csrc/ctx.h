@@ -110,7 +110,8 @@ struct Ctx {
     bool host_only = false;  // device == -1: geometry/problem logic only, every device call fails
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // second stream: work independent of the main stream (corner least squares)
-    cudaEvent_t ev_fork = nullptr;
+    cudaStream_t side2 = nullptr; // third stream: the low-rank sample overlapping the Schur least squares
+    cudaEvent_t ev_fork = nullptr, ev_fill = nullptr, ev_sample = nullptr;
 
     StackDesc stack;
     Numerics num;
@@ -163,6 +164,8 @@ struct Ctx {
     // (one-shot path): [system][j] tasks of A_super and A_sub
     std::vector<GemmTask> coupling_sup, coupling_sub;
     bool couplings_deferred = false;
+    bool lr_sample_pending = false;
+    DBuf<GemmTask> lr_tasks;  // task table of the side2 stream's GEMMs
     CodSet lr_cod;
     std::vector<DBuf<cplx>> lr_Z, lr_Rn;
 
@@ -212,6 +215,8 @@ void alloc_system(Ctx& c);
 void recover(Ctx& c);
 // low-rank couplings: compress A'_{j,j+1}, A'_{j+1,j} of every system (false if not low rank)
 bool lr_compress(Ctx& c, cplx* Au, cplx* Al);
+// start the A Omega part of the compression sample on the side2 stream (one-shot path, after the fill)
+void lr_sample_async(Ctx& c);
 // block cyclic reduction on the compressed couplings (after lr_compress)
 void bcr_solve_lr(Ctx& c, cplx* Ad);
 void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,

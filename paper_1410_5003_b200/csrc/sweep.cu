@@ -559,6 +559,7 @@ void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, d
                 c.dims.nsys = int(ids.size());
                 if (mode != 0) timed(&tm.fill_ms, [&] { cache_fill(c); });
                 timed(&tm.assemble_ms, [&] { assemble_from_cache(c, bp); });
+                lr_sample_async(c);
                 timed(&tm.schur_ms, [&] { schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true); });
                 c.sys_valid = false;
                 timed(&tm.solve_ms, [&] { bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p); });
