@@ -23,6 +23,7 @@
 // problem's own noise floor; systems whose couplings are not low rank
 // (rank > 48 of a 64-column sample) take the dense cyclic reduction.
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -34,6 +35,18 @@
 namespace qpsb {
 
 namespace {
+
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return cplx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ __forceinline__ cplx cconj(cplx a) { return cplx{a.re, -a.im}; }
+__device__ __forceinline__ double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {  // Smith's algorithm
+    if (fabs(b.re) >= fabs(b.im)) {
+        const double r = b.im / b.re, den = b.re + b.im * r;
+        return cplx{(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+    }
+    const double r = b.re / b.im, den = b.re * r + b.im;
+    return cplx{(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+}
 
 constexpr int kLrSample = 64;    // columns of the random sample
 constexpr int kLrMaxRank = 48;   // beyond this the dense reduction is used
@@ -93,6 +106,208 @@ __global__ void __launch_bounds__(256) lr_form_q_kernel(int m, int p, int r, con
             ph[size_t(i) * r + c] = cplx{x.re, -x.im};
         }
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Blocked Householder QR of the samples (m x 64, m <= 640): four 16-column
+// panels, each factored in shared memory with one thread per row (one block
+// reduction per column, combining the trailing-column products and the
+// compact-WY inner products), trailing updates as batched GEMMs with the
+// compact WY form H_15..H_0 = I - V T^* V^* (T upper triangular, LAPACK larft
+// on the conjugate reflectors).  The 64 x 64 R is then factored with column
+// pivoting (rank, ordering) and the basis P = Q Q2[:, :48] is formed by
+// applying the four block reflectors to [Q2; 0] -- every pass over the tall
+// sample is a GEMM, none streams it once per column.
+// ---------------------------------------------------------------------------
+constexpr int kQrW = 16;
+__global__ void __launch_bounds__(640, 1) qr_panel_kernel(int m, cplx* __restrict__ Y, size_t ystride, int col0,
+                                                          cplx* __restrict__ V, cplx* __restrict__ VH,
+                                                          cplx* __restrict__ T, cplx* __restrict__ TH,
+                                                          size_t vstride, size_t tstride) {
+    extern __shared__ cplx qp[];  // [kQrW][m]
+    const int b = blockIdx.x;
+    cplx* Yb = Y + size_t(b) * ystride;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ cplx red[32][kQrW];  // per-warp partial sums
+    __shared__ cplx tot[kQrW];
+    __shared__ cplx s_tau, s_inv, s_beta;
+    __shared__ cplx Ts[kQrW][kQrW];  // T~[row][col]
+    const bool own = tid < m;
+    if (own)
+        for (int j = 0; j < kQrW; ++j) qp[j * m + tid] = Yb[size_t(col0 + j) * m + tid];
+    __syncthreads();
+    // v_j on this row, rebuilt from the panel (qp holds v_j below the diagonal)
+    auto vrow = [&](int j) -> cplx {
+        const int d = col0 + j;
+        if (!own || tid < d) return cplx{0, 0};
+        if (tid == d) return cplx{1.0, 0.0};
+        return qp[j * m + tid];
+    };
+    for (int k = 0; k < kQrW; ++k) {
+        const int g0 = col0 + k;
+        // tail norm of column k below the diagonal
+        double t2 = (own && tid > g0) ? cabs2(qp[k * m + tid]) : 0.0;
+        for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        if (lane == 0) red[warp][0].re = t2;
+        __syncthreads();
+        if (tid == 0) {
+            double tail = 0.0;
+            for (int w = 0; w < nw; ++w) tail += red[w][0].re;
+            const cplx c0 = qp[k * m + g0];
+            if (tail <= DBL_MIN && c0.im * c0.im <= DBL_MIN) {  // makeHouseholder's no-op case
+                s_tau = cplx{0, 0};
+                s_beta = c0;
+                s_inv = cplx{0, 0};
+            } else {
+                double beta = sqrt(cabs2(c0) + tail);
+                if (c0.re >= 0.0) beta = -beta;
+                const cplx den{c0.re - beta, c0.im};
+                s_inv = cdiv(cplx{1.0, 0.0}, den);
+                s_tau = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
+                s_beta = cplx{beta, 0.0};
+            }
+        }
+        __syncthreads();
+        const cplx tau = s_tau;
+        // v_k on this row
+        cplx v{0, 0};
+        if (own) {
+            if (tid == g0) {
+                v = cplx{1.0, 0.0};
+                qp[k * m + tid] = s_beta;
+            } else if (tid > g0) {
+                v = cmul(qp[k * m + tid], s_inv);
+                qp[k * m + tid] = v;
+            }
+        }
+        // one reduction: s_j = v_k^* a_j (j > k) and z_l = v_l^* v_k (l < k)
+        // (two halves of eight to keep the partials in registers)
+#pragma unroll
+        for (int h = 0; h < kQrW; h += kQrW / 2) {
+            cplx part[kQrW / 2];
+#pragma unroll
+            for (int jj = 0; jj < kQrW / 2; ++jj) {
+                const int j = h + jj;
+                cplx a{0, 0};
+                if (j > k && own) a = qp[j * m + tid];
+                else if (j < k) a = vrow(j);
+                // j > k: conj(v) a ; j < k: conj(v_j) v
+                part[jj] = (j > k) ? cplx{v.re * a.re + v.im * a.im, v.re * a.im - v.im * a.re}
+                                   : cplx{a.re * v.re + a.im * v.im, a.re * v.im - a.im * v.re};
+            }
+#pragma unroll
+            for (int jj = 0; jj < kQrW / 2; ++jj) {
+                for (int o = 16; o > 0; o >>= 1) {
+                    part[jj].re += __shfl_xor_sync(0xffffffffu, part[jj].re, o);
+                    part[jj].im += __shfl_xor_sync(0xffffffffu, part[jj].im, o);
+                }
+            }
+            if (lane == 0)
+#pragma unroll
+                for (int jj = 0; jj < kQrW / 2; ++jj) red[warp][h + jj] = part[jj];
+        }
+        __syncthreads();
+        if (tid < kQrW) {
+            cplx sacc{0, 0};
+            for (int w = 0; w < nw; ++w) {
+                sacc.re += red[w][tid].re;
+                sacc.im += red[w][tid].im;
+            }
+            tot[tid] = sacc;
+        }
+        __syncthreads();
+        if (tid == 0) {  // T~ column k: T~[k][k] = conj(tau), T~[0:k, k] = -conj(tau) T~[0:k,0:k] z
+            const cplx ct = cconj(tau);
+            for (int l = 0; l < k; ++l) {
+                cplx acc{0, 0};
+                for (int q = l; q < k; ++q) {
+                    const cplx t = cmul(Ts[l][q], tot[q]);
+                    acc.re += t.re;
+                    acc.im += t.im;
+                }
+                const cplx val = cmul(ct, acc);
+                Ts[l][k] = cplx{-val.re, -val.im};
+            }
+            Ts[k][k] = ct;
+            for (int l = k + 1; l < kQrW; ++l) Ts[l][k] = cplx{0, 0};
+        }
+        // apply H_k = I - tau v v^* to the panel columns j > k
+        if (own && !(tau.re == 0.0 && tau.im == 0.0)) {
+            for (int j = k + 1; j < kQrW; ++j) {
+                const cplx ts = cmul(tau, tot[j]);
+                const cplx d = cmul(ts, v);
+                qp[j * m + tid].re -= d.re;
+                qp[j * m + tid].im -= d.im;
+            }
+        }
+        __syncthreads();
+    }
+    // write back R (rows <= diag) and the explicit V / V^*, T~ and T~^*
+    cplx* Vb = V + size_t(b) * vstride;
+    cplx* VHb = VH + size_t(b) * vstride;
+    if (own) {
+#pragma unroll
+        for (int j = 0; j < kQrW; ++j) {
+            Yb[size_t(col0 + j) * m + tid] = (tid <= col0 + j) ? qp[j * m + tid] : cplx{0, 0};
+            const cplx vj = vrow(j);
+            Vb[size_t(j) * m + tid] = vj;
+            VHb[size_t(tid) * kQrW + j] = cconj(vj);
+        }
+    }
+    if (tid < kQrW * kQrW) {
+        const int r = tid % kQrW, c = tid / kQrW;
+        T[size_t(b) * tstride + size_t(c) * kQrW + r] = Ts[r][c];
+        TH[size_t(b) * tstride + size_t(c) * kQrW + r] = cconj(Ts[c][r]);
+    }
+}
+
+// top 64 x 64 (upper triangle) of each factored sample; zeros below
+__global__ void qr_take_r_kernel(int m, int p, const cplx* __restrict__ Y, size_t ystride, cplx* __restrict__ R) {
+    const int b = blockIdx.x;
+    for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+        const int i = e % p, j = e / p;
+        R[size_t(b) * p * p + e] = i <= j ? Y[size_t(b) * ystride + size_t(j) * m + i] : cplx{0, 0};
+    }
+}
+
+// X = [Q2 (p x r); 0] (m x r), and its conjugate transpose later
+__global__ void qr_seed_kernel(int m, int p, int r, const cplx* __restrict__ Q2, size_t q2stride,
+                               cplx* __restrict__ X, size_t xstride) {
+    const int b = blockIdx.x;
+    for (size_t e = threadIdx.x; e < size_t(m) * r; e += blockDim.x) {
+        const int i = int(e % m), j = int(e / m);
+        X[size_t(b) * xstride + e] = i < p ? Q2[size_t(b) * q2stride + size_t(j) * p + i] : cplx{0, 0};
+    }
+}
+
+__global__ void conj_transpose_kernel(int m, int r, const cplx* __restrict__ X, size_t xstride,
+                                      cplx* __restrict__ XH, size_t hstride) {
+    const int b = blockIdx.y;
+    for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < size_t(m) * r;
+         e += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % m), j = int(e / m);
+        XH[size_t(b) * hstride + size_t(i) * r + j] = cconj(X[size_t(b) * xstride + e]);
+    }
+}
+
+// C_b = I (n x n, column-major, stride n^2)
+__global__ void set_identity_kernel(int n, cplx* __restrict__ C) {
+    cplx* Cb = C + size_t(blockIdx.x) * n * n;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Cb[e] = cplx{(e % n == e / n) ? 1.0 : 0.0, 0.0};
+}
+
+// W_j = [P_L(j) P_U(j)] (zeros where a coupling is absent) for every block j of
+// every system; P holds per system the I-1 sub- then the I-1 super-couplings
+__global__ void stage_bases_kernel(int I, size_t per, const cplx* __restrict__ P, cplx* __restrict__ W) {
+    const int j = blockIdx.x, a = j / I, jj = j % I;
+    const size_t qa = size_t(a) * 2 * (I - 1);
+    const cplx* pl = jj >= 1 ? P + (qa + (jj - 1)) * per : nullptr;
+    const cplx* pu = jj + 1 < I ? P + (qa + (I - 1) + jj) * per : nullptr;
+    cplx* w = W + size_t(j) * 2 * per;
+    for (size_t e = size_t(blockIdx.y) * blockDim.x + threadIdx.x; e < per; e += size_t(gridDim.y) * blockDim.x) {
+        w[e] = pl ? pl[e] : cplx{0, 0};
+        w[per + e] = pu ? pu[e] : cplx{0, 0};
     }
 }
 
@@ -244,44 +459,143 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
         }
     }
-    // column-pivoted QR of each sample, numerical rank
-    CodSet& cs = c.lr_cod;
-    cs.ensure(nc, nb, kLrSample, 1);
-    CodBatch b = cs.batch(c.lr_Y.p);
-    cod_factor_fast(b, s);
-    cod_rank(b, kLrTol, nullptr, s);
+    static const bool cpqr_only = [] {
+        const char* e = getenv("QPS_LR_QR");
+        return e && !strcmp(e, "cpqr");
+    }();
     std::vector<int> rk(nc);
-    QPS_D2H(rk.data(), cs.rank.p, sizeof(int) * nc, s);
-    QPS_CUDA(cudaStreamSynchronize(s));
     int r = 0;
-    for (int v : rk) r = std::max(r, v);
-    if (getenv("QPS_LR_TRACE")) {
-        int mn = 1 << 30;
-        double mean = 0;
-        for (int v : rk) { mn = std::min(mn, v); mean += v; }
-        fprintf(stderr, "low-rank couplings: %d blocks, rank min %d mean %.1f max %d (sample %d)\n", nc, mn,
-                mean / nc, r, kLrSample);
-    }
-    if (r > kLrMaxRank) return false;
-    // a fixed basis width keeps every system's factors independent of the batch
-    // it is solved in (the sweep's batched and one-at-a-time results agree)
-    r = kLrMaxRank;
-    c.lr_r = r;
-    // P (n x r) and P^* (r x n)
-    c.lr_P.ensure(size_t(nc) * nb * r);
-    c.lr_PH.ensure(size_t(nc) * r * nb);
-    {
-        ProfScope ps("lr_compress", s, 0.0);
-        static size_t attr = 0;
-        const size_t sm = size_t(8) * nb * sizeof(cplx);
-        if (sm > attr) {
-            QPS_CUDA(cudaFuncSetAttribute(lr_form_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(std::max<size_t>(sm, 48 * 1024))));
-            attr = std::max<size_t>(sm, 48 * 1024);
+    if (!cpqr_only && nb <= 640) {
+        // blocked Householder QR of the samples, CPQR of the 64 x 64 R
+        const int m = nb, p = kLrSample, nP = p / kQrW;
+        const size_t ys = size_t(m) * p, vs = size_t(m) * kQrW, ts = size_t(kQrW) * kQrW;
+        c.lr_V.ensure(size_t(nc) * nP * vs);
+        c.lr_VH.ensure(size_t(nc) * nP * vs);
+        c.lr_Tq.ensure(size_t(nc) * nP * ts);
+        c.lr_THq.ensure(size_t(nc) * nP * ts);
+        c.lr_W1.ensure(size_t(nc) * kQrW * p);
+        c.lr_W2.ensure(size_t(nc) * kQrW * p);
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(640 * kQrW * sizeof(cplx))));
+            attr = true;
         }
-        lr_form_q_kernel<<<dim3(nc, (r + 7) / 8), 256, size_t(8) * nb * sizeof(cplx), s>>>(
-            nb, kLrSample, r, cs.W.p, cs.tau.p, c.lr_P.p, nb, size_t(nb) * r, c.lr_PH.p, size_t(r) * nb);
+        auto V_of = [&](int q, int pn) { return c.lr_V.p + (size_t(q) * nP + pn) * vs; };
+        auto VH_of = [&](int q, int pn) { return c.lr_VH.p + (size_t(q) * nP + pn) * vs; };
+        auto T_of = [&](int q, int pn) { return c.lr_Tq.p + (size_t(q) * nP + pn) * ts; };
+        auto TH_of = [&](int q, int pn) { return c.lr_THq.p + (size_t(q) * nP + pn) * ts; };
+        for (int pn = 0; pn < nP; ++pn) {
+            const int col0 = pn * kQrW;
+            {
+                ProfScope ps("lr_qr", s, 0.0);
+                // per-problem pointers are strided: V_of(q, pn) = base + (q nP + pn) vs
+                qr_panel_kernel<<<nc, ((m + 31) / 32) * 32, size_t(m) * kQrW * sizeof(cplx), s>>>(
+                    m, c.lr_Y.p, ys, col0, c.lr_V.p + pn * vs, c.lr_VH.p + pn * vs, c.lr_Tq.p + pn * ts,
+                    c.lr_THq.p + pn * ts, size_t(nP) * vs, size_t(nP) * ts);
+                QPS_CUDA(cudaGetLastError());
+            }
+            const int rest = p - col0 - kQrW;
+            if (rest <= 0) continue;
+            std::vector<GemmTask> t1(nc), t2(nc), t3(nc);
+            for (int q = 0; q < nc; ++q) {
+                cplx* Yr = c.lr_Y.p + size_t(q) * ys + size_t(col0 + kQrW) * m;
+                t1[q] = gemm1(VH_of(q, pn), kQrW, Yr, m, m, c.lr_W1.p + size_t(q) * kQrW * p, kQrW);
+                t2[q] = gemm1(TH_of(q, pn), kQrW, c.lr_W1.p + size_t(q) * kQrW * p, kQrW, kQrW,
+                              c.lr_W2.p + size_t(q) * kQrW * p, kQrW);
+                t3[q] = gemm1(V_of(q, pn), m, c.lr_W2.p + size_t(q) * kQrW * p, kQrW, kQrW, Yr, m);
+            }
+            zgemm_batched(kQrW, rest, cplx{1, 0}, cplx{0, 0}, t1, s, c.ws.gemm_tasks, "lr_qr");
+            zgemm_batched(kQrW, rest, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks, "lr_qr");
+            zgemm_batched(m, rest, cplx{-1, 0}, cplx{1, 0}, t3, s, c.ws.gemm_tasks, "lr_qr");
+        }
+        // CPQR of R (64 x 64): rank and the ordered basis Q2
+        c.lr_R64.ensure(size_t(nc) * p * p);
+        qr_take_r_kernel<<<nc, 256, 0, s>>>(m, p, c.lr_Y.p, ys, c.lr_R64.p);
         QPS_CUDA(cudaGetLastError());
+        CodSet& cs = c.lr_cod;
+        cs.ensure(nc, p, p, 1);
+        CodBatch b = cs.batch(c.lr_R64.p);
+        cod_factor_fast(b, s);
+        cod_rank(b, kLrTol, nullptr, s);
+        QPS_D2H(rk.data(), cs.rank.p, sizeof(int) * nc, s);
+        QPS_CUDA(cudaStreamSynchronize(s));
+        for (int v : rk) r = std::max(r, v);
+        if (getenv("QPS_LR_TRACE")) {
+            int mn = 1 << 30;
+            double mean = 0;
+            for (int v : rk) { mn = std::min(mn, v); mean += v; }
+            fprintf(stderr, "low-rank couplings: %d blocks, rank min %d mean %.1f max %d (sample %d)\n", nc, mn,
+                    mean / nc, r, kLrSample);
+        }
+        if (r > kLrMaxRank) return false;
+        r = kLrMaxRank;
+        c.lr_r = r;
+        // Q2 = first r columns of the R-CPQR's Q (64 x r)
+        c.lr_Q2.ensure(size_t(nc) * p * r);
+        c.lr_Q2H.ensure(size_t(nc) * p * r);
+        lr_form_q_kernel<<<dim3(nc, (r + 7) / 8), 256, size_t(8) * p * sizeof(cplx), s>>>(
+            p, p, r, cs.W.p, cs.tau.p, c.lr_Q2.p, p, size_t(p) * r, c.lr_Q2H.p, size_t(r) * p);
+        QPS_CUDA(cudaGetLastError());
+        // P = Q [Q2; 0], Q = (I - V0 T0 V0^*) ... (I - V3 T3 V3^*)
+        c.lr_P.ensure(size_t(nc) * nb * r);
+        c.lr_PH.ensure(size_t(nc) * r * nb);
+        qr_seed_kernel<<<nc, 256, 0, s>>>(m, p, r, c.lr_Q2.p, size_t(p) * r, c.lr_P.p, size_t(nb) * r);
+        QPS_CUDA(cudaGetLastError());
+        for (int pn = nP - 1; pn >= 0; --pn) {
+            std::vector<GemmTask> t1(nc), t2(nc), t3(nc);
+            for (int q = 0; q < nc; ++q) {
+                cplx* X = c.lr_P.p + size_t(q) * nb * r;
+                t1[q] = gemm1(VH_of(q, pn), kQrW, X, nb, m, c.lr_W1.p + size_t(q) * kQrW * p, kQrW);
+                t2[q] = gemm1(T_of(q, pn), kQrW, c.lr_W1.p + size_t(q) * kQrW * p, kQrW, kQrW,
+                              c.lr_W2.p + size_t(q) * kQrW * p, kQrW);
+                t3[q] = gemm1(V_of(q, pn), m, c.lr_W2.p + size_t(q) * kQrW * p, kQrW, kQrW, X, nb);
+            }
+            zgemm_batched(kQrW, r, cplx{1, 0}, cplx{0, 0}, t1, s, c.ws.gemm_tasks, "lr_qr");
+            zgemm_batched(kQrW, r, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks, "lr_qr");
+            zgemm_batched(m, r, cplx{-1, 0}, cplx{1, 0}, t3, s, c.ws.gemm_tasks, "lr_qr");
+        }
+        conj_transpose_kernel<<<dim3(64, nc), 256, 0, s>>>(nb, r, c.lr_P.p, size_t(nb) * r, c.lr_PH.p,
+                                                           size_t(r) * nb);
+        QPS_CUDA(cudaGetLastError());
+    } else {
+// column-pivoted QR of each sample, numerical rank
+        CodSet& cs = c.lr_cod;
+        cs.ensure(nc, nb, kLrSample, 1);
+        CodBatch b = cs.batch(c.lr_Y.p);
+        cod_factor_fast(b, s);
+        cod_rank(b, kLrTol, nullptr, s);
+        QPS_D2H(rk.data(), cs.rank.p, sizeof(int) * nc, s);
+        QPS_CUDA(cudaStreamSynchronize(s));
+        for (int v : rk) r = std::max(r, v);
+        if (getenv("QPS_LR_TRACE")) {
+            int mn = 1 << 30;
+            double mean = 0;
+            for (int v : rk) { mn = std::min(mn, v); mean += v; }
+            fprintf(stderr, "low-rank couplings: %d blocks, rank min %d mean %.1f max %d (sample %d)\n", nc, mn,
+                    mean / nc, r, kLrSample);
+        }
+        if (r > kLrMaxRank) return false;
+        // a fixed basis width keeps every system's factors independent of the batch
+        // it is solved in (the sweep's batched and one-at-a-time results agree)
+        r = kLrMaxRank;
+        c.lr_r = r;
+        // P (n x r) and P^* (r x n)
+        c.lr_P.ensure(size_t(nc) * nb * r);
+        c.lr_PH.ensure(size_t(nc) * r * nb);
+        {
+            ProfScope ps("lr_compress", s, 0.0);
+            static size_t attr = 0;
+            const size_t sm = size_t(8) * nb * sizeof(cplx);
+            if (sm > attr) {
+                QPS_CUDA(cudaFuncSetAttribute(lr_form_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              int(std::max<size_t>(sm, 48 * 1024))));
+                attr = std::max<size_t>(sm, 48 * 1024);
+            }
+            lr_form_q_kernel<<<dim3(nc, (r + 7) / 8), 256, size_t(8) * nb * sizeof(cplx), s>>>(
+                nb, kLrSample, r, cs.W.p, cs.tau.p, c.lr_P.p, nb, size_t(nb) * r, c.lr_PH.p, size_t(r) * nb);
+            QPS_CUDA(cudaGetLastError());
+        }
     }
     // R = P^* C  (= P^* A + (-P^* Bc) X when deferred)
     c.lr_R.ensure(size_t(nc) * r * nb);
@@ -389,6 +703,22 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
                         "singular diagonal factor (resonant parameters?) at layer " + std::to_string(worst + 1),
                         worst + 1);
     };
+    static const bool trace = getenv("QPS_BCR_TRACE") != nullptr;  // per-level timing to stderr (debug)
+    cudaEvent_t te0 = nullptr, te1 = nullptr;
+    if (trace) {
+        QPS_CUDA(cudaEventCreate(&te0));
+        QPS_CUDA(cudaEventCreate(&te1));
+        QPS_CUDA(cudaEventRecord(te0, s));
+    }
+    auto tmark = [&](const char* what, int l, int cnt) {
+        if (!trace) return;
+        float ms = 0;
+        QPS_CUDA(cudaEventRecord(te1, s));
+        QPS_CUDA(cudaEventSynchronize(te1));
+        QPS_CUDA(cudaEventElapsedTime(&ms, te0, te1));
+        fprintf(stderr, "lr-bcr level %d (%d odd) %s: %.3f ms\n", l, cnt, what, ms);
+        QPS_CUDA(cudaEventRecord(te0, s));
+    };
     int lvl = 0;
     while (levels[lvl][0].size() > 1) {
         Level& cur = levels[lvl];
@@ -412,6 +742,7 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
                 vb.push_back(p.F);
             }
         factor(fa, fp, fd, orig);
+        tmark("factor", lvl, int(fa.size()));
         {  // stage [PL PU] (zeros where a coupling is absent), then solve in place
             QPS_CUDA(cudaMemsetAsync(Zb.p, 0, sizeof(cplx) * size_t(ns) * nodd * nb * 2 * r, s));
             for (int a = 0; a < ns; ++a)
@@ -427,6 +758,7 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
             lu_solve_batched(nb, nb, fa, fp, fd, zb, nb, 2 * r, s, c.ws);
             lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
         }
+        tmark("solve", lvl, int(fa.size()));
         // 2. even positions: cores, products, rank-r updates, new couplings, RHS
         const int nsz = (sz + 1) / 2;
         DBuf<cplx>& Rn = c.lr_Rn[lvl];
@@ -500,6 +832,7 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
         zgemm_batched(nb, nb, mone, one, upd, s, c.ws.gemm_tasks, "bcr_update");
         zgemv_batched(r, one, zero, v1, s, c.ws.gemv_tasks);
         zgemv_batched(nb, mone, one, v2, s, c.ws.gemv_tasks);
+        tmark("update", lvl, int(fa.size()));
         levels.push_back(std::move(nxt));
         ++lvl;
     }
@@ -518,6 +851,7 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
         }
         factor(fa, fp, fd, orig);
         lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
+        tmark("final", lvl, int(fa.size()));
     }
     // back substitution: eta_o = z_o - Z_L (R_L(o) eta_{o-1}) - Z_U (R_U(o) eta_{o+1})
     for (int l = lvl - 1; l >= 0; --l) {
@@ -546,6 +880,304 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
             }
         zgemv_batched(r, one, zero, t1, s, c.ws.gemv_tasks);
         zgemv_batched(nb, mone, one, t2, s, c.ws.gemv_tasks);
+    }
+    tmark("backsub", lvl, 0);
+    if (trace) {
+        QPS_CUDA(cudaEventDestroy(te0));
+        QPS_CUDA(cudaEventDestroy(te1));
+    }
+    c.eta_valid = true;
+}
+
+// ---------------------------------------------------------------------------
+// Cyclic reduction through the Woodbury identity.  The even-position updates
+// never change a block's coupling bases: after any number of levels
+//   D_j = D_j^0 - [P_L P_U] S_j,        f_j = f_j^0 - [P_L P_U] g_j
+// with S_j (2r x n) and g_j (2r) accumulated from the rank-r products.  So every
+// diagonal block is LU-factored ONCE, all I of them in one batch at level 0
+// (W_j = D_j^0^{-1} [P_L P_U], y_j = D_j^0^{-1} f_j^0 in the same pass), and a
+// block eliminated at level l >= 1 needs only its 2r x 2r capacitance matrix:
+//   C = I - S W,   Z = D^{-1} [P_L P_U] = W C^{-1},
+//   u = y - W g,   z = D^{-1} f = u + Z (S u).
+// The deep levels (a handful of blocks each) become a few small GEMMs instead
+// of a latency-bound dense LU per level; the level-0 batch runs at throughput.
+// ---------------------------------------------------------------------------
+void bcr_solve_wb(Ctx& c, cplx* Ad) {
+    ProfPhase phase("bcr");
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, ns = D.nsys, r = c.lr_r, r2 = 2 * r;
+    const size_t nb2 = D.nb2();
+    cudaStream_t s = c.stream;
+    const cplx one{1, 0}, mone{-1, 0}, zero{0, 0};
+    const int npos = ns * I;
+    c.F.ensure(size_t(npos) * nb);
+    c.F.zero(s);
+    for (int a = 0; a < ns; ++a)
+        QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
+                                 cudaMemcpyDeviceToDevice, s));
+    c.ipiv.ensure(size_t(npos) * nb);
+    const size_t dsz = lu_dinv_elems(nb);
+    c.dinv.ensure(size_t(npos) * dsz);
+    c.lr_W0.ensure(size_t(npos) * nb * r2);
+    c.lr_S.ensure(size_t(npos) * r2 * nb);
+    c.lr_g.ensure(size_t(npos) * r2);
+    c.lr_S.zero(s);
+    c.lr_g.zero(s);
+    c.lr_core.ensure(size_t(npos) * 4 * r * r);
+    c.lr_vec.ensure(size_t(npos) * 4 * r);
+    static const bool trace = getenv("QPS_BCR_TRACE") != nullptr;  // per-level timing to stderr (debug)
+    cudaEvent_t te0 = nullptr, te1 = nullptr;
+    if (trace) {
+        QPS_CUDA(cudaEventCreate(&te0));
+        QPS_CUDA(cudaEventCreate(&te1));
+        QPS_CUDA(cudaEventRecord(te0, s));
+    }
+    auto tmark = [&](const char* what, int l, int cnt) {
+        if (!trace) return;
+        float ms = 0;
+        QPS_CUDA(cudaEventRecord(te1, s));
+        QPS_CUDA(cudaEventSynchronize(te1));
+        QPS_CUDA(cudaEventElapsedTime(&ms, te0, te1));
+        fprintf(stderr, "wb-bcr level %d (%d blocks) %s: %.3f ms\n", l, cnt, what, ms);
+        QPS_CUDA(cudaEventRecord(te0, s));
+    };
+    DBuf<int> flag;
+    auto check = [&](const std::vector<int>& orig) {
+        std::vector<int> hf(orig.size());
+        QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
+        QPS_CUDA(cudaStreamSynchronize(s));
+        int worst = -1;
+        for (size_t q = 0; q < hf.size(); ++q)
+            if (hf[q] && (worst < 0 || orig[q] < worst)) worst = orig[q];
+        if (worst >= 0)
+            throw Error(QPS_ERR_SOLVER,
+                        "singular diagonal factor (resonant parameters?) at layer " + std::to_string(worst + 1),
+                        worst + 1);
+    };
+    struct Pos {
+        int idx;
+        int j;  // a * I + idx: slot of the per-block buffers
+        cplx* F;
+        const cplx *PL, *RL, *PU, *RU;
+        const cplx* Z;  // D^{-1} [P_L P_U] once eliminated (n x 2r, ld n)
+        bool updated;   // S, g nonzero
+    };
+    using Level = std::vector<std::vector<Pos>>;
+    std::vector<Level> levels;
+    auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * r2; };
+    auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
+    auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2; };
+    // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
+    {
+        Level L0(ns);
+        const size_t per = size_t(nb) * r;
+        std::vector<cplx*> fa, fd, wb, vb;
+        std::vector<int*> fp;
+        std::vector<int> orig;
+        stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, per, c.lr_P.p, c.lr_W0.p);
+        QPS_CUDA(cudaGetLastError());
+        for (int a = 0; a < ns; ++a) {
+            const size_t qa = size_t(a) * 2 * (I - 1);
+            for (int j = 0; j < I; ++j) {
+                Pos p{};
+                p.idx = j;
+                p.j = a * I + j;
+                p.F = c.F.p + size_t(p.j) * nb;
+                if (j >= 1) {
+                    p.PL = c.lr_P.p + (qa + (j - 1)) * per;
+                    p.RL = c.lr_R.p + (qa + (j - 1)) * per;
+                }
+                if (j + 1 < I) {
+                    p.PU = c.lr_P.p + (qa + (I - 1) + j) * per;
+                    p.RU = c.lr_R.p + (qa + (I - 1) + j) * per;
+                }
+                p.Z = W0_of(p.j);
+                L0[a].push_back(p);
+                fa.push_back(Ad + size_t(a) * D.sA() + j * nb2);
+                fp.push_back(c.ipiv.p + size_t(p.j) * nb);
+                fd.push_back(c.dinv.p + size_t(p.j) * dsz);
+                wb.push_back(W0_of(p.j));
+                vb.push_back(p.F);
+                orig.push_back(j);
+            }
+        }
+        flag.ensure(fa.size());
+        flag.zero(s);
+        lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
+        check(orig);
+        tmark("factor", 0, int(fa.size()));
+        lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2, s, c.ws);
+        lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
+        tmark("solve", 0, int(fa.size()));
+        levels.push_back(std::move(L0));
+    }
+    int nlev = 0;
+    {
+        int n = I;
+        while (n > 1) { n = (n + 1) / 2; ++nlev; }
+    }
+    c.lr_Z.resize(std::max(nlev + 1, 1));
+    c.lr_Rn.resize(std::max(nlev, 1));
+    const size_t rr = size_t(r) * r, rn = size_t(r) * nb;
+    // eliminate the listed blocks at level lvl (updated ones through their
+    // capacitance matrix); sets Z and overwrites F with z = D^{-1} f
+    auto eliminate = [&](std::vector<Pos*>& blk, int lvl) {
+        std::vector<Pos*> up;
+        for (Pos* p : blk)
+            if (p->updated) up.push_back(p);
+        if (up.empty()) return;
+        const int cnt = int(up.size());
+        c.lr_Cm.ensure(size_t(cnt) * r2 * r2);
+        c.lr_Ci.ensure(size_t(cnt) * r2 * r2);
+        c.lr_Cpiv.ensure(size_t(cnt) * r2);
+        const size_t cds = lu_dinv_elems(r2);
+        c.lr_Cdinv.ensure(size_t(cnt) * cds);
+        c.lr_a.ensure(size_t(cnt) * r2);
+        DBuf<cplx>& Zb = c.lr_Z[lvl];
+        Zb.ensure(size_t(cnt) * nb * r2);
+        set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Cm.p);
+        set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Ci.p);
+        QPS_CUDA(cudaGetLastError());
+        std::vector<GemmTask> m(cnt), z(cnt);
+        std::vector<GemvTask> gu(cnt), ga(cnt), gz(cnt);
+        std::vector<cplx*> ca, cd, ci;
+        std::vector<int*> cp;
+        std::vector<int> orig;
+        for (int q = 0; q < cnt; ++q) {
+            Pos& p = *up[q];
+            const cplx* W = W0_of(p.j);
+            cplx* Cm = c.lr_Cm.p + size_t(q) * r2 * r2;
+            cplx* Ci = c.lr_Ci.p + size_t(q) * r2 * r2;
+            m[q] = gemm1(S_of(p.j), r2, W, nb, nb, Cm, r2);                       // C = I - S W
+            z[q] = gemm1(W, nb, Ci, r2, r2, Zb.p + size_t(q) * nb * r2, nb);       // Z = W C^{-1}
+            gu[q] = gemv1(W, nb, g_of(p.j), r2, p.F);                              // u = y - W g
+            ga[q] = gemv1(S_of(p.j), r2, p.F, nb, c.lr_a.p + size_t(q) * r2);      // a = S u
+            gz[q] = gemv1(Zb.p + size_t(q) * nb * r2, nb, c.lr_a.p + size_t(q) * r2, r2, p.F);  // z = u + Z a
+            ca.push_back(Cm);
+            ci.push_back(Ci);
+            cd.push_back(c.lr_Cdinv.p + size_t(q) * cds);
+            cp.push_back(c.lr_Cpiv.p + size_t(q) * r2);
+            orig.push_back(p.idx);
+            p.Z = Zb.p + size_t(q) * nb * r2;
+        }
+        zgemm_batched(r2, r2, mone, one, m, s, c.ws.gemm_tasks, "wb_cap");
+        flag.ensure(cnt);
+        flag.zero(s);
+        lu_factor_batched(r2, r2, ca, cp, cd, flag.p, s, c.ws);
+        check(orig);
+        lu_solve_batched(r2, r2, ca, cp, cd, ci, r2, r2, s, c.ws);
+        zgemm_batched(nb, r2, one, zero, z, s, c.ws.gemm_tasks, "wb_cap");
+        zgemv_batched(nb, mone, one, gu, s, c.ws.gemv_tasks);
+        zgemv_batched(r2, one, zero, ga, s, c.ws.gemv_tasks);
+        zgemv_batched(nb, one, one, gz, s, c.ws.gemv_tasks);
+    };
+    int lvl = 0;
+    while (levels[lvl][0].size() > 1) {
+        Level& cur = levels[lvl];
+        const int sz = int(cur[0].size());
+        std::vector<Pos*> odd;
+        for (int a = 0; a < ns; ++a)
+            for (int o = 1; o < sz; o += 2) odd.push_back(&cur[a][o]);
+        eliminate(odd, lvl);
+        tmark("eliminate", lvl, int(odd.size()));
+        // even positions: cores, accumulated S and g, new right factors
+        const int nsz = (sz + 1) / 2;
+        DBuf<cplx>& Rn = c.lr_Rn[lvl];
+        Rn.ensure(size_t(ns) * nsz * 2 * rn);
+        std::vector<GemmTask> cores, prods, newr;
+        std::vector<GemvTask> v1;
+        Level nxt(ns);
+        for (int a = 0; a < ns; ++a) {
+            for (int e = 0; e < sz; e += 2) {
+                const Pos& pe = cur[a][e];
+                const size_t slot = size_t(a) * nsz + e / 2;
+                cplx* core = c.lr_core.p + slot * 4 * rr;  // [LU, LL, UL, UU]
+                cplx* S = S_of(pe.j);
+                cplx* g = g_of(pe.j);
+                Pos np = pe;
+                np.PL = np.RL = np.PU = np.RU = nullptr;
+                const bool hm = e >= 1, hp = e + 1 < sz;
+                if (hm) {
+                    const Pos& po = cur[a][e - 1];
+                    const cplx* ZL = po.Z;
+                    const cplx* ZU = po.Z + size_t(nb) * r;
+                    cores.push_back(gemm1(pe.RL, r, ZU, nb, nb, core + 0 * rr, r));  // R_L(e) Z_U(o)
+                    cores.push_back(gemm1(pe.RL, r, ZL, nb, nb, core + 1 * rr, r));  // R_L(e) Z_L(o)
+                    prods.push_back(gemm1(core + 0 * rr, r, po.RU, r, r, S, r2));     // S_L += (R_L Z_U) R_U(o)
+                    if (e - 2 >= 0) {
+                        cplx* Rl = Rn.p + slot * 2 * rn;
+                        newr.push_back(gemm1(core + 1 * rr, r, po.RL, r, r, Rl, r));
+                        np.PL = pe.PL;
+                        np.RL = Rl;
+                    }
+                    v1.push_back(gemv1(pe.RL, r, po.F, nb, g));  // g_L += R_L(e) z(o)
+                    np.updated = true;
+                }
+                if (hp) {
+                    const Pos& po = cur[a][e + 1];
+                    const cplx* ZL = po.Z;
+                    const cplx* ZU = po.Z + size_t(nb) * r;
+                    cores.push_back(gemm1(pe.RU, r, ZL, nb, nb, core + 2 * rr, r));  // R_U(e) Z_L(o)
+                    cores.push_back(gemm1(pe.RU, r, ZU, nb, nb, core + 3 * rr, r));  // R_U(e) Z_U(o)
+                    prods.push_back(gemm1(core + 2 * rr, r, po.RL, r, r, S + r, r2));  // S_U += (R_U Z_L) R_L(o)
+                    if (e + 2 < sz) {
+                        cplx* Ru = Rn.p + slot * 2 * rn + rn;
+                        newr.push_back(gemm1(core + 3 * rr, r, po.RU, r, r, Ru, r));
+                        np.PU = pe.PU;
+                        np.RU = Ru;
+                    }
+                    v1.push_back(gemv1(pe.RU, r, po.F, nb, g + r));
+                    np.updated = true;
+                }
+                nxt[a].push_back(np);
+            }
+        }
+        zgemm_batched(r, r, one, zero, cores, s, c.ws.gemm_tasks, "lr_core");
+        zgemm_batched(r, nb, one, one, prods, s, c.ws.gemm_tasks, "lr_core");
+        zgemm_batched(r, nb, mone, zero, newr, s, c.ws.gemm_tasks, "lr_core");  // L' = P_L (-(core) R)
+        zgemv_batched(r, one, one, v1, s, c.ws.gemv_tasks);
+        tmark("update", lvl, int(odd.size()));
+        levels.push_back(std::move(nxt));
+        ++lvl;
+    }
+    {  // final block of every system
+        std::vector<Pos*> fin;
+        for (int a = 0; a < ns; ++a) fin.push_back(&levels[lvl][a][0]);
+        eliminate(fin, lvl);
+        tmark("final", lvl, int(fin.size()));
+    }
+    // back substitution: eta_o = z_o - Z_L (R_L(o) eta_{o-1}) - Z_U (R_U(o) eta_{o+1})
+    for (int l = lvl - 1; l >= 0; --l) {
+        const Level& cur = levels[l];
+        const int sz = int(cur[0].size());
+        std::vector<GemvTask> t1, t2;
+        for (int a = 0; a < ns; ++a)
+            for (int o = 1; o < sz; o += 2) {
+                const Pos& p = cur[a][o];
+                cplx* vec = c.lr_vec.p + size_t(p.j) * 4 * r;
+                GemvTask w{};
+                if (p.RL) {
+                    t1.push_back(gemv1(p.RL, r, cur[a][o - 1].F, nb, vec));
+                    w.A[w.nseg] = p.Z; w.lda[w.nseg] = nb; w.x[w.nseg] = vec; w.n[w.nseg] = r; ++w.nseg;
+                }
+                if (p.RU && o + 1 < sz) {
+                    t1.push_back(gemv1(p.RU, r, cur[a][o + 1].F, nb, vec + r));
+                    w.A[w.nseg] = p.Z + size_t(nb) * r; w.lda[w.nseg] = nb; w.x[w.nseg] = vec + r;
+                    w.n[w.nseg] = r;
+                    ++w.nseg;
+                }
+                if (w.nseg) {
+                    w.y = p.F;
+                    t2.push_back(w);
+                }
+            }
+        zgemv_batched(r, one, zero, t1, s, c.ws.gemv_tasks);
+        zgemv_batched(nb, mone, one, t2, s, c.ws.gemv_tasks);
+    }
+    tmark("backsub", lvl, 0);
+    if (trace) {
+        QPS_CUDA(cudaEventDestroy(te0));
+        QPS_CUDA(cudaEventDestroy(te1));
     }
     c.eta_valid = true;
 }

@@ -159,6 +159,7 @@ struct Ctx {
 
     // ---- low-rank couplings (bcr_lr.cu) ----
     DBuf<cplx> lr_omega, lr_Y, lr_P, lr_PH, lr_R, lr_core, lr_T, lr_vec, lr_W, lr_G;
+    DBuf<cplx> lr_V, lr_VH, lr_Tq, lr_THq, lr_W1, lr_W2, lr_R64, lr_Q2, lr_Q2H;  // blocked QR of the samples
     int lr_omega_n = 0, lr_r = 0;
     // coupling Schur updates A'_{j,j+1} = A - B X left to the compression
     // (one-shot path): [system][j] tasks of A_super and A_sub
@@ -168,6 +169,8 @@ struct Ctx {
     DBuf<GemmTask> lr_tasks;  // task table of the side2 stream's GEMMs
     CodSet lr_cod;
     std::vector<DBuf<cplx>> lr_Z, lr_Rn;
+    DBuf<cplx> lr_W0, lr_S, lr_g, lr_Cm, lr_Ci, lr_Cdinv, lr_a;  // Woodbury cyclic reduction
+    DBuf<int> lr_Cpiv;
 
     // ---- block cyclic reduction ----
     std::vector<BcrLevels> levels;  // [level][system]
@@ -219,6 +222,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al);
 void lr_sample_async(Ctx& c);
 // block cyclic reduction on the compressed couplings (after lr_compress)
 void bcr_solve_lr(Ctx& c, cplx* Ad);
+void bcr_solve_wb(Ctx& c, cplx* Ad);
 void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
                           int ldX, size_t Xstride, double* lsq_out);
 void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,

@@ -701,8 +701,15 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         const char* e = getenv("QPS_BCR");
         return e && !strcmp(e, "dense");
     }();
+    // low-rank reduction: through the Woodbury identity (one LU batch) unless
+    // QPS_BCR=lrdirect asks for a dense LU of every eliminated block per level
+    static const bool lr_direct = [] {
+        const char* e = getenv("QPS_BCR");
+        return e && !strcmp(e, "lrdirect");
+    }();
     if (!dense_only && lr_compress(c, Au, Al)) {
-        bcr_solve_lr(c, Ad);
+        if (lr_direct) bcr_solve_lr(c, Ad);
+        else bcr_solve_wb(c, Ad);
         c.couplings_deferred = false;
         return;
     }
