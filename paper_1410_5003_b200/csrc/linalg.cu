@@ -397,12 +397,16 @@ constexpr int kMaxP = 256;
 // kFast (low-rank compression only): reciprocal-multiplies instead of the
 // FP64 divisions on each column's critical path (~600 cycles each on B200);
 // the Schur least squares keep Eigen's divisions.
-template <bool kFast>
-__global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
+// kSmem: the whole m x p problem lives in shared memory (m p <= 13.7k entries,
+// e.g. the 160 x 80 interior least squares), copied out once at the end.
+extern __shared__ cplx cod_fac_sm[];
+template <bool kFast, bool kSmem>
+__global__ void __launch_bounds__(512) cod_factor_kernel(CodBatch b) {
     const int pb = blockIdx.x;
     const int m = b.m, p = b.p, size = min(m, p);
     const cplx* Q = b.Q + size_t(pb) * m * p;
-    cplx* W = b.W + size_t(pb) * m * p;
+    cplx* Wg = b.W + size_t(pb) * m * p;
+    cplx* W = kSmem ? cod_fac_sm : Wg;
     cplx* tau = b.tau + size_t(pb) * p;
     int* perm = b.perm + size_t(pb) * p;
     __shared__ double upd[kMaxP], dir[kMaxP];
@@ -555,6 +559,8 @@ __global__ void __launch_bounds__(256) cod_factor_kernel(CodBatch b) {
         b.nzp[pb] = s_nzp;
         b.maxpiv[pb] = s_maxpiv;
     }
+    if (kSmem)
+        for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) Wg[i] = W[i];
 }
 
 __global__ void cod_rank_kernel(CodBatch b, double th, const int* __restrict__ flags) {
@@ -1109,76 +1115,131 @@ __global__ void __launch_bounds__(256) lu_panel_kernel(int n, int ld, cplx* cons
 // block: [L^{-1} | U^{-1}] as two bs x bs column-major tiles (ld bs).
 __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap,
                                                       cplx* const* __restrict__ Op, int bs, int k0_first, int mode) {
+    // Blocked in 16 x 16 tiles: the diagonal tiles are inverted concurrently
+    // (64 threads each, a 16-step recurrence), then each block row of the
+    // inverse is two small tile products, X_ij = -X_ii sum_k T_ik X_kj, so the
+    // serial chain is 16 rows plus bs/16 - 1 product steps instead of bs rows.
+    // Tiles are padded to ld bs+1 (distinct banks for the columns of a warp).
     extern __shared__ cplx smem[];
-    cplx* T = smem;            // bs x bs block of the factor (column-major)
-    cplx* X = smem + bs * bs;  // inverse being built (column-major)
+    const int lp = bs + 1, nbk = bs / 16;
+    cplx* T = smem;            // bs x bs block of the factor (column-major, ld lp)
+    cplx* X = T + bs * lp;     // inverse being built
+    cplx* Y = X + bs * lp;     // 3 scratch 16 x 16 tiles (ld 16)
+    cplx* Dinv = Y + 3 * 256;  // bs reciprocals of the diagonal
     const cplx* A = Ap[blockIdx.y];
     cplx* O = Op[blockIdx.y] + size_t(blockIdx.x) * 2 * bs * bs;
     const int k0 = k0_first + blockIdx.x * bs;
     const int sz = min(bs, n - k0);
-    for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) {
+    const int tid = threadIdx.x;
+    // rows/columns past the matrix end act as identity
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
         const int i = e % bs, j = e / bs;
-        T[e] = (i < sz && j < sz) ? A[size_t(k0 + j) * ld + k0 + i] : cplx{0, 0};
+        T[j * lp + i] = (i < sz && j < sz) ? A[size_t(k0 + j) * ld + k0 + i] : cplx{i == j ? 1.0 : 0.0, 0.0};
     }
     __syncthreads();
-    const int j = threadIdx.x >> 2, part = threadIdx.x & 3;
-    const bool active = j < bs;
+    const int g = tid >> 6, t = tid & 63, jj = t >> 2, part = t & 3;  // diagonal-tile group, its column
+    const int pr = tid & 15, pc = tid >> 4;                             // tile-product element
     if (mode & 1) {
-        for (int i = 0; i < bs; ++i) {
-            cplx sacc{0, 0};
-            if (active && i > j)
-                for (int l = j + part; l < i; l += 4) {
-                    const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
-                    sacc.re += t.re;
-                    sacc.im += t.im;
-                }
-            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 1);
-            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 1);
-            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 2);
-            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
-            if (active && part == 0)
-                X[j * bs + i] = (i == j) ? cplx{1, 0} : (i > j && i < sz) ? cplx{-sacc.re, -sacc.im} : cplx{0, 0};
-            __syncwarp();
+        for (int e = tid; e < bs * lp; e += blockDim.x) X[e] = cplx{0, 0};
+        __syncthreads();
+        if (g < nbk) {  // unit-lower diagonal tiles
+            const int o = g * 16;
+            for (int i = 0; i < 16; ++i) {
+                cplx sacc{0, 0};
+                if (i > jj)
+                    for (int l = jj + part; l < i; l += 4) {
+                        const cplx v = cmul(T[(o + l) * lp + o + i], X[(o + jj) * lp + o + l]);
+                        sacc.re += v.re;
+                        sacc.im += v.im;
+                    }
+                sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 1);
+                sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 1);
+                sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 2);
+                sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
+                if (part == 0 && i >= jj) X[(o + jj) * lp + o + i] = (i == jj) ? cplx{1, 0} : cplx{-sacc.re, -sacc.im};
+                __syncwarp();
+            }
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) O[e] = X[e];
+        for (int bi = 1; bi < nbk; ++bi) {
+            for (int bj = 0; bj < bi; ++bj) {  // Y_bj = sum_{k=bj}^{bi-1} L_{bi,k} X_{k,bj}
+                cplx acc{0, 0};
+                for (int l = bj * 16; l < bi * 16; ++l) {
+                    const cplx v = cmul(T[l * lp + bi * 16 + pr], X[(bj * 16 + pc) * lp + l]);
+                    acc.re += v.re;
+                    acc.im += v.im;
+                }
+                Y[bj * 256 + pc * 16 + pr] = acc;
+            }
+            __syncthreads();
+            for (int bj = 0; bj < bi; ++bj) {  // X_{bi,bj} = -X_{bi,bi} Y_bj
+                cplx acc{0, 0};
+                for (int m = 0; m < 16; ++m) {
+                    const cplx v = cmul(X[(bi * 16 + m) * lp + bi * 16 + pr], Y[bj * 256 + pc * 16 + m]);
+                    acc.re += v.re;
+                    acc.im += v.im;
+                }
+                X[(bj * 16 + pc) * lp + bi * 16 + pr] = cplx{-acc.re, -acc.im};
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < bs * bs; e += blockDim.x) O[e] = X[(e / bs) * lp + e % bs];
         __syncthreads();
     }
     if (mode & 2) {
         // reciprocals of the diagonal, all at once (an FP64 division on the
         // substitution's critical path costs ~600 cycles per row)
-        cplx* Dinv = T + bs * bs + bs * bs;  // bs entries after X
-        for (int i = threadIdx.x; i < bs; i += blockDim.x) {
-            const cplx d = T[i * bs + i];
-            Dinv[i] = (i < sz && !(d.re == 0.0 && d.im == 0.0)) ? cdiv(cplx{1.0, 0.0}, d) : cplx{0, 0};
+        for (int i = tid; i < bs; i += blockDim.x) {
+            const cplx d = T[i * lp + i];
+            Dinv[i] = (d.re == 0.0 && d.im == 0.0) ? cplx{0, 0} : cdiv(cplx{1.0, 0.0}, d);
         }
+        for (int e = tid; e < bs * lp; e += blockDim.x) X[e] = cplx{0, 0};
         __syncthreads();
-        for (int i = bs - 1; i >= 0; --i) {
-            cplx sacc{0, 0};
-            if (active && i < j)
-                for (int l = i + 1 + part; l <= j; l += 4) {
-                    const cplx t = cmul(T[l * bs + i], X[j * bs + l]);
-                    sacc.re += t.re;
-                    sacc.im += t.im;
+        if (g < nbk) {  // upper diagonal tiles
+            const int o = g * 16;
+            for (int i = 15; i >= 0; --i) {
+                cplx sacc{0, 0};
+                if (i < jj)
+                    for (int l = i + 1 + part; l <= jj; l += 4) {
+                        const cplx v = cmul(T[(o + l) * lp + o + i], X[(o + jj) * lp + o + l]);
+                        sacc.re += v.re;
+                        sacc.im += v.im;
+                    }
+                sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 1);
+                sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 1);
+                sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 2);
+                sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
+                if (part == 0 && i <= jj) {
+                    const cplx num{(i == jj ? 1.0 : 0.0) - sacc.re, -sacc.im};
+                    X[(o + jj) * lp + o + i] = cmul(num, Dinv[o + i]);
                 }
-            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 1);
-            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 1);
-            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, 2);
-            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, 2);
-            if (active && part == 0) {
-                cplx v{0, 0};
-                if (i < sz && j < sz && i <= j) {
-                    const cplx num{(i == j ? 1.0 : 0.0) - sacc.re, -sacc.im};
-                    v = cmul(num, Dinv[i]);
-                } else if (i == j) {
-                    v = cplx{1, 0};
-                }
-                X[j * bs + i] = v;
+                __syncwarp();
             }
-            __syncwarp();
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) O[bs * bs + e] = X[e];
+        for (int bi = nbk - 2; bi >= 0; --bi) {
+            for (int bj = bi + 1; bj < nbk; ++bj) {  // Y_bj = sum_{k=bi+1}^{bj} U_{bi,k} X_{k,bj}
+                cplx acc{0, 0};
+                for (int l = (bi + 1) * 16; l < (bj + 1) * 16; ++l) {
+                    const cplx v = cmul(T[l * lp + bi * 16 + pr], X[(bj * 16 + pc) * lp + l]);
+                    acc.re += v.re;
+                    acc.im += v.im;
+                }
+                Y[(bj - bi - 1) * 256 + pc * 16 + pr] = acc;
+            }
+            __syncthreads();
+            for (int bj = bi + 1; bj < nbk; ++bj) {  // X_{bi,bj} = -X_{bi,bi} Y_bj
+                cplx acc{0, 0};
+                for (int m = 0; m < 16; ++m) {
+                    const cplx v = cmul(X[(bi * 16 + m) * lp + bi * 16 + pr], Y[(bj - bi - 1) * 256 + pc * 16 + m]);
+                    acc.re += v.re;
+                    acc.im += v.im;
+                }
+                X[(bj * 16 + pc) * lp + bi * 16 + pr] = cplx{-acc.re, -acc.im};
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < bs * bs; e += blockDim.x) O[bs * bs + e] = X[(e / bs) * lp + e % bs];
     }
 }
 
@@ -1744,20 +1805,36 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
     QPS_CUDA(cudaGetLastError());
 }
 
+constexpr size_t kCodFacSmemMax = 216 * 1024;
+template <bool kFast>
+void launch_cod_factor(const CodBatch& b, cudaStream_t s) {
+    const size_t sm = size_t(b.m) * b.p * sizeof(cplx);
+    if (sm <= kCodFacSmemMax) {
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_factor_kernel<kFast, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCodFacSmemMax)));
+            attr = true;
+        }
+        cod_factor_kernel<kFast, true><<<b.count, 512, sm, s>>>(b);
+    } else {
+        cod_factor_kernel<kFast, false><<<b.count, 256, 0, s>>>(b);
+    }
+    QPS_CUDA(cudaGetLastError());
+}
+
 void cod_factor(const CodBatch& b, cudaStream_t s) {
     if (b.count == 0) return;
     if (b.p > kMaxP) fail(QPS_ERR_CONFIG, "qsolve: too many columns for the device COD (max 256)");
     if (b.m < b.p) fail(QPS_ERR_USAGE, "qsolve: Q must have at least as many rows as columns");
     ProfScope ps("cod_factor", s, 8.0 * b.count * (2.0 * b.m * b.p * b.p - 2.0 * b.p * b.p * b.p / 3.0));
-    cod_factor_kernel<false><<<b.count, 256, 0, s>>>(b);
-    QPS_CUDA(cudaGetLastError());
+    launch_cod_factor<false>(b, s);
 }
 void cod_factor_fast(const CodBatch& b, cudaStream_t s) {
     if (b.count == 0) return;
     if (b.p > kMaxP || b.m < b.p) fail(QPS_ERR_INTERNAL, "cod_factor_fast: bad shape");
     ProfScope ps("lr_cpqr", s, 8.0 * b.count * (2.0 * b.m * b.p * b.p - 2.0 * b.p * b.p * b.p / 3.0));
-    cod_factor_kernel<true><<<b.count, 256, 0, s>>>(b);
-    QPS_CUDA(cudaGetLastError());
+    launch_cod_factor<true>(b, s);
 }
 void cod_rank(const CodBatch& b, double th, const int* flags, cudaStream_t s) {
     if (b.count == 0) return;
@@ -1817,15 +1894,16 @@ size_t lu_dinv_elems(int n) { return size_t(2) * ((n + kTB - 1) / kTB) * kTB * k
 namespace {
 void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, int bs, int k0_first, int nblk,
                     int mode, cudaStream_t s) {
-    const size_t sh = (2 * size_t(bs) * bs + bs) * sizeof(cplx);
+    // bs: a multiple of 16, <= kTB
+    const size_t sh = (2 * size_t(bs) * (bs + 1) + 3 * 256 + bs) * sizeof(cplx);
     static bool attr = false;
     if (!attr) {
         QPS_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int((2 * kTB * kTB + kTB) * sizeof(cplx))));
+                                      int((2 * kTB * (kTB + 1) + 3 * 256 + kTB) * sizeof(cplx))));
         attr = true;
     }
     ProfScope ps("tri_inv", s, 8.0 / 3.0 * count * nblk * double(bs) * bs * bs * ((mode == 3) ? 2 : 1));
-    tri_inv_kernel<<<dim3(nblk, count), 4 * bs, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
+    tri_inv_kernel<<<dim3(nblk, count), 256, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
     QPS_CUDA(cudaGetLastError());
 }
 }  // namespace
