@@ -45,6 +45,12 @@ namespace {
 
 constexpr int kTile = 32;
 constexpr int kThreads = 128;
+#ifndef QPS_MINB_PLAIN
+#define QPS_MINB_PLAIN 5  // blocks per SM: plain one-wavenumber tiles (96 registers)
+#endif
+#ifndef QPS_MINB_SELF
+#define QPS_MINB_SELF 4   // the others (128 registers)
+#endif
 constexpr int kNear = 4 * QPS_HANKEL_NEAR_TERMS * QPS_HANKEL_XB;
 
 __device__ __forceinline__ void load_near(double* s_near, const double* g_near) {
@@ -195,9 +201,12 @@ __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, Dev
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 4) pair_fill_kernel(const PairTask* __restrict__ tasks,
-                                                             const int4* __restrict__ tiles, DevPool pool,
-                                                             const double* __restrict__ g_near, int* err) {
+// one kernel per block kind (self kind x wavenumber count): each gets its own
+// register allocation instead of the largest of the six
+template <int SELF, int NK>
+__global__ void __launch_bounds__(kThreads, (SELF == 0 && NK == 1) ? QPS_MINB_PLAIN : QPS_MINB_SELF)
+    pair_fill_kernel(const PairTask* __restrict__ tasks, const int4* __restrict__ tiles, DevPool pool,
+                     const double* __restrict__ g_near, int* err) {
     __shared__ double2 s_near2[QPS_HANKEL_XB * QPS_HANKEL_NEAR_TERMS * 2];
     __shared__ double sx[kTile], sy[kTile], snx[kTile], sny[kTile], sw[kTile];
     __shared__ PairTask T;
@@ -218,14 +227,7 @@ __global__ void __launch_bounds__(kThreads, 4) pair_fill_kernel(const PairTask* 
         }
     }
     __syncthreads();
-    switch (T.self * 2 + (T.nk - 1)) {
-        case 0: pair_tile<0, 1>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
-        case 1: pair_tile<0, 2>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
-        case 2: pair_tile<1, 1>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
-        case 3: pair_tile<1, 2>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
-        case 4: pair_tile<2, 1>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
-        default: pair_tile<2, 2>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err); break;
-    }
+    pair_tile<SELF, NK>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err);
 }
 
 __global__ void __launch_bounds__(kThreads) proxy_fill_kernel(const ProxyTask* __restrict__ tasks,
@@ -544,16 +546,39 @@ void build_tiles(const std::vector<Task>& tasks, std::vector<int4>& tiles, int (
 void launch_pair_fill(const std::vector<PairTask>& tasks, const DevPool& pool, int* d_err, cudaStream_t s,
                       DBuf<PairTask>& d_tasks, DBuf<int4>& d_tiles) {
     if (tasks.empty()) return;
+    std::vector<int4> all;
+    build_tiles<PairTask>(tasks, all, [](const PairTask& t) { return t.ns; });
+    if (all.empty()) return;
+    // group the tiles by block kind (self * 2 + nk - 1), one launch per kind
     std::vector<int4> tiles;
-    build_tiles<PairTask>(tasks, tiles, [](const PairTask& t) { return t.ns; });
-    if (tiles.empty()) return;
+    tiles.reserve(all.size());
+    size_t off[7] = {0};
+    for (int kind = 0; kind < 6; ++kind) {
+        off[kind] = tiles.size();
+        for (const int4& t : all)
+            if (tasks[t.x].self * 2 + (tasks[t.x].nk - 1) == kind) tiles.push_back(t);
+    }
+    off[6] = tiles.size();
+    if (tiles.size() != all.size()) fail(QPS_ERR_INTERNAL, "pair fill: unknown block kind");
     d_tasks.upload(tasks, s);
     d_tiles.upload(tiles, s);
     double ev = 0;
     for (const auto& t : tasks) ev += double(t.nt) * t.ns * t.nterm * t.nk;
     ProfScope ps("fill_pair", s, 200.0 * ev, 0.0, ev);
-    pair_fill_kernel<<<unsigned(tiles.size()), kThreads, 0, s>>>(d_tasks.p, d_tiles.p, pool, g_near_table, d_err);
-    QPS_CUDA(cudaGetLastError());
+    for (int kind = 0; kind < 6; ++kind) {
+        const unsigned n = unsigned(off[kind + 1] - off[kind]);
+        if (!n) continue;
+        const int4* tl = d_tiles.p + off[kind];
+        switch (kind) {
+            case 0: pair_fill_kernel<0, 1><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 1: pair_fill_kernel<0, 2><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 2: pair_fill_kernel<1, 1><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 3: pair_fill_kernel<1, 2><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 4: pair_fill_kernel<2, 1><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            default: pair_fill_kernel<2, 2><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+        }
+        QPS_CUDA(cudaGetLastError());
+    }
 }
 
 void launch_proxy_fill(const std::vector<ProxyTask>& tasks, const DevPool& pool, int* d_err, cudaStream_t s,

@@ -30,7 +30,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-PRODUCT_LIB = os.path.join(_HERE, "libqpscat_b200.so")
+PRODUCT_LIB = os.environ.get("QPS_PRODUCT_LIB") or os.path.join(_HERE, "libqpscat_b200.so")  # override: dev A/B builds
 
 
 # ---------------------------------------------------------------- errors
