@@ -125,121 +125,106 @@ __global__ void __launch_bounds__(640, 1) qr_panel_kernel(int m, cplx* __restric
                                                           cplx* __restrict__ V, cplx* __restrict__ VH,
                                                           cplx* __restrict__ T, cplx* __restrict__ TH,
                                                           size_t vstride, size_t tstride) {
+    // Per column k: warp 0 forms the tail norm and the Householder scalars;
+    // one warp per inner product -- s_j = v_k^* a_j for the panel columns to
+    // the right, z_l = v_l^* v_k for the compact-WY factor -- each a single
+    // warp reduction (the thread-per-row layout would need 16 block
+    // reductions); then every thread applies H_k to its own row.
     extern __shared__ cplx qp[];  // [kQrW][m]
     const int b = blockIdx.x;
     cplx* Yb = Y + size_t(b) * ystride;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    __shared__ cplx red[32][kQrW];  // per-warp partial sums
-    __shared__ cplx tot[kQrW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    __shared__ cplx dots[kQrW];      // s_j (j > k) and z_l (l < k) of the current column
     __shared__ cplx s_tau, s_inv, s_beta;
     __shared__ cplx Ts[kQrW][kQrW];  // T~[row][col]
     const bool own = tid < m;
     if (own)
         for (int j = 0; j < kQrW; ++j) qp[j * m + tid] = Yb[size_t(col0 + j) * m + tid];
     __syncthreads();
-    // v_j on this row, rebuilt from the panel (qp holds v_j below the diagonal)
-    auto vrow = [&](int j) -> cplx {
+    // v_j at row i, rebuilt from the panel (qp holds v_j below the diagonal)
+    auto vat = [&](int j, int i) -> cplx {
         const int d = col0 + j;
-        if (!own || tid < d) return cplx{0, 0};
-        if (tid == d) return cplx{1.0, 0.0};
-        return qp[j * m + tid];
+        if (i < d) return cplx{0, 0};
+        if (i == d) return cplx{1.0, 0.0};
+        return qp[j * m + i];
     };
     for (int k = 0; k < kQrW; ++k) {
         const int g0 = col0 + k;
-        // tail norm of column k below the diagonal
-        double t2 = (own && tid > g0) ? cabs2(qp[k * m + tid]) : 0.0;
-        for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-        if (lane == 0) red[warp][0].re = t2;
-        __syncthreads();
-        if (tid == 0) {
-            double tail = 0.0;
-            for (int w = 0; w < nw; ++w) tail += red[w][0].re;
-            const cplx c0 = qp[k * m + g0];
-            if (tail <= DBL_MIN && c0.im * c0.im <= DBL_MIN) {  // makeHouseholder's no-op case
-                s_tau = cplx{0, 0};
-                s_beta = c0;
-                s_inv = cplx{0, 0};
-            } else {
-                double beta = sqrt(cabs2(c0) + tail);
-                if (c0.re >= 0.0) beta = -beta;
-                const cplx den{c0.re - beta, c0.im};
-                s_inv = cdiv(cplx{1.0, 0.0}, den);
-                s_tau = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
-                s_beta = cplx{beta, 0.0};
-            }
-        }
-        __syncthreads();
-        const cplx tau = s_tau;
-        // v_k on this row
-        cplx v{0, 0};
-        if (own) {
-            if (tid == g0) {
-                v = cplx{1.0, 0.0};
-                qp[k * m + tid] = s_beta;
-            } else if (tid > g0) {
-                v = cmul(qp[k * m + tid], s_inv);
-                qp[k * m + tid] = v;
-            }
-        }
-        // one reduction: s_j = v_k^* a_j (j > k) and z_l = v_l^* v_k (l < k)
-        // (two halves of eight to keep the partials in registers)
-#pragma unroll
-        for (int h = 0; h < kQrW; h += kQrW / 2) {
-            cplx part[kQrW / 2];
-#pragma unroll
-            for (int jj = 0; jj < kQrW / 2; ++jj) {
-                const int j = h + jj;
-                cplx a{0, 0};
-                if (j > k && own) a = qp[j * m + tid];
-                else if (j < k) a = vrow(j);
-                // j > k: conj(v) a ; j < k: conj(v_j) v
-                part[jj] = (j > k) ? cplx{v.re * a.re + v.im * a.im, v.re * a.im - v.im * a.re}
-                                   : cplx{a.re * v.re + a.im * v.im, a.re * v.im - a.im * v.re};
-            }
-#pragma unroll
-            for (int jj = 0; jj < kQrW / 2; ++jj) {
-                for (int o = 16; o > 0; o >>= 1) {
-                    part[jj].re += __shfl_xor_sync(0xffffffffu, part[jj].re, o);
-                    part[jj].im += __shfl_xor_sync(0xffffffffu, part[jj].im, o);
+        if (warp == 0) {  // tail norm of column k below the diagonal, Householder scalars
+            double t2 = 0.0;
+            for (int i = g0 + 1 + lane; i < m; i += 32) t2 += cabs2(qp[k * m + i]);
+            for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+            if (lane == 0) {
+                const cplx c0 = qp[k * m + g0];
+                if (t2 <= DBL_MIN && c0.im * c0.im <= DBL_MIN) {  // makeHouseholder's no-op case
+                    s_tau = cplx{0, 0};
+                    s_beta = c0;
+                    s_inv = cplx{0, 0};
+                } else {
+                    double beta = sqrt(cabs2(c0) + t2);
+                    if (c0.re >= 0.0) beta = -beta;
+                    const cplx den{c0.re - beta, c0.im};
+                    s_inv = cdiv(cplx{1.0, 0.0}, den);
+                    s_tau = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
+                    s_beta = cplx{beta, 0.0};
                 }
             }
-            if (lane == 0)
-#pragma unroll
-                for (int jj = 0; jj < kQrW / 2; ++jj) red[warp][h + jj] = part[jj];
         }
         __syncthreads();
-        if (tid < kQrW) {
-            cplx sacc{0, 0};
-            for (int w = 0; w < nw; ++w) {
-                sacc.re += red[w][tid].re;
-                sacc.im += red[w][tid].im;
+        const cplx tau = s_tau, inv = s_inv;
+        // inner products over rows >= g0 (v_k vanishes above): task w < kQrW - 1
+        // is j = k + 1 + w (w < 15 - k) or l = w - (15 - k), one warp each
+        for (int task = warp; task < kQrW - 1; task += nwarp) {
+            const int nright = kQrW - 1 - k;
+            const bool right = task < nright;
+            const int c = right ? k + 1 + task : task - nright;
+            cplx acc{0, 0};
+            for (int i = g0 + lane; i < m; i += 32) {
+                const cplx vk = (i == g0) ? cplx{1.0, 0.0} : cmul(qp[k * m + i], inv);
+                const cplx a = right ? qp[c * m + i] : vat(c, i);
+                if (right) {  // conj(v_k) a_j
+                    acc.re += vk.re * a.re + vk.im * a.im;
+                    acc.im += vk.re * a.im - vk.im * a.re;
+                } else {      // conj(v_l) v_k
+                    acc.re += a.re * vk.re + a.im * vk.im;
+                    acc.im += a.re * vk.im - a.im * vk.re;
+                }
             }
-            tot[tid] = sacc;
+            for (int o = 16; o > 0; o >>= 1) {
+                acc.re += __shfl_xor_sync(0xffffffffu, acc.re, o);
+                acc.im += __shfl_xor_sync(0xffffffffu, acc.im, o);
+            }
+            if (lane == 0) dots[c] = acc;
         }
         __syncthreads();
-        if (tid == 0) {  // T~ column k: T~[k][k] = conj(tau), T~[0:k, k] = -conj(tau) T~[0:k,0:k] z
+        if (warp == 0 && lane < kQrW) {  // T~ column k: T~[k][k] = conj(tau), T~[0:k, k] = -conj(tau) T~[0:k,0:k] z
+            const int l = lane;
             const cplx ct = cconj(tau);
-            for (int l = 0; l < k; ++l) {
+            cplx val{0, 0};
+            if (l < k) {
                 cplx acc{0, 0};
                 for (int q = l; q < k; ++q) {
-                    const cplx t = cmul(Ts[l][q], tot[q]);
+                    const cplx t = cmul(Ts[l][q], dots[q]);
                     acc.re += t.re;
                     acc.im += t.im;
                 }
-                const cplx val = cmul(ct, acc);
-                Ts[l][k] = cplx{-val.re, -val.im};
+                const cplx u = cmul(ct, acc);
+                val = cplx{-u.re, -u.im};
+            } else if (l == k) {
+                val = ct;
             }
-            Ts[k][k] = ct;
-            for (int l = k + 1; l < kQrW; ++l) Ts[l][k] = cplx{0, 0};
+            Ts[l][k] = val;
         }
-        // apply H_k = I - tau v v^* to the panel columns j > k
-        if (own && !(tau.re == 0.0 && tau.im == 0.0)) {
-            for (int j = k + 1; j < kQrW; ++j) {
-                const cplx ts = cmul(tau, tot[j]);
-                const cplx d = cmul(ts, v);
-                qp[j * m + tid].re -= d.re;
-                qp[j * m + tid].im -= d.im;
-            }
+        // apply H_k = I - tau v v^* to this row of the panel columns j > k
+        if (own && tid >= g0) {
+            const cplx vk = (tid == g0) ? cplx{1.0, 0.0} : cmul(qp[k * m + tid], inv);
+            qp[k * m + tid] = (tid == g0) ? s_beta : vk;
+            if (!(tau.re == 0.0 && tau.im == 0.0))
+                for (int j = k + 1; j < kQrW; ++j) {
+                    const cplx d = cmul(cmul(tau, dots[j]), vk);
+                    qp[j * m + tid].re -= d.re;
+                    qp[j * m + tid].im -= d.im;
+                }
         }
         __syncthreads();
     }
@@ -250,7 +235,7 @@ __global__ void __launch_bounds__(640, 1) qr_panel_kernel(int m, cplx* __restric
 #pragma unroll
         for (int j = 0; j < kQrW; ++j) {
             Yb[size_t(col0 + j) * m + tid] = (tid <= col0 + j) ? qp[j * m + tid] : cplx{0, 0};
-            const cplx vj = vrow(j);
+            const cplx vj = vat(j, tid);
             Vb[size_t(j) * m + tid] = vj;
             VHb[size_t(tid) * kQrW + j] = cconj(vj);
         }

@@ -1794,7 +1794,29 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
     const char* nm = family ? family : (kmax <= 64) ? (M <= 64 ? "zgemm_k64_m64" : "zgemm_k64") : (M >= 256 && N >= 256 ? "zgemm_big" : "zgemm_mid");
     ProfScope ps(nm, s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
     if (!four_m) {
-        launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+        // tile by shape (tools/micro/gemm_cfg.cu on B200): 16 x 64 for thin
+        // products (M <= 48, or M <= 80 against a wide N), 32 x 32 for short K
+        // and small outputs (more CTAs, shorter prologue), 64 x 32 otherwise
+        // in-place products (C aliasing B, M <= 64: the triangular-tile solves)
+        // need every row of a column tile in one CTA -- the 64-row tile
+        const bool inplace = tasks[0].C == tasks[0].B[0];
+        static const bool fixed_tile = [] {  // QPS_ZGEMM_TILE=fixed: the 64 x 32 tile for every shape (debug)
+            const char* e = getenv("QPS_ZGEMM_TILE");
+            return e && !strcmp(e, "fixed");
+        }();
+        if (inplace || fixed_tile) {
+            if (inplace && M > 64) {
+                fprintf(stderr, "zgemm_batched: in-place M=%d N=%d K=%d ntasks=%zu nseg=%d\n", M, N, tasks[0].K[0],
+                        tasks.size(), tasks[0].nseg);
+                fail(QPS_ERR_INTERNAL, "zgemm_batched: in-place product taller than one tile");
+            }
+            launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+        } else if (M <= 48 || (M <= 80 && N >= 256))
+            launch_z3<2, 2, 1, 4, 2, 4>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+        else if (kmax <= 96 || (M <= 128 && N <= 128))
+            launch_z3<2, 2, 2, 2, 2, 4>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+        else
+            launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
     } else {
         const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
         for (size_t off = 0; off < tasks.size(); off += 65535) {

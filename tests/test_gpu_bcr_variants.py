@@ -3,7 +3,9 @@ reduction, low-rank reduction with a dense LU per eliminated block
 (QPS_BCR=lrdirect) and the default Woodbury reduction (one LU batch, 2r x 2r
 capacitance solves per level).  The solver variant is read once per process,
 so each runs in its own subprocess (tools/lowrank_check.py) on the config-4
-prefix (50 interfaces, 608-point blocks: the low-rank path is eligible)."""
+prefix (50 interfaces, 608-point blocks) and the config-5 prefix (4
+interfaces, blocks narrower than the QR panel kernel's warp count): the
+low-rank path is eligible for both."""
 import json
 import os
 import subprocess
@@ -15,13 +17,13 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(variant, tmp_path):
-    out = str(tmp_path / f"a_{variant or 'default'}.npy")
+def _run(variant, tmp_path, cfg, nif):
+    out = str(tmp_path / f"a_{cfg}_{variant or 'default'}.npy")
     env = dict(os.environ)
     env.pop("QPS_BCR", None)
     if variant:
         env["QPS_BCR"] = variant
-    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "lowrank_check.py"), "4", "50", out],
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "lowrank_check.py"), str(cfg), str(nif), out],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     res = json.loads(p.stdout.strip().splitlines()[-1])
@@ -29,10 +31,11 @@ def _run(variant, tmp_path):
 
 
 @pytest.mark.gpu
-def test_bcr_variants_agree(tmp_path):
-    a_wb, r_wb = _run(None, tmp_path)
-    a_lr, r_lr = _run("lrdirect", tmp_path)
-    a_dn, r_dn = _run("dense", tmp_path)
+@pytest.mark.parametrize("cfg,nif", [(4, 50), (5, 4)])
+def test_bcr_variants_agree(tmp_path, cfg, nif):
+    a_wb, r_wb = _run(None, tmp_path, cfg, nif)
+    a_lr, r_lr = _run("lrdirect", tmp_path, cfg, nif)
+    a_dn, r_dn = _run("dense", tmp_path, cfg, nif)
     n = np.linalg.norm
     # rtol 1e-10 on the Bragg amplitudes: the coupling truncation (relative
     # 1e-14 of each block) and the Woodbury capacitance solves sit far below it
