@@ -282,17 +282,21 @@ __global__ void set_identity_kernel(int n, cplx* __restrict__ C) {
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) Cb[e] = cplx{(e % n == e / n) ? 1.0 : 0.0, 0.0};
 }
 
-// W_j = [P_L(j) P_U(j)] (zeros where a coupling is absent) for every block j of
-// every system; P holds per system the I-1 sub- then the I-1 super-couplings
-__global__ void stage_bases_kernel(int I, size_t per, const cplx* __restrict__ P, cplx* __restrict__ W) {
+// W_j = [P_L(j) P_U(j) f_j] (zeros where a coupling is absent; f_j the n-vector
+// of block j, ld n) for every block j of every system, so that one solve
+// gives D^{-1} [P_L P_U] and D^{-1} f; P holds per system the I-1 sub- then
+// the I-1 super-couplings
+__global__ void stage_bases_kernel(int I, int n, size_t per, const cplx* __restrict__ P, const cplx* __restrict__ F,
+                                   cplx* __restrict__ W) {
     const int j = blockIdx.x, a = j / I, jj = j % I;
     const size_t qa = size_t(a) * 2 * (I - 1);
     const cplx* pl = jj >= 1 ? P + (qa + (jj - 1)) * per : nullptr;
     const cplx* pu = jj + 1 < I ? P + (qa + (I - 1) + jj) * per : nullptr;
-    cplx* w = W + size_t(j) * 2 * per;
+    cplx* w = W + size_t(j) * (2 * per + n);
     for (size_t e = size_t(blockIdx.y) * blockDim.x + threadIdx.x; e < per; e += size_t(gridDim.y) * blockDim.x) {
         w[e] = pl ? pl[e] : cplx{0, 0};
         w[per + e] = pu ? pu[e] : cplx{0, 0};
+        if (e < size_t(n)) w[2 * per + e] = F[size_t(j) * n + e];
     }
 }
 
@@ -903,7 +907,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     c.ipiv.ensure(size_t(npos) * nb);
     const size_t dsz = lu_dinv_elems(nb);
     c.dinv.ensure(size_t(npos) * dsz);
-    c.lr_W0.ensure(size_t(npos) * nb * r2);
+    c.lr_W0.ensure(size_t(npos) * nb * (r2 + 1));  // [W | y] per block
     c.lr_S.ensure(size_t(npos) * r2 * nb);
     c.lr_g.ensure(size_t(npos) * r2);
     c.lr_S.zero(s);
@@ -949,7 +953,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     };
     using Level = std::vector<std::vector<Pos>>;
     std::vector<Level> levels;
-    auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * r2; };
+    auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * (r2 + 1); };
     auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
     auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2; };
     // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
@@ -959,7 +963,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         std::vector<cplx*> fa, fd, wb, vb;
         std::vector<int*> fp;
         std::vector<int> orig;
-        stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, per, c.lr_P.p, c.lr_W0.p);
+        stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, c.lr_W0.p);
         QPS_CUDA(cudaGetLastError());
         for (int a = 0; a < ns; ++a) {
             const size_t qa = size_t(a) * 2 * (I - 1);
@@ -991,8 +995,10 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
         check(orig);
         tmark("factor", 0, int(fa.size()));
-        lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2, s, c.ws);
-        lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
+        lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, s, c.ws);
+        // y = D^{-1} f back into F (column 2r of every W_j)
+        QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * nb, c.lr_W0.p + size_t(r2) * nb,
+                                   sizeof(cplx) * nb * (r2 + 1), sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
         tmark("solve", 0, int(fa.size()));
         levels.push_back(std::move(L0));
     }
