@@ -1015,6 +1015,84 @@ __global__ void __launch_bounds__(256) cod_trsm_chunk_kernel(CodBatch b, cplx* B
     }
 }
 
+// Blocked back substitution (LAPACK trsm order, no explicit inverse): 16-row
+// diagonal blocks solved by substitution with 8 lanes per column, the rows
+// above updated by the solved block as small products.  T11 packed (upper,
+// column-major) and 32 columns per CTA keep two CTAs per SM; the serial chain
+// is r row steps of <= 16-term dot products instead of up-to-r-term ones.
+constexpr int kTrsmBlkCols = 32;
+__global__ void __launch_bounds__(256) cod_trsm_blk_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
+                                                           const int* __restrict__ flags) {
+    extern __shared__ cplx tbk[];
+    const int pb = blockIdx.y;
+    if (flags && !flags[pb]) return;
+    const int m = b.m, r = b.rank[pb];
+    if (r == 0) return;
+    const cplx* V = b.V + size_t(pb) * m * b.p;
+    const int lx = r + 1;                          // X ld: the 4 columns of a warp in distinct banks
+    cplx* T = tbk;                                 // packed upper: (i, j) at j (j + 1) / 2 + i
+    cplx* X = T + size_t(r) * (r + 1) / 2;         // r x kTrsmBlkCols (ld lx)
+    cplx* Tinv = X + size_t(lx) * kTrsmBlkCols;    // reciprocals of the diagonal
+    const int c0 = blockIdx.x * kTrsmBlkCols;
+    const int nc = min(kTrsmBlkCols, ncols - c0);
+    cplx* Bp = B + stride * pb + size_t(c0) * ldb;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < r * r; e += blockDim.x) {
+        const int i = e % r, j = e / r;
+        if (i <= j) T[j * (j + 1) / 2 + i] = V[size_t(j) * m + i];
+    }
+    for (int e = tid; e < r * nc; e += blockDim.x) {
+        const int i = e % r, j = e / r;
+        X[j * lx + i] = Bp[size_t(j) * ldb + i];
+    }
+    __syncthreads();
+    for (int i = tid; i < r; i += blockDim.x) Tinv[i] = cdiv(cplx{1.0, 0.0}, T[i * (i + 1) / 2 + i]);
+    __syncthreads();
+    const int col = tid >> 3, part = tid & 7;
+    const bool active = col < nc;
+    for (int b1 = r; b1 > 0; b1 -= 16) {
+        const int b0 = max(0, b1 - 16);
+        // diagonal block: rows b1-1 .. b0 by substitution
+        for (int i = b1 - 1; i >= b0; --i) {
+            cplx sacc{0, 0};
+            if (active)
+                for (int l = i + 1 + part; l < b1; l += 8) {
+                    const cplx t = cmul(T[l * (l + 1) / 2 + i], X[col * lx + l]);
+                    sacc.re += t.re;
+                    sacc.im += t.im;
+                }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, o);
+                sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, o);
+            }
+            if (active && part == 0) {
+                const cplx bi = X[col * lx + i];
+                X[col * lx + i] = cmul(cplx{bi.re - sacc.re, bi.im - sacc.im}, Tinv[i]);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // rows above: X[i] -= T[i, b0:b1] X[b0:b1]
+        for (int e = tid; e < b0 * nc; e += blockDim.x) {
+            const int i = e % b0, c = e / b0;
+            cplx acc{0, 0};
+            for (int l = b0; l < b1; ++l) {
+                const cplx t = cmul(T[l * (l + 1) / 2 + i], X[c * lx + l]);
+                acc.re += t.re;
+                acc.im += t.im;
+            }
+            X[c * lx + i].re -= acc.re;
+            X[c * lx + i].im -= acc.im;
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < r * nc; e += blockDim.x) {
+        const int i = e % r, j = e / r;
+        Bp[size_t(j) * ldb + i] = X[j * lx + i];
+    }
+}
+
 template <bool kSmem>
 __global__ void __launch_bounds__(128) cod_trsm_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
                                                        const int* __restrict__ flags) {
@@ -1887,7 +1965,21 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
     const size_t sh = size_t(b.p) * b.p * sizeof(cplx);
     const dim3 grid((ncols + 127) / 128, b.count);
     const size_t shc = (size_t(b.p) * b.p + size_t(b.p) * kTrsmCols + b.p) * sizeof(cplx);
-    if (shc <= 200 * 1024) {
+    const size_t shb = (size_t(b.p) * (b.p + 1) / 2 + size_t(b.p + 1) * kTrsmBlkCols + b.p) * sizeof(cplx);
+    static const bool unblocked = [] {  // QPS_COD_TRSM=row: the row-by-row kernel
+        const char* e = getenv("QPS_COD_TRSM");
+        return e && !strcmp(e, "row");
+    }();
+    if (!unblocked && shb <= 110 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_trsm_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(110 * 1024)));
+            attr = true;
+        }
+        cod_trsm_blk_kernel<<<dim3((ncols + kTrsmBlkCols - 1) / kTrsmBlkCols, b.count), 256, shb, s>>>(
+            b, B, ldb, stride, ncols, flags);
+    } else if (shc <= 200 * 1024) {
         static bool attr = false;
         if (!attr) {
             QPS_CUDA(cudaFuncSetAttribute(cod_trsm_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
