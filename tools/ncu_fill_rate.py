@@ -30,4 +30,12 @@ for r in rows[2:]:
                 "warps_active_pct": float(d["sm__warps_active.avg.pct_of_peak_sustained_active"]),
                 "registers": int(float(d["launch__registers_per_thread"])),
                 "evals_per_s": (evals / (t_ms * 1e-3)) if evals else None})
+if len(res) > 1:  # all captured kinds together: total flops over total time
+    tt = sum(r["duration_ms"] for r in res)
+    fl = sum(r["fp64_tflops_ncu"] * r["duration_ms"] for r in res)
+    pk = sum(r["fp64_peak_tflops_ncu"] * r["duration_ms"] for r in res)
+    res.append({"kernel": "all captured launches", "duration_ms": tt, "fp64_tflops_ncu": fl / tt,
+                "fp64_peak_tflops_ncu": pk / tt, "fp64_frac_of_peak": fl / pk,
+                "fp64_pipe_pct": sum(r["fp64_pipe_pct"] * r["duration_ms"] for r in res) / tt,
+                "evals_per_s": (evals / (tt * 1e-3)) if evals else None})
 print(json.dumps(res, indent=1))
