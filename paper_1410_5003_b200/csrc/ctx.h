@@ -1,5 +1,6 @@
 // Solver context: everything one qps_ctx owns on host and device.
 #pragma once
+#include <chrono>
 
 #include <array>
 #include <string>
@@ -193,6 +194,7 @@ struct Ctx {
     qps_phase_times times{};
     uint64_t ref_evals = 0, performed_evals = 0;
     Workspace ws;
+    std::chrono::steady_clock::time_point host_t0;  // QPS_HOST_TRACE
     DBuf<PairTask> d_pair;
     DBuf<ProxyTask> d_proxy;
     DBuf<AlpertTask> d_alpert;

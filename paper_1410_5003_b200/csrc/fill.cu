@@ -210,11 +210,14 @@ __global__ void __launch_bounds__(kThreads, (SELF == 0 && NK == 1) ? QPS_MINB_PL
     __shared__ double2 s_near2[QPS_HANKEL_XB * QPS_HANKEL_NEAR_TERMS * 2];
     __shared__ double sx[kTile], sy[kTile], snx[kTile], sny[kTile], sw[kTile];
     __shared__ PairTask T;
-    const int4 tile = tiles[blockIdx.x];
-    if (threadIdx.x == 0) T = tasks[tile.x];
+    // blockIdx.y: task of this kind {task index, row tiles, total tiles};
+    // blockIdx.x: tile within the task (row tiles fastest)
+    const int4 tk = tiles[blockIdx.y];
+    if (int(blockIdx.x) >= tk.z) return;
+    if (threadIdx.x == 0) T = tasks[tk.x];
     load_near2(s_near2, g_near);
     __syncthreads();
-    const int m0 = tile.y, j0 = tile.z;
+    const int m0 = (int(blockIdx.x) % tk.y) * kTile, j0 = (int(blockIdx.x) / tk.y) * kTile;
     if (threadIdx.x < kTile) {
         const int j = j0 + threadIdx.x;
         if (j < T.ns) {
@@ -546,36 +549,46 @@ void build_tiles(const std::vector<Task>& tasks, std::vector<int4>& tiles, int (
 void launch_pair_fill(const std::vector<PairTask>& tasks, const DevPool& pool, int* d_err, cudaStream_t s,
                       DBuf<PairTask>& d_tasks, DBuf<int4>& d_tiles) {
     if (tasks.empty()) return;
+    // one launch per block kind (self * 2 + nk - 1) over a 2-D grid (tile,
+    // task of the kind): the tile of a CTA is computed in-kernel, so no tile
+    // list is built on the host or uploaded
+    std::vector<int4> ids[6];
+    int maxt[6] = {0};
+    for (int t = 0; t < int(tasks.size()); ++t) {
+        const PairTask& T = tasks[t];
+        const int kind = T.self * 2 + (T.nk - 1);
+        if (kind < 0 || kind > 5) fail(QPS_ERR_INTERNAL, "pair fill: unknown block kind");
+        const int tm = (T.nt + kTile - 1) / kTile, tn = (T.ns + kTile - 1) / kTile;
+        if (tm * tn == 0) continue;
+        ids[kind].push_back(make_int4(t, tm, tm * tn, 0));
+        maxt[kind] = std::max(maxt[kind], tm * tn);
+    }
     std::vector<int4> all;
-    build_tiles<PairTask>(tasks, all, [](const PairTask& t) { return t.ns; });
-    if (all.empty()) return;
-    // group the tiles by block kind (self * 2 + nk - 1), one launch per kind
-    std::vector<int4> tiles;
-    tiles.reserve(all.size());
     size_t off[7] = {0};
     for (int kind = 0; kind < 6; ++kind) {
-        off[kind] = tiles.size();
-        for (const int4& t : all)
-            if (tasks[t.x].self * 2 + (tasks[t.x].nk - 1) == kind) tiles.push_back(t);
+        off[kind] = all.size();
+        all.insert(all.end(), ids[kind].begin(), ids[kind].end());
     }
-    off[6] = tiles.size();
-    if (tiles.size() != all.size()) fail(QPS_ERR_INTERNAL, "pair fill: unknown block kind");
+    off[6] = all.size();
+    if (all.empty()) return;
     d_tasks.upload(tasks, s);
-    d_tiles.upload(tiles, s);
+    d_tiles.upload(all, s);
     double ev = 0;
     for (const auto& t : tasks) ev += double(t.nt) * t.ns * t.nterm * t.nk;
     ProfScope ps("fill_pair", s, 200.0 * ev, 0.0, ev);
     for (int kind = 0; kind < 6; ++kind) {
         const unsigned n = unsigned(off[kind + 1] - off[kind]);
         if (!n) continue;
+        if (n > 65535) fail(QPS_ERR_CONFIG, "pair fill: too many blocks of one kind for one launch");
         const int4* tl = d_tiles.p + off[kind];
+        const dim3 grid(unsigned(maxt[kind]), n);
         switch (kind) {
-            case 0: pair_fill_kernel<0, 1><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 1: pair_fill_kernel<0, 2><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 2: pair_fill_kernel<1, 1><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 3: pair_fill_kernel<1, 2><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 4: pair_fill_kernel<2, 1><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            default: pair_fill_kernel<2, 2><<<n, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 0: pair_fill_kernel<0, 1><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 1: pair_fill_kernel<0, 2><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 2: pair_fill_kernel<1, 1><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 3: pair_fill_kernel<1, 2><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 4: pair_fill_kernel<2, 1><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            default: pair_fill_kernel<2, 2><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
         }
         QPS_CUDA(cudaGetLastError());
     }

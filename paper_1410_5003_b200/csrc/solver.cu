@@ -1,3 +1,4 @@
+#include <chrono>
 // Orchestration of the hot path on one B200:
 //   fill_system_fused  : every block of BlockSystem (assembly.hpp:293-483) in
 //                        three launches (pair, proxy, Alpert), alpha fused in
@@ -211,6 +212,7 @@ void fill_system_fused(Ctx& c) {
     cudaStream_t s = c.stream;
     const size_t nb2 = size_t(nb) * nb;
 
+    c.host_t0 = std::chrono::steady_clock::now();
     alloc_system(c);
     if (D.padded) {
         bool uniform = true;
@@ -423,9 +425,18 @@ void fill_system_fused(Ctx& c) {
     }
 
     const DevPool pool{c.px.p, c.py.p, c.pnx.p, c.pny.p, c.pw.p};
+    static const bool htrace = getenv("QPS_HOST_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
     launch_pair_fill(pt, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
+    auto t1 = std::chrono::steady_clock::now();
     launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.d_err.p, s, c.d_alpert);
     launch_proxy_fill(xt, pool, c.d_err.p, s, c.d_proxy, c.d_tiles);
+    auto t2 = std::chrono::steady_clock::now();
+    if (htrace)
+        fprintf(stderr, "fill host: task build %.3f ms, pair launch %.3f ms, alpert+proxy launch %.3f ms\n",
+                std::chrono::duration<double, std::milli>(t0 - c.host_t0).count(),
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
 
     write_radiation_and_rhs(c, {c.prob});
     if (D.padded) pad_identity(c);
