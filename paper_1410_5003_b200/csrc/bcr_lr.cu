@@ -29,24 +29,13 @@
 #include <cstdio>
 #include <cstring>
 
+#include "cmath.cuh"
 #include "ctx.h"
 #include "prof.h"
 
 namespace qpsb {
 
 namespace {
-
-__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return cplx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
-__device__ __forceinline__ cplx cconj(cplx a) { return cplx{a.re, -a.im}; }
-__device__ __forceinline__ double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
-__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {  // Smith's algorithm
-    if (fabs(b.re) >= fabs(b.im)) {
-        const double r = b.im / b.re, den = b.re + b.im * r;
-        return cplx{(a.re + a.im * r) / den, (a.im - a.re * r) / den};
-    }
-    const double r = b.re / b.im, den = b.re * r + b.im;
-    return cplx{(a.re * r + a.im) / den, (a.im * r - a.re) / den};
-}
 
 constexpr int kLrSample = 64;    // columns of the random sample
 constexpr int kLrMaxRank = 48;   // beyond this the dense reduction is used
@@ -134,7 +123,7 @@ __global__ void __launch_bounds__(640, 1) qr_panel_kernel(int m, cplx* __restric
     const int b = blockIdx.x;
     cplx* Yb = Y + size_t(b) * ystride;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-    __shared__ cplx dots[kQrW];      // s_j (j > k) and z_l (l < k) of the current column
+    __shared__ cplx dots[kQrW + 1];  // s_j (j > k), z_l (l < k) and the tail norm of the current column
     __shared__ cplx s_tau, s_inv, s_beta;
     __shared__ cplx Ts[kQrW][kQrW];  // T~[row][col]
     const bool own = tid < m;
@@ -150,11 +139,41 @@ __global__ void __launch_bounds__(640, 1) qr_panel_kernel(int m, cplx* __restric
     };
     for (int k = 0; k < kQrW; ++k) {
         const int g0 = col0 + k;
-        if (warp == 0) {  // tail norm of column k below the diagonal, Householder scalars
-            double t2 = 0.0;
-            for (int i = g0 + 1 + lane; i < m; i += 32) t2 += cabs2(qp[k * m + i]);
-            for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        // phase 1, one warp per task over rows > g0 with the raw column a_k
+        // (v_k = a_k / den below the diagonal, so the scale is applied after):
+        // tasks 0..14-k: raw_j = a_k^* a_j (j > k); next k: raw_l = v_l^* a_k
+        // (l < k); task 15: the tail norm |a_k|^2
+        for (int task = warp; task < kQrW; task += nwarp) {
+            const int nright = kQrW - 1 - k;
+            cplx acc{0, 0};
+            if (task == kQrW - 1) {
+                for (int i = g0 + 1 + lane; i < m; i += 32) acc.re += cabs2(qp[k * m + i]);
+            } else {
+                const bool right = task < nright;
+                const int c = right ? k + 1 + task : task - nright;
+                for (int i = g0 + 1 + lane; i < m; i += 32) {
+                    const cplx ak = qp[k * m + i];
+                    const cplx a = qp[c * m + i];  // a_j, or v_l (i > g0 lies below v_l's unit entry)
+                    if (right) {  // conj(a_k) a_j
+                        acc.re += ak.re * a.re + ak.im * a.im;
+                        acc.im += ak.re * a.im - ak.im * a.re;
+                    } else {      // conj(v_l) a_k
+                        acc.re += a.re * ak.re + a.im * ak.im;
+                        acc.im += a.re * ak.im - a.im * ak.re;
+                    }
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                acc.re += __shfl_xor_sync(0xffffffffu, acc.re, o);
+                acc.im += __shfl_xor_sync(0xffffffffu, acc.im, o);
+            }
+            if (lane == 0) dots[task == kQrW - 1 ? kQrW : (task < nright ? k + 1 + task : task - nright)] = acc;
+        }
+        __syncthreads();
+        // phase 2 (warp 0): Householder scalars, scaled inner products, T~ column k
+        if (warp == 0) {
             if (lane == 0) {
+                const double t2 = dots[kQrW].re;
                 const cplx c0 = qp[k * m + g0];
                 if (t2 <= DBL_MIN && c0.im * c0.im <= DBL_MIN) {  // makeHouseholder's no-op case
                     s_tau = cplx{0, 0};
@@ -163,59 +182,49 @@ __global__ void __launch_bounds__(640, 1) qr_panel_kernel(int m, cplx* __restric
                 } else {
                     double beta = sqrt(cabs2(c0) + t2);
                     if (c0.re >= 0.0) beta = -beta;
-                    const cplx den{c0.re - beta, c0.im};
-                    s_inv = cdiv(cplx{1.0, 0.0}, den);
-                    s_tau = cconj(cdiv(cplx{beta - c0.re, -c0.im}, cplx{beta, 0.0}));
+                    s_inv = fast_cinv(cplx{c0.re - beta, c0.im});
+                    const double rb = fast_rcp(beta);
+                    s_tau = cplx{(beta - c0.re) * rb, c0.im * rb};  // conj((beta - c0) / beta)
                     s_beta = cplx{beta, 0.0};
                 }
             }
+            __syncwarp();
+            const cplx inv = s_inv;
+            if (lane < kQrW && lane != k) {
+                const cplx raw = dots[lane];
+                if (lane > k) {  // s_j = conj(inv) raw + a_j[g0]
+                    const cplx t = cmul(cconj(inv), raw);
+                    const cplx a0 = qp[lane * m + g0];
+                    dots[lane] = cplx{t.re + a0.re, t.im + a0.im};
+                } else {         // z_l = inv raw + conj(v_l[g0])
+                    const cplx t = cmul(inv, raw);
+                    const cplx vl = vat(lane, g0);
+                    dots[lane] = cplx{t.re + vl.re, t.im - vl.im};
+                }
+            }
+            __syncwarp();
+            if (lane < kQrW) {  // T~[k][k] = conj(tau), T~[0:k, k] = -conj(tau) T~[0:k,0:k] z
+                const int l = lane;
+                const cplx ct = cconj(s_tau);
+                cplx val{0, 0};
+                if (l < k) {
+                    cplx acc{0, 0};
+                    for (int q = l; q < k; ++q) {
+                        const cplx t = cmul(Ts[l][q], dots[q]);
+                        acc.re += t.re;
+                        acc.im += t.im;
+                    }
+                    const cplx u = cmul(ct, acc);
+                    val = cplx{-u.re, -u.im};
+                } else if (l == k) {
+                    val = ct;
+                }
+                Ts[l][k] = val;
+            }
         }
         __syncthreads();
+        // phase 3: apply H_k = I - tau v v^* to this row of the panel columns j > k
         const cplx tau = s_tau, inv = s_inv;
-        // inner products over rows >= g0 (v_k vanishes above): task w < kQrW - 1
-        // is j = k + 1 + w (w < 15 - k) or l = w - (15 - k), one warp each
-        for (int task = warp; task < kQrW - 1; task += nwarp) {
-            const int nright = kQrW - 1 - k;
-            const bool right = task < nright;
-            const int c = right ? k + 1 + task : task - nright;
-            cplx acc{0, 0};
-            for (int i = g0 + lane; i < m; i += 32) {
-                const cplx vk = (i == g0) ? cplx{1.0, 0.0} : cmul(qp[k * m + i], inv);
-                const cplx a = right ? qp[c * m + i] : vat(c, i);
-                if (right) {  // conj(v_k) a_j
-                    acc.re += vk.re * a.re + vk.im * a.im;
-                    acc.im += vk.re * a.im - vk.im * a.re;
-                } else {      // conj(v_l) v_k
-                    acc.re += a.re * vk.re + a.im * vk.im;
-                    acc.im += a.re * vk.im - a.im * vk.re;
-                }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                acc.re += __shfl_xor_sync(0xffffffffu, acc.re, o);
-                acc.im += __shfl_xor_sync(0xffffffffu, acc.im, o);
-            }
-            if (lane == 0) dots[c] = acc;
-        }
-        __syncthreads();
-        if (warp == 0 && lane < kQrW) {  // T~ column k: T~[k][k] = conj(tau), T~[0:k, k] = -conj(tau) T~[0:k,0:k] z
-            const int l = lane;
-            const cplx ct = cconj(tau);
-            cplx val{0, 0};
-            if (l < k) {
-                cplx acc{0, 0};
-                for (int q = l; q < k; ++q) {
-                    const cplx t = cmul(Ts[l][q], dots[q]);
-                    acc.re += t.re;
-                    acc.im += t.im;
-                }
-                const cplx u = cmul(ct, acc);
-                val = cplx{-u.re, -u.im};
-            } else if (l == k) {
-                val = ct;
-            }
-            Ts[l][k] = val;
-        }
-        // apply H_k = I - tau v v^* to this row of the panel columns j > k
         if (own && tid >= g0) {
             const cplx vk = (tid == g0) ? cplx{1.0, 0.0} : cmul(qp[k * m + tid], inv);
             qp[k * m + tid] = (tid == g0) ? s_beta : vk;
