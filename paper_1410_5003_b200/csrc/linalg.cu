@@ -1708,29 +1708,41 @@ __global__ void maxabs_kernel(const cplx* X, int m, int n, int ld, size_t stride
     }
 }
 
-__global__ void fro_kernel(const cplx* X, int m, int n, int ld, size_t stride, double* out) {
+// Frobenius norm in one pass (plain sum of squares, as Eigen's norm()); the
+// max-scaled second pass runs only when the sum leaves the normal range.
+// maxo (optional): the max modulus from the same pass.
+__global__ void fro_kernel(const cplx* X, int m, int n, int ld, size_t stride, double* out, double* maxo) {
     const cplx* A = X + stride * blockIdx.x;
     __shared__ double sh[32];
-    double mx = 0.0;
+    double mx = 0.0, s = 0.0;
     for (int j = 0; j < n; ++j)
-        for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, sqrt(cabs2(A[size_t(j) * ld + i])));
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double a2 = cabs2(A[size_t(j) * ld + i]);
+            s += a2;
+            mx = fmax(mx, a2);
+        }
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
     __syncthreads();
     double big = 0.0;
     for (int w = 0; w < int(blockDim.x >> 5); ++w) big = fmax(big, sh[w]);
+    big = sqrt(big);
     __syncthreads();
-    double s = 0.0;
-    if (big > 0.0) {
+    double tot = block_sum(s, sh);
+    if (!(tot < 1e300) || (tot < 1e-290 && big > 0.0)) {  // out of range: rescale by the max
         const double inv = 1.0 / big;
+        s = 0.0;
         for (int j = 0; j < n; ++j)
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
                 const cplx a = A[size_t(j) * ld + i];
                 s += (a.re * inv) * (a.re * inv) + (a.im * inv) * (a.im * inv);
             }
+        tot = block_sum(s, sh);
+        if (threadIdx.x == 0) out[blockIdx.x] = big * sqrt(tot);
+    } else if (threadIdx.x == 0) {
+        out[blockIdx.x] = sqrt(tot);
     }
-    const double tot = block_sum(s, sh);
-    if (threadIdx.x == 0) out[blockIdx.x] = big * sqrt(tot);
+    if (maxo && threadIdx.x == 0) maxo[blockIdx.x] = big;
 }
 
 __global__ void copy_blocks_kernel(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride,
@@ -2265,10 +2277,11 @@ void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int coun
     maxabs_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out);
     QPS_CUDA(cudaGetLastError());
 }
-void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {
+void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s,
+                 double* maxabs_out) {
     if (count == 0) return;
-    ProfScope ps("reduce", s, 0.0, 32.0 * count * double(m) * n);
-    fro_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out);
+    ProfScope ps("reduce", s, 0.0, 16.0 * count * double(m) * n);
+    fro_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out, maxabs_out);
     QPS_CUDA(cudaGetLastError());
 }
 void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride, int m, int n,

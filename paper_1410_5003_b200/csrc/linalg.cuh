@@ -79,7 +79,8 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& A, const std::vec
 // per problem max |X_ij| over an m x n block (ld), count problems with stride
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s);
 // per problem Frobenius norm
-void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s);
+void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s,
+                 double* maxabs_out = nullptr);
 void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride, int m, int n,
                  int count, cudaStream_t s);
 // y_b = beta y_b + alpha * sum_s A_s x_s  (batched complex GEMV, up to 2 terms)

@@ -502,7 +502,8 @@ void qsolve_families(Ctx& c, std::vector<QFamily>& fams) {
         CodBatch b = cs.batch(f.Q);
         cod_factor(b, f.s);
         // scale = max(1, max |RHS|)
-        batched_maxabs(f.R, cs.m, cs.ncols, f.ldR, f.Rstride, cs.count, cs.rmax.p, f.s);
+        // max |RHS| (the acceptance scale) and ||RHS||_F (the residual's denominator) in one pass
+        batched_fro(f.R, cs.m, cs.ncols, f.ldR, f.Rstride, cs.count, cs.rnorm.p, f.s, cs.rmax.p);
         f.rmax.assign(cs.count, 0.0);
         f.xmax.assign(cs.count, 0.0);
         f.flags.assign(cs.count, 1);
@@ -583,7 +584,6 @@ void qsolve_families(Ctx& c, std::vector<QFamily>& fams) {
         }
         zgemm_batched(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, f.s, cs.tasks1);
         batched_fro(cs.E.p, cs.m, cs.ncols, cs.m, size_t(cs.m) * cs.ncols, cnt, cs.enorm.p, f.s);
-        batched_fro(f.R, cs.m, cs.ncols, f.ldR, f.Rstride, cnt, cs.rnorm.p, f.s);
         f.rmax.assign(cnt, 0.0);  // reused: residual norms
         f.xmax.assign(cnt, 0.0);
         QPS_D2H(f.rmax.data(), cs.enorm.p, sizeof(double) * cnt, f.s);
