@@ -32,9 +32,9 @@ struct Dims {
 // COD least-squares state for one family of equal-shape problems
 struct CodSet {
     int count = 0, m = 0, p = 0, ncols = 0;
-    DBuf<cplx> W, V, tau, zc, M1, Y, QH, Wz, Tb, E;
+    DBuf<cplx> W, V, tau, zc, M1, Y, QH, Wz, Tb;
     DBuf<int> perm, nzp, rank, flags;
-    DBuf<double> maxpiv, xmax, rmax, enorm, rnorm;
+    DBuf<double> maxpiv, xmax, rmax, enorm, rnorm, parts;
     DBuf<GemmTask> tasks1, tasks2;  // task tables of this family's GEMMs (families run on separate streams)
     CodBatch batch(const cplx* Q) {
         CodBatch b;
@@ -48,7 +48,6 @@ struct CodSet {
         const size_t mp = size_t(m) * p;
         W.ensure(cnt * mp); V.ensure(cnt * mp); M1.ensure(cnt * mp); Y.ensure(cnt * mp); QH.ensure(cnt * mp);
         Wz.ensure(size_t(cnt) * p * p); Tb.ensure(size_t(cnt) * p * ncols);
-        E.ensure(size_t(cnt) * m * ncols);
         tau.ensure(size_t(cnt) * p); zc.ensure(size_t(cnt) * p); perm.ensure(size_t(cnt) * p);
         nzp.ensure(cnt); rank.ensure(cnt); flags.ensure(cnt);
         maxpiv.ensure(cnt); xmax.ensure(cnt); rmax.ensure(cnt); enorm.ensure(cnt); rnorm.ensure(cnt);

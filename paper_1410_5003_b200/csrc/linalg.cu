@@ -181,9 +181,14 @@ struct Z3Cfg {
     static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double2);
 };
 
-template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+// kNorm: the epilogue stores nothing; it sums |alpha A B + beta C|^2 over the
+// tile and writes the CTA's partial to norm_part[(task0 + blockIdx.y) *
+// gridDim.x + blockIdx.x] (C is only read) -- a residual norm without the
+// residual's HBM round trip.
+template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool kNorm = false>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
-    zgemm3m_t_kernel(int M, int N, cplx alpha, cplx beta, const GemmTask* __restrict__ tasks, int tiles_m) {
+    zgemm3m_t_kernel(int M, int N, cplx alpha, cplx beta, const GemmTask* __restrict__ tasks, int tiles_m,
+                     double* __restrict__ norm_part = nullptr, size_t task0 = 0) {
     using Cfg = Z3Cfg<WMT, WNT, WARPS_M, WARPS_N, STAGES>;
     constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, NT = Cfg::NT, LDA = Cfg::LDA, LDK = Cfg::LDK;
     extern __shared__ double2 z3_smem[];
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     }
     cp_async_wait<0>();
     const bool use_beta = (beta.re != 0.0 || beta.im != 0.0);
+    double ss = 0.0;
 #pragma unroll
     for (int i = 0; i < WMT; ++i)
 #pragma unroll
@@ -292,25 +298,55 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
                         out.re += beta.re * o.re - beta.im * o.im;
                         out.im += beta.re * o.im + beta.im * o.re;
                     }
-                    *p = out;
+                    if (kNorm) ss += out.re * out.re + out.im * out.im;
+                    else *p = out;
                 }
             }
+    if (kNorm) {
+        __syncthreads();  // the staging buffers are free: reuse for the partials
+        double* red = reinterpret_cast<double*>(z3_smem);
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) red[warp] = ss;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < NT / 32; ++w) t += red[w];
+            norm_part[(task0 + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+        }
+    }
 }
 
-template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB = (WARPS_M * WARPS_N <= 4) ? 2 : 1>
-void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_t ntasks, cudaStream_t s) {
+__global__ void norm_parts_kernel(const double* __restrict__ part, int nparts, int ntasks, double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntasks) return;
+    double s = 0.0;
+    for (int q = 0; q < nparts; ++q) s += part[size_t(t) * nparts + q];
+    out[t] = sqrt(s);
+}
+
+template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB = (WARPS_M * WARPS_N <= 4) ? 2 : 1,
+          bool kNorm = false>
+void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_t ntasks, cudaStream_t s,
+               DBuf<double>* parts = nullptr, double* norms = nullptr) {
     using Cfg = Z3Cfg<WMT, WNT, WARPS_M, WARPS_N, STAGES>;
-    auto kern = zgemm3m_t_kernel<WMT, WNT, WARPS_M, WARPS_N, STAGES, MINB>;
+    auto kern = zgemm3m_t_kernel<WMT, WNT, WARPS_M, WARPS_N, STAGES, MINB, kNorm>;
     static bool attr = false;
     if (!attr) {
         QPS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
         attr = true;
     }
     const int tiles_m = (M + Cfg::BM - 1) / Cfg::BM, tiles_n = (N + Cfg::BN - 1) / Cfg::BN;
+    const int tiles = tiles_m * tiles_n;
+    if (kNorm) parts->ensure(ntasks * tiles);
     for (size_t off = 0; off < ntasks; off += 65535) {
         const unsigned cnt = unsigned(std::min<size_t>(65535, ntasks - off));
-        kern<<<dim3(tiles_m * tiles_n, cnt), Cfg::NT, Cfg::SMEM, s>>>(M, N, alpha, beta, tasks + off, tiles_m);
+        kern<<<dim3(tiles, cnt), Cfg::NT, Cfg::SMEM, s>>>(M, N, alpha, beta, tasks + off, tiles_m,
+                                                         kNorm ? parts->p : nullptr, off);
         ++g_zgemm_launches;
+    }
+    if (kNorm) {
+        norm_parts_kernel<<<unsigned((ntasks + 127) / 128), 128, 0, s>>>(parts->p, tiles, int(ntasks), norms);
+        QPS_CUDA(cudaGetLastError());
     }
 }
 
@@ -1881,6 +1917,26 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
             zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
         }
     }
+    QPS_CUDA(cudaGetLastError());
+}
+
+void zgemm_residual_norms(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
+                          DBuf<GemmTask>& d_tasks, DBuf<double>& parts, double* norms) {
+    if (tasks.empty() || M <= 0 || N <= 0) return;
+    d_tasks.upload(tasks, s);
+    int kmax = 0;
+    double fl = 0;
+    for (const auto& t : tasks)
+        for (int q = 0; q < t.nseg; ++q) {
+            kmax = std::max(kmax, t.K[q]);
+            fl += 6.0 * M * N * t.K[q];
+        }
+    ProfScope ps("zgemm_resid", s, fl, 16.0 * double(M) * N * tasks.size());
+    // same tiles as zgemm_batched's rule (the residual shapes: M = m rows of Q)
+    if (kmax <= 96 || (M <= 128 && N <= 128))
+        launch_z3<2, 2, 2, 2, 2, 4, true>(M, N, alpha, beta, d_tasks.p, tasks.size(), s, &parts, norms);
+    else
+        launch_z3<4, 2, 2, 2, 2, 3, true>(M, N, alpha, beta, d_tasks.p, tasks.size(), s, &parts, norms);
     QPS_CUDA(cudaGetLastError());
 }
 

@@ -29,6 +29,10 @@ extern std::atomic<uint64_t> g_zgemm_launches;
 // family: profiling name (string literal); default by shape
 void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
                    DBuf<GemmTask>& d_tasks, const char* family = nullptr);
+// norms[t] = || alpha A_t B_t + beta C_t ||_F per task, C only read (the
+// product is reduced in the GEMM epilogue, never stored); parts: scratch
+void zgemm_residual_norms(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
+                          DBuf<GemmTask>& d_tasks, DBuf<double>& parts, double* norms);
 
 // ---- COD least squares -----------------------------------------------------
 // Per problem b: Q_b (m x p, ld m).  Factor state lives in caller-provided

@@ -569,7 +569,7 @@ void qsolve_families(Ctx& c, std::vector<QFamily>& fams) {
         CodSet& cs = *f.cs;
         const int cnt = cs.count;
         if (cnt == 0) continue;
-        copy_blocks(f.R, f.ldR, f.Rstride, cs.E.p, cs.m, size_t(cs.m) * cs.ncols, cs.m, cs.ncols, cnt, f.s);
+        // ||Q X - R||_F reduced in the GEMM epilogue (R only read, Q X - R never stored)
         std::vector<GemmTask> tasks(cnt);
         for (int q = 0; q < cnt; ++q) {
             GemmTask& t = tasks[q];
@@ -579,11 +579,10 @@ void qsolve_families(Ctx& c, std::vector<QFamily>& fams) {
             t.B[0] = f.X + f.Xstride * q;
             t.ldb[0] = f.ldX;
             t.K[0] = cs.p;
-            t.C = cs.E.p + size_t(q) * cs.m * cs.ncols;
-            t.ldc = cs.m;
+            t.C = const_cast<cplx*>(f.R) + f.Rstride * q;
+            t.ldc = f.ldR;
         }
-        zgemm_batched(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, f.s, cs.tasks1);
-        batched_fro(cs.E.p, cs.m, cs.ncols, cs.m, size_t(cs.m) * cs.ncols, cnt, cs.enorm.p, f.s);
+        zgemm_residual_norms(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, f.s, cs.tasks1, cs.parts, cs.enorm.p);
         f.rmax.assign(cnt, 0.0);  // reused: residual norms
         f.xmax.assign(cnt, 0.0);
         QPS_D2H(f.rmax.data(), cs.enorm.p, sizeof(double) * cnt, f.s);
