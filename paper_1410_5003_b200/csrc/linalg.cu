@@ -1194,35 +1194,40 @@ __global__ void __launch_bounds__(256) lu_panel_kernel(int n, int ld, cplx* cons
 // threads) split each dot product; a column's lanes share a warp, so the
 // row-by-row recurrences need only warp-level synchronisation.  Output per
 // block: [L^{-1} | U^{-1}] as two bs x bs column-major tiles (ld bs).
-__global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap,
+__global__ void __launch_bounds__(512) tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap,
                                                       cplx* const* __restrict__ Op, int bs, int k0_first, int mode) {
     // Blocked in 16 x 16 tiles: the diagonal tiles are inverted concurrently
     // (64 threads each, a 16-step recurrence), then each block row of the
     // inverse is two small tile products, X_ij = -X_ii sum_k T_ik X_kj, so the
     // serial chain is 16 rows plus bs/16 - 1 product steps instead of bs rows.
     // Tiles are padded to ld bs+1 (distinct banks for the columns of a warp).
+    // mode 3 runs with 512 threads: L^{-1} on threads 0-255 and U^{-1} on
+    // 256-511 at the same time, each half with its own buffers and barrier.
     extern __shared__ cplx smem[];
     const int lp = bs + 1, nbk = bs / 16;
-    cplx* T = smem;            // bs x bs block of the factor (column-major, ld lp)
-    cplx* X = T + bs * lp;     // inverse being built
-    cplx* Y = X + bs * lp;     // 3 scratch 16 x 16 tiles (ld 16)
-    cplx* Dinv = Y + 3 * 256;  // bs reciprocals of the diagonal
+    const int half = (mode == 3) ? int(threadIdx.x >> 8) : 0;
+    const int which = (mode == 3) ? (half ? 2 : 1) : mode;  // 1: lower, 2: upper
+    cplx* T = smem;                                          // bs x bs block of the factor (ld lp)
+    cplx* X = T + bs * lp + half * bs * lp;                  // inverse being built
+    cplx* Y = T + 3 * bs * lp + half * 768;                  // 3 scratch 16 x 16 tiles (ld 16)
+    cplx* Dinv = T + 3 * bs * lp + 2 * 768;                  // bs reciprocals of the diagonal
     const cplx* A = Ap[blockIdx.y];
-    cplx* O = Op[blockIdx.y] + size_t(blockIdx.x) * 2 * bs * bs;
+    cplx* O = Op[blockIdx.y] + size_t(blockIdx.x) * 2 * bs * bs + (which == 2 ? size_t(bs) * bs : 0);
     const int k0 = k0_first + blockIdx.x * bs;
     const int sz = min(bs, n - k0);
-    const int tid = threadIdx.x;
     // rows/columns past the matrix end act as identity
-    for (int e = tid; e < bs * bs; e += blockDim.x) {
+    for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) {
         const int i = e % bs, j = e / bs;
         T[j * lp + i] = (i < sz && j < sz) ? A[size_t(k0 + j) * ld + k0 + i] : cplx{i == j ? 1.0 : 0.0, 0.0};
     }
     __syncthreads();
+    const int tid = threadIdx.x & 255;
+    auto bar = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + half)); };
     const int g = tid >> 6, t = tid & 63, jj = t >> 2, part = t & 3;  // diagonal-tile group, its column
     const int pr = tid & 15, pc = tid >> 4;                             // tile-product element
-    if (mode & 1) {
-        for (int e = tid; e < bs * lp; e += blockDim.x) X[e] = cplx{0, 0};
-        __syncthreads();
+    for (int e = tid; e < bs * lp; e += 256) X[e] = cplx{0, 0};
+    if (which == 1) {
+        bar();
         if (g < nbk) {  // unit-lower diagonal tiles
             const int o = g * 16;
             for (int i = 0; i < 16; ++i) {
@@ -1241,7 +1246,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
                 __syncwarp();
             }
         }
-        __syncthreads();
+        bar();
         for (int bi = 1; bi < nbk; ++bi) {
             for (int bj = 0; bj < bi; ++bj) {  // Y_bj = sum_{k=bj}^{bi-1} L_{bi,k} X_{k,bj}
                 cplx acc{0, 0};
@@ -1252,7 +1257,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
                 }
                 Y[bj * 256 + pc * 16 + pr] = acc;
             }
-            __syncthreads();
+            bar();
             for (int bj = 0; bj < bi; ++bj) {  // X_{bi,bj} = -X_{bi,bi} Y_bj
                 cplx acc{0, 0};
                 for (int m = 0; m < 16; ++m) {
@@ -1262,20 +1267,17 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
                 }
                 X[(bj * 16 + pc) * lp + bi * 16 + pr] = cplx{-acc.re, -acc.im};
             }
-            __syncthreads();
+            bar();
         }
-        for (int e = tid; e < bs * bs; e += blockDim.x) O[e] = X[(e / bs) * lp + e % bs];
-        __syncthreads();
-    }
-    if (mode & 2) {
+        for (int e = tid; e < bs * bs; e += 256) O[e] = X[(e / bs) * lp + e % bs];
+    } else {
         // reciprocals of the diagonal, all at once (an FP64 division on the
         // substitution's critical path costs ~600 cycles per row)
-        for (int i = tid; i < bs; i += blockDim.x) {
+        for (int i = tid; i < bs; i += 256) {
             const cplx d = T[i * lp + i];
             Dinv[i] = (d.re == 0.0 && d.im == 0.0) ? cplx{0, 0} : cdiv(cplx{1.0, 0.0}, d);
         }
-        for (int e = tid; e < bs * lp; e += blockDim.x) X[e] = cplx{0, 0};
-        __syncthreads();
+        bar();
         if (g < nbk) {  // upper diagonal tiles
             const int o = g * 16;
             for (int i = 15; i >= 0; --i) {
@@ -1297,7 +1299,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
                 __syncwarp();
             }
         }
-        __syncthreads();
+        bar();
         for (int bi = nbk - 2; bi >= 0; --bi) {
             for (int bj = bi + 1; bj < nbk; ++bj) {  // Y_bj = sum_{k=bi+1}^{bj} U_{bi,k} X_{k,bj}
                 cplx acc{0, 0};
@@ -1308,7 +1310,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
                 }
                 Y[(bj - bi - 1) * 256 + pc * 16 + pr] = acc;
             }
-            __syncthreads();
+            bar();
             for (int bj = bi + 1; bj < nbk; ++bj) {  // X_{bi,bj} = -X_{bi,bi} Y_bj
                 cplx acc{0, 0};
                 for (int m = 0; m < 16; ++m) {
@@ -1318,9 +1320,9 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(int n, int ld, cplx* const
                 }
                 X[(bj * 16 + pc) * lp + bi * 16 + pr] = cplx{-acc.re, -acc.im};
             }
-            __syncthreads();
+            bar();
         }
-        for (int e = tid; e < bs * bs; e += blockDim.x) O[bs * bs + e] = X[(e / bs) * lp + e % bs];
+        for (int e = tid; e < bs * bs; e += 256) O[e] = X[(e / bs) * lp + e % bs];
     }
 }
 
@@ -2044,15 +2046,16 @@ namespace {
 void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, int bs, int k0_first, int nblk,
                     int mode, cudaStream_t s) {
     // bs: a multiple of 16, <= kTB
-    const size_t sh = (2 * size_t(bs) * (bs + 1) + 3 * 256 + bs) * sizeof(cplx);
+    // layout: T | X (lower) | X (upper) | Y | Y | Dinv (mode 3 uses both halves)
+    const size_t sh = (3 * size_t(bs) * (bs + 1) + 2 * 768 + bs) * sizeof(cplx);
     static bool attr = false;
     if (!attr) {
         QPS_CUDA(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int((2 * kTB * (kTB + 1) + 3 * 256 + kTB) * sizeof(cplx))));
+                                      int((3 * kTB * (kTB + 1) + 2 * 768 + kTB) * sizeof(cplx))));
         attr = true;
     }
     ProfScope ps("tri_inv", s, 8.0 / 3.0 * count * nblk * double(bs) * bs * bs * ((mode == 3) ? 2 : 1));
-    tri_inv_kernel<<<dim3(nblk, count), 256, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
+    tri_inv_kernel<<<dim3(nblk, count), mode == 3 ? 512 : 256, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
     QPS_CUDA(cudaGetLastError());
 }
 }  // namespace
