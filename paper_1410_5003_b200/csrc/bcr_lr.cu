@@ -419,7 +419,24 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     // Y = C Omega  (= A Omega + Bc (-X Omega) when deferred)
     c.lr_Y.ensure(size_t(nc) * nb * kLrSample);
     const bool early = c.lr_sample_pending && corr;  // Y already holds A Omega
+    static const bool trace = getenv("QPS_BCR_TRACE") != nullptr;  // per-step timing to stderr (debug)
+    cudaEvent_t te0 = nullptr, te1 = nullptr;
+    if (trace) {
+        QPS_CUDA(cudaEventCreate(&te0));
+        QPS_CUDA(cudaEventCreate(&te1));
+        QPS_CUDA(cudaEventRecord(te0, s));
+    }
+    auto tmark = [&](const char* what) {
+        if (!trace) return;
+        float ms = 0;
+        QPS_CUDA(cudaEventRecord(te1, s));
+        QPS_CUDA(cudaEventSynchronize(te1));
+        QPS_CUDA(cudaEventElapsedTime(&ms, te0, te1));
+        fprintf(stderr, "lr_compress %s: %.3f ms\n", what, ms);
+        QPS_CUDA(cudaEventRecord(te0, s));
+    };
     if (c.lr_sample_pending) QPS_CUDA(cudaStreamWaitEvent(s, c.ev_sample, 0));
+    tmark("wait for the side-stream sample");
     c.lr_sample_pending = false;
     {
         std::vector<GemmTask> t(nc);
@@ -457,6 +474,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
         }
     }
+    tmark("sample correction Y += Bc (-X Omega)");
     static const bool cpqr_only = [] {
         const char* e = getenv("QPS_LR_QR");
         return e && !strcmp(e, "cpqr");
@@ -507,6 +525,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             zgemm_batched(kQrW, rest, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks, "lr_qr");
             zgemm_batched(m, rest, cplx{-1, 0}, cplx{1, 0}, t3, s, c.ws.gemm_tasks, "lr_qr");
         }
+        tmark("blocked QR of the samples");
         // CPQR of R (64 x 64): rank and the ordered basis Q2
         c.lr_R64.ensure(size_t(nc) * p * p);
         qr_take_r_kernel<<<nc, 256, 0, s>>>(m, p, c.lr_Y.p, ys, c.lr_R64.p);
@@ -553,6 +572,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             zgemm_batched(kQrW, r, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks, "lr_qr");
             zgemm_batched(m, r, cplx{-1, 0}, cplx{1, 0}, t3, s, c.ws.gemm_tasks, "lr_qr");
         }
+        tmark("rank check, Q2, P = Q [Q2; 0]");
         conj_transpose_kernel<<<dim3(64, nc), 256, 0, s>>>(nb, r, c.lr_P.p, size_t(nb) * r, c.lr_PH.p,
                                                            size_t(r) * nb);
         QPS_CUDA(cudaGetLastError());
@@ -595,6 +615,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             QPS_CUDA(cudaGetLastError());
         }
     }
+    tmark("P^*");
     // R = P^* C  (= P^* A + (-P^* Bc) X when deferred)
     c.lr_R.ensure(size_t(nc) * r * nb);
     {
@@ -621,6 +642,11 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             }
         }
         zgemm_batched(r, nb, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+    }
+    tmark("R = P^* C");
+    if (trace) {
+        QPS_CUDA(cudaEventDestroy(te0));
+        QPS_CUDA(cudaEventDestroy(te1));
     }
     return true;
 }
