@@ -309,6 +309,93 @@ __global__ void stage_bases_kernel(int I, int n, size_t per, const cplx* __restr
     }
 }
 
+// In-place inverse of each n x n matrix (n <= kGjMax, column-major, stride n^2) by
+// Gauss-Jordan elimination with partial (row) pivoting, one CTA per matrix,
+// the matrix resident in shared memory: n steps of (pivot search, row swap,
+// scaled pivot row, rank-1 elimination of every other row), then the column
+// interchanges undone in reverse.  flag[b] = 1 on an exactly zero pivot.
+constexpr int kGjMax = 112;  // 112^2 complex = 196 KB of shared memory
+__global__ void __launch_bounds__(512) gj_inverse_kernel(int n, cplx* __restrict__ C, int* __restrict__ flag) {
+    extern __shared__ cplx gj[];  // n x n, ld n
+    __shared__ int s_piv[kGjMax];
+    __shared__ cplx s_row[kGjMax], s_col[kGjMax];
+    __shared__ double s_v[16];
+    __shared__ int s_i[16];
+    cplx* Cb = C + size_t(blockIdx.x) * n * n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < n * n; e += blockDim.x) gj[e] = Cb[e];
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        // pivot: first row i >= k of largest modulus in column k
+        double v = -1.0;
+        int idx = 1 << 30;
+        if (tid < n && tid >= k) {
+            v = cabs2(gj[k * n + tid]);
+            idx = tid;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (ov > v || (ov == v && oi < idx)) {
+                v = ov;
+                idx = oi;
+            }
+        }
+        if (lane == 0 && warp < 16) {
+            s_v[warp] = v;
+            s_i[warp] = idx;
+        }
+        __syncthreads();
+        double bv = s_v[0];
+        int p = s_i[0];
+        for (int w = 1; w < (n + 31) / 32; ++w)
+            if (s_v[w] > bv || (s_v[w] == bv && s_i[w] < p)) {
+                bv = s_v[w];
+                p = s_i[w];
+            }
+        if (tid == 0) {
+            s_piv[k] = p;
+            if (!(bv > 0.0)) flag[blockIdx.x] = 1;
+        }
+        if (p != k && tid < n) {  // swap rows k and p (thread = column)
+            const cplx t = gj[tid * n + k];
+            gj[tid * n + k] = gj[tid * n + p];
+            gj[tid * n + p] = t;
+        }
+        __syncthreads();
+        const cplx a = gj[k * n + k];
+        const cplx inv = (a.re == 0.0 && a.im == 0.0) ? cplx{0, 0} : cdiv(cplx{1.0, 0.0}, a);
+        if (tid < n) {
+            s_row[tid] = (tid == k) ? inv : cmul(gj[tid * n + k], inv);
+            s_col[tid] = (tid == k) ? cplx{0, 0} : gj[k * n + tid];
+        }
+        __syncthreads();
+        for (int e = tid; e < n * n; e += blockDim.x) {
+            const int i = e % n, j = e / n;
+            if (i == k) {
+                gj[e] = s_row[j];
+            } else {
+                const cplx f = s_col[i], r = s_row[j];
+                cplx x = (j == k) ? cplx{0, 0} : gj[e];
+                x.re -= f.re * r.re - f.im * r.im;
+                x.im -= f.re * r.im + f.im * r.re;
+                gj[e] = x;
+            }
+        }
+        __syncthreads();
+    }
+    for (int k = n - 1; k >= 0; --k) {  // A^{-1} = (P A)^{-1} P: swap columns k, piv[k]
+        const int p = s_piv[k];
+        if (p != k && tid < n) {
+            const cplx t = gj[k * n + tid];
+            gj[k * n + tid] = gj[p * n + tid];
+            gj[p * n + tid] = t;
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < n * n; e += blockDim.x) Cb[e] = gj[e];
+}
+
 GemmTask gemm1(const cplx* A, int lda, const cplx* B, int ldb, int K, cplx* C, int ldc) {
     GemmTask t{};
     t.nseg = 1;
@@ -966,6 +1053,10 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         QPS_CUDA(cudaEventRecord(te0, s));
     };
     DBuf<int> flag;
+    DBuf<int> capflag;  // Gauss-Jordan capacitance inverses: flags of every level, checked at the end
+    capflag.ensure(size_t(npos) + ns);
+    capflag.zero(s);
+    std::vector<int> cap_orig;
     auto check = [&](const std::vector<int>& orig) {
         std::vector<int> hf(orig.size());
         QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
@@ -1062,8 +1153,16 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         DBuf<cplx>& Zb = c.lr_Z[lvl];
         Zb.ensure(size_t(cnt) * nb * r2);
         set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Cm.p);
-        set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Ci.p);
         QPS_CUDA(cudaGetLastError());
+        static const bool cap_lu = [] {  // QPS_WB_CAP=lu: LU + solve against I instead of Gauss-Jordan
+            const char* e = getenv("QPS_WB_CAP");
+            return e && !strcmp(e, "lu");
+        }();
+        const bool gjinv = !cap_lu && r2 <= kGjMax;
+        if (!gjinv) {
+            set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Ci.p);
+            QPS_CUDA(cudaGetLastError());
+        }
         std::vector<GemmTask> m(cnt), z(cnt);
         std::vector<GemvTask> gu(cnt), ga(cnt), gz(cnt);
         std::vector<cplx*> ca, cd, ci;
@@ -1075,7 +1174,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             cplx* Cm = c.lr_Cm.p + size_t(q) * r2 * r2;
             cplx* Ci = c.lr_Ci.p + size_t(q) * r2 * r2;
             m[q] = gemm1(S_of(p.j), r2, W, nb, nb, Cm, r2);                       // C = I - S W
-            z[q] = gemm1(W, nb, Ci, r2, r2, Zb.p + size_t(q) * nb * r2, nb);       // Z = W C^{-1}
+            z[q] = gemm1(W, nb, gjinv ? Cm : Ci, r2, r2, Zb.p + size_t(q) * nb * r2, nb);  // Z = W C^{-1}
             gu[q] = gemv1(W, nb, g_of(p.j), r2, p.F);                              // u = y - W g
             ga[q] = gemv1(S_of(p.j), r2, p.F, nb, c.lr_a.p + size_t(q) * r2);      // a = S u
             gz[q] = gemv1(Zb.p + size_t(q) * nb * r2, nb, c.lr_a.p + size_t(q) * r2, r2, p.F);  // z = u + Z a
@@ -1087,11 +1186,25 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             p.Z = Zb.p + size_t(q) * nb * r2;
         }
         zgemm_batched(r2, r2, mone, one, m, s, c.ws.gemm_tasks, "wb_cap");
-        flag.ensure(cnt);
-        flag.zero(s);
-        lu_factor_batched(r2, r2, ca, cp, cd, flag.p, s, c.ws);
-        check(orig);
-        lu_solve_batched(r2, r2, ca, cp, cd, ci, r2, r2, s, c.ws);
+        if (gjinv) {  // C <- C^{-1} in place; singular flags checked once after all levels
+            static bool attr = false;
+            if (!attr) {
+                QPS_CUDA(cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              int(kGjMax * kGjMax * sizeof(cplx))));
+                attr = true;
+            }
+            ProfScope ps("wb_gj", s, 8.0 * cnt * double(r2) * r2 * r2);
+            gj_inverse_kernel<<<cnt, 512, size_t(r2) * r2 * sizeof(cplx), s>>>(r2, c.lr_Cm.p,
+                                                                              capflag.p + cap_orig.size());
+            QPS_CUDA(cudaGetLastError());
+            cap_orig.insert(cap_orig.end(), orig.begin(), orig.end());
+        } else {
+            flag.ensure(cnt);
+            flag.zero(s);
+            lu_factor_batched(r2, r2, ca, cp, cd, flag.p, s, c.ws);
+            check(orig);
+            lu_solve_batched(r2, r2, ca, cp, cd, ci, r2, r2, s, c.ws);
+        }
         zgemm_batched(nb, r2, one, zero, z, s, c.ws.gemm_tasks, "wb_cap");
         zgemv_batched(nb, mone, one, gu, s, c.ws.gemv_tasks);
         zgemv_batched(r2, one, zero, ga, s, c.ws.gemv_tasks);
@@ -1171,6 +1284,11 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         for (int a = 0; a < ns; ++a) fin.push_back(&levels[lvl][a][0]);
         eliminate(fin, lvl);
         tmark("final", lvl, int(fin.size()));
+    }
+    if (!cap_orig.empty()) {
+        flag.ensure(cap_orig.size());
+        QPS_CUDA(cudaMemcpyAsync(flag.p, capflag.p, sizeof(int) * cap_orig.size(), cudaMemcpyDeviceToDevice, s));
+        check(cap_orig);
     }
     // back substitution: eta_o = z_o - Z_L (R_L(o) eta_{o-1}) - Z_U (R_U(o) eta_{o+1})
     for (int l = lvl - 1; l >= 0; --l) {
