@@ -396,6 +396,108 @@ __global__ void __launch_bounds__(512) gj_inverse_kernel(int n, cplx* __restrict
     for (int e = tid; e < n * n; e += blockDim.x) Cb[e] = gj[e];
 }
 
+// Register-resident variant (default): thread (j, g) = (tid / 4, tid % 4) keeps
+// rows g, g + 4, ... of column j in registers for the whole elimination.  No
+// physical row interchanges: step k pivots on the largest-modulus unused row
+// p_k of column k and applies the Jordan exchange
+//   T[p][k] = 1/a,  T[p][j] = -T[p][j]/a,  T[i][k] = T[i][k]/a,
+//   T[i][j] -= T[i][k] T[p][j]/a          (a = T[p][k]),
+// after which A^{-1}[k][p_k'] = T[p_k][k'] (rows and columns permuted on the
+// way out).  Two barriers per step; the pivot's reciprocal is computed once.
+// N (a multiple of 4) fixed at compile time: every guard folds away and the
+// row loops are straight-line selects (96 x 96 capacitance matrices, 2r = 96).
+template <int N>
+__global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict__ C, int* __restrict__ flag) {
+    constexpr int NR = N / 4;
+    static_assert(N % 4 == 0 && NR <= 32, "gj_inverse_reg_kernel: N = 4 NR, NR <= 32");
+    __shared__ cplx s_row[N], s_col[N];
+    __shared__ int s_perm[N], s_pinv[N];
+    __shared__ int s_p;
+    __shared__ cplx s_inv;
+    cplx* Cb = C + size_t(blockIdx.x) * N * N;
+    const int tid = threadIdx.x, j = tid >> 2, g = tid & 3;
+    cplx T[NR];
+    unsigned used = 0;  // bit ii: row g + 4 ii already pivotal
+#pragma unroll
+    for (int ii = 0; ii < NR; ++ii) T[ii] = Cb[size_t(j) * N + g + 4 * ii];
+    for (int k = 0; k < N; ++k) {
+        if ((k >> 3) == (tid >> 5)) {  // the warp holding column k: pivot search
+            double v = -1.0;
+            int idx = 1 << 30;
+            if (j == k) {
+#pragma unroll
+                for (int ii = 0; ii < NR; ++ii) {
+                    const double m = cabs2(T[ii]);
+                    const bool better = !((used >> ii) & 1u) && m > v;
+                    v = better ? m : v;
+                    idx = better ? g + 4 * ii : idx;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                const bool better = ov > v || (ov == v && oi < idx);
+                v = better ? ov : v;
+                idx = better ? oi : idx;
+            }
+            if (j == k && g == (idx & 3)) {  // owner of the pivot element
+                cplx a{0, 0};
+#pragma unroll
+                for (int ii = 0; ii < NR; ++ii) {
+                    const bool hit = (g + 4 * ii == idx);
+                    a.re = hit ? T[ii].re : a.re;
+                    a.im = hit ? T[ii].im : a.im;
+                }
+                const bool zero = !(v > 0.0);
+                if (zero) flag[blockIdx.x] = 1;
+                s_inv = zero ? cplx{0, 0} : fast_cinv(a);
+                s_p = idx;
+                s_perm[k] = idx;
+                s_pinv[idx] = k;
+            }
+        }
+        __syncthreads();
+        const int p = s_p, pr = p >> 2;
+        const bool own_p = g == (p & 3);
+        if (own_p) {
+            cplx rv{0, 0};
+#pragma unroll
+            for (int ii = 0; ii < NR; ++ii) {
+                rv.re = (ii == pr) ? T[ii].re : rv.re;
+                rv.im = (ii == pr) ? T[ii].im : rv.im;
+            }
+            s_row[j] = rv;
+        }
+        if (j == k) {
+#pragma unroll
+            for (int ii = 0; ii < NR; ++ii) s_col[g + 4 * ii] = T[ii];
+        }
+        __syncthreads();
+        const cplx inv = s_inv;
+        const bool colk = (j == k);
+        const cplx sr = s_row[j];
+        cplx r = cmul(sr, inv);
+        r.re = colk ? -inv.re : r.re;
+        r.im = colk ? -inv.im : r.im;
+#pragma unroll
+        for (int ii = 0; ii < NR; ++ii) {
+            const cplx c = s_col[g + 4 * ii];
+            double bre = colk ? 0.0 : T[ii].re, bim = colk ? 0.0 : T[ii].im;
+            bre -= c.re * r.re - c.im * r.im;
+            bim -= c.re * r.im + c.im * r.re;
+            const bool piv = own_p && ii == pr;
+            T[ii].re = piv ? -r.re : bre;
+            T[ii].im = piv ? -r.im : bim;
+        }
+        used |= own_p ? (1u << pr) : 0u;
+    }
+    __syncthreads();
+    const int col = s_perm[j];  // A^{-1}[pinv[i]][perm[j]] = T[i][j]
+#pragma unroll
+    for (int ii = 0; ii < NR; ++ii) Cb[size_t(col) * N + s_pinv[g + 4 * ii]] = T[ii];
+}
+
 GemmTask gemm1(const cplx* A, int lda, const cplx* B, int ldb, int K, cplx* C, int ldc) {
     GemmTask t{};
     t.nseg = 1;
@@ -1118,10 +1220,22 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }
         flag.ensure(fa.size());
         flag.zero(s);
-        lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
-        check(orig);
-        tmark("factor", 0, int(fa.size()));
-        lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, s, c.ws);
+        static const bool separate = [] {  // QPS_WB_L0=separate: factor, then solve (A/B)
+            const char* e = getenv("QPS_WB_L0");
+            return e && !strcmp(e, "separate");
+        }();
+        if (separate) {
+            lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
+            check(orig);
+            tmark("factor", 0, int(fa.size()));
+            lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, s, c.ws);
+        } else {
+            // the D_j^0 factors are used only for W_j: the forward substitution
+            // rides along the factorization
+            lu_factor_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, flag.p, s, c.ws);
+            check(orig);
+            tmark("factor+solve", 0, int(fa.size()));
+        }
         // y = D^{-1} f back into F (column 2r of every W_j)
         QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * nb, c.lr_W0.p + size_t(r2) * nb,
                                    sizeof(cplx) * nb * (r2 + 1), sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
@@ -1187,15 +1301,24 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }
         zgemm_batched(r2, r2, mone, one, m, s, c.ws.gemm_tasks, "wb_cap");
         if (gjinv) {  // C <- C^{-1} in place; singular flags checked once after all levels
-            static bool attr = false;
-            if (!attr) {
-                QPS_CUDA(cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              int(kGjMax * kGjMax * sizeof(cplx))));
-                attr = true;
-            }
+            static const bool gj_smem = [] {  // QPS_WB_GJ=smem: the shared-memory kernel (always for 2r != 96)
+                const char* e = getenv("QPS_WB_GJ");
+                return e && !strcmp(e, "smem");
+            }();
             ProfScope ps("wb_gj", s, 8.0 * cnt * double(r2) * r2 * r2);
-            gj_inverse_kernel<<<cnt, 512, size_t(r2) * r2 * sizeof(cplx), s>>>(r2, c.lr_Cm.p,
-                                                                              capflag.p + cap_orig.size());
+            if (gj_smem || r2 != 96) {
+                static bool attr = false;
+                if (!attr) {
+                    QPS_CUDA(cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  int(kGjMax * kGjMax * sizeof(cplx))));
+                    attr = true;
+                }
+                gj_inverse_kernel<<<cnt, 512, size_t(r2) * r2 * sizeof(cplx), s>>>(r2, c.lr_Cm.p,
+                                                                                  capflag.p + cap_orig.size());
+            } else {
+                int* fl = capflag.p + cap_orig.size();
+                gj_inverse_reg_kernel<96><<<cnt, 4 * 96, 0, s>>>(c.lr_Cm.p, fl);
+            }
             QPS_CUDA(cudaGetLastError());
             cap_orig.insert(cap_orig.end(), orig.begin(), orig.end());
         } else {

@@ -113,9 +113,18 @@ qps_ctx* qps_create(int device) {
     h->c.device = device;
     try {
         QPS_CUDA(cudaSetDevice(device));
-        QPS_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
-        QPS_CUDA(cudaStreamCreateWithFlags(&h->c.side, cudaStreamNonBlocking));
-        QPS_CUDA(cudaStreamCreateWithFlags(&h->c.side2, cudaStreamNonBlocking));
+        // the latency-bound chains get the higher priorities (the corner least
+        // squares, a few CTAs, above the main stream); the throughput-bound side
+        // GEMMs (side2: the low-rank sample) fill the SMs the chains leave idle
+        // instead of starving them
+        int prio_lo = 0, prio_hi = 0;
+        QPS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        const int prio_main = prio_hi < prio_lo ? prio_hi + 1 : prio_hi;
+        QPS_CUDA(cudaStreamCreateWithPriority(&h->c.stream, cudaStreamNonBlocking, prio_main));
+        QPS_CUDA(cudaStreamCreateWithPriority(&h->c.side, cudaStreamNonBlocking, prio_hi));
+        const char* sp = getenv("QPS_SAMPLE_PRIO");  // A/B: "main" puts side2 level with the main stream
+        QPS_CUDA(cudaStreamCreateWithPriority(&h->c.side2, cudaStreamNonBlocking,
+                                              (sp && !strcmp(sp, "main")) ? prio_main : prio_lo));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fork, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fill, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_sample, cudaEventDisableTiming));

@@ -36,6 +36,11 @@ struct CodSet {
     DBuf<int> perm, nzp, rank, flags;
     DBuf<double> maxpiv, xmax, rmax, enorm, rnorm, parts;
     DBuf<GemmTask> tasks1, tasks2;  // task tables of this family's GEMMs (families run on separate streams)
+    HBuf<double> h_rmax, h_xmax, h_enorm, h_rnorm;  // pinned: read back without blocking the host
+    cudaEvent_t ev = nullptr;                        // last read-back of this family
+    ~CodSet() {
+        if (ev) cudaEventDestroy(ev);
+    }
     CodBatch batch(const cplx* Q) {
         CodBatch b;
         b.count = count; b.m = m; b.p = p; b.Q = Q;
@@ -51,6 +56,8 @@ struct CodSet {
         tau.ensure(size_t(cnt) * p); zc.ensure(size_t(cnt) * p); perm.ensure(size_t(cnt) * p);
         nzp.ensure(cnt); rank.ensure(cnt); flags.ensure(cnt);
         maxpiv.ensure(cnt); xmax.ensure(cnt); rmax.ensure(cnt); enorm.ensure(cnt); rnorm.ensure(cnt);
+        h_rmax.ensure(cnt); h_xmax.ensure(cnt); h_enorm.ensure(cnt); h_rnorm.ensure(cnt);
+        if (!ev) QPS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
 };
 

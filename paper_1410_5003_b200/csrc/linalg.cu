@@ -602,7 +602,6 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
     __shared__ cplx s_den, s_zc;
     for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) V[i] = W[i];
     if (r == 0) {
-        for (size_t i = tid; i < size_t(p) * m; i += blockDim.x) QH[i] = cplx{0, 0};
         for (size_t i = tid; i < size_t(p) * p; i += blockDim.x) Wz[i] = cplx{0, 0};
         return;
     }
@@ -675,50 +674,7 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
             __syncthreads();
         }
     }
-    // QH = first r rows of Q_r^* = H_{r-1} ... H_0 (reflectors exactly as applied):
-    // column c of QH = H_{r-1} ... H_0 e_c.  Columns are independent; reflectors
-    // are applied in sequence, one warp per column with lanes over rows.
-    {
-        const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-        for (int c = warp; c < m; c += nw) {
-            cplx* col = M1 + size_t(warp) * m;  // per-warp scratch column (M1 holds >= 8 m entries)
-            for (int i = lane; i < m; i += 32) col[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
-            __syncwarp();
-            for (int kk = 0; kk < r; ++kk) {
-                const cplx tk = tau[kk];
-                if (tk.re == 0.0 && tk.im == 0.0) continue;
-                cplx t{0, 0};
-                for (int i = kk + 1 + lane; i < m; i += 32) {
-                    const cplx e = W[size_t(kk) * m + i];
-                    const cplx a = col[i];
-                    t.re += e.re * a.re + e.im * a.im;
-                    t.im += e.re * a.im - e.im * a.re;
-                }
-                for (int o = 16; o > 0; o >>= 1) {
-                    t.re += __shfl_xor_sync(0xffffffffu, t.re, o);
-                    t.im += __shfl_xor_sync(0xffffffffu, t.im, o);
-                }
-                const cplx ck = col[kk];
-                t.re += ck.re;
-                t.im += ck.im;
-                t = cmul(tk, t);
-                __syncwarp();
-                if (lane == 0) {
-                    col[kk].re -= t.re;
-                    col[kk].im -= t.im;
-                }
-                for (int i = kk + 1 + lane; i < m; i += 32) {
-                    const cplx et = cmul(W[size_t(kk) * m + i], t);
-                    col[i].re -= et.re;
-                    col[i].im -= et.im;
-                }
-                __syncwarp();
-            }
-            for (int i = lane; i < p; i += 32) QH[size_t(c) * p + i] = i < r ? col[i] : cplx{0, 0};
-            __syncwarp();
-        }
-    }
-    __syncthreads();
+    // QH: cod_qh_kernel (many CTAs per problem)
     // Wz columns: P Z^* e_c for c < r
     for (int c = tid; c < p; c += blockDim.x) {
         cplx* y = Y + size_t(c) * p;
@@ -761,6 +717,59 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
         }
         for (int i = 0; i < p; ++i) w[perm[i]] = y[i];
     }
+}
+
+// QH = first r rows of Q_r^* = H_{r-1} ... H_0 (reflectors exactly as applied)
+// for problems too large for the shared-memory operator: column c of QH is
+// H_{r-1} ... H_0 e_c, independent per column, so every CTA takes 8 columns
+// (one warp each, the column in shared memory, lanes over rows) and the
+// problem's m columns spread over m/8 CTAs instead of one.
+__global__ void __launch_bounds__(256) cod_qh_kernel(CodBatch b, const int* __restrict__ flags) {
+    const int pb = blockIdx.y;
+    if (flags && !flags[pb]) return;
+    const int m = b.m, p = b.p, r = b.rank[pb];
+    const cplx* W = b.W + size_t(pb) * m * p;
+    const cplx* tau = b.tau + size_t(pb) * p;
+    cplx* QH = b.QH + size_t(pb) * p * m;
+    extern __shared__ cplx qh_col[];  // [8][m]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = blockIdx.x * 8 + warp;
+    if (c >= m) return;
+    cplx* col = qh_col + size_t(warp) * m;
+    for (int i = lane; i < m; i += 32) col[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
+    __syncwarp();
+    for (int kk = 0; kk < r; ++kk) {
+        const cplx tk = tau[kk];
+        if (tk.re == 0.0 && tk.im == 0.0) continue;
+        const cplx* e = W + size_t(kk) * m;
+        cplx t{0, 0};
+        for (int i = kk + 1 + lane; i < m; i += 32) {
+            const cplx ei = e[i];
+            const cplx a = col[i];
+            t.re += ei.re * a.re + ei.im * a.im;
+            t.im += ei.re * a.im - ei.im * a.re;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            t.re += __shfl_xor_sync(0xffffffffu, t.re, o);
+            t.im += __shfl_xor_sync(0xffffffffu, t.im, o);
+        }
+        const cplx ck = col[kk];
+        t.re += ck.re;
+        t.im += ck.im;
+        t = cmul(tk, t);
+        __syncwarp();
+        if (lane == 0) {
+            col[kk].re -= t.re;
+            col[kk].im -= t.im;
+        }
+        for (int i = kk + 1 + lane; i < m; i += 32) {
+            const cplx et = cmul(e[i], t);
+            col[i].re -= et.re;
+            col[i].im -= et.im;
+        }
+        __syncwarp();
+    }
+    for (int i = lane; i < p; i += 32) QH[size_t(c) * p + i] = i < r ? col[i] : cplx{0, 0};
 }
 
 // Same operator with the working set in shared memory (problems with
@@ -1943,6 +1952,12 @@ void zgemm_residual_norms(int M, int N, cplx alpha, cplx beta, const std::vector
 }
 
 constexpr size_t kCodFacSmemMax = 216 * 1024;
+// Dynamic shared memory a launch of only a few latency-bound CTAs requests so
+// that no throughput kernel's CTA can share its SM (co-resident GEMM CTAs
+// were measured to slow the corner least squares 2-3x).
+constexpr size_t kLatencyReserve = 200 * 1024;
+size_t latency_reserve(int ctas) { return ctas <= 16 ? kLatencyReserve : 0; }
+
 template <bool kFast>
 void launch_cod_factor(const CodBatch& b, cudaStream_t s) {
     const size_t sm = size_t(b.m) * b.p * sizeof(cplx);
@@ -1955,7 +1970,14 @@ void launch_cod_factor(const CodBatch& b, cudaStream_t s) {
         }
         cod_factor_kernel<kFast, true><<<b.count, 512, sm, s>>>(b);
     } else {
-        cod_factor_kernel<kFast, false><<<b.count, 256, 0, s>>>(b);
+        const size_t res = latency_reserve(b.count);
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_factor_kernel<kFast, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLatencyReserve)));
+            attr = true;
+        }
+        cod_factor_kernel<kFast, false><<<b.count, 256, res, s>>>(b);
     }
     QPS_CUDA(cudaGetLastError());
 }
@@ -1992,7 +2014,22 @@ void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
         }
         cod_operator_smem_kernel<<<b.count, 256, sm, s>>>(b, flags);
     } else {
-        cod_operator_kernel<<<b.count, 256, 0, s>>>(b, flags);
+        // few large problems (the corners): latency-bound single CTAs that keep
+        // their SM to themselves (the reservation keeps GEMM CTAs off it)
+        const size_t res = latency_reserve(b.count);
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_operator_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kLatencyReserve)));
+            QPS_CUDA(cudaFuncSetAttribute(cod_qh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kLatencyReserve)));
+            attr = true;
+        }
+        cod_operator_kernel<<<b.count, 256, res, s>>>(b, flags);
+        QPS_CUDA(cudaGetLastError());
+        const size_t qs = std::max(size_t(8) * b.m * sizeof(cplx), res);
+        if (qs > kLatencyReserve) fail(QPS_ERR_INTERNAL, "cod_qh: m too large");
+        cod_qh_kernel<<<dim3((b.m + 7) / 8, b.count), 256, qs, s>>>(b, flags);
     }
     QPS_CUDA(cudaGetLastError());
 }
@@ -2034,7 +2071,14 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
         }
         cod_trsm_kernel<true><<<grid, 128, sh, s>>>(b, B, ldb, stride, ncols, flags);
     } else {
-        cod_trsm_kernel<false><<<grid, 128, 0, s>>>(b, B, ldb, stride, ncols, flags);
+        const size_t res = latency_reserve(int(grid.x * grid.y));
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(cod_trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kLatencyReserve)));
+            attr = true;
+        }
+        cod_trsm_kernel<false><<<grid, 128, res, s>>>(b, B, ldb, stride, ncols, flags);
     }
     QPS_CUDA(cudaGetLastError());
 }
@@ -2105,6 +2149,10 @@ struct LuCtx {
     int* sing;
     cudaStream_t s;
     Workspace& ws;
+    // right-hand sides carried along the recursion's spine (lu_factor_solve_batched)
+    const std::vector<cplx*>* hB = nullptr;
+    cplx* const* dB = nullptr;
+    int ldb = 0, nrhs = 0;
 };
 
 void gemm_update(LuCtx& L, int M, int N, int K, size_t aoff, size_t boff, size_t coff, cplx alpha, cplx beta,
@@ -2127,11 +2175,17 @@ void gemm_update(LuCtx& L, int M, int N, int K, size_t aoff, size_t boff, size_t
 
 // X[r0:r1, c0:c0+nc] <- L[r0:r1, r0:r1]^{-1} X (unit lower) inside the factor itself
 // (U12 of the recursive LU), leaves of <= 64 rows through on-demand tile inverses.
-void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc) {
+void trsm_lower_rhs_leaf(LuCtx& L, int r0, int r1, int bs);
+void trsm_lower_rhs_update(LuCtx& L, int r0, int h, int r1);
+
+// rhs: apply the same L^{-1} to the carried right-hand sides (one tile inverse
+// per leaf serves both)
+void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc, bool rhs = false) {
     const int m = r1 - r0;
     if (m <= kTB) {
         const int bs = (m + 15) / 16 * 16;  // tile sized to the leaf (16, 32, 48 or 64 rows)
         launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, bs, r0, 1, 1, L.s);  // tile 0 of Dinv as scratch
+        if (rhs) trsm_lower_rhs_leaf(L, r0, r1, bs);
         auto& tasks = L.ws.h_gemm;
         tasks.assign(L.count, GemmTask{});
         for (int b = 0; b < L.count; ++b) {
@@ -2149,11 +2203,12 @@ void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc) {
         return;
     }
     const int h = ((m + kTB - 1) / kTB + 1) / 2 * kTB;
-    trsm_lower_in_factor(L, r0, r0 + h, c0, nc);
+    trsm_lower_in_factor(L, r0, r0 + h, c0, nc, rhs);
     // X[r0+h:r1] -= L[r0+h:r1, r0:r0+h] X[r0:r0+h]
     gemm_update(L, m - h, nc, h, size_t(r0) * L.ld + r0 + h, size_t(c0) * L.ld + r0, size_t(c0) * L.ld + r0 + h,
                 cplx{-1, 0}, cplx{1, 0}, L.hA, L.hA, L.ld);
-    trsm_lower_in_factor(L, r0 + h, r1, c0, nc);
+    if (rhs) trsm_lower_rhs_update(L, r0, h, r1);
+    trsm_lower_in_factor(L, r0 + h, r1, c0, nc, rhs);
 }
 
 // recursive LU of columns [c0, c0 + nc) (rows c0..n), Toledo's algorithm
@@ -2194,6 +2249,174 @@ void lu_rec(LuCtx& L, int c0, int nc) {
         ProfScope ps("lu_swap", L.s, 0.0);
         launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0 + h, c0 + nc, c0, c0 + h, L.s, L.ws.perm);
     }
+}
+
+// B[r0:r1, :] <- L[r0:r1, r0:r1]^{-1} B[r0:r1, :] (unit lower, the factor's own
+// L) for the carried right-hand sides; leaves of <= 64 rows through tile inverses
+// B[r0:r1] <- (tile 0 of Dinv, bs x bs) B[r0:r1]: the leaf's L^{-1} already inverted
+void trsm_lower_rhs_leaf(LuCtx& L, int r0, int r1, int bs) {
+    const int m = r1 - r0;
+    auto& tasks = L.ws.h_gemm;
+    tasks.assign(L.count, GemmTask{});
+    for (int b = 0; b < L.count; ++b) {
+        GemmTask& t = tasks[b];
+        t.nseg = 1;
+        t.A[0] = L.hD[b];
+        t.lda[0] = bs;
+        t.B[0] = (*L.hB)[b] + r0;
+        t.ldb[0] = L.ldb;
+        t.K[0] = m;
+        t.C = (*L.hB)[b] + r0;
+        t.ldc = L.ldb;
+    }
+    zgemm_batched(m, L.nrhs, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks);
+}
+// B[r0+h:r1] -= L[r0+h:r1, r0:r0+h] B[r0:r0+h]
+void trsm_lower_rhs_update(LuCtx& L, int r0, int h, int r1) {
+    auto& tasks = L.ws.h_gemm;
+    tasks.assign(L.count, GemmTask{});
+    for (int b = 0; b < L.count; ++b) {
+        GemmTask& t = tasks[b];
+        t.nseg = 1;
+        t.A[0] = L.hA[b] + size_t(r0) * L.ld + r0 + h;
+        t.lda[0] = L.ld;
+        t.B[0] = (*L.hB)[b] + r0;
+        t.ldb[0] = L.ldb;
+        t.K[0] = h;
+        t.C = (*L.hB)[b] + r0 + h;
+        t.ldc = L.ldb;
+    }
+    zgemm_batched(r1 - r0 - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks);
+}
+
+void trsm_lower_rhs(LuCtx& L, int r0, int r1) {
+    const int m = r1 - r0;
+    auto& tasks = L.ws.h_gemm;
+    if (m <= kTB) {
+        const int bs = (m + 15) / 16 * 16;
+        launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, bs, r0, 1, 1, L.s);  // tile 0 of Dinv as scratch
+        tasks.assign(L.count, GemmTask{});
+        for (int b = 0; b < L.count; ++b) {
+            GemmTask& t = tasks[b];
+            t.nseg = 1;
+            t.A[0] = L.hD[b];
+            t.lda[0] = bs;
+            t.B[0] = (*L.hB)[b] + r0;
+            t.ldb[0] = L.ldb;
+            t.K[0] = m;
+            t.C = (*L.hB)[b] + r0;  // in place: <= 64 rows, one CTA per column tile
+            t.ldc = L.ldb;
+        }
+        zgemm_batched(m, L.nrhs, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks);
+        return;
+    }
+    const int h = ((m + kTB - 1) / kTB + 1) / 2 * kTB;
+    trsm_lower_rhs(L, r0, r0 + h);
+    tasks.assign(L.count, GemmTask{});
+    for (int b = 0; b < L.count; ++b) {  // B[r0+h:r1] -= L[r0+h:r1, r0:r0+h] B[r0:r0+h]
+        GemmTask& t = tasks[b];
+        t.nseg = 1;
+        t.A[0] = L.hA[b] + size_t(r0) * L.ld + r0 + h;
+        t.lda[0] = L.ld;
+        t.B[0] = (*L.hB)[b] + r0;
+        t.ldb[0] = L.ldb;
+        t.K[0] = h;
+        t.C = (*L.hB)[b] + r0 + h;
+        t.ldc = L.ldb;
+    }
+    zgemm_batched(m - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks);
+    trsm_lower_rhs(L, r0 + h, r1);
+}
+
+// Toledo's recursion on the spine (columns [c0, n)) with the right-hand sides
+// B carried as extra columns of every right half: each spine node applies its
+// left half's interchanges, L11^{-1} and the A21 update to B as well, so B
+// leaves the factorization as L^{-1} P B.  The spine's interchanges are not
+// copied back onto the left halves: L is not used after this solve (U is).
+void lu_rec_spine(LuCtx& L, int c0, int nc) {
+    const bool smem_leaf = size_t(L.n) * kLeaf * sizeof(cplx) <= 200 * 1024;
+    const int leaf = smem_leaf ? kLeaf : kNB;
+    if (nc <= leaf) {
+        lu_rec(L, c0, nc);
+        {
+            ProfScope ps("lu_swap", L.s, 0.0);
+            launch_row_permute(L.n, L.ldb, L.dB, L.dP, L.count, c0, c0 + nc, 0, L.nrhs, L.s, L.ws.perm);
+        }
+        trsm_lower_rhs(L, c0, c0 + nc);
+        return;
+    }
+    const int h = ((nc + leaf - 1) / leaf) / 2 * leaf;
+    lu_rec(L, c0, h);
+    {  // left-half interchanges onto the right half and the right-hand sides
+        ProfScope ps("lu_swap", L.s, 0.0);
+        launch_row_permute(L.n, L.ld, L.dA, L.dP, L.count, c0, c0 + h, c0 + h, c0 + nc, L.s, L.ws.perm);
+        launch_row_permute(L.n, L.ldb, L.dB, L.dP, L.count, c0, c0 + h, 0, L.nrhs, L.s, L.ws.perm);
+    }
+    trsm_lower_in_factor(L, c0, c0 + h, c0 + h, nc - h, true);
+    gemm_update(L, L.n - c0 - h, nc - h, h, size_t(c0) * L.ld + c0 + h, size_t(c0 + h) * L.ld + c0,
+                size_t(c0 + h) * L.ld + c0 + h, cplx{-1, 0}, cplx{1, 0}, L.hA, L.hA, L.ld);
+    {  // B[c0+h:n] -= A21 B[c0:c0+h]
+        auto& tasks = L.ws.h_gemm;
+        tasks.assign(L.count, GemmTask{});
+        for (int b = 0; b < L.count; ++b) {
+            GemmTask& t = tasks[b];
+            t.nseg = 1;
+            t.A[0] = L.hA[b] + size_t(c0) * L.ld + c0 + h;
+            t.lda[0] = L.ld;
+            t.B[0] = (*L.hB)[b] + c0;
+            t.ldb[0] = L.ldb;
+            t.K[0] = h;
+            t.C = (*L.hB)[b] + c0 + h;
+            t.ldc = L.ldb;
+        }
+        zgemm_batched(L.n - c0 - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks);
+    }
+    lu_rec_spine(L, c0 + h, nc - h);
+}
+
+// x <- U^{-1} x on 64-aligned recursive splits (U's inverse diagonal tiles in
+// hDinv, second half of each tile pair)
+void upper_solve_tiles(int n, int ld, const std::vector<cplx*>& hA, const std::vector<cplx*>& hDinv,
+                       const std::vector<cplx*>& hB, int ldb, int nrhs, cudaStream_t s, Workspace& ws) {
+    const int count = int(hA.size());
+    auto& tasks = ws.h_gemm;
+    std::function<void(int, int)> upper = [&](int b0, int b1) {
+        if (b1 - b0 == 1) {
+            const int k0 = b0 * kTB, kend = std::min(k0 + kTB, n);
+            tasks.assign(count, GemmTask{});
+            for (int b = 0; b < count; ++b) {
+                GemmTask& t = tasks[b];
+                t.nseg = 1;
+                t.A[0] = hDinv[b] + size_t(b0) * 2 * kTB * kTB + size_t(kTB) * kTB;
+                t.lda[0] = kTB;
+                t.B[0] = hB[b] + k0;
+                t.ldb[0] = ldb;
+                t.K[0] = kend - k0;
+                t.C = hB[b] + k0;
+                t.ldc = ldb;
+            }
+            zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks);
+            return;
+        }
+        const int bm = (b0 + b1 + 1) / 2;
+        upper(bm, b1);
+        const int r0 = b0 * kTB, rm = bm * kTB, r1 = std::min(b1 * kTB, n);
+        tasks.assign(count, GemmTask{});
+        for (int b = 0; b < count; ++b) {
+            GemmTask& t = tasks[b];
+            t.nseg = 1;
+            t.A[0] = hA[b] + size_t(rm) * ld + r0;
+            t.lda[0] = ld;
+            t.B[0] = hB[b] + rm;
+            t.ldb[0] = ldb;
+            t.K[0] = r1 - rm;
+            t.C = hB[b] + r0;
+            t.ldc = ldb;
+        }
+        zgemm_batched(rm - r0, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+        upper(b0, bm);
+    };
+    upper(0, (n + kTB - 1) / kTB);
 }
 
 // right-looking LU: n/16 steps of (fused panel kernel, trailing 3M GEMM with
@@ -2258,6 +2481,30 @@ void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::v
     else lu_rec(L, 0, n);
     // inverse 64x64 diagonal tiles of L and U for the GEMM-shaped solves
     launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 3, s);
+}
+
+// LU with partial pivoting of every matrix and the solve A X = B in one pass:
+// the forward substitution rides along the recursion (lu_rec_spine), the back
+// substitution uses U's inverse diagonal tiles.  The factors are left as
+// U plus an L whose rows below the spine are not re-permuted: use this only
+// when A is not solved against again.  B (ld ldb, nrhs columns) becomes X.
+void lu_factor_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,
+                             const std::vector<cplx*>& hDinv, const std::vector<cplx*>& hB, int ldb, int nrhs,
+                             int* d_singular, cudaStream_t s, Workspace& ws) {
+    const int count = int(hA.size());
+    if (count == 0) return;
+    ws.ptrs.upload(hA, s);
+    ws.iptrs.upload(hP, s);
+    ws.ptrs3.upload(hDinv, s);
+    ws.ptrs2.upload(hB, s);
+    LuCtx L{n, ld, count, hA, hP, hDinv, ws.ptrs.p, ws.iptrs.p, ws.ptrs3.p, d_singular, s, ws};
+    L.hB = &hB;
+    L.dB = ws.ptrs2.p;
+    L.ldb = ldb;
+    L.nrhs = nrhs;
+    lu_rec_spine(L, 0, n);
+    launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 2, s);  // U tiles only
+    upper_solve_tiles(n, ld, hA, hDinv, hB, ldb, nrhs, s, ws);
 }
 
 void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::vector<int*>& hP,

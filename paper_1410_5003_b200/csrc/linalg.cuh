@@ -75,6 +75,10 @@ size_t lu_dinv_elems(int n);
 void lu_factor_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv,
                        const std::vector<cplx*>& Dinv, int* d_singular, cudaStream_t s, Workspace& ws);
 // B_b <- A_b^{-1} B_b for n x nrhs right-hand sides (ldb) using those factors.
+// factor + solve A X = B in one pass (A's factors are not reusable afterwards)
+void lu_factor_solve_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv,
+                             const std::vector<cplx*>& dinv, const std::vector<cplx*>& B, int ldb, int nrhs,
+                             int* d_singular, cudaStream_t s, Workspace& ws);
 void lu_solve_batched(int n, int ld, const std::vector<cplx*>& A, const std::vector<int*>& ipiv,
                       const std::vector<cplx*>& Dinv, const std::vector<cplx*>& B, int ldb, int nrhs,
                       cudaStream_t s, Workspace& ws);

@@ -1,3 +1,4 @@
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -69,6 +70,7 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 namespace {
 struct Pending {
     std::string name;
+    cudaStream_t s;
     cudaEvent_t e0, e1;
     double flops, bytes, units;
     int nlaunch;
@@ -82,6 +84,10 @@ const char* g_phase = nullptr;
 std::vector<Pending> g_pending;
 std::map<std::string, Agg> g_agg;
 std::vector<cudaEvent_t> g_free;
+// QPS_PROF_TIMELINE: every scope's [start, end] on its stream, relative to the
+// first scope after prof_reset, printed to stderr as the scopes resolve
+cudaEvent_t g_ref = nullptr;
+bool g_ref_set = false;
 
 cudaEvent_t get_event() {
     if (!g_free.empty()) {
@@ -95,10 +101,16 @@ cudaEvent_t get_event() {
 }
 
 void resolve() {
+    static const bool timeline = getenv("QPS_PROF_TIMELINE") != nullptr;
     for (auto& p : g_pending) {
         cudaEventSynchronize(p.e1);
         float ms = 0;
         cudaEventElapsedTime(&ms, p.e0, p.e1);
+        if (timeline && g_ref_set) {
+            float t0 = 0;
+            cudaEventElapsedTime(&t0, g_ref, p.e0);
+            fprintf(stderr, "TL %-28s stream %p start %9.3f end %9.3f ms\n", p.name.c_str(), (void*)p.s, t0, t0 + ms);
+        }
         Agg& a = g_agg[p.name];
         a.launches += p.nlaunch;
         a.ms += ms;
@@ -117,6 +129,7 @@ bool prof_enabled() { return g_on; }
 void prof_reset() {
     resolve();
     g_agg.clear();
+    g_ref_set = false;
 }
 
 ProfScope::ProfScope(const char* name_, cudaStream_t s_, double flops_, double bytes_, double units_, int nl)
@@ -125,6 +138,11 @@ ProfScope::ProfScope(const char* name_, cudaStream_t s_, double flops_, double b
     if (!g_on) return;
     e0 = get_event();
     e1 = get_event();
+    if (!g_ref_set) {
+        if (!g_ref) cudaEventCreate(&g_ref);
+        cudaEventRecord(g_ref, s);
+        g_ref_set = true;
+    }
     cudaEventRecord(e0, s);
 }
 
@@ -133,7 +151,7 @@ ProfScope::~ProfScope() {
     cudaEventRecord(e1, s);
     static const bool phases = getenv("QPS_PROF_PHASES") != nullptr;
     std::string key = (phases && g_phase) ? std::string(g_phase) + ":" + name : std::string(name);
-    g_pending.push_back({key, e0, e1, flops, bytes, units, nlaunch});
+    g_pending.push_back({key, s, e0, e1, flops, bytes, units, nlaunch});
     if (g_pending.size() > 4096) resolve();
 }
 

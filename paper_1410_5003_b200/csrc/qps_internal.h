@@ -92,6 +92,31 @@ struct DBuf {
     }
 };
 
+// Pinned host buffer: small device->host reads that must not block the host
+// (a D2H copy into pageable memory returns only once the stream reaches it).
+template <class T>
+struct HBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    HBuf() = default;
+    HBuf(const HBuf&) = delete;
+    HBuf& operator=(const HBuf&) = delete;
+    ~HBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t count) {
+        if (count <= n && p) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        if (count == 0) return;
+        QPS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), count * sizeof(T)));
+        n = count;
+    }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
+};
+
 // ---------------------------------------------------------------------------
 // Host geometry (reference-equivalent arithmetic; geometry.hpp)
 // ---------------------------------------------------------------------------

@@ -489,109 +489,138 @@ struct QFamily {
     size_t Xstride;
     double* lsq_out;
     cudaStream_t s;
-    std::vector<double> rmax, xmax;
     std::vector<int> flags;
-    bool pending = true;
+    double th = 0.0;
+    int stage = 0;  // 1: a threshold step in flight, 2: residual norms in flight
 };
 
-void qsolve_families(Ctx& c, std::vector<QFamily>& fams) {
+// Each family advances on its own stream: the host polls the families' last
+// read-back events and queues the next step of whichever family is ready
+// (threshold escalation or the residual norms), so a slow family never holds
+// up another one.  Read-backs land in pinned buffers (non-blocking copies).
+void qsolve_step(Ctx& c, QFamily& f) {
+    CodSet& cs = *f.cs;
+    CodBatch b = cs.batch(f.Q);
+    cs.flags.upload(f.flags, f.s);
+    cod_rank(b, f.th, cs.flags.p, f.s);
+    cod_operator(b, cs.flags.p, f.s);
+    // X = Wz * T11^{-1} * (QH * RHS)
+    std::vector<GemmTask> t1, t2;
+    for (int q = 0; q < cs.count; ++q) {
+        if (!f.flags[q]) continue;
+        GemmTask t{};
+        t.nseg = 1;
+        t.A[0] = cs.QH.p + size_t(q) * cs.p * cs.m;
+        t.lda[0] = cs.p;
+        t.B[0] = f.R + f.Rstride * q;
+        t.ldb[0] = f.ldR;
+        t.K[0] = cs.m;
+        t.C = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
+        t.ldc = cs.p;
+        t1.push_back(t);
+        GemmTask u{};
+        u.nseg = 1;
+        u.A[0] = cs.Wz.p + size_t(q) * cs.p * cs.p;
+        u.lda[0] = cs.p;
+        u.B[0] = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
+        u.ldb[0] = cs.p;
+        u.K[0] = cs.p;
+        u.C = f.X + f.Xstride * q;
+        u.ldc = f.ldX;
+        t2.push_back(u);
+    }
+    zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t1, f.s, cs.tasks1);
+    cod_trsm(b, cs.Tb.p, cs.p, size_t(cs.p) * cs.ncols, cs.ncols, cs.flags.p, f.s);
+    zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t2, f.s, cs.tasks2);
+    batched_maxabs(f.X, cs.p, cs.ncols, f.ldX, f.Xstride, cs.count, cs.xmax.p, f.s);
+    QPS_D2H(cs.h_xmax.p, cs.xmax.p, sizeof(double) * cs.count, f.s);
+    QPS_CUDA(cudaEventRecord(cs.ev, f.s));
+    f.stage = 1;
+}
+
+// relative LSQ residual ||Q X - R|| / ||R||  (periodize.hpp:84,113-118);
+// ||Q X - R||_F reduced in the GEMM epilogue (R only read, Q X - R never stored)
+void qsolve_residuals(QFamily& f) {
+    CodSet& cs = *f.cs;
+    const int cnt = cs.count;
+    std::vector<GemmTask> tasks(cnt);
+    for (int q = 0; q < cnt; ++q) {
+        GemmTask& t = tasks[q];
+        t.nseg = 1;
+        t.A[0] = f.Q + size_t(q) * cs.m * cs.p;
+        t.lda[0] = cs.m;
+        t.B[0] = f.X + f.Xstride * q;
+        t.ldb[0] = f.ldX;
+        t.K[0] = cs.p;
+        t.C = const_cast<cplx*>(f.R) + f.Rstride * q;
+        t.ldc = f.ldR;
+    }
+    zgemm_residual_norms(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, f.s, cs.tasks1, cs.parts, cs.enorm.p);
+    QPS_D2H(cs.h_enorm.p, cs.enorm.p, sizeof(double) * cnt, f.s);
+    QPS_D2H(cs.h_rnorm.p, cs.rnorm.p, sizeof(double) * cnt, f.s);
+    QPS_CUDA(cudaEventRecord(cs.ev, f.s));
+    f.stage = 2;
+}
+
+void qsolve_poll(Ctx& c, std::vector<QFamily>& fams, bool first_only);
+
+// Queues every family to completion (X final, residual norms read back
+// asynchronously); qsolve_collect waits for the read-backs.  With
+// first_only the host returns as soon as fams[0] is complete (the others keep
+// running on their streams; call again without first_only to finish them).
+void qsolve_families(Ctx& c, std::vector<QFamily>& fams, bool first_only = false) {
     for (auto& f : fams) {
         CodSet& cs = *f.cs;
-        f.pending = cs.count > 0;
-        if (!f.pending) continue;
+        f.stage = 2;
+        if (cs.count <= 0) continue;
         CodBatch b = cs.batch(f.Q);
         cod_factor(b, f.s);
-        // scale = max(1, max |RHS|)
         // max |RHS| (the acceptance scale) and ||RHS||_F (the residual's denominator) in one pass
         batched_fro(f.R, cs.m, cs.ncols, f.ldR, f.Rstride, cs.count, cs.rnorm.p, f.s, cs.rmax.p);
-        f.rmax.assign(cs.count, 0.0);
-        f.xmax.assign(cs.count, 0.0);
+        QPS_D2H(cs.h_rmax.p, cs.rmax.p, sizeof(double) * cs.count, f.s);
         f.flags.assign(cs.count, 1);
-        QPS_D2H(f.rmax.data(), cs.rmax.p, sizeof(double) * cs.count, f.s);
+        f.th = c.qsolve_th0;
+        qsolve_step(c, f);
     }
-    for (double th = c.qsolve_th0; th <= 1.1e-10; th *= 10.0) {
-        bool any_pending = false;
+    qsolve_poll(c, fams, first_only);
+}
+
+void qsolve_poll(Ctx& c, std::vector<QFamily>& fams, bool first_only) {
+    for (;;) {
+        if (first_only && !fams.empty() && fams[0].stage == 2) return;
+        bool busy = false;
         for (auto& f : fams) {
-            if (!f.pending) continue;
-            any_pending = true;
+            if (f.stage != 1) continue;
+            busy = true;
+            const cudaError_t q = cudaEventQuery(f.cs->ev);
+            if (q == cudaErrorNotReady) continue;
+            QPS_CUDA(q);
             CodSet& cs = *f.cs;
-            CodBatch b = cs.batch(f.Q);
-            cs.flags.upload(f.flags, f.s);
-            cod_rank(b, th, cs.flags.p, f.s);
-            cod_operator(b, cs.flags.p, f.s);
-            // X = Wz * T11^{-1} * (QH * RHS)
-            std::vector<GemmTask> t1, t2;
-            for (int q = 0; q < cs.count; ++q) {
-                if (!f.flags[q]) continue;
-                GemmTask t{};
-                t.nseg = 1;
-                t.A[0] = cs.QH.p + size_t(q) * cs.p * cs.m;
-                t.lda[0] = cs.p;
-                t.B[0] = f.R + f.Rstride * q;
-                t.ldb[0] = f.ldR;
-                t.K[0] = cs.m;
-                t.C = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
-                t.ldc = cs.p;
-                t1.push_back(t);
-                GemmTask u{};
-                u.nseg = 1;
-                u.A[0] = cs.Wz.p + size_t(q) * cs.p * cs.p;
-                u.lda[0] = cs.p;
-                u.B[0] = cs.Tb.p + size_t(q) * cs.p * cs.ncols;
-                u.ldb[0] = cs.p;
-                u.K[0] = cs.p;
-                u.C = f.X + f.Xstride * q;
-                u.ldc = f.ldX;
-                t2.push_back(u);
-            }
-            zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t1, f.s, cs.tasks1);
-            cod_trsm(b, cs.Tb.p, cs.p, size_t(cs.p) * cs.ncols, cs.ncols, cs.flags.p, f.s);
-            zgemm_batched(cs.p, cs.ncols, cplx{1, 0}, cplx{0, 0}, t2, f.s, cs.tasks2);
-            batched_maxabs(f.X, cs.p, cs.ncols, f.ldX, f.Xstride, cs.count, cs.xmax.p, f.s);
-            QPS_D2H(f.xmax.data(), cs.xmax.p, sizeof(double) * cs.count, f.s);
-        }
-        if (!any_pending) break;
-        for (auto& f : fams) {
-            if (!f.pending) continue;
-            QPS_CUDA(cudaStreamSynchronize(f.s));
             bool any = false;
-            for (int q = 0; q < f.cs->count; ++q) {
-                if (!f.flags[q]) continue;
-                const double scale = std::max(1.0, f.rmax[q]);
-                if (f.xmax[q] <= 1e3 * scale) f.flags[q] = 0;  // accepted (qsolve_norm_cap, periodize.hpp:23)
+            for (int i = 0; i < cs.count; ++i) {
+                if (!f.flags[i]) continue;
+                const double scale = std::max(1.0, cs.h_rmax[i]);
+                if (cs.h_xmax[i] <= 1e3 * scale) f.flags[i] = 0;  // accepted (qsolve_norm_cap, periodize.hpp:23)
                 else any = true;
             }
-            f.pending = any;
+            // threshold escalation th0, 10 th0, ... up to 1e-10 (periodize.hpp:29-37)
+            if (any && f.th * 10.0 <= 1.1e-10) {
+                f.th *= 10.0;
+                qsolve_step(c, f);
+            } else {
+                qsolve_residuals(f);
+            }
         }
+        if (!busy) break;
     }
-    // relative LSQ residual ||Q X - R|| / ||R||  (periodize.hpp:84,113-118)
+}
+
+void qsolve_collect(std::vector<QFamily>& fams) {
     for (auto& f : fams) {
         CodSet& cs = *f.cs;
-        const int cnt = cs.count;
-        if (cnt == 0) continue;
-        // ||Q X - R||_F reduced in the GEMM epilogue (R only read, Q X - R never stored)
-        std::vector<GemmTask> tasks(cnt);
-        for (int q = 0; q < cnt; ++q) {
-            GemmTask& t = tasks[q];
-            t.nseg = 1;
-            t.A[0] = f.Q + size_t(q) * cs.m * cs.p;
-            t.lda[0] = cs.m;
-            t.B[0] = f.X + f.Xstride * q;
-            t.ldb[0] = f.ldX;
-            t.K[0] = cs.p;
-            t.C = const_cast<cplx*>(f.R) + f.Rstride * q;
-            t.ldc = f.ldR;
-        }
-        zgemm_residual_norms(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, f.s, cs.tasks1, cs.parts, cs.enorm.p);
-        f.rmax.assign(cnt, 0.0);  // reused: residual norms
-        f.xmax.assign(cnt, 0.0);
-        QPS_D2H(f.rmax.data(), cs.enorm.p, sizeof(double) * cnt, f.s);
-        QPS_D2H(f.xmax.data(), cs.rnorm.p, sizeof(double) * cnt, f.s);
-    }
-    for (auto& f : fams) {
-        if (f.cs->count == 0) continue;
-        QPS_CUDA(cudaStreamSynchronize(f.s));
-        for (int q = 0; q < f.cs->count; ++q) f.lsq_out[q] = f.rmax[q] / f.xmax[q];
+        if (cs.count <= 0) continue;
+        QPS_CUDA(cudaEventSynchronize(cs.ev));
+        for (int q = 0; q < cs.count; ++q) f.lsq_out[q] = cs.h_enorm[q] / cs.h_rnorm[q];
     }
 }
 
@@ -601,6 +630,7 @@ void qsolve_family(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, si
     f[0].cs = &cs; f[0].Q = Q; f[0].R = R; f[0].ldR = ldR; f[0].Rstride = Rstride;
     f[0].X = X; f[0].ldX = ldX; f[0].Xstride = Xstride; f[0].lsq_out = lsq_out; f[0].s = c.stream;
     qsolve_families(c, f);
+    qsolve_collect(f);
 }
 
 }  // namespace
@@ -642,18 +672,11 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
     // the side stream starts after everything queued so far (the fill) on the main stream
     QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
     QPS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-    qsolve_families(c, fams);
-    for (int a = 0; a < ns; ++a) {
-        double* l = c.lsq_all.data() + size_t(a) * (I + 1);
-        l[0] = lc[2 * a];
-        l[I] = lc[2 * a + 1];
-        for (int i = 1; i < I; ++i) l[i] = li[size_t(a) * (I - 1) + (i - 1)];
-    }
-    c.lsq.assign(c.lsq_all.begin(), c.lsq_all.begin() + (I + 1));
+    qsolve_families(c, fams, true);  // returns once the interior layers are done
     // A' updates of all systems in one batched GEMM (periodize.hpp:88-91, 115, 119):
     //   Ap_diag[j] -= B_self[j] X_self(j) + B_below[j] X_above(j+1)
     //   Ap_super[j] -= B_below[j] X_self(j+1),  Ap_sub[j] -= B_self[j+1] X_above(j+1)
-    std::vector<GemmTask> tasks;
+    std::vector<GemmTask> tasks, ctasks;
     c.coupling_sup.clear();
     c.coupling_sub.clear();
     c.couplings_deferred = false;
@@ -672,19 +695,23 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
         cplx* Aua = Au + size_t(a) * D.sU();
         cplx* Ala = Al + size_t(a) * D.sU();
         for (int j = 0; j < I; ++j) {
-            GemmTask t{};
-            t.nseg = 2;
-            t.A[0] = c.Bself.p + size_t(j) * nb * P;
-            t.lda[0] = nb;
-            xself(j, t.B[0], t.ldb[0]);
-            t.K[0] = P;
-            t.A[1] = c.Bbelow.p + size_t(j) * nb * P;
-            t.lda[1] = nb;
-            xabove(j + 1, t.B[1], t.ldb[1]);
-            t.K[1] = P;
-            t.C = Ada + j * nb2;
-            t.ldc = nb;
-            tasks.push_back(t);
+            // segments that read a corner X (j = 0: X_first, j = I-1: X_last) go
+            // to a second GEMM queued after the corner least squares finish
+            GemmTask t{}, tc{};
+            auto seg = [&](GemmTask& g, const cplx* A, bool self, int i) {
+                const int q = g.nseg++;
+                g.A[q] = A;
+                g.lda[q] = nb;
+                if (self) xself(i, g.B[q], g.ldb[q]);
+                else xabove(i, g.B[q], g.ldb[q]);
+                g.K[q] = P;
+            };
+            seg(j == 0 ? tc : t, c.Bself.p + size_t(j) * nb * P, true, j);
+            seg(j + 1 == I ? tc : t, c.Bbelow.p + size_t(j) * nb * P, false, j + 1);
+            t.C = tc.C = Ada + j * nb2;
+            t.ldc = tc.ldc = nb;
+            if (t.nseg) tasks.push_back(t);
+            if (tc.nseg) ctasks.push_back(tc);
             if (j + 1 < I) {
                 GemmTask u{};
                 u.nseg = 1;
@@ -713,6 +740,19 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
         }
     }
     zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks, "schur_update");
+    qsolve_poll(c, fams, false);  // the corner least squares (side stream)
+    // the corner terms: the main stream joins the corner stream here
+    QPS_CUDA(cudaEventRecord(c.ev_fork, c.side));
+    QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_fork, 0));
+    zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, ctasks, c.stream, c.ws.gemm_tasks, "schur_update");
+    qsolve_collect(fams);  // per-layer LSQ residuals, read back while the update runs
+    for (int a = 0; a < ns; ++a) {
+        double* l = c.lsq_all.data() + size_t(a) * (I + 1);
+        l[0] = lc[2 * a];
+        l[I] = lc[2 * a + 1];
+        for (int i = 1; i < I; ++i) l[i] = li[size_t(a) * (I - 1) + (i - 1)];
+    }
+    c.lsq.assign(c.lsq_all.begin(), c.lsq_all.begin() + (I + 1));
     c.couplings_deferred = defer_couplings && I > 1;
     c.max_lsq = 0.0;
     for (double r : c.lsq) c.max_lsq = std::max(c.max_lsq, r);
