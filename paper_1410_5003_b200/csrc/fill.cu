@@ -100,13 +100,20 @@ __device__ __forceinline__ int seg_index(const PairTask& T, int m) {
 // smooth self, 2 open-arc self) and the number of wavenumbers (the A_jj blocks
 // sum two); the specialisation removes per-pair branches and lets the two
 // wavenumber evaluations of a pair interleave
-template <int SELF, int NK>
+// Mirrored tiles stage the transposed block's entries in shared memory
+// (s_mir: 4 kinds x 16 source rows x 32 (+1) targets) and write them
+// coalesced every 16 source columns: written directly, each would be a
+// separate 16-byte store and the LSU queue stalls the tile's shared loads.
+constexpr int kMirRows = 16, kMirLd = kTile + 1;
+
+template <int SELF, int NK, bool MIRROR>
 __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, DevPool pool, const double* sx,
                                           const double* sy, const double* snx, const double* sny, const double* sw,
-                                          const double2* s_near2, int* err) {
+                                          const double2* s_near2, int* err, bool mir, cplx* s_mir) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int m = m0 + lane;
-    if (m >= T.nt) return;
+    const bool act = m < T.nt;
+    if (!MIRROR && !act) return;
     // task constants in registers
     const int nterm = T.nterm, ns = T.ns;
     constexpr int nk = NK, self = SELF;
@@ -115,8 +122,9 @@ __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, Dev
     // per-wavenumber scale factors: sign/4, sign*k/4 and (8/k)^2 for u = (8/x)^2
     const double s40 = 0.25 * sg0, s41 = 0.25 * sg1, d40 = s40 * k0, d41 = s41 * k1;
     const double u0 = 64.0 * ik0 * ik0, u1 = 64.0 * ik1 * ik1;
-    const int gt = T.t_off + m;
+    const int gt = T.t_off + (act ? m : 0);
     const double tx = pool.x[gt], ty = pool.y[gt], tnx = pool.nx[gt], tny = pool.ny[gt];
+    const double wm = MIRROR ? pool.w[gt] : 0.0;  // the target's weight as a mirrored source
     bool corrected = true;
     int mseg = 0;
     if (self == 2) {
@@ -124,10 +132,9 @@ __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, Dev
         const int ml = m - T.seg_start[mseg], n = T.seg_start[mseg + 1] - T.seg_start[mseg];
         corrected = min(ml, n - 1 - ml) >= QPS_ALPERT_A;
     }
-#pragma unroll 1
-    for (int q = warp; q < kTile; q += kThreads / 32) {
+    // one (target m, source column q) entry: original into the block, mirror into (bD.. )
+    auto entry = [&](int q, cplx& bD, cplx& bS, cplx& bT, cplx& bDs) {
         const int j = j0 + q;
-        if (j >= ns) break;
         cplx aD{0, 0}, aS{0, 0}, aT{0, 0}, aDs{0, 0};
         const double zx0 = sx[q], zy = sy[q], znx = snx[q], zny = sny[q], w = sw[q];
         const double nn = tnx * znx + tny * zny;
@@ -188,6 +195,14 @@ __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, Dev
             cmacc(aS, wc, tS);
             cmacc(aT, wc, tT);
             cmacc(aDs, wc, tDs);
+            if (MIRROR && mir) {
+                const cplx mc = T.mcoef[t];
+                const cplx wmc{wm * mc.re, wm * mc.im};
+                cmacc(bD, wmc, tDs);
+                cmacc(bS, wmc, tS);
+                cmacc(bT, wmc, tT);
+                cmacc(bDs, wmc, tD);
+            }
         }
         if (T.ident && j == m) {
             aD.re -= 1.0;
@@ -198,13 +213,52 @@ __device__ __forceinline__ void pair_tile(const PairTask& T, int m0, int j0, Dev
         store(T.oS + o, aS, T.accumulate);
         store(T.oT + o, aT, T.accumulate);
         store(T.oDs + o, aDs, T.accumulate);
+    };
+    if constexpr (!MIRROR) {
+#pragma unroll 1
+        for (int q = warp; q < kTile; q += kThreads / 32) {
+            if (j0 + q >= ns) break;
+            cplx bD, bS, bT, bDs;
+            entry(q, bD, bS, bT, bDs);
+        }
+    } else {
+#pragma unroll 1
+        for (int half = 0; half < kTile / kMirRows; ++half) {
+#pragma unroll 1
+            for (int q = half * kMirRows + warp; q < (half + 1) * kMirRows; q += kThreads / 32) {
+                if (!act || j0 + q >= ns) continue;
+                cplx bD{0, 0}, bS{0, 0}, bT{0, 0}, bDs{0, 0};
+                entry(q, bD, bS, bT, bDs);
+                if (mir) {
+                    const int rq = (q - half * kMirRows) * kMirLd + lane;
+                    s_mir[0 * kMirRows * kMirLd + rq] = bD;
+                    s_mir[1 * kMirRows * kMirLd + rq] = bS;
+                    s_mir[2 * kMirRows * kMirLd + rq] = bT;
+                    s_mir[3 * kMirRows * kMirLd + rq] = bDs;
+                }
+            }
+            if (!mir) continue;  // CTA-uniform
+            __syncthreads();
+            // rows j0 + half*16 .. +15 of the mirror block, columns m0 .. m0+31:
+            // 16 consecutive rows (256 bytes) per column
+            for (int e = threadIdx.x; e < 4 * kTile * kMirRows; e += kThreads) {
+                const int kind = e / (kTile * kMirRows), rem = e % (kTile * kMirRows);
+                const int col = rem / kMirRows, row = rem % kMirRows;
+                const int n = j0 + half * kMirRows + row, mm = m0 + col;
+                if (n >= ns || mm >= T.nt) continue;
+                cplx* base = kind == 0 ? T.mD : kind == 1 ? T.mS : kind == 2 ? T.mT : T.mDs;
+                store(base + size_t(mm) * T.mld + n, s_mir[kind * kMirRows * kMirLd + row * kMirLd + col],
+                      T.accumulate);
+            }
+            __syncthreads();
+        }
     }
 }
 
 // one kernel per block kind (self kind x wavenumber count): each gets its own
 // register allocation instead of the largest of the six
-template <int SELF, int NK>
-__global__ void __launch_bounds__(kThreads, (SELF == 0 && NK == 1) ? QPS_MINB_PLAIN : QPS_MINB_SELF)
+template <int SELF, int NK, bool MIRROR>
+__global__ void __launch_bounds__(kThreads, (SELF == 0 && NK == 1 && !MIRROR) ? QPS_MINB_PLAIN : QPS_MINB_SELF)
     pair_fill_kernel(const PairTask* __restrict__ tasks, const int4* __restrict__ tiles, DevPool pool,
                      const double* __restrict__ g_near, int* err) {
     __shared__ double2 s_near2[QPS_HANKEL_XB * QPS_HANKEL_NEAR_TERMS * 2];
@@ -217,7 +271,22 @@ __global__ void __launch_bounds__(kThreads, (SELF == 0 && NK == 1) ? QPS_MINB_PL
     if (threadIdx.x == 0) T = tasks[tk.x];
     load_near2(s_near2, g_near);
     __syncthreads();
-    const int m0 = (int(blockIdx.x) % tk.y) * kTile, j0 = (int(blockIdx.x) / tk.y) * kTile;
+    // tk.w: self block on its upper tile triangle (index c (c + 1) / 2 + r, r <= c),
+    // the strictly upper tiles mirrored onto the lower ones
+    int tr, tc;
+    if (MIRROR && tk.w) {
+        const int idx = int(blockIdx.x);
+        int cc = int((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+        while (cc * (cc + 1) / 2 > idx) --cc;
+        while ((cc + 1) * (cc + 2) / 2 <= idx) ++cc;
+        tc = cc;
+        tr = idx - cc * (cc + 1) / 2;
+    } else {
+        tr = int(blockIdx.x) % tk.y;
+        tc = int(blockIdx.x) / tk.y;
+    }
+    const int m0 = tr * kTile, j0 = tc * kTile;
+    const bool mir = MIRROR && !(tk.w && tr == tc);
     if (threadIdx.x < kTile) {
         const int j = j0 + threadIdx.x;
         if (j < T.ns) {
@@ -230,7 +299,8 @@ __global__ void __launch_bounds__(kThreads, (SELF == 0 && NK == 1) ? QPS_MINB_PL
         }
     }
     __syncthreads();
-    pair_tile<SELF, NK>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err);
+    __shared__ cplx s_mir[MIRROR ? 4 * kMirRows * kMirLd : 1];
+    pair_tile<SELF, NK, MIRROR>(T, m0, j0, pool, sx, sy, snx, sny, sw, s_near2, err, mir, s_mir);
 }
 
 __global__ void __launch_bounds__(kThreads) proxy_fill_kernel(const ProxyTask* __restrict__ tasks,
@@ -549,46 +619,55 @@ void build_tiles(const std::vector<Task>& tasks, std::vector<int4>& tiles, int (
 void launch_pair_fill(const std::vector<PairTask>& tasks, const DevPool& pool, int* d_err, cudaStream_t s,
                       DBuf<PairTask>& d_tasks, DBuf<int4>& d_tiles) {
     if (tasks.empty()) return;
-    // one launch per block kind (self * 2 + nk - 1) over a 2-D grid (tile,
-    // task of the kind): the tile of a CTA is computed in-kernel, so no tile
-    // list is built on the host or uploaded
-    std::vector<int4> ids[6];
-    int maxt[6] = {0};
+    // one launch per block kind (self * 2 + nk - 1, plus 6 + self * 2 + nk - 1
+    // for mirrored tasks) over a 2-D grid (tile, task of the kind): the tile of
+    // a CTA is computed in-kernel, so no tile list is built on the host
+    constexpr int kKinds = 10;
+    std::vector<int4> ids[kKinds];
+    int maxt[kKinds] = {0};
     for (int t = 0; t < int(tasks.size()); ++t) {
         const PairTask& T = tasks[t];
-        const int kind = T.self * 2 + (T.nk - 1);
-        if (kind < 0 || kind > 5) fail(QPS_ERR_INTERNAL, "pair fill: unknown block kind");
+        int kind = T.self * 2 + (T.nk - 1);
+        if (kind < 0 || kind > 5 || (T.mirror && T.self > 1)) fail(QPS_ERR_INTERNAL, "pair fill: unknown block kind");
+        if (T.mirror) kind += 6;
         const int tm = (T.nt + kTile - 1) / kTile, tn = (T.ns + kTile - 1) / kTile;
         if (tm * tn == 0) continue;
-        ids[kind].push_back(make_int4(t, tm, tm * tn, 0));
-        maxt[kind] = std::max(maxt[kind], tm * tn);
+        const bool tri = T.mirror && T.self == 1;
+        if (tri && tm != tn) fail(QPS_ERR_INTERNAL, "pair fill: mirrored self block must be square");
+        const int ntile = tri ? tm * (tm + 1) / 2 : tm * tn;
+        ids[kind].push_back(make_int4(t, tm, ntile, tri ? 1 : 0));
+        maxt[kind] = std::max(maxt[kind], ntile);
     }
     std::vector<int4> all;
-    size_t off[7] = {0};
-    for (int kind = 0; kind < 6; ++kind) {
+    size_t off[kKinds + 1] = {0};
+    for (int kind = 0; kind < kKinds; ++kind) {
         off[kind] = all.size();
         all.insert(all.end(), ids[kind].begin(), ids[kind].end());
     }
-    off[6] = all.size();
+    off[kKinds] = all.size();
     if (all.empty()) return;
     d_tasks.upload(tasks, s);
     d_tiles.upload(all, s);
-    double ev = 0;
-    for (const auto& t : tasks) ev += double(t.nt) * t.ns * t.nterm * t.nk;
+    double ev = 0;  // kernel evaluations produced (a mirrored pair yields two)
+    for (const auto& t : tasks) ev += double(t.nt) * t.ns * t.nterm * t.nk * (t.mirror && t.self == 0 ? 2 : 1);
     ProfScope ps("fill_pair", s, 200.0 * ev, 0.0, ev);
-    for (int kind = 0; kind < 6; ++kind) {
+    for (int kind = 0; kind < kKinds; ++kind) {
         const unsigned n = unsigned(off[kind + 1] - off[kind]);
         if (!n) continue;
         if (n > 65535) fail(QPS_ERR_CONFIG, "pair fill: too many blocks of one kind for one launch");
         const int4* tl = d_tiles.p + off[kind];
         const dim3 grid(unsigned(maxt[kind]), n);
         switch (kind) {
-            case 0: pair_fill_kernel<0, 1><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 1: pair_fill_kernel<0, 2><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 2: pair_fill_kernel<1, 1><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 3: pair_fill_kernel<1, 2><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 4: pair_fill_kernel<2, 1><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            default: pair_fill_kernel<2, 2><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 0: pair_fill_kernel<0, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 1: pair_fill_kernel<0, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 2: pair_fill_kernel<1, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 3: pair_fill_kernel<1, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 4: pair_fill_kernel<2, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 5: pair_fill_kernel<2, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 6: pair_fill_kernel<0, 1, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 7: pair_fill_kernel<0, 2, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 8: pair_fill_kernel<1, 1, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            default: pair_fill_kernel<1, 2, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
         }
         QPS_CUDA(cudaGetLastError());
     }

@@ -30,6 +30,16 @@ struct PairTask {
     int accumulate;  // 0 overwrite, 1 add
     cplx *oD, *oS, *oT, *oDs;
     int ld;
+    // Mirror (self 0 or 1): the pair (source n, target m, shift -l) has the
+    // separation -r of (m, n, l), so one Hankel evaluation also gives the
+    // transposed block's entry (n, m): S, T unchanged, D and D* exchanged,
+    // weighted by the target's weight and mcoef.  Couplings: the block
+    // A_{j+1,j} with A_{j,j+1}; smooth self blocks: the lower tile triangle
+    // from the upper one (same block).
+    int mirror;
+    cplx mcoef[3];
+    cplx *mD, *mS, *mT, *mDs;
+    int mld;
 };
 
 // Combined-field proxy columns phi_p = D + ik S and their normal-derivative

@@ -160,6 +160,25 @@ void set_quad_out(PairTask& t, cplx* base, int ld, int row_off, int col_off) {
     t.ld = ld;
 }
 
+// The transposed block shares every Hankel evaluation of t (fill.cuh, PairTask::mirror):
+// its entry (n, m) is sum_l scale_m alpha^{-l} w_m K(x_n, z_m - l d) over t's terms l.
+void set_mirror(PairTask& t, cplx* base, int ld, int row_off, int col_off, cd alpha, cd scale_m) {
+    t.mirror = 1;
+    for (int q = 0; q < t.nterm; ++q) t.mcoef[q] = C(scale_m * std::pow(alpha, -t.lsh[q]));
+    t.mD = base;
+    t.mS = base + size_t(col_off) * ld;
+    t.mT = base + row_off;
+    t.mDs = base + row_off + size_t(col_off) * ld;
+    t.mld = ld;
+}
+bool fill_mirror_enabled() {
+    static const bool on = [] {  // QPS_FILL_MIRROR=0: evaluate every block's pairs separately
+        const char* e = getenv("QPS_FILL_MIRROR");
+        return !(e && !strcmp(e, "0"));
+    }();
+    return on;
+}
+
 PairTask quad_task(int t_off, int nt, int s_off, int ns) {
     PairTask t{};
     t.t_off = t_off;
@@ -268,6 +287,7 @@ void fill_system_fused(Ctx& c) {
             t.ident = 1;
             t.accumulate = 0;
             set_quad_out(t, c.Adiag.p + j * nb2, nb, N, N);
+            if (q.smooth && fill_mirror_enabled()) set_mirror(t, c.Adiag.p + j * nb2, nb, N, N, alpha, 1.0);
             pt.push_back(t);
             AlpertTask a{};
             a.t_off = c.iface_off[j];
@@ -300,10 +320,12 @@ void fill_system_fused(Ctx& c) {
             t.ksign[0] = 1.0;
             three_shifts(t, d, alpha, -1.0);
             set_quad_out(t, c.Asup.p + j * nb2, nb, N, D.N[j + 1]);
+            // A_{j+1,j} = +tilde(coupl_up[j+1]): the same pairs transposed (k_{j+1} both)
+            if (fill_mirror_enabled()) set_mirror(t, c.Asub.p + j * nb2, nb, D.N[j + 1], N, alpha, 1.0);
             pt.push_back(t);
         }
         // A_{j,j-1} = +tilde(coupl_up[j]) (assembly.hpp:354): targets G_j, sources G_{j-1}, k_j
-        if (j >= 1) {
+        if (j >= 1 && !fill_mirror_enabled()) {
             PairTask t = quad_task(c.iface_off[j], N, c.iface_off[j - 1], D.N[j - 1]);
             t.nk = 1;
             t.k[0] = k[j];
@@ -446,7 +468,7 @@ void fill_system_fused(Ctx& c) {
     if (herr) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
     // evaluations performed: plain pairs minus band exclusions plus aux nodes
     uint64_t ev = 0;
-    for (const auto& t : pt) ev += uint64_t(t.nt) * t.ns * t.nterm * t.nk;
+    for (const auto& t : pt) ev += uint64_t(t.nt) * t.ns * t.nterm * t.nk * (t.mirror && t.self == 0 ? 2 : 1);
     for (int j = 0; j < I; ++j) {
         const auto& q = g.ifaces[j];
         const uint64_t N = q.N();
