@@ -50,6 +50,22 @@ def ncu_summary():
 CFG = 4
 
 
+def bcr_factor(phases, I, n, peak):
+    """The block solve's factorization batch (Woodbury level 0: LU with partial
+    pivoting of every n x n diagonal block and its 2r + 1 = 97 right-hand-side
+    solves) against the DMMA peak, at nominal complex flop counts (LU 8/3 n^3,
+    forward + back substitution 8 n^2 per right-hand side; n = 2N, the padding
+    to 608 not counted)."""
+    ms = phases.get("factor_ms") or 0.0
+    if ms <= 0:
+        return None
+    rhs = 97
+    fl = I * (8.0 / 3.0 * n ** 3 + 8.0 * n * n * rhs)
+    tf = fl / (ms * 1e-3) / 1e12
+    return {"ms": ms, "blocks": I, "n": n, "rhs": rhs, "nominal_flops": fl, "tflops": tf,
+            "frac_of_dmma_peak": tf / peak}
+
+
 def workload_config(I, N, num, K, theta, seed):
     return {"workload": f"cfg4: {I} seeded sinusoidal interfaces, N={N}, P={num.P}, Mw={num.Mw}, M={num.M}, "
                         f"K={K}, k~U[10,30], theta={theta:.6f}",
@@ -276,6 +292,7 @@ def main():
                 if fill_ms else None,
                 "fill_fp64_frac_ncu": fill_ncu.get("fp64_frac_of_peak"),
                 "fill_fp64_ncu_note": fill_ncu.get("note"),
+                "bcr_factor": bcr_factor(phases, I, 2 * N, peak),
                 "gemm_tflops_issued": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "gemm_tflops_complex_equiv": gemm_fl * 8.0 / 6.0 / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "fp64_peaks_tflops": peaks, "flux_error": rt["flux_error"], "R": rt["R"], "T": rt["T"],

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define QPS_ABI_VERSION 1
+#define QPS_ABI_VERSION 2
 
 typedef struct qps_ctx qps_ctx;
 typedef struct {
@@ -101,6 +101,10 @@ typedef enum {
 typedef struct {
     double fill_ms, assemble_ms, schur_ms, solve_ms, recover_ms;
     double total_ms; /* device timeline of the last qps_solve, first to last event */
+    /* inside solve_ms: the batched LU of every diagonal block with its
+     * right-hand-side solves (level 0 of the Woodbury cyclic reduction); 0 when
+     * the dense reduction ran or for the CPU oracle */
+    double factor_ms;
 } qps_phase_times;
 
 /* ---------------------------------------------------------------- context */

@@ -670,6 +670,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     }();
     std::vector<int> rk(nc);
     int r = 0;
+    bool rank_deferred = false;
     if (!cpqr_only && nb <= 640) {
         // blocked Householder QR of the samples, CPQR of the 64 x 64 R
         const int m = nb, p = kLrSample, nP = p / kQrW;
@@ -724,17 +725,14 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         CodBatch b = cs.batch(c.lr_R64.p);
         cod_factor_fast(b, s);
         cod_rank(b, kLrTol, nullptr, s);
-        QPS_D2H(rk.data(), cs.rank.p, sizeof(int) * nc, s);
-        QPS_CUDA(cudaStreamSynchronize(s));
-        for (int v : rk) r = std::max(r, v);
-        if (getenv("QPS_LR_TRACE")) {
-            int mn = 1 << 30;
-            double mean = 0;
-            for (int v : rk) { mn = std::min(mn, v); mean += v; }
-            fprintf(stderr, "low-rank couplings: %d blocks, rank min %d mean %.1f max %d (sample %d)\n", nc, mn,
-                    mean / nc, r, kLrSample);
-        }
-        if (r > kLrMaxRank) return false;
+        // the ranks are checked once the basis and the projections are queued
+        // (the basis width is fixed, kLrMaxRank): the host waits on this event
+        // while the GPU still has that work ahead of it, instead of draining
+        // the stream here
+        c.lr_rank_h.ensure(nc);
+        QPS_D2H(c.lr_rank_h.p, cs.rank.p, sizeof(int) * nc, s);
+        QPS_CUDA(cudaEventRecord(c.ev_sample, s));
+        rank_deferred = true;
         r = kLrMaxRank;
         c.lr_r = r;
         // Q2 = first r columns of the R-CPQR's Q (64 x r)
@@ -836,6 +834,19 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     if (trace) {
         QPS_CUDA(cudaEventDestroy(te0));
         QPS_CUDA(cudaEventDestroy(te1));
+    }
+    if (rank_deferred) {
+        QPS_CUDA(cudaEventSynchronize(c.ev_sample));
+        int mx = 0;
+        for (int q = 0; q < nc; ++q) mx = std::max(mx, c.lr_rank_h[q]);
+        if (getenv("QPS_LR_TRACE")) {
+            int mn = 1 << 30;
+            double mean = 0;
+            for (int q = 0; q < nc; ++q) { mn = std::min(mn, c.lr_rank_h[q]); mean += c.lr_rank_h[q]; }
+            fprintf(stderr, "low-rank couplings: %d blocks, rank min %d mean %.1f max %d (sample %d)\n", nc, mn,
+                    mean / nc, mx, kLrSample);
+        }
+        if (mx > kLrMaxRank) return false;  // not low rank: the dense reduction (A untouched so far)
     }
     return true;
 }
@@ -1184,7 +1195,12 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * (r2 + 1); };
     auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
     auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2; };
+    std::vector<int> l0_orig;  // level-0 positions whose singular flags are checked at the end
     // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
+    cudaEvent_t f0 = nullptr, f1 = nullptr;  // factor_ms of the phase times
+    QPS_CUDA(cudaEventCreate(&f0));
+    QPS_CUDA(cudaEventCreate(&f1));
+    QPS_CUDA(cudaEventRecord(f0, s));
     {
         Level L0(ns);
         const size_t per = size_t(nb) * r;
@@ -1233,9 +1249,13 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             // the D_j^0 factors are used only for W_j: the forward substitution
             // rides along the factorization
             lu_factor_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, flag.p, s, c.ws);
-            check(orig);
+            // singular flags read back asynchronously, checked after the levels
+            c.bcr_flag_h.ensure(fa.size());
+            QPS_D2H(c.bcr_flag_h.p, flag.p, sizeof(int) * fa.size(), s);
+            l0_orig = orig;
             tmark("factor+solve", 0, int(fa.size()));
         }
+        QPS_CUDA(cudaEventRecord(f1, s));
         // y = D^{-1} f back into F (column 2r of every W_j)
         QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * nb, c.lr_W0.p + size_t(r2) * nb,
                                    sizeof(cplx) * nb * (r2 + 1), sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
@@ -1407,6 +1427,24 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         for (int a = 0; a < ns; ++a) fin.push_back(&levels[lvl][a][0]);
         eliminate(fin, lvl);
         tmark("final", lvl, int(fin.size()));
+    }
+    {
+        float fms = 0;
+        QPS_CUDA(cudaEventSynchronize(f1));
+        int worst = -1;
+        for (size_t q = 0; q < l0_orig.size(); ++q)
+            if (c.bcr_flag_h[q] && (worst < 0 || l0_orig[q] < worst)) worst = l0_orig[q];
+        if (worst >= 0) {
+            QPS_CUDA(cudaEventDestroy(f0));
+            QPS_CUDA(cudaEventDestroy(f1));
+            throw Error(QPS_ERR_SOLVER,
+                        "singular diagonal factor (resonant parameters?) at layer " + std::to_string(worst + 1),
+                        worst + 1);
+        }
+        QPS_CUDA(cudaEventElapsedTime(&fms, f0, f1));
+        c.times.factor_ms = fms;
+        QPS_CUDA(cudaEventDestroy(f0));
+        QPS_CUDA(cudaEventDestroy(f1));
     }
     if (!cap_orig.empty()) {
         flag.ensure(cap_orig.size());

@@ -375,6 +375,7 @@ int qps_solve(qps_ctx* h) {
             }
         } total{c, t0, t1};
         c.ps_separate = false;
+        c.times.factor_ms = 0.0;
         run_fill(c);
         c.times.assemble_ms = 0.0;
         lr_sample_async(c);  // overlaps the Schur least squares

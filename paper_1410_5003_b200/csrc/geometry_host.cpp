@@ -16,6 +16,9 @@
 #include <exception>
 #include <limits>
 #include <thread>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "qps_internal.h"
 
@@ -249,6 +252,8 @@ HostGeometry build_geometry(const StackDesc& st, const Numerics& num) {
     g.Mw = num.Mw;
     g.M = num.M;
     g.R = num.R;
+    static const bool htrace = getenv("QPS_HOST_TRACE") != nullptr;
+    const auto tg0 = std::chrono::steady_clock::now();
     // interfaces are independent: built on host threads, each with its own
     // Fourier coefficient pool (concatenated afterwards in interface order);
     // the first failing interface (in order) raises, as the sequential reference
@@ -279,6 +284,9 @@ HostGeometry build_geometry(const StackDesc& st, const Numerics& num) {
             g.ifaces.push_back(std::move(ifs[j]));
         }
     }
+    const auto tg1 = std::chrono::steady_clock::now();
+    if (htrace)
+        fprintf(stderr, "build_geometry: interfaces %.3f ms\n", std::chrono::duration<double, std::milli>(tg1 - tg0).count());
     // build_frame (:449-478)
     g.y_U = g.ifaces.front().y_max + num.clearance * st.d;
     g.y_D = g.ifaces.back().y_min - num.clearance * st.d;

@@ -1742,8 +1742,23 @@ __global__ void __launch_bounds__(256) lu_rl_cols_kernel(int n, int ld, cplx* co
 __global__ void maxabs_kernel(const cplx* X, int m, int n, int ld, size_t stride, double* out) {
     const cplx* A = X + stride * blockIdx.x;
     double v = 0.0;
-    for (int j = 0; j < n; ++j)
-        for (int i = threadIdx.x; i < m; i += blockDim.x) v = fmax(v, sqrt(cabs2(A[size_t(j) * ld + i])));
+    if (ld == m) {  // contiguous: one linear sweep, four loads in flight per thread
+        const size_t tot = size_t(m) * n;
+        double v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        size_t e = threadIdx.x;
+        const size_t st = blockDim.x;
+        for (; e + 3 * st < tot; e += 4 * st) {
+            v = fmax(v, cabs2(A[e]));
+            v1 = fmax(v1, cabs2(A[e + st]));
+            v2 = fmax(v2, cabs2(A[e + 2 * st]));
+            v3 = fmax(v3, cabs2(A[e + 3 * st]));
+        }
+        for (; e < tot; e += st) v = fmax(v, cabs2(A[e]));
+        v = sqrt(fmax(fmax(v, v1), fmax(v2, v3)));
+    } else {
+        for (int j = 0; j < n; ++j)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) v = fmax(v, sqrt(cabs2(A[size_t(j) * ld + i])));
+    }
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     __shared__ double sh[32];
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
@@ -1762,12 +1777,32 @@ __global__ void fro_kernel(const cplx* X, int m, int n, int ld, size_t stride, d
     const cplx* A = X + stride * blockIdx.x;
     __shared__ double sh[32];
     double mx = 0.0, s = 0.0;
-    for (int j = 0; j < n; ++j)
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
-            const double a2 = cabs2(A[size_t(j) * ld + i]);
+    if (ld == m) {  // contiguous: one linear sweep, two loads in flight per thread
+        const size_t tot = size_t(m) * n, st = blockDim.x;
+        double s1 = 0.0, mx1 = 0.0;
+        size_t e = threadIdx.x;
+        for (; e + st < tot; e += 2 * st) {
+            const double a2 = cabs2(A[e]), b2 = cabs2(A[e + st]);
+            s += a2;
+            s1 += b2;
+            mx = fmax(mx, a2);
+            mx1 = fmax(mx1, b2);
+        }
+        for (; e < tot; e += st) {
+            const double a2 = cabs2(A[e]);
             s += a2;
             mx = fmax(mx, a2);
         }
+        s += s1;
+        mx = fmax(mx, mx1);
+    } else {
+        for (int j = 0; j < n; ++j)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const double a2 = cabs2(A[size_t(j) * ld + i]);
+                s += a2;
+                mx = fmax(mx, a2);
+            }
+    }
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
     __syncthreads();

@@ -90,10 +90,12 @@ class _Cplx(C.Structure):
 
 
 class _Spec(C.Structure):
+    # qps_interface_spec; the array members are plain addresses (c_void_p has the
+    # pointer ABI) so that the per-interface marshalling is integer arithmetic
     _fields_ = [("shape", C.c_int), ("offset", C.c_double), ("amplitude", C.c_double), ("phase", C.c_double),
-                ("n_cos", C.c_int), ("cosc", C.POINTER(C.c_double)), ("n_sin", C.c_int),
-                ("sinc", C.POINTER(C.c_double)), ("n_vertices", C.c_int), ("vertices", C.POINTER(C.c_double)),
-                ("n_nodes", C.c_int), ("nodes", C.POINTER(C.c_int)), ("grading_q", C.c_int)]
+                ("n_cos", C.c_int), ("cosc", C.c_void_p), ("n_sin", C.c_int),
+                ("sinc", C.c_void_p), ("n_vertices", C.c_int), ("vertices", C.c_void_p),
+                ("n_nodes", C.c_int), ("nodes", C.c_void_p), ("grading_q", C.c_int)]
 
 
 class _Num(C.Structure):
@@ -103,7 +105,8 @@ class _Num(C.Structure):
 
 class _Times(C.Structure):
     _fields_ = [("fill_ms", C.c_double), ("assemble_ms", C.c_double), ("schur_ms", C.c_double),
-                ("solve_ms", C.c_double), ("recover_ms", C.c_double), ("total_ms", C.c_double)]
+                ("solve_ms", C.c_double), ("recover_ms", C.c_double), ("total_ms", C.c_double),
+                ("factor_ms", C.c_double)]
 
 
 @dataclasses.dataclass
@@ -277,19 +280,25 @@ class Solver:
     # ------------------------------------------------------------ geometry
     def build_geometry(self, stack: LayerStack, num: NumericsParams):
         specs = (_Spec * len(stack.interfaces))()
-        keep = []
-        for s, sp in zip(specs, stack.interfaces):
-            cos = np.ascontiguousarray(sp.cosc, dtype=np.float64)
-            sin = np.ascontiguousarray(sp.sinc, dtype=np.float64)
-            ver = np.ascontiguousarray(np.array(sp.vertices, dtype=np.float64).reshape(-1))
-            nod = np.ascontiguousarray(sp.nodes, dtype=np.int32)
-            keep += [cos, sin, ver, nod]
+        # every interface's arrays packed into one double and one int buffer
+        dbl, ints, layout = [], [], []
+        for sp in stack.interfaces:
+            cos, sin = list(sp.cosc), list(sp.sinc)
+            ver = [float(v) for xy in sp.vertices for v in (xy if hasattr(xy, "__len__") else (xy,))]
+            nod = list(sp.nodes)
+            layout.append((len(dbl), len(cos), len(sin), len(ver), len(ints), len(nod)))
+            dbl += cos + sin + ver
+            ints += nod
+        dbuf = np.array(dbl + [0.0], dtype=np.float64)
+        ibuf = np.array(ints + [0], dtype=np.int32)
+        da, ia = dbuf.ctypes.data, ibuf.ctypes.data
+        for s, sp, (d0, nc, ns_, nv, i0, nn) in zip(specs, stack.interfaces, layout):
             s.shape = SHAPES[sp.shape]
             s.offset, s.amplitude, s.phase = sp.offset, sp.amplitude, sp.phase
-            s.n_cos, s.cosc = len(cos), _dptr(cos)
-            s.n_sin, s.sinc = len(sin), _dptr(sin)
-            s.n_vertices, s.vertices = len(ver) // 2, _dptr(ver)
-            s.n_nodes, s.nodes = len(nod), nod.ctypes.data_as(C.POINTER(C.c_int))
+            s.n_cos, s.cosc = nc, da + 8 * d0
+            s.n_sin, s.sinc = ns_, da + 8 * (d0 + nc)
+            s.n_vertices, s.vertices = nv // 2, da + 8 * (d0 + nc + ns_)
+            s.n_nodes, s.nodes = nn, ia + 4 * i0
             s.grading_q = sp.grading_q
         eps = np.array([m.epsilon for m in stack.materials], dtype=np.float64)
         mu = np.array([m.mu for m in stack.materials], dtype=np.float64)
