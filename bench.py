@@ -291,8 +291,11 @@ def main():
                 "fill_frac_of_dfma_peak": (200.0 * fill_units / (fill_ms * 1e-3) / 1e12) / peaks["dfma_tflops"]
                 if fill_ms else None,
                 "fill_fp64_frac_ncu": fill_ncu.get("fp64_frac_of_peak"),
+                "fill_nominal_frac_ncu": fill_ncu.get("nominal_frac_of_peak"),
                 "fill_fp64_ncu_note": fill_ncu.get("note"),
-                "bcr_factor": bcr_factor(phases, I, 2 * N, peak),
+                "bcr_factor": dict(bcr_factor(phases, I, 2 * N, peak) or {},
+                                   ncu={k: v for k, v in ncu_summary().get("bcr_level0", {}).items()
+                                        if k not in ("command",)}),
                 "gemm_tflops_issued": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "gemm_tflops_complex_equiv": gemm_fl * 8.0 / 6.0 / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "fp64_peaks_tflops": peaks, "flux_error": rt["flux_error"], "R": rt["R"], "T": rt["T"],

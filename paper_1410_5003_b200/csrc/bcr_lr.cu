@@ -29,6 +29,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cmath.cuh"
 #include "ctx.h"
 #include "prof.h"
@@ -1201,6 +1203,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     QPS_CUDA(cudaEventCreate(&f0));
     QPS_CUDA(cudaEventCreate(&f1));
     QPS_CUDA(cudaEventRecord(f0, s));
+    nvtxRangePushA("bcr_level0");  // ncu --nvtx --nvtx-include "bcr_level0/" selects this batch
     {
         Level L0(ns);
         const size_t per = size_t(nb) * r;
@@ -1256,6 +1259,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             tmark("factor+solve", 0, int(fa.size()));
         }
         QPS_CUDA(cudaEventRecord(f1, s));
+        nvtxRangePop();
         // y = D^{-1} f back into F (column 2r of every W_j)
         QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * nb, c.lr_W0.p + size_t(r2) * nb,
                                    sizeof(cplx) * nb * (r2 + 1), sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
