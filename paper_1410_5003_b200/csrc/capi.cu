@@ -400,7 +400,7 @@ int qps_get_solution(const qps_ctx* h, qps_cplx* eta, qps_cplx* cc, qps_cplx* aU
                      double* max_lsq) {
     return guarded(const_cast<qps_ctx*>(h), [&](Ctx& c) {
         need(c.have_sol, "no solution");
-        if (eta) std::memcpy(eta, c.h_eta.data(), sizeof(cplx) * c.h_eta.size());
+        if (eta) std::memcpy(eta, c.h_eta.p, sizeof(cplx) * c.h_eta_n);
         if (cc) std::memcpy(cc, c.h_c.data(), sizeof(cplx) * c.h_c.size());
         if (aU) std::memcpy(aU, c.h_aU.data(), sizeof(cplx) * c.h_aU.size());
         if (aD) std::memcpy(aD, c.h_aD.data(), sizeof(cplx) * c.h_aD.size());

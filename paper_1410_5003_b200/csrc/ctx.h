@@ -192,7 +192,9 @@ struct Ctx {
 
     // ---- solution ----
     DBuf<cplx> csol, aUd, aDd;
-    std::vector<cplx> h_eta, h_c, h_aU, h_aD;        // system 0
+    HBuf<cplx> h_eta;                                // system 0 densities (pinned: one DMA, no repack)
+    size_t h_eta_n = 0;
+    std::vector<cplx> h_c, h_aU, h_aD;               // system 0
     std::vector<cplx> h_aU_all, h_aD_all;            // nsys x (2K+1)
     std::vector<double> lsq_all;                     // nsys x (I+1)
     bool have_sol = false;

@@ -1340,12 +1340,18 @@ __global__ void __launch_bounds__(512) tri_inv_kernel(int n, int ld, cplx* const
 // scratch); row_permute_kernel then permutes columns with one warp per column
 // (coalesced reads/writes through a shared-memory staging column).
 constexpr int kPermWarps = 8;
+// Per matrix the scratch holds [perm (n) | moved rows (n) | count]: only the
+// rows the interchanges move are gathered and written back (at most
+// 2 (kend - k0) of the n - k0), e.g. 32 of ~600 rows for a 16-column leaf.
 __global__ void perm_build_kernel(int n, const int* const* __restrict__ Pp, int* __restrict__ perm_out, int k0,
                                   int kend) {
     const int* ipiv = Pp[blockIdx.x];
-    int* perm = perm_out + size_t(blockIdx.x) * n;
+    int* perm = perm_out + size_t(blockIdx.x) * (2 * n + 1);
+    int* moved = perm + n;
+    __shared__ int cnt;
     const int rows = n - k0;
     for (int i = threadIdx.x; i < rows; i += blockDim.x) perm[i] = k0 + i;
+    if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
     if (threadIdx.x == 0)
         for (int k = k0; k < kend; ++k) {
@@ -1356,21 +1362,26 @@ __global__ void perm_build_kernel(int n, const int* const* __restrict__ Pp, int*
                 perm[p - k0] = t;
             }
         }
+    __syncthreads();
+    for (int i = threadIdx.x; i < rows; i += blockDim.x)
+        if (perm[i] != k0 + i) moved[atomicAdd(&cnt, 1)] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) perm[2 * n] = cnt;
 }
-
 __global__ void __launch_bounds__(256) row_permute_kernel(int n, int ld, cplx* const* __restrict__ Ap,
                                                           const int* __restrict__ perm_all, int k0, int c0, int c1) {
     extern __shared__ cplx tmp_smem[];
     cplx* A = Ap[blockIdx.y];
-    const int* perm = perm_all + size_t(blockIdx.y) * n;
-    const int rows = n - k0;
+    const int* perm = perm_all + size_t(blockIdx.y) * (2 * n + 1);
+    const int* moved = perm + n;
+    const int cnt = perm[2 * n];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    cplx* tw = tmp_smem + size_t(warp) * rows;
+    cplx* tw = tmp_smem + size_t(warp) * (n - k0);
     for (int c = c0 + blockIdx.x * kPermWarps + warp; c < c1; c += gridDim.x * kPermWarps) {
         cplx* col = A + size_t(c) * ld;
-        for (int i = lane; i < rows; i += 32) tw[i] = col[perm[i]];
+        for (int t = lane; t < cnt; t += 32) tw[t] = col[perm[moved[t]]];
         __syncwarp();
-        for (int i = lane; i < rows; i += 32) col[k0 + i] = tw[i];
+        for (int t = lane; t < cnt; t += 32) col[k0 + moved[t]] = tw[t];
         __syncwarp();
     }
 }
@@ -2158,7 +2169,7 @@ void launch_panel_fast(int n, int ld, cplx* const* dA, int* const* dP, int c0, i
 void launch_row_permute(int n, int ld, cplx* const* dA, const int* const* dP, int count, int k0, int kend, int c0,
                         int c1, cudaStream_t s, DBuf<int>& perm) {
     if (c1 <= c0) return;
-    perm.ensure(size_t(count) * n);
+    perm.ensure(size_t(count) * (2 * n + 1));
     perm_build_kernel<<<count, 128, 0, s>>>(n, dP, perm.p, k0, kend);
     QPS_CUDA(cudaGetLastError());
     const size_t sh = size_t(kPermWarps) * (n - k0) * sizeof(cplx);

@@ -1061,15 +1061,32 @@ void recover(Ctx& c) {
     }
     zgemv_batched(P, cplx{-1, 0}, cplx{0, 0}, it, s, c.ws.gemv_tasks);
     // download: full solution of system 0, Bragg amplitudes of every system
-    std::vector<cplx> Fh(size_t(I) * nb), ch(size_t(I + 1) * P), xf(size_t(ns) * D.pC), xl(size_t(ns) * D.pC);
-    QPS_D2H(Fh.data(), c.F.p, sizeof(cplx) * Fh.size(), s);
+    std::vector<cplx> ch(size_t(I + 1) * P), xf(size_t(ns) * D.pC), xl(size_t(ns) * D.pC);
+    // eta of system 0 straight into pinned memory, the padding rows dropped by the DMA
+    size_t neta = 0;
+    bool uniform = true;
+    for (int j = 0; j < I; ++j) {
+        neta += 2 * size_t(D.N[j]);
+        uniform &= D.N[j] == D.N[0];
+    }
+    c.h_eta.ensure(neta);
+    c.h_eta_n = neta;
+    if (uniform) {
+        const size_t w = sizeof(cplx) * 2 * D.N[0];
+        QPS_CUDA(cudaMemcpy2DAsync(c.h_eta.p, w, c.F.p, sizeof(cplx) * nb, w, I, cudaMemcpyDeviceToHost, s));
+    } else {
+        size_t o = 0;
+        for (int j = 0; j < I; ++j) {
+            QPS_CUDA(cudaMemcpyAsync(c.h_eta.p + o, c.F.p + size_t(j) * nb, sizeof(cplx) * 2 * D.N[j],
+                                     cudaMemcpyDeviceToHost, s));
+            o += 2 * size_t(D.N[j]);
+        }
+    }
+    g_d2h_bytes += sizeof(cplx) * neta;
     QPS_D2H(ch.data(), c.csol.p, sizeof(cplx) * ch.size(), s);
     QPS_D2H(xf.data(), c.aUd.p, sizeof(cplx) * xf.size(), s);
     QPS_D2H(xl.data(), c.aDd.p, sizeof(cplx) * xl.size(), s);
     QPS_CUDA(cudaStreamSynchronize(s));
-    c.h_eta.clear();
-    for (int j = 0; j < I; ++j)
-        for (int i = 0; i < 2 * D.N[j]; ++i) c.h_eta.push_back(Fh[size_t(j) * nb + i]);
     for (int p = 0; p < P; ++p) {
         ch[p] = xf[p];
         ch[size_t(I) * P + p] = xl[p];
