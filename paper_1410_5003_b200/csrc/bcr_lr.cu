@@ -407,61 +407,66 @@ __global__ void __launch_bounds__(512) gj_inverse_kernel(int n, cplx* __restrict
 // after which A^{-1}[k][p_k'] = T[p_k][k'] (rows and columns permuted on the
 // way out).  Two barriers per step; the pivot's reciprocal is computed once.
 // N (a multiple of 4) fixed at compile time: every guard folds away and the
-// row loops are straight-line selects (96 x 96 capacitance matrices, 2r = 96).
+// row loops are straight-line (96 x 96 capacitance matrices, 2r = 96).
+// Thread layout tid = g N + j: a warp holds one row class g (rows g, g + 4,
+// ...) of 32 columns, so "owns the pivot row" is warp-uniform and the s_col
+// reads are warp-wide broadcasts; the pivot search reduces the column's four
+// row classes through shared memory and every thread then computes the pivot's
+// reciprocal itself (one barrier saved).
 template <int N>
 __global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict__ C, int* __restrict__ flag) {
     constexpr int NR = N / 4;
-    static_assert(N % 4 == 0 && NR <= 32, "gj_inverse_reg_kernel: N = 4 NR, NR <= 32");
-    __shared__ cplx s_row[N], s_col[N];
+    static_assert(N % 32 == 0 && NR <= 32, "gj_inverse_reg_kernel: N a multiple of 32, N <= 128");
+    __shared__ cplx s_row[N], s_col[2][N];  // s_col double-buffered: written before the first barrier
     __shared__ int s_perm[N], s_pinv[N];
-    __shared__ int s_p;
-    __shared__ cplx s_inv;
+    __shared__ double s_cv[2][4];
+    __shared__ int s_ci[2][4];
+    __shared__ cplx s_ca[2][4];
     cplx* Cb = C + size_t(blockIdx.x) * N * N;
-    const int tid = threadIdx.x, j = tid >> 2, g = tid & 3;
+    const int tid = threadIdx.x, g = tid / N, j = tid % N;
     cplx T[NR];
     unsigned used = 0;  // bit ii: row g + 4 ii already pivotal
 #pragma unroll
     for (int ii = 0; ii < NR; ++ii) T[ii] = Cb[size_t(j) * N + g + 4 * ii];
     for (int k = 0; k < N; ++k) {
-        if ((k >> 3) == (tid >> 5)) {  // the warp holding column k: pivot search
+        const int par = k & 1;
+        const bool colk = (j == k);
+        if (colk) {  // this row class's candidate in column k
             double v = -1.0;
             int idx = 1 << 30;
-            if (j == k) {
+            cplx a{0, 0};
 #pragma unroll
-                for (int ii = 0; ii < NR; ++ii) {
-                    const double m = cabs2(T[ii]);
-                    const bool better = !((used >> ii) & 1u) && m > v;
-                    v = better ? m : v;
-                    idx = better ? g + 4 * ii : idx;
-                }
+            for (int ii = 0; ii < NR; ++ii) {
+                const double m = cabs2(T[ii]);
+                const bool better = !((used >> ii) & 1u) && m > v;
+                v = better ? m : v;
+                idx = better ? g + 4 * ii : idx;
+                a.re = better ? T[ii].re : a.re;
+                a.im = better ? T[ii].im : a.im;
             }
+            s_cv[par][g] = v;
+            s_ci[par][g] = idx;
+            s_ca[par][g] = a;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-                const bool better = ov > v || (ov == v && oi < idx);
-                v = better ? ov : v;
-                idx = better ? oi : idx;
-            }
-            if (j == k && g == (idx & 3)) {  // owner of the pivot element
-                cplx a{0, 0};
-#pragma unroll
-                for (int ii = 0; ii < NR; ++ii) {
-                    const bool hit = (g + 4 * ii == idx);
-                    a.re = hit ? T[ii].re : a.re;
-                    a.im = hit ? T[ii].im : a.im;
-                }
-                const bool zero = !(v > 0.0);
-                if (zero) flag[blockIdx.x] = 1;
-                s_inv = zero ? cplx{0, 0} : fast_cinv(a);
-                s_p = idx;
-                s_perm[k] = idx;
-                s_pinv[idx] = k;
-            }
+            for (int ii = 0; ii < NR; ++ii) s_col[par][g + 4 * ii] = T[ii];
         }
         __syncthreads();
-        const int p = s_p, pr = p >> 2;
-        const bool own_p = g == (p & 3);
+        double bv = s_cv[par][0];
+        int p = s_ci[par][0], bg = 0;
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+            const double v = s_cv[par][q];
+            const int i = s_ci[par][q];
+            const bool better = v > bv || (v == bv && i < p);
+            bv = better ? v : bv;
+            p = better ? i : p;
+            bg = better ? q : bg;
+        }
+        const cplx a = s_ca[par][bg];
+        const bool zero = !(bv > 0.0);
+        const cplx inv = zero ? cplx{0, 0} : fast_cinv(a);
+        const int pr = p >> 2;
+        const bool own_p = g == (p & 3);  // warp-uniform
         if (own_p) {
             cplx rv{0, 0};
 #pragma unroll
@@ -471,26 +476,39 @@ __global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict_
             }
             s_row[j] = rv;
         }
-        if (j == k) {
-#pragma unroll
-            for (int ii = 0; ii < NR; ++ii) s_col[g + 4 * ii] = T[ii];
+        if (tid == 0) {
+            if (zero) flag[blockIdx.x] = 1;
+            s_perm[k] = p;
+            s_pinv[p] = k;
         }
         __syncthreads();
-        const cplx inv = s_inv;
-        const bool colk = (j == k);
-        const cplx sr = s_row[j];
-        cplx r = cmul(sr, inv);
-        r.re = colk ? -inv.re : r.re;
-        r.im = colk ? -inv.im : r.im;
+        if (colk) {  // T[i][k] = T[i][k] / a, T[p][k] = 1 / a
 #pragma unroll
-        for (int ii = 0; ii < NR; ++ii) {
-            const cplx c = s_col[g + 4 * ii];
-            double bre = colk ? 0.0 : T[ii].re, bim = colk ? 0.0 : T[ii].im;
-            bre -= c.re * r.re - c.im * r.im;
-            bim -= c.re * r.im + c.im * r.re;
-            const bool piv = own_p && ii == pr;
-            T[ii].re = piv ? -r.re : bre;
-            T[ii].im = piv ? -r.im : bim;
+            for (int ii = 0; ii < NR; ++ii) {
+                const cplx c = s_col[par][g + 4 * ii];
+                const bool piv = own_p && ii == pr;
+                T[ii].re = piv ? inv.re : c.re * inv.re - c.im * inv.im;
+                T[ii].im = piv ? inv.im : c.re * inv.im + c.im * inv.re;
+            }
+        } else {
+            const cplx r = cmul(s_row[j], inv);
+            if (own_p) {
+#pragma unroll
+                for (int ii = 0; ii < NR; ++ii) {
+                    const cplx c = s_col[par][g + 4 * ii];
+                    const double bre = T[ii].re - (c.re * r.re - c.im * r.im);
+                    const double bim = T[ii].im - (c.re * r.im + c.im * r.re);
+                    T[ii].re = (ii == pr) ? -r.re : bre;
+                    T[ii].im = (ii == pr) ? -r.im : bim;
+                }
+            } else {
+#pragma unroll
+                for (int ii = 0; ii < NR; ++ii) {
+                    const cplx c = s_col[par][g + 4 * ii];
+                    T[ii].re -= c.re * r.re - c.im * r.im;
+                    T[ii].im -= c.re * r.im + c.im * r.re;
+                }
+            }
         }
         used |= own_p ? (1u << pr) : 0u;
     }
