@@ -1,6 +1,7 @@
 // C-ABI of the B200 implementation (include/qpscat_b200.h).  Every entry point
 // converts exceptions into qps_status codes following the reference's error
 // taxonomy (errors.hpp:9-40) and never falls back to a CPU path.
+#include <chrono>
 #include <cstring>
 
 #include "ctx.h"
@@ -151,7 +152,7 @@ void qps_destroy(qps_ctx* h) {
     cudaStream_t s = h->c.stream, s2 = h->c.side, s3 = h->c.side2;
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
-    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample})
+    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_geo})
         if (e) cudaEventDestroy(e);
     delete h;
     if (s) cudaStreamDestroy(s);
@@ -201,8 +202,16 @@ int qps_build_geometry(qps_ctx* h, double d, int n_layers, const double* eps, co
         nm.memory_budget = num->memory_budget;
         c.stack = std::move(st);
         c.num = nm;
+        static const bool htrace = getenv("QPS_HOST_TRACE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         c.geo = build_geometry(c.stack, c.num);
+        const auto t1 = std::chrono::steady_clock::now();
         if (!c.host_only) upload_geometry(c);
+        const auto t2 = std::chrono::steady_clock::now();
+        if (htrace)
+            fprintf(stderr, "qps_build_geometry: build %.3f ms, upload %.3f ms\n",
+                    std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                    std::chrono::duration<double, std::milli>(t2 - t1).count());
         c.have_geom = true;
     });
 }

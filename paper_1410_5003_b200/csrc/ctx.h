@@ -168,6 +168,9 @@ struct Ctx {
     DBuf<cplx> lr_omega, lr_Y, lr_P, lr_PH, lr_R, lr_core, lr_T, lr_vec, lr_W, lr_G;
     DBuf<cplx> lr_V, lr_VH, lr_Tq, lr_THq, lr_W1, lr_W2, lr_R64, lr_Q2, lr_Q2H;  // blocked QR of the samples
     int lr_omega_n = 0, lr_r = 0;
+    HBuf<double> geo_h;                // pinned staging of the geometry pool (upload_geometry)
+    bool geo_h_ev_pending = false;
+    cudaEvent_t ev_geo = nullptr;
     HBuf<int> lr_rank_h;               // sample ranks, read back without a stream sync
     HBuf<int> bcr_flag_h;              // singular-factor flags of the level-0 batch (checked at the end)
     // coupling Schur updates A'_{j,j+1} = A - B X left to the compression

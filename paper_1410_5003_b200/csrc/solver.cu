@@ -66,35 +66,58 @@ cd vertical_wavenumber(double kl, double kap) {
 void upload_geometry(Ctx& c) {
     const HostGeometry& g = c.geo;
     const int I = g.I;
-    std::vector<double> x, y, nx, ny, w;
+    static const bool htrace = getenv("QPS_HOST_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    size_t total = size_t(g.ud_x.size()) * 2;
+    for (int j = 0; j < I; ++j) total += g.ifaces[j].N();
+    for (int i = 0; i <= I; ++i) total += g.wall_ys[i].size() + g.P;
+    // packed straight into a persistent pinned buffer (fresh host vectors cost
+    // ~7 ms of first-touch page faults at config 4) and copied asynchronously
+    if (c.geo_h_ev_pending) QPS_CUDA(cudaEventSynchronize(c.ev_geo));  // previous upload done with geo_h
+    c.geo_h.ensure(5 * total);
+    double *x = c.geo_h.p, *y = x + total, *nx = y + total, *ny = nx + total, *w = ny + total;
+    size_t n = 0;
     auto add = [&](double xx, double yy, double nxx, double nyy, double ww) {
-        x.push_back(xx); y.push_back(yy); nx.push_back(nxx); ny.push_back(nyy); w.push_back(ww);
+        x[n] = xx; y[n] = yy; nx[n] = nxx; ny[n] = nyy; w[n] = ww;
+        ++n;
     };
     c.iface_off.assign(I, 0);
     for (int j = 0; j < I; ++j) {
-        c.iface_off[j] = int(x.size());
+        c.iface_off[j] = int(n);
         const auto& q = g.ifaces[j];
         for (int i = 0; i < q.N(); ++i) add(q.x[i], q.y[i], q.nx[i], q.ny[i], q.w[i]);
     }
     c.wall_off.assign(I + 1, 0);
     for (int i = 0; i <= I; ++i) {
-        c.wall_off[i] = int(x.size());
+        c.wall_off[i] = int(n);
         for (double yy : g.wall_ys[i]) add(-0.5 * g.d, yy, 1.0, 0.0, 0.0);  // wall_targets, assembly.hpp:159-168
     }
-    c.U_off = int(x.size());
+    c.U_off = int(n);
     for (double xx : g.ud_x) add(xx, g.y_U, 0.0, 1.0, 0.0);  // line_targets, assembly.hpp:170-177
-    c.D_off = int(x.size());
+    c.D_off = int(n);
     for (double xx : g.ud_x) add(xx, g.y_D, 0.0, 1.0, 0.0);
     c.proxy_off.assign(I + 1, 0);
     for (int i = 0; i <= I; ++i) {
-        c.proxy_off[i] = int(x.size());
+        c.proxy_off[i] = int(n);
         for (int p = 0; p < g.P; ++p) add(g.px[i][p], g.py[i][p], g.pnx[i][p], g.pny[i][p], 0.0);
     }
-    c.px.upload(x, c.stream);
-    c.py.upload(y, c.stream);
-    c.pnx.upload(nx, c.stream);
-    c.pny.upload(ny, c.stream);
-    c.pw.upload(w, c.stream);
+    const auto t1 = std::chrono::steady_clock::now();
+    DBuf<double>* dst[5] = {&c.px, &c.py, &c.pnx, &c.pny, &c.pw};
+    for (int a = 0; a < 5; ++a) {
+        dst[a]->ensure(n);
+        QPS_CUDA(cudaMemcpyAsync(dst[a]->p, c.geo_h.p + size_t(a) * total, sizeof(double) * n,
+                                 cudaMemcpyHostToDevice, c.stream));
+    }
+    g_h2d_bytes += 5 * sizeof(double) * n;
+    // the pinned buffer is rewritten by the next upload: complete this one first
+    if (!c.ev_geo) QPS_CUDA(cudaEventCreateWithFlags(&c.ev_geo, cudaEventDisableTiming));
+    QPS_CUDA(cudaEventRecord(c.ev_geo, c.stream));
+    c.geo_h_ev_pending = true;
+    const auto t2 = std::chrono::steady_clock::now();
+    if (htrace)
+        fprintf(stderr, "upload_geometry: pack %.3f ms, upload %.3f ms (%zu points)\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count(), n);
     std::vector<SegDesc> segs;
     c.seg_first.assign(I, 0);
     for (int j = 0; j < I; ++j) {
