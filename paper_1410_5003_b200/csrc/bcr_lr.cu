@@ -595,7 +595,9 @@ void lr_sample_async(Ctx& c) {
     }
     {
         ProfPhase phase("lowrank");
-        zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, c.side2, c.lr_tasks, "lr_compress");
+        // own family: its events on the low-priority stream span its overlap
+        // with the Schur chain, so the duration is not a kernel time
+        zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, c.side2, c.lr_tasks, "lr_sample");
     }
     QPS_CUDA(cudaEventRecord(c.ev_sample, c.side2));
     c.lr_sample_pending = true;
@@ -716,9 +718,9 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             {
                 ProfScope ps("lr_qr", s, 0.0);
                 // per-problem pointers are strided: V_of(q, pn) = base + (q nP + pn) vs
-                qr_panel_kernel<<<nc, ((m + 31) / 32) * 32, size_t(m) * kQrW * sizeof(cplx), s>>>(
+                { QPS_NOTE_LAUNCH(); qr_panel_kernel<<<nc, ((m + 31) / 32) * 32, size_t(m) * kQrW * sizeof(cplx), s>>>(
                     m, c.lr_Y.p, ys, col0, c.lr_V.p + pn * vs, c.lr_VH.p + pn * vs, c.lr_Tq.p + pn * ts,
-                    c.lr_THq.p + pn * ts, size_t(nP) * vs, size_t(nP) * ts);
+                    c.lr_THq.p + pn * ts, size_t(nP) * vs, size_t(nP) * ts); }
                 QPS_CUDA(cudaGetLastError());
             }
             const int rest = p - col0 - kQrW;
@@ -738,7 +740,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         tmark("blocked QR of the samples");
         // CPQR of R (64 x 64): rank and the ordered basis Q2
         c.lr_R64.ensure(size_t(nc) * p * p);
-        qr_take_r_kernel<<<nc, 256, 0, s>>>(m, p, c.lr_Y.p, ys, c.lr_R64.p);
+        { QPS_NOTE_LAUNCH(); qr_take_r_kernel<<<nc, 256, 0, s>>>(m, p, c.lr_Y.p, ys, c.lr_R64.p); }
         QPS_CUDA(cudaGetLastError());
         CodSet& cs = c.lr_cod;
         cs.ensure(nc, p, p, 1);
@@ -758,13 +760,13 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         // Q2 = first r columns of the R-CPQR's Q (64 x r)
         c.lr_Q2.ensure(size_t(nc) * p * r);
         c.lr_Q2H.ensure(size_t(nc) * p * r);
-        lr_form_q_kernel<<<dim3(nc, (r + 7) / 8), 256, size_t(8) * p * sizeof(cplx), s>>>(
-            p, p, r, cs.W.p, cs.tau.p, c.lr_Q2.p, p, size_t(p) * r, c.lr_Q2H.p, size_t(r) * p);
+        { QPS_NOTE_LAUNCH(); lr_form_q_kernel<<<dim3(nc, (r + 7) / 8), 256, size_t(8) * p * sizeof(cplx), s>>>(
+            p, p, r, cs.W.p, cs.tau.p, c.lr_Q2.p, p, size_t(p) * r, c.lr_Q2H.p, size_t(r) * p); }
         QPS_CUDA(cudaGetLastError());
         // P = Q [Q2; 0], Q = (I - V0 T0 V0^*) ... (I - V3 T3 V3^*)
         c.lr_P.ensure(size_t(nc) * nb * r);
         c.lr_PH.ensure(size_t(nc) * r * nb);
-        qr_seed_kernel<<<nc, 256, 0, s>>>(m, p, r, c.lr_Q2.p, size_t(p) * r, c.lr_P.p, size_t(nb) * r);
+        { QPS_NOTE_LAUNCH(); qr_seed_kernel<<<nc, 256, 0, s>>>(m, p, r, c.lr_Q2.p, size_t(p) * r, c.lr_P.p, size_t(nb) * r); }
         QPS_CUDA(cudaGetLastError());
         for (int pn = nP - 1; pn >= 0; --pn) {
             std::vector<GemmTask> t1(nc), t2(nc), t3(nc);
@@ -780,8 +782,8 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             zgemm_batched(m, r, cplx{-1, 0}, cplx{1, 0}, t3, s, c.ws.gemm_tasks, "lr_qr");
         }
         tmark("rank check, Q2, P = Q [Q2; 0]");
-        conj_transpose_kernel<<<dim3(64, nc), 256, 0, s>>>(nb, r, c.lr_P.p, size_t(nb) * r, c.lr_PH.p,
-                                                           size_t(r) * nb);
+        { QPS_NOTE_LAUNCH(); conj_transpose_kernel<<<dim3(64, nc), 256, 0, s>>>(nb, r, c.lr_P.p, size_t(nb) * r, c.lr_PH.p,
+                                                           size_t(r) * nb); }
         QPS_CUDA(cudaGetLastError());
     } else {
 // column-pivoted QR of each sample, numerical rank
@@ -817,8 +819,8 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
                                               int(std::max<size_t>(sm, 48 * 1024))));
                 attr = std::max<size_t>(sm, 48 * 1024);
             }
-            lr_form_q_kernel<<<dim3(nc, (r + 7) / 8), 256, size_t(8) * nb * sizeof(cplx), s>>>(
-                nb, kLrSample, r, cs.W.p, cs.tau.p, c.lr_P.p, nb, size_t(nb) * r, c.lr_PH.p, size_t(r) * nb);
+            { QPS_NOTE_LAUNCH(); lr_form_q_kernel<<<dim3(nc, (r + 7) / 8), 256, size_t(8) * nb * sizeof(cplx), s>>>(
+                nb, kLrSample, r, cs.W.p, cs.tau.p, c.lr_P.p, nb, size_t(nb) * r, c.lr_PH.p, size_t(r) * nb); }
             QPS_CUDA(cudaGetLastError());
         }
     }
@@ -1228,7 +1230,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         std::vector<cplx*> fa, fd, wb, vb;
         std::vector<int*> fp;
         std::vector<int> orig;
-        stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, c.lr_W0.p);
+        { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, c.lr_W0.p); }
         QPS_CUDA(cudaGetLastError());
         for (int a = 0; a < ns; ++a) {
             const size_t qa = size_t(a) * 2 * (I - 1);
@@ -1308,7 +1310,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         c.lr_a.ensure(size_t(cnt) * r2);
         DBuf<cplx>& Zb = c.lr_Z[lvl];
         Zb.ensure(size_t(cnt) * nb * r2);
-        set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Cm.p);
+        { QPS_NOTE_LAUNCH(); set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Cm.p); }
         QPS_CUDA(cudaGetLastError());
         static const bool cap_lu = [] {  // QPS_WB_CAP=lu: LU + solve against I instead of Gauss-Jordan
             const char* e = getenv("QPS_WB_CAP");
@@ -1316,7 +1318,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }();
         const bool gjinv = !cap_lu && r2 <= kGjMax;
         if (!gjinv) {
-            set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Ci.p);
+            { QPS_NOTE_LAUNCH(); set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Ci.p); }
             QPS_CUDA(cudaGetLastError());
         }
         std::vector<GemmTask> m(cnt), z(cnt);
@@ -1355,11 +1357,11 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
                                                   int(kGjMax * kGjMax * sizeof(cplx))));
                     attr = true;
                 }
-                gj_inverse_kernel<<<cnt, 512, size_t(r2) * r2 * sizeof(cplx), s>>>(r2, c.lr_Cm.p,
-                                                                                  capflag.p + cap_orig.size());
+                { QPS_NOTE_LAUNCH(); gj_inverse_kernel<<<cnt, 512, size_t(r2) * r2 * sizeof(cplx), s>>>(r2, c.lr_Cm.p,
+                                                                                  capflag.p + cap_orig.size()); }
             } else {
                 int* fl = capflag.p + cap_orig.size();
-                gj_inverse_reg_kernel<96><<<cnt, 4 * 96, 0, s>>>(c.lr_Cm.p, fl);
+                { QPS_NOTE_LAUNCH(); gj_inverse_reg_kernel<96><<<cnt, 4 * 96, 0, s>>>(c.lr_Cm.p, fl); }
             }
             QPS_CUDA(cudaGetLastError());
             cap_orig.insert(cap_orig.end(), orig.begin(), orig.end());

@@ -208,9 +208,9 @@ void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, 
         }
         {
             ProfScope ps("field", s, 0.0, 0.0, evals);
-            field_kernel<<<unsigned(tiles.size()), 32 * kFieldWarps, 0, s>>>(
+            { QPS_NOTE_LAUNCH(); field_kernel<<<unsigned(tiles.size()), 32 * kFieldWarps, 0, s>>>(
                 c.field_tasks.p, c.field_tiles.p, c.field_qx.p, c.field_qy.p, pool, device_near_table(),
-                cplx{alpha.real(), alpha.imag()}, cplx{ainv.real(), ainv.imag()}, d, c.field_out.p, c.d_err.p);
+                cplx{alpha.real(), alpha.imag()}, cplx{ainv.real(), ainv.imag()}, d, c.field_out.p, c.d_err.p); }
             QPS_CUDA(cudaGetLastError());
         }
         int herr = 0;

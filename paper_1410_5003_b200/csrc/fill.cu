@@ -658,16 +658,16 @@ void launch_pair_fill(const std::vector<PairTask>& tasks, const DevPool& pool, i
         const int4* tl = d_tiles.p + off[kind];
         const dim3 grid(unsigned(maxt[kind]), n);
         switch (kind) {
-            case 0: pair_fill_kernel<0, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 1: pair_fill_kernel<0, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 2: pair_fill_kernel<1, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 3: pair_fill_kernel<1, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 4: pair_fill_kernel<2, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 5: pair_fill_kernel<2, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 6: pair_fill_kernel<0, 1, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 7: pair_fill_kernel<0, 2, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            case 8: pair_fill_kernel<1, 1, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
-            default: pair_fill_kernel<1, 2, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); break;
+            case 0: { QPS_NOTE_LAUNCH(); pair_fill_kernel<0, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 1: { QPS_NOTE_LAUNCH(); pair_fill_kernel<0, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 2: { QPS_NOTE_LAUNCH(); pair_fill_kernel<1, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 3: { QPS_NOTE_LAUNCH(); pair_fill_kernel<1, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 4: { QPS_NOTE_LAUNCH(); pair_fill_kernel<2, 1, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 5: { QPS_NOTE_LAUNCH(); pair_fill_kernel<2, 2, false><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 6: { QPS_NOTE_LAUNCH(); pair_fill_kernel<0, 1, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 7: { QPS_NOTE_LAUNCH(); pair_fill_kernel<0, 2, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            case 8: { QPS_NOTE_LAUNCH(); pair_fill_kernel<1, 1, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
+            default: { QPS_NOTE_LAUNCH(); pair_fill_kernel<1, 2, true><<<grid, kThreads, 0, s>>>(d_tasks.p, tl, pool, g_near_table, d_err); } break;
         }
         QPS_CUDA(cudaGetLastError());
     }
@@ -684,7 +684,7 @@ void launch_proxy_fill(const std::vector<ProxyTask>& tasks, const DevPool& pool,
     double ev = 0;
     for (const auto& t : tasks) ev += double(t.nt) * t.P * t.nterm;
     ProfScope ps("fill_proxy", s, 200.0 * ev, 0.0, ev);
-    proxy_fill_kernel<<<unsigned(tiles.size()), kThreads, 0, s>>>(d_tasks.p, d_tiles.p, pool, g_near_table, d_err);
+    { QPS_NOTE_LAUNCH(); proxy_fill_kernel<<<unsigned(tiles.size()), kThreads, 0, s>>>(d_tasks.p, d_tiles.p, pool, g_near_table, d_err); }
     QPS_CUDA(cudaGetLastError());
 }
 
@@ -696,8 +696,8 @@ void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const D
     const int blocks = (total_rows + 3) / 4;
     const double ev = 2.0 * 30.0 * total_rows;
     ProfScope ps("fill_alpert", s, 200.0 * ev, 0.0, ev);
-    alpert_kernel<<<blocks, 128, 0, s>>>(d_tasks.p, int(tasks.size()), total_rows, pool, d_segs, d_fourier,
-                                         g_near_table, d_err);
+    { QPS_NOTE_LAUNCH(); alpert_kernel<<<blocks, 128, 0, s>>>(d_tasks.p, int(tasks.size()), total_rows, pool, d_segs, d_fourier,
+                                         g_near_table, d_err); }
     QPS_CUDA(cudaGetLastError());
 }
 
@@ -705,7 +705,7 @@ void launch_hankel_batch(int n, const double* d_x, cplx* d_h0, cplx* d_h1, cudaS
     if (n <= 0) return;
     const int blocks = std::min((n + 255) / 256, 148 * 8);
     ProfScope ps("hankel", s, 140.0 * n, 0.0, n);
-    hankel_batch_kernel<<<blocks, 256, 0, s>>>(n, d_x, d_h0, d_h1, g_near_table);
+    { QPS_NOTE_LAUNCH(); hankel_batch_kernel<<<blocks, 256, 0, s>>>(n, d_x, d_h0, d_h1, g_near_table); }
     QPS_CUDA(cudaGetLastError());
 }
 

@@ -340,12 +340,12 @@ void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_
     if (kNorm) parts->ensure(ntasks * tiles);
     for (size_t off = 0; off < ntasks; off += 65535) {
         const unsigned cnt = unsigned(std::min<size_t>(65535, ntasks - off));
-        kern<<<dim3(tiles, cnt), Cfg::NT, Cfg::SMEM, s>>>(M, N, alpha, beta, tasks + off, tiles_m,
-                                                         kNorm ? parts->p : nullptr, off);
+        { QPS_NOTE_LAUNCH(); kern<<<dim3(tiles, cnt), Cfg::NT, Cfg::SMEM, s>>>(M, N, alpha, beta, tasks + off, tiles_m,
+                                                         kNorm ? parts->p : nullptr, off); }
         ++g_zgemm_launches;
     }
     if (kNorm) {
-        norm_parts_kernel<<<unsigned((ntasks + 127) / 128), 128, 0, s>>>(parts->p, tiles, int(ntasks), norms);
+        { QPS_NOTE_LAUNCH(); norm_parts_kernel<<<unsigned((ntasks + 127) / 128), 128, 0, s>>>(parts->p, tiles, int(ntasks), norms); }
         QPS_CUDA(cudaGetLastError());
     }
 }
@@ -1971,7 +1971,7 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
         const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
         for (size_t off = 0; off < tasks.size(); off += 65535) {
             const unsigned cnt = unsigned(std::min<size_t>(65535, tasks.size() - off));
-            zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m);
+            { QPS_NOTE_LAUNCH(); zgemm_kernel<<<dim3(tiles_m * tiles_n, cnt), 128, 0, s>>>(M, N, alpha, beta, d_tasks.p + off, tiles_m); }
         }
     }
     QPS_CUDA(cudaGetLastError());
@@ -2014,7 +2014,7 @@ void launch_cod_factor(const CodBatch& b, cudaStream_t s) {
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCodFacSmemMax)));
             attr = true;
         }
-        cod_factor_kernel<kFast, true><<<b.count, 512, sm, s>>>(b);
+        { QPS_NOTE_LAUNCH(); cod_factor_kernel<kFast, true><<<b.count, 512, sm, s>>>(b); }
     } else {
         const size_t res = latency_reserve(b.count);
         static bool attr = false;
@@ -2023,7 +2023,7 @@ void launch_cod_factor(const CodBatch& b, cudaStream_t s) {
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLatencyReserve)));
             attr = true;
         }
-        cod_factor_kernel<kFast, false><<<b.count, 256, res, s>>>(b);
+        { QPS_NOTE_LAUNCH(); cod_factor_kernel<kFast, false><<<b.count, 256, res, s>>>(b); }
     }
     QPS_CUDA(cudaGetLastError());
 }
@@ -2044,7 +2044,7 @@ void cod_factor_fast(const CodBatch& b, cudaStream_t s) {
 void cod_rank(const CodBatch& b, double th, const int* flags, cudaStream_t s) {
     if (b.count == 0) return;
     ProfScope ps("cod_rank", s, 0.0);
-    cod_rank_kernel<<<(b.count + 127) / 128, 128, 0, s>>>(b, th, flags);
+    { QPS_NOTE_LAUNCH(); cod_rank_kernel<<<(b.count + 127) / 128, 128, 0, s>>>(b, th, flags); }
     QPS_CUDA(cudaGetLastError());
 }
 void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
@@ -2058,7 +2058,7 @@ void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
                                           int(kCodSmemMax)));
             attr = true;
         }
-        cod_operator_smem_kernel<<<b.count, 256, sm, s>>>(b, flags);
+        { QPS_NOTE_LAUNCH(); cod_operator_smem_kernel<<<b.count, 256, sm, s>>>(b, flags); }
     } else {
         // few large problems (the corners): latency-bound single CTAs that keep
         // their SM to themselves (the reservation keeps GEMM CTAs off it)
@@ -2071,11 +2071,11 @@ void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
                                           int(kLatencyReserve)));
             attr = true;
         }
-        cod_operator_kernel<<<b.count, 256, res, s>>>(b, flags);
+        { QPS_NOTE_LAUNCH(); cod_operator_kernel<<<b.count, 256, res, s>>>(b, flags); }
         QPS_CUDA(cudaGetLastError());
         const size_t qs = std::max(size_t(8) * b.m * sizeof(cplx), res);
         if (qs > kLatencyReserve) fail(QPS_ERR_INTERNAL, "cod_qh: m too large");
-        cod_qh_kernel<<<dim3((b.m + 7) / 8, b.count), 256, qs, s>>>(b, flags);
+        { QPS_NOTE_LAUNCH(); cod_qh_kernel<<<dim3((b.m + 7) / 8, b.count), 256, qs, s>>>(b, flags); }
     }
     QPS_CUDA(cudaGetLastError());
 }
@@ -2097,8 +2097,8 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
                                           int(110 * 1024)));
             attr = true;
         }
-        cod_trsm_blk_kernel<<<dim3((ncols + kTrsmBlkCols - 1) / kTrsmBlkCols, b.count), 256, shb, s>>>(
-            b, B, ldb, stride, ncols, flags);
+        { QPS_NOTE_LAUNCH(); cod_trsm_blk_kernel<<<dim3((ncols + kTrsmBlkCols - 1) / kTrsmBlkCols, b.count), 256, shb, s>>>(
+            b, B, ldb, stride, ncols, flags); }
     } else if (shc <= 200 * 1024) {
         static bool attr = false;
         if (!attr) {
@@ -2106,8 +2106,8 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
                                           int(200 * 1024)));
             attr = true;
         }
-        cod_trsm_chunk_kernel<<<dim3((ncols + kTrsmCols - 1) / kTrsmCols, b.count), 256, shc, s>>>(b, B, ldb, stride,
-                                                                                                   ncols, flags);
+        { QPS_NOTE_LAUNCH(); cod_trsm_chunk_kernel<<<dim3((ncols + kTrsmCols - 1) / kTrsmCols, b.count), 256, shc, s>>>(b, B, ldb, stride,
+                                                                                                   ncols, flags); }
     } else if (sh <= 160 * 1024) {
         static size_t attr = 0;
         if (sh > attr) {
@@ -2115,7 +2115,7 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
                                           int(160 * 1024)));
             attr = 160 * 1024;
         }
-        cod_trsm_kernel<true><<<grid, 128, sh, s>>>(b, B, ldb, stride, ncols, flags);
+        { QPS_NOTE_LAUNCH(); cod_trsm_kernel<true><<<grid, 128, sh, s>>>(b, B, ldb, stride, ncols, flags); }
     } else {
         const size_t res = latency_reserve(int(grid.x * grid.y));
         static bool attr = false;
@@ -2124,7 +2124,7 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
                                           int(kLatencyReserve)));
             attr = true;
         }
-        cod_trsm_kernel<false><<<grid, 128, res, s>>>(b, B, ldb, stride, ncols, flags);
+        { QPS_NOTE_LAUNCH(); cod_trsm_kernel<false><<<grid, 128, res, s>>>(b, B, ldb, stride, ncols, flags); }
     }
     QPS_CUDA(cudaGetLastError());
 }
@@ -2145,7 +2145,7 @@ void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, 
         attr = true;
     }
     ProfScope ps("tri_inv", s, 8.0 / 3.0 * count * nblk * double(bs) * bs * bs * ((mode == 3) ? 2 : 1));
-    tri_inv_kernel<<<dim3(nblk, count), mode == 3 ? 512 : 256, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode);
+    { QPS_NOTE_LAUNCH(); tri_inv_kernel<<<dim3(nblk, count), mode == 3 ? 512 : 256, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode); }
     QPS_CUDA(cudaGetLastError());
 }
 }  // namespace
@@ -2162,15 +2162,15 @@ void launch_panel_fast(int n, int ld, cplx* const* dA, int* const* dP, int c0, i
                                       int(size_t(kRegPanelMaxRows) * kRlW * sizeof(cplx))));
         attr = true;
     }
-    lu_panel_sm2_kernel<<<count, threads, size_t(n - c0) * w * sizeof(cplx), s>>>(n, ld, dA, dP, c0, w, sing,
-                                                                                  rl_map);
+    { QPS_NOTE_LAUNCH(); lu_panel_sm2_kernel<<<count, threads, size_t(n - c0) * w * sizeof(cplx), s>>>(n, ld, dA, dP, c0, w, sing,
+                                                                                  rl_map); }
 }
 
 void launch_row_permute(int n, int ld, cplx* const* dA, const int* const* dP, int count, int k0, int kend, int c0,
                         int c1, cudaStream_t s, DBuf<int>& perm) {
     if (c1 <= c0) return;
     perm.ensure(size_t(count) * (2 * n + 1));
-    perm_build_kernel<<<count, 128, 0, s>>>(n, dP, perm.p, k0, kend);
+    { QPS_NOTE_LAUNCH(); perm_build_kernel<<<count, 128, 0, s>>>(n, dP, perm.p, k0, kend); }
     QPS_CUDA(cudaGetLastError());
     const size_t sh = size_t(kPermWarps) * (n - k0) * sizeof(cplx);
     static size_t attr = 0;
@@ -2180,7 +2180,7 @@ void launch_row_permute(int n, int ld, cplx* const* dA, const int* const* dP, in
         attr = std::max<size_t>(sh, 64 * 1024);
     }
     const int nx = std::min((c1 - c0 + kPermWarps - 1) / kPermWarps, 32);
-    row_permute_kernel<<<dim3(nx, count), 256, sh, s>>>(n, ld, dA, perm.p, k0, c0, c1);
+    { QPS_NOTE_LAUNCH(); row_permute_kernel<<<dim3(nx, count), 256, sh, s>>>(n, ld, dA, perm.p, k0, c0, c1); }
     QPS_CUDA(cudaGetLastError());
 }
 
@@ -2216,7 +2216,7 @@ void gemm_update(LuCtx& L, int M, int N, int K, size_t aoff, size_t boff, size_t
         t.C = Bbase[b] + coff;
         t.ldc = ldb;
     }
-    zgemm_batched(M, N, alpha, beta, tasks, L.s, L.ws.gemm_tasks);
+    zgemm_batched(M, N, alpha, beta, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
 }
 
 // X[r0:r1, c0:c0+nc] <- L[r0:r1, r0:r1]^{-1} X (unit lower) inside the factor itself
@@ -2245,7 +2245,7 @@ void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc, bool rhs = f
             t.C = L.hA[b] + size_t(c0) * L.ld + r0;  // in place: <= 64 rows, one CTA per column tile
             t.ldc = L.ld;
         }
-        zgemm_batched(m, nc, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks);
+        zgemm_batched(m, nc, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
         return;
     }
     const int h = ((m + kTB - 1) / kTB + 1) / 2 * kTB;
@@ -2273,9 +2273,9 @@ void lu_rec(LuCtx& L, int c0, int nc) {
                                               200 * 1024));
                 attr = true;
             }
-            lu_panel_smem_kernel<<<L.count, 256, psm, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc, L.sing);
+            { QPS_NOTE_LAUNCH(); lu_panel_smem_kernel<<<L.count, 256, psm, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc, L.sing); }
         } else {
-            lu_panel_kernel<<<L.count, 256, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, L.sing);
+            { QPS_NOTE_LAUNCH(); lu_panel_kernel<<<L.count, 256, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, L.sing); }
         }
         QPS_CUDA(cudaGetLastError());
         return;
@@ -2315,7 +2315,7 @@ void trsm_lower_rhs_leaf(LuCtx& L, int r0, int r1, int bs) {
         t.C = (*L.hB)[b] + r0;
         t.ldc = L.ldb;
     }
-    zgemm_batched(m, L.nrhs, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks);
+    zgemm_batched(m, L.nrhs, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
 }
 // B[r0+h:r1] -= L[r0+h:r1, r0:r0+h] B[r0:r0+h]
 void trsm_lower_rhs_update(LuCtx& L, int r0, int h, int r1) {
@@ -2332,7 +2332,7 @@ void trsm_lower_rhs_update(LuCtx& L, int r0, int h, int r1) {
         t.C = (*L.hB)[b] + r0 + h;
         t.ldc = L.ldb;
     }
-    zgemm_batched(r1 - r0 - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks);
+    zgemm_batched(r1 - r0 - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
 }
 
 void trsm_lower_rhs(LuCtx& L, int r0, int r1) {
@@ -2353,7 +2353,7 @@ void trsm_lower_rhs(LuCtx& L, int r0, int r1) {
             t.C = (*L.hB)[b] + r0;  // in place: <= 64 rows, one CTA per column tile
             t.ldc = L.ldb;
         }
-        zgemm_batched(m, L.nrhs, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks);
+        zgemm_batched(m, L.nrhs, cplx{1, 0}, cplx{0, 0}, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
         return;
     }
     const int h = ((m + kTB - 1) / kTB + 1) / 2 * kTB;
@@ -2370,7 +2370,7 @@ void trsm_lower_rhs(LuCtx& L, int r0, int r1) {
         t.C = (*L.hB)[b] + r0 + h;
         t.ldc = L.ldb;
     }
-    zgemm_batched(m - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks);
+    zgemm_batched(m - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
     trsm_lower_rhs(L, r0 + h, r1);
 }
 
@@ -2415,7 +2415,7 @@ void lu_rec_spine(LuCtx& L, int c0, int nc) {
             t.C = (*L.hB)[b] + c0 + h;
             t.ldc = L.ldb;
         }
-        zgemm_batched(L.n - c0 - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks);
+        zgemm_batched(L.n - c0 - h, L.nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
     }
     lu_rec_spine(L, c0 + h, nc - h);
 }
@@ -2441,7 +2441,7 @@ void upper_solve_tiles(int n, int ld, const std::vector<cplx*>& hA, const std::v
                 t.C = hB[b] + k0;
                 t.ldc = ldb;
             }
-            zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks);
+            zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
             return;
         }
         const int bm = (b0 + b1 + 1) / 2;
@@ -2459,7 +2459,7 @@ void upper_solve_tiles(int n, int ld, const std::vector<cplx*>& hA, const std::v
             t.C = hB[b] + r0;
             t.ldc = ldb;
         }
-        zgemm_batched(rm - r0, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+        zgemm_batched(rm - r0, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
         upper(b0, bm);
     };
     upper(0, (n + kTB - 1) / kTB);
@@ -2483,13 +2483,13 @@ void lu_rl(LuCtx& L) {
             if (n - k0 <= kRegPanelMaxRows)
                 launch_panel_fast(n, L.ld, L.dA, L.dP, k0, w, L.sing, L.ws.rl_map.p, L.count, L.s);
             else
-                lu_rl_panel_kernel<<<L.count, 256, size_t(n - k0) * w * sizeof(cplx), L.s>>>(n, L.ld, L.dA, L.dP, k0,
-                                                                                             w, L.sing, L.ws.rl_map.p);
+                { QPS_NOTE_LAUNCH(); lu_rl_panel_kernel<<<L.count, 256, size_t(n - k0) * w * sizeof(cplx), L.s>>>(n, L.ld, L.dA, L.dP, k0,
+                                                                                             w, L.sing, L.ws.rl_map.p); }
             QPS_CUDA(cudaGetLastError());
         }
         if (n > w) {
             ProfScope ps("lu_swap", L.s, 0.0);
-            lu_rl_cols_kernel<<<dim3((n - w + 7) / 8, L.count), 256, 0, L.s>>>(n, L.ld, L.dA, L.ws.rl_map.p, k0, w);
+            { QPS_NOTE_LAUNCH(); lu_rl_cols_kernel<<<dim3((n - w + 7) / 8, L.count), 256, 0, L.s>>>(n, L.ld, L.dA, L.ws.rl_map.p, k0, w); }
             QPS_CUDA(cudaGetLastError());
         }
         const int m = n - k0 - w;
@@ -2583,7 +2583,7 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
             t.C = hB[b] + k0;
             t.ldc = ldb;
         }
-        zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks);
+        zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
     };
     auto update = [&](int M, int K, size_t aoff, int brow, int crow) {
         tasks.assign(count, GemmTask{});
@@ -2598,7 +2598,7 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
             t.C = hB[b] + crow;
             t.ldc = ldb;
         }
-        zgemm_batched(M, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks);
+        zgemm_batched(M, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
     };
     // recursive triangular solves on 64-aligned splits: the top levels carry most
     // flops as GEMMs with K = n/2, n/4, ...
@@ -2626,14 +2626,14 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {
     if (count == 0) return;
     ProfScope ps("reduce", s, 0.0, 16.0 * count * double(m) * n);
-    maxabs_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out);
+    { QPS_NOTE_LAUNCH(); maxabs_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out); }
     QPS_CUDA(cudaGetLastError());
 }
 void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s,
                  double* maxabs_out) {
     if (count == 0) return;
     ProfScope ps("reduce", s, 0.0, 16.0 * count * double(m) * n);
-    fro_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out, maxabs_out);
+    { QPS_NOTE_LAUNCH(); fro_kernel<<<count, 256, 0, s>>>(X, m, n, ld, stride, out, maxabs_out); }
     QPS_CUDA(cudaGetLastError());
 }
 void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride, int m, int n,
@@ -2641,7 +2641,7 @@ void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, s
     if (count == 0 || m == 0 || n == 0) return;
     const int bx = int(std::min<size_t>((size_t(m) * n + 255) / 256, 1024));
     ProfScope ps("copy", s, 0.0, 32.0 * count * double(m) * n);
-    copy_blocks_kernel<<<dim3(bx, count), 256, 0, s>>>(src, lds, sstride, dst, ldd, dstride, m, n);
+    { QPS_NOTE_LAUNCH(); copy_blocks_kernel<<<dim3(bx, count), 256, 0, s>>>(src, lds, sstride, dst, ldd, dstride, m, n); }
     QPS_CUDA(cudaGetLastError());
 }
 void zgemv_batched(int M, cplx alpha, cplx beta, const std::vector<GemvTask>& tasks, cudaStream_t s,
@@ -2652,7 +2652,7 @@ void zgemv_batched(int M, cplx alpha, cplx beta, const std::vector<GemvTask>& ta
     for (const auto& t : tasks)
         for (int q = 0; q < t.nseg; ++q) fl += 8.0 * M * t.n[q];
     ProfScope ps("zgemv", s, fl, fl * 2.0);
-    zgemv_kernel<<<dim3((M + 31) / 32, unsigned(tasks.size())), 256, 0, s>>>(M, alpha, beta, d_tasks.p);
+    { QPS_NOTE_LAUNCH(); zgemv_kernel<<<dim3((M + 31) / 32, unsigned(tasks.size())), 256, 0, s>>>(M, alpha, beta, d_tasks.p); }
     QPS_CUDA(cudaGetLastError());
 }
 
@@ -2660,12 +2660,12 @@ double measure_dfma_tflops(cudaStream_t s) {
     DBuf<double> out;
     out.ensure(1);
     const int iters = 4096, blocks = 148 * 8, threads = 256;
-    dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, 64);
+    { QPS_NOTE_LAUNCH(); dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, 64); }
     cudaEvent_t e0, e1;
     QPS_CUDA(cudaEventCreate(&e0));
     QPS_CUDA(cudaEventCreate(&e1));
     QPS_CUDA(cudaEventRecord(e0, s));
-    dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, iters);
+    { QPS_NOTE_LAUNCH(); dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, iters); }
     QPS_CUDA(cudaEventRecord(e1, s));
     QPS_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
@@ -2680,12 +2680,12 @@ double measure_dmma_tflops(cudaStream_t s) {
     DBuf<double> out;
     out.ensure(1);
     const int iters = 4096, blocks = 148 * 8, threads = 256;
-    dmma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, 64);
+    { QPS_NOTE_LAUNCH(); dmma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, 64); }
     cudaEvent_t e0, e1;
     QPS_CUDA(cudaEventCreate(&e0));
     QPS_CUDA(cudaEventCreate(&e1));
     QPS_CUDA(cudaEventRecord(e0, s));
-    dmma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, iters);
+    { QPS_NOTE_LAUNCH(); dmma_peak_kernel<<<blocks, threads, 0, s>>>(out.p, iters); }
     QPS_CUDA(cudaEventRecord(e1, s));
     QPS_CUDA(cudaEventSynchronize(e1));
     float ms = 0;

@@ -134,7 +134,6 @@ void prof_reset() {
 
 ProfScope::ProfScope(const char* name_, cudaStream_t s_, double flops_, double bytes_, double units_, int nl)
     : name(name_), s(s_), flops(flops_), bytes(bytes_), units(units_), nlaunch(nl) {
-    g_launches += nl;
     if (!g_on) return;
     e0 = get_event();
     e1 = get_event();

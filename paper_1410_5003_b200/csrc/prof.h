@@ -13,6 +13,8 @@
 namespace qpsb {
 
 extern std::atomic<uint64_t> g_launches;
+// every kernel launch site of the library counts itself (qps_launch_count)
+#define QPS_NOTE_LAUNCH() (::qpsb::g_launches.fetch_add(1, std::memory_order_relaxed))
 
 void prof_enable(bool on);
 bool prof_enabled();

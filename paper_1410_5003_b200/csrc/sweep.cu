@@ -104,8 +104,8 @@ void pad_identity(Ctx& c) {
     for (int j = 0; j < D.I; ++j) n2[j] = 2 * D.N[j];
     c.d_nodes2.upload(n2, c.stream);
     const size_t tot = size_t(D.nsys) * D.I * D.nb;
-    pad_identity_kernel<<<unsigned((tot + 255) / 256), 256, 0, c.stream>>>(c.Adiag.p, D.sA(), D.nb, c.d_nodes2.p, D.I,
-                                                                            D.nsys);
+    { QPS_NOTE_LAUNCH(); pad_identity_kernel<<<unsigned((tot + 255) / 256), 256, 0, c.stream>>>(c.Adiag.p, D.sA(), D.nb, c.d_nodes2.p, D.I,
+                                                                            D.nsys); }
     QPS_CUDA(cudaGetLastError());
 }
 
@@ -453,8 +453,8 @@ void assemble_from_cache(Ctx& c, const std::vector<Problem>& probs) {
     c.d_ctiles.upload(tiles, s);
     {
         ProfScope ps("assemble", s, 0.0, bytes);
-        combine_kernel<<<unsigned(tiles.size()), 256, 0, s>>>(c.d_comb.p, c.d_ctiles.p, c.cache_pool.p, c.coef_buf.p,
-                                                              ns);
+        { QPS_NOTE_LAUNCH(); combine_kernel<<<unsigned(tiles.size()), 256, 0, s>>>(c.d_comb.p, c.d_ctiles.p, c.cache_pool.p, c.coef_buf.p,
+                                                              ns); }
         QPS_CUDA(cudaGetLastError());
     }
     if (!bt.empty()) {
@@ -462,8 +462,8 @@ void assemble_from_cache(Ctx& c, const std::vector<Problem>& probs) {
         int maxn = 0;
         for (const auto& b : bt) maxn = std::max(maxn, b.N);
         ProfScope ps("assemble", s, 0.0, 0.0);
-        band_kernel<<<dim3((maxn * 33 + 127) / 128, unsigned(bt.size())), 128, 0, s>>>(
-            c.d_band.p, int(bt.size()), c.cache_pool.p, c.coef_buf.p, ns);
+        { QPS_NOTE_LAUNCH(); band_kernel<<<dim3((maxn * 33 + 127) / 128, unsigned(bt.size())), 128, 0, s>>>(
+            c.d_band.p, int(bt.size()), c.cache_pool.p, c.coef_buf.p, ns); }
         QPS_CUDA(cudaGetLastError());
     }
     // W blocks and f per angle (assembly.hpp:414-441): O(M K) + O(N) on the host
