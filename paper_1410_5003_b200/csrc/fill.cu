@@ -25,6 +25,10 @@ namespace qpsb {
 namespace {
 __constant__ double c_alpert_nodes[QPS_ALPERT_NAUX];
 __constant__ double c_alpert_weights[QPS_ALPERT_NAUX];
+// Lagrange weights of the unclamped stencils (alpert.hpp:73-92): identical for
+// every row, computed once on the host with the kernel's own arithmetic
+__device__ double g_alpert_lw[2 * QPS_ALPERT_NAUX][16];
+__constant__ int c_alpert_t0[2 * QPS_ALPERT_NAUX];
 double* g_near_table = nullptr;
 }  // namespace
 
@@ -33,6 +37,29 @@ void upload_hankel_tables() {
     if (done) return;
     QPS_CUDA(cudaMemcpyToSymbol(c_hankel_far, qps_hankel_far_coeffs, sizeof(qps_hankel_far_coeffs)));
     QPS_CUDA(cudaMemcpyToSymbol(c_alpert_nodes, qps_alpert_nodes, sizeof(qps_alpert_nodes)));
+    {
+        double lw[2 * QPS_ALPERT_NAUX][16];
+        int t0s[2 * QPS_ALPERT_NAUX];
+        for (int lane = 0; lane < 2 * QPS_ALPERT_NAUX; ++lane) {
+            const int side = lane < QPS_ALPERT_NAUX ? -1 : 1;
+            const double xi = side * qps_alpert_nodes[lane % QPS_ALPERT_NAUX];
+            const int t0 = int(std::floor(xi)) - 16 / 2 + 1;
+            t0s[lane] = t0;
+            for (int rr = 0; rr < 16; ++rr) {
+                double num = 1.0, den = 1.0;
+                const int tr = t0 + rr;
+                for (int qq = 0; qq < 16; ++qq) {
+                    if (qq == rr) continue;
+                    const int tq = t0 + qq;
+                    num *= xi - tq;
+                    den *= double(tr - tq);
+                }
+                lw[lane][rr] = num / den;
+            }
+        }
+        QPS_CUDA(cudaMemcpyToSymbol(g_alpert_lw, lw, sizeof(lw)));
+        QPS_CUDA(cudaMemcpyToSymbol(c_alpert_t0, t0s, sizeof(t0s)));
+    }
     QPS_CUDA(cudaMemcpyToSymbol(c_alpert_weights, qps_alpert_weights, sizeof(qps_alpert_weights)));
     QPS_CUDA(cudaMalloc(&g_near_table, sizeof(qps_hankel_near_coeffs)));
     QPS_CUDA(cudaMemcpy(g_near_table, qps_hankel_near_coeffs, sizeof(qps_hankel_near_coeffs),
@@ -438,11 +465,14 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
     __shared__ cplx s_val[4][2 * QPS_ALPERT_NAUX][4];    // per warp, aux, kind
     __shared__ double s_lw[4][2 * QPS_ALPERT_NAUX][16];  // Lagrange weights
     __shared__ int s_t0[4][2 * QPS_ALPERT_NAUX];
+    __shared__ double s_lwtab[2 * QPS_ALPERT_NAUX][16];  // the unclamped weights, one copy per CTA
+    __shared__ int s_clamped[4];
     load_near(s_near, g_near);
+    for (int e = threadIdx.x; e < 2 * QPS_ALPERT_NAUX * 16; e += blockDim.x) (&s_lwtab[0][0])[e] = (&g_alpert_lw[0][0])[e];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int row = blockIdx.x * 4 + warp;
-    if (row >= total_rows) return;
+    // grid-stride over rows: the tables above are loaded once per CTA
+    for (int row = blockIdx.x * 4 + warp; row < total_rows; row += gridDim.x * 4) {
     int lo = 0, hi = ntasks - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -456,11 +486,13 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
         if (m >= segs[T.seg_first + s].offset) sidx = s;
     const SegDesc sd = segs[T.seg_first + sidx];
     const int mloc = m - sd.offset;
-    if (!T.smooth && min(mloc, sd.n - 1 - mloc) < QPS_ALPERT_A) return;  // plain fallback row
+    if (!T.smooth && min(mloc, sd.n - 1 - mloc) < QPS_ALPERT_A) continue;  // plain fallback row
     const double pi = 3.14159265358979323846;
     const double h = 2.0 * pi / sd.n;
     const int gt = T.t_off + m;
     const double xmx = pool.x[gt], xmy = pool.y[gt], nmx = pool.nx[gt], nmy = pool.ny[gt];
+    if (lane == 0) s_clamped[warp] = 0;
+    __syncwarp();
 
     if (lane < 2 * QPS_ALPERT_NAUX) {
         const int side = lane < QPS_ALPERT_NAUX ? -1 : 1;
@@ -496,10 +528,17 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
         s_val[warp][lane][2] = vT;
         s_val[warp][lane][3] = vDs;
         // alpert_stencil_start (alpert.hpp:90-92), clamped for open arcs (kernels.hpp:256)
-        int t0 = int(floor(xi)) - 16 / 2 + 1;
+        const int t0u = c_alpert_t0[lane];
+        int t0 = t0u;
         if (!T.smooth) t0 = max(-mloc, min(t0, sd.n - 16 - mloc));
         s_t0[warp][lane] = t0;
-        // lagrange_weights (alpert.hpp:73-87)
+        // lagrange_weights (alpert.hpp:73-87): the precomputed table unless clamped
+        if (t0 != t0u) s_clamped[warp] = 1;
+        if (t0 == t0u && !T.smooth) {  // open arcs: a clamped lane makes the warp use s_lw for every lane
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr) s_lw[warp][lane][rr] = s_lwtab[lane][rr];
+        }
+        if (t0 != t0u)
         for (int rr = 0; rr < 16; ++rr) {
             double num = 1.0, den = 1.0;
             const int tr = t0 + rr;
@@ -514,13 +553,14 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
     }
     __syncwarp();
     const int N = T.N;
+    const double(*lwt)[16] = s_clamped[warp] ? s_lw[warp] : s_lwtab;  // warp-uniform
     for (int c = lane; c < kBand; c += 32) {
         const int o = c - 16;  // column offset relative to the row
         cplx acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
         for (int a = 0; a < 2 * QPS_ALPERT_NAUX; ++a) {
             const int rr = o - s_t0[warp][a];
             if (rr < 0 || rr >= 16) continue;
-            const double lw = s_lw[warp][a][rr];
+            const double lw = lwt[a][rr];
             for (int kd = 0; kd < 4; ++kd) {
                 acc[kd].re += lw * s_val[warp][a][kd].re;
                 acc[kd].im += lw * s_val[warp][a][kd].im;
@@ -588,6 +628,8 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
                 for (int kd = 0; kd < 4; ++kd) wb[kd] = acc[kd];
             }
         }
+    }
+    __syncwarp();  // s_val / s_lw / s_t0 are rewritten by the warp's next row
     }
 }
 
@@ -693,7 +735,7 @@ void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const D
                    DBuf<AlpertTask>& d_tasks) {
     if (tasks.empty() || total_rows == 0) return;
     d_tasks.upload(tasks, s);
-    const int blocks = (total_rows + 3) / 4;
+    const int blocks = std::min((total_rows + 3) / 4, 148 * 16);
     const double ev = 2.0 * 30.0 * total_rows;
     ProfScope ps("fill_alpert", s, 200.0 * ev, 0.0, ev);
     { QPS_NOTE_LAUNCH(); alpert_kernel<<<blocks, 128, 0, s>>>(d_tasks.p, int(tasks.size()), total_rows, pool, d_segs, d_fourier,
