@@ -1918,6 +1918,16 @@ __global__ void dmma_peak_kernel(double* out, int iters) {
 
 }  // namespace
 
+namespace {
+bool thin48_off() {  // QPS_ZGEMM_THIN48=0: 16-row tiles for 48-row products (A/B)
+    static const bool off = [] {
+        const char* e = getenv("QPS_ZGEMM_THIN48");
+        return e && !strcmp(e, "0");
+    }();
+    return off;
+}
+}  // namespace
+
 void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
                    DBuf<GemmTask>& d_tasks, const char* family) {
     if (tasks.empty() || M <= 0 || N <= 0) return;
@@ -1961,7 +1971,11 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
                 fail(QPS_ERR_INTERNAL, "zgemm_batched: in-place product taller than one tile");
             }
             launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
-        } else if (M <= 48 || (M <= 80 && N >= 256))
+        } else if (M > 32 && M <= 48 && N >= 256 && kmax >= 256 && !thin48_off())
+            // the whole 48-row product in one CTA row: the wide operand is
+            // streamed once instead of once per 16-row tile
+            launch_z3<6, 2, 1, 4, 2, 2>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+        else if (M <= 48 || (M <= 80 && N >= 256))
             launch_z3<2, 2, 1, 4, 2, 4>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
         else if (kmax <= 96 || (M <= 128 && N <= 128))
             launch_z3<2, 2, 2, 2, 2, 4>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
