@@ -1032,7 +1032,10 @@ __global__ void __launch_bounds__(256) cod_trsm_chunk_kernel(CodBatch b, cplx* B
 // above updated by the solved block as small products.  T11 packed (upper,
 // column-major) and 32 columns per CTA keep two CTAs per SM; the serial chain
 // is r row steps of <= 16-term dot products instead of up-to-r-term ones.
-constexpr int kTrsmBlkCols = 32;
+#ifndef QPS_TRSM_BLK_COLS
+#define QPS_TRSM_BLK_COLS 32
+#endif
+constexpr int kTrsmBlkCols = QPS_TRSM_BLK_COLS;
 __global__ void __launch_bounds__(256) cod_trsm_blk_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
                                                            const int* __restrict__ flags) {
     extern __shared__ cplx tbk[];

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 
@@ -84,8 +85,24 @@ void upload_geometry(Ctx& c) {
     c.iface_off.assign(I, 0);
     for (int j = 0; j < I; ++j) {
         c.iface_off[j] = int(n);
-        const auto& q = g.ifaces[j];
-        for (int i = 0; i < q.N(); ++i) add(q.x[i], q.y[i], q.nx[i], q.ny[i], q.w[i]);
+        n += size_t(g.ifaces[j].N());
+    }
+    {  // interface nodes: independent per interface, copied on host threads
+        const int nt = std::max(1, std::min<int>(I, std::min(16u, std::max(1u, std::thread::hardware_concurrency()))));
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                for (int j = t; j < I; j += nt) {
+                    const auto& q = g.ifaces[j];
+                    const size_t o = size_t(c.iface_off[j]), cnt = size_t(q.N());
+                    std::memcpy(x + o, q.x.data(), cnt * sizeof(double));
+                    std::memcpy(y + o, q.y.data(), cnt * sizeof(double));
+                    std::memcpy(nx + o, q.nx.data(), cnt * sizeof(double));
+                    std::memcpy(ny + o, q.ny.data(), cnt * sizeof(double));
+                    std::memcpy(w + o, q.w.data(), cnt * sizeof(double));
+                }
+            });
+        for (auto& t : th) t.join();
     }
     c.wall_off.assign(I + 1, 0);
     for (int i = 0; i <= I; ++i) {
