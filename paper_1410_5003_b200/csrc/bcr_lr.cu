@@ -277,13 +277,26 @@ __global__ void qr_seed_kernel(int m, int p, int r, const cplx* __restrict__ Q2,
     }
 }
 
-__global__ void conj_transpose_kernel(int m, int r, const cplx* __restrict__ X, size_t xstride,
-                                      cplx* __restrict__ XH, size_t hstride) {
-    const int b = blockIdx.y;
-    for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < size_t(m) * r;
-         e += size_t(gridDim.x) * blockDim.x) {
-        const int i = int(e % m), j = int(e / m);
-        XH[size_t(b) * hstride + size_t(i) * r + j] = cconj(X[size_t(b) * xstride + e]);
+// XH = X^* per problem (X m x r column-major, XH r x m): a CTA owns 32 rows of X,
+// staged through shared memory so that both the read (down X's columns) and
+// the write (XH's 32 consecutive columns = one contiguous 32 r range) coalesce
+constexpr int kCtRows = 32, kCtMaxR = 64;
+static_assert(kLrMaxRank <= kCtMaxR, "conj_transpose_kernel: basis wider than its tile");
+__global__ void __launch_bounds__(256) conj_transpose_kernel(int m, int r, const cplx* __restrict__ X,
+                                                             size_t xstride, cplx* __restrict__ XH, size_t hstride) {
+    __shared__ cplx tile[kCtMaxR][kCtRows + 1];
+    const int b = blockIdx.y, i0 = blockIdx.x * kCtRows;
+    const int rows = min(kCtRows, m - i0);
+    const cplx* Xb = X + size_t(b) * xstride;
+    cplx* Hb = XH + size_t(b) * hstride + size_t(i0) * r;
+    for (int e = threadIdx.x; e < kCtRows * r; e += blockDim.x) {
+        const int ii = e % kCtRows, j = e / kCtRows;
+        if (ii < rows) tile[j][ii] = Xb[size_t(j) * m + i0 + ii];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * r; e += blockDim.x) {
+        const int ii = e / r, j = e % r;
+        Hb[e] = cconj(tile[j][ii]);
     }
 }
 
@@ -782,7 +795,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             zgemm_batched(m, r, cplx{-1, 0}, cplx{1, 0}, t3, s, c.ws.gemm_tasks, "lr_qr");
         }
         tmark("rank check, Q2, P = Q [Q2; 0]");
-        { QPS_NOTE_LAUNCH(); conj_transpose_kernel<<<dim3(64, nc), 256, 0, s>>>(nb, r, c.lr_P.p, size_t(nb) * r, c.lr_PH.p,
+        { QPS_NOTE_LAUNCH(); conj_transpose_kernel<<<dim3((nb + kCtRows - 1) / kCtRows, nc), 256, 0, s>>>(nb, r, c.lr_P.p, size_t(nb) * r, c.lr_PH.p,
                                                            size_t(r) * nb); }
         QPS_CUDA(cudaGetLastError());
     } else {
