@@ -107,6 +107,20 @@ typedef struct {
     double factor_ms;
 } qps_phase_times;
 
+/* How the last block solve ran (product diagnostics; the oracle reports
+ * bcr_path = -1, the reference's sequential block Thomas):
+ *   bcr_path        0 dense block cyclic reduction, 1 low-rank couplings in
+ *                   Woodbury form (default), 2 low-rank with per-level LU
+ *   lr_rank_max     largest numerical rank of a compressed coupling's sample
+ *   lr_probe_worst  a-posteriori test of the compression: max over couplings
+ *                   of ||(I - P P^*) C w2||_F / ||C w2||_F on an independent
+ *                   probe block w2 (above 1e-12 -> dense reduction) */
+typedef struct {
+    int bcr_path;
+    int lr_rank_max;
+    double lr_probe_worst;
+} qps_solver_diag;
+
 /* ---------------------------------------------------------------- context */
 int qps_abi_version(void);
 const char* qps_backend_name(void); /* "b200-cuda" or "reference-cpu" */
@@ -198,6 +212,7 @@ int qps_download_block(const qps_ctx* ctx, int kind, int i, qps_cplx* out, int* 
  * this implementation in its last fill. */
 int qps_fill_evals(const qps_ctx* ctx, uint64_t* reference, uint64_t* performed);
 int qps_get_phase_times(const qps_ctx* ctx, qps_phase_times* t);
+int qps_solver_diagnostics(const qps_ctx* ctx, qps_solver_diag* d);
 /* hankel01 batch (specfun.hpp:69-73): h0[n], h1[n] for host x[n] */
 int qps_hankel01(qps_ctx* ctx, int n, const double* x, qps_cplx* h0, qps_cplx* h1);
 /* qsolve(Q, RHS), periodize.hpp:25-39: min-norm least squares through the

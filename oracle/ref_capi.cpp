@@ -461,6 +461,12 @@ int qps_get_phase_times(const qps_ctx* c, qps_phase_times* t) {
     return QPS_OK;
 }
 
+int qps_solver_diagnostics(const qps_ctx* c, qps_solver_diag* d) {
+    if (!c || !d) return QPS_ERR_USAGE;
+    *d = qps_solver_diag{-1, 0, 0.0};  // the reference's block Thomas (tridiag.hpp:23-46)
+    return QPS_OK;
+}
+
 int qps_hankel01(qps_ctx* c, int n, const double* x, qps_cplx* h0, qps_cplx* h1) {
     return guarded(c, [&] {
         for (int i = 0; i < n; ++i) {

@@ -96,13 +96,26 @@ def config(cfg: int, seed: int = DEFAULT_SEED, n_interfaces: int | None = None):
         num = NumericsParams(P=P, Mw=40, M=60, K=K, R=1.5, clearance=0.75, memory_budget=1 << 40)
         return stack, num, om, -math.pi / 5, K, {"seed": seed, "I": I, "N": N}
     if cfg == 3:
+        # Tooth placement chosen so that the reference's own coincidence test
+        # (kernels.hpp:38-39, r < 1e-13 (1 + |x|)) never fires at I = 100:
+        # with q = 6 Kress grading the node nearest a corner sits
+        # ~3e-11 x (segment length) from it at 66-67 nodes per segment, but
+        # only ~3e-12 x length at 100 nodes per segment, so a 2-segment
+        # triangle (the round-1 layout) put two nodes within 1e-13 (1 + |x|)
+        # of each other across a corner from |y| ~ 20-50 on.  Both tooth kinds
+        # therefore have 4 vertices / 3 segments of {67, 67, 66} nodes
+        # (BASELINE: "2-4 vertices per period"; a triangular tooth stands on a
+        # flat land), every segment is >= 0.14 long, and the stack is centred
+        # on y = 0 (interfaces 1.0 apart, offsets 49.5 ... -49.5 at I = 100;
+        # BASELINE fixes the spacing, not the absolute height).
         I = 100 if n_interfaces is None else n_interfaces
+        top = 0.5 * (I - 1)
         ifaces = []
         for i in range(I):
             if i % 2 == 0:
                 a = rng.uniform(0.05, 0.3)
                 phi = rng.uniform(0.0, 2 * math.pi)
-                ifaces.append(_sine(-1.0 * i, a, phi, 200))
+                ifaces.append(_sine(top - 1.0 * i, a, phi, 200))
             else:
                 trapezoid = rng.uniform() >= 0.5
                 h = rng.uniform(0.1, 0.3)
@@ -110,13 +123,12 @@ def config(cfg: int, seed: int = DEFAULT_SEED, n_interfaces: int | None = None):
                     x1 = rng.uniform(-0.3, -0.1)
                     x2 = rng.uniform(0.1, 0.3)
                     verts = [(-0.5, 0.0), (x1, h), (x2, h), (0.5, 0.0)]
-                    nodes = [67, 67, 66]
                 else:
-                    xp = rng.uniform(-0.2, 0.2)
-                    verts = [(-0.5, 0.0), (xp, h), (0.5, 0.0)]
-                    nodes = [100, 100]
-                ifaces.append(InterfaceSpec(shape="polyline", offset=-1.0 * i, vertices=verts, nodes=nodes,
-                                            grading_q=6))
+                    xl = rng.uniform(-0.3, -0.1)
+                    xp = rng.uniform(0.0, 0.2)
+                    verts = [(-0.5, 0.0), (xl, 0.0), (xp, h), (0.5, 0.0)]
+                ifaces.append(InterfaceSpec(shape="polyline", offset=top - 1.0 * i, vertices=verts,
+                                            nodes=[67, 67, 66], grading_q=6))
         ks = [10.0 * rng.uniform(1.0, 3.0) for _ in range(I + 1)]
         stack, om = _stack_from_k(ks, ifaces)
         num = NumericsParams(P=60, Mw=40, M=60, K=10, R=1.5, clearance=0.75, memory_budget=1 << 40)

@@ -7,7 +7,7 @@
 // largest after ~35 of 600 (tools/coupling_rank.py).  Each coupling is
 // compressed once, C ~= P (P^* C) with P an orthonormal n x r basis from a
 // randomized range finder (C Omega, Omega n x 64) and column-pivoted QR of the
-// sample (the Eigen-semantics CPQR kernel, rank at a relative 1e-15), r the
+// sample (the Eigen-semantics CPQR kernel, rank at a relative 1e-14), r the
 // fixed basis width (48 columns, more than any coupling's rank).
 //
 // Cyclic reduction then never forms a dense D^{-1} L or D^{-1} U: with
@@ -19,7 +19,7 @@
 // right factor, and the work per elimination drops from 50.7 n^3 to about
 // n^3 (8/3 + 32 r/n) real flops -- the LU of D_o dominates.  Back-substitution:
 //   eta_o = z_o - Z_L (R_L(o) eta_{o-1}) - Z_U (R_U(o) eta_{o+1}).
-// The truncation error (relative 1e-15 of each coupling) is far below the
+// The truncation error (relative 1e-14 of each coupling) is far below the
 // problem's own noise floor; systems whose couplings are not low rank
 // (rank > 48 of a 64-column sample) take the dense cyclic reduction.
 #include <algorithm>
@@ -39,7 +39,13 @@ namespace qpsb {
 
 namespace {
 
-constexpr int kLrSample = 64;    // columns of the random sample
+constexpr int kLrSample = 64;    // columns of the random sample the basis is built from
+// a second, independent probe block sampled with it (same GEMM, no extra read of
+// the couplings): the a-posteriori test ||(I - P P^*) C w2||_F <= tol ||C w2||_F
+// of every compressed coupling; a failure takes the dense reduction
+constexpr int kLrProbe = 16;
+constexpr int kLrCols = kLrSample + kLrProbe;  // columns of Omega and of the sample Y
+constexpr double kLrProbeTol = 1e-12;
 constexpr int kLrMaxRank = 48;   // beyond this the dense reduction is used
 constexpr double kLrTol = 1e-14; // relative pivot threshold of the sample's CPQR
 
@@ -328,7 +334,10 @@ __global__ void stage_bases_kernel(int I, int n, size_t per, const cplx* __restr
 // Gauss-Jordan elimination with partial (row) pivoting, one CTA per matrix,
 // the matrix resident in shared memory: n steps of (pivot search, row swap,
 // scaled pivot row, rank-1 elimination of every other row), then the column
-// interchanges undone in reverse.  flag[b] = 1 on an exactly zero pivot.
+// interchanges undone in reverse.  flag[b] = 1 on an exactly zero pivot or
+// when rcond(C) = 1 / (||C||_1 ||C^{-1}||_1) <= 1e-15 (the reference's
+// PartialPivLU::rcond() test, tridiag.hpp:36-40, here exact: the inverse is
+// formed).
 constexpr int kGjMax = 112;  // 112^2 complex = 196 KB of shared memory
 __global__ void __launch_bounds__(512) gj_inverse_kernel(int n, cplx* __restrict__ C, int* __restrict__ flag) {
     extern __shared__ cplx gj[];  // n x n, ld n
@@ -340,6 +349,23 @@ __global__ void __launch_bounds__(512) gj_inverse_kernel(int n, cplx* __restrict
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < n * n; e += blockDim.x) gj[e] = Cb[e];
     __syncthreads();
+    // ||C||_1 and, at the end, ||C^{-1}||_1: rcond(C), tridiag.hpp:36-40
+    auto norm1 = [&]() {
+        double v = 0;
+        for (int jj = warp; jj < n; jj += blockDim.x / 32) {
+            double cs = 0;
+            for (int i = lane; i < n; i += 32) cs += hypot(gj[jj * n + i].re, gj[jj * n + i].im);
+            for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+            v = fmax(v, cs);
+        }
+        if (lane == 0) s_v[warp] = v;
+        __syncthreads();
+        double m = 0;
+        for (int w = 0; w < int(blockDim.x / 32); ++w) m = fmax(m, s_v[w]);
+        __syncthreads();
+        return m;
+    };
+    const double cnorm = norm1();
     for (int k = 0; k < n; ++k) {
         // pivot: first row i >= k of largest modulus in column k
         double v = -1.0;
@@ -408,6 +434,8 @@ __global__ void __launch_bounds__(512) gj_inverse_kernel(int n, cplx* __restrict
         }
         __syncthreads();
     }
+    const double inorm = norm1();
+    if (tid == 0 && !(1.0 / (cnorm * inorm) > kRcondMin)) flag[blockIdx.x] = 1;
     for (int e = tid; e < n * n; e += blockDim.x) Cb[e] = gj[e];
 }
 
@@ -435,8 +463,27 @@ __global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict_
     __shared__ double s_cv[2][4];
     __shared__ int s_ci[2][4];
     __shared__ cplx s_ca[2][4];
+    __shared__ double s_nm[4 * N / 32];
     cplx* Cb = C + size_t(blockIdx.x) * N * N;
     const int tid = threadIdx.x, g = tid / N, j = tid % N;
+    // ||C||_1 = max column sum, read from global memory before (and, for
+    // ||C^{-1}||_1, after) the register-resident elimination: rcond(C) for the
+    // reference's test, tridiag.hpp:36-40
+    auto norm1 = [&]() {
+        double v = 0;
+        for (int jj = tid >> 5; jj < N; jj += 4 * N / 32) {
+            double cs = 0;
+            for (int i = tid & 31; i < N; i += 32) cs += hypot(Cb[size_t(jj) * N + i].re, Cb[size_t(jj) * N + i].im);
+            for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+            v = fmax(v, cs);
+        }
+        if ((tid & 31) == 0) s_nm[tid >> 5] = v;
+        __syncthreads();
+        double m = 0;
+        for (int w = 0; w < 4 * N / 32; ++w) m = fmax(m, s_nm[w]);
+        return m;
+    };
+    const double cnorm = norm1();
     cplx T[NR];
     unsigned used = 0;  // bit ii: row g + 4 ii already pivotal
 #pragma unroll
@@ -529,6 +576,9 @@ __global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict_
     const int col = s_perm[j];  // A^{-1}[pinv[i]][perm[j]] = T[i][j]
 #pragma unroll
     for (int ii = 0; ii < NR; ++ii) Cb[size_t(col) * N + s_pinv[g + 4 * ii]] = T[ii];
+    __syncthreads();  // the block's global writes are visible to it after the barrier
+    const double inorm = norm1();
+    if (tid == 0 && !(1.0 / (cnorm * inorm) > kRcondMin)) flag[blockIdx.x] = 1;
 }
 
 GemmTask gemm1(const cplx* A, int lda, const cplx* B, int ldb, int K, cplx* C, int ldc) {
@@ -562,7 +612,7 @@ namespace {
 void lr_omega_setup(Ctx& c, cudaStream_t s) {
     const int nb = c.dims.nb;
     if (c.lr_omega_n == nb) return;
-    std::vector<cplx> om(size_t(nb) * kLrSample);
+    std::vector<cplx> om(size_t(nb) * kLrCols);
     uint64_t x = 0x9e3779b97f4a7c15ull;
     for (auto& z : om) {
         auto next = [&]() {
@@ -597,20 +647,20 @@ void lr_sample_async(Ctx& c) {
     QPS_CUDA(cudaEventRecord(c.ev_fill, c.stream));
     QPS_CUDA(cudaStreamWaitEvent(c.side2, c.ev_fill, 0));
     lr_omega_setup(c, c.side2);
-    c.lr_Y.ensure(size_t(nc) * nb * kLrSample);
+    c.lr_Y.ensure(size_t(nc) * nb * kLrCols);
     std::vector<GemmTask> t(nc);
     for (int q = 0; q < nc; ++q) {
         const int a = q / (2 * (I - 1)), rem = q % (2 * (I - 1));
         const bool sup = rem >= I - 1;
         const int j = sup ? rem - (I - 1) : rem;
         const cplx* C = (sup ? c.Asup.p : c.Asub.p) + size_t(a) * D.sU() + size_t(j) * D.nb2();
-        t[q] = gemm1(C, nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrSample, nb);
+        t[q] = gemm1(C, nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrCols, nb);
     }
     {
         ProfPhase phase("lowrank");
         // own family: its events on the low-priority stream span its overlap
         // with the Schur chain, so the duration is not a kernel time
-        zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, c.side2, c.lr_tasks, "lr_sample");
+        zgemm_batched(nb, kLrCols, cplx{1, 0}, cplx{0, 0}, t, c.side2, c.lr_tasks, "lr_sample");
     }
     QPS_CUDA(cudaEventRecord(c.ev_sample, c.side2));
     c.lr_sample_pending = true;
@@ -641,7 +691,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     };
     const int P = D.P;
     // Y = C Omega  (= A Omega + Bc (-X Omega) when deferred)
-    c.lr_Y.ensure(size_t(nc) * nb * kLrSample);
+    c.lr_Y.ensure(size_t(nc) * nb * kLrCols);
     const bool early = c.lr_sample_pending && corr;  // Y already holds A Omega
     static const bool trace = getenv("QPS_BCR_TRACE") != nullptr;  // per-step timing to stderr (debug)
     cudaEvent_t te0 = nullptr, te1 = nullptr;
@@ -665,28 +715,28 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     {
         std::vector<GemmTask> t(nc);
         if (corr) {
-            c.lr_W.ensure(size_t(nc) * P * kLrSample);
+            c.lr_W.ensure(size_t(nc) * P * kLrCols);
             std::vector<GemmTask> w(nc);
             for (int q = 0; q < nc; ++q) {
                 const GemmTask& u = corr_task(q);
-                w[q] = gemm1(u.B[0], u.ldb[0], c.lr_omega.p, nb, nb, c.lr_W.p + size_t(q) * P * kLrSample, P);
+                w[q] = gemm1(u.B[0], u.ldb[0], c.lr_omega.p, nb, nb, c.lr_W.p + size_t(q) * P * kLrCols, P);
             }
-            zgemm_batched(P, kLrSample, cplx{-1, 0}, cplx{0, 0}, w, s, c.ws.gemm_tasks, "lr_compress");
+            zgemm_batched(P, kLrCols, cplx{-1, 0}, cplx{0, 0}, w, s, c.ws.gemm_tasks, "lr_compress");
         }
         for (int q = 0; q < nc && early; ++q) {  // Y += Bc (-X Omega)
             const GemmTask& u = corr_task(q);
-            t[q] = gemm1(u.A[0], u.lda[0], c.lr_W.p + size_t(q) * P * kLrSample, P, P,
-                         c.lr_Y.p + size_t(q) * nb * kLrSample, nb);
+            t[q] = gemm1(u.A[0], u.lda[0], c.lr_W.p + size_t(q) * P * kLrCols, P, P,
+                         c.lr_Y.p + size_t(q) * nb * kLrCols, nb);
         }
-        if (early) zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        if (early) zgemm_batched(nb, kLrCols, cplx{1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
         for (int q = 0; q < nc && !early; ++q) {
-            t[q] = gemm1(coupling(q), nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrSample, nb);
+            t[q] = gemm1(coupling(q), nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrCols, nb);
             if (corr) {
                 const GemmTask& u = corr_task(q);
                 t[q].nseg = 2;
                 t[q].A[1] = u.A[0];
                 t[q].lda[1] = u.lda[0];
-                t[q].B[1] = c.lr_W.p + size_t(q) * P * kLrSample;
+                t[q].B[1] = c.lr_W.p + size_t(q) * P * kLrCols;
                 t[q].ldb[1] = P;
                 t[q].K[1] = P;
             }
@@ -695,7 +745,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             if (getenv("QPS_TRACE_LAUNCH"))
                 fprintf(stderr, "lr_compress sample GEMM is zgemm3m launch index %llu\n",
                         (unsigned long long)g_zgemm_launches.load());
-            zgemm_batched(nb, kLrSample, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+            zgemm_batched(nb, kLrCols, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
         }
     }
     tmark("sample correction Y += Bc (-X Omega)");
@@ -709,7 +759,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     if (!cpqr_only && nb <= 640) {
         // blocked Householder QR of the samples, CPQR of the 64 x 64 R
         const int m = nb, p = kLrSample, nP = p / kQrW;
-        const size_t ys = size_t(m) * p, vs = size_t(m) * kQrW, ts = size_t(kQrW) * kQrW;
+        const size_t ys = size_t(m) * kLrCols, vs = size_t(m) * kQrW, ts = size_t(kQrW) * kQrW;
         c.lr_V.ensure(size_t(nc) * nP * vs);
         c.lr_VH.ensure(size_t(nc) * nP * vs);
         c.lr_Tq.ensure(size_t(nc) * nP * ts);
@@ -802,12 +852,15 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
 // column-pivoted QR of each sample, numerical rank
         CodSet& cs = c.lr_cod;
         cs.ensure(nc, nb, kLrSample, 1);
-        CodBatch b = cs.batch(c.lr_Y.p);
+        c.lr_Yc.ensure(size_t(nc) * nb * kLrSample);  // the 64 basis columns, packed for the COD batch
+        copy_blocks(c.lr_Y.p, nb, size_t(nb) * kLrCols, c.lr_Yc.p, nb, size_t(nb) * kLrSample, nb, kLrSample, nc, s);
+        CodBatch b = cs.batch(c.lr_Yc.p);
         cod_factor_fast(b, s);
         cod_rank(b, kLrTol, nullptr, s);
         QPS_D2H(rk.data(), cs.rank.p, sizeof(int) * nc, s);
         QPS_CUDA(cudaStreamSynchronize(s));
         for (int v : rk) r = std::max(r, v);
+        c.lr_rank_max = r;
         if (getenv("QPS_LR_TRACE")) {
             int mn = 1 << 30;
             double mean = 0;
@@ -838,6 +891,30 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         }
     }
     tmark("P^*");
+    // a-posteriori test of the basis on the independent probe columns Y2 = C w2:
+    // ||Y2 - P (P^* Y2)||_F against ||Y2||_F (read back with the ranks)
+    {
+        c.lr_G2.ensure(size_t(nc) * r * kLrProbe);
+        c.lr_pn.ensure(size_t(nc) * 2);
+        std::vector<GemmTask> g(nc), e(nc);
+        for (int q = 0; q < nc; ++q) {
+            const cplx* Y2 = c.lr_Y.p + size_t(q) * nb * kLrCols + size_t(nb) * kLrSample;
+            g[q] = gemm1(c.lr_PH.p + size_t(q) * r * nb, r, Y2, nb, nb, c.lr_G2.p + size_t(q) * r * kLrProbe, r);
+            e[q] = gemm1(c.lr_P.p + size_t(q) * nb * r, nb, c.lr_G2.p + size_t(q) * r * kLrProbe, r, r,
+                         const_cast<cplx*>(Y2), nb);
+        }
+        zgemm_batched(r, kLrProbe, cplx{1, 0}, cplx{0, 0}, g, s, c.ws.gemm_tasks, "lr_compress");
+        batched_fro(c.lr_Y.p + size_t(nb) * kLrSample, nb, kLrProbe, nb, size_t(nb) * kLrCols, nc, c.lr_pn.p + nc, s);
+        zgemm_residual_norms(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, e, s, c.ws.gemm_tasks, c.lr_parts, c.lr_pn.p);
+        c.lr_pn_h.ensure(size_t(nc) * 2);
+        QPS_D2H(c.lr_pn_h.p, c.lr_pn.p, sizeof(double) * 2 * nc, s);
+        if (!rank_deferred) {
+            QPS_CUDA(cudaEventRecord(c.ev_sample, s));
+            rank_deferred = true;
+            c.lr_rank_h.ensure(nc);
+            for (int q = 0; q < nc; ++q) c.lr_rank_h[q] = 0;  // ranks already checked above
+        }
+    }
     // R = P^* C  (= P^* A + (-P^* Bc) X when deferred)
     c.lr_R.ensure(size_t(nc) * r * nb);
     {
@@ -874,6 +951,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         QPS_CUDA(cudaEventSynchronize(c.ev_sample));
         int mx = 0;
         for (int q = 0; q < nc; ++q) mx = std::max(mx, c.lr_rank_h[q]);
+        c.lr_rank_max = std::max(c.lr_rank_max, mx);
         if (getenv("QPS_LR_TRACE")) {
             int mn = 1 << 30;
             double mean = 0;
@@ -882,6 +960,20 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
                     mean / nc, mx, kLrSample);
         }
         if (mx > kLrMaxRank) return false;  // not low rank: the dense reduction (A untouched so far)
+        static const double probe_tol = [] {  // QPS_LR_PROBE_TOL: tests force the fallback with a tiny value
+            const char* e = getenv("QPS_LR_PROBE_TOL");
+            return e ? atof(e) : kLrProbeTol;
+        }();
+        double worst = 0;
+        for (int q = 0; q < nc; ++q) {
+            const double rel = c.lr_pn_h[q] / std::max(c.lr_pn_h[nc + q], 1e-300);
+            worst = std::isfinite(rel) ? std::max(worst, rel) : INFINITY;
+        }
+        c.lr_probe_worst = worst;
+        if (getenv("QPS_LR_TRACE"))
+            fprintf(stderr, "low-rank couplings: probe max ||(I - P P^*) C w2|| / ||C w2|| = %.3e (tol %.1e)\n",
+                    worst, probe_tol);
+        if (!(worst <= probe_tol)) return false;  // basis misses part of a coupling's range: dense reduction
     }
     return true;
 }
@@ -951,6 +1043,7 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
         flag.ensure(fa.size());
         flag.zero(s);
         lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
+        lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p, nullptr, s);
         std::vector<int> hf(fa.size());
         QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
         QPS_CUDA(cudaStreamSynchronize(s));
@@ -1231,6 +1324,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
     auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2; };
     std::vector<int> l0_orig;  // level-0 positions whose singular flags are checked at the end
+    bool rcond_pending = false;  // level-0 rcond flags on the side stream (c.ev_rcond)
     // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
     cudaEvent_t f0 = nullptr, f1 = nullptr;  // factor_ms of the phase times
     QPS_CUDA(cudaEventCreate(&f0));
@@ -1278,6 +1372,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }();
         if (separate) {
             lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
+            lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p, nullptr, s);
             check(orig);
             tmark("factor", 0, int(fa.size()));
             lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, s, c.ws);
@@ -1293,6 +1388,19 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }
         QPS_CUDA(cudaEventRecord(f1, s));
         nvtxRangePop();
+        if (!separate) {
+            // rcond of the level-0 U factors (left in Ad, untouched by the later
+            // levels) on the side stream, overlapping the latency-bound levels;
+            // checked with the singular flags at the end
+            QPS_CUDA(cudaStreamWaitEvent(c.side2, f1, 0));
+            c.rc_flag.ensure(npos);
+            QPS_CUDA(cudaMemsetAsync(c.rc_flag.p, 0, sizeof(int) * npos, c.side2));
+            lu_rcond_batched(nb, nb, nullptr, Ad, nb2, npos, kRcondMin, c.rc_flag.p, nullptr, c.side2);
+            c.rc_flag_h.ensure(npos);
+            QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, c.side2);
+            QPS_CUDA(cudaEventRecord(c.ev_rcond, c.side2));
+            rcond_pending = true;
+        }
         // y = D^{-1} f back into F (column 2r of every W_j)
         QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * nb, c.lr_W0.p + size_t(r2) * nb,
                                    sizeof(cplx) * nb * (r2 + 1), sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
@@ -1382,6 +1490,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             flag.ensure(cnt);
             flag.zero(s);
             lu_factor_batched(r2, r2, ca, cp, cd, flag.p, s, c.ws);
+            lu_rcond_batched(r2, r2, c.ws.ptrs.p, nullptr, 0, cnt, kRcondMin, flag.p, nullptr, s);
             check(orig);
             lu_solve_batched(r2, r2, ca, cp, cd, ci, r2, r2, s, c.ws);
         }
@@ -1468,9 +1577,14 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     {
         float fms = 0;
         QPS_CUDA(cudaEventSynchronize(f1));
+        if (rcond_pending) {  // the next use of Ad on the main stream waits for the side stream
+            QPS_CUDA(cudaStreamWaitEvent(s, c.ev_rcond, 0));
+            QPS_CUDA(cudaEventSynchronize(c.ev_rcond));
+        }
         int worst = -1;
         for (size_t q = 0; q < l0_orig.size(); ++q)
-            if (c.bcr_flag_h[q] && (worst < 0 || l0_orig[q] < worst)) worst = l0_orig[q];
+            if ((c.bcr_flag_h[q] || (rcond_pending && c.rc_flag_h[q])) && (worst < 0 || l0_orig[q] < worst))
+                worst = l0_orig[q];
         if (worst >= 0) {
             QPS_CUDA(cudaEventDestroy(f0));
             QPS_CUDA(cudaEventDestroy(f1));

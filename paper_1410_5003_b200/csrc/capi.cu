@@ -129,6 +129,7 @@ qps_ctx* qps_create(int device) {
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fork, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fill, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_sample, cudaEventDisableTiming));
+        QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_rcond, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreate(&h->c.ev0));
         QPS_CUDA(cudaEventCreate(&h->c.ev1));
         upload_hankel_tables();
@@ -152,7 +153,7 @@ void qps_destroy(qps_ctx* h) {
     cudaStream_t s = h->c.stream, s2 = h->c.side, s3 = h->c.side2;
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
-    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_geo})
+    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_rcond, h->c.ev_geo})
         if (e) cudaEventDestroy(e);
     delete h;
     if (s) cudaStreamDestroy(s);
@@ -537,6 +538,14 @@ int qps_fill_evals(const qps_ctx* h, uint64_t* reference, uint64_t* performed) {
 int qps_get_phase_times(const qps_ctx* h, qps_phase_times* t) {
     if (!h || !t) return QPS_ERR_USAGE;
     *t = h->c.times;
+    return QPS_OK;
+}
+
+int qps_solver_diagnostics(const qps_ctx* h, qps_solver_diag* d) {
+    if (!h || !d) return QPS_ERR_USAGE;
+    d->bcr_path = h->c.bcr_path;
+    d->lr_rank_max = h->c.lr_rank_max;
+    d->lr_probe_worst = h->c.lr_probe_worst;
     return QPS_OK;
 }
 

@@ -1,6 +1,7 @@
 // Solver context: everything one qps_ctx owns on host and device.
 #pragma once
 #include <chrono>
+#include <exception>
 
 #include <array>
 #include <string>
@@ -119,6 +120,7 @@ struct Ctx {
     cudaStream_t side = nullptr;  // second stream: work independent of the main stream (corner least squares)
     cudaStream_t side2 = nullptr; // third stream: the low-rank sample overlapping the Schur least squares
     cudaEvent_t ev_fork = nullptr, ev_fill = nullptr, ev_sample = nullptr;
+    cudaEvent_t ev_rcond = nullptr;  // level-0 rcond estimates done (side2)
 
     StackDesc stack;
     Numerics num;
@@ -172,7 +174,17 @@ struct Ctx {
     bool geo_h_ev_pending = false;
     cudaEvent_t ev_geo = nullptr;
     HBuf<int> lr_rank_h;               // sample ranks, read back without a stream sync
+    DBuf<cplx> lr_G2, lr_Yc;           // probe projections P^* Y2; packed samples (CPQR-only path)
+    DBuf<double> lr_pn, lr_parts;      // probe residual / probe norms per coupling; reduction scratch
+    HBuf<double> lr_pn_h;
+    double lr_probe_worst = 0;         // last compression: max ||(I - P P^*) C w2|| / ||C w2||
+    int lr_rank_max = 0;               // last compression: largest sample rank
+    int bcr_path = 0;                  // last block solve: 0 dense, 1 Woodbury low-rank, 2 low-rank per-level LU
     HBuf<int> bcr_flag_h;              // singular-factor flags of the level-0 batch (checked at the end)
+    DBuf<int> rc_flag;                 // rcond <= 1e-15 flags of the level-0 factors (tridiag.hpp:36-40)
+    DBuf<cplx> bcr_copy, bcr_cdinv;    // dense reduction: factored copies of the even blocks (rcond test)
+    DBuf<int> bcr_cpiv;
+    HBuf<int> rc_flag_h;
     // coupling Schur updates A'_{j,j+1} = A - B X left to the compression
     // (one-shot path): [system][j] tasks of A_super and A_sub
     std::vector<GemmTask> coupling_sup, coupling_sub;
@@ -264,11 +276,15 @@ struct Timer {
     Ctx& c;
     double* slot;
     Timer(Ctx& c_, double* s) : c(c_), slot(s) { QPS_CUDA(cudaEventRecord(c.ev0, c.stream)); }
-    ~Timer() noexcept(false) {
-        QPS_CUDA(cudaEventRecord(c.ev1, c.stream));
-        QPS_CUDA(cudaEventSynchronize(c.ev1));
+    // noexcept: a destructor that threw while an exception (e.g. a sticky
+    // CUDA error) is already unwinding would std::terminate the host process;
+    // the C-ABI promises status codes, so timing is skipped on that path.
+    ~Timer() noexcept {
+        if (std::uncaught_exceptions() > 0) return;
         float ms = 0;
-        QPS_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+        if (cudaEventRecord(c.ev1, c.stream) != cudaSuccess || cudaEventSynchronize(c.ev1) != cudaSuccess ||
+            cudaEventElapsedTime(&ms, c.ev0, c.ev1) != cudaSuccess)
+            return;  // the next checked CUDA call reports the error
         *slot = ms;
     }
 };

@@ -1889,6 +1889,231 @@ __global__ void __launch_bounds__(256) zgemv_kernel(int M, cplx alpha, cplx beta
 }
 
 // ---- FP64 peak microbenchmarks ----
+// ---------------------------------------------------------------------------
+// Reciprocal condition estimate of LU factors (the reference's
+// PartialPivLU::rcond() <= 1e-15 -> SolverError(layer) test, tridiag.hpp:36-40).
+// The block cyclic reduction never forms the Thomas pivots the reference tests,
+// so every block it factors -- the level-0 diagonal blocks, the dense
+// reduction's pivots at every level -- is checked on its U factor: LAPACK
+// xTRCON's estimate rcond(U) = 1 / (||U||_1 est(||U^{-1}||_1)), est by the
+// Hager/Higham 1-norm estimator in LAPACK zlacn2's iteration (at most 5
+// rounds of U^{-1} x / U^{-H} sign(y), then the alternating-sign test vector).
+// With partial pivoting L is unit lower with |l_ij| <= 1, so rcond(U) tracks
+// rcond(A) and is exactly 0 when a pivot is 0.  One CTA per block; x lives in
+// shared memory; U is swept by 32-column tiles (the diagonal triangle solved
+// by one warp from a shared-memory copy, the rest as a coalesced block GEMV).
+// ---------------------------------------------------------------------------
+constexpr int kRcT = 256, kRcW = 32;
+
+__device__ __forceinline__ cplx csign(cplx v) {  // v / |v| (1 for v = 0), zlacn2
+    const double a = hypot(v.re, v.im);
+    return a > 0.0 ? cplx{v.re / a, v.im / a} : cplx{1.0, 0.0};
+}
+
+__device__ double rc_block_sum(double v, double* red) {  // sum over the CTA
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0;
+    for (int w = 0; w < kRcT / 32; ++w) s += red[w];
+    return s;
+}
+
+__device__ int rc_block_argmax(const cplx* x, int n, double* red, int* redi) {  // first max |x_i| (izmax1)
+    double v = -1.0;
+    int idx = 1 << 30;
+    for (int i = threadIdx.x; i < n; i += kRcT) {
+        const double a = hypot(x[i].re, x[i].im);
+        if (a > v) { v = a; idx = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = v; redi[threadIdx.x >> 5] = idx; }
+    __syncthreads();
+    double bv = red[0];
+    int bi = redi[0];
+    for (int w = 1; w < kRcT / 32; ++w)
+        if (red[w] > bv || (red[w] == bv && redi[w] < bi)) { bv = red[w]; bi = redi[w]; }
+    return bi;
+}
+
+// x <- U^{-1} x (backward, 32-column tiles from the bottom)
+__device__ void rc_solve_u(const cplx* __restrict__ U, int n, int ld, cplx* x, cplx* tile) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k0 = ((n - 1) / kRcW) * kRcW; k0 >= 0; k0 -= kRcW) {
+        const int w = min(kRcW, n - k0);
+        for (int e = tid; e < kRcW * kRcW; e += kRcT) {
+            const int r = e % kRcW, c = e / kRcW;
+            if (r < w && c < w) tile[c * (kRcW + 1) + r] = U[size_t(k0 + c) * ld + k0 + r];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // the 32 pivots' reciprocals in parallel: the chain below only multiplies
+            const cplx dinv = lane < w ? cdiv(cplx{1.0, 0.0}, tile[lane * (kRcW + 1) + lane]) : cplx{0, 0};
+            cplx xi = lane < w ? x[k0 + lane] : cplx{0, 0};
+            for (int k = w - 1; k >= 0; --k) {
+                if (lane == k) xi = cmul(xi, dinv);
+                const cplx xk{__shfl_sync(0xffffffffu, xi.re, k), __shfl_sync(0xffffffffu, xi.im, k)};
+                if (lane < k) {
+                    const cplx u = tile[k * (kRcW + 1) + lane];
+                    xi.re -= u.re * xk.re - u.im * xk.im;
+                    xi.im -= u.re * xk.im + u.im * xk.re;
+                }
+            }
+            if (lane < w) x[k0 + lane] = xi;
+        }
+        __syncthreads();
+        for (int i = tid; i < k0; i += kRcT) {  // x[0:k0] -= U[0:k0, k0:k0+w] x[k0:k0+w]
+            double ar = 0, ai = 0;
+            for (int c = 0; c < w; ++c) {
+                const cplx u = U[size_t(k0 + c) * ld + i], xc = x[k0 + c];
+                ar += u.re * xc.re - u.im * xc.im;
+                ai += u.re * xc.im + u.im * xc.re;
+            }
+            x[i].re -= ar;
+            x[i].im -= ai;
+        }
+        __syncthreads();
+    }
+}
+
+// x <- U^{-H} x (forward, 32-column tiles from the top)
+__device__ void rc_solve_uh(const cplx* __restrict__ U, int n, int ld, cplx* x, cplx* tile) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k0 = 0; k0 < n; k0 += kRcW) {
+        const int w = min(kRcW, n - k0);
+        for (int c = warp; c < w; c += kRcT / 32) {  // x[k0 + c] -= U[0:k0, k0 + c]^H x[0:k0]
+            double ar = 0, ai = 0;
+            const cplx* col = U + size_t(k0 + c) * ld;
+            for (int i = lane; i < k0; i += 32) {
+                const cplx u = col[i], xi = x[i];
+                ar += u.re * xi.re + u.im * xi.im;
+                ai += u.re * xi.im - u.im * xi.re;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                ai += __shfl_xor_sync(0xffffffffu, ai, o);
+            }
+            if (lane == 0) {
+                x[k0 + c].re -= ar;
+                x[k0 + c].im -= ai;
+            }
+        }
+        for (int e = tid; e < kRcW * kRcW; e += kRcT) {
+            const int r = e % kRcW, c = e / kRcW;
+            if (r < w && c < w) tile[c * (kRcW + 1) + r] = U[size_t(k0 + c) * ld + k0 + r];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const cplx dinv = lane < w ? cconj(cdiv(cplx{1.0, 0.0}, tile[lane * (kRcW + 1) + lane])) : cplx{0, 0};
+            cplx xk = lane < w ? x[k0 + lane] : cplx{0, 0};
+            for (int i = 0; i < w; ++i) {
+                if (lane == i) xk = cmul(xk, dinv);
+                const cplx xi{__shfl_sync(0xffffffffu, xk.re, i), __shfl_sync(0xffffffffu, xk.im, i)};
+                if (lane > i && lane < w) {  // x_k -= conj(u_ik) x_i
+                    const cplx u = tile[lane * (kRcW + 1) + i];
+                    xk.re -= u.re * xi.re + u.im * xi.im;
+                    xk.im -= u.re * xi.im - u.im * xi.re;
+                }
+            }
+            if (lane < w) x[k0 + lane] = xk;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kRcT) lu_rcond_kernel(int n, int ld, const cplx* const* __restrict__ Ap,
+                                                        const cplx* __restrict__ base, size_t stride, double th,
+                                                        int* __restrict__ flag, double* __restrict__ rcond) {
+    extern __shared__ cplx rc_sm[];
+    cplx* x = rc_sm;      // n
+    cplx* tile = x + n;   // 32 x 33
+    __shared__ double red[kRcT / 32];
+    __shared__ int redi[kRcT / 32];
+    __shared__ int s_zero;
+    const cplx* U = Ap ? Ap[blockIdx.x] : base + size_t(blockIdx.x) * stride;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // ||U||_1 (max column sum of the upper triangle) and exact zero pivots
+    if (tid == 0) s_zero = 0;
+    double cmax = 0;
+    for (int j = warp; j < n; j += kRcT / 32) {
+        double sum = 0;
+        for (int i = lane; i <= j; i += 32) {
+            const cplx u = U[size_t(j) * ld + i];
+            sum += hypot(u.re, u.im);
+        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        cmax = fmax(cmax, sum);
+        if (lane == 0) {
+            const cplx d = U[size_t(j) * ld + j];
+            if (d.re == 0.0 && d.im == 0.0) s_zero = 1;
+        }
+    }
+    __syncthreads();
+    if (lane == 0) red[warp] = cmax;
+    __syncthreads();
+    double anorm = 0;
+    for (int w = 0; w < kRcT / 32; ++w) anorm = fmax(anorm, red[w]);
+    double rc = 0.0;
+    if (!s_zero && anorm > 0.0 && isfinite(anorm)) {
+        // zlacn2: x = e / n; y = U^{-1} x
+        for (int i = tid; i < n; i += kRcT) x[i] = cplx{1.0 / n, 0.0};
+        __syncthreads();
+        rc_solve_u(U, n, ld, x, tile);
+        double est = 0;
+        {
+            double a = 0;
+            for (int i = tid; i < n; i += kRcT) a += hypot(x[i].re, x[i].im);
+            est = rc_block_sum(a, red);
+        }
+        if (n > 1) {
+            for (int i = tid; i < n; i += kRcT) x[i] = csign(x[i]);
+            __syncthreads();
+            rc_solve_uh(U, n, ld, x, tile);
+            int j = rc_block_argmax(x, n, red, redi);
+            for (int iter = 2;; ++iter) {
+                __syncthreads();
+                for (int i = tid; i < n; i += kRcT) x[i] = cplx{i == j ? 1.0 : 0.0, 0.0};
+                __syncthreads();
+                rc_solve_u(U, n, ld, x, tile);
+                const double estold = est;
+                double a = 0;
+                for (int i = tid; i < n; i += kRcT) a += hypot(x[i].re, x[i].im);
+                est = rc_block_sum(a, red);
+                if (!(est > estold)) { est = fmax(est, estold); break; }
+                __syncthreads();
+                for (int i = tid; i < n; i += kRcT) x[i] = csign(x[i]);
+                __syncthreads();
+                rc_solve_uh(U, n, ld, x, tile);
+                const int jlast = j;
+                const double xl = hypot(x[jlast].re, x[jlast].im);
+                j = rc_block_argmax(x, n, red, redi);
+                const double xj = hypot(x[j].re, x[j].im);
+                if (!(xl != xj && iter < 5)) break;
+            }
+            // alternating-sign test vector x_i = (-1)^i (1 + i / (n - 1))
+            __syncthreads();
+            for (int i = tid; i < n; i += kRcT) x[i] = cplx{((i & 1) ? -1.0 : 1.0) * (1.0 + double(i) / (n - 1)), 0.0};
+            __syncthreads();
+            rc_solve_u(U, n, ld, x, tile);
+            double a = 0;
+            for (int i = tid; i < n; i += kRcT) a += hypot(x[i].re, x[i].im);
+            const double temp = 2.0 * rc_block_sum(a, red) / (3.0 * n);
+            est = fmax(est, temp);
+        }
+        rc = (est > 0.0 && isfinite(est)) ? (1.0 / anorm) / est : 0.0;
+    }
+    if (tid == 0) {
+        if (rcond) rcond[blockIdx.x] = rc;
+        if (!(rc > th)) flag[blockIdx.x] = 1;
+    }
+}
+
 __global__ void dfma_peak_kernel(double* out, int iters) {
     double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
            a7 = a0 + 7;
@@ -2638,6 +2863,21 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
     const int nblk = (n + kTB - 1) / kTB;
     lower(0, nblk);
     upper(0, nblk);
+}
+
+void lu_rcond_batched(int n, int ld, cplx* const* d_ptrs, const cplx* base, size_t stride, int count, double th,
+                      int* d_flag, double* d_rcond, cudaStream_t s) {
+    if (count == 0 || n == 0) return;
+    const size_t sm = (size_t(n) + kRcW * (kRcW + 1)) * sizeof(cplx);
+    static size_t attr = 48 * 1024;
+    if (sm > attr) {
+        QPS_CUDA(cudaFuncSetAttribute(lu_rcond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        attr = sm;
+    }
+    // ~6 triangular solves over U: 6 n^2 / 2 complex reads per block
+    ProfScope ps("lu_rcond", s, 0.0, 16.0 * 3.0 * count * double(n) * n);
+    { QPS_NOTE_LAUNCH(); lu_rcond_kernel<<<count, kRcT, sm, s>>>(n, ld, d_ptrs, base, stride, th, d_flag, d_rcond); }
+    QPS_CUDA(cudaGetLastError());
 }
 
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {

@@ -83,6 +83,16 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& A, const std::vec
                       const std::vector<cplx*>& Dinv, const std::vector<cplx*>& B, int ldb, int nrhs,
                       cudaStream_t s, Workspace& ws);
 
+// Reciprocal condition estimate of LU factors, the reference's
+// PartialPivLU::rcond() test (tridiag.hpp:36-40): per block b (d_ptrs[b], or
+// base + b * stride when d_ptrs is null) rcond(U_b) = 1 / (||U_b||_1
+// est ||U_b^{-1}||_1) with LAPACK zlacn2's Hager/Higham estimator on the U
+// factor left in the upper triangle; d_flag[b] = 1 when !(rcond > th);
+// d_rcond (may be null) receives the estimates.
+void lu_rcond_batched(int n, int ld, cplx* const* d_ptrs, const cplx* base, size_t stride, int count, double th,
+                      int* d_flag, double* d_rcond, cudaStream_t s);
+constexpr double kRcondMin = 1e-15;  // tridiag.hpp:36
+
 // ---- small utilities -------------------------------------------------------
 // per problem max |X_ij| over an m x n block (ld), count problems with stride
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s);

@@ -838,7 +838,11 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         const char* e = getenv("QPS_BCR");
         return e && !strcmp(e, "lrdirect");
     }();
+    c.lr_rank_max = 0;
+    c.lr_probe_worst = 0;
+    c.bcr_path = 0;
     if (!dense_only && lr_compress(c, Au, Al)) {
+        c.bcr_path = lr_direct ? 2 : 1;
         if (lr_direct) bcr_solve_lr(c, Ad);
         else bcr_solve_wb(c, Ad);
         c.couplings_deferred = false;
@@ -896,6 +900,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         flag.ensure(fa.size());
         flag.zero(s);
         lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
+        lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p, nullptr, s);
         std::vector<int> hf(fa.size());
         QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
         QPS_CUDA(cudaStreamSynchronize(s));
@@ -904,6 +909,32 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             if (hf[b] && (worst < 0 || orig[b] < worst)) worst = orig[b];
         if (worst >= 0) singular_error(worst);
     };
+    // The reference tests rcond of its Thomas pivots (tridiag.hpp:36-40), the
+    // first of which is A'_00 itself.  The reduction factors the odd positions
+    // unmodified at level 0 and updates the even ones first, so the original
+    // even blocks are checked on a factored copy: every diagonal block of the
+    // periodized system passes the rcond test, as on the Woodbury path.
+    if (I > 1) {
+        const int ne = (I + 1) / 2;
+        c.bcr_copy.ensure(size_t(ns) * ne * nb2);
+        c.bcr_cpiv.ensure(size_t(ns) * ne * nb);
+        c.bcr_cdinv.ensure(size_t(ns) * ne * dsz);
+        std::vector<cplx*> ea, ed;
+        std::vector<int*> ep;
+        std::vector<int> eo;
+        for (int a = 0; a < ns; ++a) {
+            copy_blocks(Ad + size_t(a) * D.sA(), nb, 2 * nb2, c.bcr_copy.p + size_t(a) * ne * nb2, nb, nb2, nb, nb, ne,
+                        s);
+            for (int q = 0; q < ne; ++q) {
+                const size_t b = size_t(a) * ne + q;
+                ea.push_back(c.bcr_copy.p + b * nb2);
+                ep.push_back(c.bcr_cpiv.p + b * nb);
+                ed.push_back(c.bcr_cdinv.p + b * dsz);
+                eo.push_back(2 * q);
+            }
+        }
+        factor(ea, ep, ed, eo);
+    }
     int lvl = 0;
     static const bool trace = getenv("QPS_BCR_TRACE") != nullptr;  // per-level timing to stderr (debug)
     auto tmark = [&](const char* what, int l, int cnt) {

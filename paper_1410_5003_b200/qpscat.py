@@ -103,6 +103,10 @@ class _Num(C.Structure):
                 ("grading_q", C.c_int), ("clearance", C.c_double), ("memory_budget", C.c_uint64)]
 
 
+class _Diag(C.Structure):
+    _fields_ = [("bcr_path", C.c_int), ("lr_rank_max", C.c_int), ("lr_probe_worst", C.c_double)]
+
+
 class _Times(C.Structure):
     _fields_ = [("fill_ms", C.c_double), ("assemble_ms", C.c_double), ("schur_ms", C.c_double),
                 ("solve_ms", C.c_double), ("recover_ms", C.c_double), ("total_ms", C.c_double),
@@ -194,6 +198,7 @@ def _bind(lib):
         "qps_download_block": (C.c_int, [vp, C.c_int, C.c_int, vp, P(C.c_int), P(C.c_int)]),
         "qps_fill_evals": (C.c_int, [vp, P(C.c_uint64), P(C.c_uint64)]),
         "qps_get_phase_times": (C.c_int, [vp, P(_Times)]),
+        "qps_solver_diagnostics": (C.c_int, [vp, P(_Diag)]),
         "qps_hankel01": (C.c_int, [vp, C.c_int, P(C.c_double), vp, vp]),
         "qps_measure_fp64_peaks": (C.c_int, [vp, P(C.c_double), P(C.c_double)]),
         "qps_prof_enable": (C.c_int, [vp, C.c_int]),
@@ -466,6 +471,14 @@ class Solver:
         t = _Times()
         self._check(self.lib.qps_get_phase_times(self.h, C.byref(t)))
         return {f: getattr(t, f) for f, _ in _Times._fields_}
+
+    def solver_diagnostics(self):
+        """How the last block solve ran: bcr_path (-1 reference Thomas, 0 dense
+        cyclic reduction, 1 low-rank Woodbury, 2 low-rank per-level LU),
+        lr_rank_max, lr_probe_worst (a-posteriori compression test)."""
+        d = _Diag()
+        self._check(self.lib.qps_solver_diagnostics(self.h, C.byref(d)))
+        return {f: getattr(d, f) for f, _ in _Diag._fields_}
 
     def hankel01(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -63,3 +63,24 @@ def gpu(product_lib):
     assert s.backend == "b200-cuda"
     yield s
     s.close()
+
+
+_PARITY = []
+
+
+@pytest.fixture()
+def parity_report():
+    """Record measured error vs the oracle's noise floor; printed in the
+    terminal summary (visible under -q) as 'name: quantity err (floor f)'."""
+    def rec(name, items):
+        _PARITY.append((name, items))
+    return rec
+
+
+def pytest_terminal_summary(terminalreporter):
+    if not _PARITY:
+        return
+    terminalreporter.section("parity vs oracle (measured error, oracle 1-ulp floor)")
+    for name, items in _PARITY:
+        parts = [f"{k} {v[0]:.3g} (floor {v[1]:.3g})" for k, v in items.items()]
+        terminalreporter.write_line(f"{name}: " + ", ".join(parts))
