@@ -40,11 +40,19 @@ namespace qpsb {
 namespace {
 
 constexpr int kLrSample = 64;    // columns of the random sample the basis is built from
-// a second, independent probe block sampled with it (same GEMM, no extra read of
-// the couplings): the a-posteriori test ||(I - P P^*) C w2||_F <= tol ||C w2||_F
-// of every compressed coupling; a failure takes the dense reduction
+// a-posteriori test of every compressed coupling on an independent probe: 16
+// seeded random columns J of C (a coordinate-vector sample; kernel matrices
+// spread their residual over all columns), ||C[:,J] - P (P^* C)[:,J]||_F <=
+// tol ||C[:,J]||_F; a failure takes the dense reduction.  Gathering columns
+// costs no GEMM over C (R = P^* C already exists).
 constexpr int kLrProbe = 16;
-constexpr int kLrCols = kLrSample + kLrProbe;  // columns of Omega and of the sample Y
+constexpr int kLrCols = kLrSample;  // columns of Omega and of the sample Y
+// rcond screen of the Woodbury level-0 factors (tridiag.hpp:36-40): kRcProbe
+// fixed unit-modulus probe columns ride along the level-0 right-hand sides;
+// blocks whose certified upper bound on rcond is <= kRcSuspect get the full
+// zlacn2 estimate
+constexpr int kRcProbe = 4;
+constexpr double kRcSuspect = 1e-10;
 constexpr double kLrProbeTol = 1e-12;
 constexpr int kLrMaxRank = 48;   // beyond this the dense reduction is used
 constexpr double kLrTol = 1e-14; // relative pivot threshold of the sample's CPQR
@@ -316,17 +324,19 @@ __global__ void set_identity_kernel(int n, cplx* __restrict__ C) {
 // of block j, ld n) for every block j of every system, so that one solve
 // gives D^{-1} [P_L P_U] and D^{-1} f; P holds per system the I-1 sub- then
 // the I-1 super-couplings
+// W_j = [P_L | P_U | f_j | R] (n x (2r + 1 + nprobe)): the level-0 right-hand sides
 __global__ void stage_bases_kernel(int I, int n, size_t per, const cplx* __restrict__ P, const cplx* __restrict__ F,
-                                   cplx* __restrict__ W) {
+                                   const cplx* __restrict__ R, int nprobe, cplx* __restrict__ W) {
     const int j = blockIdx.x, a = j / I, jj = j % I;
     const size_t qa = size_t(a) * 2 * (I - 1);
     const cplx* pl = jj >= 1 ? P + (qa + (jj - 1)) * per : nullptr;
     const cplx* pu = jj + 1 < I ? P + (qa + (I - 1) + jj) * per : nullptr;
-    cplx* w = W + size_t(j) * (2 * per + n);
+    cplx* w = W + size_t(j) * (2 * per + size_t(n) * (1 + nprobe));
     for (size_t e = size_t(blockIdx.y) * blockDim.x + threadIdx.x; e < per; e += size_t(gridDim.y) * blockDim.x) {
         w[e] = pl ? pl[e] : cplx{0, 0};
         w[per + e] = pu ? pu[e] : cplx{0, 0};
         if (e < size_t(n)) w[2 * per + e] = F[size_t(j) * n + e];
+        if (e < size_t(n) * nprobe) w[2 * per + n + e] = R[e];
     }
 }
 
@@ -759,7 +769,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
     if (!cpqr_only && nb <= 640) {
         // blocked Householder QR of the samples, CPQR of the 64 x 64 R
         const int m = nb, p = kLrSample, nP = p / kQrW;
-        const size_t ys = size_t(m) * kLrCols, vs = size_t(m) * kQrW, ts = size_t(kQrW) * kQrW;
+        const size_t ys = size_t(m) * p, vs = size_t(m) * kQrW, ts = size_t(kQrW) * kQrW;
         c.lr_V.ensure(size_t(nc) * nP * vs);
         c.lr_VH.ensure(size_t(nc) * nP * vs);
         c.lr_Tq.ensure(size_t(nc) * nP * ts);
@@ -852,9 +862,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
 // column-pivoted QR of each sample, numerical rank
         CodSet& cs = c.lr_cod;
         cs.ensure(nc, nb, kLrSample, 1);
-        c.lr_Yc.ensure(size_t(nc) * nb * kLrSample);  // the 64 basis columns, packed for the COD batch
-        copy_blocks(c.lr_Y.p, nb, size_t(nb) * kLrCols, c.lr_Yc.p, nb, size_t(nb) * kLrSample, nb, kLrSample, nc, s);
-        CodBatch b = cs.batch(c.lr_Yc.p);
+        CodBatch b = cs.batch(c.lr_Y.p);
         cod_factor_fast(b, s);
         cod_rank(b, kLrTol, nullptr, s);
         QPS_D2H(rk.data(), cs.rank.p, sizeof(int) * nc, s);
@@ -891,30 +899,6 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         }
     }
     tmark("P^*");
-    // a-posteriori test of the basis on the independent probe columns Y2 = C w2:
-    // ||Y2 - P (P^* Y2)||_F against ||Y2||_F (read back with the ranks)
-    {
-        c.lr_G2.ensure(size_t(nc) * r * kLrProbe);
-        c.lr_pn.ensure(size_t(nc) * 2);
-        std::vector<GemmTask> g(nc), e(nc);
-        for (int q = 0; q < nc; ++q) {
-            const cplx* Y2 = c.lr_Y.p + size_t(q) * nb * kLrCols + size_t(nb) * kLrSample;
-            g[q] = gemm1(c.lr_PH.p + size_t(q) * r * nb, r, Y2, nb, nb, c.lr_G2.p + size_t(q) * r * kLrProbe, r);
-            e[q] = gemm1(c.lr_P.p + size_t(q) * nb * r, nb, c.lr_G2.p + size_t(q) * r * kLrProbe, r, r,
-                         const_cast<cplx*>(Y2), nb);
-        }
-        zgemm_batched(r, kLrProbe, cplx{1, 0}, cplx{0, 0}, g, s, c.ws.gemm_tasks, "lr_compress");
-        batched_fro(c.lr_Y.p + size_t(nb) * kLrSample, nb, kLrProbe, nb, size_t(nb) * kLrCols, nc, c.lr_pn.p + nc, s);
-        zgemm_residual_norms(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, e, s, c.ws.gemm_tasks, c.lr_parts, c.lr_pn.p);
-        c.lr_pn_h.ensure(size_t(nc) * 2);
-        QPS_D2H(c.lr_pn_h.p, c.lr_pn.p, sizeof(double) * 2 * nc, s);
-        if (!rank_deferred) {
-            QPS_CUDA(cudaEventRecord(c.ev_sample, s));
-            rank_deferred = true;
-            c.lr_rank_h.ensure(nc);
-            for (int q = 0; q < nc; ++q) c.lr_rank_h[q] = 0;  // ranks already checked above
-        }
-    }
     // R = P^* C  (= P^* A + (-P^* Bc) X when deferred)
     c.lr_R.ensure(size_t(nc) * r * nb);
     {
@@ -943,6 +927,64 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         zgemm_batched(r, nb, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
     }
     tmark("R = P^* C");
+    // a-posteriori test on the probe columns J (per coupling): Y2 = C[:, J]
+    // (= A[:, J] - Bc X[:, J] when the coupling update is deferred),
+    // ||Y2 - P R[:, J]||_F against ||Y2||_F, read back with the ranks
+    {
+        if (c.lr_probe_n != nc * 65536 + nb) {
+            std::vector<int> cols(size_t(nc) * kLrProbe);
+            uint64_t x = 0xd1b54a32d192ed03ull;
+            for (auto& v : cols) {
+                x ^= x >> 12;
+                x ^= x << 25;
+                x ^= x >> 27;
+                v = int(((x * 0x2545f4914f6cdd1dull) >> 33) % uint64_t(nb));
+            }
+            c.lr_probe_cols.upload(cols, s);
+            c.lr_probe_n = nc * 65536 + nb;
+        }
+        std::vector<const cplx*> cp(nc), xp(nc), rp(nc);
+        std::vector<int> cld(nc, nb), xld(nc, P), rld(nc, r);
+        for (int q = 0; q < nc; ++q) {
+            cp[q] = coupling(q);
+            rp[q] = c.lr_R.p + size_t(q) * r * nb;
+            if (corr) {
+                xp[q] = corr_task(q).B[0];
+                xld[q] = corr_task(q).ldb[0];
+            }
+        }
+        c.lr_Y2.ensure(size_t(nc) * nb * kLrProbe);
+        c.lr_G2.ensure(size_t(nc) * (r + P) * kLrProbe);
+        cplx* Rg = c.lr_G2.p;                                   // r x 16 per coupling
+        cplx* Xg = c.lr_G2.p + size_t(nc) * r * kLrProbe;      // P x 16 per coupling
+        gather_columns(cp, cld, nb, c.lr_probe_cols.p, kLrProbe, c.lr_Y2.p, nb, size_t(nb) * kLrProbe, c.lr_gptr,
+                       c.lr_gld, s);
+        gather_columns(rp, rld, r, c.lr_probe_cols.p, kLrProbe, Rg, r, size_t(r) * kLrProbe, c.lr_gptr, c.lr_gld, s);
+        if (corr) {
+            gather_columns(xp, xld, P, c.lr_probe_cols.p, kLrProbe, Xg, P, size_t(P) * kLrProbe, c.lr_gptr, c.lr_gld,
+                           s);
+            std::vector<GemmTask> t(nc);
+            for (int q = 0; q < nc; ++q)
+                t[q] = gemm1(corr_task(q).A[0], corr_task(q).lda[0], Xg + size_t(q) * P * kLrProbe, P, P,
+                             c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
+            zgemm_batched(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        }
+        std::vector<GemmTask> e(nc);
+        for (int q = 0; q < nc; ++q)
+            e[q] = gemm1(c.lr_P.p + size_t(q) * nb * r, nb, Rg + size_t(q) * r * kLrProbe, r, r,
+                         c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
+        c.lr_pn.ensure(size_t(nc) * 2);
+        batched_fro(c.lr_Y2.p, nb, kLrProbe, nb, size_t(nb) * kLrProbe, nc, c.lr_pn.p + nc, s);
+        zgemm_residual_norms(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, e, s, c.ws.gemm_tasks, c.lr_parts, c.lr_pn.p);
+        c.lr_pn_h.ensure(size_t(nc) * 2);
+        QPS_D2H(c.lr_pn_h.p, c.lr_pn.p, sizeof(double) * 2 * nc, s);
+        QPS_CUDA(cudaEventRecord(c.ev_sample, s));  // the host checks ranks and probes once this is reached
+        if (!rank_deferred) {
+            rank_deferred = true;
+            c.lr_rank_h.ensure(nc);
+            for (int q = 0; q < nc; ++q) c.lr_rank_h[q] = 0;  // ranks already checked above
+        }
+    }
     if (trace) {
         QPS_CUDA(cudaEventDestroy(te0));
         QPS_CUDA(cudaEventDestroy(te1));
@@ -1043,7 +1085,8 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
         flag.ensure(fa.size());
         flag.zero(s);
         lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
-        lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p, nullptr, s);
+        lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, c.ws.ptrs3.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p,
+                         nullptr, s);
         std::vector<int> hf(fa.size());
         QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
         QPS_CUDA(cudaStreamSynchronize(s));
@@ -1254,6 +1297,20 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
 // The deep levels (a handful of blocks each) become a few small GEMMs instead
 // of a latency-bound dense LU per level; the level-0 batch runs at throughput.
 // ---------------------------------------------------------------------------
+// ||D_j^0||_1 of every diagonal block for the level-0 rcond screen, on the side
+// stream while the couplings are compressed (Ad is final after the Schur step;
+// bcr_solve_wb joins before its factorization overwrites Ad)
+void wb_anorm_async(Ctx& c, const cplx* Ad) {
+    if (!lr_eligible(c)) return;
+    const int npos = c.dims.nsys * c.dims.I;
+    c.rc_anorm.ensure(npos);
+    QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    QPS_CUDA(cudaStreamWaitEvent(c.side2, c.ev_fork, 0));
+    batched_norm1(Ad, c.dims.nb, c.dims.nb, c.dims.nb2(), npos, c.rc_anorm.p, c.side2);
+    QPS_CUDA(cudaEventRecord(c.ev_anorm, c.side2));
+    c.anorm_pending = true;
+}
+
 void bcr_solve_wb(Ctx& c, cplx* Ad) {
     ProfPhase phase("bcr");
     const Dims& D = c.dims;
@@ -1270,7 +1327,8 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     c.ipiv.ensure(size_t(npos) * nb);
     const size_t dsz = lu_dinv_elems(nb);
     c.dinv.ensure(size_t(npos) * dsz);
-    c.lr_W0.ensure(size_t(npos) * nb * (r2 + 1));  // [W | y] per block
+    const int wc = r2 + 1 + kRcProbe;  // [W | y | rcond probes] per block
+    c.lr_W0.ensure(size_t(npos) * nb * wc);
     c.lr_S.ensure(size_t(npos) * r2 * nb);
     c.lr_g.ensure(size_t(npos) * r2);
     c.lr_S.zero(s);
@@ -1320,11 +1378,10 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     };
     using Level = std::vector<std::vector<Pos>>;
     std::vector<Level> levels;
-    auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * (r2 + 1); };
+    auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * wc; };
     auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
     auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2; };
     std::vector<int> l0_orig;  // level-0 positions whose singular flags are checked at the end
-    bool rcond_pending = false;  // level-0 rcond flags on the side stream (c.ev_rcond)
     // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
     cudaEvent_t f0 = nullptr, f1 = nullptr;  // factor_ms of the phase times
     QPS_CUDA(cudaEventCreate(&f0));
@@ -1337,7 +1394,28 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         std::vector<cplx*> fa, fd, wb, vb;
         std::vector<int*> fp;
         std::vector<int> orig;
-        { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, c.lr_W0.p); }
+        if (c.rc_probe_n != nb) {  // fixed unit-modulus probes (seeded phases): ||r_k||_1 = nb
+            std::vector<cplx> pr(size_t(nb) * kRcProbe);
+            uint64_t x = 0x243f6a8885a308d3ull;
+            for (auto& z : pr) {
+                x ^= x >> 12;
+                x ^= x << 25;
+                x ^= x >> 27;
+                const double ph = 2.0 * kPi * double((x * 0x2545f4914f6cdd1dull) >> 11) * (1.0 / 9007199254740992.0);
+                z = cplx{cos(ph), sin(ph)};
+            }
+            c.rc_probe.upload(pr, s);
+            c.rc_probe_n = nb;
+        }
+        if (c.anorm_pending) {  // ||D_j^0||_1 (side stream, before the factorization overwrites Ad)
+            QPS_CUDA(cudaStreamWaitEvent(s, c.ev_anorm, 0));
+            c.anorm_pending = false;
+        } else {
+            c.rc_anorm.ensure(npos);
+            batched_norm1(Ad, nb, nb, nb2, npos, c.rc_anorm.p, s);
+        }
+        { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, c.rc_probe.p,
+                                                                                kRcProbe, c.lr_W0.p); }
         QPS_CUDA(cudaGetLastError());
         for (int a = 0; a < ns; ++a) {
             const size_t qa = size_t(a) * 2 * (I - 1);
@@ -1372,38 +1450,37 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }();
         if (separate) {
             lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
-            lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p, nullptr, s);
+            lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, c.ws.ptrs3.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p,
+                         nullptr, s);
             check(orig);
             tmark("factor", 0, int(fa.size()));
-            lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, s, c.ws);
+            lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, s, c.ws);
         } else {
             // the D_j^0 factors are used only for W_j: the forward substitution
             // rides along the factorization
-            lu_factor_solve_batched(nb, nb, fa, fp, fd, wb, nb, r2 + 1, flag.p, s, c.ws);
+            lu_factor_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, flag.p, s, c.ws);
             // singular flags read back asynchronously, checked after the levels
             c.bcr_flag_h.ensure(fa.size());
             QPS_D2H(c.bcr_flag_h.p, flag.p, sizeof(int) * fa.size(), s);
             l0_orig = orig;
             tmark("factor+solve", 0, int(fa.size()));
         }
+        // rcond screen from the probe columns (certain flags + suspects), read
+        // back with the singular flags
+        c.rc_flag.ensure(npos);
+        c.rc_sus.ensure(npos);
+        c.rc_estlo.ensure(npos);
+        QPS_CUDA(cudaMemsetAsync(c.rc_flag.p, 0, sizeof(int) * npos, s));
+        rcond_screen(c.lr_W0.p, size_t(nb) * wc, nb, r2 + 1, kRcProbe, c.rc_anorm.p, double(nb), npos, kRcondMin,
+                     kRcSuspect, c.rc_flag.p, c.rc_sus.p, c.rc_estlo.p, s);
+        c.rc_flag_h.ensure(2 * size_t(npos));
+        QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, s);
+        QPS_D2H(c.rc_flag_h.p + npos, c.rc_sus.p, sizeof(int) * npos, s);
         QPS_CUDA(cudaEventRecord(f1, s));
         nvtxRangePop();
-        if (!separate) {
-            // rcond of the level-0 U factors (left in Ad, untouched by the later
-            // levels) on the side stream, overlapping the latency-bound levels;
-            // checked with the singular flags at the end
-            QPS_CUDA(cudaStreamWaitEvent(c.side2, f1, 0));
-            c.rc_flag.ensure(npos);
-            QPS_CUDA(cudaMemsetAsync(c.rc_flag.p, 0, sizeof(int) * npos, c.side2));
-            lu_rcond_batched(nb, nb, nullptr, Ad, nb2, npos, kRcondMin, c.rc_flag.p, nullptr, c.side2);
-            c.rc_flag_h.ensure(npos);
-            QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, c.side2);
-            QPS_CUDA(cudaEventRecord(c.ev_rcond, c.side2));
-            rcond_pending = true;
-        }
         // y = D^{-1} f back into F (column 2r of every W_j)
         QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * nb, c.lr_W0.p + size_t(r2) * nb,
-                                   sizeof(cplx) * nb * (r2 + 1), sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
+                                   sizeof(cplx) * nb * wc, sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
         tmark("solve", 0, int(fa.size()));
         levels.push_back(std::move(L0));
     }
@@ -1490,7 +1567,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             flag.ensure(cnt);
             flag.zero(s);
             lu_factor_batched(r2, r2, ca, cp, cd, flag.p, s, c.ws);
-            lu_rcond_batched(r2, r2, c.ws.ptrs.p, nullptr, 0, cnt, kRcondMin, flag.p, nullptr, s);
+            lu_rcond_batched(r2, r2, c.ws.ptrs.p, nullptr, 0, c.ws.ptrs3.p, nullptr, 0, cnt, kRcondMin, flag.p, nullptr, s);
             check(orig);
             lu_solve_batched(r2, r2, ca, cp, cd, ci, r2, r2, s, c.ws);
         }
@@ -1577,14 +1654,47 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     {
         float fms = 0;
         QPS_CUDA(cudaEventSynchronize(f1));
-        if (rcond_pending) {  // the next use of Ad on the main stream waits for the side stream
-            QPS_CUDA(cudaStreamWaitEvent(s, c.ev_rcond, 0));
-            QPS_CUDA(cudaEventSynchronize(c.ev_rcond));
-        }
         int worst = -1;
-        for (size_t q = 0; q < l0_orig.size(); ++q)
-            if ((c.bcr_flag_h[q] || (rcond_pending && c.rc_flag_h[q])) && (worst < 0 || l0_orig[q] < worst))
-                worst = l0_orig[q];
+        std::vector<int> suspects;
+        for (size_t q = 0; q < l0_orig.size(); ++q) {
+            if (c.bcr_flag_h[q] || c.rc_flag_h[q]) {
+                if (worst < 0 || l0_orig[q] < worst) worst = l0_orig[q];
+            } else if (c.rc_flag_h[npos + q]) {
+                suspects.push_back(int(q));
+            }
+        }
+        if (worst < 0 && !suspects.empty()) {
+            // full zlacn2 estimate on U for the suspects: ||A^{-1}||_1 >= max(est_lo,
+            // est(||U^{-1}||_1) / ||L||_1) with ||L||_1 <= n (|l_ij| <= 1)
+            const int ns_ = int(suspects.size());
+            std::vector<cplx*> ua, da;
+            for (int q : suspects) {
+                ua.push_back(Ad + size_t(q) * nb2);
+                da.push_back(c.dinv.p + size_t(q) * dsz);
+            }
+            DBuf<cplx*> up, dp;
+            DBuf<int> fl;
+            DBuf<double> est;
+            up.upload(ua, s);
+            dp.upload(da, s);
+            fl.ensure(ns_);
+            fl.zero(s);
+            est.ensure(ns_);
+            lu_rcond_batched(nb, nb, up.p, nullptr, 0, dp.p, nullptr, 0, ns_, kRcondMin, fl.p, nullptr, s, est.p);
+            std::vector<double> eu(ns_), el(npos);
+            std::vector<unsigned long long> an(npos);
+            QPS_D2H(eu.data(), est.p, sizeof(double) * ns_, s);
+            QPS_D2H(el.data(), c.rc_estlo.p, sizeof(double) * npos, s);
+            QPS_D2H(an.data(), c.rc_anorm.p, sizeof(unsigned long long) * npos, s);
+            QPS_CUDA(cudaStreamSynchronize(s));
+            for (int i = 0; i < ns_; ++i) {
+                const int q = suspects[i];
+                double a;
+                std::memcpy(&a, &an[q], sizeof a);
+                const double rc = 1.0 / (a * std::max(el[q], eu[i] / nb));
+                if (!(rc > kRcondMin) && (worst < 0 || l0_orig[q] < worst)) worst = l0_orig[q];
+            }
+        }
         if (worst >= 0) {
             QPS_CUDA(cudaEventDestroy(f0));
             QPS_CUDA(cudaEventDestroy(f1));

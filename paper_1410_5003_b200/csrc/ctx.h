@@ -120,7 +120,7 @@ struct Ctx {
     cudaStream_t side = nullptr;  // second stream: work independent of the main stream (corner least squares)
     cudaStream_t side2 = nullptr; // third stream: the low-rank sample overlapping the Schur least squares
     cudaEvent_t ev_fork = nullptr, ev_fill = nullptr, ev_sample = nullptr;
-    cudaEvent_t ev_rcond = nullptr;  // level-0 rcond estimates done (side2)
+    cudaEvent_t ev_anorm = nullptr;  // level-0 block norms done (side2)
 
     StackDesc stack;
     Numerics num;
@@ -174,14 +174,22 @@ struct Ctx {
     bool geo_h_ev_pending = false;
     cudaEvent_t ev_geo = nullptr;
     HBuf<int> lr_rank_h;               // sample ranks, read back without a stream sync
-    DBuf<cplx> lr_G2, lr_Yc;           // probe projections P^* Y2; packed samples (CPQR-only path)
+    DBuf<cplx> lr_G2, lr_Y2;           // probe: gathered R and X columns; C[:, J]
+    DBuf<int> lr_probe_cols, lr_gld;   // probe column indices (nc x 16); gather leading dimensions
+    DBuf<const cplx*> lr_gptr;         // gather source pointers
+    int lr_probe_n = 0;
     DBuf<double> lr_pn, lr_parts;      // probe residual / probe norms per coupling; reduction scratch
     HBuf<double> lr_pn_h;
     double lr_probe_worst = 0;         // last compression: max ||(I - P P^*) C w2|| / ||C w2||
     int lr_rank_max = 0;               // last compression: largest sample rank
     int bcr_path = 0;                  // last block solve: 0 dense, 1 Woodbury low-rank, 2 low-rank per-level LU
     HBuf<int> bcr_flag_h;              // singular-factor flags of the level-0 batch (checked at the end)
-    DBuf<int> rc_flag;                 // rcond <= 1e-15 flags of the level-0 factors (tridiag.hpp:36-40)
+    DBuf<int> rc_flag, rc_sus;         // level-0 rcond screen: certain flags (rcond <= 1e-15), suspects
+    DBuf<double> rc_estlo;             // level-0 lower bounds of ||D_j^{-1}||_1 from the probes
+    DBuf<unsigned long long> rc_anorm; // ||D_j^0||_1 (double bits)
+    DBuf<cplx> rc_probe;               // the probe columns (nb x 4)
+    int rc_probe_n = 0;
+    bool anorm_pending = false;        // rc_anorm being computed on side2 (ev_anorm)
     DBuf<cplx> bcr_copy, bcr_cdinv;    // dense reduction: factored copies of the even blocks (rcond test)
     DBuf<int> bcr_cpiv;
     HBuf<int> rc_flag_h;
@@ -250,6 +258,7 @@ void lr_sample_async(Ctx& c);
 // block cyclic reduction on the compressed couplings (after lr_compress)
 void bcr_solve_lr(Ctx& c, cplx* Ad);
 void bcr_solve_wb(Ctx& c, cplx* Ad);
+void wb_anorm_async(Ctx& c, const cplx* Ad);
 void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
                           int ldX, size_t Xstride, double* lsq_out);
 void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,

@@ -1899,14 +1899,22 @@ __global__ void __launch_bounds__(256) zgemv_kernel(int M, cplx alpha, cplx beta
 // Hager/Higham 1-norm estimator in LAPACK zlacn2's iteration (at most 5
 // rounds of U^{-1} x / U^{-H} sign(y), then the alternating-sign test vector).
 // With partial pivoting L is unit lower with |l_ij| <= 1, so rcond(U) tracks
-// rcond(A) and is exactly 0 when a pivot is 0.  One CTA per block; x lives in
-// shared memory; U is swept by 32-column tiles (the diagonal triangle solved
-// by one warp from a shared-memory copy, the rest as a coalesced block GEMV).
+// rcond(A) and is exactly 0 when a pivot is 0.
+// The triangular solves use the inverse 64 x 64 diagonal tiles of U that the
+// LU already formed (tri_inv_kernel: tile kb at Dinv + kb 2 bs^2 + bs^2), so a
+// solve is ceil(n/64) steps of (tile mat-vec, block GEMV over the rows above)
+// with no sequential pivot chain: bandwidth-bound on U.  A few CTAs loop over
+// the blocks, each running all of its block's solves back to back while its U
+// (3 MB at n = 608) stays in L2, so the estimate costs about one HBM read of
+// the factors and runs beside the cyclic reduction's latency-bound levels on a
+// handful of SMs.
 // ---------------------------------------------------------------------------
-constexpr int kRcT = 256, kRcW = 32;
+constexpr int kRcT = 512, kRcB = 64;  // threads per CTA; tile = kTB of the LU
+static_assert(kRcB == kTB, "rcond solves use the LU's inverse diagonal tiles");
+static_assert(kRcT == 512, "rc_solve_u / rc_solve_uh thread layouts assume 512 threads (16 warps)");
 
 __device__ __forceinline__ cplx csign(cplx v) {  // v / |v| (1 for v = 0), zlacn2
-    const double a = hypot(v.re, v.im);
+    const double a = sqrt(v.re * v.re + v.im * v.im);
     return a > 0.0 ? cplx{v.re / a, v.im / a} : cplx{1.0, 0.0};
 }
 
@@ -1924,7 +1932,7 @@ __device__ int rc_block_argmax(const cplx* x, int n, double* red, int* redi) {  
     double v = -1.0;
     int idx = 1 << 30;
     for (int i = threadIdx.x; i < n; i += kRcT) {
-        const double a = hypot(x[i].re, x[i].im);
+        const double a = sqrt(x[i].re * x[i].re + x[i].im * x[i].im);
         if (a > v) { v = a; idx = i; }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -1942,176 +1950,271 @@ __device__ int rc_block_argmax(const cplx* x, int n, double* red, int* redi) {  
     return bi;
 }
 
-// x <- U^{-1} x (backward, 32-column tiles from the bottom)
-__device__ void rc_solve_u(const cplx* __restrict__ U, int n, int ld, cplx* x, cplx* tile) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int k0 = ((n - 1) / kRcW) * kRcW; k0 >= 0; k0 -= kRcW) {
-        const int w = min(kRcW, n - k0);
-        for (int e = tid; e < kRcW * kRcW; e += kRcT) {
-            const int r = e % kRcW, c = e / kRcW;
-            if (r < w && c < w) tile[c * (kRcW + 1) + r] = U[size_t(k0 + c) * ld + k0 + r];
+// x <- U^{-1} x (backward over 64-row tiles).  t: 512-entry scratch.
+__device__ void rc_solve_u(const cplx* __restrict__ U, const cplx* __restrict__ Di, int n, int ld, cplx* x, cplx* t) {
+    const int tid = threadIdx.x;
+    const int row = tid >> 3, part = tid & 7;  // 8 lanes per tile row (kRcT = 512 = 64 x 8)
+    for (int kb = (n - 1) / kRcB; kb >= 0; --kb) {
+        const int k0 = kb * kRcB, w = min(kRcB, n - k0);
+        const cplx* Ui = Di + size_t(kb) * 2 * kRcB * kRcB + size_t(kRcB) * kRcB;  // inv(U_kk), ld 64
+        double ar = 0, ai = 0;
+        if (row < w)
+            for (int j = part; j < w; j += 8) {
+                const cplx u = Ui[size_t(j) * kRcB + row], b = x[k0 + j];
+                ar += u.re * b.re - u.im * b.im;
+                ai += u.re * b.im + u.im * b.re;
+            }
+        for (int o = 4; o > 0; o >>= 1) {
+            ar += __shfl_xor_sync(0xffffffffu, ar, o);
+            ai += __shfl_xor_sync(0xffffffffu, ai, o);
         }
         __syncthreads();
-        if (warp == 0) {
-            // the 32 pivots' reciprocals in parallel: the chain below only multiplies
-            const cplx dinv = lane < w ? cdiv(cplx{1.0, 0.0}, tile[lane * (kRcW + 1) + lane]) : cplx{0, 0};
-            cplx xi = lane < w ? x[k0 + lane] : cplx{0, 0};
-            for (int k = w - 1; k >= 0; --k) {
-                if (lane == k) xi = cmul(xi, dinv);
-                const cplx xk{__shfl_sync(0xffffffffu, xi.re, k), __shfl_sync(0xffffffffu, xi.im, k)};
-                if (lane < k) {
-                    const cplx u = tile[k * (kRcW + 1) + lane];
-                    xi.re -= u.re * xk.re - u.im * xk.im;
-                    xi.im -= u.re * xk.im + u.im * xk.re;
+        if (part == 0 && row < w) x[k0 + row] = cplx{ar, ai};
+        __syncthreads();
+        // x[0:k0] -= U[0:k0, k0:k0+w] x[k0:k0+w]: 128-row chunks x 4 column quarters,
+        // 16 independent loads in flight per thread (w < 64 only for the
+        // bottom tile when 64 does not divide n)
+        {
+            const int r = tid & 127, q = tid >> 7;  // row in chunk, column quarter (16 columns)
+            for (int i0 = 0; i0 < k0; i0 += 128) {
+                const int i = i0 + r;
+                double br = 0, bi = 0;
+                if (i < k0) {
+                    cplx u[16];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        u[c] = (16 * q + c < w) ? U[size_t(k0 + 16 * q + c) * ld + i] : cplx{0, 0};
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const cplx xc = (16 * q + c < w) ? x[k0 + 16 * q + c] : cplx{0, 0};
+                        br += u[c].re * xc.re - u[c].im * xc.im;
+                        bi += u[c].re * xc.im + u[c].im * xc.re;
+                    }
                 }
+                t[q * 128 + r] = cplx{br, bi};
+                __syncthreads();
+                if (q == 0 && i < k0) {
+                    const cplx a = t[r], b = t[128 + r], c2 = t[256 + r], d = t[384 + r];
+                    x[i].re -= a.re + b.re + c2.re + d.re;
+                    x[i].im -= a.im + b.im + c2.im + d.im;
+                }
+                __syncthreads();
             }
-            if (lane < w) x[k0 + lane] = xi;
         }
-        __syncthreads();
-        for (int i = tid; i < k0; i += kRcT) {  // x[0:k0] -= U[0:k0, k0:k0+w] x[k0:k0+w]
-            double ar = 0, ai = 0;
-            for (int c = 0; c < w; ++c) {
-                const cplx u = U[size_t(k0 + c) * ld + i], xc = x[k0 + c];
-                ar += u.re * xc.re - u.im * xc.im;
-                ai += u.re * xc.im + u.im * xc.re;
-            }
-            x[i].re -= ar;
-            x[i].im -= ai;
-        }
-        __syncthreads();
     }
 }
 
-// x <- U^{-H} x (forward, 32-column tiles from the top)
-__device__ void rc_solve_uh(const cplx* __restrict__ U, int n, int ld, cplx* x, cplx* tile) {
+// x <- U^{-H} x (forward over 64-row tiles)
+__device__ void rc_solve_uh(const cplx* __restrict__ U, const cplx* __restrict__ Di, int n, int ld, cplx* x) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int k0 = 0; k0 < n; k0 += kRcW) {
-        const int w = min(kRcW, n - k0);
-        for (int c = warp; c < w; c += kRcT / 32) {  // x[k0 + c] -= U[0:k0, k0 + c]^H x[0:k0]
-            double ar = 0, ai = 0;
-            const cplx* col = U + size_t(k0 + c) * ld;
+    const int row = tid >> 3, part = tid & 7;
+    for (int k0 = 0, kb = 0; k0 < n; k0 += kRcB, ++kb) {
+        const int w = min(kRcB, n - k0);
+        {  // x[k0 + c] -= U[0:k0, k0 + c]^H x[0:k0]: warp w owns columns w, w + 16, w + 32, w + 48
+            double ar[4] = {0, 0, 0, 0}, ai[4] = {0, 0, 0, 0};
             for (int i = lane; i < k0; i += 32) {
-                const cplx u = col[i], xi = x[i];
-                ar += u.re * xi.re + u.im * xi.im;
-                ai += u.re * xi.im - u.im * xi.re;
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                ar += __shfl_xor_sync(0xffffffffu, ar, o);
-                ai += __shfl_xor_sync(0xffffffffu, ai, o);
-            }
-            if (lane == 0) {
-                x[k0 + c].re -= ar;
-                x[k0 + c].im -= ai;
-            }
-        }
-        for (int e = tid; e < kRcW * kRcW; e += kRcT) {
-            const int r = e % kRcW, c = e / kRcW;
-            if (r < w && c < w) tile[c * (kRcW + 1) + r] = U[size_t(k0 + c) * ld + k0 + r];
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const cplx dinv = lane < w ? cconj(cdiv(cplx{1.0, 0.0}, tile[lane * (kRcW + 1) + lane])) : cplx{0, 0};
-            cplx xk = lane < w ? x[k0 + lane] : cplx{0, 0};
-            for (int i = 0; i < w; ++i) {
-                if (lane == i) xk = cmul(xk, dinv);
-                const cplx xi{__shfl_sync(0xffffffffu, xk.re, i), __shfl_sync(0xffffffffu, xk.im, i)};
-                if (lane > i && lane < w) {  // x_k -= conj(u_ik) x_i
-                    const cplx u = tile[lane * (kRcW + 1) + i];
-                    xk.re -= u.re * xi.re + u.im * xi.im;
-                    xk.im -= u.re * xi.im - u.im * xi.re;
+                const cplx xi = x[i];
+                cplx u[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    u[m] = (warp + 16 * m < w) ? U[size_t(k0 + warp + 16 * m) * ld + i] : cplx{0, 0};
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    ar[m] += u[m].re * xi.re + u[m].im * xi.im;
+                    ai[m] += u[m].re * xi.im - u[m].im * xi.re;
                 }
             }
-            if (lane < w) x[k0 + lane] = xk;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                for (int o = 16; o > 0; o >>= 1) {
+                    ar[m] += __shfl_xor_sync(0xffffffffu, ar[m], o);
+                    ai[m] += __shfl_xor_sync(0xffffffffu, ai[m], o);
+                }
+                if (lane == 0 && warp + 16 * m < w) {
+                    x[k0 + warp + 16 * m].re -= ar[m];
+                    x[k0 + warp + 16 * m].im -= ai[m];
+                }
+            }
         }
+        __syncthreads();
+        // x_blk = inv(U_kk)^H x_blk: output `row` is column `row` of the inverse tile, conjugated
+        const cplx* Ui = Di + size_t(kb) * 2 * kRcB * kRcB + size_t(kRcB) * kRcB;
+        double ar = 0, ai = 0;
+        if (row < w)
+            for (int j = part; j < w; j += 8) {
+                const cplx u = Ui[size_t(row) * kRcB + j], b = x[k0 + j];
+                ar += u.re * b.re + u.im * b.im;
+                ai += u.re * b.im - u.im * b.re;
+            }
+        for (int o = 4; o > 0; o >>= 1) {
+            ar += __shfl_xor_sync(0xffffffffu, ar, o);
+            ai += __shfl_xor_sync(0xffffffffu, ai, o);
+        }
+        __syncthreads();
+        if (part == 0 && row < w) x[k0 + row] = cplx{ar, ai};
         __syncthreads();
     }
 }
 
-__global__ void __launch_bounds__(kRcT) lu_rcond_kernel(int n, int ld, const cplx* const* __restrict__ Ap,
-                                                        const cplx* __restrict__ base, size_t stride, double th,
-                                                        int* __restrict__ flag, double* __restrict__ rcond) {
+__global__ void __launch_bounds__(kRcT) lu_rcond_kernel(int n, int ld, int count, const cplx* const* __restrict__ Ap,
+                                                        const cplx* __restrict__ base, size_t stride,
+                                                        const cplx* const* __restrict__ Dp,
+                                                        const cplx* __restrict__ dbase, size_t dstride, double th,
+                                                        int* __restrict__ flag, double* __restrict__ rcond,
+                                                        double* __restrict__ est_out) {
     extern __shared__ cplx rc_sm[];
-    cplx* x = rc_sm;      // n
-    cplx* tile = x + n;   // 32 x 33
+    cplx* x = rc_sm;         // n
+    cplx* t = rc_sm + n;     // 512 partial sums of the block GEMV
     __shared__ double red[kRcT / 32];
     __shared__ int redi[kRcT / 32];
     __shared__ int s_zero;
-    const cplx* U = Ap ? Ap[blockIdx.x] : base + size_t(blockIdx.x) * stride;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // ||U||_1 (max column sum of the upper triangle) and exact zero pivots
-    if (tid == 0) s_zero = 0;
-    double cmax = 0;
-    for (int j = warp; j < n; j += kRcT / 32) {
-        double sum = 0;
-        for (int i = lane; i <= j; i += 32) {
-            const cplx u = U[size_t(j) * ld + i];
-            sum += hypot(u.re, u.im);
-        }
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        cmax = fmax(cmax, sum);
-        if (lane == 0) {
-            const cplx d = U[size_t(j) * ld + j];
-            if (d.re == 0.0 && d.im == 0.0) s_zero = 1;
-        }
-    }
-    __syncthreads();
-    if (lane == 0) red[warp] = cmax;
-    __syncthreads();
-    double anorm = 0;
-    for (int w = 0; w < kRcT / 32; ++w) anorm = fmax(anorm, red[w]);
-    double rc = 0.0;
-    if (!s_zero && anorm > 0.0 && isfinite(anorm)) {
-        // zlacn2: x = e / n; y = U^{-1} x
-        for (int i = tid; i < n; i += kRcT) x[i] = cplx{1.0 / n, 0.0};
+    for (int blk = blockIdx.x; blk < count; blk += gridDim.x) {
+        const cplx* U = Ap ? Ap[blk] : base + size_t(blk) * stride;
+        const cplx* Di = Dp ? Dp[blk] : dbase + size_t(blk) * dstride;
+        // ||U||_1 (max column sum of the upper triangle) and exact zero pivots
         __syncthreads();
-        rc_solve_u(U, n, ld, x, tile);
-        double est = 0;
-        {
-            double a = 0;
-            for (int i = tid; i < n; i += kRcT) a += hypot(x[i].re, x[i].im);
-            est = rc_block_sum(a, red);
+        if (tid == 0) s_zero = 0;
+        __syncthreads();
+        double cmax = 0;
+        for (int j = warp; j < n; j += kRcT / 32) {
+            double sum = 0;
+#pragma unroll 4
+            for (int i = lane; i <= j; i += 32) {
+                const cplx u = U[size_t(j) * ld + i];
+                sum += sqrt(u.re * u.re + u.im * u.im);
+            }
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            cmax = fmax(cmax, sum);
+            if (lane == 0) {
+                const cplx d = U[size_t(j) * ld + j];
+                if (d.re == 0.0 && d.im == 0.0) s_zero = 1;
+            }
         }
-        if (n > 1) {
-            for (int i = tid; i < n; i += kRcT) x[i] = csign(x[i]);
-            __syncthreads();
-            rc_solve_uh(U, n, ld, x, tile);
-            int j = rc_block_argmax(x, n, red, redi);
-            for (int iter = 2;; ++iter) {
-                __syncthreads();
-                for (int i = tid; i < n; i += kRcT) x[i] = cplx{i == j ? 1.0 : 0.0, 0.0};
-                __syncthreads();
-                rc_solve_u(U, n, ld, x, tile);
-                const double estold = est;
+        if (lane == 0) red[warp] = cmax;
+        __syncthreads();
+        double anorm = 0;
+        for (int w = 0; w < kRcT / 32; ++w) anorm = fmax(anorm, red[w]);
+        double rc = 0.0;
+        if (!s_zero && anorm > 0.0 && isfinite(anorm)) {
+            auto sum_abs = [&]() {
                 double a = 0;
-                for (int i = tid; i < n; i += kRcT) a += hypot(x[i].re, x[i].im);
-                est = rc_block_sum(a, red);
-                if (!(est > estold)) { est = fmax(est, estold); break; }
-                __syncthreads();
+                for (int i = tid; i < n; i += kRcT) a += sqrt(x[i].re * x[i].re + x[i].im * x[i].im);
+                return rc_block_sum(a, red);
+            };
+            // zlacn2: x = e / n; y = U^{-1} x
+            __syncthreads();
+            for (int i = tid; i < n; i += kRcT) x[i] = cplx{1.0 / n, 0.0};
+            __syncthreads();
+            rc_solve_u(U, Di, n, ld, x, t);
+            double est = sum_abs();
+            if (n > 1) {
                 for (int i = tid; i < n; i += kRcT) x[i] = csign(x[i]);
                 __syncthreads();
-                rc_solve_uh(U, n, ld, x, tile);
-                const int jlast = j;
-                const double xl = hypot(x[jlast].re, x[jlast].im);
-                j = rc_block_argmax(x, n, red, redi);
-                const double xj = hypot(x[j].re, x[j].im);
-                if (!(xl != xj && iter < 5)) break;
+                rc_solve_uh(U, Di, n, ld, x);
+                int j = rc_block_argmax(x, n, red, redi);
+                for (int iter = 2;; ++iter) {
+                    __syncthreads();
+                    for (int i = tid; i < n; i += kRcT) x[i] = cplx{i == j ? 1.0 : 0.0, 0.0};
+                    __syncthreads();
+                    rc_solve_u(U, Di, n, ld, x, t);
+                    const double estold = est;
+                    est = sum_abs();
+                    if (!(est > estold)) { est = fmax(est, estold); break; }
+                    __syncthreads();
+                    for (int i = tid; i < n; i += kRcT) x[i] = csign(x[i]);
+                    __syncthreads();
+                    rc_solve_uh(U, Di, n, ld, x);
+                    const int jlast = j;
+                    const double xl = sqrt(x[jlast].re * x[jlast].re + x[jlast].im * x[jlast].im);
+                    j = rc_block_argmax(x, n, red, redi);
+                    const double xj = sqrt(x[j].re * x[j].re + x[j].im * x[j].im);
+                    if (!(xl != xj && iter < 5)) break;
+                }
+                // alternating-sign test vector x_i = (-1)^i (1 + i / (n - 1))
+                __syncthreads();
+                for (int i = tid; i < n; i += kRcT)
+                    x[i] = cplx{((i & 1) ? -1.0 : 1.0) * (1.0 + double(i) / (n - 1)), 0.0};
+                __syncthreads();
+                rc_solve_u(U, Di, n, ld, x, t);
+                const double temp = 2.0 * sum_abs() / (3.0 * n);
+                est = fmax(est, temp);
             }
-            // alternating-sign test vector x_i = (-1)^i (1 + i / (n - 1))
-            __syncthreads();
-            for (int i = tid; i < n; i += kRcT) x[i] = cplx{((i & 1) ? -1.0 : 1.0) * (1.0 + double(i) / (n - 1)), 0.0};
-            __syncthreads();
-            rc_solve_u(U, n, ld, x, tile);
-            double a = 0;
-            for (int i = tid; i < n; i += kRcT) a += hypot(x[i].re, x[i].im);
-            const double temp = 2.0 * rc_block_sum(a, red) / (3.0 * n);
-            est = fmax(est, temp);
+            rc = (est > 0.0 && isfinite(est)) ? (1.0 / anorm) / est : 0.0;
+            if (tid == 0 && est_out) est_out[blk] = est;
+        } else if (tid == 0 && est_out) {
+            est_out[blk] = INFINITY;
         }
-        rc = (est > 0.0 && isfinite(est)) ? (1.0 / anorm) / est : 0.0;
+        if (tid == 0) {
+            if (rcond) rcond[blk] = rc;
+            if (!(rc > th)) flag[blk] = 1;
+        }
     }
-    if (tid == 0) {
-        if (rcond) rcond[blockIdx.x] = rc;
-        if (!(rc > th)) flag[blockIdx.x] = 1;
+}
+
+// ||A_b||_1 of each n x n block (max column sum of moduli), as the IEEE bits of a
+// non-negative double (their integer order is the numeric order: atomicMax)
+__global__ void __launch_bounds__(256) colsum_max_kernel(const cplx* __restrict__ A, int n, int ld, size_t stride,
+                                                         unsigned long long* __restrict__ out) {
+    const cplx* Ab = A + size_t(blockIdx.x) * stride;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double m = 0;
+    for (int j = blockIdx.y * 8 + warp; j < n; j += gridDim.y * 8) {
+        double sum = 0;
+#pragma unroll 4
+        for (int i = lane; i < n; i += 32) {
+            const cplx u = Ab[size_t(j) * ld + i];
+            sum += sqrt(u.re * u.re + u.im * u.im);
+        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        m = fmax(m, sum);
     }
+    if (lane == 0 && m > 0.0) atomicMax(out + blockIdx.x, (unsigned long long)__double_as_longlong(m));
+}
+
+// Screen of the Woodbury level-0 factors: est_lo = max_k ||A^{-1} r_k||_1 /
+// ||r_k||_1 over the probe columns solved with the level-0 right-hand sides is
+// a lower bound of ||A^{-1}||_1, so rc_up = 1 / (||A||_1 est_lo) bounds rcond
+// from above: rc_up <= th_def certifies rcond <= th_def; rc_up <= th_sus marks
+// the block for the full zlacn2 estimate.
+__global__ void __launch_bounds__(256) rc_screen_kernel(const cplx* __restrict__ W, size_t wstride, int n, int col0,
+                                                        int nprobe, const unsigned long long* __restrict__ anorm,
+                                                        double rnorm1, double th_def, double th_sus,
+                                                        int* __restrict__ flag, int* __restrict__ sus,
+                                                        double* __restrict__ est_lo) {
+    __shared__ double red[8];
+    const cplx* Wb = W + size_t(blockIdx.x) * wstride;
+    double best = 0;
+    for (int k = 0; k < nprobe; ++k) {
+        double a = 0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const cplx v = Wb[size_t(col0 + k) * n + i];
+            a += sqrt(v.re * v.re + v.im * v.im);
+        }
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        __syncthreads();
+        double t = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+        best = isfinite(t) ? fmax(best, t / rnorm1) : INFINITY;
+    }
+    if (threadIdx.x == 0) {
+        const double an = __longlong_as_double((long long)anorm[blockIdx.x]);
+        const double rc = 1.0 / (an * best);
+        est_lo[blockIdx.x] = best;
+        if (!(rc > th_def)) flag[blockIdx.x] = 1;
+        sus[blockIdx.x] = !(rc > th_sus);
+    }
+}
+
+__global__ void gather_columns_kernel(const cplx* const* __restrict__ src, const int* __restrict__ ld, int rows,
+                                      const int* __restrict__ cols, int ncols, cplx* __restrict__ dst, int ldd,
+                                      size_t dstride) {
+    const int q = blockIdx.x, k = blockIdx.y;
+    const cplx* a = src[q] + size_t(cols[size_t(q) * ncols + k]) * ld[q];
+    cplx* d = dst + size_t(q) * dstride + size_t(k) * ldd;
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) d[i] = a[i];
 }
 
 __global__ void dfma_peak_kernel(double* out, int iters) {
@@ -2865,18 +2968,56 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
     upper(0, nblk);
 }
 
-void lu_rcond_batched(int n, int ld, cplx* const* d_ptrs, const cplx* base, size_t stride, int count, double th,
-                      int* d_flag, double* d_rcond, cudaStream_t s) {
+void lu_rcond_batched(int n, int ld, cplx* const* d_ptrs, const cplx* base, size_t stride, cplx* const* d_dinv,
+                      const cplx* dbase, size_t dstride, int count, double th, int* d_flag, double* d_rcond,
+                      cudaStream_t s, double* d_est) {
     if (count == 0 || n == 0) return;
-    const size_t sm = (size_t(n) + kRcW * (kRcW + 1)) * sizeof(cplx);
+    const size_t sm = (size_t(n) + kRcT) * sizeof(cplx);
     static size_t attr = 48 * 1024;
     if (sm > attr) {
         QPS_CUDA(cudaFuncSetAttribute(lu_rcond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         attr = sm;
     }
-    // ~6 triangular solves over U: 6 n^2 / 2 complex reads per block
-    ProfScope ps("lu_rcond", s, 0.0, 16.0 * 3.0 * count * double(n) * n);
-    { QPS_NOTE_LAUNCH(); lu_rcond_kernel<<<count, kRcT, sm, s>>>(n, ld, d_ptrs, base, stride, th, d_flag, d_rcond); }
+    // ~6 triangular solves, U read from HBM about once (the CTA's block stays in L2)
+    ProfScope ps("lu_rcond", s, 0.0, 16.0 * 0.5 * count * double(n) * n);
+    static const int ctas = [] {  // QPS_RCOND_CTAS: CTAs of the estimate (default 32: U of 32 blocks fits L2)
+        const char* e = getenv("QPS_RCOND_CTAS");
+        return e ? std::max(1, atoi(e)) : 32;
+    }();
+    const int grid = std::min(count, ctas);
+    { QPS_NOTE_LAUNCH(); lu_rcond_kernel<<<grid, kRcT, sm, s>>>(n, ld, count, d_ptrs, base, stride, d_dinv, dbase, dstride,
+                                                                 th, d_flag, d_rcond, d_est); }
+    QPS_CUDA(cudaGetLastError());
+}
+
+void batched_norm1(const cplx* A, int n, int ld, size_t stride, int count, unsigned long long* d_out,
+                   cudaStream_t s) {
+    if (count == 0 || n == 0) return;
+    QPS_CUDA(cudaMemsetAsync(d_out, 0, sizeof(unsigned long long) * count, s));
+    ProfScope ps("reduce", s, 0.0, 16.0 * count * double(n) * n);
+    { QPS_NOTE_LAUNCH(); colsum_max_kernel<<<dim3(count, 8), 256, 0, s>>>(A, n, ld, stride, d_out); }
+    QPS_CUDA(cudaGetLastError());
+}
+
+void rcond_screen(const cplx* W, size_t wstride, int n, int col0, int nprobe, const unsigned long long* d_anorm,
+                  double rnorm1, int count, double th_def, double th_sus, int* d_flag, int* d_sus, double* d_est_lo,
+                  cudaStream_t s) {
+    if (count == 0) return;
+    { QPS_NOTE_LAUNCH(); rc_screen_kernel<<<count, 256, 0, s>>>(W, wstride, n, col0, nprobe, d_anorm, rnorm1, th_def,
+                                                                 th_sus, d_flag, d_sus, d_est_lo); }
+    QPS_CUDA(cudaGetLastError());
+}
+
+void gather_columns(const std::vector<const cplx*>& src, const std::vector<int>& ld, int rows, const int* d_cols,
+                    int ncols, cplx* dst, int ldd, size_t dstride, DBuf<const cplx*>& pbuf, DBuf<int>& lbuf,
+                    cudaStream_t s) {
+    const int n = int(src.size());
+    if (n == 0 || rows == 0 || ncols == 0) return;
+    pbuf.upload(src, s);
+    lbuf.upload(ld, s);
+    ProfScope ps("copy", s, 0.0, 32.0 * n * double(rows) * ncols);
+    { QPS_NOTE_LAUNCH(); gather_columns_kernel<<<dim3(n, ncols), 128, 0, s>>>(pbuf.p, lbuf.p, rows, d_cols, ncols, dst,
+                                                                              ldd, dstride); }
     QPS_CUDA(cudaGetLastError());
 }
 

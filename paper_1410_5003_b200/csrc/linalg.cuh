@@ -87,11 +87,29 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& A, const std::vec
 // PartialPivLU::rcond() test (tridiag.hpp:36-40): per block b (d_ptrs[b], or
 // base + b * stride when d_ptrs is null) rcond(U_b) = 1 / (||U_b||_1
 // est ||U_b^{-1}||_1) with LAPACK zlacn2's Hager/Higham estimator on the U
-// factor left in the upper triangle; d_flag[b] = 1 when !(rcond > th);
-// d_rcond (may be null) receives the estimates.
-void lu_rcond_batched(int n, int ld, cplx* const* d_ptrs, const cplx* base, size_t stride, int count, double th,
-                      int* d_flag, double* d_rcond, cudaStream_t s);
+// factor left in the upper triangle, solving with the LU's inverse diagonal
+// tiles (d_dinv[b] or dbase + b * dstride, lu_dinv_elems layout, U half
+// filled); d_flag[b] = 1 when !(rcond > th); d_rcond / d_est (may be null)
+// receive the estimates of rcond(U) and of ||U^{-1}||_1.
+void lu_rcond_batched(int n, int ld, cplx* const* d_ptrs, const cplx* base, size_t stride, cplx* const* d_dinv,
+                      const cplx* dbase, size_t dstride, int count, double th, int* d_flag, double* d_rcond,
+                      cudaStream_t s, double* d_est = nullptr);
+// ||A_b||_1 of count n x n blocks (base + b stride), as double bits (see rcond_screen)
+void batched_norm1(const cplx* A, int n, int ld, size_t stride, int count, unsigned long long* d_out,
+                   cudaStream_t s);
+// rc_up_b = 1 / (||A_b||_1 max_k ||W_b[:, col0 + k]||_1 / rnorm1) for the nprobe
+// solved probe columns of W_b (n x ..., ld n, base + b wstride): d_flag[b] = 1
+// when rc_up <= th_def (certain), d_sus[b] = rc_up <= th_sus, d_est_lo[b] the
+// lower bound of ||A_b^{-1}||_1
+void rcond_screen(const cplx* W, size_t wstride, int n, int col0, int nprobe, const unsigned long long* d_anorm,
+                  double rnorm1, int count, double th_def, double th_sus, int* d_flag, int* d_sus, double* d_est_lo,
+                  cudaStream_t s);
 constexpr double kRcondMin = 1e-15;  // tridiag.hpp:36
+// dst_q[:, k] = src_q[:, cols[q * ncols + k]] (rows x ncols per problem q; src_q
+// column-major with leading dimension ld[q]); pointer/ld tables staged in pbuf/lbuf
+void gather_columns(const std::vector<const cplx*>& src, const std::vector<int>& ld, int rows, const int* d_cols,
+                    int ncols, cplx* dst, int ldd, size_t dstride, DBuf<const cplx*>& pbuf, DBuf<int>& lbuf,
+                    cudaStream_t s);
 
 // ---- small utilities -------------------------------------------------------
 // per problem max |X_ij| over an m x n block (ld), count problems with stride

@@ -841,12 +841,18 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     c.lr_rank_max = 0;
     c.lr_probe_worst = 0;
     c.bcr_path = 0;
+    c.anorm_pending = false;
+    if (!dense_only && !lr_direct) wb_anorm_async(c, Ad);  // overlaps the compression
     if (!dense_only && lr_compress(c, Au, Al)) {
         c.bcr_path = lr_direct ? 2 : 1;
         if (lr_direct) bcr_solve_lr(c, Ad);
         else bcr_solve_wb(c, Ad);
         c.couplings_deferred = false;
         return;
+    }
+    if (c.anorm_pending) {  // the side stream's norms read Ad: join before the factorization rewrites it
+        QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_anorm, 0));
+        c.anorm_pending = false;
     }
     if (c.couplings_deferred) {  // the dense reduction needs the periodized couplings
         std::vector<GemmTask> t(c.coupling_sup);
@@ -900,7 +906,8 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         flag.ensure(fa.size());
         flag.zero(s);
         lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
-        lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p, nullptr, s);
+        lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, c.ws.ptrs3.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p,
+                         nullptr, s);
         std::vector<int> hf(fa.size());
         QPS_D2H(hf.data(), flag.p, sizeof(int) * hf.size(), s);
         QPS_CUDA(cudaStreamSynchronize(s));

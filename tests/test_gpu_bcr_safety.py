@@ -35,7 +35,7 @@ def unitary(rng, n):
     return q * (np.diag(r) / np.abs(np.diag(r)))
 
 
-def stack(I, rank, seed, bad=None):
+def stack(I, rank, seed, bad=None, smin=0.0):
     """Diagonally dominant blocks (4 I + 0.3 N(0,1)/sqrt(n) scale), couplings of
     the given rank (None: full rank).  Block `bad` is replaced by U diag(s) V^*
     with s_min = 0 (numerically singular, not exactly), and the couplings that
@@ -55,7 +55,7 @@ def stack(I, rank, seed, bad=None):
     if bad is not None:
         U, V = unitary(rng, n), unitary(rng, n)
         s = np.linspace(2.0, 1.0, n)
-        s[-1] = 0.0
+        s[-1] = smin
         Ad[bad] = (U * s) @ V.conj().T
         u = U[:, -1:]
         if bad >= 1:
@@ -77,6 +77,17 @@ def test_numerically_singular_block_names_its_layer(gpu, oracle, rank, bad):
         gpu.block_lu_solve_blocks(Ad, Au, Al, f)
     assert eo.value.layer == bad + 1
     assert eg.value.layer == eo.value.layer
+
+
+@pytest.mark.parametrize("rank", [12, None])
+def test_ill_conditioned_block_is_not_rejected(gpu, oracle, rank):
+    """rcond ~ 1e-12 (above the reference's 1e-15): the product's probe screen
+    marks the block as a suspect, the full zlacn2 estimate clears it, and both
+    implementations solve (to the conditioning of the problem)."""
+    Ad, Au, Al, f = stack(6, rank, 21, bad=3, smin=2e-12)
+    eo = oracle.block_lu_solve_blocks(Ad, Au, Al, f)
+    eta = gpu.block_lu_solve_blocks(Ad, Au, Al, f)
+    assert np.linalg.norm(eta - eo) < 1e-3 * np.linalg.norm(eo)
 
 
 def test_full_rank_couplings_take_the_dense_fallback(gpu, oracle):
