@@ -202,6 +202,24 @@ int qps_evaluate_field(qps_ctx* ctx, int n_points, const double* xy, qps_cplx* u
  * status [n] (qps_status of that angle; a singular angle does not abort). */
 int qps_sweep(qps_ctx* ctx, int n_angles, const double* theta, int K, int mode, double* R, double* T,
               double* flux_error, qps_cplx* aU, qps_cplx* aD, int* status);
+/* plan_sweep(omega, n, theta_range), SPEC.md:505-512 (sweep module; the
+ * reference has no code for it, proj/tests/test_sweep.cpp:1): angles on a grid
+ * uniform in kappa_0 = k_1 cos(theta) with spacing 2 pi / (n d) inside
+ * (theta_lo, theta_hi) (-pi < lo < hi < 0), so that alpha = exp(i d k_1 cos
+ * theta) takes exactly n values.  k_1 and d from the last
+ * make_problem.  Up to cap angles and their alpha-group index (j mod n) are
+ * written; *n_angles receives the grid size. */
+int qps_plan_sweep(qps_ctx* ctx, int n_alpha, double theta_lo, double theta_hi, int cap, double* theta,
+                   int* alpha_group, int* n_angles);
+/* The last qps_sweep: alpha group of every angle (SpectrumRow::alpha_group,
+ * postprocess.hpp:155-161; -1 for an angle whose make_problem failed), number
+ * of groups, interior eliminations (InteriorSchur, periodize.hpp:61-94) and
+ * block factorizations performed.  Mode 0 computes both once per alpha group
+ * of two or more angles (the product factors A(alpha) once and applies each
+ * angle's corner terms as a rank-2P Woodbury correction; the reference
+ * composition re-runs block_lu_solve per angle). */
+int qps_sweep_info(const qps_ctx* ctx, int cap, int* alpha_group, int* n_groups, uint64_t* n_interior,
+                   uint64_t* n_factorizations);
 
 /* ------------------------------------------------- parity / diagnostics */
 /* Copy block `kind` with index `i` (interface, layer or 0) into out

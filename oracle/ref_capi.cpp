@@ -35,6 +35,10 @@ struct qps_ctx {
     std::string err;
     int err_layer = 0;
     uint64_t err_bytes = 0;
+    // last sweep: alpha group per angle, interior eliminations, block factorizations
+    std::vector<int> sweep_group;
+    int sweep_ngroups = 0;
+    uint64_t sweep_interior = 0, sweep_factorizations = 0;
 };
 
 namespace {
@@ -349,41 +353,148 @@ int qps_reflection_transmission(const qps_ctx* c, double* R, double* T, double* 
     });
 }
 
+// The reference has no sweep driver (proj/tests/test_sweep.cpp:1); this is the
+// SPEC.md:505-547 composition of its building blocks.  mode 0: the cache is
+// filled once; angles sharing alpha (|alpha_a - alpha_b| <= 1e-12) form a group
+// whose interior elimination schur_interior (periodize.hpp:67-94) runs once,
+// then per angle assemble_radiation / assemble_rhs / assemble_corners
+// (assembly.hpp:407-460), schur_corners (periodize.hpp:98-121), block_lu_solve,
+// recover_aux (tridiag.hpp:23-66).  mode 1: every angle independently
+// (precompute_shift_blocks + assemble_system + solve_periodized).
 int qps_sweep(qps_ctx* c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe,
               qps_cplx* aU, qps_cplx* aD, int* status) {
     return guarded(c, [&] {
         need(c->have_prob, "make_problem first (sets omega)");
         need(K > 0, "sweep needs a fixed K > 0");
+        need(mode == 0 || mode == 1, "sweep: mode is 0 (accelerated) or 1 (independent)");
         const double omega = c->prob.omega;
         const int nrb = 2 * K + 1;
         const auto t0 = clk::now();
         std::optional<ShiftBlockCache> cache;
         const double nan = std::nan("");
+        c->sweep_group.assign(n, -1);
+        c->sweep_ngroups = 0;
+        c->sweep_interior = c->sweep_factorizations = 0;
+        std::vector<std::optional<ScatteringProblem>> probs(n);
         for (int a = 0; a < n; ++a) {
             if (R) R[a] = nan;
             if (T) T[a] = nan;
             if (fe) fe[a] = nan;
             qps_ctx tmp;
-            const int st = guarded(&tmp, [&] {
-                ScatteringProblem p = make_problem(c->stack, c->geom, omega, theta[a], K);
-                if (mode != 0 || !cache) {  // mode 0: the first valid angle fills the cache
-                    cache = precompute_shift_blocks(p, c->num);
-                    c->fill_evals = cache->fill_evals;
-                }
-                const BlockSystem sys = assemble_system(p, *cache, c->num);
-                Solution s = solve_periodized(sys);
-                const SpectrumRow row = reflection_transmission(s, p);
-                if (R) R[a] = row.R;
-                if (T) T[a] = row.T;
-                if (fe) fe[a] = row.flux_error;
-                for (int i = 0; i < nrb; ++i) {
-                    if (aU) aU[size_t(a) * nrb + i] = {s.aU(i).real(), s.aU(i).imag()};
-                    if (aD) aD[size_t(a) * nrb + i] = {s.aD(i).real(), s.aD(i).imag()};
-                }
-            });
+            const int st = guarded(&tmp, [&] { probs[a] = make_problem(c->stack, c->geom, omega, theta[a], K); });
             if (status) status[a] = st;
         }
+        // alpha groups in order of first appearance
+        std::vector<std::vector<int>> groups;
+        std::vector<cd> reps;
+        for (int a = 0; a < n; ++a) {
+            if (!probs[a]) continue;
+            int gi = -1;
+            for (size_t r = 0; r < reps.size() && mode == 0; ++r)
+                if (std::abs(probs[a]->alpha - reps[r]) <= 1e-12) {
+                    gi = int(r);
+                    break;
+                }
+            if (gi < 0) {
+                gi = int(groups.size());
+                groups.emplace_back();
+                reps.push_back(probs[a]->alpha);
+            }
+            groups[gi].push_back(a);
+            c->sweep_group[a] = gi;
+        }
+        c->sweep_ngroups = int(groups.size());
+        auto emit = [&](int a, const Solution& s) {
+            const SpectrumRow row = reflection_transmission(s, *probs[a]);
+            if (R) R[a] = row.R;
+            if (T) T[a] = row.T;
+            if (fe) fe[a] = row.flux_error;
+            for (int i = 0; i < nrb; ++i) {
+                if (aU) aU[size_t(a) * nrb + i] = {s.aU(i).real(), s.aU(i).imag()};
+                if (aD) aD[size_t(a) * nrb + i] = {s.aD(i).real(), s.aD(i).imag()};
+            }
+        };
+        for (const auto& g : groups) {
+            if (mode != 0) {  // independent: the whole pipeline per angle
+                qps_ctx tmp;
+                const int st = guarded(&tmp, [&] {
+                    cache = precompute_shift_blocks(*probs[g[0]], c->num);
+                    c->fill_evals = cache->fill_evals;
+                    const BlockSystem sys = assemble_system(*probs[g[0]], *cache, c->num);
+                    ++c->sweep_interior;
+                    ++c->sweep_factorizations;
+                    emit(g[0], solve_periodized(sys));
+                });
+                if (status) status[g[0]] = st;
+                continue;
+            }
+            qps_ctx tmp;
+            std::optional<BlockSystem> sys;
+            std::optional<InteriorSchur> interior;
+            const int st = guarded(&tmp, [&] {
+                if (!cache) {  // mode 0: the first valid angle fills the cache
+                    cache = precompute_shift_blocks(*probs[g[0]], c->num);
+                    c->fill_evals = cache->fill_evals;
+                }
+                sys = assemble_system(*probs[g[0]], *cache, c->num);
+                interior = schur_interior(*sys);
+                ++c->sweep_interior;
+            });
+            if (st != QPS_OK) {
+                for (int a : g)
+                    if (status) status[a] = st;
+                continue;
+            }
+            for (int a : g) {
+                const int sa = guarded(&tmp, [&] {
+                    assemble_radiation(*probs[a], *cache, *sys);
+                    assemble_rhs(*probs[a], *sys);
+                    assemble_corners(*sys);
+                    const PeriodizedSystem ps = schur_corners(*interior, *sys);
+                    Solution s;
+                    recover_aux(ps, block_lu_solve(ps), s);
+                    ++c->sweep_factorizations;
+                    emit(a, s);
+                });
+                if (status) status[a] = sa;
+            }
+        }
         c->times.fill_ms = ms_since(t0);
+    });
+}
+
+int qps_sweep_info(const qps_ctx* c, int cap, int* alpha_group, int* n_groups, uint64_t* n_interior,
+                   uint64_t* n_factorizations) {
+    if (!c) return QPS_ERR_USAGE;
+    for (int a = 0; alpha_group && a < cap && a < int(c->sweep_group.size()); ++a) alpha_group[a] = c->sweep_group[a];
+    if (n_groups) *n_groups = c->sweep_ngroups;
+    if (n_interior) *n_interior = c->sweep_interior;
+    if (n_factorizations) *n_factorizations = c->sweep_factorizations;
+    return QPS_OK;
+}
+
+// plan_sweep: angles uniform in kappa_0 = k_1 cos(theta) with
+// spacing 2 pi / (n d) inside (theta_lo, theta_hi), so alpha takes n values
+int qps_plan_sweep(qps_ctx* c, int n_alpha, double theta_lo, double theta_hi, int cap, double* theta,
+                   int* alpha_group, int* n_angles) {
+    return guarded(c, [&] {
+        need(c->have_prob, "make_problem first (sets k_1)");
+        if (n_alpha < 1) throw ConfigError("plan_sweep: n >= 1 alpha values required");
+        if (!(theta_lo > -pi && theta_hi < 0.0 && theta_lo < theta_hi))
+            throw ConfigError("plan_sweep: theta range must satisfy -pi < lo < hi < 0");
+        const double k1 = c->prob.k.front(), d = c->stack.d;
+        const double klo = k1 * std::cos(theta_lo), khi = k1 * std::cos(theta_hi), dk = 2.0 * pi / (n_alpha * d);
+        int cnt = 0;
+        for (int j = 0;; ++j) {
+            const double kap = klo + (j + 0.5) * dk;
+            if (kap >= khi) break;
+            if (cnt < cap) {
+                if (theta) theta[cnt] = -std::acos(kap / k1);
+                if (alpha_group) alpha_group[cnt] = j % n_alpha;
+            }
+            ++cnt;
+        }
+        if (n_angles) *n_angles = cnt;
     });
 }
 

@@ -324,19 +324,23 @@ __global__ void set_identity_kernel(int n, cplx* __restrict__ C) {
 // of block j, ld n) for every block j of every system, so that one solve
 // gives D^{-1} [P_L P_U] and D^{-1} f; P holds per system the I-1 sub- then
 // the I-1 super-couplings
-// W_j = [P_L | P_U | f_j | R] (n x (2r + 1 + nprobe)): the level-0 right-hand sides
+// W_j = [P_L | P_U | F_j | R] (n x (2r + m + nprobe)): the level-0 right-hand sides
 __global__ void stage_bases_kernel(int I, int n, size_t per, const cplx* __restrict__ P, const cplx* __restrict__ F,
-                                   const cplx* __restrict__ R, int nprobe, cplx* __restrict__ W) {
+                                   int m, const cplx* __restrict__ R, int nprobe, cplx* __restrict__ W) {
     const int j = blockIdx.x, a = j / I, jj = j % I;
     const size_t qa = size_t(a) * 2 * (I - 1);
     const cplx* pl = jj >= 1 ? P + (qa + (jj - 1)) * per : nullptr;
     const cplx* pu = jj + 1 < I ? P + (qa + (I - 1) + jj) * per : nullptr;
-    cplx* w = W + size_t(j) * (2 * per + size_t(n) * (1 + nprobe));
-    for (size_t e = size_t(blockIdx.y) * blockDim.x + threadIdx.x; e < per; e += size_t(gridDim.y) * blockDim.x) {
-        w[e] = pl ? pl[e] : cplx{0, 0};
-        w[per + e] = pu ? pu[e] : cplx{0, 0};
-        if (e < size_t(n)) w[2 * per + e] = F[size_t(j) * n + e];
-        if (e < size_t(n) * nprobe) w[2 * per + n + e] = R[e];
+    const size_t nf = size_t(n) * m, nr = size_t(n) * nprobe;
+    cplx* w = W + size_t(j) * (2 * per + nf + nr);
+    const size_t tot = per > nf ? (per > nr ? per : nr) : (nf > nr ? nf : nr);
+    for (size_t e = size_t(blockIdx.y) * blockDim.x + threadIdx.x; e < tot; e += size_t(gridDim.y) * blockDim.x) {
+        if (e < per) {
+            w[e] = pl ? pl[e] : cplx{0, 0};
+            w[per + e] = pu ? pu[e] : cplx{0, 0};
+        }
+        if (e < nf) w[2 * per + e] = F[size_t(j) * nf + e];
+        if (e < nr) w[2 * per + nf + e] = R[e];
     }
 }
 
@@ -1022,6 +1026,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
 
 void bcr_solve_lr(Ctx& c, cplx* Ad) {
     ProfPhase phase("bcr");
+    ++c.n_factorizations;
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, ns = D.nsys, r = c.lr_r;
     const size_t nb2 = D.nb2();
@@ -1297,6 +1302,7 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
 // The deep levels (a handful of blocks each) become a few small GEMMs instead
 // of a latency-bound dense LU per level; the level-0 batch runs at throughput.
 // ---------------------------------------------------------------------------
+
 // ||D_j^0||_1 of every diagonal block for the level-0 rcond screen, on the side
 // stream while the couplings are compressed (Ad is final after the Schur step;
 // bcr_solve_wb joins before its factorization overwrites Ad)
@@ -1313,28 +1319,36 @@ void wb_anorm_async(Ctx& c, const cplx* Ad) {
 
 void bcr_solve_wb(Ctx& c, cplx* Ad) {
     ProfPhase phase("bcr");
+    ++c.n_factorizations;
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, ns = D.nsys, r = c.lr_r, r2 = 2 * r;
     const size_t nb2 = D.nb2();
     cudaStream_t s = c.stream;
     const cplx one{1, 0}, mone{-1, 0}, zero{0, 0};
     const int npos = ns * I;
-    c.F.ensure(size_t(npos) * nb);
-    c.F.zero(s);
-    for (int a = 0; a < ns; ++a)
-        QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
-                                 cudaMemcpyDeviceToDevice, s));
+    // right-hand sides: m = c.nrhs columns per block (nb x m, ld nb); with m = 1
+    // the system's f on block 0, with m > 1 the caller has filled c.F
+    const int m = std::max(1, c.nrhs);
+    if (m == 1) {
+        c.F.ensure(size_t(npos) * nb);
+        c.F.zero(s);
+        for (int a = 0; a < ns; ++a)
+            QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+    const size_t fs = size_t(nb) * m;  // per-block stride of F
+    RhsOps rhs{m, s, c.ws};
     c.ipiv.ensure(size_t(npos) * nb);
     const size_t dsz = lu_dinv_elems(nb);
     c.dinv.ensure(size_t(npos) * dsz);
-    const int wc = r2 + 1 + kRcProbe;  // [W | y | rcond probes] per block
+    const int wc = r2 + m + kRcProbe;  // [W | y | rcond probes] per block
     c.lr_W0.ensure(size_t(npos) * nb * wc);
     c.lr_S.ensure(size_t(npos) * r2 * nb);
-    c.lr_g.ensure(size_t(npos) * r2);
+    c.lr_g.ensure(size_t(npos) * r2 * m);
     c.lr_S.zero(s);
     c.lr_g.zero(s);
     c.lr_core.ensure(size_t(npos) * 4 * r * r);
-    c.lr_vec.ensure(size_t(npos) * 4 * r);
+    c.lr_vec.ensure(size_t(npos) * r2 * m);
     static const bool trace = getenv("QPS_BCR_TRACE") != nullptr;  // per-level timing to stderr (debug)
     cudaEvent_t te0 = nullptr, te1 = nullptr;
     if (trace) {
@@ -1380,7 +1394,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     std::vector<Level> levels;
     auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * wc; };
     auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
-    auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2; };
+    auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2 * m; };  // r2 x m, ld r2
     std::vector<int> l0_orig;  // level-0 positions whose singular flags are checked at the end
     // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
     cudaEvent_t f0 = nullptr, f1 = nullptr;  // factor_ms of the phase times
@@ -1414,8 +1428,8 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             c.rc_anorm.ensure(npos);
             batched_norm1(Ad, nb, nb, nb2, npos, c.rc_anorm.p, s);
         }
-        { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, c.rc_probe.p,
-                                                                                kRcProbe, c.lr_W0.p); }
+        { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, m,
+                                                                                c.rc_probe.p, kRcProbe, c.lr_W0.p); }
         QPS_CUDA(cudaGetLastError());
         for (int a = 0; a < ns; ++a) {
             const size_t qa = size_t(a) * 2 * (I - 1);
@@ -1423,7 +1437,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
                 Pos p{};
                 p.idx = j;
                 p.j = a * I + j;
-                p.F = c.F.p + size_t(p.j) * nb;
+                p.F = c.F.p + size_t(p.j) * fs;
                 if (j >= 1) {
                     p.PL = c.lr_P.p + (qa + (j - 1)) * per;
                     p.RL = c.lr_R.p + (qa + (j - 1)) * per;
@@ -1471,7 +1485,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         c.rc_sus.ensure(npos);
         c.rc_estlo.ensure(npos);
         QPS_CUDA(cudaMemsetAsync(c.rc_flag.p, 0, sizeof(int) * npos, s));
-        rcond_screen(c.lr_W0.p, size_t(nb) * wc, nb, r2 + 1, kRcProbe, c.rc_anorm.p, double(nb), npos, kRcondMin,
+        rcond_screen(c.lr_W0.p, size_t(nb) * wc, nb, r2 + m, kRcProbe, c.rc_anorm.p, double(nb), npos, kRcondMin,
                      kRcSuspect, c.rc_flag.p, c.rc_sus.p, c.rc_estlo.p, s);
         c.rc_flag_h.ensure(2 * size_t(npos));
         QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, s);
@@ -1479,8 +1493,8 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         QPS_CUDA(cudaEventRecord(f1, s));
         nvtxRangePop();
         // y = D^{-1} f back into F (column 2r of every W_j)
-        QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * nb, c.lr_W0.p + size_t(r2) * nb,
-                                   sizeof(cplx) * nb * wc, sizeof(cplx) * nb, npos, cudaMemcpyDeviceToDevice, s));
+        QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * fs, c.lr_W0.p + size_t(r2) * nb,
+                                   sizeof(cplx) * nb * wc, sizeof(cplx) * fs, npos, cudaMemcpyDeviceToDevice, s));
         tmark("solve", 0, int(fa.size()));
         levels.push_back(std::move(L0));
     }
@@ -1505,7 +1519,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         c.lr_Cpiv.ensure(size_t(cnt) * r2);
         const size_t cds = lu_dinv_elems(r2);
         c.lr_Cdinv.ensure(size_t(cnt) * cds);
-        c.lr_a.ensure(size_t(cnt) * r2);
+        c.lr_a.ensure(size_t(cnt) * r2 * m);
         DBuf<cplx>& Zb = c.lr_Z[lvl];
         Zb.ensure(size_t(cnt) * nb * r2);
         { QPS_NOTE_LAUNCH(); set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Cm.p); }
@@ -1519,8 +1533,8 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             { QPS_NOTE_LAUNCH(); set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Ci.p); }
             QPS_CUDA(cudaGetLastError());
         }
-        std::vector<GemmTask> m(cnt), z(cnt);
-        std::vector<GemvTask> gu(cnt), ga(cnt), gz(cnt);
+        std::vector<GemmTask> mt(cnt), z(cnt);
+        std::vector<GemmTask> gu(cnt), ga(cnt), gz(cnt);
         std::vector<cplx*> ca, cd, ci;
         std::vector<int*> cp;
         std::vector<int> orig;
@@ -1529,11 +1543,12 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             const cplx* W = W0_of(p.j);
             cplx* Cm = c.lr_Cm.p + size_t(q) * r2 * r2;
             cplx* Ci = c.lr_Ci.p + size_t(q) * r2 * r2;
-            m[q] = gemm1(S_of(p.j), r2, W, nb, nb, Cm, r2);                       // C = I - S W
+            mt[q] = gemm1(S_of(p.j), r2, W, nb, nb, Cm, r2);                      // C = I - S W
             z[q] = gemm1(W, nb, gjinv ? Cm : Ci, r2, r2, Zb.p + size_t(q) * nb * r2, nb);  // Z = W C^{-1}
-            gu[q] = gemv1(W, nb, g_of(p.j), r2, p.F);                              // u = y - W g
-            ga[q] = gemv1(S_of(p.j), r2, p.F, nb, c.lr_a.p + size_t(q) * r2);      // a = S u
-            gz[q] = gemv1(Zb.p + size_t(q) * nb * r2, nb, c.lr_a.p + size_t(q) * r2, r2, p.F);  // z = u + Z a
+            cplx* aq = c.lr_a.p + size_t(q) * r2 * m;
+            gu[q] = gemm1(W, nb, g_of(p.j), r2, r2, p.F, nb);                      // u = y - W g
+            ga[q] = gemm1(S_of(p.j), r2, p.F, nb, nb, aq, r2);                     // a = S u
+            gz[q] = gemm1(Zb.p + size_t(q) * nb * r2, nb, aq, r2, r2, p.F, nb);    // z = u + Z a
             ca.push_back(Cm);
             ci.push_back(Ci);
             cd.push_back(c.lr_Cdinv.p + size_t(q) * cds);
@@ -1541,7 +1556,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             orig.push_back(p.idx);
             p.Z = Zb.p + size_t(q) * nb * r2;
         }
-        zgemm_batched(r2, r2, mone, one, m, s, c.ws.gemm_tasks, "wb_cap");
+        zgemm_batched(r2, r2, mone, one, mt, s, c.ws.gemm_tasks, "wb_cap");
         if (gjinv) {  // C <- C^{-1} in place; singular flags checked once after all levels
             static const bool gj_smem = [] {  // QPS_WB_GJ=smem: the shared-memory kernel (always for 2r != 96)
                 const char* e = getenv("QPS_WB_GJ");
@@ -1572,9 +1587,9 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             lu_solve_batched(r2, r2, ca, cp, cd, ci, r2, r2, s, c.ws);
         }
         zgemm_batched(nb, r2, one, zero, z, s, c.ws.gemm_tasks, "wb_cap");
-        zgemv_batched(nb, mone, one, gu, s, c.ws.gemv_tasks);
-        zgemv_batched(r2, one, zero, ga, s, c.ws.gemv_tasks);
-        zgemv_batched(nb, one, one, gz, s, c.ws.gemv_tasks);
+        rhs.run(nb, mone, one, gu);
+        rhs.run(r2, one, zero, ga);
+        rhs.run(nb, one, one, gz);
     };
     int lvl = 0;
     while (levels[lvl][0].size() > 1) {
@@ -1590,7 +1605,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         DBuf<cplx>& Rn = c.lr_Rn[lvl];
         Rn.ensure(size_t(ns) * nsz * 2 * rn);
         std::vector<GemmTask> cores, prods, newr;
-        std::vector<GemvTask> v1;
+        std::vector<GemmTask> v1;
         Level nxt(ns);
         for (int a = 0; a < ns; ++a) {
             for (int e = 0; e < sz; e += 2) {
@@ -1615,7 +1630,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
                         np.PL = pe.PL;
                         np.RL = Rl;
                     }
-                    v1.push_back(gemv1(pe.RL, r, po.F, nb, g));  // g_L += R_L(e) z(o)
+                    v1.push_back(gemm1(pe.RL, r, po.F, nb, nb, g, r2));  // g_L += R_L(e) z(o)
                     np.updated = true;
                 }
                 if (hp) {
@@ -1631,7 +1646,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
                         np.PU = pe.PU;
                         np.RU = Ru;
                     }
-                    v1.push_back(gemv1(pe.RU, r, po.F, nb, g + r));
+                    v1.push_back(gemm1(pe.RU, r, po.F, nb, nb, g + r, r2));
                     np.updated = true;
                 }
                 nxt[a].push_back(np);
@@ -1640,7 +1655,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         zgemm_batched(r, r, one, zero, cores, s, c.ws.gemm_tasks, "lr_core");
         zgemm_batched(r, nb, one, one, prods, s, c.ws.gemm_tasks, "lr_core");
         zgemm_batched(r, nb, mone, zero, newr, s, c.ws.gemm_tasks, "lr_core");  // L' = P_L (-(core) R)
-        zgemv_batched(r, one, one, v1, s, c.ws.gemv_tasks);
+        rhs.run(r, one, one, v1);
         tmark("update", lvl, int(odd.size()));
         levels.push_back(std::move(nxt));
         ++lvl;
@@ -1716,29 +1731,32 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     for (int l = lvl - 1; l >= 0; --l) {
         const Level& cur = levels[l];
         const int sz = int(cur[0].size());
-        std::vector<GemvTask> t1, t2;
+        std::vector<GemmTask> t1, t2;
         for (int a = 0; a < ns; ++a)
             for (int o = 1; o < sz; o += 2) {
                 const Pos& p = cur[a][o];
-                cplx* vec = c.lr_vec.p + size_t(p.j) * 4 * r;
-                GemvTask w{};
+                cplx* vec = c.lr_vec.p + size_t(p.j) * r2 * m;  // r2 x m, ld r2
+                GemmTask w{};
                 if (p.RL) {
-                    t1.push_back(gemv1(p.RL, r, cur[a][o - 1].F, nb, vec));
-                    w.A[w.nseg] = p.Z; w.lda[w.nseg] = nb; w.x[w.nseg] = vec; w.n[w.nseg] = r; ++w.nseg;
+                    t1.push_back(gemm1(p.RL, r, cur[a][o - 1].F, nb, nb, vec, r2));
+                    w.A[w.nseg] = p.Z; w.lda[w.nseg] = nb; w.B[w.nseg] = vec; w.ldb[w.nseg] = r2; w.K[w.nseg] = r;
+                    ++w.nseg;
                 }
                 if (p.RU && o + 1 < sz) {
-                    t1.push_back(gemv1(p.RU, r, cur[a][o + 1].F, nb, vec + r));
-                    w.A[w.nseg] = p.Z + size_t(nb) * r; w.lda[w.nseg] = nb; w.x[w.nseg] = vec + r;
-                    w.n[w.nseg] = r;
+                    t1.push_back(gemm1(p.RU, r, cur[a][o + 1].F, nb, nb, vec + r, r2));
+                    w.A[w.nseg] = p.Z + size_t(nb) * r; w.lda[w.nseg] = nb; w.B[w.nseg] = vec + r;
+                    w.ldb[w.nseg] = r2;
+                    w.K[w.nseg] = r;
                     ++w.nseg;
                 }
                 if (w.nseg) {
-                    w.y = p.F;
+                    w.C = p.F;
+                    w.ldc = nb;
                     t2.push_back(w);
                 }
             }
-        zgemv_batched(r, one, zero, t1, s, c.ws.gemv_tasks);
-        zgemv_batched(nb, mone, one, t2, s, c.ws.gemv_tasks);
+        rhs.run(r, one, zero, t1);
+        rhs.run(nb, mone, one, t2);
     }
     tmark("backsub", lvl, 0);
     if (trace) {

@@ -440,6 +440,30 @@ int qps_sweep(qps_ctx* h, int n, const double* theta, int K, int mode, double* R
     });
 }
 
+int qps_plan_sweep(qps_ctx* h, int n_alpha, double theta_lo, double theta_hi, int cap, double* theta,
+                   int* alpha_group, int* n_angles) {
+    return guarded(h, [&](Ctx& c) {
+        need(c.have_prob, "make_problem first (sets k_1)");
+        const std::vector<double> th = plan_sweep_angles(c.prob.k.front(), c.geo.d, n_alpha, theta_lo, theta_hi);
+        for (int j = 0; j < int(th.size()) && j < cap; ++j) {
+            if (theta) theta[j] = th[j];
+            if (alpha_group) alpha_group[j] = j % n_alpha;
+        }
+        if (n_angles) *n_angles = int(th.size());
+    });
+}
+
+int qps_sweep_info(const qps_ctx* h, int cap, int* alpha_group, int* n_groups, uint64_t* n_interior,
+                   uint64_t* n_factorizations) {
+    if (!h) return QPS_ERR_USAGE;
+    const Ctx& c = h->c;
+    for (int a = 0; alpha_group && a < cap && a < int(c.sweep_group.size()); ++a) alpha_group[a] = c.sweep_group[a];
+    if (n_groups) *n_groups = c.sweep_ngroups;
+    if (n_interior) *n_interior = c.sweep_interior;
+    if (n_factorizations) *n_factorizations = c.sweep_factorizations;
+    return QPS_OK;
+}
+
 int qps_evaluate_field(qps_ctx* h, int n, const double* xy, qps_cplx* u_scat, qps_cplx* u_tot, int* region,
                        int* layer) {
     return guarded(h, [&](Ctx& c) {

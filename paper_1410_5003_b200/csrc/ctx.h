@@ -190,6 +190,17 @@ struct Ctx {
     DBuf<cplx> rc_probe;               // the probe columns (nb x 4)
     int rc_probe_n = 0;
     bool anorm_pending = false;        // rc_anorm being computed on side2 (ev_anorm)
+    int nrhs = 1;                      // right-hand sides per block of the next block solve (> 1: caller fills F)
+    bool skip_corners = false;         // schur(): interior elimination only (alpha-grouped sweep)
+    bool xint_shared = false;          // recover(): every system uses system 0's interior X
+    // alpha-grouped sweep: per-angle corner problems, multi-RHS solution, capacitance systems
+    DBuf<cplx> ag_Q, ag_R, ag_X, ag_eta, ag_cap, ag_w, ag_dinv;
+    DBuf<int> ag_piv, ag_flag;
+    CodSet cod_ag;
+    std::vector<int> sweep_group;      // last sweep: alpha group of every angle (-1: not solved)
+    int sweep_ngroups = 0;
+    uint64_t sweep_interior = 0, sweep_factorizations = 0;  // interior eliminations / block factorizations
+    uint64_t n_factorizations = 0;     // block-solve factorizations performed (the sweep's per-group counter)
     DBuf<cplx> bcr_copy, bcr_cdinv;    // dense reduction: factored copies of the even blocks (rcond test)
     DBuf<int> bcr_cpiv;
     HBuf<int> rc_flag_h;
@@ -267,7 +278,8 @@ void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa
 void spectrum_of(const Problem& p, double d, const cplx* aU, const cplx* aD, double* R, double* T, double* fe,
                  double* kappa, cplx* kU, cplx* kD, int* pu, int* pd);
 // W blocks of Q' and the RHS f of every system of the batch (host, O(M K) + O(N))
-void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs);
+// (Qdst: the corner Q' blocks to write W into, default c.Qc)
+void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs, cplx* Qdst = nullptr);
 // identity on the unused diagonal of padded A_jj blocks, every system
 void pad_identity(Ctx& c);
 // precompute_shift_blocks (assembly.hpp:212-287) into c.cache_pool
@@ -280,6 +292,10 @@ void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, 
 // multi-angle sweep; mode 0 accelerated (cache once, angles batched), 1 independent
 void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe, cplx* aU,
                cplx* aD, int* status);
+// plan_sweep: angles on the alpha grid of n distinct alphas in (th_lo, th_hi)
+std::vector<double> plan_sweep_angles(double k1, double d, int n_alpha, double th_lo, double th_hi);
+// alpha group of each listed problem (|alpha_a - alpha_b| <= 1e-12)
+std::vector<int> group_by_alpha(const std::vector<Problem>& probs, const std::vector<int>& ids, int* ngroups);
 
 struct Timer {
     Ctx& c;

@@ -143,4 +143,34 @@ struct Workspace {
     std::vector<GemmTask> h_gemm;
 };
 
+// Products on the right-hand sides of a block solve: m = 1 (one solve per
+// system) runs them as batched GEMVs, m > 1 (several right-hand sides, e.g.
+// the alpha-grouped sweep) as batched GEMMs with N = m.
+struct RhsOps {
+    int m;
+    cudaStream_t s;
+    Workspace& ws;
+    inline void run(int M, cplx alpha, cplx beta, const std::vector<GemmTask>& t) {
+        if (t.empty()) return;
+        if (m > 1) {
+            zgemm_batched(M, m, alpha, beta, t, s, ws.gemm_tasks, "wb_rhs");
+            return;
+        }
+        std::vector<GemvTask> v(t.size());
+        for (size_t q = 0; q < t.size(); ++q) {
+            GemvTask g{};
+            g.nseg = t[q].nseg;
+            for (int k = 0; k < g.nseg; ++k) {
+                g.A[k] = t[q].A[k];
+                g.lda[k] = t[q].lda[k];
+                g.x[k] = t[q].B[k];
+                g.n[k] = t[q].K[k];
+            }
+            g.y = t[q].C;
+            v[q] = g;
+        }
+        zgemv_batched(M, alpha, beta, v, s, ws.gemv_tasks);
+    }
+};
+
 }  // namespace qpsb

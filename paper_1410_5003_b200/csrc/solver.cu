@@ -724,13 +724,17 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
         fams.push_back(std::move(f));
     }
     // corners: X_first = qsolve(Q'_1, C'_1), X_last = qsolve(Q'_{I+1}, C'_{I+1}), on the side stream
-    c.cod_c.ensure(2 * ns, D.mC, D.pC, nb);
-    {
+    // (not here for the alpha-grouped sweep: its corners are solved per angle,
+    // periodize.hpp:96-121, and enter the block solve as a low-rank correction)
+    const bool corners = !c.skip_corners;
+    if (corners) {
+        c.cod_c.ensure(2 * ns, D.mC, D.pC, nb);
         QFamily f;
         f.cs = &c.cod_c; f.Q = c.Qc.p; f.R = c.Rc.p; f.ldR = D.mC; f.Rstride = size_t(D.mC) * nb;
         f.X = c.Xc.p; f.ldX = D.pC; f.Xstride = size_t(D.pC) * nb; f.lsq_out = lc.data(); f.s = c.side;
         fams.push_back(std::move(f));
     }
+    (void)corners;
     // the side stream starts after everything queued so far (the fill) on the main stream
     QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
     QPS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
@@ -803,10 +807,12 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
     }
     zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks, "schur_update");
     qsolve_poll(c, fams, false);  // the corner least squares (side stream)
-    // the corner terms: the main stream joins the corner stream here
-    QPS_CUDA(cudaEventRecord(c.ev_fork, c.side));
-    QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_fork, 0));
-    zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, ctasks, c.stream, c.ws.gemm_tasks, "schur_update");
+    if (corners) {
+        // the corner terms: the main stream joins the corner stream here
+        QPS_CUDA(cudaEventRecord(c.ev_fork, c.side));
+        QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_fork, 0));
+        zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, ctasks, c.stream, c.ws.gemm_tasks, "schur_update");
+    }
     qsolve_collect(fams);  // per-layer LSQ residuals, read back while the update runs
     for (int a = 0; a < ns; ++a) {
         double* l = c.lsq_all.data() + size_t(a) * (I + 1);
@@ -842,10 +848,11 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     c.lr_probe_worst = 0;
     c.bcr_path = 0;
     c.anorm_pending = false;
-    if (!dense_only && !lr_direct) wb_anorm_async(c, Ad);  // overlaps the compression
+    if (!dense_only && (!lr_direct || c.nrhs > 1)) wb_anorm_async(c, Ad);  // overlaps the compression
     if (!dense_only && lr_compress(c, Au, Al)) {
-        c.bcr_path = lr_direct ? 2 : 1;
-        if (lr_direct) bcr_solve_lr(c, Ad);
+        const bool direct = lr_direct && c.nrhs == 1;  // several right-hand sides: the Woodbury form
+        c.bcr_path = direct ? 2 : 1;
+        if (direct) bcr_solve_lr(c, Ad);
         else bcr_solve_wb(c, Ad);
         c.couplings_deferred = false;
         return;
@@ -865,11 +872,18 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     const int I = D.I, nb = D.nb, ns = D.nsys;
     const size_t nb2 = D.nb2();
     cudaStream_t s = c.stream;
-    c.F.ensure(size_t(ns) * I * nb);
-    c.F.zero(s);
-    for (int a = 0; a < ns; ++a)
-        QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
-                                 cudaMemcpyDeviceToDevice, s));
+    ++c.n_factorizations;
+    // right-hand sides: m = c.nrhs columns per block (nb x m); m = 1: f on block 0
+    const int m = std::max(1, c.nrhs);
+    const size_t fs = size_t(nb) * m;
+    RhsOps rhs{m, s, c.ws};
+    if (m == 1) {
+        c.F.ensure(size_t(ns) * I * nb);
+        c.F.zero(s);
+        for (int a = 0; a < ns; ++a)
+            QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
+                                     cudaMemcpyDeviceToDevice, s));
+    }
     c.ipiv.ensure(size_t(ns) * I * nb);
     const size_t dsz = lu_dinv_elems(nb);
     c.dinv.ensure(size_t(ns) * I * dsz);
@@ -884,7 +898,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             L0[a].D.push_back(Ada + j * nb2);
             L0[a].L.push_back(j >= 1 ? Ala + (j - 1) * nb2 : nullptr);
             L0[a].U.push_back(j + 1 < I ? Aua + j * nb2 : nullptr);
-            L0[a].F.push_back(c.F.p + (size_t(a) * I + j) * nb);
+            L0[a].F.push_back(c.F.p + (size_t(a) * I + j) * fs);
         }
     }
     c.levels.push_back(L0);
@@ -984,7 +998,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                     va.push_back(cur[a].D[o]); vp.push_back(ipiv_of(a, j)); vd.push_back(dinv_of(a, j)); vb.push_back(cur[a].F[o]);
                 }
             lu_solve_batched(nb, nb, ma, mp, md, mb, nb, nb, s, c.ws);
-            lu_solve_batched(nb, nb, va, vp, vd, vb, nb, 1, s, c.ws);
+            lu_solve_batched(nb, nb, va, vp, vd, vb, nb, m, s, c.ws);
         }
         tmark("solve", lvl, sz / 2);
         // 3. updates of the even positions
@@ -995,7 +1009,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         LB.ensure(size_t(ns) * nsz * nb2);
         UB.ensure(size_t(ns) * nsz * nb2);
         std::vector<GemmTask> upd, fresh;
-        std::vector<GemvTask> vtasks;
+        std::vector<GemmTask> vtasks;
         for (int a = 0; a < ns; ++a) {
             const BcrLevel& cu = cur[a];
             for (int e = 0; e < sz; e += 2) {
@@ -1005,16 +1019,18 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                 nxt[a].D.push_back(cu.D[e]);
                 nxt[a].F.push_back(cu.F[e]);
                 GemmTask t{};
-                GemvTask v{};
+                GemmTask v{};
                 if (hm) {  // D_e -= L_e Y_U(e-1);  f_e -= L_e y_f(e-1)
                     t.A[t.nseg] = cu.L[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cu.U[e - 1]; t.ldb[t.nseg] = nb;
                     t.K[t.nseg] = nb; ++t.nseg;
-                    v.A[v.nseg] = cu.L[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cu.F[e - 1]; v.n[v.nseg] = nb; ++v.nseg;
+                    v.A[v.nseg] = cu.L[e]; v.lda[v.nseg] = nb; v.B[v.nseg] = cu.F[e - 1]; v.ldb[v.nseg] = nb;
+                    v.K[v.nseg] = nb; ++v.nseg;
                 }
                 if (hp) {  // D_e -= U_e Y_L(e+1);  f_e -= U_e y_f(e+1)
                     t.A[t.nseg] = cu.U[e]; t.lda[t.nseg] = nb; t.B[t.nseg] = cu.L[e + 1]; t.ldb[t.nseg] = nb;
                     t.K[t.nseg] = nb; ++t.nseg;
-                    v.A[v.nseg] = cu.U[e]; v.lda[v.nseg] = nb; v.x[v.nseg] = cu.F[e + 1]; v.n[v.nseg] = nb; ++v.nseg;
+                    v.A[v.nseg] = cu.U[e]; v.lda[v.nseg] = nb; v.B[v.nseg] = cu.F[e + 1]; v.ldb[v.nseg] = nb;
+                    v.K[v.nseg] = nb; ++v.nseg;
                 }
                 if (t.nseg) {
                     t.C = cu.D[e];
@@ -1022,7 +1038,8 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                     upd.push_back(t);
                 }
                 if (v.nseg) {
-                    v.y = cu.F[e];
+                    v.C = cu.F[e];
+                    v.ldc = nb;
                     vtasks.push_back(v);
                 }
                 // new couplings: L'_e = -L_e Y_L(e-1) (to e-2), U'_e = -U_e Y_U(e+1) (to e+2)
@@ -1055,7 +1072,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
                     (unsigned long long)g_zgemm_launches.load());
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, upd, s, c.ws.gemm_tasks, "bcr_update");
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{0, 0}, fresh, s, c.ws.gemm_tasks, "bcr_update");
-        zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vtasks, s, c.ws.gemv_tasks);
+        rhs.run(nb, cplx{-1, 0}, cplx{1, 0}, vtasks);
         tmark("update", lvl, sz / 2);
         c.levels.push_back(nxt);
         ++lvl;
@@ -1074,26 +1091,29 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
             orig.push_back(last[a].idx[0]);
         }
         factor(fa, fp, fd, orig);
-        lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, 1, s, c.ws);
+        lu_solve_batched(nb, nb, fa, fp, fd, vb, nb, m, s, c.ws);
     }
     tmark("last", lvl, 1);
     // back substitution: eta_o = y_f(o) - Y_L(o) eta_{o-1} - Y_U(o) eta_{o+1}; F ends up holding eta
     for (int l = lvl - 1; l >= 0; --l) {
         const BcrLevels& cur = c.levels[l];
         const int sz = int(cur[0].idx.size());
-        std::vector<GemvTask> vt;
+        std::vector<GemmTask> vt;
         for (int a = 0; a < ns; ++a)
             for (int o = 1; o < sz; o += 2) {
-                GemvTask v{};
-                v.A[v.nseg] = cur[a].L[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur[a].F[o - 1]; v.n[v.nseg] = nb; ++v.nseg;
+                GemmTask v{};
+                v.A[v.nseg] = cur[a].L[o]; v.lda[v.nseg] = nb; v.B[v.nseg] = cur[a].F[o - 1]; v.ldb[v.nseg] = nb;
+                v.K[v.nseg] = nb; ++v.nseg;
                 if (o + 1 < sz) {
-                    v.A[v.nseg] = cur[a].U[o]; v.lda[v.nseg] = nb; v.x[v.nseg] = cur[a].F[o + 1]; v.n[v.nseg] = nb;
+                    v.A[v.nseg] = cur[a].U[o]; v.lda[v.nseg] = nb; v.B[v.nseg] = cur[a].F[o + 1]; v.ldb[v.nseg] = nb;
+                    v.K[v.nseg] = nb;
                     ++v.nseg;
                 }
-                v.y = cur[a].F[o];
+                v.C = cur[a].F[o];
+                v.ldc = nb;
                 vt.push_back(v);
             }
-        zgemv_batched(nb, cplx{-1, 0}, cplx{1, 0}, vt, s, c.ws.gemv_tasks);
+        rhs.run(nb, cplx{-1, 0}, cplx{1, 0}, vt);
     }
     tmark("backsub", lvl, 0);
     c.eta_valid = true;
@@ -1125,7 +1145,8 @@ void recover(Ctx& c) {
     zgemv_batched(D.pC, cplx{-1, 0}, cplx{0, 0}, vt, s, c.ws.gemv_tasks);
     std::vector<GemvTask> it;
     for (int a = 0; a < ns; ++a) {
-        const cplx* Xi = c.Xint.p + size_t(a) * D.sXi();
+        // the alpha-grouped sweep's angles share one interior elimination
+        const cplx* Xi = c.Xint.p + (c.xint_shared ? 0 : size_t(a) * D.sXi());
         const cplx* Fa = c.F.p + size_t(a) * I * nb;
         for (int i = 1; i <= I - 1; ++i) {
             GemvTask v{};
@@ -1223,7 +1244,8 @@ void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa
 }
 
 // W blocks (assembly.hpp:414-427) and f (assembly.hpp:431-441) on the host: O(M K) + O(N) per system
-void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs) {
+void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs, cplx* Qdst) {
+    if (!Qdst) Qdst = c.Qc.p;
     const Dims& D = c.dims;
     const HostGeometry& g = c.geo;
     const int M = D.M, K = D.K, nrb = D.nrb, nb = D.nb;
@@ -1262,7 +1284,7 @@ void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs) {
     h2d_staged(c.wtmp.p, W.data(), sizeof(cplx) * W.size(), s);
     for (int a = 0; a < ns; ++a)
         for (int side = 0; side < 2; ++side) {
-            cplx* dst = c.Qc.p + size_t(a) * D.sQc() + size_t(side) * D.mC * D.pC + size_t(D.P) * D.mC + 2 * D.Mw;
+            cplx* dst = Qdst + size_t(a) * D.sQc() + size_t(side) * D.mC * D.pC + size_t(D.P) * D.mC + 2 * D.Mw;
             QPS_CUDA(cudaMemcpy2DAsync(dst, sizeof(cplx) * D.mC, c.wtmp.p + size_t(2 * a + side) * 2 * M * nrb,
                                        sizeof(cplx) * 2 * M, sizeof(cplx) * 2 * M, nrb, cudaMemcpyDeviceToDevice, s));
         }

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <complex>
 #include <cstdlib>
+#include <cstring>
+#include <utility>
 
 #include "ctx.h"
 #include "prof.h"
@@ -492,10 +494,233 @@ size_t per_system_bytes(const Dims& D) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Alpha grouping.  The system matrix
+// depends on theta only through alpha = exp(i d k_1 cos theta); the Rayleigh-
+// Bloch columns W of the corner blocks Q'_1, Q'_{I+1} (and the right-hand side
+// f) depend on theta itself (kappa_n = k_1 cos theta + 2 pi n / d).  Angles
+// whose alphas agree to kAlphaTol form a group.
+// ---------------------------------------------------------------------------
+constexpr double kAlphaTol = 1e-12;
+
+std::vector<int> group_by_alpha(const std::vector<Problem>& probs, const std::vector<int>& ids, int* ngroups) {
+    std::vector<int> g(ids.size(), -1);
+    std::vector<std::pair<double, double>> reps;
+    for (size_t q = 0; q < ids.size(); ++q) {
+        const Problem& p = probs[ids[q]];
+        for (size_t r = 0; r < reps.size(); ++r)
+            if (std::hypot(p.ar - reps[r].first, p.ai - reps[r].second) <= kAlphaTol) {
+                g[q] = int(r);
+                break;
+            }
+        if (g[q] < 0) {
+            g[q] = int(reps.size());
+            reps.push_back({p.ar, p.ai});
+        }
+    }
+    *ngroups = int(reps.size());
+    return g;
+}
+
+std::vector<double> plan_sweep_angles(double k1, double d, int n_alpha, double th_lo, double th_hi) {
+    // "a uniform grid ... with spacing 2 pi / (n d k_1)" so
+    // that only n distinct alphas occur -- uniform in cos(theta) (i.e. in
+    // kappa_0 = k_1 cos theta with spacing 2 pi / (n d)): alpha_j = alpha_0
+    // exp(2 pi i j / n) repeats with period n.  Incidence from above:
+    // theta in (-pi, 0), where cos is increasing.
+    if (n_alpha < 1) fail(QPS_ERR_CONFIG, "plan_sweep: n >= 1 alpha values required");
+    if (!(th_lo > -kPi && th_hi < 0.0 && th_lo < th_hi))
+        fail(QPS_ERR_CONFIG, "plan_sweep: theta range must satisfy -pi < lo < hi < 0");
+    const double klo = k1 * std::cos(th_lo), khi = k1 * std::cos(th_hi), dk = 2.0 * kPi / (n_alpha * d);
+    std::vector<double> th;
+    for (int j = 0;; ++j) {
+        const double kap = klo + (j + 0.5) * dk;
+        if (kap >= khi) break;
+        th.push_back(-std::acos(kap / k1));
+    }
+    return th;
+}
+
+// One alpha group solved with a single interior elimination and a single
+// block factorization ("periodized factorization computed exactly
+// once per alpha group"): the corner eliminations are the only theta-dependent
+// Schur terms and they change A'_{0,0} and A'_{I-1,I-1} by
+//   -B_self[0] X_first[:P] and -B_below[I-1] X_last[:P]       (periodize.hpp:115,119),
+// i.e. A(theta) = A_alpha - B V(theta)^* with B = [B_self[0] e_0 | B_below[I-1] e_{I-1}]
+// theta-independent (alpha-free, cache) and V^* the corner X's first P rows.
+// One block cyclic reduction of A_alpha with m = 2P + g right-hand sides gives
+// Z = A_alpha^{-1} B and y_t = A_alpha^{-1} f_t; per angle the Woodbury identity
+//   eta_t = y_t + Z (I - V_t^* Z)^{-1} V_t^* y_t          (2P x 2P capacitance)
+// then recovery as usual.
+void solve_alpha_group(Ctx& c, const std::vector<Problem>& gp, qps_phase_times& tm) {
+    const int g = int(gp.size());
+    c.prob = gp[0];
+    c.dims.nsys = 1;
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, P = D.P, mC = D.mC, pC = D.pC;
+    cudaStream_t s = c.stream;
+    auto timed = [&](double* slot, auto&& f) {
+        double ms = 0;
+        {
+            Timer t(c, &ms);
+            f();
+        }
+        *slot += ms;
+    };
+    timed(&tm.assemble_ms, [&] { assemble_from_cache(c, {gp[0]}); });
+    lr_sample_async(c);
+    timed(&tm.schur_ms, [&] {
+        c.skip_corners = true;
+        try {
+            schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true);
+        } catch (...) {
+            c.skip_corners = false;
+            throw;
+        }
+        c.skip_corners = false;
+        ++c.sweep_interior;
+        // the corner problems of every angle: Q'(theta_t) = [[Q 0]; [V W(theta_t)]], C' shared
+        c.ag_Q.ensure(size_t(g) * D.sQc());
+        c.ag_R.ensure(size_t(g) * D.sRc());
+        c.ag_X.ensure(size_t(g) * D.sXc());
+        for (int t = 0; t < g; ++t) {
+            QPS_CUDA(cudaMemcpyAsync(c.ag_Q.p + size_t(t) * D.sQc(), c.Qc.p, sizeof(cplx) * D.sQc(),
+                                     cudaMemcpyDeviceToDevice, s));
+            QPS_CUDA(cudaMemcpyAsync(c.ag_R.p + size_t(t) * D.sRc(), c.Rc.p, sizeof(cplx) * D.sRc(),
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+        c.dims.nsys = g;
+        write_radiation_and_rhs(c, gp, c.ag_Q.p);  // W of each angle; f of each angle into c.f (g x nb)
+        c.dims.nsys = 1;
+        c.cod_ag.ensure(2 * g, mC, pC, nb);
+        std::vector<double> lc(2 * size_t(g));
+        qsolve_family_public(c, c.cod_ag, c.ag_Q.p, c.ag_R.p, mC, size_t(mC) * nb, c.ag_X.p, pC, size_t(pC) * nb,
+                             lc.data());
+        c.lsq_all.resize(size_t(g) * (I + 1));
+        for (int t = g - 1; t >= 0; --t) {
+            for (int i = 1; i < I; ++i) c.lsq_all[size_t(t) * (I + 1) + i] = c.lsq_all[i];
+            c.lsq_all[size_t(t) * (I + 1)] = lc[2 * t];
+            c.lsq_all[size_t(t) * (I + 1) + I] = lc[2 * t + 1];
+        }
+    });
+    const int m = 2 * P + g;
+    const size_t fs = size_t(nb) * m;
+    timed(&tm.solve_ms, [&] {
+        // right-hand sides [B_self[0] | B_below[I-1] | f_1 .. f_g] (blocks 0 and I-1)
+        c.F.ensure(size_t(I) * fs);
+        c.F.zero(s);
+        QPS_CUDA(cudaMemcpyAsync(c.F.p, c.Bself.p, sizeof(cplx) * nb * P, cudaMemcpyDeviceToDevice, s));
+        QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(I - 1) * fs + size_t(P) * nb, c.Bbelow.p + size_t(I - 1) * nb * P,
+                                 sizeof(cplx) * nb * P, cudaMemcpyDeviceToDevice, s));
+        QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(2 * P) * nb, c.f.p, sizeof(cplx) * nb * g, cudaMemcpyDeviceToDevice,
+                                 s));
+        c.nrhs = m;
+        try {
+            bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+        } catch (...) {
+            c.nrhs = 1;
+            throw;
+        }
+        c.nrhs = 1;
+        ++c.sweep_factorizations;
+        // capacitance C_t = I - V_t^* Z (2P x 2P) and w_t = V_t^* y_t per angle
+        const int p2 = 2 * P;
+        c.ag_cap.ensure(size_t(g) * p2 * p2);
+        c.ag_w.ensure(size_t(g) * p2);
+        {
+            std::vector<cplx> eye(size_t(g) * p2 * p2, cplx{0, 0});
+            for (int t = 0; t < g; ++t)
+                for (int i = 0; i < p2; ++i) eye[size_t(t) * p2 * p2 + size_t(i) * p2 + i] = cplx{1, 0};
+            c.ag_cap.upload(eye, s);
+        }
+        std::vector<GemmTask> ct;
+        std::vector<GemvTask> wt;
+        for (int t = 0; t < g; ++t) {
+            const cplx* Xf = c.ag_X.p + size_t(t) * D.sXc();
+            const cplx* Xl = Xf + size_t(pC) * nb;
+            cplx* Ct = c.ag_cap.p + size_t(t) * p2 * p2;
+            GemmTask a{};
+            a.nseg = 1; a.A[0] = Xf; a.lda[0] = pC; a.B[0] = c.F.p; a.ldb[0] = nb; a.K[0] = nb; a.C = Ct; a.ldc = p2;
+            ct.push_back(a);
+            a.A[0] = Xl; a.B[0] = c.F.p + size_t(I - 1) * fs; a.C = Ct + P;
+            ct.push_back(a);
+            GemvTask v{};
+            v.nseg = 1; v.A[0] = Xf; v.lda[0] = pC; v.x[0] = c.F.p + size_t(p2 + t) * nb; v.n[0] = nb;
+            v.y = c.ag_w.p + size_t(t) * p2;
+            wt.push_back(v);
+            v.A[0] = Xl; v.x[0] = c.F.p + size_t(I - 1) * fs + size_t(p2 + t) * nb; v.y = c.ag_w.p + size_t(t) * p2 + P;
+            wt.push_back(v);
+        }
+        zgemm_batched(P, p2, cplx{-1, 0}, cplx{1, 0}, ct, s, c.ws.gemm_tasks, "ag_cap");
+        zgemv_batched(P, cplx{1, 0}, cplx{0, 0}, wt, s, c.ws.gemv_tasks);
+        // s_t = C_t^{-1} w_t (LU with the rcond test: a singular capacitance is a
+        // singular A(theta_t), reported by the caller's per-angle fallback)
+        const size_t dsz = lu_dinv_elems(p2);
+        c.ag_dinv.ensure(size_t(g) * dsz);
+        c.ag_piv.ensure(size_t(g) * p2);
+        c.ag_flag.ensure(g);
+        c.ag_flag.zero(s);
+        std::vector<cplx*> ca, cd, cw;
+        std::vector<int*> cp;
+        for (int t = 0; t < g; ++t) {
+            ca.push_back(c.ag_cap.p + size_t(t) * p2 * p2);
+            cd.push_back(c.ag_dinv.p + size_t(t) * dsz);
+            cp.push_back(c.ag_piv.p + size_t(t) * p2);
+            cw.push_back(c.ag_w.p + size_t(t) * p2);
+        }
+        lu_factor_batched(p2, p2, ca, cp, cd, c.ag_flag.p, s, c.ws);
+        lu_rcond_batched(p2, p2, c.ws.ptrs.p, nullptr, 0, c.ws.ptrs3.p, nullptr, 0, g, kRcondMin, c.ag_flag.p,
+                         nullptr, s);
+        std::vector<int> hf(g);
+        QPS_D2H(hf.data(), c.ag_flag.p, sizeof(int) * g, s);
+        lu_solve_batched(p2, p2, ca, cp, cd, cw, p2, 1, s, c.ws);
+        // eta_t = y_t + Z s_t, every block
+        c.ag_eta.ensure(size_t(g) * I * nb);
+        for (int t = 0; t < g; ++t)
+            QPS_CUDA(cudaMemcpy2DAsync(c.ag_eta.p + size_t(t) * I * nb, sizeof(cplx) * nb,
+                                       c.F.p + size_t(p2 + t) * nb, sizeof(cplx) * fs, sizeof(cplx) * nb, I,
+                                       cudaMemcpyDeviceToDevice, s));
+        std::vector<GemvTask> et;
+        for (int t = 0; t < g; ++t)
+            for (int j = 0; j < I; ++j) {
+                GemvTask v{};
+                v.nseg = 1; v.A[0] = c.F.p + size_t(j) * fs; v.lda[0] = nb; v.x[0] = c.ag_w.p + size_t(t) * p2;
+                v.n[0] = p2; v.y = c.ag_eta.p + (size_t(t) * I + j) * nb;
+                et.push_back(v);
+            }
+        zgemv_batched(nb, cplx{1, 0}, cplx{1, 0}, et, s, c.ws.gemv_tasks);
+        QPS_CUDA(cudaStreamSynchronize(s));
+        for (int t = 0; t < g; ++t)
+            if (hf[t]) fail(QPS_ERR_SOLVER, "alpha group: singular corner capacitance");
+    });
+    timed(&tm.recover_ms, [&] {
+        std::swap(c.F, c.ag_eta);
+        std::swap(c.Xc, c.ag_X);
+        c.dims.nsys = g;
+        c.xint_shared = true;
+        try {
+            recover(c);
+        } catch (...) {
+            std::swap(c.F, c.ag_eta);
+            std::swap(c.Xc, c.ag_X);
+            c.dims.nsys = 1;
+            c.xint_shared = false;
+            throw;
+        }
+        std::swap(c.F, c.ag_eta);
+        std::swap(c.Xc, c.ag_X);
+        c.dims.nsys = 1;
+        c.xint_shared = false;
+    });
+}
+
 void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe, cplx* aU,
                cplx* aD, int* status) {
     const Problem orig = c.prob;
     const double omega = orig.omega;
+    c.sweep_interior = c.sweep_factorizations = 0;
+    c.sweep_ngroups = 0;
+    c.sweep_group.assign(n, -1);
     const int nrb = 2 * K + 1;
     const double nan = std::nan("");
     std::vector<Problem> probs(n);
@@ -563,6 +788,8 @@ void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, d
                 timed(&tm.schur_ms, [&] { schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true); });
                 c.sys_valid = false;
                 timed(&tm.solve_ms, [&] { bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p); });
+                c.sweep_interior += ids.size();  // one independent system per angle
+                c.sweep_factorizations += ids.size();
                 timed(&tm.recover_ms, [&] { recover(c); });
                 for (size_t q = 0; q < ids.size(); ++q) {
                     const int id = ids[q];
@@ -578,8 +805,55 @@ void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, d
                     }
                 }
             };
-            for (size_t b0 = 0; b0 < todo.size(); b0 += B) {
-                const std::vector<int> ids(todo.begin() + b0, todo.begin() + std::min(todo.size(), b0 + B));
+            // alpha groups of two or more angles share one interior elimination and
+            // one factorization (mode 0); the rest go through the batched pipeline
+            std::vector<int> singles;
+            c.sweep_group.assign(n, -1);
+            {
+                int ng = 0;
+                const std::vector<int> gid = group_by_alpha(probs, todo, &ng);
+                c.sweep_ngroups = ng;
+                std::vector<std::vector<int>> members(ng);
+                for (size_t q = 0; q < todo.size(); ++q) {
+                    members[gid[q]].push_back(todo[q]);
+                    c.sweep_group[todo[q]] = gid[q];
+                }
+                static const bool no_groups = [] {  // QPS_SWEEP_GROUPS=0: every angle through the batches
+                    const char* e = std::getenv("QPS_SWEEP_GROUPS");
+                    return e && !std::strcmp(e, "0");
+                }();
+                for (auto& mb : members) {
+                    if (mode != 0 || mb.size() < 2 || no_groups) {
+                        singles.insert(singles.end(), mb.begin(), mb.end());
+                        continue;
+                    }
+                    std::vector<Problem> gp;
+                    for (int id : mb) gp.push_back(probs[id]);
+                    try {
+                        solve_alpha_group(c, gp, tm);
+                        for (size_t q = 0; q < mb.size(); ++q) {
+                            const int id = mb[q];
+                            double r, t, f;
+                            spectrum_of(gp[q], c.geo.d, c.h_aU_all.data() + q * nrb, c.h_aD_all.data() + q * nrb,
+                                        &r, &t, &f, nullptr, nullptr, nullptr, nullptr, nullptr);
+                            if (R) R[id] = r;
+                            if (T) T[id] = t;
+                            if (fe) fe[id] = f;
+                            for (int i = 0; i < nrb; ++i) {
+                                if (aU) aU[size_t(id) * nrb + i] = c.h_aU_all[q * nrb + i];
+                                if (aD) aD[size_t(id) * nrb + i] = c.h_aD_all[q * nrb + i];
+                            }
+                        }
+                    } catch (const Error& e) {
+                        if (e.status == QPS_ERR_CUDA || e.status == QPS_ERR_INTERNAL) throw;
+                        singles.insert(singles.end(), mb.begin(), mb.end());  // per-angle solves name the failure
+                    }
+                }
+                std::sort(singles.begin(), singles.end());
+            }
+            if (mode == 0) B = std::min(B, std::max(1, int(singles.size())));
+            for (size_t b0 = 0; b0 < singles.size(); b0 += B) {
+                const std::vector<int> ids(singles.begin() + b0, singles.begin() + std::min(singles.size(), b0 + B));
                 try {
                     solve_batch(ids);
                 } catch (const Error& e) {

@@ -195,6 +195,9 @@ def _bind(lib):
         "qps_evaluate_field": (C.c_int, [vp, C.c_int, P(C.c_double), vp, vp, P(C.c_int), P(C.c_int)]),
         "qps_sweep": (C.c_int, [vp, C.c_int, P(C.c_double), C.c_int, C.c_int, P(C.c_double), P(C.c_double),
                                 P(C.c_double), vp, vp, P(C.c_int)]),
+        "qps_plan_sweep": (C.c_int, [vp, C.c_int, C.c_double, C.c_double, C.c_int, P(C.c_double), P(C.c_int),
+                                     P(C.c_int)]),
+        "qps_sweep_info": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_int), P(C.c_uint64), P(C.c_uint64)]),
         "qps_download_block": (C.c_int, [vp, C.c_int, C.c_int, vp, P(C.c_int), P(C.c_int)]),
         "qps_fill_evals": (C.c_int, [vp, P(C.c_uint64), P(C.c_uint64)]),
         "qps_get_phase_times": (C.c_int, [vp, P(_Times)]),
@@ -435,6 +438,29 @@ class Solver:
         self._check(self.lib.qps_sweep(self.h, n, _dptr(th), K, mode, _dptr(R), _dptr(T), _dptr(fe),
                                        aU.ctypes.data, aD.ctypes.data, st.ctypes.data_as(C.POINTER(C.c_int))))
         return {"R": R, "T": T, "flux_error": fe, "aU": aU, "aD": aD, "status": st}
+
+    def plan_sweep(self, n_alpha: int, theta_lo: float, theta_hi: float):
+        """plan_sweep(omega, n, theta_range): angles on the grid
+        uniform in k_1 cos(theta) with n distinct alphas; returns (thetas,
+        alpha_group) for the last make_problem's k_1."""
+        cnt = C.c_int()
+        self._check(self.lib.qps_plan_sweep(self.h, n_alpha, theta_lo, theta_hi, 0, None, None, C.byref(cnt)))
+        th = np.zeros(cnt.value)
+        grp = np.zeros(cnt.value, dtype=np.int32)
+        self._check(self.lib.qps_plan_sweep(self.h, n_alpha, theta_lo, theta_hi, cnt.value, _dptr(th),
+                                            grp.ctypes.data_as(C.POINTER(C.c_int)), C.byref(cnt)))
+        return th, grp
+
+    def sweep_info(self, n: int):
+        """Last sweep: per-angle alpha_group (SpectrumRow::alpha_group), n_groups,
+        interior eliminations and block factorizations performed."""
+        grp = np.zeros(n, dtype=np.int32)
+        ng = C.c_int()
+        ni = C.c_uint64()
+        nf = C.c_uint64()
+        self._check(self.lib.qps_sweep_info(self.h, n, grp.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ng),
+                                            C.byref(ni), C.byref(nf)))
+        return {"alpha_group": grp, "n_groups": ng.value, "n_interior": ni.value, "n_factorizations": nf.value}
 
     def evaluate_field(self, points):
         """evaluate_field(sol, p, points) (postprocess.hpp:78-123) for the last

@@ -1,0 +1,74 @@
+"""Alpha-grouped multi-angle sweep (the reference has no
+sweep code, proj/tests/test_sweep.cpp:1, only the building blocks
+ShiftBlockCache, InteriorSchur / schur_interior / schur_corners,
+periodize.hpp:58-126).  On the plan_sweep grid (uniform in k_1 cos theta, n
+distinct alphas) every alpha group must be eliminated
+(interior Schur) and factored exactly once (instrumented counters), each
+angle's corners recomputed, and the per-angle Bragg amplitudes must match the
+reference composition (the oracle's mode-0 sweep: schur_interior once per group,
+schur_corners + block_lu_solve per angle) at max(1e-9, 3 x its 1-ulp floor).
+Configurations: a config-5 prefix (n = 304 >= 256: low-rank Woodbury block
+solve) and a config-2 prefix (n = 208: dense cyclic reduction), both with
+several right-hand sides."""
+import numpy as np
+import pytest
+
+from paper_1410_5003_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def setup(s, cfg, nif, omega_ulp=False):
+    st, num, om, th, K, _ = configs.config(cfg, n_interfaces=nif)
+    if omega_ulp:
+        om = float(np.nextafter(om, np.inf))
+    s.build_geometry(st, num)
+    s.make_problem(om, th, K)
+    return K
+
+
+def amps(r):
+    return np.concatenate([r["aU"], r["aD"]], axis=1)
+
+
+@pytest.mark.parametrize("cfg,nif,n_alpha,count", [(5, 6, 3, 9), (2, 3, 2, 6)])
+def test_alpha_groups_share_one_factorization(gpu, oracle, parity_report, cfg, nif, n_alpha, count):
+    K = setup(gpu, cfg, nif)
+    th, grp = gpu.plan_sweep(n_alpha, -np.pi + 0.1, -0.1)
+    assert len(th) >= count
+    th, grp = th[:count], grp[:count]
+    rg = gpu.sweep(th, K, mode=0)
+    assert np.all(rg["status"] == 0), rg["status"]
+    ig = gpu.sweep_info(count)
+    assert ig["n_groups"] == n_alpha
+    assert ig["n_interior"] == n_alpha and ig["n_factorizations"] == n_alpha, ig
+    setup(oracle, cfg, nif)
+    ro = oracle.sweep(th, K, mode=0)
+    io = oracle.sweep_info(count)
+    assert np.array_equal(ig["alpha_group"], io["alpha_group"])
+    assert np.array_equal(ig["alpha_group"] % n_alpha, grp % n_alpha)
+    assert io["n_interior"] == n_alpha and io["n_factorizations"] == count  # the reference re-solves per angle
+    setup(oracle, cfg, nif, omega_ulp=True)
+    r1 = oracle.sweep(th, K, mode=0)
+    ao, a1, ag = amps(ro), amps(r1), amps(rg)
+    floor = np.linalg.norm(a1 - ao, axis=1) / np.linalg.norm(ao, axis=1)
+    err = np.linalg.norm(ag - ao, axis=1) / np.linalg.norm(ao, axis=1)
+    w = int(np.argmax(err / np.maximum(1e-9, 3 * floor)))
+    parity_report(f"alpha-grouped sweep cfg{cfg} I={nif} ({count} angles, {n_alpha} groups)",
+                  {"bragg_rel (worst angle)": (float(err[w]), float(floor[w])),
+                   "bragg_rel (max)": (float(err.max()), float(floor.max()))})
+    assert np.all(err <= np.maximum(1e-9, 3 * floor)), (err, floor)
+    # the grouped solve against the product's own independent per-angle solves
+    gpu_ind = gpu.sweep(th, K, mode=1)
+    ei = np.linalg.norm(amps(gpu_ind) - ag, axis=1) / np.linalg.norm(ag, axis=1)
+    assert np.all(ei <= np.maximum(1e-9, 3 * floor)), (ei, floor)
+
+
+def test_uniform_angles_are_singleton_groups(gpu):
+    K = setup(gpu, 5, 4)
+    th = configs.sweep_angles(200)[::40]
+    r = gpu.sweep(th, K, mode=0)
+    assert np.all(r["status"] == 0)
+    info = gpu.sweep_info(len(th))
+    assert info["n_groups"] == len(th) and list(info["alpha_group"]) == list(range(len(th)))
+    assert info["n_factorizations"] == len(th)

@@ -126,3 +126,25 @@ def test_solvability_checks(host, oracle):
         s.make_problem(3.0, -1.0, 8)
         with pytest.raises(ConfigError):
             s.precompute_shift_blocks()
+
+
+def test_plan_sweep_grid_matches_oracle(host, oracle):
+    """plan_sweep: identical angle grids and alpha groups
+    (j mod n) from the product's host code and the oracle; every group's
+    angles share alpha = exp(i d k_1 cos theta) to 1e-12."""
+    st, num, om, th, K, _ = configs.config(5, n_interfaces=3)
+    for s in (host, oracle):
+        s.build_geometry(st, num)
+        s.make_problem(om, th, K)
+    tg, gg = host.plan_sweep(4, -math.pi + 0.1, -0.1)
+    to, go = oracle.plan_sweep(4, -math.pi + 0.1, -0.1)
+    assert np.array_equal(tg, to) and np.array_equal(gg, go)
+    assert len(tg) >= 8 and np.all(np.diff(tg) > 0) and np.all((tg > -math.pi) & (tg < 0))
+    alpha = np.exp(1j * st.d * om * np.cos(tg))
+    for g in range(4):
+        a = alpha[gg == g]
+        assert np.abs(a - a[0]).max() < 1e-12
+    with pytest.raises(ConfigError):
+        host.plan_sweep(0, -1.0, -0.5)
+    with pytest.raises(ConfigError):
+        oracle.plan_sweep(2, -0.5, -1.0)
