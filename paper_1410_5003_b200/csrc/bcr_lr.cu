@@ -55,6 +55,14 @@ constexpr int kRcProbe = 4;
 constexpr double kRcSuspect = 1e-10;
 constexpr double kLrProbeTol = 1e-12;
 constexpr int kLrMaxRank = 48;   // beyond this the dense reduction is used
+// width of the compressed bases (>= any accepted rank; QPS_LR_BASIS overrides, <= kLrSample)
+int lr_basis() {
+    static const int b = [] {
+        const char* e = getenv("QPS_LR_BASIS");
+        return e ? std::max(kLrMaxRank, std::min(kLrSample, atoi(e))) : kLrMaxRank;
+    }();
+    return b;
+}
 constexpr double kLrTol = 1e-14; // relative pivot threshold of the sample's CPQR
 
 // P_b = first r columns of Q (Q^* = H_{r-1} ... H_0 as applied by the CPQR, so
@@ -832,7 +840,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         QPS_D2H(c.lr_rank_h.p, cs.rank.p, sizeof(int) * nc, s);
         QPS_CUDA(cudaEventRecord(c.ev_sample, s));
         rank_deferred = true;
-        r = kLrMaxRank;
+        r = lr_basis();
         c.lr_r = r;
         // Q2 = first r columns of the R-CPQR's Q (64 x r)
         c.lr_Q2.ensure(size_t(nc) * p * r);
@@ -883,7 +891,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         if (r > kLrMaxRank) return false;
         // a fixed basis width keeps every system's factors independent of the batch
         // it is solved in (the sweep's batched and one-at-a-time results agree)
-        r = kLrMaxRank;
+        r = lr_basis();
         c.lr_r = r;
         // P (n x r) and P^* (r x n)
         c.lr_P.ensure(size_t(nc) * nb * r);

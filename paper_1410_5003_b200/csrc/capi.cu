@@ -391,7 +391,11 @@ int qps_solve(qps_ctx* h) {
         lr_sample_async(c);  // overlaps the Schur least squares
         {
             Timer t(c, &c.times.schur_ms);
-            schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true);
+            static const bool no_defer = [] {  // QPS_DEFER=0: form the coupling updates explicitly (A/B)
+                const char* e = getenv("QPS_DEFER");
+                return e && !strcmp(e, "0");
+            }();
+            schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, !no_defer);
         }
         c.sys_valid = false;  // A now holds A'
         {
