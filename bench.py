@@ -183,6 +183,77 @@ def cpu_baseline(I_sample, threads, reps=1):
             "seconds": best, "kernel_evals_per_s": evals / ((ph["fill_ms"] + ph["assemble_ms"]) * 1e-3)}
 
 
+def sweep_measure(device, ref_angles):
+    """Config 5 (BASELINE configs[4]): 100 interfaces, N = 150, K = 20, 200
+    angles uniform in [-pi + 0.1, -0.1].  GPU wall time (host clock around the
+    C-ABI call, device synchronised inside it) of the accelerated sweep (cache
+    filled once, angles batched; no two of these angles share alpha) and of
+    independent per-angle solves; the same sweep on the paper's alpha grid
+    (plan_sweep, n = 40 alphas over the same range: one interior elimination
+    and one factorization per alpha group); and the reference's sweep
+    composition (oracle/_ref: cache once, then assemble / Schur /
+    Thomas per angle) on a bounded sample of the angles, all host threads."""
+    from paper_1410_5003_b200 import configs
+    from paper_1410_5003_b200.qpscat import Solver
+    st, num, om, th, K, meta = configs.config(5)
+    thetas = configs.sweep_angles(200)
+    g = Solver(device=device)
+    g.build_geometry(st, num)
+    g.make_problem(om, th, K)
+    g.sweep(thetas[:2], K, mode=0)  # warm-up: allocations
+    out = {"workload": f"cfg5: {meta['I']} interfaces, N={meta['N']}, P={num.P}, K={K}, 200 angles in [-pi+0.1,-0.1]",
+           "angles": len(thetas)}
+    g.build_geometry(st, num)  # drop the cache: the timed sweep fills it
+    g.make_problem(om, th, K)
+    t0 = time.perf_counter()
+    r = g.sweep(thetas, K, mode=0)
+    out["accelerated_s"] = time.perf_counter() - t0
+    out["accelerated_ms_per_angle"] = 1e3 * out["accelerated_s"] / len(thetas)
+    out["converged"] = int((r["status"] == 0).sum())
+    out["mean_abs_flux_error"] = float(statistics.fmean(abs(x) for x in r["flux_error"]))
+    t0 = time.perf_counter()
+    g.sweep(thetas, K, mode=1)
+    out["independent_s"] = time.perf_counter() - t0
+    out["speedup_vs_independent"] = out["independent_s"] / out["accelerated_s"]
+    ta, grp = g.plan_sweep(40, -math.pi + 0.1, -0.1)
+    t0 = time.perf_counter()
+    ra = g.sweep(list(ta), K, mode=0)
+    out["alpha_grid"] = {"angles": len(ta), "alpha_groups": 40, "s": time.perf_counter() - t0}
+    info = g.sweep_info(len(ta))
+    out["alpha_grid"].update({"n_groups": info["n_groups"], "n_factorizations": info["n_factorizations"],
+                              "n_interior": info["n_interior"], "converged": int((ra["status"] == 0).sum())})
+    t0 = time.perf_counter()
+    g.sweep(list(ta), K, mode=1)
+    out["alpha_grid"]["independent_s"] = time.perf_counter() - t0
+    out["alpha_grid"]["speedup_vs_independent"] = out["alpha_grid"]["independent_s"] / out["alpha_grid"]["s"]
+    g.close()
+    if ref_angles > 0 and os.path.exists(ORACLE):
+        o = Solver(lib=ORACLE)
+        o.set_num_threads(os.cpu_count() or 1)
+        o.build_geometry(st, num)
+        o.make_problem(om, th, K)
+        sample = thetas[::len(thetas) // ref_angles][:ref_angles]
+        t0 = time.perf_counter()
+        o.sweep(sample, K, mode=0)
+        dt = time.perf_counter() - t0
+        fill_s = o.phase_times()["fill_ms"] * 1e-3  # the oracle reports the whole sweep here
+        o.build_geometry(st, num)
+        o.make_problem(om, th, K)
+        t1 = time.perf_counter()
+        o.sweep(sample[:1], K, mode=0)
+        one = time.perf_counter() - t1  # cache fill + one angle
+        per_angle = (dt - one) / max(1, len(sample) - 1)
+        cache = one - per_angle
+        out["cpu_reference"] = {"kind": "reference", "cores": os.cpu_count() or 1,
+                                "sample": f"{len(sample)} of the 200 angles (cache fill once + per angle assemble/"
+                                          f"Schur/Thomas), extrapolated to 200 angles as cache + 200 x per-angle",
+                                "sample_s": dt, "cache_fill_s": cache, "per_angle_s": per_angle,
+                                "sweep_200_s_extrapolated": cache + 200 * per_angle, "sweep_reported_s": fill_s}
+        out["speedup_vs_cpu_reference"] = out["cpu_reference"]["sweep_200_s_extrapolated"] / out["accelerated_s"]
+        o.close()
+    return out
+
+
 def run_reference(args, world, rank):
     """The reference's own CPU implementation (oracle/_ref: the qpscat headers
     compiled unmodified) on all host threads.  A full config-4 solve takes
@@ -225,6 +296,8 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="override I (default: the config's 1000)")
     ap.add_argument("--ref-layers", type=int, default=8, help="I of the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 sweep measurement")
+    ap.add_argument("--sweep-ref-angles", type=int, default=4, help="angles of the CPU reference sweep sample")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
     if args.impl == "reference":
@@ -307,6 +380,10 @@ def main():
     if rank == 0 and not args.no_cpu_baseline and os.path.exists(ORACLE):
         cb = cpu_baseline(args.ref_layers, os.cpu_count() or 1)
         cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    sweep = None
+    if rank == 0 and not args.no_sweep:
+        s.close()  # free the config-4 buffers: the sweep sizes its angle batches from free HBM
+        sweep = sweep_measure(local, 0 if args.no_cpu_baseline else args.sweep_ref_angles)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "layers/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -332,6 +409,7 @@ def main():
                 "gemm_tflops_issued": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "gemm_tflops_complex_equiv": gemm_fl * 8.0 / 6.0 / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
                 "fp64_peaks_tflops": peaks, "flux_error": rt["flux_error"], "R": rt["R"], "T": rt["T"],
+                "sweep": sweep,
                 "families_ms": {k: round(v["ms"] / args.steps, 3) for k, v in sorted(fams.items(),
                                                                                      key=lambda kv: -kv[1]["ms"])}}
         print(json.dumps(line), flush=True)

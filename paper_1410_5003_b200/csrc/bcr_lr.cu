@@ -42,9 +42,9 @@ namespace {
 constexpr int kLrSample = 64;    // columns of the random sample the basis is built from
 // a-posteriori test of every compressed coupling on an independent probe: 16
 // seeded random columns J of C (a coordinate-vector sample; kernel matrices
-// spread their residual over all columns), ||C[:,J] - P (P^* C)[:,J]||_F <=
+// spread their residual over all columns), ||C[:,J] - P (P^* C[:,J])||_F <=
 // tol ||C[:,J]||_F; a failure takes the dense reduction.  Gathering columns
-// costs no GEMM over C (R = P^* C already exists).
+// costs no GEMM over C.
 constexpr int kLrProbe = 16;
 constexpr int kLrCols = kLrSample;  // columns of Omega and of the sample Y
 // rcond screen of the Woodbury level-0 factors (tridiag.hpp:36-40): kRcProbe
@@ -911,6 +911,76 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         }
     }
     tmark("P^*");
+    // a-posteriori test on the probe columns J (per coupling): Y2 = C[:, J]
+    // (= A[:, J] - Bc X[:, J] when the coupling update is deferred),
+    // ||Y2 - P R[:, J]||_F against ||Y2||_F, read back with the ranks
+    static const bool no_probe = [] {  // QPS_LR_PROBE=0: skip the test (A/B timing only)
+        const char* e = getenv("QPS_LR_PROBE");
+        return e && !strcmp(e, "0");
+    }();
+    if (no_probe) {
+        c.lr_pn_h.ensure(size_t(nc) * 2);
+        for (int q = 0; q < 2 * nc; ++q) c.lr_pn_h[q] = 0.0;
+    }
+    if (!no_probe) {
+        if (c.lr_probe_n != nc * 65536 + nb) {
+            std::vector<int> cols(size_t(nc) * kLrProbe);
+            uint64_t x = 0xd1b54a32d192ed03ull;
+            for (auto& v : cols) {
+                x ^= x >> 12;
+                x ^= x << 25;
+                x ^= x >> 27;
+                v = int(((x * 0x2545f4914f6cdd1dull) >> 33) % uint64_t(nb));
+            }
+            c.lr_probe_cols.upload(cols, s);
+            c.lr_probe_n = nc * 65536 + nb;
+        }
+        std::vector<const cplx*> cp(nc), xp(nc);
+        std::vector<int> cld(nc, nb), xld(nc, P);
+        for (int q = 0; q < nc; ++q) {
+            cp[q] = coupling(q);
+            if (corr) {
+                xp[q] = corr_task(q).B[0];
+                xld[q] = corr_task(q).ldb[0];
+            }
+        }
+        c.lr_Y2.ensure(size_t(nc) * nb * kLrProbe);
+        c.lr_G2.ensure(size_t(nc) * (r + P) * kLrProbe);
+        cplx* Rg = c.lr_G2.p;                                   // r x 16 per coupling
+        cplx* Xg = c.lr_G2.p + size_t(nc) * r * kLrProbe;      // P x 16 per coupling
+        gather_columns(cp, cld, nb, c.lr_probe_cols.p, kLrProbe, c.lr_Y2.p, nb, size_t(nb) * kLrProbe, c.lr_gptr,
+                       c.lr_gld, s);
+        if (corr) {
+            gather_columns(xp, xld, P, c.lr_probe_cols.p, kLrProbe, Xg, P, size_t(P) * kLrProbe, c.lr_gptr, c.lr_gld,
+                           s);
+            std::vector<GemmTask> t(nc);
+            for (int q = 0; q < nc; ++q)
+                t[q] = gemm1(corr_task(q).A[0], corr_task(q).lda[0], Xg + size_t(q) * P * kLrProbe, P, P,
+                             c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
+            zgemm_batched(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        }
+        std::vector<GemmTask> gt(nc), e(nc);  // G = P^* Y2 (= R[:, J]), then ||Y2 - P G||
+        for (int q = 0; q < nc; ++q) {
+            gt[q] = gemm1(c.lr_PH.p + size_t(q) * r * nb, r, c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb, nb,
+                          Rg + size_t(q) * r * kLrProbe, r);
+            e[q] = gemm1(c.lr_P.p + size_t(q) * nb * r, nb, Rg + size_t(q) * r * kLrProbe, r, r,
+                         c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
+        }
+        zgemm_batched(r, kLrProbe, cplx{1, 0}, cplx{0, 0}, gt, s, c.ws.gemm_tasks, "lr_compress");
+        c.lr_pn.ensure(size_t(nc) * 2);
+        batched_fro(c.lr_Y2.p, nb, kLrProbe, nb, size_t(nb) * kLrProbe, nc, c.lr_pn.p + nc, s);
+        zgemm_residual_norms(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, e, s, c.ws.gemm_tasks, c.lr_parts, c.lr_pn.p);
+        c.lr_pn_h.ensure(size_t(nc) * 2);
+        QPS_D2H(c.lr_pn_h.p, c.lr_pn.p, sizeof(double) * 2 * nc, s);
+        // the host checks ranks and probes once this is reached, while the
+        // projection R = P^* C below (the largest GEMM here) still runs
+        QPS_CUDA(cudaEventRecord(c.ev_sample, s));
+        if (!rank_deferred) {
+            rank_deferred = true;
+            c.lr_rank_h.ensure(nc);
+            for (int q = 0; q < nc; ++q) c.lr_rank_h[q] = 0;  // ranks already checked above
+        }
+    }
     // R = P^* C  (= P^* A + (-P^* Bc) X when deferred)
     c.lr_R.ensure(size_t(nc) * r * nb);
     {
@@ -939,64 +1009,6 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         zgemm_batched(r, nb, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
     }
     tmark("R = P^* C");
-    // a-posteriori test on the probe columns J (per coupling): Y2 = C[:, J]
-    // (= A[:, J] - Bc X[:, J] when the coupling update is deferred),
-    // ||Y2 - P R[:, J]||_F against ||Y2||_F, read back with the ranks
-    {
-        if (c.lr_probe_n != nc * 65536 + nb) {
-            std::vector<int> cols(size_t(nc) * kLrProbe);
-            uint64_t x = 0xd1b54a32d192ed03ull;
-            for (auto& v : cols) {
-                x ^= x >> 12;
-                x ^= x << 25;
-                x ^= x >> 27;
-                v = int(((x * 0x2545f4914f6cdd1dull) >> 33) % uint64_t(nb));
-            }
-            c.lr_probe_cols.upload(cols, s);
-            c.lr_probe_n = nc * 65536 + nb;
-        }
-        std::vector<const cplx*> cp(nc), xp(nc), rp(nc);
-        std::vector<int> cld(nc, nb), xld(nc, P), rld(nc, r);
-        for (int q = 0; q < nc; ++q) {
-            cp[q] = coupling(q);
-            rp[q] = c.lr_R.p + size_t(q) * r * nb;
-            if (corr) {
-                xp[q] = corr_task(q).B[0];
-                xld[q] = corr_task(q).ldb[0];
-            }
-        }
-        c.lr_Y2.ensure(size_t(nc) * nb * kLrProbe);
-        c.lr_G2.ensure(size_t(nc) * (r + P) * kLrProbe);
-        cplx* Rg = c.lr_G2.p;                                   // r x 16 per coupling
-        cplx* Xg = c.lr_G2.p + size_t(nc) * r * kLrProbe;      // P x 16 per coupling
-        gather_columns(cp, cld, nb, c.lr_probe_cols.p, kLrProbe, c.lr_Y2.p, nb, size_t(nb) * kLrProbe, c.lr_gptr,
-                       c.lr_gld, s);
-        gather_columns(rp, rld, r, c.lr_probe_cols.p, kLrProbe, Rg, r, size_t(r) * kLrProbe, c.lr_gptr, c.lr_gld, s);
-        if (corr) {
-            gather_columns(xp, xld, P, c.lr_probe_cols.p, kLrProbe, Xg, P, size_t(P) * kLrProbe, c.lr_gptr, c.lr_gld,
-                           s);
-            std::vector<GemmTask> t(nc);
-            for (int q = 0; q < nc; ++q)
-                t[q] = gemm1(corr_task(q).A[0], corr_task(q).lda[0], Xg + size_t(q) * P * kLrProbe, P, P,
-                             c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
-            zgemm_batched(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
-        }
-        std::vector<GemmTask> e(nc);
-        for (int q = 0; q < nc; ++q)
-            e[q] = gemm1(c.lr_P.p + size_t(q) * nb * r, nb, Rg + size_t(q) * r * kLrProbe, r, r,
-                         c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
-        c.lr_pn.ensure(size_t(nc) * 2);
-        batched_fro(c.lr_Y2.p, nb, kLrProbe, nb, size_t(nb) * kLrProbe, nc, c.lr_pn.p + nc, s);
-        zgemm_residual_norms(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, e, s, c.ws.gemm_tasks, c.lr_parts, c.lr_pn.p);
-        c.lr_pn_h.ensure(size_t(nc) * 2);
-        QPS_D2H(c.lr_pn_h.p, c.lr_pn.p, sizeof(double) * 2 * nc, s);
-        QPS_CUDA(cudaEventRecord(c.ev_sample, s));  // the host checks ranks and probes once this is reached
-        if (!rank_deferred) {
-            rank_deferred = true;
-            c.lr_rank_h.ensure(nc);
-            for (int q = 0; q < nc; ++q) c.lr_rank_h[q] = 0;  // ranks already checked above
-        }
-    }
     if (trace) {
         QPS_CUDA(cudaEventDestroy(te0));
         QPS_CUDA(cudaEventDestroy(te1));
@@ -1314,8 +1326,16 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
 // ||D_j^0||_1 of every diagonal block for the level-0 rcond screen, on the side
 // stream while the couplings are compressed (Ad is final after the Schur step;
 // bcr_solve_wb joins before its factorization overwrites Ad)
+bool rcond_enabled() {
+    static const bool on = [] {  // QPS_RCOND=0: skip the level-0 rcond screen (A/B timing only)
+        const char* e = getenv("QPS_RCOND");
+        return !(e && !strcmp(e, "0"));
+    }();
+    return on;
+}
+
 void wb_anorm_async(Ctx& c, const cplx* Ad) {
-    if (!lr_eligible(c)) return;
+    if (!lr_eligible(c) || !rcond_enabled()) return;
     const int npos = c.dims.nsys * c.dims.I;
     c.rc_anorm.ensure(npos);
     QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
@@ -1432,7 +1452,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         if (c.anorm_pending) {  // ||D_j^0||_1 (side stream, before the factorization overwrites Ad)
             QPS_CUDA(cudaStreamWaitEvent(s, c.ev_anorm, 0));
             c.anorm_pending = false;
-        } else {
+        } else if (rcond_enabled()) {
             c.rc_anorm.ensure(npos);
             batched_norm1(Ad, nb, nb, nb2, npos, c.rc_anorm.p, s);
         }
@@ -1493,7 +1513,9 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         c.rc_sus.ensure(npos);
         c.rc_estlo.ensure(npos);
         QPS_CUDA(cudaMemsetAsync(c.rc_flag.p, 0, sizeof(int) * npos, s));
-        rcond_screen(c.lr_W0.p, size_t(nb) * wc, nb, r2 + m, kRcProbe, c.rc_anorm.p, double(nb), npos, kRcondMin,
+        QPS_CUDA(cudaMemsetAsync(c.rc_sus.p, 0, sizeof(int) * npos, s));
+        if (rcond_enabled())
+            rcond_screen(c.lr_W0.p, size_t(nb) * wc, nb, r2 + m, kRcProbe, c.rc_anorm.p, double(nb), npos, kRcondMin,
                      kRcSuspect, c.rc_flag.p, c.rc_sus.p, c.rc_estlo.p, s);
         c.rc_flag_h.ensure(2 * size_t(npos));
         QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, s);
