@@ -182,6 +182,21 @@ int qps_get_solution(const qps_ctx* ctx, qps_cplx* eta, qps_cplx* c, qps_cplx* a
 int qps_reflection_transmission(const qps_ctx* ctx, double* R, double* T, double* flux_error, double* kappa,
                                 qps_cplx* kU, qps_cplx* kD, int* prop_up, int* prop_down);
 
+/* Replace the current Solution (tridiag.hpp:11-17) by caller data -- the
+ * reference's post-processing takes a Solution argument (evaluate_field,
+ * residual_suite): eta[sum 2N_j], c[(I+1)*P], aU[2K+1], aD[2K+1].  Needs a
+ * problem (make_problem) on this context. */
+int qps_set_solution(qps_ctx* ctx, const qps_cplx* eta, const qps_cplx* c, const qps_cplx* aU, const qps_cplx* aD);
+
+/* ---------------------------------------------------------- residual suite */
+/* residual_suite(sol, p, num, interfaces), postprocess.hpp:369-399, of the
+ * current solution: ResidualReport{wall_qp, radiation, interface}
+ * (postprocess.hpp:186-190).  The product sums every potential on the device. */
+int qps_residual_suite(qps_ctx* ctx, int n_interfaces, const int* interfaces, double* wall_qp, double* radiation,
+                       double* interface_res);
+/* interface_matching_residual(sol, p, num, j, n_probe), postprocess.hpp:263-365 */
+int qps_interface_matching_residual(qps_ctx* ctx, int j, int n_probe, double* out);
+
 /* ------------------------------------------------------ field evaluation */
 /* evaluate_field(sol, p, points), postprocess.hpp:78-123, for the last solve:
  * xy[2n] interleaved points (any cell: x is mapped into the central cell and

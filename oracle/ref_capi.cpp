@@ -335,6 +335,58 @@ int qps_get_solution(const qps_ctx* c, qps_cplx* eta, qps_cplx* cc, qps_cplx* aU
     });
 }
 
+int qps_set_solution(qps_ctx* c, const qps_cplx* eta, const qps_cplx* cc, const qps_cplx* aU, const qps_cplx* aD) {
+    return guarded(c, [&] {
+        need(c->have_prob, "make_problem first");
+        const int I = c->prob.n_interfaces(), P = c->num.P, nrb = 2 * c->prob.K + 1;
+        Solution s;
+        size_t o = 0;
+        for (int j = 0; j < I; ++j) {
+            const int n = 2 * c->geom.interfaces[j].quad.total();
+            Vec e(n);
+            for (int i = 0; i < n; ++i) e(i) = cd(eta[o + i].re, eta[o + i].im);
+            s.eta.push_back(e);
+            o += n;
+        }
+        for (int l = 0; l <= I; ++l) {
+            Vec v(P);
+            for (int i = 0; i < P; ++i) v(i) = cd(cc[size_t(l) * P + i].re, cc[size_t(l) * P + i].im);
+            s.c.push_back(v);
+        }
+        s.aU = Vec(nrb);
+        s.aD = Vec(nrb);
+        for (int i = 0; i < nrb; ++i) {
+            s.aU(i) = cd(aU[i].re, aU[i].im);
+            s.aD(i) = cd(aD[i].re, aD[i].im);
+        }
+        s.flux_error = flux_error(s, c->prob);
+        c->sol = s;
+    });
+}
+
+// residual_suite / interface_matching_residual (postprocess.hpp:263-399)
+int qps_residual_suite(qps_ctx* c, int n_interfaces, const int* interfaces, double* wall_qp, double* radiation,
+                       double* interface_res) {
+    return guarded(c, [&] {
+        need(c->sol.has_value(), "no solution");
+        const ResidualReport r = residual_suite(*c->sol, c->prob, c->num,
+                                                std::vector<int>(interfaces, interfaces + n_interfaces));
+        if (wall_qp) *wall_qp = r.wall_qp;
+        if (radiation) *radiation = r.radiation;
+        if (interface_res) *interface_res = r.interface;
+    });
+}
+
+int qps_interface_matching_residual(qps_ctx* c, int j, int n_probe, double* out) {
+    return guarded(c, [&] {
+        need(c->sol.has_value(), "no solution");
+        need(j >= 0 && j < c->prob.n_interfaces(), "interface_matching_residual: interface index out of range");
+        need(n_probe >= 1, "interface_matching_residual: n_probe >= 1");
+        const double r = interface_matching_residual(*c->sol, c->prob, c->num, j, n_probe);
+        if (out) *out = r;
+    });
+}
+
 int qps_reflection_transmission(const qps_ctx* c, double* R, double* T, double* fe, double* kappa, qps_cplx* kU,
                                 qps_cplx* kD, int* pu, int* pd) {
     return guarded(const_cast<qps_ctx*>(c), [&] {

@@ -424,6 +424,58 @@ int qps_get_solution(const qps_ctx* h, qps_cplx* eta, qps_cplx* cc, qps_cplx* aU
     });
 }
 
+int qps_set_solution(qps_ctx* h, const qps_cplx* eta, const qps_cplx* cc, const qps_cplx* aU, const qps_cplx* aD) {
+    return guarded(h, [&](Ctx& c) {
+        need_device(c);
+        need(c.have_prob, "make_problem first");
+        need(eta && cc && aU && aD, "set_solution: null array");
+        if (c.dims.nb == 0 || c.dims.I != c.geo.I || c.dims.K != c.prob.K) setup_dims(c, false);
+        c.dims.nsys = 1;
+        const Dims& D = c.dims;
+        const int I = D.I, nrb = 2 * c.prob.K + 1;
+        size_t neta = 0;
+        for (int j = 0; j < I; ++j) neta += 2 * size_t(D.N[j]);
+        c.h_eta.ensure(neta);
+        c.h_eta_n = neta;
+        std::memcpy(c.h_eta.p, eta, sizeof(cplx) * neta);
+        c.F.ensure(size_t(I) * D.nb);
+        c.F.zero(c.stream);
+        size_t o = 0;
+        for (int j = 0; j < I; ++j) {
+            QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(j) * D.nb, eta + o, sizeof(cplx) * 2 * D.N[j],
+                                     cudaMemcpyHostToDevice, c.stream));
+            o += 2 * size_t(D.N[j]);
+        }
+        QPS_CUDA(cudaStreamSynchronize(c.stream));
+        c.h_c.assign(reinterpret_cast<const cplx*>(cc), reinterpret_cast<const cplx*>(cc) + size_t(I + 1) * D.P);
+        c.h_aU.assign(reinterpret_cast<const cplx*>(aU), reinterpret_cast<const cplx*>(aU) + nrb);
+        c.h_aD.assign(reinterpret_cast<const cplx*>(aD), reinterpret_cast<const cplx*>(aD) + nrb);
+        c.lsq.assign(I + 1, 0.0);
+        c.max_lsq = 0.0;
+        c.have_sol = true;
+        c.eta_valid = true;
+    });
+}
+
+int qps_residual_suite(qps_ctx* h, int n_interfaces, const int* interfaces, double* wall_qp, double* radiation,
+                       double* interface_res) {
+    return guarded(h, [&](Ctx& c) {
+        need_device(c);
+        need(c.have_sol, "no solution");
+        need(n_interfaces >= 0 && (n_interfaces == 0 || interfaces), "residual_suite: bad interface list");
+        residual_suite(c, std::vector<int>(interfaces, interfaces + n_interfaces), wall_qp, radiation, interface_res);
+    });
+}
+
+int qps_interface_matching_residual(qps_ctx* h, int j, int n_probe, double* out) {
+    return guarded(h, [&](Ctx& c) {
+        need_device(c);
+        need(c.have_sol, "no solution");
+        const double r = interface_matching_residual(c, j, n_probe);
+        if (out) *out = r;
+    });
+}
+
 int qps_reflection_transmission(const qps_ctx* h, double* R, double* T, double* fe, double* kappa, qps_cplx* kU,
                                 qps_cplx* kD, int* pu, int* pd) {
     return guarded(const_cast<qps_ctx*>(h), [&](Ctx& c) {

@@ -96,6 +96,7 @@ struct BandTask {
 };
 
 // evaluate_field: one layer's sources and its range of the sorted point list
+constexpr int kFieldTile = 32;  // points per CTA of the field kernel
 struct FieldTask {
     double k;
     int nsrc;               // interfaces bounding the layer (0..2)
@@ -199,6 +200,9 @@ struct Ctx {
     CodSet cod_ag;
     std::vector<int> sweep_group;      // last sweep: alpha group of every angle (-1: not solved)
     int sweep_ngroups = 0;
+    // residual suite: private source pool and refined densities
+    DBuf<double> res_px, res_py, res_pnx, res_pny, res_pw;
+    DBuf<cplx> res_eta;
     uint64_t sweep_interior = 0, sweep_factorizations = 0;  // interior eliminations / block factorizations
     uint64_t n_factorizations = 0;     // block-solve factorizations performed (the sweep's per-group counter)
     DBuf<cplx> bcr_copy, bcr_cdinv;    // dense reduction: factored copies of the even blocks (rcond test)
@@ -289,6 +293,15 @@ void assemble_from_cache(Ctx& c, const std::vector<Problem>& probs);
 // evaluate_field (postprocess.hpp:78-123) for the last solution; region 0 above
 // y_U, 1 inside a layer, 2 below y_D
 void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, int* region, int* layer);
+// device sums of layer representations for explicit tasks (field.cu): points
+// qx/qy grouped per task, tiles (task, first point) of kFieldTile points,
+// sources and proxies at offsets of `pool`
+void field_sums(Ctx& c, const std::vector<FieldTask>& tasks, const std::vector<int2>& tiles,
+                const std::vector<double>& qx, const std::vector<double>& qy, const DevPool& pool,
+                std::vector<cplx>& out);
+// residual_suite / interface_matching_residual (postprocess.hpp:263-399) of the last solution
+double interface_matching_residual(Ctx& c, int j, int n_probe);
+void residual_suite(Ctx& c, const std::vector<int>& ifaces, double* wall_qp, double* radiation, double* iface);
 // multi-angle sweep; mode 0 accelerated (cache once, angles batched), 1 independent
 void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe, cplx* aU,
                cplx* aD, int* status);

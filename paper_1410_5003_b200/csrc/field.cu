@@ -22,7 +22,7 @@ namespace {
 
 using cd = std::complex<double>;
 
-constexpr int kFieldPts = 32, kFieldWarps = 4;
+constexpr int kFieldPts = kFieldTile, kFieldWarps = 4;
 
 __global__ void __launch_bounds__(32 * kFieldWarps) field_kernel(const FieldTask* __restrict__ tasks,
                                                                  const int2* __restrict__ tiles,
@@ -122,13 +122,11 @@ __global__ void __launch_bounds__(32 * kFieldWarps) field_kernel(const FieldTask
 
 }  // namespace
 
-void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, int* region, int* layer_out) {
-    const HostGeometry& g = c.geo;
+void field_sums(Ctx& c, const std::vector<FieldTask>& tasks, const std::vector<int2>& tiles,
+                const std::vector<double>& qx, const std::vector<double>& qy, const DevPool& pool,
+                std::vector<cplx>& out) {
     const Problem& pb = c.prob;
-    const Dims& D = c.dims;
-    const double d = g.d;
-    const int I = g.I;
-    const cd alpha(pb.ar, pb.ai);
+    const std::complex<double> alpha(pb.ar, pb.ai), ainv = 1.0 / alpha;
     cudaStream_t s = c.stream;
     {  // this translation unit's copy of the far-field Hankel table (hankel.cuh)
         static bool uploaded = false;
@@ -137,6 +135,43 @@ void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, 
             uploaded = true;
         }
     }
+    const int n = int(qx.size());
+    out.assign(n, cplx{0, 0});
+    if (n == 0 || tiles.empty()) return;
+    c.field_qx.upload(qx, s);
+    c.field_qy.upload(qy, s);
+    c.field_tasks.upload(tasks, s);
+    c.field_tiles.upload(tiles, s);
+    c.field_out.ensure(n);
+    QPS_CUDA(cudaMemsetAsync(c.d_err.p, 0, sizeof(int), s));
+    double evals = 0;
+    for (const auto& t : tasks) {
+        double per = t.P;
+        for (int q = 0; q < t.nsrc; ++q) per += 3.0 * t.ns[q];
+        evals += per * t.npt;
+    }
+    {
+        ProfScope ps("field", s, 0.0, 0.0, evals);
+        { QPS_NOTE_LAUNCH(); field_kernel<<<unsigned(tiles.size()), 32 * kFieldWarps, 0, s>>>(
+            c.field_tasks.p, c.field_tiles.p, c.field_qx.p, c.field_qy.p, pool, device_near_table(),
+            cplx{alpha.real(), alpha.imag()}, cplx{ainv.real(), ainv.imag()}, c.geo.d, c.field_out.p, c.d_err.p); }
+        QPS_CUDA(cudaGetLastError());
+    }
+    int herr = 0;
+    QPS_D2H(out.data(), c.field_out.p, sizeof(cplx) * n, s);
+    QPS_D2H(&herr, c.d_err.p, sizeof(int), s);
+    QPS_CUDA(cudaStreamSynchronize(s));
+    if (herr) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
+}
+
+void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, int* region, int* layer_out) {
+    const HostGeometry& g = c.geo;
+    const Problem& pb = c.prob;
+    const Dims& D = c.dims;
+    const double d = g.d;
+    const int I = g.I;
+    const cd alpha(pb.ar, pb.ai);
+    cudaStream_t s = c.stream;
     // classification in the central cell (postprocess.hpp:85-95)
     std::vector<int> cell(n), reg(n), lay(n);
     for (int i = 0; i < n; ++i) {
@@ -192,32 +227,8 @@ void evaluate_field(Ctx& c, int n, const double* xy, cplx* u_scat, cplx* u_tot, 
             tasks.push_back(t);
             for (int p0 = 0; p0 < cnt; p0 += kFieldPts) tiles.push_back(make_int2(ti, p0));
         }
-        c.field_qx.upload(qx, s);
-        c.field_qy.upload(qy, s);
-        c.field_tasks.upload(tasks, s);
-        c.field_tiles.upload(tiles, s);
-        c.field_out.ensure(nl);
-        QPS_CUDA(cudaMemsetAsync(c.d_err.p, 0, sizeof(int), s));
         const DevPool pool{c.px.p, c.py.p, c.pnx.p, c.pny.p, c.pw.p};
-        const cd ainv = 1.0 / alpha;
-        double evals = 0;
-        for (const auto& t : tasks) {
-            double per = t.P;
-            for (int q = 0; q < t.nsrc; ++q) per += 3.0 * t.ns[q];
-            evals += per * t.npt;
-        }
-        {
-            ProfScope ps("field", s, 0.0, 0.0, evals);
-            { QPS_NOTE_LAUNCH(); field_kernel<<<unsigned(tiles.size()), 32 * kFieldWarps, 0, s>>>(
-                c.field_tasks.p, c.field_tiles.p, c.field_qx.p, c.field_qy.p, pool, device_near_table(),
-                cplx{alpha.real(), alpha.imag()}, cplx{ainv.real(), ainv.imag()}, d, c.field_out.p, c.d_err.p); }
-            QPS_CUDA(cudaGetLastError());
-        }
-        int herr = 0;
-        QPS_D2H(u_layer.data(), c.field_out.p, sizeof(cplx) * nl, s);
-        QPS_D2H(&herr, c.d_err.p, sizeof(int), s);
-        QPS_CUDA(cudaStreamSynchronize(s));
-        if (herr) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
+        field_sums(c, tasks, tiles, qx, qy, pool, u_layer);
     }
     std::vector<cd> us(n, cd(0.0, 0.0));
     for (int t = 0; t < nl; ++t) {

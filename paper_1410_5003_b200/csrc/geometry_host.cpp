@@ -241,6 +241,11 @@ HostInterface build_interface(const qps_interface_spec& sp, double d, std::vecto
 
 }  // namespace
 
+HostInterface build_interface_geometry(const qps_interface_spec& sp, double d) {
+    std::vector<double> pool;  // Fourier coefficients stay on the host here
+    return build_interface(sp, d, pool);
+}
+
 HostGeometry build_geometry(const StackDesc& st, const Numerics& num) {
     const int I = int(st.ifaces.size());
     if (int(st.eps.size()) != I + 1) fail(QPS_ERR_CONFIG, "stack needs exactly one more layer than interfaces");

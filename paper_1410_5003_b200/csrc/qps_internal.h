@@ -176,6 +176,8 @@ struct Numerics {
 };
 
 HostGeometry build_geometry(const StackDesc& st, const Numerics& num);
+// build_interface_geometry (geometry.hpp:423-447): one interface's quadrature
+HostInterface build_interface_geometry(const qps_interface_spec& sp, double d);
 
 struct Problem {
     double omega = 0, theta = 0;

@@ -195,6 +195,9 @@ def _bind(lib):
         "qps_evaluate_field": (C.c_int, [vp, C.c_int, P(C.c_double), vp, vp, P(C.c_int), P(C.c_int)]),
         "qps_sweep": (C.c_int, [vp, C.c_int, P(C.c_double), C.c_int, C.c_int, P(C.c_double), P(C.c_double),
                                 P(C.c_double), vp, vp, P(C.c_int)]),
+        "qps_set_solution": (C.c_int, [vp, vp, vp, vp, vp]),
+        "qps_residual_suite": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_double), P(C.c_double), P(C.c_double)]),
+        "qps_interface_matching_residual": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_double)]),
         "qps_plan_sweep": (C.c_int, [vp, C.c_int, C.c_double, C.c_double, C.c_int, P(C.c_double), P(C.c_int),
                                      P(C.c_int)]),
         "qps_sweep_info": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_int), P(C.c_uint64), P(C.c_uint64)]),
@@ -438,6 +441,26 @@ class Solver:
         self._check(self.lib.qps_sweep(self.h, n, _dptr(th), K, mode, _dptr(R), _dptr(T), _dptr(fe),
                                        aU.ctypes.data, aD.ctypes.data, st.ctypes.data_as(C.POINTER(C.c_int))))
         return {"R": R, "T": T, "flux_error": fe, "aU": aU, "aD": aD, "status": st}
+
+    def set_solution(self, eta, c, aU, aD):
+        """Load a Solution (tridiag.hpp:11-17) for post-processing: eta flat
+        [tau_0; sigma_0; tau_1; ...], c (I+1, P), aU, aD (2K+1)."""
+        arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.complex128).ravel()) for a in (eta, c, aU, aD)]
+        self._check(self.lib.qps_set_solution(self.h, *[a.ctypes.data for a in arrs]))
+
+    def residual_suite(self, interfaces):
+        """ResidualReport of the current solution (residual_suite,
+        postprocess.hpp:369-399): dict(wall_qp, radiation, interface)."""
+        ifs = np.ascontiguousarray(interfaces, dtype=np.int32)
+        w, r, i = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.lib.qps_residual_suite(self.h, len(ifs), ifs.ctypes.data_as(C.POINTER(C.c_int)),
+                                                C.byref(w), C.byref(r), C.byref(i)))
+        return {"wall_qp": w.value, "radiation": r.value, "interface": i.value}
+
+    def interface_matching_residual(self, j: int, n_probe: int = 4):
+        out = C.c_double()
+        self._check(self.lib.qps_interface_matching_residual(self.h, j, n_probe, C.byref(out)))
+        return out.value
 
     def plan_sweep(self, n_alpha: int, theta_lo: float, theta_hi: float):
         """plan_sweep(omega, n, theta_range): angles on the grid
