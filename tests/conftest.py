@@ -82,5 +82,5 @@ def pytest_terminal_summary(terminalreporter):
         return
     terminalreporter.section("parity vs oracle (measured error, oracle 1-ulp floor)")
     for name, items in _PARITY:
-        parts = [f"{k} {v[0]:.3g} (floor {v[1]:.3g})" for k, v in items.items()]
+        parts = [f"{k} {v[0]:.3g} ({v[2] if len(v) > 2 else 'floor'} {v[1]:.3g})" for k, v in items.items()]
         terminalreporter.write_line(f"{name}: " + ", ".join(parts))
