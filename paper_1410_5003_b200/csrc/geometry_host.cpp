@@ -149,6 +149,13 @@ void push_node(HostInterface& q, V2 z, V2 t_for_speed, V2 t_for_normal, double h
 
 HostInterface build_interface(const qps_interface_spec& sp, double d, std::vector<double>& pool) {
     HostInterface g;
+    {  // one allocation per array (the interfaces are built on concurrent host threads)
+        size_t n = 0;
+        for (int i = 0; i < sp.n_nodes; ++i) n += size_t(std::max(0, sp.nodes[i]));
+        if (sp.shape != QPS_SHAPE_POLYLINE) n = sp.n_nodes > 0 ? size_t(std::max(0, sp.nodes[0])) : 70;
+        if (sp.shape == QPS_SHAPE_POLYLINE && sp.n_nodes == 1) n *= size_t(std::max(1, sp.n_vertices - 1));
+        for (auto* v : {&g.x, &g.y, &g.nx, &g.ny, &g.w, &g.speed}) v->reserve(n);
+    }
     if (sp.shape == QPS_SHAPE_POLYLINE) {
         // make_interface_segments (:335-357) + build_corner_quadrature (:149-200)
         const int nv = sp.n_vertices;
