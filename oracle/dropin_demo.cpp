@@ -48,10 +48,10 @@ int main() {
     dev.precompute_shift_blocks();
     dev.assemble_system();
     dev.schur_complement();
+    const Mat a00 = dev.block(QPS_BLK_AP_DIAG, 0);  // A' is factored in place by the block solve
     const std::vector<Vec> eta = dev.block_lu_solve();
     Solution step;
     dev.recover_aux(step);
-    const Mat a00 = dev.block(QPS_BLK_AP_DIAG, 0);
     const double dstep = std::abs(step.aU(prob.K) - ref.aU(prob.K));
     std::printf("step-wise     : |aU0 diff| = %.2e, eta blocks %zu, A'_00 %ldx%ld\n", dstep, eta.size(),
                 long(a00.rows()), long(a00.cols()));
