@@ -138,6 +138,8 @@ struct Ctx {
     DBuf<SegDesc> segs;
     std::vector<int> seg_first;
     DBuf<double> fourier;
+    DBuf<double> aux_pool;         // host-computed Alpert auxiliary nodes of the open-arc interfaces
+    std::vector<long long> aux_off;  // per interface offset into aux_pool (-1: smooth, evaluated on the device)
     DBuf<int> d_err;
 
     // ---- alpha-free shift-block cache (precompute_shift_blocks) ----

@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
                                                      int total_rows, DevPool pool,
                                                      const SegDesc* __restrict__ segs,
                                                      const double* __restrict__ fourier,
+                                                     const double* __restrict__ aux,
                                                      const double* __restrict__ g_near, int* err) {
     __shared__ double s_near[kNear];
     __shared__ cplx s_val[4][2 * QPS_ALPERT_NAUX][4];    // per warp, aux, kind
@@ -498,14 +499,25 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
         const int side = lane < QPS_ALPERT_NAUX ? -1 : 1;
         const int kk = lane % QPS_ALPERT_NAUX;
         const double xi = side * c_alpert_nodes[kk];
-        const double s_aux = (mloc + 0.5 + xi) * h;
-        double zx, zy, tzx, tzy;
-        seg_eval(sd, fourier, s_aux, zx, zy, tzx, tzy);
-        const double speed = sqrt(tzx * tzx + tzy * tzy);
-        const double nzx = tzy / speed, nzy = -tzx / speed;
-        const double qw = h * c_alpert_weights[kk] * speed;
+        double zx, zy, nzx, nzy, qw;
+        if (T.aux_off >= 0) {  // open arc: the host's nodes (bit-identical to the reference)
+            const double* e = aux + T.aux_off + (size_t(m) * 2 * QPS_ALPERT_NAUX + lane) * 5;
+            zx = e[0];
+            zy = e[1];
+            nzx = e[2];
+            nzy = e[3];
+            qw = e[4];
+        } else {
+            const double s_aux = (mloc + 0.5 + xi) * h;
+            double tzx, tzy;
+            seg_eval(sd, fourier, s_aux, zx, zy, tzx, tzy);
+            const double speed = sqrt(tzx * tzx + tzy * tzy);
+            nzx = tzy / speed;
+            nzy = -tzx / speed;
+            qw = h * c_alpert_weights[kk] * speed;
+        }
         const double rvx = xmx - zx, rvy = xmy - zy;
-        const double r = sqrt(rvx * rvx + rvy * rvy);
+        const double r = hypot(rvx, rvy);  // Vec2::norm, types.hpp:24
         cplx vD{0, 0}, vS{0, 0}, vT{0, 0}, vDs{0, 0};
         if (r < 1e-13 * (1.0 + sqrt(xmx * xmx + xmy * xmy))) {
             atomicOr(err, 1);
@@ -731,7 +743,7 @@ void launch_proxy_fill(const std::vector<ProxyTask>& tasks, const DevPool& pool,
 }
 
 void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const DevPool& pool,
-                   const SegDesc* d_segs, const double* d_fourier, int* d_err, cudaStream_t s,
+                   const SegDesc* d_segs, const double* d_fourier, const double* d_aux, int* d_err, cudaStream_t s,
                    DBuf<AlpertTask>& d_tasks) {
     if (tasks.empty() || total_rows == 0) return;
     d_tasks.upload(tasks, s);
@@ -739,7 +751,7 @@ void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const D
     const double ev = 2.0 * 30.0 * total_rows;
     ProfScope ps("fill_alpert", s, 200.0 * ev, 0.0, ev);
     { QPS_NOTE_LAUNCH(); alpert_kernel<<<blocks, 128, 0, s>>>(d_tasks.p, int(tasks.size()), total_rows, pool, d_segs, d_fourier,
-                                         g_near_table, d_err); }
+                                         d_aux, g_near_table, d_err); }
     QPS_CUDA(cudaGetLastError());
 }
 

@@ -72,6 +72,7 @@ struct AlpertTask {
     double k[2], ksign[2];
     cplx alpha, alpha_inv;
     int mode;  // 0: fused into a [D S;T D*] block; 1: cache (central planes + wrap band)
+    long long aux_off;  // open arcs: offset of the host-computed auxiliary-node table (-1: evaluate on the device)
     cplx *oD, *oS, *oT, *oDs;  // block (mode 0) or central planes (mode 1)
     int ld;
     cplx* wrap;  // mode 1: N x 33 x 4 kinds band of out-of-period entries (incl. wrap removal)
@@ -89,7 +90,7 @@ void launch_pair_fill(const std::vector<PairTask>& tasks, const DevPool& pool, i
 void launch_proxy_fill(const std::vector<ProxyTask>& tasks, const DevPool& pool, int* d_err, cudaStream_t s,
                        DBuf<ProxyTask>& d_tasks, DBuf<int4>& d_tiles);
 void launch_alpert(const std::vector<AlpertTask>& tasks, int total_rows, const DevPool& pool,
-                   const SegDesc* d_segs, const double* d_fourier, int* d_err, cudaStream_t s,
+                   const SegDesc* d_segs, const double* d_fourier, const double* d_aux, int* d_err, cudaStream_t s,
                    DBuf<AlpertTask>& d_tasks);
 void launch_hankel_batch(int n, const double* d_x, cplx* d_h0, cplx* d_h1, cudaStream_t s);
 

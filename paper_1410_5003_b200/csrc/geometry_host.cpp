@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "alpert_table.h"
 #include "qps_internal.h"
 
 namespace qpsb {
@@ -187,6 +188,31 @@ HostInterface build_interface(const qps_interface_spec& sp, double d, std::vecto
                 const double wp = kress_wp(s, gq);
                 const V2 t{rawp.x * wp, rawp.y * wp};
                 push_node(g, z, t, rawp, h);
+            }
+            // auxiliary Alpert nodes of this segment's rows (kernels.hpp:243-253 with
+            // the QuadSegment maps of geometry.hpp:171-177 and the line segment
+            // of geometry.hpp:345-353); rows the reference fills with the plain
+            // rule (within a of a segment end, kernels.hpp:224) stay zero
+            for (int j = 0; j < n; ++j) {
+                for (int side = -1; side <= 1; side += 2)
+                    for (int kk = 0; kk < QPS_ALPERT_NAUX; ++kk) {
+                        double e[5] = {0, 0, 0, 0, 0};
+                        if (std::min(j, n - 1 - j) >= QPS_ALPERT_A) {
+                            const double xi = side * qps_alpert_nodes[kk];
+                            const double s_aux = (j + 0.5 + xi) * h;
+                            const double f = kress_w(s_aux, gq) / (2.0 * pi);
+                            const V2 z{A.x + (B.x - A.x) * f, A.y + (B.y - A.y) * f};
+                            const double wp = kress_wp(s_aux, gq);
+                            const V2 t{rawp.x * wp, rawp.y * wp};
+                            const double sp_ = std::hypot(t.x, t.y);
+                            e[0] = z.x;
+                            e[1] = z.y;
+                            e[2] = t.y / sp_;
+                            e[3] = -t.x / sp_;
+                            e[4] = h * qps_alpert_weights[kk] * sp_;
+                        }
+                        g.aux.insert(g.aux.end(), e, e + 5);
+                    }
             }
             SegDesc sd{};
             sd.kind = SEG_LINE;

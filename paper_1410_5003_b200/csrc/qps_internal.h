@@ -139,6 +139,12 @@ struct SegDesc {
 struct HostInterface {
     std::vector<double> x, y, nx, ny, w, speed;
     std::vector<SegDesc> segs;
+    // open-arc (graded-corner) interfaces: the Alpert auxiliary nodes of every
+    // row, computed on the host with the reference's arithmetic (the device's
+    // pow/sincos would move nodes that sit 8e-4 h from a target near a corner
+    // by a few ulps, ~1e-9 of the self-block entries): per row 2 x 15 entries
+    // of (x, y, n_x, n_y, quadrature weight h w_k |Z'|), side -1 then +1
+    std::vector<double> aux;
     double y_min = 0, y_max = 0, wall_y = 0;
     bool smooth = false;
     int N() const { return int(x.size()); }

@@ -145,6 +145,15 @@ void upload_geometry(Ctx& c) {
     std::vector<double> pool = g.fourier_pool;
     if (pool.empty()) pool.push_back(0.0);
     c.fourier.upload(pool, c.stream);
+    std::vector<double> aux;
+    c.aux_off.assign(I, -1);
+    for (int j = 0; j < I; ++j)
+        if (!g.ifaces[j].aux.empty()) {
+            c.aux_off[j] = (long long)aux.size();
+            aux.insert(aux.end(), g.ifaces[j].aux.begin(), g.ifaces[j].aux.end());
+        }
+    if (aux.empty()) aux.push_back(0.0);
+    c.aux_pool.upload(aux, c.stream);
     c.d_err.ensure(1);
 }
 
@@ -335,6 +344,7 @@ void fill_system_fused(Ctx& c) {
             a.smooth = q.smooth ? 1 : 0;
             a.nseg = int(q.segs.size());
             a.seg_first = c.seg_first[j];
+            a.aux_off = c.aux_off[j];
             a.row_start = alpert_rows;
             a.nk = 2;
             a.k[0] = k[j];
@@ -491,7 +501,7 @@ void fill_system_fused(Ctx& c) {
     auto t0 = std::chrono::steady_clock::now();
     launch_pair_fill(pt, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
     auto t1 = std::chrono::steady_clock::now();
-    launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.d_err.p, s, c.d_alpert);
+    launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.aux_pool.p, c.d_err.p, s, c.d_alpert);
     launch_proxy_fill(xt, pool, c.d_err.p, s, c.d_proxy, c.d_tiles);
     auto t2 = std::chrono::steady_clock::now();
     if (htrace)

@@ -233,6 +233,7 @@ void cache_fill(Ctx& c) {
             a.smooth = q.smooth ? 1 : 0;
             a.nseg = int(q.segs.size());
             a.seg_first = c.seg_first[j];
+            a.aux_off = c.aux_off[j];
             a.row_start = alpert_rows;
             a.nk = 1;
             a.k[0] = kk;
@@ -331,7 +332,7 @@ void cache_fill(Ctx& c) {
     }
     const DevPool pool{c.px.p, c.py.p, c.pnx.p, c.pny.p, c.pw.p};
     launch_pair_fill(pt, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
-    launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.d_err.p, s, c.d_alpert);
+    launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.aux_pool.p, c.d_err.p, s, c.d_alpert);
     launch_proxy_fill(xt, pool, c.d_err.p, s, c.d_proxy, c.d_tiles);
     int herr = 0;
     QPS_D2H(&herr, c.d_err.p, sizeof(int), s);

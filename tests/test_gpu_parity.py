@@ -5,17 +5,19 @@ Fill: every block of BlockSystem (assembly.hpp:293-315) element-wise.
 Tolerances (max-norm, relative to the block's max entry):
   plain Nystrom / proxy / radiation blocks   1e-12
   A_diag (Alpert-corrected self blocks)      1e-9  (hypersingular T-kind
-      corrections of size ~1e4-1e5 cancel in k_up - k_dn; 1-ulp differences in
-      auxiliary-node coordinates (device sincos/FMA) survive at ~1e-10)
-      except rows/columns within a + 3 = 13 nodes of a graded corner (the rows
-      the reference fills with the plain punctured rule, kernels.hpp:203-204,
-      and the first rows with clamped Alpert stencils, kernels.hpp:256); the
-      rest of a graded-corner self block agrees to 1e-8 (open item: ~2e-9
-      residual of unknown origin, far below config 3's own physics noise
-      floor of ~1e-2, tools/noise_floor.py). (open-arc segment
-      ends), where adjacent nodes are ~1e-11 apart and each entry is the
-      rounding residue of cancelling ~1e11-size kernels in BOTH implementations
-      (the oracle's own values there are e.g. exactly -2^-17): 1e-3.
+      corrections of size ~1e4-1e5 cancel in k_up - k_dn)
+  A_diag of graded-corner interfaces: per entry max(3 x floor, 1e-9), floor =
+      the largest change of the oracle's own entry under omega +- 1 ulp,
+      every interface offset +- 1 ulp, the polyline vertices +- 1 ulp, and
+      the reference compiled with FMA contraction (oracle/_ref/
+      libqpscat_ref_fma.so).  Next to a corner the graded nodes are 1e-7 apart
+      and an entry (k_up minus k_dn kernels) is the rounding residue of
+      terms up to 1e10 times larger (a 40-digit mpmath evaluation of one such
+      entry is 8 % away from the oracle's own value); the two builds of the
+      reference differ there by up to 3e-5 of the block scale, and so does
+      the GPU.  (Round 1 asserted 1e-3 inside 13-node corner zones; the
+      residual it carried came from device-evaluated Alpert auxiliary nodes,
+      now tabulated on the host, and a reference constant 1 ulp off.)
 Solution: the raw densities eta are NOT compared: Q_i is numerically
 rank-deficient at these sizes and equally valid residual minimizers differ by
 O(1) in eta (proj/tests/test_periodize.cpp:119-126; the oracle moves eta by
@@ -25,10 +27,15 @@ outputs are compared against the oracle's own noise floor measured here:
   |R_gpu - R_ref|, |T_gpu - T_ref|                 <= max(1e-8, 10 * floor_RT)
 where floor = change of the oracle's own outputs under a 1-ulp change of omega.
 """
+import copy
+import os
+
 import numpy as np
 import pytest
 
+from conftest import ORACLE_LIB
 from paper_1410_5003_b200 import configs
+from paper_1410_5003_b200.qpscat import Solver
 
 pytestmark = pytest.mark.gpu
 
@@ -52,6 +59,42 @@ def setup(s, cfg, nif, omega_scale=None):
     return st, num
 
 
+ORACLE_FMA = os.path.join(os.path.dirname(ORACLE_LIB), "libqpscat_ref_fma.so")
+
+
+def corner_floor(cfg, nif):
+    """Per-entry rounding floor of the reference's graded-corner self blocks
+    (see the module docstring), relative to each block's max entry."""
+    st, num, om, th, K, _ = configs.config(cfg, n_interfaces=nif)
+
+    def fill(lib, stack, omega):
+        s = Solver(lib=lib)
+        s.build_geometry(stack, num)
+        s.make_problem(omega, th, K)
+        s.precompute_shift_blocks()
+        s.assemble_system()
+        out = {j: s.download_block("A_diag", j) for j, sp in enumerate(stack.interfaces) if sp.shape == "polyline"}
+        s.close()
+        return out
+
+    base = fill(ORACLE_LIB, st, om)
+    runs = [fill(ORACLE_FMA, st, om)] + [fill(ORACLE_LIB, st, float(np.nextafter(om, sgn))) for sgn in (np.inf, -np.inf)]
+    for sgn in (np.inf, -np.inf):
+        s2 = copy.deepcopy(st)
+        for sp in s2.interfaces:
+            sp.offset = float(np.nextafter(sp.offset, sgn))
+        runs.append(fill(ORACLE_LIB, s2, om))
+        for comp in (0, 1):
+            s3 = copy.deepcopy(st)
+            for sp in s3.interfaces:
+                if sp.shape == "polyline":
+                    sp.vertices = [v if q in (0, len(sp.vertices) - 1) else
+                                   tuple(float(np.nextafter(x, sgn)) if c == comp else x for c, x in enumerate(v))
+                                   for q, v in enumerate(sp.vertices)]
+            runs.append(fill(ORACLE_LIB, s3, om))
+    return {j: np.max([np.abs(r[j] - b) for r in runs], axis=0) / np.abs(b).max() for j, b in base.items()}
+
+
 @pytest.mark.parametrize("cfg,nif", CASES)
 def test_fill_blocks_match_oracle(gpu, oracle, cfg, nif):
     for s in (gpu, oracle):
@@ -71,23 +114,11 @@ def test_fill_blocks_match_oracle(gpu, oracle, cfg, nif):
             g, o = gpu.download_block(name, i), oracle.download_block(name, i)
             assert g.shape == o.shape, (name, i)
             if name == "A_diag" and st.interfaces[i].shape == "polyline":
-                N = g.shape[0] // 2
-                ends = np.zeros(N, dtype=bool)
-                nodes = st.interfaces[i].nodes
-                nseg = len(st.interfaces[i].vertices) - 1
-                counts = nodes if len(nodes) == nseg else nodes * nseg
-                off = 0
-                for n in counts:
-                    ends[off:off + 13] = True
-                    ends[off + n - 13:off + n] = True
-                    off += n
-                ends2 = np.concatenate([ends, ends])
-                mask = ends2[:, None] | ends2[None, :]
+                floor = corner_floor(cfg, nif)[i]
                 scale = np.abs(o).max()
-                d = np.abs(g - o)
-                # open item: ~2e-9 residual on graded-corner interfaces
-                assert d[~mask].max() / scale < 1e-8, (name, i, d[~mask].max() / scale)
-                assert d[mask].max() / scale < 1e-3, (name, i, d[mask].max() / scale)
+                d = np.abs(g - o) / scale
+                bar = np.maximum(3 * floor, 1e-9)
+                assert np.all(d <= bar), (name, i, d.max(), int((d > bar).sum()))
                 continue
             assert rel(g, o) < tol, (name, i, rel(g, o))
     assert gpu.fill_evals()["reference"] == oracle.fill_evals()["reference"]
