@@ -1345,6 +1345,38 @@ void wb_anorm_async(Ctx& c, const cplx* Ad) {
     c.anorm_pending = true;
 }
 
+void wb_factor_async(Ctx& c, cplx* Ad) {
+    const Dims& D = c.dims;
+    const int npos = D.nsys * D.I, nb = D.nb;
+    const size_t nb2 = D.nb2(), dsz = lu_dinv_elems(nb);
+    cudaStream_t fs = c.side;
+    QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // A' is final (the Schur updates are queued)
+    QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_fork, 0));
+    if (c.anorm_pending) QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_anorm, 0));  // the norms read Ad first
+    c.ipiv.ensure(size_t(npos) * nb);
+    c.dinv.ensure(size_t(npos) * dsz);
+    c.l0_flag.ensure(npos);
+    c.l0_flag.zero(fs);
+    std::vector<cplx*> fa(npos), fd(npos);
+    std::vector<int*> fp(npos);
+    for (int q = 0; q < npos; ++q) {
+        fa[q] = Ad + size_t(q) * nb2;
+        fp[q] = c.ipiv.p + size_t(q) * nb;
+        fd[q] = c.dinv.p + size_t(q) * dsz;
+    }
+    if (!c.ev_f0) {
+        QPS_CUDA(cudaEventCreate(&c.ev_f0));
+        QPS_CUDA(cudaEventCreate(&c.ev_f1));
+    }
+    QPS_CUDA(cudaEventRecord(c.ev_f0, fs));
+    nvtxRangePushA("bcr_level0");
+    lu_factor_batched(nb, nb, fa, fp, fd, c.l0_flag.p, fs, c.ws2);
+    nvtxRangePop();
+    QPS_CUDA(cudaEventRecord(c.ev_f1, fs));
+    QPS_CUDA(cudaEventRecord(c.ev_factor, fs));
+    c.factor_pending = true;
+}
+
 void bcr_solve_wb(Ctx& c, cplx* Ad) {
     ProfPhase phase("bcr");
     ++c.n_factorizations;
@@ -1424,6 +1456,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
     auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2 * m; };  // r2 x m, ld r2
     std::vector<int> l0_orig;  // level-0 positions whose singular flags are checked at the end
+    bool early_factor = false;  // level 0 factored by wb_factor_async
     // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
     cudaEvent_t f0 = nullptr, f1 = nullptr;  // factor_ms of the phase times
     QPS_CUDA(cudaEventCreate(&f0));
@@ -1490,7 +1523,17 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             const char* e = getenv("QPS_WB_L0");
             return e && !strcmp(e, "separate");
         }();
-        if (separate) {
+        if (c.factor_pending) {
+            // factored on the side stream during the compression: solve only
+            QPS_CUDA(cudaStreamWaitEvent(s, c.ev_factor, 0));
+            c.factor_pending = false;
+            early_factor = true;
+            lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, s, c.ws);
+            c.bcr_flag_h.ensure(fa.size());
+            QPS_D2H(c.bcr_flag_h.p, c.l0_flag.p, sizeof(int) * fa.size(), s);
+            l0_orig = orig;
+            tmark("solve with the early factors", 0, int(fa.size()));
+        } else if (separate) {
             lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
             lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, c.ws.ptrs3.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p,
                          nullptr, s);
@@ -1749,6 +1792,11 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }
         QPS_CUDA(cudaEventElapsedTime(&fms, f0, f1));
         c.times.factor_ms = fms;
+        if (early_factor) {  // the factorization itself ran on the side stream
+            float ef = 0;
+            QPS_CUDA(cudaEventElapsedTime(&ef, c.ev_f0, c.ev_f1));
+            c.times.factor_ms = fms + ef;
+        }
         QPS_CUDA(cudaEventDestroy(f0));
         QPS_CUDA(cudaEventDestroy(f1));
     }

@@ -130,6 +130,7 @@ qps_ctx* qps_create(int device) {
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fill, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_sample, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_anorm, cudaEventDisableTiming));
+        QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_factor, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreate(&h->c.ev0));
         QPS_CUDA(cudaEventCreate(&h->c.ev1));
         upload_hankel_tables();
@@ -153,7 +154,8 @@ void qps_destroy(qps_ctx* h) {
     cudaStream_t s = h->c.stream, s2 = h->c.side, s3 = h->c.side2;
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
-    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_geo})
+    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_factor, h->c.ev_f0,
+                          h->c.ev_f1, h->c.ev_geo})
         if (e) cudaEventDestroy(e);
     delete h;
     if (s) cudaStreamDestroy(s);
@@ -386,21 +388,36 @@ int qps_solve(qps_ctx* h) {
         } total{c, t0, t1};
         c.ps_separate = false;
         c.times.factor_ms = 0.0;
-        run_fill(c);
-        c.times.assemble_ms = 0.0;
-        lr_sample_async(c);  // overlaps the Schur least squares
-        {
-            Timer t(c, &c.times.schur_ms);
-            static const bool no_defer = [] {  // QPS_DEFER=0: form the coupling updates explicitly (A/B)
-                const char* e = getenv("QPS_DEFER");
-                return e && !strcmp(e, "0");
-            }();
-            schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, !no_defer);
-        }
-        c.sys_valid = false;  // A now holds A'
-        {
-            Timer t(c, &c.times.solve_ms);
-            bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+        for (int attempt = 0;; ++attempt) {
+            run_fill(c);
+            c.times.assemble_ms = 0.0;
+            lr_sample_async(c);  // overlaps the Schur least squares
+            {
+                Timer t(c, &c.times.schur_ms);
+                static const bool no_defer = [] {  // QPS_DEFER=0: form the coupling updates explicitly (A/B)
+                    const char* e = getenv("QPS_DEFER");
+                    return e && !strcmp(e, "0");
+                }();
+                schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, !no_defer);
+            }
+            c.sys_valid = false;  // A now holds A'
+            try {
+                Timer t(c, &c.times.solve_ms);
+                c.allow_early = true;
+                bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p);
+                c.allow_early = false;
+            } catch (const Error& e) {
+                c.allow_early = false;
+                // couplings not low rank after the early level-0 factorization: once more, dense
+                if (attempt == 0 && e.status == QPS_ERR_INTERNAL && e.what() == std::string(kRetryDense)) {
+                    c.force_dense = true;
+                    continue;
+                }
+                c.force_dense = false;
+                throw;
+            }
+            c.force_dense = false;
+            break;
         }
         c.ps_valid = false;
         {

@@ -193,6 +193,13 @@ struct Ctx {
     DBuf<cplx> rc_probe;               // the probe columns (nb x 4)
     int rc_probe_n = 0;
     bool anorm_pending = false;        // rc_anorm being computed on side2 (ev_anorm)
+    // Woodbury level 0 factored on the side stream while the couplings are
+    // compressed on the main stream (wb_factor_async); force_dense: the retry
+    // after a compression that failed once that factorization had started
+    bool factor_pending = false, force_dense = false;
+    bool allow_early = false;          // set by callers that handle the kRetryDense re-run
+    cudaEvent_t ev_factor = nullptr, ev_f0 = nullptr, ev_f1 = nullptr;
+    DBuf<int> l0_flag;
     int nrhs = 1;                      // right-hand sides per block of the next block solve (> 1: caller fills F)
     bool skip_corners = false;         // schur(): interior elimination only (alpha-grouped sweep)
     bool xint_shared = false;          // recover(): every system uses system 0's interior X
@@ -244,6 +251,7 @@ struct Ctx {
     qps_phase_times times{};
     uint64_t ref_evals = 0, performed_evals = 0;
     Workspace ws;
+    Workspace ws2;                     // task tables of the early level-0 factorization (stream side)
     std::chrono::steady_clock::time_point host_t0;  // QPS_HOST_TRACE
     DBuf<PairTask> d_pair;
     DBuf<ProxyTask> d_proxy;
@@ -276,6 +284,9 @@ void lr_sample_async(Ctx& c);
 void bcr_solve_lr(Ctx& c, cplx* Ad);
 void bcr_solve_wb(Ctx& c, cplx* Ad);
 void wb_anorm_async(Ctx& c, const cplx* Ad);
+// factor every diagonal block of the Woodbury reduction (level 0) on the side
+// stream; bcr_solve_wb then only solves with the factors
+void wb_factor_async(Ctx& c, cplx* Ad);
 void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
                           int ldX, size_t Xstride, double* lsq_out);
 void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,

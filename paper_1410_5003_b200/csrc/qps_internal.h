@@ -34,6 +34,8 @@ struct Error : std::runtime_error {
         : std::runtime_error(msg), status(st), layer(layer_), bytes(bytes_) {}
 };
 [[noreturn]] inline void fail(int st, const std::string& msg) { throw Error(st, msg); }
+// internal: the block solve must be re-run with the dense reduction (bcr_solve)
+constexpr const char* kRetryDense = "qpsb: retry with the dense cyclic reduction";
 
 // counted device->host copy
 #define QPS_D2H(dst, src, bytes, stream)                                                   \

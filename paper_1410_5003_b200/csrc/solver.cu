@@ -854,12 +854,21 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         const char* e = getenv("QPS_BCR");
         return e && !strcmp(e, "lrdirect");
     }();
+    static const bool early_off = [] {  // QPS_WB_EARLY=0: factor level 0 after the compression (A/B)
+        const char* e = getenv("QPS_WB_EARLY");
+        return e && !strcmp(e, "0");
+    }();
     c.lr_rank_max = 0;
     c.lr_probe_worst = 0;
     c.bcr_path = 0;
     c.anorm_pending = false;
-    if (!dense_only && (!lr_direct || c.nrhs > 1)) wb_anorm_async(c, Ad);  // overlaps the compression
-    if (!dense_only && lr_compress(c, Au, Al)) {
+    c.factor_pending = false;
+    const bool woodbury = !dense_only && !c.force_dense && (!lr_direct || c.nrhs > 1);
+    if (woodbury) wb_anorm_async(c, Ad);  // overlaps the compression
+    // the level-0 factorization does not depend on the compressed bases: it
+    // runs on the side stream while the main stream compresses the couplings
+    if (woodbury && !early_off && c.allow_early && c.anorm_pending) wb_factor_async(c, Ad);
+    if (!dense_only && !c.force_dense && lr_compress(c, Au, Al)) {
         const bool direct = lr_direct && c.nrhs == 1;  // several right-hand sides: the Woodbury form
         c.bcr_path = direct ? 2 : 1;
         if (direct) bcr_solve_lr(c, Ad);
@@ -870,6 +879,14 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     if (c.anorm_pending) {  // the side stream's norms read Ad: join before the factorization rewrites it
         QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_anorm, 0));
         c.anorm_pending = false;
+    }
+    if (c.factor_pending) {
+        // the couplings turned out not to be low rank after the diagonal blocks
+        // were factored in place: the dense reduction needs them unfactored,
+        // so the caller re-runs the solve with force_dense
+        QPS_CUDA(cudaStreamSynchronize(c.side));
+        c.factor_pending = false;
+        throw Error(QPS_ERR_INTERNAL, kRetryDense);
     }
     if (c.couplings_deferred) {  // the dense reduction needs the periodized couplings
         std::vector<GemmTask> t(c.coupling_sup);

@@ -784,11 +784,27 @@ void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, d
                 c.prob = bp[0];
                 c.dims.nsys = int(ids.size());
                 if (mode != 0) timed(&tm.fill_ms, [&] { cache_fill(c); });
-                timed(&tm.assemble_ms, [&] { assemble_from_cache(c, bp); });
-                lr_sample_async(c);
-                timed(&tm.schur_ms, [&] { schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true); });
-                c.sys_valid = false;
-                timed(&tm.solve_ms, [&] { bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p); });
+                for (int attempt = 0;; ++attempt) {
+                    timed(&tm.assemble_ms, [&] { assemble_from_cache(c, bp); });
+                    lr_sample_async(c);
+                    timed(&tm.schur_ms, [&] { schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, true); });
+                    c.sys_valid = false;
+                    try {
+                        c.allow_early = true;
+                        timed(&tm.solve_ms, [&] { bcr_solve(c, c.Adiag.p, c.Asup.p, c.Asub.p); });
+                        c.allow_early = false;
+                    } catch (const Error& e) {
+                        c.allow_early = false;
+                        if (attempt == 0 && e.status == QPS_ERR_INTERNAL && e.what() == std::string(kRetryDense)) {
+                            c.force_dense = true;  // couplings not low rank: the batch once more, dense
+                            continue;
+                        }
+                        c.force_dense = false;
+                        throw;
+                    }
+                    c.force_dense = false;
+                    break;
+                }
                 c.sweep_interior += ids.size();  // one independent system per angle
                 c.sweep_factorizations += ids.size();
                 timed(&tm.recover_ms, [&] { recover(c); });

@@ -2,16 +2,18 @@
 oracle, i.e. the reference headers compiled unmodified against oracle/shim).
 
 For each case the oracle solves the seeded configuration of
-paper_1410_5003_b200/configs.py nominally and under four 1-ulp perturbations
-(omega up/down: every k_i moves; theta up/down: alpha and kappa_n move), and
-stores
+paper_1410_5003_b200/configs.py nominally and under eight perturbations of 1
+and 2 ulp (omega up/down: every k_i moves; theta up/down: alpha and kappa_n
+move), and stores
   * the Bragg amplitudes aU, aD (reflection_transmission's inputs,
     tridiag.hpp:11-17), R, T, flux_error (postprocess.hpp:134-180),
   * the total field u at fixed off-interface probes (evaluate_field,
     postprocess.hpp:82-123; one probe above y_U, below y_D and ~10 at
     mid-layer heights down the stack -- SURVEY §8(c)'s protocol),
-  * the oracle's 1-ulp noise floor = the largest change of those outputs
-    under the four perturbations.
+  * the oracle's ulp-level noise floor = the largest change of those outputs
+    under the eight perturbations (the outputs of a rank-deficient least-
+    squares elimination are a random sample of equally valid minimisers; the
+    maximum over eight samples bounds that spread more robustly than one).
 The GPU tests (tests/test_gpu_golden.py) assert the product against these
 numbers at <= max(1e-9, 3 x floor).
 
@@ -76,9 +78,18 @@ def solve_once(s, st, num, om, th, K, pts):
             "seconds": dt}
 
 
+def ulps(x, n):
+    for _ in range(abs(n)):
+        x = float(np.nextafter(x, np.inf if n > 0 else -np.inf))
+    return x
+
+
 def perturbations(om, th):
-    return {"omega+1ulp": (float(np.nextafter(om, np.inf)), th), "omega-1ulp": (float(np.nextafter(om, -np.inf)), th),
-            "theta+1ulp": (om, float(np.nextafter(th, np.inf))), "theta-1ulp": (om, float(np.nextafter(th, -np.inf)))}
+    out = {}
+    for n in (1, -1, 2, -2):
+        out[f"omega{n:+d}ulp"] = (ulps(om, n), th)
+        out[f"theta{n:+d}ulp"] = (om, ulps(th, n))
+    return out
 
 
 def single(name, cfg, nif, threads):
@@ -123,9 +134,10 @@ def sweep(name, cfg, threads):
     nom = run(om, thetas)
     a0 = np.concatenate([nom["aU"], nom["aD"]], axis=1)
     floors = []
-    pert = [(float(np.nextafter(om, np.inf)), thetas), (float(np.nextafter(om, -np.inf)), thetas),
-            (om, [float(np.nextafter(t, np.inf)) for t in thetas]),
-            (om, [float(np.nextafter(t, -np.inf)) for t in thetas])]
+    pert = []
+    for n in (1, -1, 2, -2):
+        pert.append((ulps(om, n), thetas))
+        pert.append((om, [ulps(t, n) for t in thetas]))
     for o2, ths in pert:
         p = run(o2, ths)
         a = np.concatenate([p["aU"], p["aD"]], axis=1)

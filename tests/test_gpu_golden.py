@@ -6,8 +6,9 @@ anomaly), configs 1-2, and the config-5 sweep (I = 100, 20 of its 200 angles).
 
 Bar (north star: 1e-9 relative in the Bragg coefficients), per quantity:
     err <= max(1e-9, 3 x floor)
-where floor is the oracle's own 1-ulp noise floor recorded in the fixture (the
-largest change of that output when omega or theta moves by one ulp).  Raw
+where floor is the oracle's own ulp-level noise floor recorded in the fixture
+(the largest change of that output when omega or theta moves by one or two
+ulps).  Raw
 densities are not compared (Q_i is numerically rank-deficient; equally valid
 minimisers differ O(1) in eta, proj/tests/test_periodize.cpp:119-126); the
 field at fixed off-interface probes (evaluate_field, postprocess.hpp:82-123)
