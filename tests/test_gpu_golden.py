@@ -6,6 +6,8 @@ anomaly), configs 1-2, and the config-5 sweep (I = 100, 20 of its 200 angles).
 
 Bar (north star: 1e-9 relative in the Bragg coefficients), per quantity:
     err <= max(1e-9, 3 x floor)
+(R and T share the larger of their two floors: R + T = 1 up to the flux
+error, so any perturbation trades one against the other.)
 where floor is the oracle's own ulp-level noise floor recorded in the fixture
 (the largest change of that output when omega or theta moves by one or two
 ulps).  Raw
@@ -63,6 +65,9 @@ def test_single_angle_matches_oracle_fixture(gpu, parity_report, name):
             "field_rel": float(np.abs(u - u0).max() / np.abs(u0).max())}
     parity_report(name, {k: (errs[k], fl[k]) for k in errs}
                   | {"flux_error": (rt["flux_error"], g["flux_error"])})
+    # R + T = 1 up to the flux error, so a perturbation moves R and T together:
+    # both are held to the larger of their two floors
+    fl = dict(fl, dR=max(fl["dR"], fl["dT"]), dT=max(fl["dR"], fl["dT"]))
     for k, e in errs.items():
         assert e <= bar(fl[k]), (name, k, e, fl[k])
 
@@ -88,4 +93,5 @@ def test_sweep_matches_oracle_fixture(gpu, parity_report):
                                              "dT (max)": (float(dT.max()), max(fl["dT"]))})
     for i in range(len(err)):
         assert err[i] <= bar(fl["bragg_rel"][i]), (i, err[i], fl["bragg_rel"][i])
-        assert dR[i] <= bar(fl["dR"][i]) and dT[i] <= bar(fl["dT"][i]), (i, dR[i], dT[i])
+        frt = max(fl["dR"][i], fl["dT"][i])  # R + T = 1 up to the flux error
+        assert dR[i] <= bar(frt) and dT[i] <= bar(frt), (i, dR[i], dT[i])
