@@ -290,6 +290,61 @@ __global__ void qr_take_r_kernel(int m, int p, const cplx* __restrict__ Y, size_
 }
 
 // X = [Q2 (p x r); 0] (m x r), and its conjugate transpose later
+// Compact-WY merge of nb panels of width kQrW (zlarft's block recurrence):
+// T (64 x 64, upper triangular) from the panels' own T_k (kQrW x kQrW, at
+// Tp + k kQrW^2 per problem, stride tpstride) and G = V^* V (only its blocks
+// G_ij, i < j, are read; column-major, ld 64):
+//   T_kk = T_k,  T_{0:k, k} = -T_{0:k, 0:k} (G_{0:k, k} T_k).
+__global__ void __launch_bounds__(256) wy_merge_kernel(int nb, const cplx* __restrict__ Tp, size_t tpstride,
+                                                       const cplx* __restrict__ G, cplx* __restrict__ Tout) {
+    constexpr int W = kQrW, P = 4 * kQrW;
+    extern __shared__ cplx wy_sm[];
+    cplx (*T)[P + 1] = reinterpret_cast<cplx (*)[P + 1]>(wy_sm);            // T[row][col]
+    cplx (*M)[W + 1] = reinterpret_cast<cplx (*)[W + 1]>(wy_sm + P * (P + 1));  // G_{0:k,k} T_k
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int n = nb * W;
+    const cplx* Gb = G + size_t(b) * P * P;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int r = e % n, cc = e / n;
+        const int kb = cc / W;
+        cplx v{0, 0};
+        if (r / W == kb) v = Tp[size_t(b) * tpstride + size_t(kb) * W * W + size_t(cc % W) * W + (r % W)];
+        T[r][cc] = v;
+    }
+    __syncthreads();
+    for (int k = 1; k < nb; ++k) {
+        const int rows = k * W;
+        for (int e = tid; e < rows * W; e += blockDim.x) {  // M = G_{0:k,k} T_k
+            const int r = e % rows, j = e / rows;
+            cplx acc{0, 0};
+            for (int q = 0; q < W; ++q) {
+                const cplx g = Gb[size_t(k * W + q) * P + r];
+                const cplx t = T[k * W + q][k * W + j];
+                acc.re += g.re * t.re - g.im * t.im;
+                acc.im += g.re * t.im + g.im * t.re;
+            }
+            M[r][j] = acc;
+        }
+        __syncthreads();
+        for (int e = tid; e < rows * W; e += blockDim.x) {  // T_{0:k,k} = -T_{0:k,0:k} M
+            const int r = e % rows, j = e / rows;
+            cplx acc{0, 0};
+            for (int q = r; q < rows; ++q) {  // T_{0:k,0:k} is upper triangular
+                const cplx t = T[r][q];
+                const cplx mm = M[q][j];
+                acc.re += t.re * mm.re - t.im * mm.im;
+                acc.im += t.re * mm.im + t.im * mm.re;
+            }
+            T[r][k * W + j] = cplx{-acc.re, -acc.im};
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < P * P; e += blockDim.x) {
+        const int r = e % P, cc = e / P;
+        Tout[size_t(b) * P * P + e] = (r < n && cc < n) ? T[r][cc] : cplx{0, 0};
+    }
+}
+
 __global__ void qr_seed_kernel(int m, int p, int r, const cplx* __restrict__ Q2, size_t q2stride,
                                cplx* __restrict__ X, size_t xstride) {
     const int b = blockIdx.x;
@@ -853,18 +908,46 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         c.lr_PH.ensure(size_t(nc) * r * nb);
         { QPS_NOTE_LAUNCH(); qr_seed_kernel<<<nc, 256, 0, s>>>(m, p, r, c.lr_Q2.p, size_t(p) * r, c.lr_P.p, size_t(nb) * r); }
         QPS_CUDA(cudaGetLastError());
-        for (int pn = nP - 1; pn >= 0; --pn) {
-            std::vector<GemmTask> t1(nc), t2(nc), t3(nc);
-            for (int q = 0; q < nc; ++q) {
-                cplx* X = c.lr_P.p + size_t(q) * nb * r;
-                t1[q] = gemm1(VH_of(q, pn), kQrW, X, nb, m, c.lr_W1.p + size_t(q) * kQrW * p, kQrW);
-                t2[q] = gemm1(T_of(q, pn), kQrW, c.lr_W1.p + size_t(q) * kQrW * p, kQrW, kQrW,
-                              c.lr_W2.p + size_t(q) * kQrW * p, kQrW);
-                t3[q] = gemm1(V_of(q, pn), m, c.lr_W2.p + size_t(q) * kQrW * p, kQrW, kQrW, X, nb);
+        // the four panels' reflectors as one compact WY, Q = I - V T V^* with
+        // V = [V0 V1 V2 V3] (m x 64, the panels are stored contiguously) and T
+        // upper triangular from the block recurrence T_{0:k,k} =
+        // -T_{0:k,0:k} (V_{0:k}^* V_k) T_kk (zlarft, forward): P = [Q2; 0] -
+        // V (T (V^* [Q2; 0])), where V^* [Q2; 0] only reads V's first 64 rows
+        c.lr_Gq.ensure(size_t(nc) * p * p);
+        c.lr_Tall.ensure(size_t(nc) * p * p);
+        c.lr_W1a.ensure(size_t(nc) * p * r);
+        c.lr_W2a.ensure(size_t(nc) * p * r);
+        {
+            std::vector<GemmTask> gt;
+            gt.reserve(size_t(nc) * nP * (nP - 1) / 2);
+            for (int q = 0; q < nc; ++q)
+                for (int j = 1; j < nP; ++j)
+                    for (int i = 0; i < j; ++i)  // G_ij = V_i^* V_j (V_j vanishes above row 16 j)
+                        gt.push_back(gemm1(VH_of(q, i) + size_t(j) * kQrW * kQrW, kQrW,
+                                           V_of(q, j) + size_t(j) * kQrW, m, m - j * kQrW,
+                                           c.lr_Gq.p + size_t(q) * p * p + size_t(j) * kQrW * p + i * kQrW, p));
+            zgemm_batched(kQrW, kQrW, cplx{1, 0}, cplx{0, 0}, gt, s, c.ws.gemm_tasks, "lr_qr");
+            constexpr size_t wy_sm = (size_t(4 * kQrW) * (4 * kQrW + 1) + size_t(4 * kQrW) * (kQrW + 1)) * sizeof(cplx);
+            static bool wy_attr = false;
+            if (!wy_attr) {
+                QPS_CUDA(cudaFuncSetAttribute(wy_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wy_sm)));
+                wy_attr = true;
             }
-            zgemm_batched(kQrW, r, cplx{1, 0}, cplx{0, 0}, t1, s, c.ws.gemm_tasks, "lr_qr");
-            zgemm_batched(kQrW, r, cplx{1, 0}, cplx{0, 0}, t2, s, c.ws.gemm_tasks, "lr_qr");
-            zgemm_batched(m, r, cplx{-1, 0}, cplx{1, 0}, t3, s, c.ws.gemm_tasks, "lr_qr");
+            { QPS_NOTE_LAUNCH(); wy_merge_kernel<<<nc, 256, wy_sm, s>>>(nP, c.lr_Tq.p, size_t(nP) * kQrW * kQrW,
+                                                                          c.lr_Gq.p, c.lr_Tall.p); }
+            QPS_CUDA(cudaGetLastError());
+            std::vector<GemmTask> w1(size_t(nc) * nP), w2(nc), pu(nc);
+            for (int q = 0; q < nc; ++q) {
+                for (int pn = 0; pn < nP; ++pn)  // W1 = V^*[0:64, :] Q2
+                    w1[size_t(q) * nP + pn] = gemm1(VH_of(q, pn), kQrW, c.lr_Q2.p + size_t(q) * p * r, p, p,
+                                                   c.lr_W1a.p + size_t(q) * p * r + pn * kQrW, p);
+                w2[q] = gemm1(c.lr_Tall.p + size_t(q) * p * p, p, c.lr_W1a.p + size_t(q) * p * r, p, p,
+                              c.lr_W2a.p + size_t(q) * p * r, p);
+                pu[q] = gemm1(V_of(q, 0), m, c.lr_W2a.p + size_t(q) * p * r, p, p, c.lr_P.p + size_t(q) * nb * r, nb);
+            }
+            zgemm_batched(kQrW, r, cplx{1, 0}, cplx{0, 0}, w1, s, c.ws.gemm_tasks, "lr_qr");
+            zgemm_batched(p, r, cplx{1, 0}, cplx{0, 0}, w2, s, c.ws.gemm_tasks, "lr_qr");
+            zgemm_batched(m, r, cplx{-1, 0}, cplx{1, 0}, pu, s, c.ws.gemm_tasks, "lr_qr");
         }
         tmark("rank check, Q2, P = Q [Q2; 0]");
         { QPS_NOTE_LAUNCH(); conj_transpose_kernel<<<dim3((nb + kCtRows - 1) / kCtRows, nc), 256, 0, s>>>(nb, r, c.lr_P.p, size_t(nb) * r, c.lr_PH.p,
@@ -1013,6 +1096,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         QPS_CUDA(cudaEventDestroy(te0));
         QPS_CUDA(cudaEventDestroy(te1));
     }
+    tl_mark(c, "compress", s);
     if (rank_deferred) {
         QPS_CUDA(cudaEventSynchronize(c.ev_sample));
         int mx = 0;
@@ -1302,6 +1386,7 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
         zgemv_batched(nb, mone, one, t2, s, c.ws.gemv_tasks);
     }
     tmark("backsub", lvl, 0);
+    tl_mark(c, "backsub", s);
     if (trace) {
         QPS_CUDA(cudaEventDestroy(te0));
         QPS_CUDA(cudaEventDestroy(te1));
@@ -1349,7 +1434,11 @@ void wb_factor_async(Ctx& c, cplx* Ad) {
     const Dims& D = c.dims;
     const int npos = D.nsys * D.I, nb = D.nb;
     const size_t nb2 = D.nb2(), dsz = lu_dinv_elems(nb);
-    cudaStream_t fs = c.side;
+    static const bool low = [] {  // QPS_FACTOR_STREAM=side2: the low-priority stream (A/B)
+        const char* e = getenv("QPS_FACTOR_STREAM");
+        return e && !strcmp(e, "side2");
+    }();
+    cudaStream_t fs = low ? c.side2 : c.side;
     QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // A' is final (the Schur updates are queued)
     QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_fork, 0));
     if (c.anorm_pending) QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_anorm, 0));  // the norms read Ad first
@@ -1373,6 +1462,7 @@ void wb_factor_async(Ctx& c, cplx* Ad) {
     lu_factor_batched(nb, nb, fa, fp, fd, c.l0_flag.p, fs, c.ws2);
     nvtxRangePop();
     QPS_CUDA(cudaEventRecord(c.ev_f1, fs));
+    tl_mark(c, "factor(side)", fs);
     QPS_CUDA(cudaEventRecord(c.ev_factor, fs));
     c.factor_pending = true;
 }
@@ -1564,6 +1654,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, s);
         QPS_D2H(c.rc_flag_h.p + npos, c.rc_sus.p, sizeof(int) * npos, s);
         QPS_CUDA(cudaEventRecord(f1, s));
+        tl_mark(c, "level0", s);
         nvtxRangePop();
         // y = D^{-1} f back into F (column 2r of every W_j)
         QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * fs, c.lr_W0.p + size_t(r2) * nb,
@@ -1733,6 +1824,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         levels.push_back(std::move(nxt));
         ++lvl;
     }
+    tl_mark(c, "levels", s);
     {  // final block of every system
         std::vector<Pos*> fin;
         for (int a = 0; a < ns; ++a) fin.push_back(&levels[lvl][a][0]);
@@ -1837,6 +1929,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         rhs.run(nb, mone, one, t2);
     }
     tmark("backsub", lvl, 0);
+    tl_mark(c, "backsub", s);
     if (trace) {
         QPS_CUDA(cudaEventDestroy(te0));
         QPS_CUDA(cudaEventDestroy(te1));

@@ -388,8 +388,10 @@ int qps_solve(qps_ctx* h) {
         } total{c, t0, t1};
         c.ps_separate = false;
         c.times.factor_ms = 0.0;
+        tl_mark(c, "start", c.stream);
         for (int attempt = 0;; ++attempt) {
             run_fill(c);
+            tl_mark(c, "fill", c.stream);
             c.times.assemble_ms = 0.0;
             lr_sample_async(c);  // overlaps the Schur least squares
             {
@@ -400,6 +402,7 @@ int qps_solve(qps_ctx* h) {
                 }();
                 schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, !no_defer);
             }
+            tl_mark(c, "schur", c.stream);
             c.sys_valid = false;  // A now holds A'
             try {
                 Timer t(c, &c.times.solve_ms);
@@ -424,6 +427,8 @@ int qps_solve(qps_ctx* h) {
             Timer t(c, &c.times.recover_ms);
             recover(c);
         }
+        tl_mark(c, "recover", c.stream);
+        tl_report(c);
     });
 }
 

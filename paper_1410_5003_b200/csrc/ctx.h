@@ -178,6 +178,7 @@ struct Ctx {
     cudaEvent_t ev_geo = nullptr;
     HBuf<int> lr_rank_h;               // sample ranks, read back without a stream sync
     DBuf<cplx> lr_G2, lr_Y2;           // probe: gathered R and X columns; C[:, J]
+    DBuf<cplx> lr_Tall, lr_W1a, lr_W2a, lr_Gq;  // compact-WY T of the sample QR, V^* V, products
     DBuf<int> lr_probe_cols, lr_gld;   // probe column indices (nc x 16); gather leading dimensions
     DBuf<const cplx*> lr_gptr;         // gather source pointers
     int lr_probe_n = 0;
@@ -198,6 +199,10 @@ struct Ctx {
     // after a compression that failed once that factorization had started
     bool factor_pending = false, force_dense = false;
     bool allow_early = false;          // set by callers that handle the kRetryDense re-run
+    // QPS_TIMELINE=1: non-blocking timing events at phase boundaries on their
+    // own streams, printed after qps_solve (critical-path study, no syncs)
+    std::vector<std::pair<const char*, cudaEvent_t>> tl_marks;
+    std::vector<cudaEvent_t> tl_pool;
     cudaEvent_t ev_factor = nullptr, ev_f0 = nullptr, ev_f1 = nullptr;
     DBuf<int> l0_flag;
     int nrhs = 1;                      // right-hand sides per block of the next block solve (> 1: caller fills F)
@@ -322,6 +327,32 @@ void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, d
 std::vector<double> plan_sweep_angles(double k1, double d, int n_alpha, double th_lo, double th_hi);
 // alpha group of each listed problem (|alpha_a - alpha_b| <= 1e-12)
 std::vector<int> group_by_alpha(const std::vector<Problem>& probs, const std::vector<int>& ids, int* ngroups);
+
+inline bool timeline_on() {
+    static const bool on = getenv("QPS_TIMELINE") != nullptr;
+    return on;
+}
+inline void tl_mark(Ctx& c, const char* what, cudaStream_t s) {
+    if (!timeline_on()) return;
+    cudaEvent_t e;
+    if (c.tl_pool.empty()) cudaEventCreate(&e);
+    else { e = c.tl_pool.back(); c.tl_pool.pop_back(); }
+    cudaEventRecord(e, s);
+    c.tl_marks.push_back({what, e});
+}
+inline void tl_report(Ctx& c) {
+    if (!timeline_on() || c.tl_marks.empty()) return;
+    cudaDeviceSynchronize();
+    fprintf(stderr, "timeline (ms from %s):", c.tl_marks.front().first);
+    for (auto& m : c.tl_marks) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c.tl_marks.front().second, m.second);
+        fprintf(stderr, " %s %.2f |", m.first, ms);
+        c.tl_pool.push_back(m.second);
+    }
+    fprintf(stderr, "\n");
+    c.tl_marks.clear();
+}
 
 struct Timer {
     Ctx& c;

@@ -749,6 +749,7 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
     QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
     QPS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
     qsolve_families(c, fams, true);  // returns once the interior layers are done
+    tl_mark(c, "schur:interior-lsq", c.stream);
     // A' updates of all systems in one batched GEMM (periodize.hpp:88-91, 115, 119):
     //   Ap_diag[j] -= B_self[j] X_self(j) + B_below[j] X_above(j+1)
     //   Ap_super[j] -= B_below[j] X_self(j+1),  Ap_sub[j] -= B_self[j+1] X_above(j+1)
