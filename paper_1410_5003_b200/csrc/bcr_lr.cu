@@ -1064,6 +1064,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             for (int q = 0; q < nc; ++q) c.lr_rank_h[q] = 0;  // ranks already checked above
         }
     }
+    wb_level0_async(c);  // level 0 on the factor stream, overlapping the projection below
     // R = P^* C  (= P^* A + (-P^* Bc) X when deferred)
     c.lr_R.ensure(size_t(nc) * r * nb);
     {
@@ -1430,6 +1431,82 @@ void wb_anorm_async(Ctx& c, const cplx* Ad) {
     c.anorm_pending = true;
 }
 
+// fixed unit-modulus probes (seeded phases), ||r_k||_1 = nb
+void rc_probes(Ctx& c, int nb, cudaStream_t s) {
+    if (c.rc_probe_n == nb) return;
+    std::vector<cplx> pr(size_t(nb) * kRcProbe);
+    uint64_t x = 0x243f6a8885a308d3ull;
+    for (auto& z : pr) {
+        x ^= x >> 12;
+        x ^= x << 25;
+        x ^= x >> 27;
+        const double ph = 2.0 * kPi * double((x * 0x2545f4914f6cdd1dull) >> 11) * (1.0 / 9007199254740992.0);
+        z = cplx{cos(ph), sin(ph)};
+    }
+    c.rc_probe.upload(pr, s);
+    c.rc_probe_n = nb;
+}
+
+// single right-hand side per system: f on block 0 of every system (c.F)
+void wb_stage_rhs(Ctx& c, cudaStream_t s) {
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, ns = D.nsys;
+    c.F.ensure(size_t(ns) * I * nb);
+    c.F.zero(s);
+    for (int a = 0; a < ns; ++a)
+        QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
+                                 cudaMemcpyDeviceToDevice, s));
+}
+
+// Level 0 of the Woodbury reduction on the factor stream as soon as the
+// compressed bases exist: W_j = D_j^{-1} [P_L P_U f_j probes] with the factors
+// of wb_factor_async, the rcond screen, y = D^{-1} f into F -- overlapping the
+// projection R = P^* C that the main stream runs next (lr_compress)
+void wb_level0_async(Ctx& c) {
+    if (!c.factor_pending || !c.wb_Ad) return;
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, ns = D.nsys, r = c.lr_r, r2 = 2 * r, npos = ns * I;
+    const int m = std::max(1, c.nrhs);
+    const size_t nb2 = D.nb2(), dsz = lu_dinv_elems(nb), fs = size_t(nb) * m, per = size_t(nb) * r;
+    const int wc = r2 + m + kRcProbe;
+    cudaStream_t f = c.factor_stream;
+    QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // the bases P are queued
+    QPS_CUDA(cudaStreamWaitEvent(f, c.ev_fork, 0));
+    if (m == 1) wb_stage_rhs(c, f);
+    rc_probes(c, nb, f);
+    c.lr_W0.ensure(size_t(npos) * nb * wc);
+    { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, f>>>(I, nb, per, c.lr_P.p, c.F.p, m,
+                                                                            c.rc_probe.p, kRcProbe, c.lr_W0.p); }
+    QPS_CUDA(cudaGetLastError());
+    std::vector<cplx*> fa(npos), fd(npos), wb(npos);
+    std::vector<int*> fp(npos);
+    for (int q = 0; q < npos; ++q) {
+        fa[q] = c.wb_Ad + size_t(q) * nb2;
+        fp[q] = c.ipiv.p + size_t(q) * nb;
+        fd[q] = c.dinv.p + size_t(q) * dsz;
+        wb[q] = c.lr_W0.p + size_t(q) * nb * wc;
+    }
+    lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, f, c.ws2);
+    c.bcr_flag_h.ensure(npos);
+    QPS_D2H(c.bcr_flag_h.p, c.l0_flag.p, sizeof(int) * npos, f);
+    c.rc_flag.ensure(npos);
+    c.rc_sus.ensure(npos);
+    c.rc_estlo.ensure(npos);
+    QPS_CUDA(cudaMemsetAsync(c.rc_flag.p, 0, sizeof(int) * npos, f));
+    QPS_CUDA(cudaMemsetAsync(c.rc_sus.p, 0, sizeof(int) * npos, f));
+    if (rcond_enabled())
+        rcond_screen(c.lr_W0.p, size_t(nb) * wc, nb, r2 + m, kRcProbe, c.rc_anorm.p, double(nb), npos, kRcondMin,
+                     kRcSuspect, c.rc_flag.p, c.rc_sus.p, c.rc_estlo.p, f);
+    c.rc_flag_h.ensure(2 * size_t(npos));
+    QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, f);
+    QPS_D2H(c.rc_flag_h.p + npos, c.rc_sus.p, sizeof(int) * npos, f);
+    QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * fs, c.lr_W0.p + size_t(r2) * nb, sizeof(cplx) * nb * wc,
+                               sizeof(cplx) * fs, npos, cudaMemcpyDeviceToDevice, f));
+    tl_mark(c, "level0-solve(side)", f);
+    QPS_CUDA(cudaEventRecord(c.ev_l0, f));
+    c.l0_async = true;
+}
+
 void wb_factor_async(Ctx& c, cplx* Ad) {
     const Dims& D = c.dims;
     const int npos = D.nsys * D.I, nb = D.nb;
@@ -1439,6 +1516,9 @@ void wb_factor_async(Ctx& c, cplx* Ad) {
         return e && !strcmp(e, "side2");
     }();
     cudaStream_t fs = low ? c.side2 : c.side;
+    c.factor_stream = fs;
+    c.wb_Ad = Ad;
+    c.l0_async = false;
     QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // A' is final (the Schur updates are queued)
     QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_fork, 0));
     if (c.anorm_pending) QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_anorm, 0));  // the norms read Ad first
@@ -1479,20 +1559,14 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     // right-hand sides: m = c.nrhs columns per block (nb x m, ld nb); with m = 1
     // the system's f on block 0, with m > 1 the caller has filled c.F
     const int m = std::max(1, c.nrhs);
-    if (m == 1) {
-        c.F.ensure(size_t(npos) * nb);
-        c.F.zero(s);
-        for (int a = 0; a < ns; ++a)
-            QPS_CUDA(cudaMemcpyAsync(c.F.p + size_t(a) * I * nb, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
-                                     cudaMemcpyDeviceToDevice, s));
-    }
+    if (m == 1 && !c.l0_async) wb_stage_rhs(c, s);
     const size_t fs = size_t(nb) * m;  // per-block stride of F
     RhsOps rhs{m, s, c.ws};
     c.ipiv.ensure(size_t(npos) * nb);
     const size_t dsz = lu_dinv_elems(nb);
     c.dinv.ensure(size_t(npos) * dsz);
     const int wc = r2 + m + kRcProbe;  // [W | y | rcond probes] per block
-    c.lr_W0.ensure(size_t(npos) * nb * wc);
+    if (!c.l0_async) c.lr_W0.ensure(size_t(npos) * nb * wc);
     c.lr_S.ensure(size_t(npos) * r2 * nb);
     c.lr_g.ensure(size_t(npos) * r2 * m);
     c.lr_S.zero(s);
@@ -1547,6 +1621,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2 * m; };  // r2 x m, ld r2
     std::vector<int> l0_orig;  // level-0 positions whose singular flags are checked at the end
     bool early_factor = false;  // level 0 factored by wb_factor_async
+    const bool l0_async_done = c.l0_async;  // and solved by wb_level0_async
     // ---- level 0: factor every block, W = D^{-1} [P_L P_U], y = D^{-1} f
     cudaEvent_t f0 = nullptr, f1 = nullptr;  // factor_ms of the phase times
     QPS_CUDA(cudaEventCreate(&f0));
@@ -1559,29 +1634,21 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         std::vector<cplx*> fa, fd, wb, vb;
         std::vector<int*> fp;
         std::vector<int> orig;
-        if (c.rc_probe_n != nb) {  // fixed unit-modulus probes (seeded phases): ||r_k||_1 = nb
-            std::vector<cplx> pr(size_t(nb) * kRcProbe);
-            uint64_t x = 0x243f6a8885a308d3ull;
-            for (auto& z : pr) {
-                x ^= x >> 12;
-                x ^= x << 25;
-                x ^= x >> 27;
-                const double ph = 2.0 * kPi * double((x * 0x2545f4914f6cdd1dull) >> 11) * (1.0 / 9007199254740992.0);
-                z = cplx{cos(ph), sin(ph)};
-            }
-            c.rc_probe.upload(pr, s);
-            c.rc_probe_n = nb;
-        }
-        if (c.anorm_pending) {  // ||D_j^0||_1 (side stream, before the factorization overwrites Ad)
+        if (!c.l0_async) rc_probes(c, nb, s);
+        if (c.l0_async) {
+            c.anorm_pending = false;  // the factor stream already waited for the norms and solved level 0
+        } else if (c.anorm_pending) {  // ||D_j^0||_1 (side stream, before the factorization overwrites Ad)
             QPS_CUDA(cudaStreamWaitEvent(s, c.ev_anorm, 0));
             c.anorm_pending = false;
         } else if (rcond_enabled()) {
             c.rc_anorm.ensure(npos);
             batched_norm1(Ad, nb, nb, nb2, npos, c.rc_anorm.p, s);
         }
-        { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, m,
-                                                                                c.rc_probe.p, kRcProbe, c.lr_W0.p); }
-        QPS_CUDA(cudaGetLastError());
+        if (!c.l0_async) {
+            { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, s>>>(I, nb, per, c.lr_P.p, c.F.p, m,
+                                                                                    c.rc_probe.p, kRcProbe, c.lr_W0.p); }
+            QPS_CUDA(cudaGetLastError());
+        }
         for (int a = 0; a < ns; ++a) {
             const size_t qa = size_t(a) * 2 * (I - 1);
             for (int j = 0; j < I; ++j) {
@@ -1613,7 +1680,15 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             const char* e = getenv("QPS_WB_L0");
             return e && !strcmp(e, "separate");
         }();
-        if (c.factor_pending) {
+        if (c.l0_async) {
+            // factored and solved on the factor stream (wb_factor_async +
+            // wb_level0_async) while the couplings were compressed
+            QPS_CUDA(cudaStreamWaitEvent(s, c.ev_l0, 0));
+            c.l0_async = false;
+            c.factor_pending = false;
+            early_factor = true;
+            l0_orig = orig;
+        } else if (c.factor_pending) {
             // factored on the side stream during the compression: solve only
             QPS_CUDA(cudaStreamWaitEvent(s, c.ev_factor, 0));
             c.factor_pending = false;
@@ -1642,6 +1717,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         }
         // rcond screen from the probe columns (certain flags + suspects), read
         // back with the singular flags
+        if (!early_factor || !l0_async_done) {
         c.rc_flag.ensure(npos);
         c.rc_sus.ensure(npos);
         c.rc_estlo.ensure(npos);
@@ -1653,12 +1729,14 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         c.rc_flag_h.ensure(2 * size_t(npos));
         QPS_D2H(c.rc_flag_h.p, c.rc_flag.p, sizeof(int) * npos, s);
         QPS_D2H(c.rc_flag_h.p + npos, c.rc_sus.p, sizeof(int) * npos, s);
+        }
         QPS_CUDA(cudaEventRecord(f1, s));
         tl_mark(c, "level0", s);
         nvtxRangePop();
         // y = D^{-1} f back into F (column 2r of every W_j)
-        QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * fs, c.lr_W0.p + size_t(r2) * nb,
-                                   sizeof(cplx) * nb * wc, sizeof(cplx) * fs, npos, cudaMemcpyDeviceToDevice, s));
+        if (!l0_async_done)
+            QPS_CUDA(cudaMemcpy2DAsync(c.F.p, sizeof(cplx) * fs, c.lr_W0.p + size_t(r2) * nb,
+                                       sizeof(cplx) * nb * wc, sizeof(cplx) * fs, npos, cudaMemcpyDeviceToDevice, s));
         tmark("solve", 0, int(fa.size()));
         levels.push_back(std::move(L0));
     }

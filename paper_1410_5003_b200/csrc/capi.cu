@@ -131,6 +131,7 @@ qps_ctx* qps_create(int device) {
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_sample, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_anorm, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_factor, cudaEventDisableTiming));
+        QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_l0, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreate(&h->c.ev0));
         QPS_CUDA(cudaEventCreate(&h->c.ev1));
         upload_hankel_tables();
@@ -154,7 +155,7 @@ void qps_destroy(qps_ctx* h) {
     cudaStream_t s = h->c.stream, s2 = h->c.side, s3 = h->c.side2;
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
-    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_factor, h->c.ev_f0,
+    for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_factor, h->c.ev_l0, h->c.ev_f0,
                           h->c.ev_f1, h->c.ev_geo})
         if (e) cudaEventDestroy(e);
     delete h;

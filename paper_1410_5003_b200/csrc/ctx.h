@@ -199,6 +199,10 @@ struct Ctx {
     // after a compression that failed once that factorization had started
     bool factor_pending = false, force_dense = false;
     bool allow_early = false;          // set by callers that handle the kRetryDense re-run
+    bool l0_async = false;             // level 0 solved on the factor stream (wb_level0_async, ev_l0)
+    cudaEvent_t ev_l0 = nullptr;
+    cudaStream_t factor_stream = nullptr;
+    cplx* wb_Ad = nullptr;             // the diagonal blocks being factored early
     // QPS_TIMELINE=1: non-blocking timing events at phase boundaries on their
     // own streams, printed after qps_solve (critical-path study, no syncs)
     std::vector<std::pair<const char*, cudaEvent_t>> tl_marks;
@@ -292,6 +296,8 @@ void wb_anorm_async(Ctx& c, const cplx* Ad);
 // factor every diagonal block of the Woodbury reduction (level 0) on the side
 // stream; bcr_solve_wb then only solves with the factors
 void wb_factor_async(Ctx& c, cplx* Ad);
+// level 0 solved on the factor stream once the compressed bases exist (called by lr_compress)
+void wb_level0_async(Ctx& c);
 void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int ldR, size_t Rstride, cplx* X,
                           int ldX, size_t Xstride, double* lsq_out);
 void host_spectrum(const Ctx& c, double* R, double* T, double* fe, double* kappa, cplx* kU, cplx* kD, int* pu,
