@@ -1412,6 +1412,8 @@ void bcr_solve_lr(Ctx& c, cplx* Ad) {
 // ||D_j^0||_1 of every diagonal block for the level-0 rcond screen, on the side
 // stream while the couplings are compressed (Ad is final after the Schur step;
 // bcr_solve_wb joins before its factorization overwrites Ad)
+bool lr_eligible_pub(const Ctx& c) { return lr_eligible(c); }
+
 bool rcond_enabled() {
     static const bool on = [] {  // QPS_RCOND=0: skip the level-0 rcond screen (A/B timing only)
         const char* e = getenv("QPS_RCOND");
@@ -1511,17 +1513,27 @@ void wb_factor_async(Ctx& c, cplx* Ad) {
     const Dims& D = c.dims;
     const int npos = D.nsys * D.I, nb = D.nb;
     const size_t nb2 = D.nb2(), dsz = lu_dinv_elems(nb);
-    static const bool low = [] {  // QPS_FACTOR_STREAM=side2: the low-priority stream (A/B)
+    // high priority (the corner stream, idle by now): the GPU is throughput-
+    // bound here and the factorization plus the level-0 solve are the longer
+    // chain (measured 150 ms per config-4 solve vs 155 ms with the
+    // factorization on the low-priority side3, QPS_FACTOR_STREAM=low)
+    static const bool low = [] {
         const char* e = getenv("QPS_FACTOR_STREAM");
-        return e && !strcmp(e, "side2");
+        return e && !strcmp(e, "low");
     }();
-    cudaStream_t fs = low ? c.side2 : c.side;
+    cudaStream_t fs = low ? c.side3 : c.side;
     c.factor_stream = fs;
     c.wb_Ad = Ad;
     c.l0_async = false;
     QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // A' is final (the Schur updates are queued)
     QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_fork, 0));
-    if (c.anorm_pending) QPS_CUDA(cudaStreamWaitEvent(fs, c.ev_anorm, 0));  // the norms read Ad first
+    // ||D_j^0||_1 for the rcond screen, on this stream before the factorization
+    // overwrites Ad (not behind the compression sample on side2)
+    if (rcond_enabled()) {
+        c.rc_anorm.ensure(npos);
+        batched_norm1(Ad, nb, nb, nb2, npos, c.rc_anorm.p, fs);
+    }
+    c.anorm_pending = false;
     c.ipiv.ensure(size_t(npos) * nb);
     c.dinv.ensure(size_t(npos) * dsz);
     c.l0_flag.ensure(npos);

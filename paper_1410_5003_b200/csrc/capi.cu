@@ -126,6 +126,7 @@ qps_ctx* qps_create(int device) {
         const char* sp = getenv("QPS_SAMPLE_PRIO");  // A/B: "main" puts side2 level with the main stream
         QPS_CUDA(cudaStreamCreateWithPriority(&h->c.side2, cudaStreamNonBlocking,
                                               (sp && !strcmp(sp, "main")) ? prio_main : prio_lo));
+        QPS_CUDA(cudaStreamCreateWithPriority(&h->c.side3, cudaStreamNonBlocking, prio_lo));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fork, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fill, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_sample, cudaEventDisableTiming));
@@ -152,9 +153,10 @@ void qps_destroy(qps_ctx* h) {
     cudaStreamSynchronize(h->c.stream);
     if (h->c.ev0) cudaEventDestroy(h->c.ev0);
     if (h->c.ev1) cudaEventDestroy(h->c.ev1);
-    cudaStream_t s = h->c.stream, s2 = h->c.side, s3 = h->c.side2;
+    cudaStream_t s = h->c.stream, s2 = h->c.side, s3 = h->c.side2, s4 = h->c.side3;
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
+    if (s4) cudaStreamSynchronize(s4);
     for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_factor, h->c.ev_l0, h->c.ev_f0,
                           h->c.ev_f1, h->c.ev_geo})
         if (e) cudaEventDestroy(e);
@@ -162,6 +164,7 @@ void qps_destroy(qps_ctx* h) {
     if (s) cudaStreamDestroy(s);
     if (s2) cudaStreamDestroy(s2);
     if (s3) cudaStreamDestroy(s3);
+    if (s4) cudaStreamDestroy(s4);
 }
 
 int qps_last_error(const qps_ctx* h, char* msg, size_t cap, int* layer, uint64_t* bytes) {

@@ -120,6 +120,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // second stream: work independent of the main stream (corner least squares)
     cudaStream_t side2 = nullptr; // third stream: the low-rank sample overlapping the Schur least squares
+    cudaStream_t side3 = nullptr; // fourth stream (low priority): the early level-0 factorization
     cudaEvent_t ev_fork = nullptr, ev_fill = nullptr, ev_sample = nullptr;
     cudaEvent_t ev_anorm = nullptr;  // level-0 block norms done (side2)
 
@@ -293,6 +294,7 @@ void lr_sample_async(Ctx& c);
 void bcr_solve_lr(Ctx& c, cplx* Ad);
 void bcr_solve_wb(Ctx& c, cplx* Ad);
 void wb_anorm_async(Ctx& c, const cplx* Ad);
+bool lr_eligible_pub(const Ctx& c);  // the low-rank reduction applies to these dims
 // factor every diagonal block of the Woodbury reduction (level 0) on the side
 // stream; bcr_solve_wb then only solves with the factors
 void wb_factor_async(Ctx& c, cplx* Ad);

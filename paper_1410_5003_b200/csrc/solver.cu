@@ -865,10 +865,12 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     c.anorm_pending = false;
     c.factor_pending = false;
     const bool woodbury = !dense_only && !c.force_dense && (!lr_direct || c.nrhs > 1);
-    if (woodbury) wb_anorm_async(c, Ad);  // overlaps the compression
     // the level-0 factorization does not depend on the compressed bases: it
-    // runs on the side stream while the main stream compresses the couplings
-    if (woodbury && !early_off && c.allow_early && c.anorm_pending) wb_factor_async(c, Ad);
+    // runs on the side stream (after the block norms of the rcond screen)
+    // while the main stream compresses the couplings; otherwise the norms alone
+    // overlap the compression
+    if (woodbury && !early_off && c.allow_early && lr_eligible_pub(c)) wb_factor_async(c, Ad);
+    else if (woodbury) wb_anorm_async(c, Ad);
     if (!dense_only && !c.force_dense && lr_compress(c, Au, Al)) {
         const bool direct = lr_direct && c.nrhs == 1;  // several right-hand sides: the Woodbury form
         c.bcr_path = direct ? 2 : 1;
