@@ -1488,7 +1488,9 @@ void wb_level0_async(Ctx& c) {
         fd[q] = c.dinv.p + size_t(q) * dsz;
         wb[q] = c.lr_W0.p + size_t(q) * nb * wc;
     }
+    nvtxRangePushA("bcr_level0");  // the level-0 batch: factorization (wb_factor_async) and this solve
     lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, f, c.ws2);
+    nvtxRangePop();
     c.bcr_flag_h.ensure(npos);
     QPS_D2H(c.bcr_flag_h.p, c.l0_flag.p, sizeof(int) * npos, f);
     c.rc_flag.ensure(npos);
