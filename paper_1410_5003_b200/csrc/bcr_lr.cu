@@ -64,6 +64,10 @@ int lr_basis() {
     return b;
 }
 constexpr double kLrTol = 1e-14; // relative pivot threshold of the sample's CPQR
+// row ID: relative pivot threshold of the sample's LU.  The couplings' singular
+// values level off at the fill's rounding (~6e-16 of the largest) and the LU
+// pivots of that noise at ~1e-14; the a-posteriori probe tolerance is 1e-12
+constexpr double kIdTol = 1e-12;
 
 // P_b = first r columns of Q (Q^* = H_{r-1} ... H_0 as applied by the CPQR, so
 // Q e_c = H_0^* ... H_c^* e_c), and PH_b = P_b^*.  One warp per column.
@@ -658,6 +662,229 @@ __global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict_
     if (tid == 0 && !(1.0 / (cnorm * inorm) > kRcondMin)) flag[blockIdx.x] = 1;
 }
 
+// ---------------------------------------------------------------------------
+// Interpolative compression of the couplings (randomized row ID).
+//
+// From the sample Y = C Omega (m x 64) an LU with partial pivoting selects 64
+// pivot rows; the first r of them are the skeleton rows I, and
+//   C ~= L (L1^{-1} C[I, :]),   L = the first r columns of the unit lower
+// factor (original row order, |L| <= 1), L1 = L[I, :] (unit lower triangular).
+// The row relations that reproduce Y from Y[I, :] reproduce C from C[I, :]
+// (Y's rows are C's rows times Omega): the residual on Y is the Schur
+// complement after r steps, and the a-posteriori probe tests C itself.  The
+// right factor needs only the r gathered rows of C -- no projection GEMM over
+// the couplings (the orthonormal form P (P^* C) read all of C a second time).
+//
+// lr_id_kernel: one CTA per coupling, one thread per row of Y (m <= 640),
+// 16-column panels in registers.  Rows are never interchanged: each thread
+// remembers the step at which its row became a pivot, a pivot search runs over
+// the rows not yet chosen, and the trailing columns of the rows still live are
+// updated in place in Y through U12 = L11^{-1} Y[pivots, later columns].
+// ---------------------------------------------------------------------------
+constexpr int kIdW = 8;                        // panel width
+constexpr int kIdThreads = 640;                // one thread per sample row
+constexpr int kIdWarps = kIdThreads / 32;
+constexpr int kIdPanels = kLrSample / kIdW;
+static_assert(kLrSample % kIdW == 0, "lr_id_kernel: sample width is a multiple of the panel");
+size_t id_smem_bytes(int r) {
+    return (size_t(2) * kIdWarps * kIdW + size_t(kIdW) * kLrSample + size_t(kIdW) * kIdW + size_t(r) * (r + 1)) *
+           sizeof(cplx);
+}
+
+__global__ void __launch_bounds__(kIdThreads, 1)
+    lr_id_kernel(int m, cplx* __restrict__ Y, size_t ys, int r, cplx* __restrict__ Lo, size_t lstride,
+                 cplx* __restrict__ L1i, int* __restrict__ piv_out, int* __restrict__ rank_out, double tol) {
+    extern __shared__ cplx id_sm[];
+    cplx* cand = id_sm;                       // [2][kIdWarps][kIdW] candidate pivot rows (panel columns)
+    cplx* U12 = cand + 2 * kIdWarps * kIdW;   // [kIdW][kLrSample]
+    cplx* L11 = U12 + kIdW * kLrSample;       // [kIdW][kIdW]
+    cplx* L1 = L11 + kIdW * kIdW;             // [r][r + 1]
+    __shared__ double cval[2][kIdWarps];
+    __shared__ int cidx[2][kIdWarps];
+    __shared__ double udiag[kLrSample];
+    __shared__ int spiv[kLrSample];
+    const int q = blockIdx.x;
+    cplx* Yq = Y + size_t(q) * ys;
+    cplx* Lq = Lo + size_t(q) * lstride;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool own = tid < m;
+    int mystep = own ? (1 << 30) : -1;  // step at which this row became a pivot
+    for (int p = 0; p < kIdPanels; ++p) {
+        const int c0 = p * kIdW;
+        cplx s[kIdW];
+#pragma unroll
+        for (int jj = 0; jj < kIdW; ++jj) s[jj] = own ? Yq[size_t(c0 + jj) * m + tid] : cplx{0, 0};
+#pragma unroll
+        for (int kk = 0; kk < kIdW; ++kk) {
+            const int k = c0 + kk, par = kk & 1;
+            const bool live = mystep > k;
+            double v = live ? cabs2(s[kk]) : -1.0;
+            int idx = live ? tid : (1 << 30);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                if (ov > v || (ov == v && oi < idx)) {
+                    v = ov;
+                    idx = oi;
+                }
+            }
+            if (idx == tid) {  // this warp's candidate publishes its panel row
+                cplx* cr = cand + (par * kIdWarps + warp) * kIdW;
+#pragma unroll
+                for (int jj = kk; jj < kIdW; ++jj) cr[jj] = s[jj];
+                cval[par][warp] = v;
+                cidx[par][warp] = idx;
+            } else if (lane == 0 && idx == (1 << 30)) {
+                cval[par][warp] = -1.0;
+                cidx[par][warp] = 1 << 30;
+            }
+            __syncthreads();
+            double bv = lane < kIdWarps ? cval[par][lane] : -1.0;
+            int bi = lane < kIdWarps ? cidx[par][lane] : (1 << 30);
+            int bw = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int ow = __shfl_xor_sync(0xffffffffu, bw, o);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                    bv = ov;
+                    bi = oi;
+                    bw = ow;
+                }
+            }
+            const cplx* prow = cand + (par * kIdWarps + bw) * kIdW;
+            if (tid == 0) {
+                spiv[k] = bi;
+                udiag[k] = bv > 0.0 ? sqrt(bv) : 0.0;
+            }
+            if (tid == bi) mystep = k;
+            if (live && tid != bi) {
+                const cplx d = prow[kk];
+                const bool zero = (d.re == 0.0 && d.im == 0.0);
+                const cplx l = zero ? cplx{0, 0} : cmul(s[kk], fast_cinv(d));
+                s[kk] = l;
+#pragma unroll
+                for (int jj = kk + 1; jj < kIdW; ++jj) {
+                    const cplx u = prow[jj];
+                    s[jj].re -= l.re * u.re - l.im * u.im;
+                    s[jj].im -= l.re * u.im + l.im * u.re;
+                }
+            }
+        }
+        // left factor columns c0.. (< r): L values of live rows, the unit of
+        // each pivot row at its own step, zero after it
+        if (own) {
+#pragma unroll
+            for (int kk = 0; kk < kIdW; ++kk) {
+                const int k = c0 + kk;
+                if (k < r) {
+                    const cplx v = mystep == k ? cplx{1, 0} : (mystep < k ? cplx{0, 0} : s[kk]);
+                    Lq[size_t(k) * m + tid] = v;
+                }
+            }
+        }
+        if (p + 1 == kIdPanels) break;
+        // L11 of this panel: row kk0 of the pivot chosen at step c0 + kk0
+        const int kk0 = mystep - c0;
+        if (own && kk0 >= 0 && kk0 < kIdW) {
+#pragma unroll
+            for (int kk = 0; kk < kIdW; ++kk)
+                L11[kk0 * kIdW + kk] = kk < kk0 ? s[kk] : (kk == kk0 ? cplx{1, 0} : cplx{0, 0});
+        }
+        __syncthreads();
+        // U12 = L11^{-1} Y[pivots of this panel, later columns] (one thread per column)
+        const int ncol = kLrSample - c0 - kIdW;
+        if (tid < ncol) {
+            const size_t col = size_t(c0 + kIdW + tid) * m;
+#pragma unroll 1
+            for (int kk = 0; kk < kIdW; ++kk) {
+                cplx a = Yq[col + spiv[c0 + kk]];
+                for (int k2 = 0; k2 < kk; ++k2) {
+                    const cplx lv = L11[kk * kIdW + k2], u = U12[k2 * kLrSample + tid];
+                    a.re -= lv.re * u.re - lv.im * u.im;
+                    a.im -= lv.re * u.im + lv.im * u.re;
+                }
+                U12[kk * kLrSample + tid] = a;
+            }
+        }
+        __syncthreads();
+        // trailing columns of the rows still live: Y[i, j] -= sum_kk L[i, kk] U12[kk, j]
+        if (own && mystep >= c0 + kIdW) {
+#pragma unroll 2
+            for (int t = 0; t < ncol; ++t) {
+                const size_t at = size_t(c0 + kIdW + t) * m + tid;
+                cplx a = Yq[at];
+#pragma unroll
+                for (int kk = 0; kk < kIdW; ++kk) {
+                    const cplx u = U12[kk * kLrSample + t];
+                    a.re -= s[kk].re * u.re - s[kk].im * u.im;
+                    a.im -= s[kk].re * u.im + s[kk].im * u.re;
+                }
+                Yq[at] = a;
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();  // the left factor's global writes are visible to the block
+    // numerical rank: last pivot above tol x the largest
+    if (tid == 0) {
+        double mx = 0.0;
+        for (int k = 0; k < kLrSample; ++k) mx = fmax(mx, udiag[k]);
+        int rk = 0;
+        for (int k = 0; k < kLrSample; ++k)
+            if (udiag[k] > tol * mx) rk = k + 1;
+        rank_out[q] = rk;
+    }
+    if (tid < r) piv_out[size_t(q) * r + tid] = spiv[tid];
+    // L1 = L[I, :r] (unit lower), then its inverse column by column (one warp per column)
+    for (int e = tid; e < r * r; e += kIdThreads) {
+        const int t = e % r, t2 = e / r;
+        L1[t * (r + 1) + t2] = Lq[size_t(t2) * m + spiv[t]];
+    }
+    __syncthreads();
+    cplx* Li = L1i + size_t(q) * r * r;
+    for (int c = warp; c < r; c += kIdWarps) {
+        cplx x0 = lane == c ? cplx{1, 0} : cplx{0, 0};
+        cplx x1 = lane + 32 == c ? cplx{1, 0} : cplx{0, 0};
+        for (int tp = c; tp + 1 < r; ++tp) {
+            const cplx src = tp < 32 ? x0 : x1;
+            cplx xt;
+            xt.re = __shfl_sync(0xffffffffu, src.re, tp & 31);
+            xt.im = __shfl_sync(0xffffffffu, src.im, tp & 31);
+            if (lane > tp && lane < r) {
+                const cplx lv = L1[lane * (r + 1) + tp];
+                x0.re -= lv.re * xt.re - lv.im * xt.im;
+                x0.im -= lv.re * xt.im + lv.im * xt.re;
+            }
+            if (lane + 32 > tp && lane + 32 < r) {
+                const cplx lv = L1[(lane + 32) * (r + 1) + tp];
+                x1.re -= lv.re * xt.re - lv.im * xt.im;
+                x1.im -= lv.re * xt.im + lv.im * xt.re;
+            }
+        }
+        if (lane < r) Li[size_t(c) * r + lane] = x0;
+        if (lane + 32 < r) Li[size_t(c) * r + lane + 32] = x1;
+    }
+}
+
+// rows[q][0..nr) of src_q (ld lds_q) over ncols columns -> dst_q (nr x ncols, ld nr)
+__global__ void __launch_bounds__(256) gather_rows_kernel(const cplx* const* __restrict__ src,
+                                                          const int* __restrict__ lds, const int* __restrict__ rows,
+                                                          int nr, int ncols, cplx* __restrict__ dst, size_t dstride) {
+    const int q = blockIdx.y;
+    const cplx* a = src[q];
+    const size_t ld = size_t(lds[q]);
+    const int* rw = rows + size_t(q) * nr;
+    cplx* d = dst + size_t(q) * dstride;
+    const int total = nr * ncols;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int t = e % nr, j = e / nr;
+        d[e] = a[size_t(j) * ld + rw[t]];
+    }
+}
+
 GemmTask gemm1(const cplx* A, int lda, const cplx* B, int ldb, int K, cplx* C, int ldc) {
     GemmTask t{};
     t.nseg = 1;
@@ -743,6 +970,38 @@ void lr_sample_async(Ctx& c) {
     c.lr_sample_pending = true;
 }
 
+// Accept the compression once the sample ranks and probe norms are on the host
+// (ev_sample): false sends the system to the dense reduction.
+static bool lr_accept(Ctx& c, int nc) {
+    QPS_CUDA(cudaEventSynchronize(c.ev_sample));
+    int mx = 0;
+    for (int q = 0; q < nc; ++q) mx = std::max(mx, c.lr_rank_h[q]);
+    c.lr_rank_max = std::max(c.lr_rank_max, mx);
+    if (getenv("QPS_LR_TRACE")) {
+        int mn = 1 << 30;
+        double mean = 0;
+        for (int q = 0; q < nc; ++q) { mn = std::min(mn, c.lr_rank_h[q]); mean += c.lr_rank_h[q]; }
+        fprintf(stderr, "low-rank couplings: %d blocks, rank min %d mean %.1f max %d (sample %d)\n", nc, mn,
+                mean / nc, mx, kLrSample);
+    }
+    if (mx > kLrMaxRank) return false;  // not low rank: the dense reduction (A untouched so far)
+    static const double probe_tol = [] {  // QPS_LR_PROBE_TOL: tests force the fallback with a tiny value
+        const char* e = getenv("QPS_LR_PROBE_TOL");
+        return e ? atof(e) : kLrProbeTol;
+    }();
+    double worst = 0;
+    for (int q = 0; q < nc; ++q) {
+        const double rel = c.lr_pn_h[q] / std::max(c.lr_pn_h[nc + q], 1e-300);
+        worst = std::isfinite(rel) ? std::max(worst, rel) : INFINITY;
+    }
+    c.lr_probe_worst = worst;
+    if (getenv("QPS_LR_TRACE"))
+        fprintf(stderr, "low-rank couplings: probe max ||(I - P P^*) C w2|| / ||C w2|| = %.3e (tol %.1e)\n",
+                worst, probe_tol);
+    if (!(worst <= probe_tol)) return false;  // basis misses part of a coupling's range: dense reduction
+    return true;
+}
+
 // Compress every coupling of every system: c.lr_P / c.lr_R (per coupling,
 // n x r ld nb and r x n ld r), ordered [system][sub 0..I-2][super 0..I-2].
 bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
@@ -826,6 +1085,140 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         }
     }
     tmark("sample correction Y += Bc (-X Omega)");
+    static const bool id_off = [] {  // QPS_LR_ID=0: the orthonormal basis P (P^* C) instead (A/B)
+        const char* e = getenv("QPS_LR_ID");
+        return e && !strcmp(e, "0");
+    }();
+    if (!id_off && nb <= kIdThreads && lr_basis() <= kLrSample) {
+        const int r = lr_basis();
+        c.lr_r = r;
+        c.lr_P.ensure(size_t(nc) * nb * r);
+        c.lr_L1i.ensure(size_t(nc) * r * r);
+        c.lr_piv.ensure(size_t(nc) * r);
+        c.lr_rank_d.ensure(nc);
+        {
+            ProfScope ps("lr_id", s, 0.0);
+            const size_t sm = id_smem_bytes(r);
+            static size_t attr = 0;
+            if (sm > attr) {
+                QPS_CUDA(cudaFuncSetAttribute(lr_id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                attr = sm;
+            }
+            { QPS_NOTE_LAUNCH(); lr_id_kernel<<<nc, kIdThreads, sm, s>>>(nb, c.lr_Y.p, size_t(nb) * kLrCols, r, c.lr_P.p,
+                                                                         size_t(nb) * r, c.lr_L1i.p, c.lr_piv.p,
+                                                                         c.lr_rank_d.p, kIdTol); }
+            QPS_CUDA(cudaGetLastError());
+        }
+        c.lr_rank_h.ensure(nc);
+        QPS_D2H(c.lr_rank_h.p, c.lr_rank_d.p, sizeof(int) * nc, s);
+        tmark("row ID of the samples");
+        wb_level0_async(c);  // the left factors exist: level 0 on the factor stream from here
+        // R = L1^{-1} C[I, :]   (C[I, :] = A[I, :] - Bc[I, :] X when deferred)
+        c.lr_G.ensure(size_t(nc) * r * nb);
+        c.lr_R.ensure(size_t(nc) * r * nb);
+        std::vector<const cplx*> src(nc);
+        std::vector<int> lds(nc, nb);
+        for (int q = 0; q < nc; ++q) src[q] = coupling(q);
+        auto gather_rows = [&](const std::vector<const cplx*>& sp, const std::vector<int>& ld, int ncols, cplx* dst,
+                               size_t dstride) {
+            c.lr_gptr.upload(sp, s);
+            c.lr_gld.upload(ld, s);
+            ProfScope ps("copy", s, 0.0, 32.0 * nc * double(r) * ncols);
+            const int per = r * ncols;
+            const dim3 grid(std::min(64, (per + 255) / 256), nc);
+            { QPS_NOTE_LAUNCH(); gather_rows_kernel<<<grid, 256, 0, s>>>(c.lr_gptr.p, c.lr_gld.p, c.lr_piv.p, r, ncols,
+                                                                          dst, dstride); }
+            QPS_CUDA(cudaGetLastError());
+        };
+        gather_rows(src, lds, nb, c.lr_G.p, size_t(r) * nb);
+        if (corr) {
+            c.lr_W.ensure(size_t(nc) * r * P);
+            std::vector<const cplx*> bs(nc);
+            std::vector<int> bl(nc);
+            for (int q = 0; q < nc; ++q) {
+                bs[q] = corr_task(q).A[0];
+                bl[q] = corr_task(q).lda[0];
+            }
+            gather_rows(bs, bl, P, c.lr_W.p, size_t(r) * P);
+            std::vector<GemmTask> t(nc);
+            for (int q = 0; q < nc; ++q)
+                t[q] = gemm1(c.lr_W.p + size_t(q) * r * P, r, corr_task(q).B[0], corr_task(q).ldb[0], P,
+                             c.lr_G.p + size_t(q) * r * nb, r);
+            zgemm_batched(r, nb, cplx{-1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        }
+        {
+            std::vector<GemmTask> t(nc);
+            for (int q = 0; q < nc; ++q)
+                t[q] = gemm1(c.lr_L1i.p + size_t(q) * r * r, r, c.lr_G.p + size_t(q) * r * nb, r, r,
+                             c.lr_R.p + size_t(q) * r * nb, r);
+            zgemm_batched(r, nb, cplx{1, 0}, cplx{0, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        }
+        tmark("R = L1^{-1} C[I, :]");
+        // a-posteriori probe: ||C[:, J] - L R[:, J]||_F against ||C[:, J]||_F
+        static const bool no_probe_id = [] {
+            const char* e = getenv("QPS_LR_PROBE");
+            return e && !strcmp(e, "0");
+        }();
+        c.lr_pn_h.ensure(size_t(nc) * 2);
+        if (no_probe_id) {
+            for (int q = 0; q < 2 * nc; ++q) c.lr_pn_h[q] = 0.0;
+        } else {
+            if (c.lr_probe_n != nc * 65536 + nb) {
+                std::vector<int> cols(size_t(nc) * kLrProbe);
+                uint64_t x = 0xd1b54a32d192ed03ull;
+                for (auto& v : cols) {
+                    x ^= x >> 12;
+                    x ^= x << 25;
+                    x ^= x >> 27;
+                    v = int(((x * 0x2545f4914f6cdd1dull) >> 33) % uint64_t(nb));
+                }
+                c.lr_probe_cols.upload(cols, s);
+                c.lr_probe_n = nc * 65536 + nb;
+            }
+            std::vector<const cplx*> xp(nc), rp(nc);
+            std::vector<int> xld(nc, P), rld(nc, r);
+            for (int q = 0; q < nc; ++q) {
+                rp[q] = c.lr_R.p + size_t(q) * r * nb;
+                if (corr) {
+                    xp[q] = corr_task(q).B[0];
+                    xld[q] = corr_task(q).ldb[0];
+                }
+            }
+            c.lr_Y2.ensure(size_t(nc) * nb * kLrProbe);
+            c.lr_G2.ensure(size_t(nc) * (r + P) * kLrProbe);
+            cplx* Rg = c.lr_G2.p;                               // r x 16 per coupling
+            cplx* Xg = c.lr_G2.p + size_t(nc) * r * kLrProbe;  // P x 16 per coupling
+            gather_columns(src, lds, nb, c.lr_probe_cols.p, kLrProbe, c.lr_Y2.p, nb, size_t(nb) * kLrProbe, c.lr_gptr,
+                           c.lr_gld, s);
+            if (corr) {
+                gather_columns(xp, xld, P, c.lr_probe_cols.p, kLrProbe, Xg, P, size_t(P) * kLrProbe, c.lr_gptr,
+                               c.lr_gld, s);
+                std::vector<GemmTask> t(nc);
+                for (int q = 0; q < nc; ++q)
+                    t[q] = gemm1(corr_task(q).A[0], corr_task(q).lda[0], Xg + size_t(q) * P * kLrProbe, P, P,
+                                 c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
+                zgemm_batched(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+            }
+            gather_columns(rp, rld, r, c.lr_probe_cols.p, kLrProbe, Rg, r, size_t(r) * kLrProbe, c.lr_gptr, c.lr_gld,
+                           s);
+            std::vector<GemmTask> e(nc);
+            for (int q = 0; q < nc; ++q)
+                e[q] = gemm1(c.lr_P.p + size_t(q) * nb * r, nb, Rg + size_t(q) * r * kLrProbe, r, r,
+                             c.lr_Y2.p + size_t(q) * nb * kLrProbe, nb);
+            c.lr_pn.ensure(size_t(nc) * 2);
+            batched_fro(c.lr_Y2.p, nb, kLrProbe, nb, size_t(nb) * kLrProbe, nc, c.lr_pn.p + nc, s);
+            zgemm_residual_norms(nb, kLrProbe, cplx{-1, 0}, cplx{1, 0}, e, s, c.ws.gemm_tasks, c.lr_parts, c.lr_pn.p);
+            QPS_D2H(c.lr_pn_h.p, c.lr_pn.p, sizeof(double) * 2 * nc, s);
+        }
+        QPS_CUDA(cudaEventRecord(c.ev_sample, s));
+        tmark("probe");
+        if (trace) {
+            QPS_CUDA(cudaEventDestroy(te0));
+            QPS_CUDA(cudaEventDestroy(te1));
+        }
+        tl_mark(c, "compress", s);
+        return lr_accept(c, nc);
+    }
     static const bool cpqr_only = [] {
         const char* e = getenv("QPS_LR_QR");
         return e && !strcmp(e, "cpqr");
@@ -1098,34 +1491,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         QPS_CUDA(cudaEventDestroy(te1));
     }
     tl_mark(c, "compress", s);
-    if (rank_deferred) {
-        QPS_CUDA(cudaEventSynchronize(c.ev_sample));
-        int mx = 0;
-        for (int q = 0; q < nc; ++q) mx = std::max(mx, c.lr_rank_h[q]);
-        c.lr_rank_max = std::max(c.lr_rank_max, mx);
-        if (getenv("QPS_LR_TRACE")) {
-            int mn = 1 << 30;
-            double mean = 0;
-            for (int q = 0; q < nc; ++q) { mn = std::min(mn, c.lr_rank_h[q]); mean += c.lr_rank_h[q]; }
-            fprintf(stderr, "low-rank couplings: %d blocks, rank min %d mean %.1f max %d (sample %d)\n", nc, mn,
-                    mean / nc, mx, kLrSample);
-        }
-        if (mx > kLrMaxRank) return false;  // not low rank: the dense reduction (A untouched so far)
-        static const double probe_tol = [] {  // QPS_LR_PROBE_TOL: tests force the fallback with a tiny value
-            const char* e = getenv("QPS_LR_PROBE_TOL");
-            return e ? atof(e) : kLrProbeTol;
-        }();
-        double worst = 0;
-        for (int q = 0; q < nc; ++q) {
-            const double rel = c.lr_pn_h[q] / std::max(c.lr_pn_h[nc + q], 1e-300);
-            worst = std::isfinite(rel) ? std::max(worst, rel) : INFINITY;
-        }
-        c.lr_probe_worst = worst;
-        if (getenv("QPS_LR_TRACE"))
-            fprintf(stderr, "low-rank couplings: probe max ||(I - P P^*) C w2|| / ||C w2|| = %.3e (tol %.1e)\n",
-                    worst, probe_tol);
-        if (!(worst <= probe_tol)) return false;  // basis misses part of a coupling's range: dense reduction
-    }
+    if (rank_deferred) return lr_accept(c, nc);
     return true;
 }
 
