@@ -1826,6 +1826,34 @@ void wb_stage_rhs(Ctx& c, cudaStream_t s) {
                                  cudaMemcpyDeviceToDevice, s));
 }
 
+// QPS_L0_CHUNKS (1..4, default 1): chunks of the early level-0 batch.  Measured
+// at config 4: no gain (the GPU is busy throughout that window), kept for A/B
+int l0_chunk_count(int npos) {
+    static const int n = [] {
+        const char* e = getenv("QPS_L0_CHUNKS");
+        return e ? std::max(1, std::min(Ctx::kL0MaxChunks, atoi(e))) : 1;
+    }();
+    return npos >= 64 * n ? n : 1;
+}
+int l0_chunk_begin(int npos, int nch, int k) { return int((int64_t(npos) * k) / nch); }
+void l0_streams(Ctx& c) {
+    if (c.l0_s[0]) return;
+    // below the main stream by default: the main stream's compression (whose
+    // bases every chunk's solve needs) must not be starved by the factorization
+    int lo = 0, hi = 0;
+    QPS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const int main_prio = hi < lo ? hi + 1 : hi;
+    const char* e = getenv("QPS_L0_PRIO");  // hi | main | below (default) | lo
+    int prio = std::min(lo, main_prio + 1);
+    if (e && !strcmp(e, "hi")) prio = hi;
+    else if (e && !strcmp(e, "main")) prio = main_prio;
+    else if (e && !strcmp(e, "lo")) prio = lo;
+    for (int k = 0; k < Ctx::kL0MaxChunks; ++k) {
+        QPS_CUDA(cudaStreamCreateWithPriority(&c.l0_s[k], cudaStreamNonBlocking, prio));
+        QPS_CUDA(cudaEventCreateWithFlags(&c.l0_ev[k], cudaEventDisableTiming));
+    }
+}
+
 // Level 0 of the Woodbury reduction on the factor stream as soon as the
 // compressed bases exist: W_j = D_j^{-1} [P_L P_U f_j probes] with the factors
 // of wb_factor_async, the rcond screen, y = D^{-1} f into F -- overlapping the
@@ -1838,13 +1866,19 @@ void wb_level0_async(Ctx& c) {
     const size_t nb2 = D.nb2(), dsz = lu_dinv_elems(nb), fs = size_t(nb) * m, per = size_t(nb) * r;
     const int wc = r2 + m + kRcProbe;
     cudaStream_t f = c.factor_stream;
-    QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // the bases P are queued
-    QPS_CUDA(cudaStreamWaitEvent(f, c.ev_fork, 0));
-    if (m == 1) wb_stage_rhs(c, f);
-    rc_probes(c, nb, f);
+    // the right-hand sides [P_L P_U f probes] are staged on the main stream
+    // (where the bases were just produced): with a chunked factorization each
+    // chunk's solve then waits only for its own factors
+    cudaStream_t st = c.l0_chunks > 1 ? c.stream : f;
+    if (st != c.stream) {
+        QPS_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // the bases P are queued
+        QPS_CUDA(cudaStreamWaitEvent(f, c.ev_fork, 0));
+    }
+    if (m == 1) wb_stage_rhs(c, st);
+    rc_probes(c, nb, st);
     c.lr_W0.ensure(size_t(npos) * nb * wc);
-    { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, f>>>(I, nb, per, c.lr_P.p, c.F.p, m,
-                                                                            c.rc_probe.p, kRcProbe, c.lr_W0.p); }
+    { QPS_NOTE_LAUNCH(); stage_bases_kernel<<<dim3(npos, 16), 256, 0, st>>>(I, nb, per, c.lr_P.p, c.F.p, m,
+                                                                             c.rc_probe.p, kRcProbe, c.lr_W0.p); }
     QPS_CUDA(cudaGetLastError());
     std::vector<cplx*> fa(npos), fd(npos), wb(npos);
     std::vector<int*> fp(npos);
@@ -1855,7 +1889,21 @@ void wb_level0_async(Ctx& c) {
         wb[q] = c.lr_W0.p + size_t(q) * nb * wc;
     }
     nvtxRangePushA("bcr_level0");  // the level-0 batch: factorization (wb_factor_async) and this solve
-    lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, f, c.ws2);
+    if (c.l0_chunks == 1) {
+        lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, f, c.ws2);
+    } else {
+        QPS_CUDA(cudaEventRecord(c.ev_fork, st));  // staged
+        for (int k = 0; k < c.l0_chunks; ++k) {
+            const int b0 = l0_chunk_begin(npos, c.l0_chunks, k), b1 = l0_chunk_begin(npos, c.l0_chunks, k + 1);
+            QPS_CUDA(cudaStreamWaitEvent(c.l0_s[k], c.ev_fork, 0));
+            const std::vector<cplx*> ca(fa.begin() + b0, fa.begin() + b1), cd(fd.begin() + b0, fd.begin() + b1),
+                cw(wb.begin() + b0, wb.begin() + b1);
+            const std::vector<int*> cp(fp.begin() + b0, fp.begin() + b1);
+            lu_solve_batched(nb, nb, ca, cp, cd, cw, nb, wc, c.l0_s[k], c.l0_ws[k]);
+            QPS_CUDA(cudaEventRecord(c.l0_ev[k], c.l0_s[k]));
+            QPS_CUDA(cudaStreamWaitEvent(f, c.l0_ev[k], 0));
+        }
+    }
     nvtxRangePop();
     c.bcr_flag_h.ensure(npos);
     QPS_D2H(c.bcr_flag_h.p, c.l0_flag.p, sizeof(int) * npos, f);
@@ -1919,7 +1967,22 @@ void wb_factor_async(Ctx& c, cplx* Ad) {
     }
     QPS_CUDA(cudaEventRecord(c.ev_f0, fs));
     nvtxRangePushA("bcr_level0");
-    lu_factor_batched(nb, nb, fa, fp, fd, c.l0_flag.p, fs, c.ws2);
+    c.l0_chunks = l0_chunk_count(npos);
+    if (c.l0_chunks == 1) {
+        lu_factor_batched(nb, nb, fa, fp, fd, c.l0_flag.p, fs, c.ws2);
+    } else {
+        l0_streams(c);
+        QPS_CUDA(cudaEventRecord(c.ev_fork, fs));  // the norms have read Ad
+        for (int k = 0; k < c.l0_chunks; ++k) {
+            const int b0 = l0_chunk_begin(npos, c.l0_chunks, k), b1 = l0_chunk_begin(npos, c.l0_chunks, k + 1);
+            QPS_CUDA(cudaStreamWaitEvent(c.l0_s[k], c.ev_fork, 0));
+            const std::vector<cplx*> ca(fa.begin() + b0, fa.begin() + b1), cd(fd.begin() + b0, fd.begin() + b1);
+            const std::vector<int*> cp(fp.begin() + b0, fp.begin() + b1);
+            lu_factor_batched(nb, nb, ca, cp, cd, c.l0_flag.p + b0, c.l0_s[k], c.l0_ws[k]);
+            QPS_CUDA(cudaEventRecord(c.l0_ev[k], c.l0_s[k]));
+            QPS_CUDA(cudaStreamWaitEvent(fs, c.l0_ev[k], 0));  // fs joins every chunk (fallback paths wait on fs)
+        }
+    }
     nvtxRangePop();
     QPS_CUDA(cudaEventRecord(c.ev_f1, fs));
     tl_mark(c, "factor(side)", fs);

@@ -160,7 +160,16 @@ void qps_destroy(qps_ctx* h) {
     for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_factor, h->c.ev_l0, h->c.ev_f0,
                           h->c.ev_f1, h->c.ev_geo})
         if (e) cudaEventDestroy(e);
+    std::vector<cudaStream_t> l0s;
+    for (int i = 0; i < qpsb::Ctx::kL0MaxChunks; ++i) {
+        if (h->c.l0_s[i]) {
+            cudaStreamSynchronize(h->c.l0_s[i]);
+            l0s.push_back(h->c.l0_s[i]);
+        }
+        if (h->c.l0_ev[i]) cudaEventDestroy(h->c.l0_ev[i]);
+    }
     delete h;
+    for (cudaStream_t x : l0s) cudaStreamDestroy(x);
     if (s) cudaStreamDestroy(s);
     if (s2) cudaStreamDestroy(s2);
     if (s3) cudaStreamDestroy(s3);

@@ -264,6 +264,14 @@ struct Ctx {
     uint64_t ref_evals = 0, performed_evals = 0;
     Workspace ws;
     Workspace ws2;                     // task tables of the early level-0 factorization (stream side)
+    // the early level-0 batch split into chunks on their own streams, so the
+    // latency-bound panels of one chunk overlap the GEMMs of another and a
+    // chunk's solve starts as soon as its own factors exist
+    static constexpr int kL0MaxChunks = 4;
+    cudaStream_t l0_s[kL0MaxChunks] = {};
+    cudaEvent_t l0_ev[kL0MaxChunks] = {};
+    Workspace l0_ws[kL0MaxChunks];
+    int l0_chunks = 1;
     std::chrono::steady_clock::time_point host_t0;  // QPS_HOST_TRACE
     DBuf<PairTask> d_pair;
     DBuf<ProxyTask> d_proxy;

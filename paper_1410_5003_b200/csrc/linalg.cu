@@ -1207,7 +1207,8 @@ __global__ void __launch_bounds__(256) lu_panel_kernel(int n, int ld, cplx* cons
 // row-by-row recurrences need only warp-level synchronisation.  Output per
 // block: [L^{-1} | U^{-1}] as two bs x bs column-major tiles (ld bs).
 __global__ void __launch_bounds__(512) tri_inv_kernel(int n, int ld, cplx* const* __restrict__ Ap,
-                                                      cplx* const* __restrict__ Op, int bs, int k0_first, int mode) {
+                                                      cplx* const* __restrict__ Op, int bs, int k0_first, int mode,
+                                                      int tile0) {
     // Blocked in 16 x 16 tiles: the diagonal tiles are inverted concurrently
     // (64 threads each, a 16-step recurrence), then each block row of the
     // inverse is two small tile products, X_ij = -X_ii sum_k T_ik X_kj, so the
@@ -1224,7 +1225,7 @@ __global__ void __launch_bounds__(512) tri_inv_kernel(int n, int ld, cplx* const
     cplx* Y = T + 3 * bs * lp + half * 768;                  // 3 scratch 16 x 16 tiles (ld 16)
     cplx* Dinv = T + 3 * bs * lp + 2 * 768;                  // bs reciprocals of the diagonal
     const cplx* A = Ap[blockIdx.y];
-    cplx* O = Op[blockIdx.y] + size_t(blockIdx.x) * 2 * bs * bs + (which == 2 ? size_t(bs) * bs : 0);
+    cplx* O = Op[blockIdx.y] + size_t(tile0 + blockIdx.x) * 2 * bs * bs + (which == 2 ? size_t(bs) * bs : 0);
     const int k0 = k0_first + blockIdx.x * bs;
     const int sz = min(bs, n - k0);
     // rows/columns past the matrix end act as identity
@@ -1707,6 +1708,202 @@ __global__ void __launch_bounds__(kRegPanelMaxRows, 1)
         int* mp = rl_map + size_t(blockIdx.x) * kRlMap;
         for (int q = 0; q < 32; ++q) mp[q] = perm[q];
         for (int q = kRlW; q < 32; ++q) mp[32 + q - kRlW] = rowof[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Wide LU panel: one CTA factors a whole (n - c0) x w column panel (w <= 64)
+// of one matrix -- the bottom of the recursion in one launch instead of four
+// 16-column panels, their interchanges, tile inverses and K <= 32 updates.
+// One thread per row (n - c0 <= 640); 8-column sub-panels in registers.
+// Rows stay in place while the panel is factored: each thread remembers the
+// step at which its row became a pivot and the pivot search runs over the
+// rows not chosen yet; after each sub-panel the later columns of the panel
+// are updated in place through U12 = L11^{-1} A[pivot rows, later columns].
+// At the end the LAPACK interchange sequence is replayed on row indices
+// (ipiv, 0-based absolute rows as lu_panel_sm2 writes them) and the panel's
+// rows are moved to their final positions, so the factors leave exactly as a
+// sequential partial-pivoting LU would lay them out.
+// ---------------------------------------------------------------------------
+constexpr int kWpMax = 64;                     // widest panel
+constexpr int kWpSub = 8;                      // sub-panel (register) width
+constexpr int kWpThreads = 640;                // one thread per row
+constexpr int kWpWarps = kWpThreads / 32;
+
+__global__ void __launch_bounds__(kWpThreads, 1)
+    lu_wpanel_kernel(int n, int ld, cplx* const* __restrict__ Ap, int* const* __restrict__ Pp, int c0, int w,
+                     int* __restrict__ singular) {
+    __shared__ cplx cand[2][kWpWarps][kWpSub];
+    __shared__ double cval[2][kWpWarps];
+    __shared__ int cidx[2][kWpWarps];
+    __shared__ cplx L11[kWpSub][kWpSub];
+    __shared__ cplx U12[kWpSub][kWpMax];
+    __shared__ int spv[kWpMax];
+    __shared__ int rowat[kWpThreads], posof[kWpThreads];
+    cplx* A = Ap[blockIdx.x];
+    const int rows = n - c0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const bool own = tid < rows;
+    cplx* arow = A + size_t(c0) * ld + c0 + tid;  // this thread's row, column c0
+    int mystep = own ? (1 << 30) : -1;
+    bool sing = false;
+    for (int p0 = 0; p0 < w; p0 += kWpSub) {
+        const int sw = min(kWpSub, w - p0);
+        cplx s[kWpSub];
+#pragma unroll
+        for (int jj = 0; jj < kWpSub; ++jj) s[jj] = (own && jj < sw) ? arow[size_t(p0 + jj) * ld] : cplx{0, 0};
+#pragma unroll
+        for (int kk = 0; kk < kWpSub; ++kk) {
+            if (kk >= sw) break;
+            const int k = p0 + kk, par = kk & 1;
+            const bool live = mystep > k;
+            double v = live ? cabs2(s[kk]) : -1.0;
+            int idx = live ? tid : (1 << 30);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                if (ov > v || (ov == v && oi < idx)) {
+                    v = ov;
+                    idx = oi;
+                }
+            }
+            if (idx == tid) {
+#pragma unroll
+                for (int jj = kk; jj < kWpSub; ++jj) cand[par][warp][jj] = s[jj];
+                cval[par][warp] = v;
+                cidx[par][warp] = idx;
+            } else if (lane == 0 && idx == (1 << 30)) {
+                cval[par][warp] = -1.0;
+                cidx[par][warp] = 1 << 30;
+            }
+            __syncthreads();
+            double bv = lane < nw ? cval[par][lane] : -1.0;
+            int bi = lane < nw ? cidx[par][lane] : (1 << 30);
+            int bw = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int ow = __shfl_xor_sync(0xffffffffu, bw, o);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                    bv = ov;
+                    bi = oi;
+                    bw = ow;
+                }
+            }
+            const cplx* prow = cand[par][bw];
+            if (tid == 0) spv[k] = bi;
+            if (tid == bi) mystep = k;
+            const cplx d = prow[kk];
+            const bool zero = (d.re == 0.0 && d.im == 0.0);
+            sing |= zero;
+            if (live && tid != bi) {
+                const cplx l = zero ? s[kk] : cmul(s[kk], fast_cinv(d));
+                s[kk] = l;
+#pragma unroll
+                for (int jj = kk + 1; jj < kWpSub; ++jj) {
+                    const cplx u = prow[jj];
+                    s[jj].re -= l.re * u.re - l.im * u.im;
+                    s[jj].im -= l.re * u.im + l.im * u.re;
+                }
+            }
+        }
+        // sub-panel back in place (L of live rows, U / L of its pivot rows)
+        if (own) {
+#pragma unroll
+            for (int jj = 0; jj < kWpSub; ++jj)
+                if (jj < sw) arow[size_t(p0 + jj) * ld] = s[jj];
+        }
+        const int ncol = w - p0 - sw;
+        if (ncol <= 0) break;
+        // L11: row kk0 of the pivot chosen at step p0 + kk0
+        const int kk0 = mystep - p0;
+        if (own && kk0 >= 0 && kk0 < sw) {
+#pragma unroll
+            for (int kk = 0; kk < kWpSub; ++kk) L11[kk0][kk] = kk < kk0 ? s[kk] : cplx{0, 0};
+        }
+        __syncthreads();
+        if (tid < ncol) {  // U12 = L11^{-1} A[pivots, later columns], one thread per column
+            const cplx* col = A + size_t(c0 + p0 + sw + tid) * ld + c0;
+            cplx u[kWpSub];
+#pragma unroll
+            for (int kk = 0; kk < kWpSub; ++kk)  // independent gathers in flight
+                if (kk < sw) u[kk] = col[spv[p0 + kk]];
+#pragma unroll
+            for (int kk = 0; kk < kWpSub; ++kk) {
+#pragma unroll
+                for (int k2 = 0; k2 < kk; ++k2) {
+                    const cplx lv = L11[kk][k2];
+                    u[kk].re -= lv.re * u[k2].re - lv.im * u[k2].im;
+                    u[kk].im -= lv.re * u[k2].im + lv.im * u[k2].re;
+                }
+                if (kk < sw) U12[kk][tid] = u[kk];
+            }
+        }
+        __syncthreads();
+        // later columns of the panel: live rows and this sub-panel's pivot rows
+        // (with their multipliers from before they were chosen)
+        if (own && mystep >= p0) {
+            cplx lv[kWpSub];
+#pragma unroll
+            for (int kk = 0; kk < kWpSub; ++kk)
+                lv[kk] = (kk < sw && p0 + kk < mystep) ? s[kk] : cplx{0, 0};
+            cplx* dst = arow + size_t(p0 + sw) * ld;
+            constexpr int kLd = 4;  // columns' loads in flight, then their updates
+            for (int t0 = 0; t0 < ncol; t0 += kLd) {
+                cplx a[kLd];
+#pragma unroll
+                for (int q = 0; q < kLd; ++q)
+                    if (t0 + q < ncol) a[q] = dst[size_t(t0 + q) * ld];
+#pragma unroll
+                for (int q = 0; q < kLd; ++q) {
+#pragma unroll
+                    for (int kk = 0; kk < kWpSub; ++kk) {
+                        const cplx u = U12[kk][t0 + q];
+                        a[q].re -= lv[kk].re * u.re - lv[kk].im * u.im;
+                        a[q].im -= lv[kk].re * u.im + lv[kk].im * u.re;
+                    }
+                    if (t0 + q < ncol) dst[size_t(t0 + q) * ld] = a[q];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (sing && tid == 0) singular[blockIdx.x] = 1;
+    // replay the interchange sequence on row indices
+    for (int i = tid; i < rows; i += blockDim.x) {
+        rowat[i] = i;
+        posof[i] = i;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int* ipiv = Pp[blockIdx.x];
+        for (int k = 0; k < w; ++k) {
+            const int p = spv[k], loc = posof[p], other = rowat[k];
+            ipiv[c0 + k] = c0 + loc;
+            rowat[k] = p;
+            rowat[loc] = other;
+            posof[p] = k;
+            posof[other] = loc;
+        }
+    }
+    __syncthreads();
+    // move every row of the panel to its final position, 8 columns at a time
+    const int dest = own ? posof[tid] : 0;
+    for (int p0 = 0; p0 < w; p0 += kWpSub) {
+        cplx v[kWpSub];
+#pragma unroll
+        for (int jj = 0; jj < kWpSub; ++jj)
+            if (own && p0 + jj < w) v[jj] = arow[size_t(p0 + jj) * ld];
+        __syncthreads();
+        if (own && dest != tid) {
+            cplx* drow = A + size_t(c0) * ld + c0 + dest;
+#pragma unroll
+            for (int jj = 0; jj < kWpSub; ++jj)
+                if (p0 + jj < w) drow[size_t(p0 + jj) * ld] = v[jj];
+        }
+        __syncthreads();
     }
 }
 
@@ -2283,6 +2480,9 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
     for (const auto& t : tasks)
         for (int q = 0; q < t.nseg; ++q) kmax = std::max(kmax, t.K[q]);
     const char* nm = family ? family : (kmax <= 64) ? (M <= 64 ? "zgemm_k64_m64" : "zgemm_k64") : (M >= 256 && N >= 256 ? "zgemm_big" : "zgemm_mid");
+    static const bool trace_shapes = getenv("QPS_TRACE_GEMM") != nullptr;  // shapes to stderr (profiling aid)
+    if (trace_shapes)
+        fprintf(stderr, "gemm %s M=%d N=%d K=%d nseg=%d tasks=%zu\n", nm, M, N, kmax, tasks[0].nseg, tasks.size());
     ProfScope ps(nm, s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
     if (!four_m) {
         // tile by shape (tools/micro/gemm_cfg.cu on B200): 16 x 64 for thin
@@ -2479,7 +2679,7 @@ size_t lu_dinv_elems(int n) { return size_t(2) * ((n + kTB - 1) / kTB) * kTB * k
 
 namespace {
 void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, int bs, int k0_first, int nblk,
-                    int mode, cudaStream_t s) {
+                    int mode, cudaStream_t s, int tile0 = 0) {
     // bs: a multiple of 16, <= kTB
     // layout: T | X (lower) | X (upper) | Y | Y | Dinv (mode 3 uses both halves)
     const size_t sh = (3 * size_t(bs) * (bs + 1) + 2 * 768 + bs) * sizeof(cplx);
@@ -2490,7 +2690,8 @@ void launch_tri_inv(int n, int ld, cplx* const* dA, cplx* const* dO, int count, 
         attr = true;
     }
     ProfScope ps("tri_inv", s, 8.0 / 3.0 * count * nblk * double(bs) * bs * bs * ((mode == 3) ? 2 : 1));
-    { QPS_NOTE_LAUNCH(); tri_inv_kernel<<<dim3(nblk, count), mode == 3 ? 512 : 256, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode); }
+    { QPS_NOTE_LAUNCH(); tri_inv_kernel<<<dim3(nblk, count), mode == 3 ? 512 : 256, sh, s>>>(n, ld, dA, dO, bs, k0_first, mode,
+                                                                                                tile0); }
     QPS_CUDA(cudaGetLastError());
 }
 }  // namespace
@@ -2564,9 +2765,23 @@ void gemm_update(LuCtx& L, int M, int N, int K, size_t aoff, size_t boff, size_t
     zgemm_batched(M, N, alpha, beta, tasks, L.s, L.ws.gemm_tasks, "lu_gemm");
 }
 
+// leaf width of the recursion: 64-column panels in one CTA (lu_wpanel_kernel)
+// for matrices of <= 640 rows (QPS_LU_WIDE=0: 16-column shared-memory panels)
+bool wide_leaf(int n) {
+    static const bool off = [] {
+        const char* e = getenv("QPS_LU_WIDE");
+        return e && !strcmp(e, "0");
+    }();
+    return !off && n <= kWpThreads;
+}
+int lu_leaf(int n) {
+    if (wide_leaf(n)) return kWpMax;
+    return size_t(n) * kLeaf * sizeof(cplx) <= 200 * 1024 ? kLeaf : kNB;
+}
+
 // X[r0:r1, c0:c0+nc] <- L[r0:r1, r0:r1]^{-1} X (unit lower) inside the factor itself
 // (U12 of the recursive LU), leaves of <= 64 rows through on-demand tile inverses.
-void trsm_lower_rhs_leaf(LuCtx& L, int r0, int r1, int bs);
+void trsm_lower_rhs_leaf(LuCtx& L, int r0, int r1, int bs, size_t toff);
 void trsm_lower_rhs_update(LuCtx& L, int r0, int h, int r1);
 
 // rhs: apply the same L^{-1} to the carried right-hand sides (one tile inverse
@@ -2574,15 +2789,19 @@ void trsm_lower_rhs_update(LuCtx& L, int r0, int h, int r1);
 void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc, bool rhs = false) {
     const int m = r1 - r0;
     if (m <= kTB) {
-        const int bs = (m + 15) / 16 * 16;  // tile sized to the leaf (16, 32, 48 or 64 rows)
-        launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, bs, r0, 1, 1, L.s);  // tile 0 of Dinv as scratch
-        if (rhs) trsm_lower_rhs_leaf(L, r0, r1, bs);
+        // wide leaves: the tile's own inverse (r0 is 64-aligned); otherwise a
+        // tile sized to the leaf (16, 32, 48 or 64 rows) in tile 0 as scratch
+        const bool own_tile = wide_leaf(L.n);
+        const int bs = own_tile ? kTB : (m + 15) / 16 * 16;
+        const size_t toff = own_tile ? size_t(r0 / kTB) * 2 * kTB * kTB : 0;
+        if (!own_tile) launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, bs, r0, 1, 1, L.s);
+        if (rhs) trsm_lower_rhs_leaf(L, r0, r1, bs, toff);
         auto& tasks = L.ws.h_gemm;
         tasks.assign(L.count, GemmTask{});
         for (int b = 0; b < L.count; ++b) {
             GemmTask& t = tasks[b];
             t.nseg = 1;
-            t.A[0] = L.hD[b];
+            t.A[0] = L.hD[b] + toff;
             t.lda[0] = bs;
             t.B[0] = L.hA[b] + size_t(c0) * L.ld + r0;
             t.ldb[0] = L.ld;
@@ -2606,10 +2825,18 @@ void trsm_lower_in_factor(LuCtx& L, int r0, int r1, int c0, int nc, bool rhs = f
 void lu_rec(LuCtx& L, int c0, int nc) {
     const size_t psm = size_t(L.n - c0) * kLeaf * sizeof(cplx);
     const bool smem_leaf = size_t(L.n) * kLeaf * sizeof(cplx) <= 200 * 1024;
-    const int leaf = smem_leaf ? kLeaf : kNB;
+    const int leaf = lu_leaf(L.n);
     if (nc <= leaf) {
         ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(L.n - c0) * nc * nc / 2.0);
-        if (nc <= kRlW && L.n - c0 <= kRegPanelMaxRows) {
+        if (wide_leaf(L.n)) {
+            const int threads = ((L.n - c0 + 31) / 32) * 32;
+            { QPS_NOTE_LAUNCH(); lu_wpanel_kernel<<<L.count, threads, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc, L.sing); }
+            QPS_CUDA(cudaGetLastError());
+            // the leaf is a 64-aligned diagonal tile whose L and U are final:
+            // invert both into its Dinv slot now (the trsm of U12 and the
+            // level-0 solves read them; no final pass over all tiles)
+            launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, kTB, c0, 1, 3, L.s, c0 / kTB);
+        } else if (nc <= kRlW && L.n - c0 <= kRegPanelMaxRows) {
             launch_panel_fast(L.n, L.ld, L.dA, L.dP, c0, nc, L.sing, nullptr, L.count, L.s);
         } else if (smem_leaf) {
             static bool attr = false;
@@ -2645,14 +2872,14 @@ void lu_rec(LuCtx& L, int c0, int nc) {
 // B[r0:r1, :] <- L[r0:r1, r0:r1]^{-1} B[r0:r1, :] (unit lower, the factor's own
 // L) for the carried right-hand sides; leaves of <= 64 rows through tile inverses
 // B[r0:r1] <- (tile 0 of Dinv, bs x bs) B[r0:r1]: the leaf's L^{-1} already inverted
-void trsm_lower_rhs_leaf(LuCtx& L, int r0, int r1, int bs) {
+void trsm_lower_rhs_leaf(LuCtx& L, int r0, int r1, int bs, size_t toff) {
     const int m = r1 - r0;
     auto& tasks = L.ws.h_gemm;
     tasks.assign(L.count, GemmTask{});
     for (int b = 0; b < L.count; ++b) {
         GemmTask& t = tasks[b];
         t.nseg = 1;
-        t.A[0] = L.hD[b];
+        t.A[0] = L.hD[b] + toff;
         t.lda[0] = bs;
         t.B[0] = (*L.hB)[b] + r0;
         t.ldb[0] = L.ldb;
@@ -2684,13 +2911,15 @@ void trsm_lower_rhs(LuCtx& L, int r0, int r1) {
     const int m = r1 - r0;
     auto& tasks = L.ws.h_gemm;
     if (m <= kTB) {
-        const int bs = (m + 15) / 16 * 16;
-        launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, bs, r0, 1, 1, L.s);  // tile 0 of Dinv as scratch
+        const bool own_tile = wide_leaf(L.n);
+        const int bs = own_tile ? kTB : (m + 15) / 16 * 16;
+        const size_t toff = own_tile ? size_t(r0 / kTB) * 2 * kTB * kTB : 0;
+        if (!own_tile) launch_tri_inv(L.n, L.ld, L.dA, L.dD, L.count, bs, r0, 1, 1, L.s);  // tile 0 as scratch
         tasks.assign(L.count, GemmTask{});
         for (int b = 0; b < L.count; ++b) {
             GemmTask& t = tasks[b];
             t.nseg = 1;
-            t.A[0] = L.hD[b];
+            t.A[0] = L.hD[b] + toff;
             t.lda[0] = bs;
             t.B[0] = (*L.hB)[b] + r0;
             t.ldb[0] = L.ldb;
@@ -2725,8 +2954,7 @@ void trsm_lower_rhs(LuCtx& L, int r0, int r1) {
 // leaves the factorization as L^{-1} P B.  The spine's interchanges are not
 // copied back onto the left halves: L is not used after this solve (U is).
 void lu_rec_spine(LuCtx& L, int c0, int nc) {
-    const bool smem_leaf = size_t(L.n) * kLeaf * sizeof(cplx) <= 200 * 1024;
-    const int leaf = smem_leaf ? kLeaf : kNB;
+    const int leaf = lu_leaf(L.n);
     if (nc <= leaf) {
         lu_rec(L, c0, nc);
         {
@@ -2870,8 +3098,9 @@ void lu_factor_batched(int n, int ld, const std::vector<cplx*>& hA, const std::v
     const bool use_rl = rl_ok && (mode == 2 || (mode == 0 && count <= rl_max));
     if (use_rl) lu_rl(L);
     else lu_rec(L, 0, n);
-    // inverse 64x64 diagonal tiles of L and U for the GEMM-shaped solves
-    launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 3, s);
+    // inverse 64x64 diagonal tiles of L and U for the GEMM-shaped solves (the
+    // wide leaves of the recursion have inverted their own tiles)
+    if (use_rl || !wide_leaf(n)) launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 3, s);
 }
 
 // LU with partial pivoting of every matrix and the solve A X = B in one pass:
@@ -2894,7 +3123,7 @@ void lu_factor_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const 
     L.ldb = ldb;
     L.nrhs = nrhs;
     lu_rec_spine(L, 0, n);
-    launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 2, s);  // U tiles only
+    if (!wide_leaf(n)) launch_tri_inv(n, ld, ws.ptrs.p, ws.ptrs3.p, count, kTB, 0, (n + kTB - 1) / kTB, 2, s);  // U tiles
     upper_solve_tiles(n, ld, hA, hDinv, hB, ldb, nrhs, s, ws);
 }
 
