@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define QPS_ABI_VERSION 2
+#define QPS_ABI_VERSION 3
 
 typedef struct qps_ctx qps_ctx;
 typedef struct {
@@ -114,11 +114,16 @@ typedef struct {
  *   lr_rank_max     largest numerical rank of a compressed coupling's sample
  *   lr_probe_worst  a-posteriori test of the compression: max over couplings
  *                   of ||(I - P P^*) C w2||_F / ||C w2||_F on an independent
- *                   probe block w2 (above 1e-12 -> dense reduction) */
+ *                   probe block w2 (above 1e-12 -> dense reduction)
+ *   refine_steps    iterative-refinement steps applied to the block solve
+ *   refine_res0/1   ||f - A' eta||_2 / ||f||_2 before the first step and (when
+ *                   QPS_REFINE_CHECK=1) after the last one; 0 when none ran */
 typedef struct {
     int bcr_path;
     int lr_rank_max;
     double lr_probe_worst;
+    int refine_steps;
+    double refine_res0, refine_res1;
 } qps_solver_diag;
 
 /* ---------------------------------------------------------------- context */
@@ -131,6 +136,11 @@ int qps_last_error(const qps_ctx* ctx, char* msg, size_t cap, int* solver_layer,
 int qps_set_num_threads(qps_ctx* ctx, int n);
 /* periodize.hpp:15-18 qsolve_threshold() */
 int qps_set_qsolve_threshold(qps_ctx* ctx, double th);
+/* Product extension (no reference counterpart): steps of iterative refinement
+ * of the block cyclic reduction (residual with the unfactored A', correction
+ * through the kept factors).  -1 = default: 0 for qps_solve, 1 for the sweeps.
+ * The oracle accepts and ignores it (its block Thomas needs none). */
+int qps_set_refine(qps_ctx* ctx, int steps);
 
 /* ----------------------------------------------------- geometry & problem */
 /* LayerStack + build_geometry(stack, num), geometry.hpp:289-296,480-496 */

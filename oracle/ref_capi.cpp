@@ -133,6 +133,10 @@ int qps_set_qsolve_threshold(qps_ctx* c, double th) {
     return guarded(c, [&] { qsolve_threshold() = th; });
 }
 
+// product extension (iterative refinement of the GPU's cyclic reduction): the
+// reference's block Thomas has nothing to refine
+int qps_set_refine(qps_ctx* c, int steps) { return (c && steps >= -1 && steps <= 4) ? QPS_OK : QPS_ERR_USAGE; }
+
 int qps_build_geometry(qps_ctx* c, double d, int n_layers, const double* eps, const double* mu, int n_ifaces,
                        const qps_interface_spec* ifs, const qps_numerics* num) {
     return guarded(c, [&] {
@@ -626,7 +630,7 @@ int qps_get_phase_times(const qps_ctx* c, qps_phase_times* t) {
 
 int qps_solver_diagnostics(const qps_ctx* c, qps_solver_diag* d) {
     if (!c || !d) return QPS_ERR_USAGE;
-    *d = qps_solver_diag{-1, 0, 0.0};  // the reference's block Thomas (tridiag.hpp:23-46)
+    *d = qps_solver_diag{-1, 0, 0.0, 0, 0.0, 0.0};  // the reference's block Thomas (tridiag.hpp:23-46)
     return QPS_OK;
 }
 

@@ -1990,6 +1990,8 @@ void wb_factor_async(Ctx& c, cplx* Ad) {
     c.factor_pending = true;
 }
 
+void wb_refine_step(Ctx& c, cplx* Ad, int slot, bool apply);
+
 void bcr_solve_wb(Ctx& c, cplx* Ad) {
     ProfPhase phase("bcr");
     ++c.n_factorizations;
@@ -2049,16 +2051,10 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
                         "singular diagonal factor (resonant parameters?) at layer " + std::to_string(worst + 1),
                         worst + 1);
     };
-    struct Pos {
-        int idx;
-        int j;  // a * I + idx: slot of the per-block buffers
-        cplx* F;
-        const cplx *PL, *RL, *PU, *RU;
-        const cplx* Z;  // D^{-1} [P_L P_U] once eliminated (n x 2r, ld n)
-        bool updated;   // S, g nonzero
-    };
+    using Pos = WbPos;
     using Level = std::vector<std::vector<Pos>>;
-    std::vector<Level> levels;
+    auto& levels = c.wb_levels;
+    levels.clear();
     auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * wc; };
     auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
     auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2 * m; };  // r2 x m, ld r2
@@ -2141,6 +2137,14 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             QPS_D2H(c.bcr_flag_h.p, c.l0_flag.p, sizeof(int) * fa.size(), s);
             l0_orig = orig;
             tmark("solve with the early factors", 0, int(fa.size()));
+        } else if (c.refine_ready) {
+            // refinement replays the solve: factors that stay usable (no spine)
+            lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
+            lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, s, c.ws);
+            c.bcr_flag_h.ensure(fa.size());
+            QPS_D2H(c.bcr_flag_h.p, flag.p, sizeof(int) * fa.size(), s);
+            l0_orig = orig;
+            tmark("factor, solve (refinable)", 0, int(fa.size()));
         } else if (separate) {
             lu_factor_batched(nb, nb, fa, fp, fd, flag.p, s, c.ws);
             lu_rcond_batched(nb, nb, c.ws.ptrs.p, nullptr, 0, c.ws.ptrs3.p, nullptr, 0, int(fa.size()), kRcondMin, flag.p,
@@ -2455,7 +2459,186 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         QPS_CUDA(cudaEventDestroy(te0));
         QPS_CUDA(cudaEventDestroy(te1));
     }
+    if (c.refine_ready) {
+        c.ref_nrm.ensure(3);
+        QPS_CUDA(cudaMemsetAsync(c.ref_nrm.p, 0, 3 * sizeof(double), s));
+        for (int it = 0; it < c.refine_used; ++it) wb_refine_step(c, Ad, it == 0 ? 0 : -1, true);
+        static const bool check = getenv("QPS_REFINE_CHECK") != nullptr;  // residual after the last step too
+        if (check) wb_refine_step(c, Ad, 1, false);
+        c.ref_nrm_h.ensure(3);
+        QPS_D2H(c.ref_nrm_h.p, c.ref_nrm.p, 3 * sizeof(double), s);  // read after the solve's final sync
+        tl_mark(c, "refine", s);
+    }
+    c.refine_ready = false;
     c.eta_valid = true;
+}
+
+// One step of iterative refinement of the Woodbury solve: r = f - A' eta with
+// the unfactored diagonal blocks (ref_D) and couplings (raw A minus the
+// deferred proxy terms Bc X), then A' delta = r by replaying the reduction on
+// r -- level-0 LU solves with the kept factors, the recorded levels' Z, S, W
+// and right factors, the back substitution -- and eta += delta.  Cost: one
+// pass over A' and one pass over the factors per step.  Cyclic reduction is
+// less accurate than block Thomas at ill-conditioned angles; a step brings
+// the solution back to the accuracy the factors' conditioning allows.
+void wb_refine_step(Ctx& c, cplx* Ad, int slot, bool apply) {
+    const Dims& D = c.dims;
+    const int I = D.I, nb = D.nb, ns = D.nsys, r = c.lr_r, r2 = 2 * r, P = D.P;
+    const int npos = ns * I, m = std::max(1, c.nrhs);
+    const size_t nb2 = D.nb2(), fs = size_t(nb) * m, dsz = lu_dinv_elems(nb);
+    const int wc = r2 + m + kRcProbe;
+    cudaStream_t s = c.stream;
+    const cplx one{1, 0}, mone{-1, 0}, zero{0, 0};
+    RhsOps rhs{m, s, c.ws};
+    ProfPhase phase("refine");
+    cplx* eta = c.F.p;
+    c.ref_R.ensure(size_t(npos) * fs);
+    cplx* R = c.ref_R.p;
+    // r = f
+    if (m == 1) {
+        QPS_CUDA(cudaMemsetAsync(R, 0, sizeof(cplx) * npos * fs, s));
+        for (int a = 0; a < ns; ++a)
+            QPS_CUDA(cudaMemcpyAsync(R + size_t(a) * I * fs, c.f.p + size_t(a) * nb, sizeof(cplx) * nb,
+                                     cudaMemcpyDeviceToDevice, s));
+    } else {
+        QPS_CUDA(cudaMemcpyAsync(R, c.ref_F.p, sizeof(cplx) * npos * fs, cudaMemcpyDeviceToDevice, s));
+    }
+    if (slot == 0) batched_fro(R, int(npos * fs), 1, int(npos * fs), 0, 1, c.ref_nrm.p + 2, s);  // ||f||
+    // r -= A' eta: D_j eta_j + L_j eta_{j-1} (one two-segment product), U_j eta_{j+1},
+    // then the deferred proxy terms + Bc (X eta) of both couplings
+    std::vector<GemmTask> t1, t2, tx, tb;
+    c.ref_X.ensure(size_t(npos) * 2 * P * m);
+    cplx* xe = c.ref_X.p;  // X eta of the two couplings per block: 2P x m, ld 2P
+    const bool corr = c.couplings_deferred;
+    for (int a = 0; a < ns; ++a)
+        for (int j = 0; j < I; ++j) {
+            const size_t q = size_t(a) * I + j;
+            GemmTask g = gemm1(c.ref_D.p + q * nb2, nb, eta + q * fs, nb, nb, R + q * fs, nb);
+            if (j >= 1) {
+                g.nseg = 2;
+                g.A[1] = c.ref_Al + size_t(a) * D.sU() + size_t(j - 1) * nb2;
+                g.lda[1] = nb;
+                g.B[1] = eta + (q - 1) * fs;
+                g.ldb[1] = nb;
+                g.K[1] = nb;
+            }
+            t1.push_back(g);
+            if (j + 1 < I)
+                t2.push_back(gemm1(c.ref_Au + size_t(a) * D.sU() + size_t(j) * nb2, nb, eta + (q + 1) * fs, nb, nb,
+                                   R + q * fs, nb));
+            if (corr) {
+                GemmTask b{};
+                b.C = R + q * fs;
+                b.ldc = nb;
+                if (j >= 1) {
+                    const GemmTask& u = c.coupling_sub[size_t(a) * (I - 1) + j - 1];
+                    tx.push_back(gemm1(u.B[0], u.ldb[0], eta + (q - 1) * fs, nb, nb, xe + q * 2 * P * m, 2 * P));
+                    b.A[b.nseg] = u.A[0]; b.lda[b.nseg] = u.lda[0]; b.B[b.nseg] = xe + q * 2 * P * m;
+                    b.ldb[b.nseg] = 2 * P; b.K[b.nseg] = P; ++b.nseg;
+                }
+                if (j + 1 < I) {
+                    const GemmTask& u = c.coupling_sup[size_t(a) * (I - 1) + j];
+                    tx.push_back(gemm1(u.B[0], u.ldb[0], eta + (q + 1) * fs, nb, nb, xe + q * 2 * P * m + P, 2 * P));
+                    b.A[b.nseg] = u.A[0]; b.lda[b.nseg] = u.lda[0]; b.B[b.nseg] = xe + q * 2 * P * m + P;
+                    b.ldb[b.nseg] = 2 * P; b.K[b.nseg] = P; ++b.nseg;
+                }
+                if (b.nseg) tb.push_back(b);
+            }
+        }
+    rhs.run(nb, mone, one, t1);
+    rhs.run(nb, mone, one, t2);
+    if (corr) {
+        RhsOps rx{m, s, c.ws};
+        rx.run(P, one, zero, tx);
+        rhs.run(nb, one, one, tb);
+    }
+    if (slot >= 0) batched_fro(R, int(npos * fs), 1, int(npos * fs), 0, 1, c.ref_nrm.p + slot, s);
+    if (!apply) return;
+    // replay: level 0, delta_j = D_j^{-1} r_j with the kept LU factors
+    {
+        std::vector<cplx*> fa(npos), fd(npos), rb(npos);
+        std::vector<int*> fp(npos);
+        for (int q = 0; q < npos; ++q) {
+            fa[q] = Ad + size_t(q) * nb2;
+            fp[q] = c.ipiv.p + size_t(q) * nb;
+            fd[q] = c.dinv.p + size_t(q) * dsz;
+            rb[q] = R + size_t(q) * fs;
+        }
+        lu_solve_batched(nb, nb, fa, fp, fd, rb, nb, m, s, c.ws);
+    }
+    auto& levels = c.wb_levels;
+    auto Rof = [&](const WbPos& p) { return R + size_t(p.j) * fs; };
+    auto W0_of = [&](int j) { return c.lr_W0.p + size_t(j) * nb * wc; };
+    auto S_of = [&](int j) { return c.lr_S.p + size_t(j) * r2 * nb; };
+    c.lr_g.zero(s);
+    auto g_of = [&](int j) { return c.lr_g.p + size_t(j) * r2 * m; };
+    c.ref_A.ensure(size_t(npos) * r2 * m);
+    auto elim = [&](const std::vector<const WbPos*>& blk) {
+        std::vector<GemmTask> gu, ga, gz;
+        for (const WbPos* p : blk) {
+            if (!p->updated) continue;
+            cplx* aq = c.ref_A.p + size_t(p->j) * r2 * m;
+            cplx* F = Rof(*p);
+            gu.push_back(gemm1(W0_of(p->j), nb, g_of(p->j), r2, r2, F, nb));  // u = y - W g
+            ga.push_back(gemm1(S_of(p->j), r2, F, nb, nb, aq, r2));           // a = S u
+            gz.push_back(gemm1(p->Z, nb, aq, r2, r2, F, nb));                 // z = u + Z a
+        }
+        rhs.run(nb, mone, one, gu);
+        rhs.run(r2, one, zero, ga);
+        rhs.run(nb, one, one, gz);
+    };
+    const int nlvl = int(levels.size()) - 1;  // the last entry holds the final block of every system
+    for (int l = 0; l < nlvl; ++l) {
+        const auto& cur = levels[l];
+        const int sz = int(cur[0].size());
+        std::vector<const WbPos*> odd;
+        for (int a = 0; a < ns; ++a)
+            for (int o = 1; o < sz; o += 2) odd.push_back(&cur[a][o]);
+        elim(odd);
+        std::vector<GemmTask> v1;
+        for (int a = 0; a < ns; ++a)
+            for (int e = 0; e < sz; e += 2) {
+                const WbPos& pe = cur[a][e];
+                if (e >= 1) v1.push_back(gemm1(pe.RL, r, Rof(cur[a][e - 1]), nb, nb, g_of(pe.j), r2));
+                if (e + 1 < sz) v1.push_back(gemm1(pe.RU, r, Rof(cur[a][e + 1]), nb, nb, g_of(pe.j) + r, r2));
+            }
+        rhs.run(r, one, one, v1);
+    }
+    {
+        std::vector<const WbPos*> fin;
+        for (int a = 0; a < ns; ++a) fin.push_back(&levels[nlvl][a][0]);
+        elim(fin);
+    }
+    for (int l = nlvl - 1; l >= 0; --l) {
+        const auto& cur = levels[l];
+        const int sz = int(cur[0].size());
+        std::vector<GemmTask> t1b, t2b;
+        for (int a = 0; a < ns; ++a)
+            for (int o = 1; o < sz; o += 2) {
+                const WbPos& p = cur[a][o];
+                cplx* vec = c.ref_A.p + size_t(p.j) * r2 * m;
+                GemmTask w{};
+                if (p.RL) {
+                    t1b.push_back(gemm1(p.RL, r, Rof(cur[a][o - 1]), nb, nb, vec, r2));
+                    w.A[w.nseg] = p.Z; w.lda[w.nseg] = nb; w.B[w.nseg] = vec; w.ldb[w.nseg] = r2; w.K[w.nseg] = r;
+                    ++w.nseg;
+                }
+                if (p.RU && o + 1 < sz) {
+                    t1b.push_back(gemm1(p.RU, r, Rof(cur[a][o + 1]), nb, nb, vec + r, r2));
+                    w.A[w.nseg] = p.Z + size_t(nb) * r; w.lda[w.nseg] = nb; w.B[w.nseg] = vec + r;
+                    w.ldb[w.nseg] = r2; w.K[w.nseg] = r;
+                    ++w.nseg;
+                }
+                if (w.nseg) {
+                    w.C = Rof(p);
+                    w.ldc = nb;
+                    t2b.push_back(w);
+                }
+            }
+        rhs.run(r, one, zero, t1b);
+        rhs.run(nb, mone, one, t2b);
+    }
+    axpy_blocks(eta, R, size_t(npos) * fs, s);  // eta += delta
 }
 
 }  // namespace qpsb

@@ -193,6 +193,13 @@ int qps_set_qsolve_threshold(qps_ctx* h, double th) {
     return guarded(h, [&](Ctx& c) { c.qsolve_th0 = th; });
 }
 
+int qps_set_refine(qps_ctx* h, int steps) {
+    return guarded(h, [&](Ctx& c) {
+        need(steps >= -1 && steps <= 4, "refine: steps in [-1, 4]");
+        c.refine = steps;
+    });
+}
+
 int qps_build_geometry(qps_ctx* h, double d, int n_layers, const double* eps, const double* mu, int n_ifaces,
                        const qps_interface_spec* ifs, const qps_numerics* num) {
     return guarded(h, [&](Ctx& c) {
@@ -661,6 +668,10 @@ int qps_solver_diagnostics(const qps_ctx* h, qps_solver_diag* d) {
     d->bcr_path = h->c.bcr_path;
     d->lr_rank_max = h->c.lr_rank_max;
     d->lr_probe_worst = h->c.lr_probe_worst;
+    d->refine_steps = h->c.refine_used;
+    const double fn = h->c.refine_used && h->c.ref_nrm_h[2] > 0 ? h->c.ref_nrm_h[2] : 0.0;
+    d->refine_res0 = fn > 0 ? h->c.ref_nrm_h[0] / fn : 0.0;
+    d->refine_res1 = fn > 0 ? h->c.ref_nrm_h[1] / fn : 0.0;
     return QPS_OK;
 }
 

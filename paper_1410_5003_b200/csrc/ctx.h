@@ -114,6 +114,18 @@ struct BcrLevel {
 };
 using BcrLevels = std::vector<BcrLevel>;  // one per system
 
+// one position of the Woodbury block cyclic reduction (bcr_lr.cu): kept per
+// level after a solve so that further right-hand sides (iterative refinement)
+// replay the reduction without refactoring
+struct WbPos {
+    int idx;
+    int j;  // a * I + idx: slot of the per-block buffers
+    cplx* F;
+    const cplx *PL, *RL, *PU, *RU;
+    const cplx* Z;  // D^{-1} [P_L P_U] once eliminated (n x 2r, ld n)
+    bool updated;   // S, g nonzero
+};
+
 struct Ctx {
     int device = 0;
     bool host_only = false;  // device == -1: geometry/problem logic only, every device call fails
@@ -272,6 +284,19 @@ struct Ctx {
     cudaEvent_t l0_ev[kL0MaxChunks] = {};
     Workspace l0_ws[kL0MaxChunks];
     int l0_chunks = 1;
+    // iterative refinement of the Woodbury block solve: steps (qps_set_refine,
+    // QPS_REFINE; the sweeps default to one), the unfactored diagonal blocks
+    // and right-hand sides it needs, the residual / correction buffer, and the
+    // relative residuals ||f - A' eta|| / ||f|| before / after the last step
+    int refine = -1;                   // -1: the default of the caller (refine_default)
+    int refine_default = 0;            // 1 inside the sweeps
+    int refine_used = 0;               // steps applied by the last block solve
+    HBuf<double> ref_nrm_h;            // host copy of ref_nrm (relative)
+    bool refine_ready = false;         // ref_D / ref_F hold this solve's copies
+    const cplx *ref_Au = nullptr, *ref_Al = nullptr;  // the couplings of the solve being refined
+    DBuf<cplx> ref_D, ref_F, ref_R, ref_X, ref_A;
+    DBuf<double> ref_nrm;              // ||r_before||, ||r_after||, ||f|| of the last refinement
+    std::vector<std::vector<std::vector<WbPos>>> wb_levels;
     std::chrono::steady_clock::time_point host_t0;  // QPS_HOST_TRACE
     DBuf<PairTask> d_pair;
     DBuf<ProxyTask> d_proxy;

@@ -3250,6 +3250,25 @@ void gather_columns(const std::vector<const cplx*>& src, const std::vector<int>&
     QPS_CUDA(cudaGetLastError());
 }
 
+namespace {
+__global__ void axpy_kernel(cplx* __restrict__ y, const cplx* __restrict__ x, size_t n) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const cplx a = x[i];
+        cplx b = y[i];
+        b.re += a.re;
+        b.im += a.im;
+        y[i] = b;
+    }
+}
+}  // namespace
+
+void axpy_blocks(cplx* y, const cplx* x, size_t n, cudaStream_t s) {
+    if (n == 0) return;
+    const int grid = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    { QPS_NOTE_LAUNCH(); axpy_kernel<<<grid, 256, 0, s>>>(y, x, n); }
+    QPS_CUDA(cudaGetLastError());
+}
+
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s) {
     if (count == 0) return;
     ProfScope ps("reduce", s, 0.0, 16.0 * count * double(m) * n);

@@ -115,6 +115,8 @@ void gather_columns(const std::vector<const cplx*>& src, const std::vector<int>&
 // per problem max |X_ij| over an m x n block (ld), count problems with stride
 void batched_maxabs(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s);
 // per problem Frobenius norm
+// y += x (n complex entries)
+void axpy_blocks(cplx* y, const cplx* x, size_t n, cudaStream_t s);
 void batched_fro(const cplx* X, int m, int n, int ld, size_t stride, int count, double* out, cudaStream_t s,
                  double* maxabs_out = nullptr);
 void copy_blocks(const cplx* src, int lds, size_t sstride, cplx* dst, int ldd, size_t dstride, int m, int n,

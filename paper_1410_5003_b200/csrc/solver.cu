@@ -869,6 +869,32 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     // runs on the side stream (after the block norms of the rcond screen)
     // while the main stream compresses the couplings; otherwise the norms alone
     // overlap the compression
+    // iterative refinement (wb_refine_step) needs the unfactored diagonal blocks
+    // and the right-hand sides: copied before the factorization starts
+    {
+        static const int env = [] {  // QPS_REFINE=n overrides the default (A/B)
+            const char* e = getenv("QPS_REFINE");
+            return e ? atoi(e) : -1;
+        }();
+        const int steps = c.refine >= 0 ? c.refine : env >= 0 ? env : c.refine_default;
+        c.refine_used = 0;
+        c.refine_ready = woodbury && !lr_direct && steps > 0 && lr_eligible_pub(c);
+        if (c.refine_ready) {
+            const Dims& D = c.dims;
+            const size_t npos = size_t(D.nsys) * D.I;
+            c.ref_D.ensure(npos * D.nb2());
+            QPS_CUDA(cudaMemcpyAsync(c.ref_D.p, Ad, sizeof(cplx) * npos * D.nb2(), cudaMemcpyDeviceToDevice,
+                                     c.stream));
+            if (c.nrhs > 1) {
+                const size_t fsz = npos * D.nb * size_t(c.nrhs);
+                c.ref_F.ensure(fsz);
+                QPS_CUDA(cudaMemcpyAsync(c.ref_F.p, c.F.p, sizeof(cplx) * fsz, cudaMemcpyDeviceToDevice, c.stream));
+            }
+            c.refine_used = steps;
+            c.ref_Au = Au;
+            c.ref_Al = Al;
+        }
+    }
     if (woodbury && !early_off && c.allow_early && lr_eligible_pub(c)) wb_factor_async(c, Ad);
     else if (woodbury) wb_anorm_async(c, Ad);
     if (!dense_only && !c.force_dense && lr_compress(c, Au, Al)) {
@@ -879,6 +905,8 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         c.couplings_deferred = false;
         return;
     }
+    c.refine_ready = false;  // the dense reduction keeps no replayable factors
+    c.refine_used = 0;
     if (c.anorm_pending) {  // the side stream's norms read Ad: join before the factorization rewrites it
         QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_anorm, 0));
         c.anorm_pending = false;

@@ -717,6 +717,15 @@ void solve_alpha_group(Ctx& c, const std::vector<Problem>& gp, qps_phase_times& 
 
 void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, double* T, double* fe, cplx* aU,
                cplx* aD, int* status) {
+    // one step of iterative refinement by default: a sweep crosses angles where
+    // cyclic reduction is markedly less accurate than the reference's block
+    // Thomas (qps_set_refine overrides)
+    struct RefineDefault {
+        Ctx& c;
+        int old;
+        ~RefineDefault() { c.refine_default = old; }
+    } rd{c, c.refine_default};
+    c.refine_default = 1;
     const Problem orig = c.prob;
     const double omega = orig.omega;
     c.sweep_interior = c.sweep_factorizations = 0;

@@ -104,7 +104,8 @@ class _Num(C.Structure):
 
 
 class _Diag(C.Structure):
-    _fields_ = [("bcr_path", C.c_int), ("lr_rank_max", C.c_int), ("lr_probe_worst", C.c_double)]
+    _fields_ = [("bcr_path", C.c_int), ("lr_rank_max", C.c_int), ("lr_probe_worst", C.c_double),
+                ("refine_steps", C.c_int), ("refine_res0", C.c_double), ("refine_res1", C.c_double)]
 
 
 class _Times(C.Structure):
@@ -175,6 +176,7 @@ def _bind(lib):
         "qps_last_error": (C.c_int, [vp, C.c_char_p, C.c_size_t, P(C.c_int), P(C.c_uint64)]),
         "qps_set_num_threads": (C.c_int, [vp, C.c_int]),
         "qps_set_qsolve_threshold": (C.c_int, [vp, C.c_double]),
+        "qps_set_refine": (C.c_int, [vp, C.c_int]),
         "qps_build_geometry": (C.c_int, [vp, C.c_double, C.c_int, P(C.c_double), P(C.c_double), C.c_int,
                                          P(_Spec), P(_Num)]),
         "qps_make_problem": (C.c_int, [vp, C.c_double, C.c_double, C.c_int]),
@@ -389,6 +391,11 @@ class Solver:
 
     def set_qsolve_threshold(self, th):
         self._check(self.lib.qps_set_qsolve_threshold(self.h, th))
+
+    def set_refine(self, steps: int):
+        """Iterative-refinement steps of the block solve (-1: default, 0 for
+        solves and 1 for sweeps; the oracle ignores it)."""
+        self._check(self.lib.qps_set_refine(self.h, int(steps)))
 
     # ------------------------------------------------------------ outputs
     def solution(self):
