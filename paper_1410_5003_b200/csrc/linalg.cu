@@ -245,6 +245,18 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         if (st < nchunks) issue(st, st);
         cp_async_commit();
     }
+    if (beta.re != 0.0 || beta.im != 0.0) {
+        // the epilogue reads C: pull this CTA's tile into L2 now, so the
+        // read-modify-write at the end does not wait on HBM (short-K products
+        // spend a large share of their time in that dependent load)
+        for (int e = tid; e < BN * (BM / 4); e += NT) {
+            const int col = n0 + e / (BM / 4), row = m0 + (e % (BM / 4)) * 4;  // 4 complex = 64 B per prefetch
+            if (col < N && row < M) {
+                const cplx* p = T.C + size_t(col) * T.ldc + row;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+            }
+        }
+    }
     for (int c = 0; c < nchunks; ++c) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
