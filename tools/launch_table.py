@@ -11,6 +11,7 @@ path = sys.argv[1]
 rng = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else None
 shapes = "--shapes" in sys.argv
 rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+rows = rows[next(i for i, r in enumerate(rows) if r and r[0] == "ID"):]  # skip program output before the CSV
 h = rows[0]
 iname, iid, imet, ival = h.index("Kernel Name"), h.index("ID"), h.index("Metric Name"), h.index("Metric Value")
 inv = [i for i, c in enumerate(h) if "Push/Pop_Range" in c]
