@@ -950,6 +950,7 @@ void lr_sample_async(Ctx& c) {
     const int nc = 2 * ns * (I - 1);
     QPS_CUDA(cudaEventRecord(c.ev_fill, c.stream));
     QPS_CUDA(cudaStreamWaitEvent(c.side2, c.ev_fill, 0));
+    if (c.fill_pending) QPS_CUDA(cudaStreamWaitEvent(c.side2, c.ev_fillB, 0));  // the couplings of a split fill
     lr_omega_setup(c, c.side2);
     c.lr_Y.ensure(size_t(nc) * nb * kLrCols);
     std::vector<GemmTask> t(nc);

@@ -410,7 +410,14 @@ int qps_solve(qps_ctx* h) {
         c.times.factor_ms = 0.0;
         tl_mark(c, "start", c.stream);
         for (int attempt = 0;; ++attempt) {
-            run_fill(c);
+            c.fill_overlap = true;  // the Schur least squares start while the big blocks fill
+            try {
+                run_fill(c);
+            } catch (...) {
+                c.fill_overlap = false;
+                throw;
+            }
+            c.fill_overlap = false;
             tl_mark(c, "fill", c.stream);
             c.times.assemble_ms = 0.0;
             lr_sample_async(c);  // overlaps the Schur least squares

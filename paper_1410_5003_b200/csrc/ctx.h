@@ -302,6 +302,16 @@ struct Ctx {
     DBuf<ProxyTask> d_proxy;
     DBuf<AlpertTask> d_alpert;
     DBuf<int4> d_tiles;
+    // one-shot solves split the fill: the wall / radiation blocks and the proxy
+    // blocks that the Schur least squares read first on the main stream, the
+    // couplings, self blocks and their Alpert corrections on side3, joined
+    // before the A' update (fill_overlap; opt-in QPS_FILL_OVERLAP=1, no gain measured)
+    bool fill_overlap = false, fill_pending = false, fill_err_pending = false;
+    cudaEvent_t ev_fillB = nullptr;
+    cudaStream_t fill_stream = nullptr;
+    DBuf<PairTask> d_pair2;
+    DBuf<int4> d_tiles2;
+    HBuf<int> fill_err_h;
     std::string err_msg;
     int err_layer = 0;
     uint64_t err_bytes = 0;
@@ -346,7 +356,7 @@ void spectrum_of(const Problem& p, double d, const cplx* aU, const cplx* aD, dou
 // (Qdst: the corner Q' blocks to write W into, default c.Qc)
 void write_radiation_and_rhs(Ctx& c, const std::vector<Problem>& probs, cplx* Qdst = nullptr);
 // identity on the unused diagonal of padded A_jj blocks, every system
-void pad_identity(Ctx& c);
+void pad_identity(Ctx& c, cudaStream_t s = nullptr);
 // precompute_shift_blocks (assembly.hpp:212-287) into c.cache_pool
 void cache_fill(Ctx& c);
 // assemble_system (assembly.hpp:462-483) for dims.nsys angles from the cache

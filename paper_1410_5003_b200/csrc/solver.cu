@@ -281,6 +281,10 @@ void fill_system_fused(Ctx& c) {
     const size_t nb2 = size_t(nb) * nb;
 
     c.host_t0 = std::chrono::steady_clock::now();
+    if (c.fill_pending || c.fill_err_pending) {  // an aborted solve left the big-block half in flight
+        QPS_CUDA(cudaStreamSynchronize(c.fill_stream));
+        c.fill_pending = c.fill_err_pending = false;
+    }
     alloc_system(c);
     if (D.padded) {
         bool uniform = true;
@@ -499,9 +503,44 @@ void fill_system_fused(Ctx& c) {
     const DevPool pool{c.px.p, c.py.p, c.pnx.p, c.pny.p, c.pw.p};
     static const bool htrace = getenv("QPS_HOST_TRACE") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
-    launch_pair_fill(pt, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
+    // opt-in (QPS_FILL_OVERLAP=1): measured no gain at config 4 -- the least-
+    // squares kernels (one CTA of up to 216 KB shared memory per problem) and
+    // the fill kernels both occupy every SM, so neither fills the other's gaps
+    static const bool overlap_on = [] {
+        const char* e = getenv("QPS_FILL_OVERLAP");
+        return e && !strcmp(e, "1");
+    }();
+    const bool split = c.fill_overlap && overlap_on && c.side && c.side3;
+    c.fill_pending = false;
+    if (split) {
+        // the big blocks (couplings, self blocks + Alpert, identity padding) on
+        // side3 while the main stream fills what the Schur least squares read
+        // first (wall / radiation blocks, proxy blocks) and starts them
+        std::vector<PairTask> early, late;
+        for (const auto& t : pt) (t.self == 0 && !t.mirror ? early : late).push_back(t);
+        if (!c.ev_fillB) QPS_CUDA(cudaEventCreateWithFlags(&c.ev_fillB, cudaEventDisableTiming));
+        // high priority (the corner stream, idle until the Schur step): the big
+        // blocks gate the A' update, the least squares beside them are latency-bound
+        static const bool low = [] {  // QPS_FILL_STREAM=low: side3 (low priority) instead (A/B)
+            const char* e = getenv("QPS_FILL_STREAM");
+            return e && !strcmp(e, "low");
+        }();
+        c.fill_stream = low ? c.side3 : c.side;
+        const cudaStream_t fb = c.fill_stream;
+        QPS_CUDA(cudaEventRecord(c.ev_fork, s));
+        QPS_CUDA(cudaStreamWaitEvent(fb, c.ev_fork, 0));
+        launch_pair_fill(late, pool, c.d_err.p, fb, c.d_pair2, c.d_tiles2);
+        launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.aux_pool.p, c.d_err.p, fb, c.d_alpert);
+        if (D.padded) pad_identity(c, fb);
+        QPS_CUDA(cudaEventRecord(c.ev_fillB, fb));
+        tl_mark(c, "fill(big blocks)", fb);
+        c.fill_pending = true;
+        launch_pair_fill(early, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
+    } else {
+        launch_pair_fill(pt, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
+    }
     auto t1 = std::chrono::steady_clock::now();
-    launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.aux_pool.p, c.d_err.p, s, c.d_alpert);
+    if (!split) launch_alpert(at, alpert_rows, pool, c.segs.p, c.fourier.p, c.aux_pool.p, c.d_err.p, s, c.d_alpert);
     launch_proxy_fill(xt, pool, c.d_err.p, s, c.d_proxy, c.d_tiles);
     auto t2 = std::chrono::steady_clock::now();
     if (htrace)
@@ -511,11 +550,13 @@ void fill_system_fused(Ctx& c) {
                 std::chrono::duration<double, std::milli>(t2 - t1).count());
 
     write_radiation_and_rhs(c, {c.prob});
-    if (D.padded) pad_identity(c);
-    int herr = 0;
-    QPS_D2H(&herr, c.d_err.p, sizeof(int), s);
-    QPS_CUDA(cudaStreamSynchronize(s));
-    if (herr) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
+    if (!split) {
+        if (D.padded) pad_identity(c);
+        int herr = 0;
+        QPS_D2H(&herr, c.d_err.p, sizeof(int), s);
+        QPS_CUDA(cudaStreamSynchronize(s));
+        if (herr) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
+    }  // else: checked by fill_join once both halves are done
     // evaluations performed: plain pairs minus band exclusions plus aux nodes
     uint64_t ev = 0;
     for (const auto& t : pt) ev += uint64_t(t.nt) * t.ns * t.nterm * t.nk * (t.mirror && t.self == 0 ? 2 : 1);
@@ -538,6 +579,25 @@ void fill_system_fused(Ctx& c) {
     c.performed_evals = ev;
     c.ref_evals = reference_fill_evals(g);
     c.sys_valid = true;
+}
+
+// The main stream joins the big-block half of a split fill; check_now: read the
+// coincidence flag of both halves (host wait on the fill only)
+void fill_join(Ctx& c, bool check_now) {
+    if (c.fill_pending) {
+        QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_fillB, 0));
+        c.fill_pending = false;
+        c.fill_err_h.ensure(1);
+        c.fill_err_h[0] = 0;
+        QPS_D2H(c.fill_err_h.p, c.d_err.p, sizeof(int), c.stream);
+        QPS_CUDA(cudaEventRecord(c.ev_fillB, c.stream));
+        c.fill_err_pending = true;
+    }
+    if (check_now && c.fill_err_pending) {
+        QPS_CUDA(cudaEventSynchronize(c.ev_fillB));
+        c.fill_err_pending = false;
+        if (c.fill_err_h[0]) fail(QPS_ERR_SINGULARITY, "kernel evaluated at coincident target/source pair");
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -816,6 +876,7 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
             }
         }
     }
+    fill_join(c, false);  // the diagonal blocks of a split fill
     zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, tasks, c.stream, c.ws.gemm_tasks, "schur_update");
     qsolve_poll(c, fams, false);  // the corner least squares (side stream)
     if (corners) {
@@ -825,6 +886,7 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, ctasks, c.stream, c.ws.gemm_tasks, "schur_update");
     }
     qsolve_collect(fams);  // per-layer LSQ residuals, read back while the update runs
+    fill_join(c, true);    // coincidence flag of a split fill
     for (int a = 0; a < ns; ++a) {
         double* l = c.lsq_all.data() + size_t(a) * (I + 1);
         l[0] = lc[2 * a];

@@ -100,13 +100,14 @@ __global__ void pad_identity_kernel(cplx* __restrict__ A, size_t sA, int nb, con
 
 }  // namespace
 
-void pad_identity(Ctx& c) {
+void pad_identity(Ctx& c, cudaStream_t s) {
     const Dims& D = c.dims;
+    if (!s) s = c.stream;
     std::vector<int> n2(D.I);
     for (int j = 0; j < D.I; ++j) n2[j] = 2 * D.N[j];
-    c.d_nodes2.upload(n2, c.stream);
+    c.d_nodes2.upload(n2, s);
     const size_t tot = size_t(D.nsys) * D.I * D.nb;
-    { QPS_NOTE_LAUNCH(); pad_identity_kernel<<<unsigned((tot + 255) / 256), 256, 0, c.stream>>>(c.Adiag.p, D.sA(), D.nb, c.d_nodes2.p, D.I,
+    { QPS_NOTE_LAUNCH(); pad_identity_kernel<<<unsigned((tot + 255) / 256), 256, 0, s>>>(c.Adiag.p, D.sA(), D.nb, c.d_nodes2.p, D.I,
                                                                             D.nsys); }
     QPS_CUDA(cudaGetLastError());
 }
