@@ -2468,6 +2468,15 @@ bool thin48_off() {  // QPS_ZGEMM_THIN48=0: 16-row tiles for 48-row products (A/
 }
 }  // namespace
 
+// QPS_ZGEMM_WIDE=1: the 64 x 32 tile for large K and outputs (the round-1 rule, A/B)
+bool wide_tiles() {
+    static const bool on = [] {
+        const char* e = getenv("QPS_ZGEMM_WIDE");
+        return e && !strcmp(e, "1");
+    }();
+    return on;
+}
+
 void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTask>& tasks, cudaStream_t s,
                    DBuf<GemmTask>& d_tasks, const char* family) {
     if (tasks.empty() || M <= 0 || N <= 0) return;
@@ -2497,9 +2506,9 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
         fprintf(stderr, "gemm %s M=%d N=%d K=%d nseg=%d tasks=%zu\n", nm, M, N, kmax, tasks[0].nseg, tasks.size());
     ProfScope ps(nm, s, fl, by, 0.0, int((tasks.size() + 65534) / 65535));
     if (!four_m) {
-        // tile by shape (tools/micro/gemm_cfg.cu on B200): 16 x 64 for thin
-        // products (M <= 48, or M <= 80 against a wide N), 32 x 32 for short K
-        // and small outputs (more CTAs, shorter prologue), 64 x 32 otherwise
+        // tile by shape (tools/micro/gemm_cfg.cu, gemm_cfg2.cu on B200): 16 x 64
+        // for thin products (M <= 48, or M <= 80 against a wide N), 32 x 32
+        // otherwise
         // in-place products (C aliasing B, M <= 64: the triangular-tile solves)
         // need every row of a column tile in one CTA -- the 64-row tile
         const bool inplace = tasks[0].C == tasks[0].B[0];
@@ -2520,7 +2529,11 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
             launch_z3<6, 2, 1, 4, 2, 2>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
         else if (M <= 48 || (M <= 80 && N >= 256))
             launch_z3<2, 2, 1, 4, 2, 4>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
-        else if (kmax <= 96 || (M <= 128 && N <= 128))
+        else if (kmax <= 96 || (M <= 128 && N <= 128) || !wide_tiles())
+            // 32 x 32 (4 CTAs per SM): with every task's operands in HBM it
+            // beats the 64 x 32 tile on every hot-path shape (tools/micro/
+            // gemm_cfg2.cu: 288^2 x 320 LU update 5.56 vs 5.94 ms, 608^2 x 160
+            // Schur update 12.85 vs 13.17 ms, 74-79 % of the DMMA peak)
             launch_z3<2, 2, 2, 2, 2, 4>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
         else
             launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
