@@ -1862,12 +1862,18 @@ __global__ void __launch_bounds__(kWpThreads, 1)
             for (int kk = 0; kk < kWpSub; ++kk)
                 lv[kk] = (kk < sw && p0 + kk < mystep) ? s[kk] : cplx{0, 0};
             cplx* dst = arow + size_t(p0 + sw) * ld;
-            constexpr int kLd = 4;  // columns' loads in flight, then their updates
+            constexpr int kLd = 4;  // a group of columns; the next group's loads fly during its updates
+            cplx an[kLd];
+#pragma unroll
+            for (int q = 0; q < kLd; ++q)
+                if (q < ncol) an[q] = dst[size_t(q) * ld];
             for (int t0 = 0; t0 < ncol; t0 += kLd) {
                 cplx a[kLd];
 #pragma unroll
+                for (int q = 0; q < kLd; ++q) a[q] = an[q];
+#pragma unroll
                 for (int q = 0; q < kLd; ++q)
-                    if (t0 + q < ncol) a[q] = dst[size_t(t0 + q) * ld];
+                    if (t0 + kLd + q < ncol) an[q] = dst[size_t(t0 + kLd + q) * ld];
 #pragma unroll
                 for (int q = 0; q < kLd; ++q) {
 #pragma unroll
