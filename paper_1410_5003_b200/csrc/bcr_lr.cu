@@ -2282,6 +2282,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         rhs.run(nb, one, one, gz);
     };
     int lvl = 0;
+    nvtxRangePushA("bcr_levels");  // the levels, final block and back substitution (ncu --nvtx-include)
     while (levels[lvl][0].size() > 1) {
         Level& cur = levels[lvl];
         const int sz = int(cur[0].size());
@@ -2454,6 +2455,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         rhs.run(r, one, zero, t1);
         rhs.run(nb, mone, one, t2);
     }
+    nvtxRangePop();
     tmark("backsub", lvl, 0);
     tl_mark(c, "backsub", s);
     if (trace) {
