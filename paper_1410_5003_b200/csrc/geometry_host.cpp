@@ -259,12 +259,31 @@ HostInterface build_interface(const qps_interface_spec& sp, double d, std::vecto
         g.segs.push_back(sd);
         g.smooth = true;
     }
+    // y range over the reference's 2049-point scan (geometry.hpp:449-460).  A
+    // sine attains the scan's extremes at the grid points next to its peaks and
+    // troughs (sin changes by ~1e-6 between neighbours there, far above
+    // rounding), so only those points and the ends are evaluated -- with the
+    // same expression, hence the same doubles as the full scan
     double ymin = std::numeric_limits<double>::infinity(), ymax = -ymin;
-    for (int k = 0; k <= 2048; ++k) {
+    auto probe = [&](int k) {
         const double x = -0.5 * d + d * k / 2048.0;
         const double y = spec_y_of_x(sp, d, x);
         ymin = std::min(ymin, y);
         ymax = std::max(ymax, y);
+    };
+    if (sp.shape == QPS_SHAPE_SINE) {
+        probe(0);
+        probe(2048);
+        // theta_k = 2 pi (k / 2048 - 1/2) + phase; extremes of sin at pi/2 + pi m
+        for (int m = -6; m <= 6; ++m) {
+            const double kc = ((0.5 * pi + pi * m - sp.phase) / (2.0 * pi) + 0.5) * 2048.0;
+            if (!(kc > -8.0 && kc < 2056.0)) continue;
+            const int k0 = int(std::floor(kc));
+            for (int k = k0 - 3; k <= k0 + 4; ++k)
+                if (k >= 0 && k <= 2048) probe(k);
+        }
+    } else {
+        for (int k = 0; k <= 2048; ++k) probe(k);
     }
     g.y_min = ymin;
     g.y_max = ymax;
@@ -354,18 +373,27 @@ HostGeometry build_geometry(const StackDesc& st, const Numerics& num) {
     g.py.resize(I + 1);
     g.pnx.resize(I + 1);
     g.pny.resize(I + 1);
+    // the circle's angles are the same for every layer: cos/sin once (the
+    // values are bit-identical to evaluating them per layer)
+    std::vector<double> pcos(num.P), psin(num.P);
+    for (int p = 0; p < num.P; ++p) {
+        const double ang = 2.0 * pi * p / num.P;
+        pcos[p] = std::cos(ang);
+        psin[p] = std::sin(ang);
+    }
     for (int i = 0; i <= I; ++i) {
         const double hi = (i == 0) ? g.y_U : g.ifaces[i - 1].y_max;
         const double lo = (i == I) ? g.y_D : g.ifaces[i].y_min;
         const double cx = 0.0, cy = 0.5 * (lo + hi);
         g.pc_x[i] = cx;
         g.pc_y[i] = cy;
+        g.pnx[i] = pcos;
+        g.pny[i] = psin;
+        g.px[i].resize(num.P);
+        g.py[i].resize(num.P);
         for (int p = 0; p < num.P; ++p) {
-            const double ang = 2.0 * pi * p / num.P;
-            g.pnx[i].push_back(std::cos(ang));
-            g.pny[i].push_back(std::sin(ang));
-            g.px[i].push_back(cx + num.R * std::cos(ang));
-            g.py[i].push_back(cy + num.R * std::sin(ang));
+            g.px[i][p] = cx + num.R * pcos[p];
+            g.py[i][p] = cy + num.R * psin[p];
         }
     }
     return g;

@@ -398,15 +398,22 @@ class Solver:
         self._check(self.lib.qps_set_refine(self.h, int(steps)))
 
     # ------------------------------------------------------------ outputs
-    def solution(self):
+    def solution(self, out=None):
+        """The last solve's Solution.  `out`: a previous result of this call
+        whose arrays are overwritten in place (repeated solves of one
+        configuration skip the allocation and first-touch of 10 MB)."""
         info = self.problem_info()
         ntot = 2 * sum(info["N"])
         nrb = 2 * info["K"] + 1
-        eta = np.zeros(ntot, dtype=np.complex128)
-        c = np.zeros((info["I"] + 1) * self.num.P, dtype=np.complex128)
-        aU = np.zeros(nrb, dtype=np.complex128)
-        aD = np.zeros(nrb, dtype=np.complex128)
-        lsq = np.zeros(info["I"] + 1)
+        if out is not None and out["eta_flat"].size == ntot and out["aU"].size == nrb and \
+                out["c"].size == (info["I"] + 1) * self.num.P:
+            eta, c, aU, aD, lsq = out["eta_flat"], out["c"], out["aU"], out["aD"], out["lsq_residual"]
+        else:
+            eta = np.zeros(ntot, dtype=np.complex128)
+            c = np.zeros((info["I"] + 1) * self.num.P, dtype=np.complex128)
+            aU = np.zeros(nrb, dtype=np.complex128)
+            aD = np.zeros(nrb, dtype=np.complex128)
+            lsq = np.zeros(info["I"] + 1)
         mx = C.c_double()
         self._check(self.lib.qps_get_solution(self.h, eta.ctypes.data, c.ctypes.data, aU.ctypes.data,
                                               aD.ctypes.data, _dptr(lsq), C.byref(mx)))
