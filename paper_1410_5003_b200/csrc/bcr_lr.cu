@@ -2463,13 +2463,15 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         QPS_CUDA(cudaEventDestroy(te1));
     }
     if (c.refine_ready) {
-        c.ref_nrm.ensure(3);
-        QPS_CUDA(cudaMemsetAsync(c.ref_nrm.p, 0, 3 * sizeof(double), s));
+        const size_t np3 = 3 * size_t(c.dims.nsys) * c.dims.I;  // per-block norms: r before, r after, f
+        c.ref_nrm.ensure(np3);
+        QPS_CUDA(cudaMemsetAsync(c.ref_nrm.p, 0, np3 * sizeof(double), s));
         for (int it = 0; it < c.refine_used; ++it) wb_refine_step(c, Ad, it == 0 ? 0 : -1, true);
         static const bool check = getenv("QPS_REFINE_CHECK") != nullptr;  // residual after the last step too
         if (check) wb_refine_step(c, Ad, 1, false);
-        c.ref_nrm_h.ensure(3);
-        QPS_D2H(c.ref_nrm_h.p, c.ref_nrm.p, 3 * sizeof(double), s);  // read after the solve's final sync
+        c.ref_nrm_h.ensure(np3);
+        QPS_D2H(c.ref_nrm_h.p, c.ref_nrm.p, np3 * sizeof(double), s);  // combined after the solve's final sync
+        c.ref_nrm_n = int(np3 / 3);
         tl_mark(c, "refine", s);
     }
     c.refine_ready = false;
@@ -2506,7 +2508,8 @@ void wb_refine_step(Ctx& c, cplx* Ad, int slot, bool apply) {
     } else {
         QPS_CUDA(cudaMemcpyAsync(R, c.ref_F.p, sizeof(cplx) * npos * fs, cudaMemcpyDeviceToDevice, s));
     }
-    if (slot == 0) batched_fro(R, int(npos * fs), 1, int(npos * fs), 0, 1, c.ref_nrm.p + 2, s);  // ||f||
+    // norms per block (one CTA each; combined on the host by the diagnostics)
+    if (slot == 0) batched_fro(R, nb, m, nb, fs, npos, c.ref_nrm.p + 2 * size_t(npos), s);  // ||f||
     // r -= A' eta: D_j eta_j + L_j eta_{j-1} (one two-segment product), U_j eta_{j+1},
     // then the deferred proxy terms + Bc (X eta) of both couplings
     std::vector<GemmTask> t1, t2, tx, tb;
@@ -2555,7 +2558,7 @@ void wb_refine_step(Ctx& c, cplx* Ad, int slot, bool apply) {
         rx.run(P, one, zero, tx);
         rhs.run(nb, one, one, tb);
     }
-    if (slot >= 0) batched_fro(R, int(npos * fs), 1, int(npos * fs), 0, 1, c.ref_nrm.p + slot, s);
+    if (slot >= 0) batched_fro(R, nb, m, nb, fs, npos, c.ref_nrm.p + size_t(slot) * npos, s);
     if (!apply) return;
     // replay: level 0, delta_j = D_j^{-1} r_j with the kept LU factors
     {

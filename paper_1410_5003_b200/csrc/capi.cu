@@ -676,9 +676,14 @@ int qps_solver_diagnostics(const qps_ctx* h, qps_solver_diag* d) {
     d->lr_rank_max = h->c.lr_rank_max;
     d->lr_probe_worst = h->c.lr_probe_worst;
     d->refine_steps = h->c.refine_used;
-    const double fn = h->c.refine_used && h->c.ref_nrm_h[2] > 0 ? h->c.ref_nrm_h[2] : 0.0;
-    d->refine_res0 = fn > 0 ? h->c.ref_nrm_h[0] / fn : 0.0;
-    d->refine_res1 = fn > 0 ? h->c.ref_nrm_h[1] / fn : 0.0;
+    double nr[3] = {0, 0, 0};  // sqrt of the sums of the per-block squared norms
+    const int nbk = h->c.refine_used ? h->c.ref_nrm_n : 0;
+    for (int q = 0; q < 3; ++q) {
+        for (int b = 0; b < nbk; ++b) nr[q] += h->c.ref_nrm_h[size_t(q) * nbk + b] * h->c.ref_nrm_h[size_t(q) * nbk + b];
+        nr[q] = std::sqrt(nr[q]);
+    }
+    d->refine_res0 = nr[2] > 0 ? nr[0] / nr[2] : 0.0;
+    d->refine_res1 = nr[2] > 0 ? nr[1] / nr[2] : 0.0;
     return QPS_OK;
 }
 

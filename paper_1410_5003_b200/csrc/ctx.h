@@ -291,11 +291,12 @@ struct Ctx {
     int refine = -1;                   // -1: the default of the caller (refine_default)
     int refine_default = 0;            // 1 inside the sweeps
     int refine_used = 0;               // steps applied by the last block solve
-    HBuf<double> ref_nrm_h;            // host copy of ref_nrm (relative)
+    HBuf<double> ref_nrm_h;            // host copy of ref_nrm
+    int ref_nrm_n = 0;                 // blocks per slot of ref_nrm
     bool refine_ready = false;         // ref_D / ref_F hold this solve's copies
     const cplx *ref_Au = nullptr, *ref_Al = nullptr;  // the couplings of the solve being refined
     DBuf<cplx> ref_D, ref_F, ref_R, ref_X, ref_A;
-    DBuf<double> ref_nrm;              // ||r_before||, ||r_after||, ||f|| of the last refinement
+    DBuf<double> ref_nrm;              // per-block ||r_before||, ||r_after||, ||f|| of the last refinement
     std::vector<std::vector<std::vector<WbPos>>> wb_levels;
     std::chrono::steady_clock::time_point host_t0;  // QPS_HOST_TRACE
     DBuf<PairTask> d_pair;
