@@ -2474,6 +2474,8 @@ bool thin48_off() {  // QPS_ZGEMM_THIN48=0: 16-row tiles for 48-row products (A/
 }
 }  // namespace
 
+constexpr int kThinN = 8;  // products with N <= 8 use the 128 x 8 tile
+
 // QPS_ZGEMM_WIDE=1: the 64 x 32 tile for large K and outputs (the round-1 rule, A/B)
 bool wide_tiles() {
     static const bool on = [] {
@@ -2522,7 +2524,12 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
             const char* e = getenv("QPS_ZGEMM_TILE");
             return e && !strcmp(e, "fixed");
         }();
-        if (inplace || fixed_tile) {
+        if (N <= kThinN && !fixed_tile) {
+            // narrow right-hand-side groups: 128 x 8 tiles (one N tile; in place
+            // too, every row of a column tile stays in one CTA)
+            if (inplace && M > 128) fail(QPS_ERR_INTERNAL, "zgemm_batched: in-place product taller than one tile");
+            launch_z3<4, 1, 4, 1, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+        } else if (inplace || fixed_tile) {
             if (inplace && M > 64) {
                 fprintf(stderr, "zgemm_batched: in-place M=%d N=%d K=%d ntasks=%zu nseg=%d\n", M, N, tasks[0].K[0],
                         tasks.size(), tasks[0].nseg);
@@ -3174,6 +3181,10 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
     }
     auto& tasks = ws.h_gemm;
     // leaf: B[k0:kend] <- inverse tile * B[k0:kend] (in place, <= 64 rows)
+    // column groups: the multiple of 32 (full N tiles of the 32 x 32 GEMM
+    // tile) and a narrow remainder (<= 8 columns: the 128 x 8 tile), instead of
+    // a last 32-wide tile mostly empty (e.g. 101 = 96 + 5 level-0 right-hand sides)
+    int cb0 = 0, cb1 = nrhs;  // the group being solved
     auto leaf = [&](int bi, int which) {
         const int k0 = bi * kTB, kend = std::min(k0 + kTB, n);
         tasks.assign(count, GemmTask{});
@@ -3182,13 +3193,13 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
             t.nseg = 1;
             t.A[0] = hDinv[b] + size_t(bi) * 2 * kTB * kTB + (which ? size_t(kTB) * kTB : 0);
             t.lda[0] = kTB;
-            t.B[0] = hB[b] + k0;
+            t.B[0] = hB[b] + size_t(cb0) * ldb + k0;
             t.ldb[0] = ldb;
             t.K[0] = kend - k0;
-            t.C = hB[b] + k0;
+            t.C = hB[b] + size_t(cb0) * ldb + k0;
             t.ldc = ldb;
         }
-        zgemm_batched(kend - k0, nrhs, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
+        zgemm_batched(kend - k0, cb1 - cb0, cplx{1, 0}, cplx{0, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
     };
     auto update = [&](int M, int K, size_t aoff, int brow, int crow) {
         tasks.assign(count, GemmTask{});
@@ -3197,13 +3208,13 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
             t.nseg = 1;
             t.A[0] = hA[b] + aoff;
             t.lda[0] = ld;
-            t.B[0] = hB[b] + brow;
+            t.B[0] = hB[b] + size_t(cb0) * ldb + brow;
             t.ldb[0] = ldb;
             t.K[0] = K;
-            t.C = hB[b] + crow;
+            t.C = hB[b] + size_t(cb0) * ldb + crow;
             t.ldc = ldb;
         }
-        zgemm_batched(M, nrhs, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
+        zgemm_batched(M, cb1 - cb0, cplx{-1, 0}, cplx{1, 0}, tasks, s, ws.gemm_tasks, "lu_gemm");
     };
     // recursive triangular solves on 64-aligned splits: the top levels carry most
     // flops as GEMMs with K = n/2, n/4, ...
@@ -3224,8 +3235,18 @@ void lu_solve_batched(int n, int ld, const std::vector<cplx*>& hA, const std::ve
         upper(b0, bm);
     };
     const int nblk = (n + kTB - 1) / kTB;
+    const int rem = nrhs % 32;
+    const int nmain = (rem >= 1 && rem <= kThinN && nrhs > 32) ? nrhs - rem : nrhs;
+    cb0 = 0;
+    cb1 = nmain;
     lower(0, nblk);
     upper(0, nblk);
+    if (nmain < nrhs) {
+        cb0 = nmain;
+        cb1 = nrhs;
+        lower(0, nblk);
+        upper(0, nblk);
+    }
 }
 
 void lu_rcond_batched(int n, int ld, cplx* const* d_ptrs, const cplx* base, size_t stride, cplx* const* d_dinv,
