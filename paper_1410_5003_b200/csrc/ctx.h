@@ -37,6 +37,7 @@ struct CodSet {
     DBuf<int> perm, nzp, rank, flags;
     DBuf<double> maxpiv, xmax, rmax, enorm, rnorm, parts;
     DBuf<GemmTask> tasks1, tasks2;  // task tables of this family's GEMMs (families run on separate streams)
+    DBuf<GemmTask> trsm_tasks;      // the blocked back substitution's device-built tasks
     HBuf<double> h_rmax, h_xmax, h_enorm, h_rnorm;  // pinned: read back without blocking the host
     cudaEvent_t ev = nullptr;                        // last read-back of this family
     ~CodSet() {
@@ -47,6 +48,7 @@ struct CodSet {
         b.count = count; b.m = m; b.p = p; b.Q = Q;
         b.W = W.p; b.V = V.p; b.tau = tau.p; b.zc = zc.p; b.perm = perm.p; b.nzp = nzp.p;
         b.maxpiv = maxpiv.p; b.rank = rank.p; b.QH = QH.p; b.Wz = Wz.p; b.M1 = M1.p; b.Y = Y.p;
+        b.trsm_tasks = trsm_tasks.p;
         return b;
     }
     void ensure(int cnt, int m_, int p_, int ncols_) {
@@ -56,6 +58,7 @@ struct CodSet {
         Wz.ensure(size_t(cnt) * p * p); Tb.ensure(size_t(cnt) * p * ncols);
         tau.ensure(size_t(cnt) * p); zc.ensure(size_t(cnt) * p); perm.ensure(size_t(cnt) * p);
         nzp.ensure(cnt); rank.ensure(cnt); flags.ensure(cnt);
+        trsm_tasks.ensure(size_t(cnt) * ((p + 15) / 16));
         maxpiv.ensure(cnt); xmax.ensure(cnt); rmax.ensure(cnt); enorm.ensure(cnt); rnorm.ensure(cnt);
         h_rmax.ensure(cnt); h_xmax.ensure(cnt); h_enorm.ensure(cnt); h_rnorm.ensure(cnt);
         if (!ev) QPS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));

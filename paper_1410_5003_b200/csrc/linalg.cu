@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     }
     cp_async_wait<0>();
     const bool use_beta = (beta.re != 0.0 || beta.im != 0.0);
+    const int Mt = T.mlim == 0 ? M : (T.mlim > 0 ? min(M, T.mlim) : 0);
     double ss = 0.0;
 #pragma unroll
     for (int i = 0; i < WMT; ++i)
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             for (int e = 0; e < 2; ++e) {
                 const int row = m0 + wm + 8 * i + (lane >> 2);
                 const int col = n0 + wn + 8 * j + 2 * (lane & 3) + e;
-                if (row < M && col < N) {
+                if (row < Mt && col < N) {
                     const double P = acc[0][i][j][e], Q = acc[1][i][j][e], S = acc[2][i][j][e];
                     const double vr = P - Q, vi = S - P - Q;
                     cplx out{alpha.re * vr - alpha.im * vi, alpha.re * vi + alpha.im * vr};
@@ -1118,6 +1119,77 @@ __global__ void __launch_bounds__(256) cod_trsm_blk_kernel(CodBatch b, cplx* B, 
         const int i = e % r, j = e / r;
         Bp[size_t(j) * ldb + i] = X[j * lx + i];
     }
+}
+
+// Blocked back substitution (LAPACK xTRSM order, left-looking from the bottom
+// in 16-row blocks aligned to each problem's rank r): block s covers rows
+// [lo, hi), hi = r - 16 s, lo = max(0, hi - 16); its rows first take the
+// product of the rows already solved below (a batched DMMA GEMM, tasks built
+// on the device from the ranks), then the 16 x 16 diagonal block is solved by
+// substitution, one thread per right-hand-side column.
+__global__ void cod_trsm_tasks_kernel(CodBatch b, cplx* B, int ldb, size_t stride, const int* __restrict__ flags,
+                                      int nsteps) {
+    const int pb = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pb >= b.count) return;
+    const int m = b.m, r = b.rank[pb];
+    const bool on = !flags || flags[pb];
+    const cplx* V = b.V + size_t(pb) * m * b.p;
+    cplx* Bp = B + stride * pb;
+    for (int st = 0; st < nsteps; ++st) {
+        const int hi = r - 16 * st, lo = max(0, hi - 16);
+        const bool act = on && hi > 0 && st > 0;
+        GemmTask t{};
+        t.nseg = 1;
+        t.A[0] = V + size_t(act ? hi : 0) * m + (act ? lo : 0);
+        t.lda[0] = m;
+        t.B[0] = Bp + (act ? hi : 0);
+        t.ldb[0] = ldb;
+        t.K[0] = act ? r - hi : 0;
+        t.C = Bp + (act ? lo : 0);
+        t.ldc = ldb;
+        t.mlim = act ? hi - lo : -1;
+        b.trsm_tasks[size_t(st) * b.count + pb] = t;
+    }
+}
+__global__ void __launch_bounds__(128) cod_trsm_diag_kernel(CodBatch b, cplx* B, int ldb, size_t stride, int ncols,
+                                                            const int* __restrict__ flags, int st) {
+    const int pb = blockIdx.y;
+    if (flags && !flags[pb]) return;
+    const int m = b.m, r = b.rank[pb];
+    const int hi = r - 16 * st, lo = max(0, hi - 16), h = hi - lo;
+    if (hi <= 0) return;
+    __shared__ cplx Tb[16][17];
+    __shared__ cplx Ti[16];
+    const cplx* V = b.V + size_t(pb) * m * b.p;
+    for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+        const int i = e & 15, j = e >> 4;
+        Tb[i][j] = (i <= j && j < h) ? V[size_t(lo + j) * m + lo + i] : cplx{0, 0};
+    }
+    __syncthreads();
+    if (threadIdx.x < h) Ti[threadIdx.x] = cdiv(cplx{1.0, 0.0}, Tb[threadIdx.x][threadIdx.x]);
+    __syncthreads();
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncols) return;
+    cplx* x = B + stride * pb + size_t(c) * ldb + lo;
+    cplx v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = i < h ? x[i] : cplx{0, 0};
+#pragma unroll
+    for (int i = 15; i >= 0; --i) {
+        if (i < h) {
+            cplx a = v[i];
+#pragma unroll
+            for (int l = i + 1; l < 16; ++l) {  // T[i][l] = 0 beyond h
+                const cplx t = Tb[i][l];
+                a.re -= t.re * v[l].re - t.im * v[l].im;
+                a.im -= t.re * v[l].im + t.im * v[l].re;
+            }
+            v[i] = cmul(a, Ti[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        if (i < h) x[i] = v[i];
 }
 
 template <bool kSmem>
@@ -2669,11 +2741,23 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
     const dim3 grid((ncols + 127) / 128, b.count);
     const size_t shc = (size_t(b.p) * b.p + size_t(b.p) * kTrsmCols + b.p) * sizeof(cplx);
     const size_t shb = (size_t(b.p) * (b.p + 1) / 2 + size_t(b.p + 1) * kTrsmBlkCols + b.p) * sizeof(cplx);
-    static const bool unblocked = [] {  // QPS_COD_TRSM=row: the row-by-row kernel
-        const char* e = getenv("QPS_COD_TRSM");
-        return e && !strcmp(e, "row");
-    }();
-    if (!unblocked && shb <= 110 * 1024) {
+    static const char* mode = getenv("QPS_COD_TRSM");  // row: row-by-row kernel; blk: one-kernel blocked (A/B)
+    const bool unblocked = mode && !strcmp(mode, "row");
+    const bool onekernel = mode && !strcmp(mode, "blk");
+    if (!unblocked && !onekernel && b.trsm_tasks && b.count >= 64) {
+        // many problems: left-looking 16-row blocks, GEMMs on the DMMA pipe
+        const int nst = (b.p + 15) / 16;
+        { QPS_NOTE_LAUNCH(); cod_trsm_tasks_kernel<<<(b.count + 127) / 128, 128, 0, s>>>(b, B, ldb, stride, flags, nst); }
+        QPS_CUDA(cudaGetLastError());
+        for (int st = 0; st < nst; ++st) {
+            if (st > 0)
+                launch_z3<2, 2, 1, 4, 2, 4>(16, ncols, cplx{-1, 0}, cplx{1, 0}, b.trsm_tasks + size_t(st) * b.count,
+                                           b.count, s);
+            { QPS_NOTE_LAUNCH(); cod_trsm_diag_kernel<<<dim3((ncols + 127) / 128, b.count), 128, 0, s>>>(
+                b, B, ldb, stride, ncols, flags, st); }
+            QPS_CUDA(cudaGetLastError());
+        }
+    } else if (!unblocked && shb <= 110 * 1024) {
         static bool attr = false;
         if (!attr) {
             QPS_CUDA(cudaFuncSetAttribute(cod_trsm_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

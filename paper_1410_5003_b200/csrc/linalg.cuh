@@ -21,6 +21,7 @@ struct GemmTask {
     int nseg;
     cplx* C;
     int ldc;
+    int mlim;  // rows of C written: 0 = all M, > 0 = the first mlim, < 0 = none (device-built tasks)
 };
 
 struct Workspace;  // forward
@@ -52,6 +53,7 @@ struct CodBatch {
     cplx* Wz = nullptr;       // count x (p*p): P Z^* [I_r; 0] (cols >= rank zero), ld p
     cplx* M1 = nullptr;       // count x (m*p) scratch
     cplx* Y = nullptr;        // count x (p*m) scratch
+    GemmTask* trsm_tasks = nullptr;  // count x ceil(p/16) device-built tasks of the blocked cod_trsm
 };
 // rows 0..rank_b-1 of B_b (p x ncols, ld ldb, stride) <- T11_b^{-1} B_b, T11 in
 // the RZ-reduced factor V_b (ld m): the backward-stable triangular step of the
