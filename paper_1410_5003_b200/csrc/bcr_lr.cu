@@ -885,6 +885,68 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const cplx* const* __r
     }
 }
 
+// ---------------------------------------------------------------------------
+// Sparse sign sketch: Y = alpha C Omega with Omega (ncols x 64) holding
+// kSkZeta = 8 entries +-1 per row (each source column of C is added, with a
+// sign, to 8 of the 64 sample columns).  Replaces the dense Gaussian sample
+// GEMM of the range finder: C is read once (HBM-bound) instead of 6 M N K
+// tensor flops (a sparse sign map captures the couplings' range as the
+// Gaussian one does: tools/sparse_sketch_check.py).  Omega is stored per
+// sample column as (source column, sign) lists sorted by source column; a CTA
+// covers 32 rows of one task, stages its source columns through shared memory
+// 64 at a time (each read once), and warp w sums sample columns 8w..8w+7 in
+// registers (each lane its own row).
+// ---------------------------------------------------------------------------
+constexpr int kSkCols = 64, kSkZeta = 8, kSkChunk = 64;
+constexpr size_t kSkSmem = size_t(kSkChunk) * 33 * sizeof(cplx);
+// col_ptr[j * (nchunks + 1) + c]: first entry of sample column j whose source
+// column is >= c * kSkChunk; entries packed ((source mod kSkChunk) * 33 << 1) | negative
+__global__ void __launch_bounds__(256) sparse_sketch_kernel(const cplx* const* __restrict__ src,
+                                                            const int* __restrict__ lds, int M, int ncols,
+                                                            const int* __restrict__ col_ptr,
+                                                            const int* __restrict__ ent, cplx alpha,
+                                                            cplx* __restrict__ Y, int ldy, size_t ystride) {
+    extern __shared__ cplx sk_sm[];  // staged source columns [kSkChunk][33] (32 rows + pad)
+    const int q = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int r0 = blockIdx.x * 32;
+    const cplx* A = src[q];
+    const size_t ld = size_t(lds[q]);
+    const int nch = (ncols + kSkChunk - 1) / kSkChunk;
+    cplx acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = cplx{0, 0};
+    for (int ch = 0; ch < nch; ++ch) {
+        const int c0 = ch * kSkChunk, cn = min(kSkChunk, ncols - c0);
+        // each source column of the chunk read once (32 rows: 512 B per column)
+#pragma unroll
+        for (int u = 0; u < 32 * kSkChunk / 256; ++u) {
+            const int e = tid + 256 * u, i = e >> 5, rr = e & 31;
+            sk_sm[i * 33 + rr] = (i < cn && r0 + rr < M) ? A[size_t(c0 + i) * ld + r0 + rr] : cplx{0, 0};
+        }
+        __syncthreads();
+        // warp w: sample columns 8 w .. 8 w + 7, lane: row
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = 8 * w + k;
+            const int e0 = col_ptr[j * (nch + 1) + ch], e1 = col_ptr[j * (nch + 1) + ch + 1];
+            // entries: (staged row offset << 1) | negative (offset precomputed on the host)
+            for (int e = e0; e < e1; ++e) {
+                const int pk = ent[e];
+                const cplx v = sk_sm[(pk >> 1) + lane];
+                acc[k].re += (pk & 1) ? -v.re : v.re;
+                acc[k].im += (pk & 1) ? -v.im : v.im;
+            }
+        }
+        __syncthreads();
+    }
+    const int row = r0 + lane;
+    if (row < M) {
+        cplx* y = Y + size_t(q) * ystride + row;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) y[size_t(8 * w + k) * ldy] = cmul(alpha, acc[k]);
+    }
+}
+
 GemmTask gemm1(const cplx* A, int lda, const cplx* B, int ldb, int K, cplx* C, int ldc) {
     GemmTask t{};
     t.nseg = 1;
@@ -928,7 +990,65 @@ void lr_omega_setup(Ctx& c, cudaStream_t s) {
         z = cplx{next(), next()};
     }
     c.lr_omega.upload(om, s);
+    // the sparse sign sketch: kSkZeta distinct sample columns per source
+    // column, random signs (seeded, fixed), listed per sample column
+    std::vector<std::vector<int>> colent(kSkCols);
+    uint64_t y = 0x853c49e6748fea9bull;
+    auto rnd = [&]() {
+        y ^= y >> 12;
+        y ^= y << 25;
+        y ^= y >> 27;
+        return (y * 0x2545f4914f6cdd1dull) >> 33;
+    };
+    for (int i = 0; i < nb; ++i) {
+        int cols[kSkCols];
+        for (int j = 0; j < kSkCols; ++j) cols[j] = j;
+        for (int t = 0; t < kSkZeta; ++t) {  // partial Fisher-Yates: kSkZeta distinct columns
+            const int j = t + int(rnd() % uint64_t(kSkCols - t));
+            std::swap(cols[t], cols[j]);
+            colent[cols[t]].push_back(((i % kSkChunk) * 33 << 1) | int(rnd() & 1u) | ((i / kSkChunk) << 20));
+        }
+    }
+    const int nch = (nb + kSkChunk - 1) / kSkChunk;
+    std::vector<int> ptr(size_t(kSkCols) * (nch + 1)), ent;
+    for (int j = 0; j < kSkCols; ++j) {  // entries sorted by source column (generated in order)
+        const int base = int(ent.size());
+        for (int ch = 0; ch <= nch; ++ch) {  // chunk index parked in bits 20.. while sorting out the ranges
+            int k = 0;
+            while (k < int(colent[j].size()) && (colent[j][k] >> 20) < ch) ++k;
+            ptr[size_t(j) * (nch + 1) + ch] = base + k;
+        }
+        for (int v : colent[j]) ent.push_back(v & ((1 << 20) - 1));
+    }
+    c.lr_sk_ptr.upload(ptr, s);
+    c.lr_sk_ent.upload(ent, s);
     c.lr_omega_n = nb;
+}
+
+// QPS_LR_SKETCH=dense: the dense Gaussian sample GEMM (A/B)
+bool sparse_sketch_on() {
+    static const bool dense = [] {
+        const char* e = getenv("QPS_LR_SKETCH");
+        return e && !strcmp(e, "dense");
+    }();
+    return !dense;
+}
+
+// Y_q = alpha C_q Omega for every task (C_q: M rows, ld ld_q), 64 columns
+void sparse_sketch(Ctx& c, const std::vector<const cplx*>& src, const std::vector<int>& ld, int M, cplx alpha,
+                   cplx* Y, int ldy, size_t ystride, DBuf<const cplx*>& pbuf, DBuf<int>& lbuf, cudaStream_t s) {
+    if (src.empty()) return;
+    pbuf.upload(src, s);
+    lbuf.upload(ld, s);
+    ProfScope ps("lr_sketch", s, 0.0, 16.0 * double(src.size()) * M * c.dims.nb);
+    static bool attr = false;
+    if (!attr) {
+        QPS_CUDA(cudaFuncSetAttribute(sparse_sketch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSkSmem)));
+        attr = true;
+    }
+    { QPS_NOTE_LAUNCH(); sparse_sketch_kernel<<<dim3((M + 31) / 32, unsigned(src.size())), 256, kSkSmem, s>>>(
+        pbuf.p, lbuf.p, M, c.dims.nb, c.lr_sk_ptr.p, c.lr_sk_ent.p, alpha, Y, ldy, ystride); }
+    QPS_CUDA(cudaGetLastError());
 }
 bool lr_eligible(const Ctx& c) {
     static const bool dense_only = [] {
@@ -954,18 +1074,24 @@ void lr_sample_async(Ctx& c) {
     lr_omega_setup(c, c.side2);
     c.lr_Y.ensure(size_t(nc) * nb * kLrCols);
     std::vector<GemmTask> t(nc);
+    std::vector<const cplx*> srcs(nc);
     for (int q = 0; q < nc; ++q) {
         const int a = q / (2 * (I - 1)), rem = q % (2 * (I - 1));
         const bool sup = rem >= I - 1;
         const int j = sup ? rem - (I - 1) : rem;
         const cplx* C = (sup ? c.Asup.p : c.Asub.p) + size_t(a) * D.sU() + size_t(j) * D.nb2();
         t[q] = gemm1(C, nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrCols, nb);
+        srcs[q] = C;
     }
     {
         ProfPhase phase("lowrank");
         // own family: its events on the low-priority stream span its overlap
         // with the Schur chain, so the duration is not a kernel time
-        zgemm_batched(nb, kLrCols, cplx{1, 0}, cplx{0, 0}, t, c.side2, c.lr_tasks, "lr_sample");
+        if (sparse_sketch_on())
+            sparse_sketch(c, srcs, std::vector<int>(nc, nb), nb, cplx{1, 0}, c.lr_Y.p, nb, size_t(nb) * kLrCols,
+                          c.lr_skp, c.lr_skl, c.side2);
+        else
+            zgemm_batched(nb, kLrCols, cplx{1, 0}, cplx{0, 0}, t, c.side2, c.lr_tasks, "lr_sample");
     }
     QPS_CUDA(cudaEventRecord(c.ev_sample, c.side2));
     c.lr_sample_pending = true;
@@ -1054,11 +1180,18 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         if (corr) {
             c.lr_W.ensure(size_t(nc) * P * kLrCols);
             std::vector<GemmTask> w(nc);
+            std::vector<const cplx*> xs(nc);
+            std::vector<int> xl(nc);
             for (int q = 0; q < nc; ++q) {
                 const GemmTask& u = corr_task(q);
                 w[q] = gemm1(u.B[0], u.ldb[0], c.lr_omega.p, nb, nb, c.lr_W.p + size_t(q) * P * kLrCols, P);
+                xs[q] = u.B[0];
+                xl[q] = u.ldb[0];
             }
-            zgemm_batched(P, kLrCols, cplx{-1, 0}, cplx{0, 0}, w, s, c.ws.gemm_tasks, "lr_compress");
+            if (sparse_sketch_on())
+                sparse_sketch(c, xs, xl, P, cplx{-1, 0}, c.lr_W.p, P, size_t(P) * kLrCols, c.lr_skp, c.lr_skl, s);
+            else
+                zgemm_batched(P, kLrCols, cplx{-1, 0}, cplx{0, 0}, w, s, c.ws.gemm_tasks, "lr_compress");
         }
         for (int q = 0; q < nc && early; ++q) {  // Y += Bc (-X Omega)
             const GemmTask& u = corr_task(q);
@@ -1066,7 +1199,20 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
                          c.lr_Y.p + size_t(q) * nb * kLrCols, nb);
         }
         if (early) zgemm_batched(nb, kLrCols, cplx{1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
-        for (int q = 0; q < nc && !early; ++q) {
+        if (!early && sparse_sketch_on()) {
+            // Y = C Omega (sparse), then Y += Bc (-X Omega)
+            std::vector<const cplx*> cs(nc);
+            for (int q = 0; q < nc; ++q) cs[q] = coupling(q);
+            sparse_sketch(c, cs, std::vector<int>(nc, nb), nb, cplx{1, 0}, c.lr_Y.p, nb, size_t(nb) * kLrCols,
+                          c.lr_skp, c.lr_skl, s);
+            for (int q = 0; q < nc && corr; ++q) {
+                const GemmTask& u = corr_task(q);
+                t[q] = gemm1(u.A[0], u.lda[0], c.lr_W.p + size_t(q) * P * kLrCols, P, P,
+                             c.lr_Y.p + size_t(q) * nb * kLrCols, nb);
+            }
+            if (corr) zgemm_batched(nb, kLrCols, cplx{1, 0}, cplx{1, 0}, t, s, c.ws.gemm_tasks, "lr_compress");
+        }
+        for (int q = 0; q < nc && !early && !sparse_sketch_on(); ++q) {
             t[q] = gemm1(coupling(q), nb, c.lr_omega.p, nb, nb, c.lr_Y.p + size_t(q) * nb * kLrCols, nb);
             if (corr) {
                 const GemmTask& u = corr_task(q);
@@ -1078,7 +1224,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
                 t[q].K[1] = P;
             }
         }
-        if (!early) {
+        if (!early && !sparse_sketch_on()) {
             if (getenv("QPS_TRACE_LAUNCH"))
                 fprintf(stderr, "lr_compress sample GEMM is zgemm3m launch index %llu\n",
                         (unsigned long long)g_zgemm_launches.load());

@@ -188,6 +188,9 @@ struct Ctx {
     // ---- low-rank couplings (bcr_lr.cu) ----
     DBuf<cplx> lr_omega, lr_Y, lr_P, lr_PH, lr_R, lr_core, lr_T, lr_vec, lr_W, lr_G;
     DBuf<cplx> lr_L1i;                 // row ID: inverse unit-lower L1 = L[I, :] per coupling (r x r)
+    DBuf<int> lr_sk_ptr, lr_sk_ent;    // sparse sign sketch (per 8-column slice: packed column/slot/sign)
+    DBuf<const cplx*> lr_skp;          // sketch source pointers
+    DBuf<int> lr_skl;                  // sketch source leading dimensions
     DBuf<int> lr_piv, lr_rank_d;       // row ID: skeleton rows I (r per coupling); sample ranks
     DBuf<cplx> lr_V, lr_VH, lr_Tq, lr_THq, lr_W1, lr_W2, lr_R64, lr_Q2, lr_Q2H;  // blocked QR of the samples
     int lr_omega_n = 0, lr_r = 0;
