@@ -3,15 +3,20 @@
 // The off-diagonal blocks of the periodized system, A'_{j,j+1} and A'_{j+1,j}
 // (interface-to-interface interactions across one layer, minus the rank-P
 // proxy correction), are numerically low rank: at config 4 (interfaces one
-// period apart, k up to 30) their singular values fall below 1e-15 of the
-// largest after ~35 of 600 (tools/coupling_rank.py).  Each coupling is
-// compressed once, C ~= P (P^* C) with P an orthonormal n x r basis from a
-// randomized range finder (C Omega, Omega n x 64) and column-pivoted QR of the
-// sample (the Eigen-semantics CPQR kernel, rank at a relative 1e-14), r the
-// fixed basis width (48 columns, more than any coupling's rank).
+// period apart, k up to 30) their singular values fall to the fill's rounding
+// (~6e-16 of the largest) after ~35 of 600 (tools/coupling_rank.py).  Each
+// coupling is compressed once from a sample Y = C Omega (Omega a 64-column
+// sparse sign map, sparse_sketch_kernel) by a randomized row interpolative
+// decomposition (lr_id_kernel): C ~= L (L1^{-1} C[I, :]) with the r = 48
+// skeleton rows I of an LU with partial pivoting of Y, L its unit-lower factor
+// (|L| <= 1), rank test at a relative pivot of 1e-12 (rank > 48 -> dense
+// reduction) and an a-posteriori probe on 16 random columns (1e-12).
+// (QPS_LR_ID=0 keeps the orthonormal form C ~= P (P^* C) from a blocked
+// Householder QR and column-pivoted QR of the sample, rank at 1e-14.)
 //
 // Cyclic reduction then never forms a dense D^{-1} L or D^{-1} U: with
-// L = P_L R_L and U = P_U R_U (R = P^* C, r x n) an odd elimination needs
+// L = P_L R_L and U = P_U R_U (P the left factor, R the r x n right factor) an
+// odd elimination needs
 //   Z = D_o^{-1} [P_L P_U]                   (n x 2r solve instead of n x 2n)
 //   D_e -= P_L (R_L Z_U) R_U + P_U (R_U Z_L) R_L       (rank-r updates)
 //   L'_e = P_L (-(R_L Z_L) R_L(o))  U'_e = P_U (-(R_U Z_U) R_U(o))
@@ -19,9 +24,9 @@
 // right factor, and the work per elimination drops from 50.7 n^3 to about
 // n^3 (8/3 + 32 r/n) real flops -- the LU of D_o dominates.  Back-substitution:
 //   eta_o = z_o - Z_L (R_L(o) eta_{o-1}) - Z_U (R_U(o) eta_{o+1}).
-// The truncation error (relative 1e-14 of each coupling) is far below the
-// problem's own noise floor; systems whose couplings are not low rank
-// (rank > 48 of a 64-column sample) take the dense cyclic reduction.
+// The default solve (bcr_solve_wb) runs this through the Woodbury identity:
+// every diagonal block is LU-factored once at level 0 and the deeper levels
+// only solve 2r x 2r capacitance systems.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -63,7 +68,7 @@ int lr_basis() {
     }();
     return b;
 }
-constexpr double kLrTol = 1e-14; // relative pivot threshold of the sample's CPQR
+constexpr double kLrTol = 1e-14; // relative pivot threshold of the sample's CPQR (QPS_LR_ID=0 path)
 // row ID: relative pivot threshold of the sample's LU.  The couplings' singular
 // values level off at the fill's rounding (~6e-16 of the largest) and the LU
 // pivots of that noise at ~1e-14; the a-posteriori probe tolerance is 1e-12
