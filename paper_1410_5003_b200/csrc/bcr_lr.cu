@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict_
         double v = 0;
         for (int jj = tid >> 5; jj < N; jj += 4 * N / 32) {
             double cs = 0;
-            for (int i = tid & 31; i < N; i += 32) cs += hypot(Cb[size_t(jj) * N + i].re, Cb[size_t(jj) * N + i].im);
+            for (int i = tid & 31; i < N; i += 32) cs += sqrt(cabs2(Cb[size_t(jj) * N + i]));  // |z| (no hypot: magnitudes are tame)
             for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
             v = fmax(v, cs);
         }
@@ -2349,6 +2349,22 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
     const size_t rr = size_t(r) * r, rn = size_t(r) * nb;
     // eliminate the listed blocks at level lvl (updated ones through their
     // capacitance matrix); sets Z and overwrites F with z = D^{-1} f
+    // the right-hand-side half of every level (u = y - W g, a = S u,
+    // z = u + Z a, g += R z) runs on the side stream, one level behind the
+    // factor half that only the next level's factors depend on: the deep
+    // levels' latency-bound launches of the two halves overlap
+    static const bool rhs_side_off = [] {  // QPS_WB_RHS_STREAM=0: both halves on the main stream (A/B)
+        const char* e = getenv("QPS_WB_RHS_STREAM");
+        return e && !strcmp(e, "0");
+    }();
+    const cudaStream_t rs = rhs_side_off ? s : c.side;
+    RhsOps rhs2{m, rs, rhs_side_off ? c.ws : c.ws2};
+    if (!c.ev_rhs) QPS_CUDA(cudaEventCreateWithFlags(&c.ev_rhs, cudaEventDisableTiming));
+    if (rs != s) {  // the side stream starts after level 0 (y, W) is in place
+        QPS_CUDA(cudaEventRecord(c.ev_rhs, s));
+        QPS_CUDA(cudaStreamWaitEvent(rs, c.ev_rhs, 0));
+    }
+    c.lr_a.ensure(size_t(npos) * r2 * m);  // per position: the RHS half may lag a level behind
     auto eliminate = [&](std::vector<Pos*>& blk, int lvl) {
         std::vector<Pos*> up;
         for (Pos* p : blk)
@@ -2360,7 +2376,6 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         c.lr_Cpiv.ensure(size_t(cnt) * r2);
         const size_t cds = lu_dinv_elems(r2);
         c.lr_Cdinv.ensure(size_t(cnt) * cds);
-        c.lr_a.ensure(size_t(cnt) * r2 * m);
         DBuf<cplx>& Zb = c.lr_Z[lvl];
         Zb.ensure(size_t(cnt) * nb * r2);
         { QPS_NOTE_LAUNCH(); set_identity_kernel<<<cnt, 256, 0, s>>>(r2, c.lr_Cm.p); }
@@ -2386,7 +2401,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             cplx* Ci = c.lr_Ci.p + size_t(q) * r2 * r2;
             mt[q] = gemm1(S_of(p.j), r2, W, nb, nb, Cm, r2);                      // C = I - S W
             z[q] = gemm1(W, nb, gjinv ? Cm : Ci, r2, r2, Zb.p + size_t(q) * nb * r2, nb);  // Z = W C^{-1}
-            cplx* aq = c.lr_a.p + size_t(q) * r2 * m;
+            cplx* aq = c.lr_a.p + size_t(p.j) * r2 * m;
             gu[q] = gemm1(W, nb, g_of(p.j), r2, r2, p.F, nb);                      // u = y - W g
             ga[q] = gemm1(S_of(p.j), r2, p.F, nb, nb, aq, r2);                     // a = S u
             gz[q] = gemm1(Zb.p + size_t(q) * nb * r2, nb, aq, r2, r2, p.F, nb);    // z = u + Z a
@@ -2428,9 +2443,13 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
             lu_solve_batched(r2, r2, ca, cp, cd, ci, r2, r2, s, c.ws);
         }
         zgemm_batched(nb, r2, one, zero, z, s, c.ws.gemm_tasks, "wb_cap");
-        rhs.run(nb, mone, one, gu);
-        rhs.run(r2, one, zero, ga);
-        rhs.run(nb, one, one, gz);
+        if (rs != s) {  // Z of this level is queued
+            QPS_CUDA(cudaEventRecord(c.ev_rhs, s));
+            QPS_CUDA(cudaStreamWaitEvent(rs, c.ev_rhs, 0));
+        }
+        rhs2.run(nb, mone, one, gu);
+        rhs2.run(r2, one, zero, ga);
+        rhs2.run(nb, one, one, gz);
     };
     int lvl = 0;
     nvtxRangePushA("bcr_levels");  // the levels, final block and back substitution (ncu --nvtx-include)
@@ -2497,7 +2516,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         zgemm_batched(r, r, one, zero, cores, s, c.ws.gemm_tasks, "lr_core");
         zgemm_batched(r, nb, one, one, prods, s, c.ws.gemm_tasks, "lr_core");
         zgemm_batched(r, nb, mone, zero, newr, s, c.ws.gemm_tasks, "lr_core");  // L' = P_L (-(core) R)
-        rhs.run(r, one, one, v1);
+        rhs2.run(r, one, one, v1);
         tmark("update", lvl, int(odd.size()));
         levels.push_back(std::move(nxt));
         ++lvl;
@@ -2574,6 +2593,10 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
         flag.ensure(cap_orig.size());
         QPS_CUDA(cudaMemcpyAsync(flag.p, capflag.p, sizeof(int) * cap_orig.size(), cudaMemcpyDeviceToDevice, s));
         check(cap_orig);
+    }
+    if (rs != s) {  // the right-hand-side half joins the main stream
+        QPS_CUDA(cudaEventRecord(c.ev_rhs, rs));
+        QPS_CUDA(cudaStreamWaitEvent(s, c.ev_rhs, 0));
     }
     // back substitution: eta_o = z_o - Z_L (R_L(o) eta_{o-1}) - Z_U (R_U(o) eta_{o+1})
     for (int l = lvl - 1; l >= 0; --l) {

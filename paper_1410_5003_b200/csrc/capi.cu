@@ -158,7 +158,7 @@ void qps_destroy(qps_ctx* h) {
     if (s3) cudaStreamSynchronize(s3);
     if (s4) cudaStreamSynchronize(s4);
     for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_factor, h->c.ev_l0, h->c.ev_f0,
-                          h->c.ev_f1, h->c.ev_geo})
+                          h->c.ev_f1, h->c.ev_geo, h->c.ev_fillB, h->c.ev_rhs})
         if (e) cudaEventDestroy(e);
     std::vector<cudaStream_t> l0s;
     for (int i = 0; i < qpsb::Ctx::kL0MaxChunks; ++i) {

@@ -315,6 +315,7 @@ struct Ctx {
     // before the A' update (fill_overlap; opt-in QPS_FILL_OVERLAP=1, no gain measured)
     bool fill_overlap = false, fill_pending = false, fill_err_pending = false;
     cudaEvent_t ev_fillB = nullptr;
+    cudaEvent_t ev_rhs = nullptr;      // level fork/join of the Woodbury reduction's right-hand-side half
     cudaStream_t fill_stream = nullptr;
     DBuf<PairTask> d_pair2;
     DBuf<int4> d_tiles2;
