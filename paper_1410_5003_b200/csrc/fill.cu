@@ -592,25 +592,29 @@ __global__ void __launch_bounds__(128) alpert_kernel(const AlpertTask* __restric
                 ph = jraw < 0 ? T.alpha_inv : T.alpha;
             }
             const size_t off = size_t(col) * T.ld + m;
-            cplx* outs[4] = {T.oD, T.oS, T.oT, T.oDs};
+            cplx* outs[4] = {T.oD, T.oS, T.oT, T.oDs};  // the four quadrants: distinct entries
+            cplx v[4];
+#pragma unroll
+            for (int kd = 0; kd < 4; ++kd) v[kd] = outs[kd][off];  // four loads in flight
+#pragma unroll
             for (int kd = 0; kd < 4; ++kd) {
-                cplx* p = outs[kd] + off;
-                cplx v = *p;
-                v.re += ph.re * acc[kd].re - ph.im * acc[kd].im;
-                v.im += ph.re * acc[kd].im + ph.im * acc[kd].re;
-                *p = v;
+                v[kd].re += ph.re * acc[kd].re - ph.im * acc[kd].im;
+                v[kd].im += ph.re * acc[kd].im + ph.im * acc[kd].re;
+                outs[kd][off] = v[kd];
             }
         } else {
             if (jraw >= 0 && jraw < sd.n) {
                 if (!any) continue;
                 const size_t off = size_t(sd.offset + jraw) * T.ld + m;
                 cplx* outs[4] = {T.oD, T.oS, T.oT, T.oDs};
+                cplx v[4];
+#pragma unroll
+                for (int kd = 0; kd < 4; ++kd) v[kd] = outs[kd][off];
+#pragma unroll
                 for (int kd = 0; kd < 4; ++kd) {
-                    cplx* p = outs[kd] + off;
-                    cplx v = *p;
-                    v.re += acc[kd].re;
-                    v.im += acc[kd].im;
-                    *p = v;
+                    v[kd].re += acc[kd].re;
+                    v[kd].im += acc[kd].im;
+                    outs[kd][off] = v[kd];
                 }
             } else {
                 // out-of-period: Alpert spill plus (smooth) removal of the band
