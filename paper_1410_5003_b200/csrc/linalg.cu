@@ -2612,8 +2612,13 @@ void zgemm_batched(int M, int N, cplx alpha, cplx beta, const std::vector<GemmTa
             // the whole 48-row product in one CTA row: the wide operand is
             // streamed once instead of once per 16-row tile
             launch_z3<6, 2, 1, 4, 2, 2>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
-        else if (M <= 48 || (M <= 80 && N >= 256))
+        else if (M <= 48 || (M > 64 && M <= 80 && N >= 256))
             launch_z3<2, 2, 1, 4, 2, 4>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
+        else if (M <= 64 && N >= 256)
+            // 64-row products against a wide N: one 64 x 32 tile row (LU U12
+            // updates: 24.8 vs 18.3 TF/s for the 16 x 64 tile at 64 x 288 x 64;
+            // the 80-row Schur products stay on 16 x 64)
+            launch_z3<4, 2, 2, 2, 2, 3>(M, N, alpha, beta, d_tasks.p, tasks.size(), s);
         else if (kmax <= 96 || (M <= 128 && N <= 128) || !wide_tiles())
             // 32 x 32 (4 CTAs per SM): with every task's operands in HBM it
             // beats the 64 x 32 tile on every hot-path shape (tools/micro/
@@ -2750,9 +2755,13 @@ void cod_trsm(const CodBatch& b, cplx* B, int ldb, size_t stride, int ncols, con
         { QPS_NOTE_LAUNCH(); cod_trsm_tasks_kernel<<<(b.count + 127) / 128, 128, 0, s>>>(b, B, ldb, stride, flags, nst); }
         QPS_CUDA(cudaGetLastError());
         for (int st = 0; st < nst; ++st) {
-            if (st > 0)
+            if (st > 0) {
+                static const bool trace_shapes = getenv("QPS_TRACE_GEMM") != nullptr;
+                if (trace_shapes)
+                    fprintf(stderr, "gemm cod_trsm M=16 N=%d K=%d nseg=1 tasks=%d\n", ncols, 16 * st, b.count);
                 launch_z3<2, 2, 1, 4, 2, 4>(16, ncols, cplx{-1, 0}, cplx{1, 0}, b.trsm_tasks + size_t(st) * b.count,
                                            b.count, s);
+            }
             { QPS_NOTE_LAUNCH(); cod_trsm_diag_kernel<<<dim3((ncols + 127) / 128, b.count), 128, 0, s>>>(
                 b, B, ldb, stride, ncols, flags, st); }
             QPS_CUDA(cudaGetLastError());
