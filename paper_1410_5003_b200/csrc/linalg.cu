@@ -786,9 +786,10 @@ __global__ void __launch_bounds__(256) cod_qh_kernel(CodBatch b, const int* __re
 }
 
 // Same operator with the working set in shared memory (problems with
-// (m p + max(p^2, 8 m)) complex entries <= kCodSmemMax): region 1 holds the RZ
+// (m p + max(p^2, 32 m)) complex entries <= kCodSmemMax): region 1 holds the RZ
 // reflectors V, then the QR reflectors W; region 2 the Wz work columns
-// (row-major, conflict-free per thread column), then the per-warp QH columns.
+// (row-major, conflict-free per thread column), then the per-warp QH columns
+// (four per warp).
 constexpr size_t kCodSmemMax = 220 * 1024;
 __global__ void __launch_bounds__(256) cod_operator_smem_kernel(CodBatch b, const int* __restrict__ flags) {
     extern __shared__ cplx cod_sm[];
@@ -937,44 +938,70 @@ __global__ void __launch_bounds__(256) cod_operator_smem_kernel(CodBatch b, cons
     for (size_t i = tid; i < size_t(m) * p; i += blockDim.x) V[i] = W[i];
     __syncthreads();
     const cplx* Ws = V;
-    // QH = first r rows of H_{r-1} ... H_0: one warp per column, lanes over rows
+    // QH = first r rows of H_{r-1} ... H_0: each warp carries four columns at
+    // once (lanes over rows), so the four dot products' shuffle reductions of
+    // each reflector overlap instead of running one column after another
     {
+        constexpr int kC = 4;
         const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-        cplx* col = R2 + size_t(warp) * m;
-        for (int c = warp; c < m; c += nw) {
-            for (int i = lane; i < m; i += 32) col[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
+        cplx* cols = R2 + size_t(warp) * kC * m;
+        for (int cb = warp * kC; cb < m; cb += nw * kC) {
+#pragma unroll
+            for (int j = 0; j < kC; ++j)
+                for (int i = lane; i < m; i += 32) cols[j * m + i] = cplx{i == cb + j ? 1.0 : 0.0, 0.0};
             __syncwarp();
             for (int kk = 0; kk < r; ++kk) {
                 const cplx tk = tau[kk];
                 if (tk.re == 0.0 && tk.im == 0.0) continue;
-                cplx t{0, 0};
+                cplx t[kC];
+#pragma unroll
+                for (int j = 0; j < kC; ++j) t[j] = cplx{0, 0};
                 for (int i = kk + 1 + lane; i < m; i += 32) {
                     const cplx e = Ws[size_t(kk) * m + i];
-                    const cplx a = col[i];
-                    t.re += e.re * a.re + e.im * a.im;
-                    t.im += e.re * a.im - e.im * a.re;
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {
+                        const cplx a = cols[j * m + i];
+                        t[j].re += e.re * a.re + e.im * a.im;
+                        t[j].im += e.re * a.im - e.im * a.re;
+                    }
                 }
-                for (int o = 16; o > 0; o >>= 1) {
-                    t.re += __shfl_xor_sync(0xffffffffu, t.re, o);
-                    t.im += __shfl_xor_sync(0xffffffffu, t.im, o);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {
+                        t[j].re += __shfl_xor_sync(0xffffffffu, t[j].re, o);
+                        t[j].im += __shfl_xor_sync(0xffffffffu, t[j].im, o);
+                    }
+#pragma unroll
+                for (int j = 0; j < kC; ++j) {
+                    const cplx ck = cols[j * m + kk];
+                    t[j].re += ck.re;
+                    t[j].im += ck.im;
+                    t[j] = cmul(tk, t[j]);
                 }
-                const cplx ck = col[kk];
-                t.re += ck.re;
-                t.im += ck.im;
-                t = cmul(tk, t);
                 __syncwarp();
                 if (lane == 0) {
-                    col[kk].re -= t.re;
-                    col[kk].im -= t.im;
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {
+                        cols[j * m + kk].re -= t[j].re;
+                        cols[j * m + kk].im -= t[j].im;
+                    }
                 }
                 for (int i = kk + 1 + lane; i < m; i += 32) {
-                    const cplx et = cmul(Ws[size_t(kk) * m + i], t);
-                    col[i].re -= et.re;
-                    col[i].im -= et.im;
+                    const cplx e = Ws[size_t(kk) * m + i];
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {
+                        const cplx et = cmul(e, t[j]);
+                        cols[j * m + i].re -= et.re;
+                        cols[j * m + i].im -= et.im;
+                    }
                 }
                 __syncwarp();
             }
-            for (int i = lane; i < p; i += 32) QH[size_t(c) * p + i] = i < r ? col[i] : cplx{0, 0};
+#pragma unroll
+            for (int j = 0; j < kC; ++j)
+                if (cb + j < m)
+                    for (int i = lane; i < p; i += 32) QH[size_t(cb + j) * p + i] = i < r ? cols[j * m + i] : cplx{0, 0};
             __syncwarp();
         }
     }
@@ -2710,7 +2737,7 @@ void cod_rank(const CodBatch& b, double th, const int* flags, cudaStream_t s) {
 void cod_operator(const CodBatch& b, const int* flags, cudaStream_t s) {
     if (b.count == 0) return;
     ProfScope ps("cod_operator", s, 8.0 * b.count * (double(b.m) * b.p * b.p + double(b.p) * b.p * b.p));
-    const size_t sm = (size_t(b.m) * b.p + std::max(size_t(b.p) * b.p, size_t(8) * b.m)) * sizeof(cplx);
+    const size_t sm = (size_t(b.m) * b.p + std::max(size_t(b.p) * b.p, size_t(32) * b.m)) * sizeof(cplx);
     if (sm <= kCodSmemMax) {
         static bool attr = false;
         if (!attr) {
