@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(256) cod_operator_kernel(CodBatch b, const int
         }
         for (int i = 0; i < p; ++i) y[i] = cplx{i == c ? 1.0 : 0.0, 0.0};
         if (r < p) {
-            for (int k = 0; k < r; ++k) {
+            for (int k = c; k < r; ++k) {  // reflectors k < c leave e_c unchanged
                 const cplx tk = zc[k];
                 if (k != r - 1) {
                     const cplx t = y[k];
@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(256) cod_operator_smem_kernel(CodBatch b, cons
             auto y = [&](int i) -> cplx& { return R2[size_t(i) * p + c]; };
             for (int i = 0; i < p; ++i) y(i) = cplx{i == c ? 1.0 : 0.0, 0.0};
             if (r < p) {
-                for (int k = 0; k < r; ++k) {
+                for (int k = c; k < r; ++k) {  // reflectors k < c leave e_c unchanged
                     const cplx tk = zs[k];
                     if (k != r - 1) {
                         const cplx t = y(k);
