@@ -2041,8 +2041,10 @@ void wb_level0_async(Ctx& c) {
         wb[q] = c.lr_W0.p + size_t(q) * nb * wc;
     }
     nvtxRangePushA("bcr_level0");  // the level-0 batch: factorization (wb_factor_async) and this solve
+    tl_mark(c, "level0-staged(side)", f);
     if (c.l0_chunks == 1) {
         lu_solve_batched(nb, nb, fa, fp, fd, wb, nb, wc, f, c.ws2);
+        tl_mark(c, "level0-solved(side)", f);
     } else {
         QPS_CUDA(cudaEventRecord(c.ev_fork, st));  // staged
         for (int k = 0; k < c.l0_chunks; ++k) {
