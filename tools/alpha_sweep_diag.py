@@ -1,3 +1,4 @@
+"""Alpha-grouped sweep diagnostic: Bragg amplitudes of the GPU sweep (grouped and independent modes) against the oracle on a config-5 prefix at alpha-grid angles."""
 import sys, os, numpy as np, json
 sys.path.insert(0, ".")
 from paper_1410_5003_b200 import configs

@@ -1,3 +1,4 @@
+"""Config-3 prefixes on the oracle or the GPU: which interface counts solve and which raise SingularityError. usage: python tools/cfg3_probe.py oracle|gpu I..."""
 import sys, os
 sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
 from paper_1410_5003_b200 import Solver, configs

@@ -1,3 +1,4 @@
+"""End-to-end split of one config-4 call sequence through the public API: geometry, problem, solve (host and device time), solution readback."""
 import time, sys
 sys.path.insert(0, '.')
 from paper_1410_5003_b200 import configs

@@ -1,3 +1,4 @@
+"""Graded-corner self block (config-3 prefix): GPU vs oracle A_diag entries, split inside / outside the corner zones."""
 import sys
 import numpy as np
 sys.path.insert(0, ".")

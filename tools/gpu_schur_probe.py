@@ -1,3 +1,4 @@
+"""Config 1: the GPU's periodization pieces (Qp, Cp, Schur complements) against the oracle's, block by block."""
 import sys
 import numpy as np
 sys.path.insert(0, ".")

@@ -1,3 +1,4 @@
+"""Aggregate an ncu launch list CSV by kernel name, grid and block size: launches and serialised time. usage: python tools/ncu_parse.py launches.csv [top]"""
 import csv,collections,sys
 rows=[r for r in csv.reader(open(sys.argv[1])) if len(r)>10]
 h=rows[0]; ki=h.index("Kernel Name"); mi=h.index("Metric Name"); vi=h.index("Metric Value"); ii=h.index("ID")

@@ -1,3 +1,4 @@
+"""GPU COD least squares (qsolve) against numpy's pseudo-inverse on random full-rank and rank-deficient shapes, including the solver's 160 x 80 x 1216 case."""
 import numpy as np, sys
 sys.path.insert(0, ".")
 from paper_1410_5003_b200.qpscat import Solver

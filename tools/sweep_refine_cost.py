@@ -1,3 +1,4 @@
+"""Config-5 sweep time with 0 and 1 refinement steps per angle (the cost of the sweeps' default refinement)."""
 import sys, time, math
 sys.path.insert(0, '.')
 from paper_1410_5003_b200 import configs
