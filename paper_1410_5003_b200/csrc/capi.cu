@@ -161,6 +161,10 @@ void qps_destroy(qps_ctx* h) {
                           h->c.ev_f1, h->c.ev_geo, h->c.ev_fillB, h->c.ev_rhs})
         if (e) cudaEventDestroy(e);
     std::vector<cudaStream_t> l0s;
+    if (h->c.lsq_stream) {
+        cudaStreamSynchronize(h->c.lsq_stream);
+        l0s.push_back(h->c.lsq_stream);
+    }
     for (int i = 0; i < qpsb::Ctx::kL0MaxChunks; ++i) {
         if (h->c.l0_s[i]) {
             cudaStreamSynchronize(h->c.l0_s[i]);
@@ -427,7 +431,7 @@ int qps_solve(qps_ctx* h) {
                     const char* e = getenv("QPS_DEFER");
                     return e && !strcmp(e, "0");
                 }();
-                schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, !no_defer);
+                schur(c, c.Adiag.p, c.Asup.p, c.Asub.p, !no_defer, true);
             }
             tl_mark(c, "schur", c.stream);
             c.sys_valid = false;  // A now holds A'
@@ -454,6 +458,7 @@ int qps_solve(qps_ctx* h) {
             Timer t(c, &c.times.recover_ms);
             recover(c);
         }
+        schur_finish(c);  // the per-layer LSQ residuals (low-priority stream)
         tl_mark(c, "recover", c.stream);
         tl_report(c);
     });

@@ -316,6 +316,12 @@ struct Ctx {
     bool fill_overlap = false, fill_pending = false, fill_err_pending = false;
     cudaEvent_t ev_fillB = nullptr;
     cudaEvent_t ev_rhs = nullptr;      // level fork/join of the Woodbury reduction's right-hand-side half
+    // one-shot solves: the interior least squares' residual norms (reported
+    // only) run on a low-priority stream beside the A' update and the block
+    // solve; schur_finish joins them and fills lsq / max_lsq
+    cudaStream_t lsq_stream = nullptr;
+    bool lsq_pending = false, lsq_corners = false;
+    std::vector<double> lsq_li, lsq_lc;
     cudaStream_t fill_stream = nullptr;
     DBuf<PairTask> d_pair2;
     DBuf<int4> d_tiles2;
@@ -333,7 +339,10 @@ void setup_dims(Ctx& c, bool check_solvable = true);
 void fill_system_fused(Ctx& c);
 // Schur complements in place on (A_diag, A_super, A_sub) or on the A' copies,
 // for all dims.nsys systems (system a at base + a * stride)
-void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings = false);
+// defer_lsq: leave the per-layer LSQ residuals in flight (schur_finish)
+void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings = false, bool defer_lsq = false);
+// joins deferred LSQ residual norms into the main stream and fills lsq / max_lsq
+void schur_finish(Ctx& c);
 // block cyclic reduction of all systems with RHS f (per system); eta in c.F
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
 // allocate the per-system buffers of the assembled system for dims.nsys systems

@@ -621,6 +621,7 @@ struct QFamily {
     size_t Xstride;
     double* lsq_out;
     cudaStream_t s;
+    cudaStream_t rs = nullptr;  // residual norms on this stream (forked from s) when set
     std::vector<int> flags;
     double th = 0.0;
     int stage = 0;  // 1: a threshold step in flight, 2: residual norms in flight
@@ -687,10 +688,16 @@ void qsolve_residuals(QFamily& f) {
         t.C = const_cast<cplx*>(f.R) + f.Rstride * q;
         t.ldc = f.ldR;
     }
-    zgemm_residual_norms(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, f.s, cs.tasks1, cs.parts, cs.enorm.p);
-    QPS_D2H(cs.h_enorm.p, cs.enorm.p, sizeof(double) * cnt, f.s);
-    QPS_D2H(cs.h_rnorm.p, cs.rnorm.p, sizeof(double) * cnt, f.s);
-    QPS_CUDA(cudaEventRecord(cs.ev, f.s));
+    cudaStream_t s = f.s;
+    if (f.rs) {  // X is final on f.s: fork
+        QPS_CUDA(cudaEventRecord(cs.ev, f.s));
+        QPS_CUDA(cudaStreamWaitEvent(f.rs, cs.ev, 0));
+        s = f.rs;
+    }
+    zgemm_residual_norms(cs.m, cs.ncols, cplx{1, 0}, cplx{-1, 0}, tasks, s, cs.tasks1, cs.parts, cs.enorm.p);
+    QPS_D2H(cs.h_enorm.p, cs.enorm.p, sizeof(double) * cnt, s);
+    QPS_D2H(cs.h_rnorm.p, cs.rnorm.p, sizeof(double) * cnt, s);
+    QPS_CUDA(cudaEventRecord(cs.ev, s));
     f.stage = 2;
 }
 
@@ -772,8 +779,45 @@ void qsolve_family_public(Ctx& c, CodSet& cs, const cplx* Q, const cplx* R, int 
     qsolve_family(c, cs, Q, R, ldR, Rstride, X, ldX, Xstride, lsq_out);
 }
 
-void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
+namespace {
+// per-layer LSQ residuals of every system from the interior (li) and corner
+// (lc) families into lsq_all, lsq, max_lsq
+void lsq_assemble(Ctx& c, const std::vector<double>& li, const std::vector<double>& lc) {
+    const int I = c.dims.I, ns = c.dims.nsys;
+    for (int a = 0; a < ns; ++a) {
+        double* l = c.lsq_all.data() + size_t(a) * (I + 1);
+        l[0] = lc[2 * a];
+        l[I] = lc[2 * a + 1];
+        for (int i = 1; i < I; ++i) l[i] = li[size_t(a) * (I - 1) + (i - 1)];
+    }
+    c.lsq.assign(c.lsq_all.begin(), c.lsq_all.begin() + (I + 1));
+    c.max_lsq = 0.0;
+    for (double r : c.lsq) c.max_lsq = std::max(c.max_lsq, r);
+}
+}  // namespace
+
+void schur_finish(Ctx& c) {
+    if (!c.lsq_pending) return;
+    c.lsq_pending = false;
+    const int I = c.dims.I, ns = c.dims.nsys;
+    if (I > 1) {
+        CodSet& cs = c.cod_int;
+        QPS_CUDA(cudaStreamWaitEvent(c.stream, cs.ev, 0));  // the solve's timing covers the residuals
+        QPS_CUDA(cudaEventSynchronize(cs.ev));
+        for (int q = 0; q < cs.count; ++q) c.lsq_li[q] = cs.h_enorm[q] / cs.h_rnorm[q];
+    }
+    if (c.lsq_corners) {
+        CodSet& cs = c.cod_c;
+        QPS_CUDA(cudaEventSynchronize(cs.ev));
+        for (int q = 0; q < cs.count; ++q) c.lsq_lc[q] = cs.h_enorm[q] / cs.h_rnorm[q];
+    }
+    (void)ns;
+    lsq_assemble(c, c.lsq_li, c.lsq_lc);
+}
+
+void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings, bool defer_lsq) {
     ProfPhase phase("schur");
+    schur_finish(c);  // a previous solve's residuals (an aborted attempt) are read before reuse
     const Dims& D = c.dims;
     const int I = D.I, nb = D.nb, P = D.P, ns = D.nsys;
     if (P <= 0) fail(QPS_ERR_CONFIG, "periodization needs P > 0 proxy points per layer");
@@ -783,14 +827,27 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
     c.lsq_all.assign(size_t(ns) * (I + 1), 0.0);
     // interior layers i = 1..I-1 of every system: X = qsolve(Q_i, [C_above_i C_self_i])
     // (system a's interior layers are contiguous after system a-1's)
-    std::vector<double> li(size_t(ns) * (I > 1 ? I - 1 : 0));
-    std::vector<double> lc(2 * size_t(ns));
+    std::vector<double>& li = c.lsq_li;
+    std::vector<double>& lc = c.lsq_lc;
+    li.assign(size_t(ns) * (I > 1 ? I - 1 : 0), 0.0);
+    lc.assign(2 * size_t(ns), 0.0);
+    static const bool lsq_side = [] {  // QPS_LSQ_STREAM=0: residual norms on the main stream (A/B)
+        const char* e = getenv("QPS_LSQ_STREAM");
+        return !(e && !strcmp(e, "0"));
+    }();
+    defer_lsq = defer_lsq && lsq_side;
+    if (defer_lsq && !c.lsq_stream) {
+        int lo = 0, hi = 0;
+        QPS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        QPS_CUDA(cudaStreamCreateWithPriority(&c.lsq_stream, cudaStreamNonBlocking, lo));
+    }
     std::vector<QFamily> fams;
     if (I > 1) {
         c.cod_int.ensure(ns * (I - 1), D.mI, P, 2 * nb);
         QFamily f;
         f.cs = &c.cod_int; f.Q = c.Qint.p; f.R = c.Rint.p; f.ldR = D.mI; f.Rstride = size_t(D.mI) * 2 * nb;
         f.X = c.Xint.p; f.ldX = P; f.Xstride = size_t(P) * 2 * nb; f.lsq_out = li.data(); f.s = c.stream;
+        if (defer_lsq) f.rs = c.lsq_stream;
         fams.push_back(std::move(f));
     }
     // corners: X_first = qsolve(Q'_1, C'_1), X_last = qsolve(Q'_{I+1}, C'_{I+1}), on the side stream
@@ -885,18 +942,15 @@ void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings) {
         QPS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_fork, 0));
         zgemm_batched(nb, nb, cplx{-1, 0}, cplx{1, 0}, ctasks, c.stream, c.ws.gemm_tasks, "schur_update");
     }
-    qsolve_collect(fams);  // per-layer LSQ residuals, read back while the update runs
-    fill_join(c, true);    // coincidence flag of a split fill
-    for (int a = 0; a < ns; ++a) {
-        double* l = c.lsq_all.data() + size_t(a) * (I + 1);
-        l[0] = lc[2 * a];
-        l[I] = lc[2 * a + 1];
-        for (int i = 1; i < I; ++i) l[i] = li[size_t(a) * (I - 1) + (i - 1)];
+    if (defer_lsq) {
+        c.lsq_pending = true;
+        c.lsq_corners = corners;
+    } else {
+        qsolve_collect(fams);  // per-layer LSQ residuals, read back while the update runs
+        lsq_assemble(c, li, lc);
     }
-    c.lsq.assign(c.lsq_all.begin(), c.lsq_all.begin() + (I + 1));
+    fill_join(c, true);    // coincidence flag of a split fill
     c.couplings_deferred = defer_couplings && I > 1;
-    c.max_lsq = 0.0;
-    for (double r : c.lsq) c.max_lsq = std::max(c.max_lsq, r);
     c.ps_valid = true;
 }
 
