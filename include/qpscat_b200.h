@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define QPS_ABI_VERSION 3
+#define QPS_ABI_VERSION 4
 
 typedef struct qps_ctx qps_ctx;
 typedef struct {
@@ -117,13 +117,19 @@ typedef struct {
  *                   probe block w2 (above 1e-12 -> dense reduction)
  *   refine_steps    iterative-refinement steps applied to the block solve
  *   refine_res0/1   ||f - A' eta||_2 / ||f||_2 before the first step and (when
- *                   QPS_REFINE_CHECK=1) after the last one; 0 when none ran */
+ *                   QPS_REFINE_CHECK=1) after the last one; 0 when none ran
+ *   lr_width        columns of the compressed coupling bases: the widest
+ *                   accepted rank rounded up to 8 (48 at most; 0 when dense)
+ *   lr_width_retry  1 when the truncated bases failed the probe and the solve
+ *                   ran again at the full width */
 typedef struct {
     int bcr_path;
     int lr_rank_max;
     double lr_probe_worst;
     int refine_steps;
     double refine_res0, refine_res1;
+    int lr_width;
+    int lr_width_retry;
 } qps_solver_diag;
 
 /* ---------------------------------------------------------------- context */

@@ -630,7 +630,7 @@ int qps_get_phase_times(const qps_ctx* c, qps_phase_times* t) {
 
 int qps_solver_diagnostics(const qps_ctx* c, qps_solver_diag* d) {
     if (!c || !d) return QPS_ERR_USAGE;
-    *d = qps_solver_diag{-1, 0, 0.0, 0, 0.0, 0.0};  // the reference's block Thomas (tridiag.hpp:23-46)
+    *d = qps_solver_diag{-1, 0, 0.0, 0, 0.0, 0.0, 0, 0};  // the reference's block Thomas (tridiag.hpp:23-46)
     return QPS_OK;
 }
 

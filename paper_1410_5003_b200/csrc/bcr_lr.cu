@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(512) gj_inverse_kernel(int n, cplx* __restrict
 template <int N>
 __global__ void __launch_bounds__(4 * N) gj_inverse_reg_kernel(cplx* __restrict__ C, int* __restrict__ flag) {
     constexpr int NR = N / 4;
-    static_assert(N % 32 == 0 && NR <= 32, "gj_inverse_reg_kernel: N a multiple of 32, N <= 128");
+    static_assert(N % 16 == 0 && NR <= 32, "gj_inverse_reg_kernel: N a multiple of 16, N <= 128");
     __shared__ cplx s_row[N], s_col[2][N];  // s_col double-buffered: written before the first barrier
     __shared__ int s_perm[N], s_pinv[N];
     __shared__ double s_cv[2][4];
@@ -952,6 +952,27 @@ __global__ void __launch_bounds__(256) sparse_sketch_kernel(const cplx* const* _
     }
 }
 
+// the first r2 of the r1 columns of every coupling's ID factors (adaptive
+// basis width): L (nb x r1 -> nb x r2, the leading columns are contiguous),
+// L1^{-1} (leading r2 x r2 block: the inverse of a leading block of a lower
+// triangular matrix), skeleton rows
+__global__ void __launch_bounds__(256) id_compact_kernel(int nb, int r1, int r2, const cplx* __restrict__ P1,
+                                                         const cplx* __restrict__ L1, const int* __restrict__ piv1,
+                                                         cplx* __restrict__ P2, cplx* __restrict__ L2,
+                                                         int* __restrict__ piv2) {
+    const int q = blockIdx.y;
+    const size_t pn = size_t(nb) * r2;
+    const cplx* src = P1 + size_t(q) * nb * r1;
+    cplx* dst = P2 + size_t(q) * pn;
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < pn; e += size_t(gridDim.x) * blockDim.x)
+        dst[e] = src[e];
+    if (blockIdx.x == 0) {
+        for (int e = threadIdx.x; e < r2 * r2; e += blockDim.x)
+            L2[size_t(q) * r2 * r2 + e] = L1[size_t(q) * r1 * r1 + size_t(e / r2) * r1 + e % r2];
+        for (int e = threadIdx.x; e < r2; e += blockDim.x) piv2[size_t(q) * r2 + e] = piv1[size_t(q) * r1 + e];
+    }
+}
+
 GemmTask gemm1(const cplx* A, int lda, const cplx* B, int ldb, int K, cplx* C, int ldc) {
     GemmTask t{};
     t.nseg = 1;
@@ -1242,7 +1263,7 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         return e && !strcmp(e, "0");
     }();
     if (!id_off && nb <= kIdThreads && lr_basis() <= kLrSample) {
-        const int r = lr_basis();
+        int r = lr_basis();
         c.lr_r = r;
         c.lr_P.ensure(size_t(nc) * nb * r);
         c.lr_L1i.ensure(size_t(nc) * r * r);
@@ -1263,6 +1284,37 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
         }
         c.lr_rank_h.ensure(nc);
         QPS_D2H(c.lr_rank_h.p, c.lr_rank_d.p, sizeof(int) * nc, s);
+        // adaptive width: the widest accepted rank rounded up to 8 columns
+        // (config 4: 39 -> 40 instead of 48) -- every later product, the level-0
+        // right-hand sides and the 2r x 2r capacitances shrink with it.  The
+        // host waits for the ranks here; the factorization is queued already.
+        static const bool adapt = [] {  // QPS_LR_ADAPT=0: always lr_basis() columns (A/B)
+            const char* e = getenv("QPS_LR_ADAPT");
+            return !(e && !strcmp(e, "0"));
+        }();
+        c.lr_width_retry = false;
+        if (adapt && !c.lr_full_width) {
+            if (!c.ev_rank) QPS_CUDA(cudaEventCreateWithFlags(&c.ev_rank, cudaEventDisableTiming));
+            QPS_CUDA(cudaEventRecord(c.ev_rank, s));
+            QPS_CUDA(cudaEventSynchronize(c.ev_rank));
+            int mx = 0;
+            for (int q = 0; q < nc; ++q) mx = std::max(mx, c.lr_rank_h[q]);
+            const int rn = std::max(16, (mx + 7) / 8 * 8);
+            if (mx <= kLrMaxRank && rn < r) {
+                c.lr_Pc.ensure(size_t(nc) * nb * rn);
+                c.lr_L1ic.ensure(size_t(nc) * rn * rn);
+                c.lr_pivc.ensure(size_t(nc) * rn);
+                { QPS_NOTE_LAUNCH(); id_compact_kernel<<<dim3(16, nc), 256, 0, s>>>(nb, r, rn, c.lr_P.p, c.lr_L1i.p,
+                                                                                   c.lr_piv.p, c.lr_Pc.p,
+                                                                                   c.lr_L1ic.p, c.lr_pivc.p); }
+                QPS_CUDA(cudaGetLastError());
+                std::swap(c.lr_P, c.lr_Pc);
+                std::swap(c.lr_L1i, c.lr_L1ic);
+                std::swap(c.lr_piv, c.lr_pivc);
+                r = rn;
+                c.lr_r = r;
+            }
+        }
         tmark("row ID of the samples");
         wb_level0_async(c);  // the left factors exist: level 0 on the factor stream from here
         // R = L1^{-1} C[I, :]   (C[I, :] = A[I, :] - Bc[I, :] X when deferred)
@@ -1369,7 +1421,11 @@ bool lr_compress(Ctx& c, cplx* Au, cplx* Al) {
             QPS_CUDA(cudaEventDestroy(te1));
         }
         tl_mark(c, "compress", s);
-        return lr_accept(c, nc);
+        const bool ok = lr_accept(c, nc);
+        // a truncated width that fails (rank within the limit, probe missed):
+        // the caller retries at the full width before going dense
+        if (!ok && r < lr_basis() && c.lr_rank_max <= kLrMaxRank) c.lr_width_retry = true;
+        return ok;
     }
     static const bool cpqr_only = [] {
         const char* e = getenv("QPS_LR_QR");
@@ -2421,7 +2477,7 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
                 return e && !strcmp(e, "smem");
             }();
             ProfScope ps("wb_gj", s, 8.0 * cnt * double(r2) * r2 * r2);
-            if (gj_smem || r2 != 96) {
+            if (gj_smem || r2 % 16 || r2 < 32 || r2 > 96) {
                 static bool attr = false;
                 if (!attr) {
                     QPS_CUDA(cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2432,7 +2488,14 @@ void bcr_solve_wb(Ctx& c, cplx* Ad) {
                                                                                   capflag.p + cap_orig.size()); }
             } else {
                 int* fl = capflag.p + cap_orig.size();
-                { QPS_NOTE_LAUNCH(); gj_inverse_reg_kernel<96><<<cnt, 4 * 96, 0, s>>>(c.lr_Cm.p, fl); }
+                QPS_NOTE_LAUNCH();
+                switch (r2) {  // 2r for the adaptive widths r = 16, 24, ..., 48
+                    case 32: gj_inverse_reg_kernel<32><<<cnt, 4 * 32, 0, s>>>(c.lr_Cm.p, fl); break;
+                    case 48: gj_inverse_reg_kernel<48><<<cnt, 4 * 48, 0, s>>>(c.lr_Cm.p, fl); break;
+                    case 64: gj_inverse_reg_kernel<64><<<cnt, 4 * 64, 0, s>>>(c.lr_Cm.p, fl); break;
+                    case 80: gj_inverse_reg_kernel<80><<<cnt, 4 * 80, 0, s>>>(c.lr_Cm.p, fl); break;
+                    default: gj_inverse_reg_kernel<96><<<cnt, 4 * 96, 0, s>>>(c.lr_Cm.p, fl); break;
+                }
             }
             QPS_CUDA(cudaGetLastError());
             cap_orig.insert(cap_orig.end(), orig.begin(), orig.end());

@@ -158,7 +158,7 @@ void qps_destroy(qps_ctx* h) {
     if (s3) cudaStreamSynchronize(s3);
     if (s4) cudaStreamSynchronize(s4);
     for (cudaEvent_t e : {h->c.ev_fork, h->c.ev_fill, h->c.ev_sample, h->c.ev_anorm, h->c.ev_factor, h->c.ev_l0, h->c.ev_f0,
-                          h->c.ev_f1, h->c.ev_geo, h->c.ev_fillB, h->c.ev_rhs})
+                          h->c.ev_f1, h->c.ev_geo, h->c.ev_fillB, h->c.ev_rhs, h->c.ev_rank})
         if (e) cudaEventDestroy(e);
     std::vector<cudaStream_t> l0s;
     if (h->c.lsq_stream) {
@@ -442,15 +442,13 @@ int qps_solve(qps_ctx* h) {
                 c.allow_early = false;
             } catch (const Error& e) {
                 c.allow_early = false;
-                // couplings not low rank after the early level-0 factorization: once more, dense
-                if (attempt == 0 && e.status == QPS_ERR_INTERNAL && e.what() == std::string(kRetryDense)) {
-                    c.force_dense = true;
-                    continue;
-                }
-                c.force_dense = false;
+                // couplings not low rank (or not at the truncated width) after the
+                // early level-0 factorization: once more, dense (full width)
+                if (solve_retry(c, e)) continue;
+                c.force_dense = c.lr_full_width = false;
                 throw;
             }
-            c.force_dense = false;
+            c.force_dense = c.lr_full_width = false;
             break;
         }
         c.ps_valid = false;
@@ -689,6 +687,8 @@ int qps_solver_diagnostics(const qps_ctx* h, qps_solver_diag* d) {
     }
     d->refine_res0 = nr[2] > 0 ? nr[0] / nr[2] : 0.0;
     d->refine_res1 = nr[2] > 0 ? nr[1] / nr[2] : 0.0;
+    d->lr_width = h->c.bcr_path ? h->c.lr_r : 0;
+    d->lr_width_retry = h->c.lr_width_retried ? 1 : 0;
     return QPS_OK;
 }
 

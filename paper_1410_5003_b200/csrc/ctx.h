@@ -192,6 +192,10 @@ struct Ctx {
     DBuf<const cplx*> lr_skp;          // sketch source pointers
     DBuf<int> lr_skl;                  // sketch source leading dimensions
     DBuf<int> lr_piv, lr_rank_d;       // row ID: skeleton rows I (r per coupling); sample ranks
+    // adaptive basis width: the ID's first r' <= r columns repacked here, then swapped in
+    DBuf<cplx> lr_Pc, lr_L1ic;
+    DBuf<int> lr_pivc;
+    cudaEvent_t ev_rank = nullptr;     // the ID's ranks are on the host
     DBuf<cplx> lr_V, lr_VH, lr_Tq, lr_THq, lr_W1, lr_W2, lr_R64, lr_Q2, lr_Q2H;  // blocked QR of the samples
     int lr_omega_n = 0, lr_r = 0;
     HBuf<double> geo_h;                // pinned staging of the geometry pool (upload_geometry)
@@ -220,6 +224,10 @@ struct Ctx {
     // after a compression that failed once that factorization had started
     bool factor_pending = false, force_dense = false;
     bool allow_early = false;          // set by callers that handle the kRetryDense re-run
+    // lr_full_width: the kRetryWidth re-run (no adaptive basis width);
+    // lr_width_retry: lr_compress failed its probe with a truncated width
+    bool lr_full_width = false, lr_width_retry = false;
+    bool lr_width_retried = false;     // diagnostics: the last solve needed the full-width re-run
     bool l0_async = false;             // level 0 solved on the factor stream (wb_level0_async, ev_l0)
     cudaEvent_t ev_l0 = nullptr;
     cudaStream_t factor_stream = nullptr;
@@ -343,6 +351,21 @@ void fill_system_fused(Ctx& c);
 void schur(Ctx& c, cplx* Ad, cplx* Au, cplx* Al, bool defer_couplings = false, bool defer_lsq = false);
 // joins deferred LSQ residual norms into the main stream and fills lsq / max_lsq
 void schur_finish(Ctx& c);
+// a solve attempt threw e: true when the caller should run it once more
+// (kRetryWidth -> full basis width, kRetryDense -> dense reduction; each once)
+inline bool solve_retry(Ctx& c, const Error& e) {
+    if (e.status != QPS_ERR_INTERNAL) return false;
+    if (e.what() == std::string(kRetryWidth) && !c.lr_full_width) {
+        c.lr_full_width = true;
+        c.lr_width_retried = true;
+        return true;
+    }
+    if (e.what() == std::string(kRetryDense) && !c.force_dense) {
+        c.force_dense = true;
+        return true;
+    }
+    return false;
+}
 // block cyclic reduction of all systems with RHS f (per system); eta in c.F
 void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al);
 // allocate the per-system buffers of the assembled system for dims.nsys systems

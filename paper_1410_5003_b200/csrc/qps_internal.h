@@ -36,6 +36,9 @@ struct Error : std::runtime_error {
 [[noreturn]] inline void fail(int st, const std::string& msg) { throw Error(st, msg); }
 // internal: the block solve must be re-run with the dense reduction (bcr_solve)
 constexpr const char* kRetryDense = "qpsb: retry with the dense cyclic reduction";
+// the adaptive (truncated) coupling bases failed the a-posteriori probe after the
+// early level-0 factorization: once more with the full basis width
+constexpr const char* kRetryWidth = "qpsb: retry with the full low-rank basis width";
 
 // counted device->host copy
 #define QPS_D2H(dst, src, bytes, stream)                                                   \

@@ -976,6 +976,7 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
         return e && !strcmp(e, "0");
     }();
     c.lr_rank_max = 0;
+    if (!c.lr_full_width) c.lr_width_retried = false;  // kept through the full-width re-run
     c.lr_probe_worst = 0;
     c.bcr_path = 0;
     c.anorm_pending = false;
@@ -1013,7 +1014,24 @@ void bcr_solve(Ctx& c, cplx* Ad, cplx* Au, cplx* Al) {
     }
     if (woodbury && !early_off && c.allow_early && lr_eligible_pub(c)) wb_factor_async(c, Ad);
     else if (woodbury) wb_anorm_async(c, Ad);
-    if (!dense_only && !c.force_dense && lr_compress(c, Au, Al)) {
+    bool lr_ok = !dense_only && !c.force_dense && lr_compress(c, Au, Al);
+    if (!lr_ok && c.lr_width_retry) {
+        // the truncated bases failed the probe: the full width (A untouched
+        // unless the early factorization ran, then the caller re-runs)
+        c.lr_width_retry = false;
+        if (c.factor_pending) {
+            QPS_CUDA(cudaStreamSynchronize(c.factor_stream ? c.factor_stream : c.side));
+            c.factor_pending = false;
+            throw Error(QPS_ERR_INTERNAL, kRetryWidth);
+        }
+        const bool fw = c.lr_full_width;
+        c.lr_full_width = true;
+        c.lr_width_retried = true;
+        lr_ok = lr_compress(c, Au, Al);
+        c.lr_full_width = fw;
+        c.lr_width_retry = false;
+    }
+    if (lr_ok) {
         const bool direct = lr_direct && c.nrhs == 1;  // several right-hand sides: the Woodbury form
         c.bcr_path = direct ? 2 : 1;
         if (direct) bcr_solve_lr(c, Ad);

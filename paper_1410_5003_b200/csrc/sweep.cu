@@ -805,14 +805,11 @@ void run_sweep(Ctx& c, int n, const double* theta, int K, int mode, double* R, d
                         c.allow_early = false;
                     } catch (const Error& e) {
                         c.allow_early = false;
-                        if (attempt == 0 && e.status == QPS_ERR_INTERNAL && e.what() == std::string(kRetryDense)) {
-                            c.force_dense = true;  // couplings not low rank: the batch once more, dense
-                            continue;
-                        }
-                        c.force_dense = false;
+                        if (solve_retry(c, e)) continue;  // the batch once more: full width / dense
+                        c.force_dense = c.lr_full_width = false;
                         throw;
                     }
-                    c.force_dense = false;
+                    c.force_dense = c.lr_full_width = false;
                     break;
                 }
                 c.sweep_interior += ids.size();  // one independent system per angle

@@ -105,7 +105,8 @@ class _Num(C.Structure):
 
 class _Diag(C.Structure):
     _fields_ = [("bcr_path", C.c_int), ("lr_rank_max", C.c_int), ("lr_probe_worst", C.c_double),
-                ("refine_steps", C.c_int), ("refine_res0", C.c_double), ("refine_res1", C.c_double)]
+                ("refine_steps", C.c_int), ("refine_res0", C.c_double), ("refine_res1", C.c_double),
+                ("lr_width", C.c_int), ("lr_width_retry", C.c_int)]
 
 
 class _Times(C.Structure):

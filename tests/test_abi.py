@@ -25,7 +25,7 @@ def test_product_exports_every_symbol(product_lib):
     assert not missing, missing
     lib.qps_backend_name.restype = ctypes.c_char_p
     assert lib.qps_backend_name() == b"b200-cuda"
-    assert lib.qps_abi_version() == 3
+    assert lib.qps_abi_version() == 4
 
 
 def test_oracle_exports_every_symbol(oracle_lib):
