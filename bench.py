@@ -50,16 +50,17 @@ def ncu_summary():
 CFG = 4
 
 
-def bcr_factor(phases, I, n, peak):
+def bcr_factor(phases, I, n, peak, width):
     """The block solve's factorization batch (Woodbury level 0: LU with partial
-    pivoting of every n x n diagonal block and its 2r + 1 = 97 right-hand-side
-    solves) against the DMMA peak, at nominal complex flop counts (LU 8/3 n^3,
-    forward + back substitution 8 n^2 per right-hand side; n = 2N, the padding
-    to 608 not counted)."""
+    pivoting of every n x n diagonal block and its 2r + 1 right-hand-side
+    solves, r = the adaptive basis width: 40 at config 4) against the DMMA
+    peak, at nominal complex flop counts (LU 8/3 n^3, forward + back
+    substitution 8 n^2 per right-hand side; n = 2N, the padding to 608 not
+    counted)."""
     ms = phases.get("factor_ms") or 0.0
-    if ms <= 0:
+    if ms <= 0 or width <= 0:
         return None
-    rhs = 97
+    rhs = 2 * width + 1
     fl = I * (8.0 / 3.0 * n ** 3 + 8.0 * n * n * rhs)
     tf = fl / (ms * 1e-3) / 1e12
     return {"ms": ms, "blocks": I, "n": n, "rhs": rhs, "nominal_flops": fl, "tflops": tf,
@@ -332,6 +333,7 @@ def main():
     step_ms = allmax(dist, sum(totals) / len(totals))
     value = world * I / (step_ms * 1e-3)
     rt = s.reflection_transmission()
+    diag = s.solver_diagnostics()
     evals = s.fill_evals()
     # dominant kernel family over the timed region (main-stream families: the
     # compression sample runs on a low-priority side stream and its events span
@@ -409,7 +411,8 @@ def main():
                 "fill_fp64_frac_ncu": fill_ncu.get("fp64_frac_of_peak"),
                 "fill_nominal_frac_ncu": fill_ncu.get("nominal_frac_of_peak"),
                 "fill_fp64_ncu_note": fill_ncu.get("note"),
-                "bcr_factor": dict(bcr_factor(phases, I, 2 * N, peak) or {},
+                "lr_basis_width": diag["lr_width"],
+                "bcr_factor": dict(bcr_factor(phases, I, 2 * N, peak, diag["lr_width"]) or {},
                                    ncu={k: v for k, v in ncu_summary().get("bcr_level0", {}).items()
                                         if k not in ("command",)}),
                 "gemm_tflops_issued": gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
