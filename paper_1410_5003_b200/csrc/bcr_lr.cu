@@ -902,10 +902,10 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const cplx* const* __r
 // 64 at a time (each read once), and warp w sums sample columns 8w..8w+7 in
 // registers (each lane its own row).
 // ---------------------------------------------------------------------------
-constexpr int kSkCols = 64, kSkZeta = 8, kSkChunk = 64;
+constexpr int kSkCols = 64, kSkZeta = 8, kSkChunk = 32;
 constexpr size_t kSkSmem = size_t(kSkChunk) * 33 * sizeof(cplx);
 // col_ptr[j * (nchunks + 1) + c]: first entry of sample column j whose source
-// column is >= c * kSkChunk; entries packed ((source mod kSkChunk) * 33 << 1) | negative
+// column is >= c * kSkChunk; entries packed ((source mod kSkChunk) << 1) | negative
 __global__ void __launch_bounds__(256) sparse_sketch_kernel(const cplx* const* __restrict__ src,
                                                             const int* __restrict__ lds, int M, int ncols,
                                                             const int* __restrict__ col_ptr,
@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(256) sparse_sketch_kernel(const cplx* const* _
             // entries: (staged row offset << 1) | negative (offset precomputed on the host)
             for (int e = e0; e < e1; ++e) {
                 const int pk = ent[e];
-                const cplx v = sk_sm[(pk >> 1) + lane];
+                const cplx v = sk_sm[(pk >> 1) * 33 + lane];
                 acc[k].re += (pk & 1) ? -v.re : v.re;
                 acc[k].im += (pk & 1) ? -v.im : v.im;
             }
@@ -970,6 +970,90 @@ __global__ void __launch_bounds__(256) id_compact_kernel(int nb, int r1, int r2,
         for (int e = threadIdx.x; e < r2 * r2; e += blockDim.x)
             L2[size_t(q) * r2 * r2 + e] = L1[size_t(q) * r1 * r1 + size_t(e / r2) * r1 + e % r2];
         for (int e = threadIdx.x; e < r2; e += blockDim.x) piv2[size_t(q) * r2 + e] = piv1[size_t(q) * r1 + e];
+    }
+}
+
+// Two rows per lane (64 per CTA) and the whole sparse map (column pointers and
+// entries, ~22 KB at nb = 608) in shared memory: every entry's index and sign
+// is a broadcast shared load amortised over two rows instead of a global load
+// per row, which left the one-row kernel at 1.8 TB/s waiting on L1/L2
+// (long-scoreboard stalls).  Same per-row summation order, so Y is bitwise the
+// one-row kernel's.
+constexpr int kSkRows = 64, kSkLd = kSkRows + 1;
+size_t sk2_smem_bytes(int nptr, int nent) {
+    return size_t(2) * kSkChunk * kSkLd * sizeof(cplx) + sizeof(int) * size_t(nptr + nent);
+}
+__device__ __forceinline__ void sk_cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+}
+__global__ void __launch_bounds__(256, 2) sparse_sketch2_kernel(const cplx* const* __restrict__ src,
+                                                                const int* __restrict__ lds, int M, int ncols,
+                                                                const int* __restrict__ col_ptr,
+                                                                const int* __restrict__ ent, int nent, cplx alpha,
+                                                                cplx* __restrict__ Y, int ldy, size_t ystride) {
+    extern __shared__ cplx sk_sm[];  // two staged chunks [kSkChunk][kSkLd], then the map
+    const int nch = (ncols + kSkChunk - 1) / kSkChunk, nptr = kSkCols * (nch + 1);
+    int* s_ptr = reinterpret_cast<int*>(sk_sm + 2 * kSkChunk * kSkLd);
+    int* s_ent = s_ptr + nptr;
+    const int q = blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int r0 = blockIdx.x * kSkRows;
+    for (int e = tid; e < nptr; e += blockDim.x) s_ptr[e] = col_ptr[e];
+    for (int e = tid; e < nent; e += blockDim.x) s_ent[e] = ent[e];
+    const cplx* A = src[q];
+    const size_t ld = size_t(lds[q]);
+    cplx acc[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k][0] = acc[k][1] = cplx{0, 0};
+    // each source column of a chunk read once (64 rows: 1 KB per column),
+    // asynchronously into the other buffer while this one is summed
+    auto stage = [&](int ch, int buf) {
+        const int c0 = ch * kSkChunk, cn = min(kSkChunk, ncols - c0);
+        cplx* dst = sk_sm + buf * kSkChunk * kSkLd;
+#pragma unroll
+        for (int u = 0; u < kSkRows * kSkChunk / 256; ++u) {
+            const int e = tid + 256 * u, i = e / kSkRows, rr = e % kSkRows;
+            const bool ok = i < cn && r0 + rr < M;
+            sk_cp_async16(dst + i * kSkLd + rr, ok ? (const void*)(A + size_t(c0 + i) * ld + r0 + rr) : (const void*)A,
+                          ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    stage(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) {
+            stage(ch + 1, (ch + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncthreads();  // chunk ch landed (and, at ch = 0, the map)
+        const cplx* cur = sk_sm + (ch & 1) * kSkChunk * kSkLd;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = 8 * w + k;
+            const int e0 = s_ptr[j * (nch + 1) + ch], e1 = s_ptr[j * (nch + 1) + ch + 1];
+            for (int e = e0; e < e1; ++e) {
+                const int pk = s_ent[e];
+                const cplx* col = cur + (pk >> 1) * kSkLd + lane;
+                const cplx v0 = col[0], v1 = col[32];
+                const double sg = (pk & 1) ? -1.0 : 1.0;  // acc + (-v) == fma(-1, v, acc): same rounding
+                acc[k][0].re = fma(sg, v0.re, acc[k][0].re);
+                acc[k][0].im = fma(sg, v0.im, acc[k][0].im);
+                acc[k][1].re = fma(sg, v1.re, acc[k][1].re);
+                acc[k][1].im = fma(sg, v1.im, acc[k][1].im);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int row = r0 + lane + 32 * h;
+        if (row < M) {
+            cplx* y = Y + size_t(q) * ystride + row;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[size_t(8 * w + k) * ldy] = cmul(alpha, acc[k][h]);
+        }
     }
 }
 
@@ -1032,7 +1116,7 @@ void lr_omega_setup(Ctx& c, cudaStream_t s) {
         for (int t = 0; t < kSkZeta; ++t) {  // partial Fisher-Yates: kSkZeta distinct columns
             const int j = t + int(rnd() % uint64_t(kSkCols - t));
             std::swap(cols[t], cols[j]);
-            colent[cols[t]].push_back(((i % kSkChunk) * 33 << 1) | int(rnd() & 1u) | ((i / kSkChunk) << 20));
+            colent[cols[t]].push_back(((i % kSkChunk) << 1) | int(rnd() & 1u) | ((i / kSkChunk) << 20));
         }
     }
     const int nch = (nb + kSkChunk - 1) / kSkChunk;
@@ -1067,13 +1151,33 @@ void sparse_sketch(Ctx& c, const std::vector<const cplx*>& src, const std::vecto
     pbuf.upload(src, s);
     lbuf.upload(ld, s);
     ProfScope ps("lr_sketch", s, 0.0, 16.0 * double(src.size()) * M * c.dims.nb);
-    static bool attr = false;
-    if (!attr) {
-        QPS_CUDA(cudaFuncSetAttribute(sparse_sketch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSkSmem)));
-        attr = true;
+    const int nb = c.dims.nb, nch = (nb + kSkChunk - 1) / kSkChunk;
+    const int nptr = kSkCols * (nch + 1), nent = kSkZeta * nb;
+    const size_t sm2 = sk2_smem_bytes(nptr, nent);
+    static const bool v1 = [] {  // QPS_LR_SKETCH=v1: the one-row-per-lane kernel (A/B)
+        const char* e = getenv("QPS_LR_SKETCH");
+        return e && !strcmp(e, "v1");
+    }();
+    if (!v1 && sm2 <= 200 * 1024) {
+        static size_t attr2 = 0;
+        if (sm2 > attr2) {
+            QPS_CUDA(cudaFuncSetAttribute(sparse_sketch2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(200 * 1024)));
+            attr2 = 200 * 1024;
+        }
+        { QPS_NOTE_LAUNCH(); sparse_sketch2_kernel<<<dim3((M + kSkRows - 1) / kSkRows, unsigned(src.size())), 256, sm2,
+                                                      s>>>(pbuf.p, lbuf.p, M, nb, c.lr_sk_ptr.p, c.lr_sk_ent.p, nent,
+                                                           alpha, Y, ldy, ystride); }
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            QPS_CUDA(cudaFuncSetAttribute(sparse_sketch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kSkSmem)));
+            attr = true;
+        }
+        { QPS_NOTE_LAUNCH(); sparse_sketch_kernel<<<dim3((M + 31) / 32, unsigned(src.size())), 256, kSkSmem, s>>>(
+            pbuf.p, lbuf.p, M, nb, c.lr_sk_ptr.p, c.lr_sk_ent.p, alpha, Y, ldy, ystride); }
     }
-    { QPS_NOTE_LAUNCH(); sparse_sketch_kernel<<<dim3((M + 31) / 32, unsigned(src.size())), 256, kSkSmem, s>>>(
-        pbuf.p, lbuf.p, M, c.dims.nb, c.lr_sk_ptr.p, c.lr_sk_ent.p, alpha, Y, ldy, ystride); }
     QPS_CUDA(cudaGetLastError());
 }
 bool lr_eligible(const Ctx& c) {
