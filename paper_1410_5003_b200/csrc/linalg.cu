@@ -158,6 +158,33 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n LAB_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+
 
 // ---------------------------------------------------------------------------
 // 3M: three real DMMAs per complex 8x8x4 step instead of four,
@@ -185,7 +212,15 @@ struct Z3Cfg {
 // tile and writes the CTA's partial to norm_part[(task0 + blockIdx.y) *
 // gridDim.x + blockIdx.x] (C is only read) -- a residual norm without the
 // residual's HBM round trip.
-template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool kNorm = false>
+//
+// kBulk: the stages are filled by TMA bulk copies (cp.async.bulk, one per tile
+// column: A's BK columns of BM rows, B's BN columns of BK entries, each a
+// contiguous run in HBM) issued by warp 0 and completing on one mbarrier per
+// stage, instead of 16-byte cp.async per thread.  Rows past M and columns past
+// N are not copied (their stale entries reach only accumulators that are never
+// stored); the K tail of the last chunk is zero-filled in both operands.  Same
+// products in the same order: results are bitwise those of the cp.async path.
+template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool kNorm = false, bool kBulk = false>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     zgemm3m_t_kernel(int M, int N, cplx alpha, cplx beta, const GemmTask* __restrict__ tasks, int tiles_m,
                      double* __restrict__ norm_part = nullptr, size_t task0 = 0) {
@@ -240,10 +275,48 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
 #pragma unroll
             for (int j = 0; j < WNT; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
 
+    uint64_t* bars = reinterpret_cast<uint64_t*>(z3_smem + STAGES * Cfg::STAGE);
+    // warp 0: chunk c into stage `stage` by bulk copies (kBulk)
+    auto issue_bulk = [&](int c, int stage) {
+        const int sgi = c < c0n ? 0 : 1;
+        const int k0 = (c < c0n ? c : c - c0n) * BK;
+        const cplx* __restrict__ A = T.A[sgi];
+        const cplx* __restrict__ B = T.B[sgi];
+        const int lda = T.lda[sgi], ldb = T.ldb[sgi];
+        const int kv = min(BK, T.K[sgi] - k0), rows = min(BM, M - m0), cols = min(BN, N - n0);
+        double2* As = z3_smem + stage * Cfg::STAGE;
+        double2* Bs = As + BK * LDA;
+        uint64_t* bar = bars + stage;
+        if (lane == 0) mbar_expect_tx(bar, unsigned(kv * rows + cols * kv) * 16u);
+        __syncwarp();
+        for (int kk = lane; kk < BK; kk += 32) {
+            if (kk < kv)
+                bulk_g2s(As + kk * LDA, A + size_t(k0 + kk) * lda + m0, unsigned(rows) * 16u, bar);
+            else
+                for (int i = 0; i < BM; ++i) As[kk * LDA + i] = make_double2(0.0, 0.0);
+        }
+        for (int col = lane; col < cols; col += 32) {
+            bulk_g2s(Bs + col * LDK, B + size_t(n0 + col) * ldb + k0, unsigned(kv) * 16u, bar);
+            for (int kk = kv; kk < BK; ++kk) Bs[col * LDK + kk] = make_double2(0.0, 0.0);
+        }
+        // the zero fill (generic proxy) before any later bulk write of this stage
+        if (kv < BK) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    };
+    if (kBulk) {
+        if (tid == 0) {
+            for (int st = 0; st < STAGES; ++st) mbar_init(bars + st, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (warp == 0)
+            for (int st = 0; st < STAGES - 1; ++st)
+                if (st < nchunks) issue_bulk(st, st);
+    } else {
 #pragma unroll
-    for (int st = 0; st < STAGES - 1; ++st) {
-        if (st < nchunks) issue(st, st);
-        cp_async_commit();
+        for (int st = 0; st < STAGES - 1; ++st) {
+            if (st < nchunks) issue(st, st);
+            cp_async_commit();
+        }
     }
     if (beta.re != 0.0 || beta.im != 0.0) {
         // the epilogue reads C: pull this CTA's tile into L2 now, so the
@@ -258,10 +331,16 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         }
     }
     for (int c = 0; c < nchunks; ++c) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1, (c + STAGES - 1) % STAGES);
-        cp_async_commit();
+        if (kBulk) {
+            mbar_wait(bars + c % STAGES, unsigned(c / STAGES) & 1u);
+            __syncthreads();  // every warp is done with the stage refilled next
+            if (warp == 0 && c + STAGES - 1 < nchunks) issue_bulk(c + STAGES - 1, (c + STAGES - 1) % STAGES);
+        } else {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            if (c + STAGES - 1 < nchunks) issue(c + STAGES - 1, (c + STAGES - 1) % STAGES);
+            cp_async_commit();
+        }
         const double2* As = z3_smem + (c % STAGES) * Cfg::STAGE;
         const double2* Bs = As + BK * LDA;
 #pragma unroll
@@ -289,7 +368,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
             }
         }
     }
-    cp_async_wait<0>();
+    if (!kBulk) cp_async_wait<0>();
     const bool use_beta = (beta.re != 0.0 || beta.im != 0.0);
     const int Mt = T.mlim == 0 ? M : (T.mlim > 0 ? min(M, T.mlim) : 0);
     double ss = 0.0;
@@ -337,15 +416,25 @@ __global__ void norm_parts_kernel(const double* __restrict__ part, int nparts, i
     out[t] = sqrt(s);
 }
 
+// QPS_ZGEMM_BULK=1: TMA bulk-copy staging instead of cp.async (A/B)
+bool zgemm_bulk() {
+    static const bool on = [] {
+        const char* e = getenv("QPS_ZGEMM_BULK");
+        return e && !strcmp(e, "1");
+    }();
+    return on;
+}
+
 template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB = (WARPS_M * WARPS_N <= 4) ? 2 : 1,
-          bool kNorm = false>
-void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_t ntasks, cudaStream_t s,
-               DBuf<double>* parts = nullptr, double* norms = nullptr) {
+          bool kNorm = false, bool kBulk = false>
+void launch_z3_impl(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_t ntasks, cudaStream_t s,
+                    DBuf<double>* parts, double* norms) {
     using Cfg = Z3Cfg<WMT, WNT, WARPS_M, WARPS_N, STAGES>;
-    auto kern = zgemm3m_t_kernel<WMT, WNT, WARPS_M, WARPS_N, STAGES, MINB, kNorm>;
+    auto kern = zgemm3m_t_kernel<WMT, WNT, WARPS_M, WARPS_N, STAGES, MINB, kNorm, kBulk>;
+    const size_t smem = Cfg::SMEM + (kBulk ? 8 * STAGES : 0);
     static bool attr = false;
     if (!attr) {
-        QPS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
+        QPS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = true;
     }
     const int tiles_m = (M + Cfg::BM - 1) / Cfg::BM, tiles_n = (N + Cfg::BN - 1) / Cfg::BN;
@@ -353,7 +442,7 @@ void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_
     if (kNorm) parts->ensure(ntasks * tiles);
     for (size_t off = 0; off < ntasks; off += 65535) {
         const unsigned cnt = unsigned(std::min<size_t>(65535, ntasks - off));
-        { QPS_NOTE_LAUNCH(); kern<<<dim3(tiles, cnt), Cfg::NT, Cfg::SMEM, s>>>(M, N, alpha, beta, tasks + off, tiles_m,
+        { QPS_NOTE_LAUNCH(); kern<<<dim3(tiles, cnt), Cfg::NT, smem, s>>>(M, N, alpha, beta, tasks + off, tiles_m,
                                                          kNorm ? parts->p : nullptr, off); }
         ++g_zgemm_launches;
     }
@@ -361,6 +450,18 @@ void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_
         { QPS_NOTE_LAUNCH(); norm_parts_kernel<<<unsigned((ntasks + 127) / 128), 128, 0, s>>>(parts->p, tiles, int(ntasks), norms); }
         QPS_CUDA(cudaGetLastError());
     }
+}
+
+template <int WMT, int WNT, int WARPS_M, int WARPS_N, int STAGES, int MINB = (WARPS_M * WARPS_N <= 4) ? 2 : 1,
+          bool kNorm = false>
+void launch_z3(int M, int N, cplx alpha, cplx beta, const GemmTask* tasks, size_t ntasks, cudaStream_t s,
+               DBuf<double>* parts = nullptr, double* norms = nullptr) {
+    if (zgemm_bulk())
+        launch_z3_impl<WMT, WNT, WARPS_M, WARPS_N, STAGES, MINB, kNorm, true>(M, N, alpha, beta, tasks, ntasks, s,
+                                                                              parts, norms);
+    else
+        launch_z3_impl<WMT, WNT, WARPS_M, WARPS_N, STAGES, MINB, kNorm, false>(M, N, alpha, beta, tasks, ntasks, s,
+                                                                               parts, norms);
 }
 
 // ---------------------------------------------------------------------------
