@@ -125,7 +125,8 @@ qps_ctx* qps_create(int device) {
         QPS_CUDA(cudaStreamCreateWithPriority(&h->c.side, cudaStreamNonBlocking, prio_hi));
         const char* sp = getenv("QPS_SAMPLE_PRIO");  // A/B: "main" puts side2 level with the main stream
         QPS_CUDA(cudaStreamCreateWithPriority(&h->c.side2, cudaStreamNonBlocking,
-                                              (sp && !strcmp(sp, "main")) ? prio_main : prio_lo));
+                                              (sp && !strcmp(sp, "main")) ? prio_main
+                                              : (sp && !strcmp(sp, "hi")) ? prio_hi : prio_lo));
         QPS_CUDA(cudaStreamCreateWithPriority(&h->c.side3, cudaStreamNonBlocking, prio_lo));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fork, cudaEventDisableTiming));
         QPS_CUDA(cudaEventCreateWithFlags(&h->c.ev_fill, cudaEventDisableTiming));
@@ -415,16 +416,18 @@ int qps_solve(qps_ctx* h) {
         tl_mark(c, "start", c.stream);
         for (int attempt = 0;; ++attempt) {
             c.fill_overlap = true;  // the Schur least squares start while the big blocks fill
+            c.sketch_in_fill = true;
+            c.sketch_launched = false;
             try {
                 run_fill(c);
             } catch (...) {
-                c.fill_overlap = false;
+                c.fill_overlap = c.sketch_in_fill = false;
                 throw;
             }
-            c.fill_overlap = false;
+            c.fill_overlap = c.sketch_in_fill = false;
             tl_mark(c, "fill", c.stream);
             c.times.assemble_ms = 0.0;
-            lr_sample_async(c);  // overlaps the Schur least squares
+            if (!c.sketch_launched) lr_sample_async(c);  // overlaps the Schur least squares
             {
                 Timer t(c, &c.times.schur_ms);
                 static const bool no_defer = [] {  // QPS_DEFER=0: form the coupling updates explicitly (A/B)

@@ -322,6 +322,8 @@ struct Ctx {
     // couplings, self blocks and their Alpert corrections on side3, joined
     // before the A' update (fill_overlap; opt-in QPS_FILL_OVERLAP=1, no gain measured)
     bool fill_overlap = false, fill_pending = false, fill_err_pending = false;
+    bool sketch_in_fill = false;   // one-shot solve: the fill launches the coupling sketch (set by qps_solve)
+    bool sketch_launched = false;  // ... and did (lr_sample_async already queued)
     cudaEvent_t ev_fillB = nullptr;
     cudaEvent_t ev_rhs = nullptr;      // level fork/join of the Woodbury reduction's right-hand-side half
     // one-shot solves: the interior least squares' residual norms (reported

@@ -268,6 +268,19 @@ void alloc_system(Ctx& c) {
     c.f.ensure(ns * D.nb);
 }
 
+// QPS_SKETCH_EARLY=1: the coupling sketch launched right after the coupling
+// blocks, beside the rest of the fill (A/B; measured no gain at config 4: on a
+// low-priority stream it still waits for the fill's last wave, on a high-
+// priority one it lengthens the fill by as much as it saves later, 105.3 vs
+// 105.3 / 105.9 ms -- the fill CTAs and the sketch CTAs do not share SMs)
+static bool sketch_early_on() {
+    static const bool on = [] {
+        const char* e = getenv("QPS_SKETCH_EARLY");
+        return e && !strcmp(e, "1");
+    }();
+    return on;
+}
+
 void fill_system_fused(Ctx& c) {
     const Dims& D = c.dims;
     const HostGeometry& g = c.geo;
@@ -536,6 +549,16 @@ void fill_system_fused(Ctx& c) {
         tl_mark(c, "fill(big blocks)", fb);
         c.fill_pending = true;
         launch_pair_fill(early, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
+    } else if (c.sketch_in_fill && sketch_early_on()) {
+        // the couplings first, then the low-rank sketch of them on side2 (HBM-
+        // bound: it streams beside the FP64-bound self-block fill) -- the
+        // blocks are disjoint, so the fill's results are unchanged
+        std::vector<PairTask> cpl, rest;
+        for (const auto& t : pt) (t.mirror && t.self == 0 ? cpl : rest).push_back(t);
+        launch_pair_fill(cpl, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
+        lr_sample_async(c);
+        c.sketch_launched = true;
+        launch_pair_fill(rest, pool, c.d_err.p, s, c.d_pair2, c.d_tiles2);
     } else {
         launch_pair_fill(pt, pool, c.d_err.p, s, c.d_pair, c.d_tiles);
     }
