@@ -1942,9 +1942,20 @@ constexpr int kWpSub = 8;                      // sub-panel (register) width
 constexpr int kWpThreads = 640;                // one thread per row
 constexpr int kWpWarps = kWpThreads / 32;
 
+// kStaged: the in-panel trailing update streams each thread's row of the later
+// columns through a private cp.async pipeline in shared memory (kWpSt stages of
+// kWpLd columns, (kWpSt - 1) kWpLd columns in flight per thread) instead of
+// register double-buffering 4 columns: the update is bound by the L2 round
+// trips of those loads.  Each thread reads back only what it copied itself, so
+// the pipeline needs no barrier.  Same operations in the same order.
+constexpr int kWpLd = 4, kWpSt = 4;
+size_t wpanel_smem(int threads) { return size_t(kWpSt) * kWpLd * threads * sizeof(cplx); }
+
+template <bool kStaged>
 __global__ void __launch_bounds__(kWpThreads, 1)
     lu_wpanel_kernel(int n, int ld, cplx* const* __restrict__ Ap, int* const* __restrict__ Pp, int c0, int w,
                      int* __restrict__ singular) {
+    extern __shared__ cplx wp_stage[];  // [kWpSt][kWpLd][blockDim.x] (kStaged)
     __shared__ cplx cand[2][kWpWarps][kWpSub];
     __shared__ double cval[2][kWpWarps];
     __shared__ int cidx[2][kWpWarps];
@@ -2062,6 +2073,42 @@ __global__ void __launch_bounds__(kWpThreads, 1)
             for (int kk = 0; kk < kWpSub; ++kk)
                 lv[kk] = (kk < sw && p0 + kk < mystep) ? s[kk] : cplx{0, 0};
             cplx* dst = arow + size_t(p0 + sw) * ld;
+            if (kStaged) {
+                const int nt = blockDim.x, ngrp = (ncol + kWpLd - 1) / kWpLd;
+                auto issue = [&](int gi) {
+                    cplx* st = wp_stage + size_t((gi % kWpSt) * kWpLd) * nt + tid;
+#pragma unroll
+                    for (int q = 0; q < kWpLd; ++q) {
+                        const int t = gi * kWpLd + q;
+                        const bool ok = t < ncol;
+                        cp_async16(st + size_t(q) * nt, ok ? (const void*)(dst + size_t(t) * ld) : (const void*)dst, ok);
+                    }
+                };
+#pragma unroll
+                for (int gi = 0; gi < kWpSt - 1; ++gi) {
+                    if (gi < ngrp) issue(gi);
+                    cp_async_commit();
+                }
+                for (int gi = 0; gi < ngrp; ++gi) {
+                    if (gi + kWpSt - 1 < ngrp) issue(gi + kWpSt - 1);
+                    cp_async_commit();
+                    cp_async_wait<kWpSt - 1>();
+                    const cplx* st = wp_stage + size_t((gi % kWpSt) * kWpLd) * nt + tid;
+#pragma unroll
+                    for (int q = 0; q < kWpLd; ++q) {
+                        const int t = gi * kWpLd + q;
+                        cplx a = st[size_t(q) * nt];
+#pragma unroll
+                        for (int kk = 0; kk < kWpSub; ++kk) {
+                            const cplx u = U12[kk][min(t, kWpMax - 1)];
+                            a.re -= lv[kk].re * u.re - lv[kk].im * u.im;
+                            a.im -= lv[kk].re * u.im + lv[kk].im * u.re;
+                        }
+                        if (t < ncol) dst[size_t(t) * ld] = a;
+                    }
+                }
+                cp_async_wait<0>();
+            } else {
             constexpr int kLd = 4;  // a group of columns; the next group's loads fly during its updates
             cplx an[kLd];
 #pragma unroll
@@ -2084,6 +2131,7 @@ __global__ void __launch_bounds__(kWpThreads, 1)
                     }
                     if (t0 + q < ncol) dst[size_t(t0 + q) * ld] = a[q];
                 }
+            }
             }
         }
         __syncthreads();
@@ -3089,7 +3137,23 @@ void lu_rec(LuCtx& L, int c0, int nc) {
         ProfScope ps("lu_panel", L.s, 8.0 * L.count * double(L.n - c0) * nc * nc / 2.0);
         if (wide_leaf(L.n)) {
             const int threads = ((L.n - c0 + 31) / 32) * 32;
-            { QPS_NOTE_LAUNCH(); lu_wpanel_kernel<<<L.count, threads, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc, L.sing); }
+            static const bool staged = [] {  // QPS_WP_STAGED=0: register double-buffered update (A/B)
+                const char* e = getenv("QPS_WP_STAGED");
+                return !(e && !strcmp(e, "0"));
+            }();
+            if (staged) {
+                static bool attr = false;
+                if (!attr) {
+                    QPS_CUDA(cudaFuncSetAttribute(lu_wpanel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  int(wpanel_smem(kWpThreads))));
+                    attr = true;
+                }
+                { QPS_NOTE_LAUNCH(); lu_wpanel_kernel<true><<<L.count, threads, wpanel_smem(threads), L.s>>>(
+                    L.n, L.ld, L.dA, L.dP, c0, nc, L.sing); }
+            } else {
+                { QPS_NOTE_LAUNCH(); lu_wpanel_kernel<false><<<L.count, threads, 0, L.s>>>(L.n, L.ld, L.dA, L.dP, c0, nc,
+                                                                                       L.sing); }
+            }
             QPS_CUDA(cudaGetLastError());
             // the leaf is a 64-aligned diagonal tile whose L and U are final:
             // invert both into its Dinv slot now (the trsm of U12 and the
