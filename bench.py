@@ -341,12 +341,15 @@ def main():
     # the roofline family is the level-0 LU batch's GEMMs (lu_gemm), the
     # largest main-path tensor family; side-stream families (the compression
     # sample / sketch) span their overlap with other work and are excluded
-    side = ("lr_sample", "lr_sketch")
+    side = ("lr_sample", "lr_sketch", "zgemm_resid")
     dom = ("lu_gemm", stats["lu_gemm"]) if "lu_gemm" in stats else \
         max(((k, v) for k, v in stats.items() if k not in side and v["flops"] > 0), key=lambda kv: kv[1]["ms"])
     fams = {k: v for k, v in stats.items()}
-    gemm_ms = sum(v["ms"] for k, v in fams.items() if k.startswith("zgemm"))
-    gemm_fl = sum(v["flops"] for k, v in fams.items() if k.startswith("zgemm"))
+    # zgemm_resid (the least squares' residual norms) runs on the low-priority
+    # side stream: its event span covers its overlap with the A' update, so it
+    # is kept out of the GEMM rate like the other side-stream families
+    gemm_ms = sum(v["ms"] for k, v in fams.items() if k.startswith("zgemm") and k not in side)
+    gemm_fl = sum(v["flops"] for k, v in fams.items() if k.startswith("zgemm") and k not in side)
     fill = {k: v for k, v in fams.items() if k.startswith("fill_")}
     fill_ms = sum(v["ms"] for v in fill.values())
     fill_units = sum(v["units"] for v in fill.values())
@@ -425,7 +428,14 @@ def main():
                 "fp64_peaks_tflops": peaks, "flux_error": rt["flux_error"], "R": rt["R"], "T": rt["T"],
                 "sweep": sweep,
                 "families_ms": {k: round(v["ms"] / args.steps, 3) for k, v in sorted(fams.items(),
-                                                                                     key=lambda kv: -kv[1]["ms"])}}
+                                                                                     key=lambda kv: -kv[1]["ms"])
+                                if k not in side},
+                "families_side_stream_span_ms": {k: round(v["ms"] / args.steps, 3) for k, v in fams.items()
+                                                 if k in side},
+                "families_note": "per-step event time of each main-stream kernel family; side-stream families "
+                                 "(low-priority streams overlapping the main path) are listed separately because "
+                                 "their event spans include the time they wait behind main-stream kernels and are "
+                                 "not kernel durations (profiles/*_launches.csv has those)"}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
